@@ -1,0 +1,225 @@
+/*
+ * fsw.h — C-ABI of libfsw: FaaSwap-style swap-in-and-execute of an inference model on B200.
+ *
+ * Paper: "FaaSwap: SLO-Aware, GPU-Efficient Serverless Inference via Model Swapping"
+ * (arXiv 2306.03622).  Citations "PAPER.md:n" are lines of the paper's LaTeX source.
+ *
+ * The problem statement the calls follow:
+ *   - functions publish models; requests invoke them
+ *   - models are kept in host memory and bound to a GPU of the pool on each request
+ *     ("late binding")               -> fsw_register_model / fsw_invoke
+ *   - transfer of later layers overlaps computation of earlier layers, layer by layer
+ *     ("Model swapping and pipeline execution") -> fsw_invoke (cold path)
+ *   - a host copy is always kept; eviction only invalidates the GPU region
+ *     ("Model eviction")                      -> fsw_evict
+ *   - all GPU memory is pre-allocated and managed as blocks by the server
+ *     ("Memory allocation and block management") -> fsw_pool_stats
+ *   - one request per GPU at a time    -> invoke concurrency rule
+ *   - no detailed model knowledge is needed; the paper records the
+ *     parameter access pattern of the first run.  Here the access
+ *     pattern is given explicitly as the layer table; its order IS the swap order.
+ *
+ * Conventions (all calls):
+ *   - every function returns fsw_status; no C++ exception crosses the ABI;
+ *     fsw_last_error() returns a thread-local message for the last failure.
+ *   - all pointers are HOST pointers; device memory is library-owned and never exported
+ *     (except the debug read-back copies below, which copy into caller host buffers).
+ *   - sizes are bytes unless noted.  Failed calls leave no partial state.
+ */
+#ifndef FSW_H
+#define FSW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FSW_OK = 0,
+    FSW_EINVAL = 1,    /* malformed table, bad argument, output buffer too small          */
+    FSW_ENOTFOUND = 2, /* unknown model id                                                 */
+    FSW_ENOMEM = 3,    /* pool too small even after evicting every idle model; host OOM    */
+    FSW_EBUSY = 4,     /* evict / unregister while an invoke of that model is in flight    */
+    FSW_ESTATE = 5,    /* evict of a model not resident on that GPU                        */
+    FSW_ECUDA = 6,     /* CUDA runtime failure (includes: no CUDA device)                  */
+    FSW_ETIMEOUT = 7,  /* a layer kernel's ready-flag spin hit the watchdog                */
+    FSW_ETOPO = 8      /* striping requested over GPUs that cannot reach the target        */
+} fsw_status;
+
+/* ---------------------------------------------------------------------------------------
+ * Context
+ * ------------------------------------------------------------------------------------- */
+#define FSW_NO_OVERLAP   0x1u /* swap completes before the first layer kernel starts
+                                 ("Non-pipeline" column of PAPER.md Table 4; also needed under
+                                 ncu / compute-sanitizer, which serialise kernels)             */
+#define FSW_DMA_BASELINE 0x2u /* swap by copy-engine DMA (cudaMemcpyAsync from pinned memory,
+                                 the paper's mechanism) instead of SM copy kernels */
+#define FSW_HOST_WC      0x4u /* back host stores with write-combined pinned pages            */
+
+typedef struct {
+    uint32_t n_gpus;                  /* GPUs in the pool; 0 = all visible devices           */
+    const int32_t* gpu_ids;           /* n_gpus CUDA device ordinals, or NULL = 0..n_gpus-1   */
+    uint64_t pool_bytes_per_gpu;      /* weight pool per GPU, pre-allocated at init; 0 = 64 GiB
+                                         (capped at 60% of free memory)                       */
+    uint64_t workspace_bytes_per_gpu; /* activation workspace per GPU; 0 = 512 MiB            */
+    uint32_t copy_ctas;               /* CTAs of the swap kernel; 0 = 32                      */
+    uint32_t copy_threads;            /* threads per swap CTA (multiple of 32); 0 = 256       */
+    uint64_t chunk_bytes;             /* swap piece size (the paper's "group size",
+                                         PAPER.md:600-604); multiple of 256; 0 = 256 KiB       */
+    uint64_t stripe_min_bytes;        /* reserved for striped swap; 0 = 256 MiB               */
+    uint32_t flags;                   /* FSW_NO_OVERLAP | FSW_DMA_BASELINE | FSW_HOST_WC       */
+} fsw_config;
+
+typedef struct fsw_ctx fsw_ctx; /* opaque; one per process */
+
+/* Create the per-GPU runtime: one shared CUDA context per GPU with all kernels preloaded
+ * (PAPER.md:551-555), the pre-allocated weight pool, workspace and streams.
+ * cfg may be NULL (defaults).  Returns FSW_ECUDA when no CUDA device is present.            */
+fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out);
+void fsw_shutdown(fsw_ctx* ctx);
+const char* fsw_last_error(void);
+const char* fsw_version(void);
+
+/* ---------------------------------------------------------------------------------------
+ * Model description (layer table)
+ * ------------------------------------------------------------------------------------- */
+enum { FSW_DT_BF16 = 0, FSW_DT_F32 = 1, FSW_DT_I32 = 2 };
+
+enum {
+    FSW_OP_EMBED = 1,     /* out[t] = Σ_j table_j[row_j(t)]                  refs: tables
+                             attr[0] = n tables, attr[1+j] = FSW_RULE_* of table j          */
+    FSW_OP_LAYERNORM = 2, /* out = (x−μ)/√(σ²+eps)·γ + β over the last dim    refs: γ, β
+                             attr[0] = eps as IEEE float bits                               */
+    FSW_OP_LINEAR = 3,    /* out[i] = act(x[r0+i]·Wᵀ + b + in1[i]),  W [N][K] refs: W [, b]
+                             attr[0] = FSW_ACT_*, attr[1] = r0, attr[2] = rows (0 = all)    */
+    FSW_OP_ATTENTION = 4, /* in0 row t = [q | k | v] (H·dh each); out = softmax(qkᵀ/√dh)·v
+                             attr[0] = H, attr[1] = dh, attr[2] = causal                     */
+    FSW_OP_CONV2D = 5,    /* NHWC, W [Cout][R][S][Cin];  out = act(conv + b + in1)  refs: W, b
+                             attr[0] = FSW_ACT_*, attr[1] = stride, attr[2] = pad            */
+    FSW_OP_MAXPOOL = 6,   /* attr[0] = k, attr[1] = stride, attr[2] = pad (pad = −∞)         */
+    FSW_OP_AVGPOOL = 7    /* global average over H·W: [H][W][C] -> [1][C]                    */
+};
+enum { FSW_ACT_NONE = 0, FSW_ACT_RELU = 1, FSW_ACT_GELU_ERF = 2, FSW_ACT_GELU_TANH = 3, FSW_ACT_TANH = 4 };
+enum { FSW_RULE_IDS = 0, FSW_RULE_POSITION = 1, FSW_RULE_ZERO = 2 };
+
+/* A weight tensor inside the caller's blob: row-major, `bytes` = numel · sizeof(dtype),
+ * offset 16-B aligned.  Tensors may be referenced by several layers (tied weights).       */
+typedef struct { uint64_t offset, bytes; uint32_t dtype, rank; uint32_t shape[4]; } fsw_tensor;
+/* An activation slot (a named buffer in the per-GPU workspace); dtype = storage dtype.   */
+typedef struct { uint32_t dtype, rank; uint32_t shape[4]; } fsw_slot;
+/* A layer: op, its weight tensors refs[first_ref .. first_ref+n_refs), activation slots
+ * in0 / in1 (−1 = none) and out (must differ from in0 and in1).                           */
+typedef struct { uint32_t op, first_ref, n_refs; int32_t in0, in1, out; int32_t attr[8]; } fsw_layer;
+
+#define FSW_REG_ADOPT 0x1u /* reserved: pin the caller's buffer in place (not yet supported) */
+
+typedef struct {
+    const char* name;
+    const void* weights; uint64_t weight_bytes;        /* caller-owned; copied (FSW_REG_COPY)  */
+    const fsw_tensor* tensors; uint32_t n_tensors;
+    const uint32_t* refs; uint32_t n_refs;
+    const fsw_slot* slots; uint32_t n_slots;
+    const fsw_layer* layers; uint32_t n_layers;        /* execution order == swap order        */
+    int32_t input_slot, output_slot;
+    uint32_t flags;
+} fsw_model_desc;
+
+/* Validate the table, lay the weights out in the library's pinned, mapped host store in
+ * execution order (each layer's tensors contiguous, 256-B aligned; GEMM weights re-laid in
+ * the tensor-core tile order described in DESIGN.md §4), and register it for zero-copy
+ * device access.  Untimed, one-time (the paper's model repository).
+ * The caller may free `weights` on return.  Errors: EINVAL (bad table), ENOMEM, ECUDA.   */
+fsw_status fsw_register_model(fsw_ctx* ctx, const fsw_model_desc* desc, uint32_t* model_id);
+/* EBUSY while an invoke of the model is in flight; evicts it from every GPU first.        */
+fsw_status fsw_unregister_model(fsw_ctx* ctx, uint32_t model_id);
+
+typedef struct {
+    uint64_t store_bytes;      /* host-store bytes (= bytes moved by one cold swap)         */
+    uint64_t algorithmic_bytes;/* Σ tensor bytes (excludes alignment / tile padding)        */
+    uint32_t n_layers, n_tensors, n_gemm_layers;
+    uint64_t input_bytes, output_bytes;
+    uint32_t output_dtype;
+} fsw_model_info;
+fsw_status fsw_model_info_get(fsw_ctx* ctx, uint32_t model_id, fsw_model_info* out);
+
+/* Where tensor `tensor` sits in the host store (and in HBM when resident, same offsets).
+ * layout 0 = row-major copy of the caller bytes; 1 = tensor-core tiles
+ * with rows padded to rows_pad and columns (K) padded to cols_pad.                      */
+typedef struct { uint64_t offset, bytes; uint32_t layout, rows, cols, rows_pad, cols_pad, owner_layer; } fsw_store_tensor;
+fsw_status fsw_store_tensor_get(fsw_ctx* ctx, uint32_t model_id, uint32_t tensor, fsw_store_tensor* out);
+
+/* ---------------------------------------------------------------------------------------
+ * Invoke
+ * ------------------------------------------------------------------------------------- */
+enum { FSW_SWAP_RESIDENT = 0, FSW_SWAP_HOST = 1, FSW_SWAP_PEER = 2, FSW_SWAP_STRIPED = 3 };
+
+typedef struct {
+    double total_ms;        /* host wall clock: call entry -> output in the caller buffer   */
+    double device_ms;       /* CUDA events around the invoke graph on the launching stream  */
+    double swap_ms;         /* CUDA events around the swap kernel on its own stream         */
+    double swap_span_ms;    /* %globaltimer: first piece claimed -> last piece released     */
+    double compute_tail_ms; /* %globaltimer: last piece released -> last layer finished     */
+    uint64_t bytes_swapped;
+    double link_gbps;       /* bytes_swapped / swap_ms                                       */
+    int32_t gpu;
+    uint32_t swap_kind;     /* FSW_SWAP_*                                                     */
+    uint32_t n_sources;
+    uint32_t n_kernels;     /* kernels launched by this invoke (incl. the swap kernel)       */
+} fsw_invoke_stats;
+
+/* Run one request: pick a GPU (resident and idle first, then the lowest idle id,
+ * PAPER.md:845-850 / SPEC tie-break), allocate a pool extent (evicting LRU idle models),
+ * swap in pipelined with execution (cold) or run resident (warm), return the output.
+ * input_bytes must equal the input slot size; output_cap ≥ the output slot size.
+ * Blocks while every GPU is busy (one request per GPU).                     */
+fsw_status fsw_invoke(fsw_ctx* ctx, uint32_t model_id, const void* input, uint64_t input_bytes,
+                      void* output, uint64_t output_cap, fsw_invoke_stats* stats /* nullable */);
+
+enum { FSW_ORDER_EXEC = 0, FSW_ORDER_REVERSE = 1, FSW_ORDER_RANDOM = 2 };
+typedef struct {
+    int32_t gpu;          /* −1 = scheduler's choice                                           */
+    uint32_t stripe_mask; /* reserved (striped swap)                                           */
+    uint64_t chunk_bytes; /* 0 = ctx default                                                   */
+    uint32_t order;       /* FSW_ORDER_* : order in which swap pieces are claimed (tests)      */
+    uint32_t order_seed;
+    uint32_t copy_ctas;   /* 0 = ctx default                                                   */
+    uint32_t flags;       /* FSW_NO_OVERLAP | FSW_DMA_BASELINE, OR-ed with the ctx flags       */
+} fsw_invoke_opts;
+fsw_status fsw_invoke_ex(fsw_ctx* ctx, uint32_t model_id, const fsw_invoke_opts* opts,
+                         const void* input, uint64_t input_bytes, void* output, uint64_t output_cap,
+                         fsw_invoke_stats* stats);
+
+/* Invalidate the model's extent on `gpu` (−1 = every GPU).  No device→host copy
+ * (PAPER.md:611-614).  ESTATE if not resident there, EBUSY if an invoke is in flight.    */
+fsw_status fsw_evict(fsw_ctx* ctx, uint32_t model_id, int32_t gpu);
+
+typedef struct {
+    uint64_t capacity, used, largest_free;
+    uint32_t n_resident, n_extents;
+    uint64_t n_evictions, bytes_swapped_total, n_invokes_cold, n_invokes_warm;
+} fsw_pool_stats;
+fsw_status fsw_pool_stats_get(fsw_ctx* ctx, int32_t gpu, fsw_pool_stats* out);
+fsw_status fsw_n_gpus(fsw_ctx* ctx, uint32_t* n);
+
+/* Debug / test read-back (copies into caller host memory). */
+fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, void* dst, uint64_t cap);
+fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
+/* Activation slot of the last invoke of `model_id` on `gpu` (valid until the next invoke). */
+fsw_status fsw_debug_read_slot(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, int32_t slot, void* dst, uint64_t cap);
+
+/* ---------------------------------------------------------------------------------------
+ * Extent allocator of the weight pool (pure host logic, usable without a GPU; tests).
+ * Best-fit over a free list of [offset, size) extents with coalescing on free.
+ * ------------------------------------------------------------------------------------- */
+typedef struct fsw_arena fsw_arena;
+fsw_arena* fsw_arena_create(uint64_t capacity, uint64_t align);
+void fsw_arena_destroy(fsw_arena* a);
+fsw_status fsw_arena_alloc(fsw_arena* a, uint64_t bytes, uint64_t* offset); /* ENOMEM if no fit */
+fsw_status fsw_arena_free(fsw_arena* a, uint64_t offset);                   /* EINVAL if unknown */
+void fsw_arena_stats(const fsw_arena* a, uint64_t* used, uint64_t* largest_free, uint32_t* n_allocated);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSW_H */

@@ -1,0 +1,97 @@
+// device.cuh — sm_100a device helpers shared by the libfsw kernels (inline PTX).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "kernels.h"
+
+namespace fsw {
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Streaming 128-bit load that does not allocate in L1 (host-mapped source, read once).
+__device__ __forceinline__ uint4 ld_stream_v4(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// Layer-kernel side of the ready-flag protocol: one thread spins with
+// back-off until the layer's byte counter reaches its region size, then the caller does a
+// CTA barrier.  The acquire pairs with the swap kernel's red.release; the barrier extends
+// the ordering to the rest of the CTA.  A watchdog turns a lost release into an error word.
+__device__ __forceinline__ void wait_ready_thread(const Wait& w) {
+    if (w.ready == nullptr) return;
+    if (ld_acquire_gpu(w.ready) >= w.target) return;
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 64;
+    while (ld_acquire_gpu(w.ready) < w.target) {
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+        if (globaltimer() - t0 > kWatchdogNs) {
+            atomicExch(&w.ctl->err, 1);
+            atomicExch(&w.ctl->err_layer, w.layer);
+            break;
+        }
+    }
+}
+
+__device__ __forceinline__ void wait_ready_cta(const Wait& w) {
+    if (w.ready == nullptr) return;
+    if (threadIdx.x == 0) wait_ready_thread(w);
+    __syncthreads();
+}
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+__device__ __forceinline__ uint16_t f32_to_bf16(float f) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
+    return 0.5f * x * (1.0f + tanhf(k0 * (x + 0.044715f * x * x * x)));
+}
+__device__ __forceinline__ float apply_act(int act, float x) {
+    switch (act) {
+        case FSW_ACT_RELU: return fmaxf(x, 0.0f);
+        case FSW_ACT_GELU_ERF: return gelu_erf(x);
+        case FSW_ACT_GELU_TANH: return gelu_tanh(x);
+        case FSW_ACT_TANH: return tanhf(x);
+        default: return x;
+    }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+}  // namespace fsw

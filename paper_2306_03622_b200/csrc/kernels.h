@@ -1,0 +1,109 @@
+// kernels.h — launch interface between the host runtime (runtime.cpp) and the sm_100a
+// kernels (*.cu).  Plain C++ (no device code); included by both sides of libfsw.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fsw.h"
+
+namespace fsw {
+
+// Per-GPU device-side invoke descriptor, written by the first node of every invoke graph
+// (one small H2D from pinned staging).  Kernels find the model's extent through it, so a
+// graph built once per (model, GPU) stays valid whichever pool extent the model lands in.
+struct DevDesc {
+    uint8_t* wbase;       // base of the model's extent in the weight pool (HBM)
+    uint64_t generation;  // invoke counter (debug)
+};
+
+// Per-GPU device control block (zeroed at the root of each cold graph except `err`).
+struct DevCtl {
+    uint32_t ticket;          // next swap piece to claim
+    uint32_t started;         // swap CTAs that have begun executing
+    uint32_t pad0[2];
+    unsigned long long t_first;  // %globaltimer when the first piece was claimed
+    unsigned long long t_last;   // %globaltimer when the last piece was released
+    unsigned long long t_end;    // %globaltimer when the last layer kernel finished
+    int32_t err;                 // watchdog / protocol error word (sticky until cleared)
+    int32_t err_layer;
+};
+
+// One swap piece: a byte range of one layer's region (pieces never straddle layers).
+struct Piece {
+    uint64_t off;     // offset in the host store == offset in the extent
+    uint32_t bytes;   // multiple of 16
+    uint32_t layer;   // ready counter to bump
+};
+
+// Readiness wait for a layer kernel: spin until ready[idx] >= target (bytes of the layer).
+struct Wait {
+    const uint32_t* ready;  // nullptr = no wait (warm invoke / no weights)
+    uint32_t target;
+    DevCtl* ctl;
+    int32_t layer;
+};
+
+constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
+// ---- swap ---------------------------------------------------------------------------------
+void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, const DevDesc* desc,
+                 const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* ctl);
+void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
+void launch_signal(cudaStream_t s, uint32_t* ready, uint32_t layer, uint32_t bytes, DevCtl* ctl, int last);
+void launch_finish(cudaStream_t s, DevCtl* ctl);
+
+// ---- layer ops ----------------------------------------------------------------------------
+struct EmbedArgs {
+    const int32_t* ids; int n_tables; uint64_t table_off[4]; uint32_t table_rows[4]; int rule[4];
+    uint32_t T, C; float* out; uint16_t* out_bf16;
+};
+void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a);
+
+struct LnArgs {
+    const float* in; uint32_t rows, C; float eps; uint64_t g_off, b_off;
+    float* out_f32; uint16_t* out_bf16;
+};
+void launch_layernorm(cudaStream_t s, const DevDesc* d, Wait w, const LnArgs& a);
+
+struct GemvArgs {  // y[i][o] = act(x[r0+i]·W[o] + b[o] + res[i][o]),  W row-major [N][K] bf16
+    const void* x; int x_bf16; uint32_t ldx, r0, rows, K, N;
+    uint64_t w_off, b_off; int has_bias, act;
+    const void* res; int res_bf16;
+    void* out; int out_bf16; uint16_t* out2;
+};
+void launch_gemv(cudaStream_t s, const DevDesc* d, Wait w, const GemvArgs& a);
+
+struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA, W tiled
+    uint32_t M, N, K, n_pad;     // K = padded K (multiple of 64), n_pad = tiled rows
+    uint64_t w_off, b_off; int has_bias, act;
+    const void* res; int res_bf16; uint32_t ld_res;
+    void* out; int out_bf16; uint32_t ld_out;
+    uint16_t* out2;     // optional bf16 shadow of an f32 output (same ld)
+    int bn;                      // tile N: 32, 64 or 128
+};
+void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a);
+
+struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; };
+void launch_attention(cudaStream_t s, const AttnArgs& a);
+
+struct Im2colArgs {
+    const uint16_t* in; uint32_t H, W, C;
+    uint16_t* out; uint32_t P, Q, R, S, stride, pad, K, Kpad;
+};
+void launch_im2col(cudaStream_t s, const Im2colArgs& a);
+
+struct PoolArgs {
+    const uint16_t* in; uint32_t H, W, C; uint32_t P, Q, k, stride, pad;
+    uint16_t* out; float* out_f32;
+};
+void launch_maxpool(cudaStream_t s, const PoolArgs& a);
+void launch_avgpool(cudaStream_t s, const PoolArgs& a);
+
+void init_gemm_attrs();
+void init_ops_attrs();
+
+// Host helper: build the TMA descriptor of a row-major bf16 activation [rows][cols].
+bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems);
+
+}  // namespace fsw

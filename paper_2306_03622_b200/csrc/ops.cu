@@ -1,0 +1,306 @@
+// ops.cu — the non-GEMM layer kernels (HBM/latency-bound at batch 1): embedding gather,
+// LayerNorm, GEMV (M = 1 linears: MLP, pooler, fc, LM head), attention core, im2col,
+// max/avg pooling.  Each kernel that reads weights first waits on its layer's ready
+// counter (device.cuh), which is how "each layer's kernels start as soon as its weights
+// land" (BASELINE.json north_star).
+#include "device.cuh"
+
+namespace fsw {
+
+// ------------------------------------------------------------------------------------------
+// EMBED: out[t][c] = Σ_j table_j[row_j(t)][c]   (fp32 sum of bf16 rows)
+// ------------------------------------------------------------------------------------------
+__global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
+    wait_ready_cta(w);
+    const uint32_t t = blockIdx.x;
+    const uint8_t* wb = d->wbase;
+    uint32_t row[4];
+    for (int j = 0; j < a.n_tables; ++j) {
+        uint32_t r = a.rule[j] == FSW_RULE_IDS ? (uint32_t)a.ids[t] : (a.rule[j] == FSW_RULE_POSITION ? t : 0u);
+        if (r >= a.table_rows[j]) {  // out-of-range id: flag it, read row 0
+            if (threadIdx.x == 0) atomicExch(&w.ctl->err, 3);
+            r = 0;
+        }
+        row[j] = r;
+    }
+    for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) {
+        float s = 0.0f;
+        for (int j = 0; j < a.n_tables; ++j) {
+            const uint16_t* tab = reinterpret_cast<const uint16_t*>(wb + a.table_off[j]);
+            s += bf16_to_f32(tab[(uint64_t)row[j] * a.C + c]);
+        }
+        if (a.out) a.out[(uint64_t)t * a.C + c] = s;
+        if (a.out_bf16) a.out_bf16[(uint64_t)t * a.C + c] = f32_to_bf16(s);
+    }
+}
+
+void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) {
+    k_embed<<<a.T, 256, 0, s>>>(d, w, a);
+}
+
+// ------------------------------------------------------------------------------------------
+// LAYERNORM: one warp per row, row held in registers (C <= 2048), fp32 statistics.
+// ------------------------------------------------------------------------------------------
+constexpr int kLnMaxPerLane = 64;
+
+__global__ void __launch_bounds__(256) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
+    wait_ready_cta(w);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (r >= a.rows) return;
+    const float* x = a.in + (uint64_t)r * a.C;
+    float v[kLnMaxPerLane];
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kLnMaxPerLane; ++j) {
+        const uint32_t c = lane + 32u * j;
+        v[j] = c < a.C ? x[c] : 0.0f;
+        s += v[j];
+    }
+    const float mu = warp_sum(s) / (float)a.C;
+    float q = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kLnMaxPerLane; ++j) {
+        const uint32_t c = lane + 32u * j;
+        const float dlt = c < a.C ? v[j] - mu : 0.0f;
+        q += dlt * dlt;
+    }
+    const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
+    const uint16_t* g = reinterpret_cast<const uint16_t*>(d->wbase + a.g_off);
+    const uint16_t* b = reinterpret_cast<const uint16_t*>(d->wbase + a.b_off);
+#pragma unroll
+    for (int j = 0; j < kLnMaxPerLane; ++j) {
+        const uint32_t c = lane + 32u * j;
+        if (c < a.C) {
+            const float y = (v[j] - mu) * inv * bf16_to_f32(g[c]) + bf16_to_f32(b[c]);
+            if (a.out_f32) a.out_f32[(uint64_t)r * a.C + c] = y;
+            if (a.out_bf16) a.out_bf16[(uint64_t)r * a.C + c] = f32_to_bf16(y);
+        }
+    }
+}
+
+void launch_layernorm(cudaStream_t s, const DevDesc* d, Wait w, const LnArgs& a) {
+    k_layernorm<<<(a.rows + 7) / 8, 256, 0, s>>>(d, w, a);
+}
+
+// ------------------------------------------------------------------------------------------
+// GEMV (rows <= 8): one warp per output feature, 16-B coalesced weight loads along K,
+// x staged once per CTA in shared memory as fp32.  HBM-bound: bytes = N·K·2.
+// ------------------------------------------------------------------------------------------
+constexpr int kGemvMaxRows = 8;
+
+template <int R>
+__global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wait w, GemvArgs a) {
+    extern __shared__ float xs[];  // [R][K]
+    for (uint32_t i = threadIdx.x; i < R * a.K; i += blockDim.x) {
+        const uint32_t r = i / a.K, k = i - r * a.K;
+        const uint64_t src = (uint64_t)(a.r0 + r) * a.ldx + k;
+        xs[i] = r >= a.rows ? 0.0f : a.x_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.x)[src])
+                         : reinterpret_cast<const float*>(a.x)[src];
+    }
+    if (threadIdx.x == 0) wait_ready_thread(w);
+    __syncthreads();  // publishes xs and the acquired weights to the CTA
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    const uint8_t* wb = d->wbase;
+    const uint32_t k8n = a.K >> 3;
+    for (uint32_t o = gwarp; o < a.N; o += nwarps) {
+        const uint4* wr = reinterpret_cast<const uint4*>(wb + a.w_off + (uint64_t)o * a.K * 2);
+        float acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = 0.0f;
+#pragma unroll 4
+        for (uint32_t k8 = lane; k8 < k8n; k8 += 32) {
+            const uint4 wv = __ldcg(wr + k8);
+            const uint32_t wu[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float w0 = __uint_as_float(wu[h] << 16), w1 = __uint_as_float(wu[h] & 0xffff0000u);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float* xr = xs + r * a.K + k8 * 8 + 2 * h;
+                    acc[r] = fmaf(w0, xr[0], acc[r]);
+                    acc[r] = fmaf(w1, xr[1], acc[r]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = warp_sum(acc[r]);
+        if (lane < R && lane < a.rows) {
+            float v = 0.0f;
+#pragma unroll
+            for (int r = 0; r < R; ++r) v = (r == (int)lane) ? acc[r] : v;
+            const uint64_t oi = (uint64_t)lane * a.N + o;
+            if (a.has_bias) v += bf16_to_f32(reinterpret_cast<const uint16_t*>(wb + a.b_off)[o]);
+            if (a.res) v += a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[oi])
+                                       : reinterpret_cast<const float*>(a.res)[oi];
+            v = apply_act(a.act, v);
+            if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
+            else reinterpret_cast<float*>(a.out)[oi] = v;
+            if (a.out2) a.out2[oi] = f32_to_bf16(v);
+        }
+    }
+}
+
+void launch_gemv(cudaStream_t s, const DevDesc* d, Wait w, const GemvArgs& a) {
+    const size_t smem = sizeof(float) * a.K * (a.rows <= 1 ? 1 : kGemvMaxRows);
+    int ctas = (int)((a.N + 7) / 8);
+    if (ctas > 148 * 4) ctas = 148 * 4;
+    if (ctas < 1) ctas = 1;
+    if (a.rows <= 1) {
+        k_gemv<1><<<ctas, 256, smem, s>>>(d, w, a);
+    } else {
+        k_gemv<kGemvMaxRows><<<ctas, 256, smem, s>>>(d, w, a);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// ATTENTION core, one CTA per (head, 32 query rows); K/V of the head staged in shared memory
+// as fp32 (K rows padded by one float against bank conflicts); fp32 softmax.
+// ------------------------------------------------------------------------------------------
+constexpr int kAttnRows = 32;
+
+__global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
+    extern __shared__ float sm[];
+    const uint32_t T = a.T, dh = a.dh, D = a.H * dh, W3 = 3 * D;
+    const uint32_t h = blockIdx.x, t0 = blockIdx.y * kAttnRows;
+    const uint32_t nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t kend = a.causal ? min(T, t0 + kAttnRows) : T;  // keys this CTA needs
+    float* Ks = sm;                          // [T][dh+1]
+    float* Vs = Ks + T * (dh + 1);           // [T][dh]
+    float* Ps = Vs + T * dh;                 // [nwarp][T]
+    float* Qs = Ps + nwarp * T;              // [nwarp][dh]
+    for (uint32_t i = threadIdx.x; i < kend * dh; i += blockDim.x) {
+        const uint32_t j = i / dh, c = i - j * dh;
+        const uint16_t* row = a.qkv + (uint64_t)j * W3 + h * dh + c;
+        Ks[j * (dh + 1) + c] = bf16_to_f32(row[D]);
+        Vs[j * dh + c] = bf16_to_f32(row[2 * D]);
+    }
+    __syncthreads();
+    const float scale = rsqrtf((float)dh);
+    float* P = Ps + warp * T;
+    float* q = Qs + warp * dh;
+    for (uint32_t t = t0 + warp; t < min(T, t0 + kAttnRows); t += nwarp) {
+        for (uint32_t c = lane; c < dh; c += 32) q[c] = bf16_to_f32(a.qkv[(uint64_t)t * W3 + h * dh + c]) * scale;
+        __syncwarp();
+        const uint32_t jmax = a.causal ? t + 1 : T;
+        float mx = -INFINITY;
+        for (uint32_t j = lane; j < jmax; j += 32) {
+            const float* kr = Ks + j * (dh + 1);
+            float s = 0.0f;
+            for (uint32_t c = 0; c < dh; ++c) s = fmaf(q[c], kr[c], s);
+            P[j] = s;
+            mx = fmaxf(mx, s);
+        }
+        mx = warp_max(mx);
+        float z = 0.0f;
+        for (uint32_t j = lane; j < jmax; j += 32) {
+            const float e = __expf(P[j] - mx);
+            P[j] = e;
+            z += e;
+        }
+        z = warp_sum(z);
+        __syncwarp();
+        const float iz = 1.0f / z;
+        for (uint32_t c = lane; c < dh; c += 32) {
+            float acc = 0.0f;
+            for (uint32_t j = 0; j < jmax; ++j) acc = fmaf(P[j], Vs[j * dh + c], acc);
+            a.out[(uint64_t)t * D + h * dh + c] = f32_to_bf16(acc * iz);
+        }
+        __syncwarp();
+    }
+}
+
+void launch_attention(cudaStream_t s, const AttnArgs& a) {
+    const int threads = 256, nwarp = threads / 32;
+    const size_t smem = sizeof(float) * (a.T * (a.dh + 1) + a.T * a.dh + nwarp * a.T + nwarp * a.dh);
+    dim3 grid(a.H, (a.T + kAttnRows - 1) / kAttnRows);
+    k_attention<<<grid, threads, smem, s>>>(a);
+}
+
+// ------------------------------------------------------------------------------------------
+// IM2COL (NHWC bf16 -> [P·Q][Kpad] bf16, k = (r·S + s)·C + c, zero padding / tail)
+// ------------------------------------------------------------------------------------------
+__global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per thread
+    const uint32_t k8n = a.Kpad >> 3;
+    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (uint64_t)a.P * a.Q * k8n) return;
+    const uint32_t pq = (uint32_t)(idx / k8n), k = (uint32_t)(idx - (uint64_t)pq * k8n) * 8;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (k < a.K) {
+        const uint32_t rs = k / a.C, c = k - rs * a.C, r = rs / a.S, s = rs - r * a.S;
+        const uint32_t p = pq / a.Q, q = pq - p * a.Q;
+        const int ih = (int)(p * a.stride) - (int)a.pad + (int)r, iw = (int)(q * a.stride) - (int)a.pad + (int)s;
+        if (ih >= 0 && iw >= 0 && ih < (int)a.H && iw < (int)a.W)
+            v = *reinterpret_cast<const uint4*>(a.in + ((uint64_t)ih * a.W + iw) * a.C + c);
+    }
+    *reinterpret_cast<uint4*>(a.out + (uint64_t)pq * a.Kpad + k) = v;
+}
+
+__global__ void k_im2col_scalar(Im2colArgs a) {
+    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (uint64_t)a.P * a.Q * a.Kpad) return;
+    const uint32_t pq = (uint32_t)(idx / a.Kpad), k = (uint32_t)(idx - (uint64_t)pq * a.Kpad);
+    uint16_t v = 0;
+    if (k < a.K) {
+        const uint32_t rs = k / a.C, c = k - rs * a.C, r = rs / a.S, s = rs - r * a.S;
+        const uint32_t p = pq / a.Q, q = pq - p * a.Q;
+        const int ih = (int)(p * a.stride) - (int)a.pad + (int)r, iw = (int)(q * a.stride) - (int)a.pad + (int)s;
+        if (ih >= 0 && iw >= 0 && ih < (int)a.H && iw < (int)a.W) v = a.in[((uint64_t)ih * a.W + iw) * a.C + c];
+    }
+    a.out[idx] = v;
+}
+
+void launch_im2col(cudaStream_t s, const Im2colArgs& a) {
+    if (a.C % 8 == 0) {
+        const uint64_t n = (uint64_t)a.P * a.Q * (a.Kpad / 8);
+        k_im2col_vec8<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+    } else {
+        const uint64_t n = (uint64_t)a.P * a.Q * a.Kpad;
+        k_im2col_scalar<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// pooling (NHWC bf16)
+// ------------------------------------------------------------------------------------------
+__global__ void k_maxpool(PoolArgs a) {
+    const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (uint64_t)a.P * a.Q * a.C) return;
+    const uint32_t c = (uint32_t)(idx % a.C), pq = (uint32_t)(idx / a.C), p = pq / a.Q, q = pq - p * a.Q;
+    float m = -INFINITY;
+    for (uint32_t r = 0; r < a.k; ++r)
+        for (uint32_t s = 0; s < a.k; ++s) {
+            const int ih = (int)(p * a.stride) - (int)a.pad + (int)r, iw = (int)(q * a.stride) - (int)a.pad + (int)s;
+            if (ih < 0 || iw < 0 || ih >= (int)a.H || iw >= (int)a.W) continue;
+            m = fmaxf(m, bf16_to_f32(a.in[((uint64_t)ih * a.W + iw) * a.C + c]));
+        }
+    a.out[idx] = f32_to_bf16(m);
+}
+
+void launch_maxpool(cudaStream_t s, const PoolArgs& a) {
+    const uint64_t n = (uint64_t)a.P * a.Q * a.C;
+    k_maxpool<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+}
+
+__global__ void k_avgpool(PoolArgs a) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= a.C) return;
+    const uint32_t hw = a.H * a.W;
+    float s = 0.0f;
+    for (uint32_t i = 0; i < hw; ++i) s += bf16_to_f32(a.in[(uint64_t)i * a.C + c]);
+    a.out_f32[c] = s / (float)hw;
+}
+
+void launch_avgpool(cudaStream_t s, const PoolArgs& a) {
+    k_avgpool<<<(a.C + 127) / 128, 128, 0, s>>>(a);
+}
+
+void init_ops_attrs() {
+    cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemv<kGemvMaxRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+}  // namespace fsw

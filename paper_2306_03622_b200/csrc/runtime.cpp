@@ -1,0 +1,1245 @@
+// runtime.cpp — libfsw host runtime behind include/fsw.h.
+//
+// Layers: C-ABI -> host runtime (host store, weight pool, invoke orchestrator,
+// per-(model, GPU) execution plans and CUDA graphs) -> sm_100a kernels (kernels.h).
+//
+// Paper mapping:
+//   model repository in host memory ........ HostStore
+//   GPU executor, one shared runtime/GPU .... Gpu
+//   pre-allocated pool + block management ... Arena
+//   late binding + on-demand swapping ....... invoke()
+//   pipelined model execution ............... cold graph: swap kernel ‖ flag-gated layers
+//   eviction by invalidation ................ evict()
+//   one request per GPU ..................... Gpu::busy
+#include <sys/mman.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "fsw.h"
+#include "kernels.h"
+
+using namespace fsw;
+
+// ==========================================================================================
+// errors
+// ==========================================================================================
+static thread_local std::string g_err;
+
+static fsw_status fail(fsw_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(FSW_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                           __FILE__, __LINE__);                                    \
+    } while (0)
+
+extern "C" const char* fsw_last_error(void) { return g_err.c_str(); }
+extern "C" const char* fsw_version(void) { return "fsw 0.1 (sm_100a)"; }
+
+static inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+static double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// ==========================================================================================
+// Arena: best-fit extent allocator with coalescing (the pre-allocated pool)
+// ==========================================================================================
+struct fsw_arena {
+    uint64_t capacity, align;
+    std::map<uint64_t, uint64_t> free_;   // offset -> size
+    std::map<uint64_t, uint64_t> used_;   // offset -> size
+};
+
+extern "C" fsw_arena* fsw_arena_create(uint64_t capacity, uint64_t align) {
+    if (align == 0 || (align & (align - 1))) return nullptr;
+    auto* a = new fsw_arena{capacity / align * align, align, {}, {}};
+    if (a->capacity) a->free_[0] = a->capacity;
+    return a;
+}
+extern "C" void fsw_arena_destroy(fsw_arena* a) { delete a; }
+
+extern "C" fsw_status fsw_arena_alloc(fsw_arena* a, uint64_t bytes, uint64_t* offset) {
+    if (!a || !offset || bytes == 0) return fail(FSW_EINVAL, "arena_alloc: bad argument");
+    const uint64_t need = align_up(bytes, a->align);
+    auto best = a->free_.end();
+    for (auto it = a->free_.begin(); it != a->free_.end(); ++it)
+        if (it->second >= need && (best == a->free_.end() || it->second < best->second)) best = it;
+    if (best == a->free_.end()) return fail(FSW_ENOMEM, "arena_alloc: no free extent of %llu bytes", (unsigned long long)need);
+    const uint64_t off = best->first, sz = best->second;
+    a->free_.erase(best);
+    if (sz > need) a->free_[off + need] = sz - need;
+    a->used_[off] = need;
+    *offset = off;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_arena_free(fsw_arena* a, uint64_t offset) {
+    if (!a) return fail(FSW_EINVAL, "arena_free: null arena");
+    auto it = a->used_.find(offset);
+    if (it == a->used_.end()) return fail(FSW_EINVAL, "arena_free: %llu is not an allocated extent", (unsigned long long)offset);
+    uint64_t off = it->first, sz = it->second;
+    a->used_.erase(it);
+    auto nx = a->free_.lower_bound(off);
+    if (nx != a->free_.end() && off + sz == nx->first) {
+        sz += nx->second;
+        a->free_.erase(nx);
+    }
+    auto pv = a->free_.lower_bound(off);
+    if (pv != a->free_.begin()) {
+        --pv;
+        if (pv->first + pv->second == off) {
+            off = pv->first;
+            sz += pv->second;
+            a->free_.erase(pv);
+        }
+    }
+    a->free_[off] = sz;
+    return FSW_OK;
+}
+
+extern "C" void fsw_arena_stats(const fsw_arena* a, uint64_t* used, uint64_t* largest_free, uint32_t* n_allocated) {
+    uint64_t u = 0, lf = 0;
+    if (a) {
+        for (auto& kv : a->used_) u += kv.second;
+        for (auto& kv : a->free_) lf = std::max(lf, kv.second);
+    }
+    if (used) *used = u;
+    if (largest_free) *largest_free = lf;
+    if (n_allocated) *n_allocated = a ? (uint32_t)a->used_.size() : 0;
+}
+
+// ==========================================================================================
+// model + plans
+// ==========================================================================================
+enum { LAYOUT_ROWMAJOR = 0, LAYOUT_TILED = 1 };
+
+struct TensorInfo {
+    fsw_tensor t;
+    uint64_t st_off = 0, st_bytes = 0;
+    uint32_t layout = LAYOUT_ROWMAJOR, rows = 0, cols = 0, rows_pad = 0, cols_pad = 0;
+    int owner = -1;
+    bool placed = false;
+};
+
+enum KernelKind { K_EMBED, K_LN, K_GEMV, K_GEMM, K_ATTN, K_IM2COL, K_MAXPOOL, K_AVGPOOL };
+
+struct Launch {  // one kernel of the layer graph (addresses resolved for one GPU workspace)
+    KernelKind kind;
+    int layer;
+    EmbedArgs embed;
+    LnArgs ln;
+    GemvArgs gemv;
+    GemmArgs gemm;
+    CUtensorMap tmap;
+    AttnArgs attn;
+    Im2colArgs im2col;
+    PoolArgs pool;
+};
+
+struct Gpu;
+
+struct GraphKey {
+    int cold, flags, order;
+    uint64_t chunk;
+    uint32_t seed, ctas, extra;
+    bool operator<(const GraphKey& o) const {
+        return std::tie(cold, flags, order, chunk, seed, ctas, extra) <
+               std::tie(o.cold, o.flags, o.order, o.chunk, o.seed, o.ctas, o.extra);
+    }
+};
+
+struct PieceSet {
+    Piece* dev = nullptr;
+    std::vector<Piece> host;
+};
+
+struct Plan {  // one model on one GPU
+    bool built = false;
+    std::vector<Launch> launches;
+    std::vector<uint64_t> slot_off;      // workspace offset of each slot
+    std::vector<int64_t> shadow_off;     // bf16 shadow of an f32 slot, or -1
+    uint64_t ws_bytes = 0;
+    std::map<GraphKey, cudaGraphExec_t> graphs;
+    std::map<std::tuple<uint64_t, int, uint32_t>, PieceSet> pieces;  // (chunk, order, seed)
+};
+
+struct Model {
+    uint32_t id;
+    std::string name;
+    std::vector<TensorInfo> tensors;
+    std::vector<uint32_t> refs;
+    std::vector<fsw_slot> slots;
+    std::vector<fsw_layer> layers;
+    std::vector<uint64_t> region_off, region_bytes;
+    int32_t input_slot, output_slot;
+    uint64_t input_bytes = 0, output_bytes = 0, algorithmic_bytes = 0;
+    uint32_t n_gemm = 0;
+    uint8_t* store = nullptr;  // pinned, mapped host store (execution order)
+    uint64_t store_bytes = 0, store_alloc = 0;
+    bool store_wc = false;
+    // residency per GPU
+    std::vector<int64_t> extent;       // pool offset, or -1
+    std::vector<uint64_t> last_use;
+    std::vector<std::unique_ptr<Plan>> plans;
+    int inflight = 0;
+};
+
+struct Gpu {
+    int dev = 0;
+    cudaStream_t sx = nullptr, sc = nullptr;
+    uint8_t* pool = nullptr;
+    uint64_t pool_bytes = 0;
+    fsw_arena* arena = nullptr;
+    uint8_t* ws = nullptr;
+    uint64_t ws_bytes = 0;
+    uint32_t* ready = nullptr;
+    uint32_t ready_cap = 0;
+    DevCtl* ctl = nullptr;
+    uint8_t* dstage = nullptr;   // device: [DevDesc | pad | input]
+    uint8_t* hstage = nullptr;   // pinned: same layout
+    uint8_t* hout = nullptr;     // pinned: output
+    DevCtl* hctl = nullptr;      // pinned: ctl copy
+    uint64_t stage_cap = 0, out_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr, evfork = nullptr, evjoin = nullptr;
+    bool busy = false;
+    uint64_t generation = 0;
+    // stats
+    uint64_t n_evictions = 0, bytes_swapped_total = 0, n_cold = 0, n_warm = 0;
+};
+
+constexpr uint64_t kStageHdr = 256;
+
+struct fsw_ctx {
+    fsw_config cfg{};
+    std::vector<Gpu> gpus;
+    std::vector<std::unique_ptr<Model>> models;  // index = id (nullptr after unregister)
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t clock = 0;
+};
+
+// ==========================================================================================
+// init / shutdown
+// ==========================================================================================
+static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
+    CU(cudaSetDevice(g.dev));
+    CU(cudaFree(nullptr));  // create the context now (one shared runtime per GPU)
+    init_gemm_attrs();
+    init_ops_attrs();
+    CU(cudaStreamCreateWithFlags(&g.sx, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&g.sc, cudaStreamNonBlocking));
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t want = c->cfg.pool_bytes_per_gpu ? c->cfg.pool_bytes_per_gpu : (64ull << 30);
+    want = std::min<uint64_t>(want, (uint64_t)(free_b * 0.6));
+    g.pool_bytes = want / (64 << 10) * (64 << 10);
+    CU(cudaMalloc(&g.pool, g.pool_bytes));
+    g.arena = fsw_arena_create(g.pool_bytes, 64 << 10);
+    g.ws_bytes = c->cfg.workspace_bytes_per_gpu ? c->cfg.workspace_bytes_per_gpu : (512ull << 20);
+    CU(cudaMalloc(&g.ws, g.ws_bytes));
+    g.ready_cap = 1u << 16;
+    CU(cudaMalloc(&g.ready, sizeof(uint32_t) * g.ready_cap));
+    CU(cudaMemset(g.ready, 0, sizeof(uint32_t) * g.ready_cap));
+    CU(cudaMalloc(&g.ctl, sizeof(DevCtl)));
+    CU(cudaMemset(g.ctl, 0, sizeof(DevCtl)));
+    g.stage_cap = 16ull << 20;
+    g.out_cap = 16ull << 20;
+    CU(cudaMalloc(&g.dstage, g.stage_cap));
+    CU(cudaHostAlloc(&g.hstage, g.stage_cap, cudaHostAllocPortable));
+    CU(cudaHostAlloc(&g.hout, g.out_cap, cudaHostAllocPortable));
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&g.hctl), sizeof(DevCtl), cudaHostAllocPortable));
+    memset(g.hstage, 0, kStageHdr);
+    for (cudaEvent_t* e : {&g.ev0, &g.ev1, &g.evs0, &g.evs1}) CU(cudaEventCreate(e));
+    CU(cudaEventCreateWithFlags(&g.evfork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&g.evjoin, cudaEventDisableTiming));
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
+    if (!out) return fail(FSW_EINVAL, "fsw_init: out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(FSW_ECUDA, "fsw_init: no CUDA device (%s)", e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+    auto c = std::make_unique<fsw_ctx>();
+    if (cfg) c->cfg = *cfg;
+    if (c->cfg.copy_ctas == 0) c->cfg.copy_ctas = 32;
+    if (c->cfg.copy_threads == 0) c->cfg.copy_threads = 256;
+    if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 256 << 10;
+    if (c->cfg.stripe_min_bytes == 0) c->cfg.stripe_min_bytes = 256ull << 20;
+    if (c->cfg.chunk_bytes % 256 || c->cfg.copy_threads % 32 || c->cfg.copy_threads > 512)
+        return fail(FSW_EINVAL, "fsw_init: chunk_bytes must be a multiple of 256, copy_threads a multiple of 32 <= 512");
+    uint32_t n = c->cfg.n_gpus ? c->cfg.n_gpus : (uint32_t)ndev;
+    c->gpus.resize(n);
+    for (uint32_t i = 0; i < n; ++i) {
+        c->gpus[i].dev = c->cfg.gpu_ids ? c->cfg.gpu_ids[i] : (int)i;
+        if (c->gpus[i].dev < 0 || c->gpus[i].dev >= ndev) return fail(FSW_EINVAL, "fsw_init: bad gpu id %d", c->gpus[i].dev);
+        fsw_status s = init_gpu(c.get(), c->gpus[i]);
+        if (s != FSW_OK) return s;
+    }
+    c->cfg.gpu_ids = nullptr;
+    *out = c.release();
+    return FSW_OK;
+}
+
+static void free_plan(Gpu& g, Plan& p) {
+    cudaSetDevice(g.dev);
+    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second);
+    p.graphs.clear();
+    for (auto& kv : p.pieces) cudaFree(kv.second.dev);
+    p.pieces.clear();
+}
+
+static void free_store(Model& m) {
+    if (!m.store) return;
+    if (m.store_wc) {
+        cudaFreeHost(m.store);
+    } else {
+        cudaHostUnregister(m.store);
+        munmap(m.store, m.store_alloc);
+    }
+    m.store = nullptr;
+}
+
+extern "C" void fsw_shutdown(fsw_ctx* c) {
+    if (!c) return;
+    for (auto& m : c->models) {
+        if (!m) continue;
+        for (size_t i = 0; i < c->gpus.size(); ++i)
+            if (m->plans[i]) free_plan(c->gpus[i], *m->plans[i]);
+        free_store(*m);
+    }
+    for (auto& g : c->gpus) {
+        cudaSetDevice(g.dev);
+        cudaStreamSynchronize(g.sx);
+        cudaStreamSynchronize(g.sc);
+        cudaFree(g.pool);
+        cudaFree(g.ws);
+        cudaFree(g.ready);
+        cudaFree(g.ctl);
+        cudaFree(g.dstage);
+        cudaFreeHost(g.hstage);
+        cudaFreeHost(g.hout);
+        cudaFreeHost(g.hctl);
+        for (cudaEvent_t e : {g.ev0, g.ev1, g.evs0, g.evs1, g.evfork, g.evjoin}) cudaEventDestroy(e);
+        cudaStreamDestroy(g.sx);
+        cudaStreamDestroy(g.sc);
+        fsw_arena_destroy(g.arena);
+    }
+    delete c;
+}
+
+extern "C" fsw_status fsw_n_gpus(fsw_ctx* c, uint32_t* n) {
+    if (!c || !n) return fail(FSW_EINVAL, "fsw_n_gpus: NULL");
+    *n = (uint32_t)c->gpus.size();
+    return FSW_OK;
+}
+
+// ==========================================================================================
+// registration: validation + host store (execution order, GEMM weights tiled)
+// ==========================================================================================
+static uint64_t slot_numel(const fsw_slot& s) {
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < s.rank; ++i) n *= s.shape[i];
+    return n;
+}
+static uint32_t dt_size(uint32_t dt) { return dt == FSW_DT_BF16 ? 2 : 4; }
+static uint64_t slot_bytes(const fsw_slot& s) { return slot_numel(s) * dt_size(s.dtype); }
+static uint32_t slot_cols(const fsw_slot& s) { return s.rank ? s.shape[s.rank - 1] : 1; }
+static uint64_t slot_rows(const fsw_slot& s) { return slot_numel(s) / std::max<uint32_t>(1, slot_cols(s)); }
+
+// Rows of in0 a LINEAR layer reads.
+static uint64_t linear_rows(const Model& m, const fsw_layer& L) {
+    const uint64_t rin = slot_rows(m.slots[L.in0]);
+    return L.attr[2] > 0 ? (uint64_t)L.attr[2] : rin;
+}
+static bool linear_is_gemm(const Model& m, const fsw_layer& L) { return linear_rows(m, L) > 8; }
+
+// Tile order of a GEMM weight W[N][K]: 1024-B atoms of 8 rows x 64 bf16,
+// atoms ordered k-tile-major; inside an atom row r is 128 B at r·128 and its 16-B chunk c
+// sits at chunk position c ^ r (the UMMA/TMA SWIZZLE_128B pattern).  Padding is zero.
+static inline uint64_t tiled_off(uint64_t n, uint64_t k, uint64_t n_pad) {
+    return ((k / 64) * (n_pad / 8) + n / 8) * 1024 + (n % 8) * 128 + ((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
+}
+
+static fsw_status validate(const fsw_model_desc* d) {
+    if (!d || !d->weights || !d->tensors || !d->slots || !d->layers || d->n_layers == 0)
+        return fail(FSW_EINVAL, "register: incomplete description");
+    for (uint32_t i = 0; i < d->n_tensors; ++i) {
+        const fsw_tensor& t = d->tensors[i];
+        if (t.dtype > FSW_DT_F32 || t.rank == 0 || t.rank > 4) return fail(FSW_EINVAL, "tensor %u: bad dtype/rank", i);
+        uint64_t n = 1;
+        for (uint32_t j = 0; j < t.rank; ++j) n *= t.shape[j];
+        if (n * dt_size(t.dtype) != t.bytes) return fail(FSW_EINVAL, "tensor %u: bytes != numel*size", i);
+        if (t.offset % 16) return fail(FSW_EINVAL, "tensor %u: offset not 16-B aligned", i);
+        if (t.offset + t.bytes > d->weight_bytes) return fail(FSW_EINVAL, "tensor %u: beyond weight_bytes", i);
+    }
+    // overlap check
+    std::vector<std::pair<uint64_t, uint64_t>> iv;
+    for (uint32_t i = 0; i < d->n_tensors; ++i) iv.push_back({d->tensors[i].offset, d->tensors[i].offset + d->tensors[i].bytes});
+    std::sort(iv.begin(), iv.end());
+    for (size_t i = 1; i < iv.size(); ++i)
+        if (iv[i].first < iv[i - 1].second) return fail(FSW_EINVAL, "tensors overlap in the weight blob");
+    for (uint32_t i = 0; i < d->n_slots; ++i)
+        if (d->slots[i].dtype > FSW_DT_I32 || d->slots[i].rank == 0 || d->slots[i].rank > 4)
+            return fail(FSW_EINVAL, "slot %u: bad dtype/rank", i);
+    if (d->input_slot < 0 || d->input_slot >= (int)d->n_slots || d->output_slot < 0 || d->output_slot >= (int)d->n_slots)
+        return fail(FSW_EINVAL, "bad input/output slot");
+    for (uint32_t i = 0; i < d->n_refs; ++i)
+        if (d->refs[i] >= d->n_tensors) return fail(FSW_EINVAL, "ref %u out of range", i);
+    for (uint32_t i = 0; i < d->n_layers; ++i) {
+        const fsw_layer& L = d->layers[i];
+        if (L.first_ref + L.n_refs > d->n_refs) return fail(FSW_EINVAL, "layer %u: refs out of range", i);
+        auto bad_slot = [&](int s) { return s < -1 || s >= (int)d->n_slots; };
+        if (bad_slot(L.in0) || bad_slot(L.in1) || L.out < 0 || L.out >= (int)d->n_slots || L.in0 < 0)
+            return fail(FSW_EINVAL, "layer %u: bad slot index", i);
+        if (L.out == L.in0 || L.out == L.in1) return fail(FSW_EINVAL, "layer %u: in-place layers are not allowed", i);
+        if (L.out == d->input_slot) return fail(FSW_EINVAL, "layer %u: writes the input slot", i);
+    }
+    return FSW_OK;
+}
+
+// Per-op checks that depend on shapes and the kernels' supported dtypes.
+static fsw_status check_layer(const Model& m, uint32_t li) {
+    const fsw_layer& L = m.layers[li];
+    const fsw_slot& si = m.slots[L.in0];
+    const fsw_slot& so = m.slots[L.out];
+    auto ref = [&](uint32_t j) -> const fsw_tensor& { return m.tensors[m.refs[L.first_ref + j]].t; };
+    switch (L.op) {
+        case FSW_OP_EMBED: {
+            if (L.attr[0] < 1 || L.attr[0] > 4 || (uint32_t)L.attr[0] != L.n_refs) return fail(FSW_EINVAL, "layer %u: EMBED tables", li);
+            if (si.dtype != FSW_DT_I32 || so.rank != 2 || so.dtype == FSW_DT_I32) return fail(FSW_EINVAL, "layer %u: EMBED slots", li);
+            for (uint32_t j = 0; j < L.n_refs; ++j)
+                if (ref(j).dtype != FSW_DT_BF16 || ref(j).rank != 2 || ref(j).shape[1] != so.shape[1])
+                    return fail(FSW_EINVAL, "layer %u: EMBED table %u shape", li, j);
+            if (slot_numel(si) != so.shape[0]) return fail(FSW_EINVAL, "layer %u: EMBED ids vs rows", li);
+            break;
+        }
+        case FSW_OP_LAYERNORM:
+            if (L.n_refs != 2 || si.dtype != FSW_DT_F32 || so.dtype == FSW_DT_I32 || slot_numel(si) != slot_numel(so))
+                return fail(FSW_EINVAL, "layer %u: LAYERNORM needs f32 input, 2 refs", li);
+            if (slot_cols(si) > 2048 || ref(0).shape[0] != slot_cols(si)) return fail(FSW_EINVAL, "layer %u: LAYERNORM width", li);
+            break;
+        case FSW_OP_LINEAR: {
+            if (L.n_refs < 1 || L.n_refs > 2) return fail(FSW_EINVAL, "layer %u: LINEAR refs", li);
+            const fsw_tensor& W = ref(0);
+            if (W.rank != 2 || W.dtype != FSW_DT_BF16 || W.shape[1] != slot_cols(si)) return fail(FSW_EINVAL, "layer %u: LINEAR W shape", li);
+            if (W.shape[1] % 8) return fail(FSW_EINVAL, "layer %u: LINEAR K must be a multiple of 8", li);
+            const uint64_t rows = linear_rows(m, L);
+            if ((uint64_t)L.attr[1] + rows > slot_rows(si) || slot_numel(so) != rows * W.shape[0] || so.dtype == FSW_DT_I32)
+                return fail(FSW_EINVAL, "layer %u: LINEAR rows/out shape", li);
+            if (L.in1 >= 0 && (slot_numel(m.slots[L.in1]) != slot_numel(so) || m.slots[L.in1].dtype == FSW_DT_I32))
+                return fail(FSW_EINVAL, "layer %u: LINEAR residual shape", li);
+            if (rows > 8) {
+                if (L.attr[1] != 0 || rows != slot_rows(si)) return fail(FSW_EINVAL, "layer %u: GEMM path needs all rows", li);
+                if (slot_cols(si) % 8) return fail(FSW_EINVAL, "layer %u: GEMM K alignment", li);
+            } else if (si.dtype == FSW_DT_I32 || slot_cols(si) * 4 > 200 * 1024 / (rows > 1 ? 8 : 1)) {
+                return fail(FSW_EINVAL, "layer %u: GEMV input too wide", li);
+            }
+            if (L.n_refs == 2 && (ref(1).shape[0] != W.shape[0] || ref(1).dtype != FSW_DT_BF16))
+                return fail(FSW_EINVAL, "layer %u: LINEAR bias", li);
+            break;
+        }
+        case FSW_OP_ATTENTION: {
+            const int H = L.attr[0], dh = L.attr[1];
+            if (si.dtype != FSW_DT_BF16 || so.dtype != FSW_DT_BF16 || si.rank != 2 || H <= 0 || dh <= 0 || dh > 256 ||
+                si.shape[1] != (uint32_t)(3 * H * dh) || so.shape[1] != (uint32_t)(H * dh) || so.shape[0] != si.shape[0] ||
+                si.shape[0] > 256 || dh > 128)
+                return fail(FSW_EINVAL, "layer %u: ATTENTION shapes/dtypes (bf16 qkv [T][3Hdh], T<=256, dh<=128)", li);
+            break;
+        }
+        case FSW_OP_CONV2D: {
+            if (L.n_refs != 2 || si.rank != 3 || so.rank != 3 || si.dtype != FSW_DT_BF16 || so.dtype != FSW_DT_BF16)
+                return fail(FSW_EINVAL, "layer %u: CONV2D needs bf16 NHWC slots and W, b", li);
+            const fsw_tensor& W = ref(0);
+            if (W.rank != 4 || W.shape[0] != so.shape[2] || W.shape[3] != si.shape[2] || W.shape[1] != W.shape[2])
+                return fail(FSW_EINVAL, "layer %u: CONV2D weight shape", li);
+            const int st = L.attr[1], pad = L.attr[2];
+            if (st < 1 || pad < 0) return fail(FSW_EINVAL, "layer %u: CONV2D stride/pad", li);
+            const uint32_t ho = (si.shape[0] + 2 * pad - W.shape[1]) / st + 1, wo = (si.shape[1] + 2 * pad - W.shape[2]) / st + 1;
+            if (so.shape[0] != ho || so.shape[1] != wo) return fail(FSW_EINVAL, "layer %u: CONV2D output size", li);
+            if (so.shape[2] % 8) return fail(FSW_EINVAL, "layer %u: CONV2D Cout must be a multiple of 8", li);
+            if (L.in1 >= 0 && (m.slots[L.in1].dtype != FSW_DT_BF16 || slot_numel(m.slots[L.in1]) != slot_numel(so)))
+                return fail(FSW_EINVAL, "layer %u: CONV2D residual", li);
+            break;
+        }
+        case FSW_OP_MAXPOOL:
+            if (si.rank != 3 || so.rank != 3 || si.dtype != FSW_DT_BF16 || so.dtype != FSW_DT_BF16 || si.shape[2] != so.shape[2])
+                return fail(FSW_EINVAL, "layer %u: MAXPOOL", li);
+            break;
+        case FSW_OP_AVGPOOL:
+            if (si.rank != 3 || si.dtype != FSW_DT_BF16 || so.dtype != FSW_DT_F32 || slot_numel(so) != si.shape[2])
+                return fail(FSW_EINVAL, "layer %u: AVGPOOL", li);
+            break;
+        default:
+            return fail(FSW_EINVAL, "layer %u: unknown op %u", li, L.op);
+    }
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, uint32_t* model_id) {
+    if (!c || !model_id) return fail(FSW_EINVAL, "register: NULL argument");
+    fsw_status s = validate(d);
+    if (s != FSW_OK) return s;
+    auto m = std::make_unique<Model>();
+    m->name = d->name ? d->name : "";
+    m->tensors.resize(d->n_tensors);
+    for (uint32_t i = 0; i < d->n_tensors; ++i) {
+        m->tensors[i].t = d->tensors[i];
+        m->algorithmic_bytes += d->tensors[i].bytes;
+    }
+    m->refs.assign(d->refs, d->refs + d->n_refs);
+    m->slots.assign(d->slots, d->slots + d->n_slots);
+    m->layers.assign(d->layers, d->layers + d->n_layers);
+    m->input_slot = d->input_slot;
+    m->output_slot = d->output_slot;
+    m->input_bytes = slot_bytes(m->slots[d->input_slot]);
+    m->output_bytes = slot_bytes(m->slots[d->output_slot]);
+    for (uint32_t i = 0; i < d->n_layers; ++i)
+        if ((s = check_layer(*m, i)) != FSW_OK) return s;
+
+    // --- layouts: GEMM weights tiled, everything else row-major ---
+    for (uint32_t li = 0; li < d->n_layers; ++li) {
+        const fsw_layer& L = m->layers[li];
+        const bool gemm = L.op == FSW_OP_CONV2D || (L.op == FSW_OP_LINEAR && linear_is_gemm(*m, L));
+        if (gemm) m->n_gemm++;
+        for (uint32_t j = 0; j < L.n_refs; ++j) {
+            TensorInfo& ti = m->tensors[m->refs[L.first_ref + j]];
+            const bool want_tiled = gemm && j == 0;
+            if (ti.owner >= 0) {
+                if ((ti.layout == LAYOUT_TILED) != want_tiled)
+                    return fail(FSW_EINVAL, "layer %u: tensor shared between a GEMM and a non-GEMM use", li);
+                continue;
+            }
+            ti.owner = (int)li;
+            if (want_tiled) {
+                ti.layout = LAYOUT_TILED;
+                ti.rows = ti.t.shape[0];
+                ti.cols = (uint32_t)(ti.t.bytes / 2 / ti.t.shape[0]);
+                ti.rows_pad = (uint32_t)align_up(ti.rows, 16);
+                ti.cols_pad = (uint32_t)align_up(ti.cols, 64);
+                ti.st_bytes = (uint64_t)ti.rows_pad * ti.cols_pad * 2;
+            } else {
+                ti.layout = LAYOUT_ROWMAJOR;
+                ti.st_bytes = ti.t.bytes;
+            }
+        }
+    }
+    // --- store offsets: layer regions in execution order, 256-B aligned ---
+    m->region_off.assign(d->n_layers, 0);
+    m->region_bytes.assign(d->n_layers, 0);
+    uint64_t cur = 0;
+    for (uint32_t li = 0; li < d->n_layers; ++li) {
+        const fsw_layer& L = m->layers[li];
+        m->region_off[li] = cur;
+        for (uint32_t j = 0; j < L.n_refs; ++j) {
+            TensorInfo& ti = m->tensors[m->refs[L.first_ref + j]];
+            if (ti.owner != (int)li || ti.placed) continue;  // owned by an earlier layer / listed twice
+            ti.placed = true;
+            ti.st_off = cur;
+            cur = align_up(cur + ti.st_bytes, 256);
+        }
+        m->region_bytes[li] = cur - m->region_off[li];
+        if (m->region_bytes[li] >= (1ull << 32)) return fail(FSW_EINVAL, "layer %u: weights exceed 4 GiB", li);
+    }
+    // tensors not referenced by any layer are not swapped (not part of the access pattern)
+    m->store_bytes = cur;
+    if (m->store_bytes == 0) return fail(FSW_EINVAL, "register: model has no weights");
+
+    // --- host store: pinned + mapped (cudaHostRegister of THP-backed mmap), or WC pinned ---
+    const bool wc = (c->cfg.flags & FSW_HOST_WC) != 0;
+    m->store_alloc = align_up(m->store_bytes, 2 << 20);
+    if (wc) {
+        CU(cudaSetDevice(c->gpus[0].dev));
+        void* p = nullptr;
+        CU(cudaHostAlloc(&p, m->store_alloc, cudaHostAllocPortable | cudaHostAllocMapped | cudaHostAllocWriteCombined));
+        m->store = static_cast<uint8_t*>(p);
+        m->store_wc = true;
+    } else {
+        void* p = mmap(nullptr, m->store_alloc, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (p == MAP_FAILED) return fail(FSW_ENOMEM, "register: mmap of %llu bytes failed", (unsigned long long)m->store_alloc);
+        madvise(p, m->store_alloc, MADV_HUGEPAGE);
+        m->store = static_cast<uint8_t*>(p);
+    }
+    // pack (zero padding everywhere; first touch happens here)
+    const uint8_t* src = static_cast<const uint8_t*>(d->weights);
+    memset(m->store, 0, m->store_alloc);
+    for (auto& ti : m->tensors) {
+        if (ti.owner < 0) continue;
+        if (ti.layout == LAYOUT_ROWMAJOR) {
+            memcpy(m->store + ti.st_off, src + ti.t.offset, ti.t.bytes);
+        } else {
+            const uint16_t* w = reinterpret_cast<const uint16_t*>(src + ti.t.offset);
+            for (uint64_t n = 0; n < ti.rows; ++n)
+                for (uint64_t k = 0; k < ti.cols; ++k)
+                    memcpy(m->store + ti.st_off + tiled_off(n, k, ti.rows_pad), &w[n * ti.cols + k], 2);
+        }
+    }
+    if (!wc) {
+        CU(cudaSetDevice(c->gpus[0].dev));
+        cudaError_t e = cudaHostRegister(m->store, m->store_alloc, cudaHostRegisterPortable | cudaHostRegisterMapped);
+        if (e != cudaSuccess) {
+            munmap(m->store, m->store_alloc);
+            m->store = nullptr;
+            return fail(FSW_ECUDA, "register: cudaHostRegister: %s", cudaGetErrorString(e));
+        }
+    }
+    m->extent.assign(c->gpus.size(), -1);
+    m->last_use.assign(c->gpus.size(), 0);
+    m->plans.resize(c->gpus.size());
+    std::lock_guard<std::mutex> lk(c->mu);
+    m->id = (uint32_t)c->models.size();
+    *model_id = m->id;
+    c->models.push_back(std::move(m));
+    return FSW_OK;
+}
+
+static Model* find_model(fsw_ctx* c, uint32_t id) {
+    if (!c || id >= c->models.size()) return nullptr;
+    return c->models[id].get();
+}
+
+extern "C" fsw_status fsw_model_info_get(fsw_ctx* c, uint32_t id, fsw_model_info* out) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!out) return fail(FSW_EINVAL, "NULL out");
+    out->store_bytes = m->store_bytes;
+    out->algorithmic_bytes = m->algorithmic_bytes;
+    out->n_layers = (uint32_t)m->layers.size();
+    out->n_tensors = (uint32_t)m->tensors.size();
+    out->n_gemm_layers = m->n_gemm;
+    out->input_bytes = m->input_bytes;
+    out->output_bytes = m->output_bytes;
+    out->output_dtype = m->slots[m->output_slot].dtype;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_store_tensor_get(fsw_ctx* c, uint32_t id, uint32_t t, fsw_store_tensor* out) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!out || t >= m->tensors.size()) return fail(FSW_EINVAL, "bad tensor index");
+    const TensorInfo& ti = m->tensors[t];
+    *out = {ti.st_off, ti.st_bytes, ti.layout, ti.rows, ti.cols, ti.rows_pad, ti.cols_pad, (uint32_t)ti.owner};
+    return FSW_OK;
+}
+
+// ==========================================================================================
+// plan: workspace layout + kernel list for one (model, GPU)
+// ==========================================================================================
+static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
+    Gpu& g = c->gpus[gi];
+    auto p = std::make_unique<Plan>();
+    const size_t ns = m.slots.size();
+    // which f32 slots feed a GEMM (need a bf16 shadow)
+    std::vector<bool> need_shadow(ns, false);
+    uint64_t scratch = 0;  // im2col scratch
+    for (auto& L : m.layers) {
+        if (L.op == FSW_OP_LINEAR && linear_is_gemm(m, L) && m.slots[L.in0].dtype == FSW_DT_F32) need_shadow[L.in0] = true;
+        if (L.op == FSW_OP_CONV2D) {
+            const fsw_slot& si = m.slots[L.in0];
+            const fsw_slot& so = m.slots[L.out];
+            const fsw_tensor& W = m.tensors[m.refs[L.first_ref]].t;
+            const bool direct = W.shape[1] == 1 && L.attr[1] == 1 && L.attr[2] == 0 && si.shape[2] % 64 == 0;
+            if (!direct) {
+                const uint64_t K = (uint64_t)W.shape[1] * W.shape[2] * W.shape[3];
+                scratch = std::max(scratch, (uint64_t)so.shape[0] * so.shape[1] * align_up(K, 64) * 2);
+            }
+        }
+    }
+    uint64_t off = 0;
+    p->slot_off.resize(ns);
+    p->shadow_off.assign(ns, -1);
+    const uint64_t stage_input_off = kStageHdr;  // input slot lives in the device stage
+    for (size_t i = 0; i < ns; ++i) {
+        if ((int)i == m.input_slot) {
+            p->slot_off[i] = UINT64_MAX;
+            continue;
+        }
+        p->slot_off[i] = off;
+        off = align_up(off + slot_bytes(m.slots[i]), 1024);
+        if (need_shadow[i]) {
+            p->shadow_off[i] = (int64_t)off;
+            off = align_up(off + slot_numel(m.slots[i]) * 2, 1024);
+        }
+    }
+    const uint64_t scratch_off = off;
+    off = align_up(off + scratch, 1024);
+    p->ws_bytes = off;
+    if (off > g.ws_bytes) return fail(FSW_ENOMEM, "plan: workspace needs %llu bytes > %llu", (unsigned long long)off, (unsigned long long)g.ws_bytes);
+    if (m.input_bytes + kStageHdr > g.stage_cap || m.output_bytes > g.out_cap) return fail(FSW_ENOMEM, "plan: input/output too large");
+
+    auto sptr = [&](int s) -> uint8_t* {
+        if (s < 0) return nullptr;
+        if (s == m.input_slot) return g.dstage + stage_input_off;
+        return g.ws + p->slot_off[s];
+    };
+    auto shadow = [&](int s) -> uint16_t* {
+        return (s >= 0 && p->shadow_off[s] >= 0) ? reinterpret_cast<uint16_t*>(g.ws + p->shadow_off[s]) : nullptr;
+    };
+    auto ref = [&](const fsw_layer& L, uint32_t j) -> const TensorInfo& { return m.tensors[m.refs[L.first_ref + j]]; };
+    auto pick_bn = [](uint32_t n_pad, uint64_t m_tiles) {
+        // small-M GEMMs are weight-streaming: prefer more CTAs (narrow tiles) when the grid is small
+        for (int bn : {128, 64, 32, 16})
+            if (n_pad % bn == 0 && m_tiles * (n_pad / bn) >= 120) return bn;
+        for (int bn : {16, 32, 64, 128})
+            if (n_pad % bn == 0) return bn;
+        return 16;
+    };
+
+    CU(cudaSetDevice(g.dev));
+    for (uint32_t li = 0; li < m.layers.size(); ++li) {
+        const fsw_layer& L = m.layers[li];
+        const fsw_slot& si = m.slots[L.in0];
+        const fsw_slot& so = m.slots[L.out];
+        Launch x{};
+        x.layer = (int)li;
+        switch (L.op) {
+            case FSW_OP_EMBED: {
+                x.kind = K_EMBED;
+                EmbedArgs& a = x.embed;
+                a.ids = reinterpret_cast<const int32_t*>(sptr(L.in0));
+                a.n_tables = L.attr[0];
+                for (int j = 0; j < a.n_tables; ++j) {
+                    a.table_off[j] = ref(L, j).st_off;
+                    a.table_rows[j] = ref(L, j).t.shape[0];
+                    a.rule[j] = L.attr[1 + j];
+                }
+                a.T = so.shape[0];
+                a.C = so.shape[1];
+                if (so.dtype == FSW_DT_F32) {
+                    a.out = reinterpret_cast<float*>(sptr(L.out));
+                    a.out_bf16 = shadow(L.out);
+                } else {
+                    a.out_bf16 = reinterpret_cast<uint16_t*>(sptr(L.out));
+                }
+                break;
+            }
+            case FSW_OP_LAYERNORM: {
+                x.kind = K_LN;
+                LnArgs& a = x.ln;
+                a.in = reinterpret_cast<const float*>(sptr(L.in0));
+                a.C = slot_cols(si);
+                a.rows = (uint32_t)slot_rows(si);
+                float eps;
+                memcpy(&eps, &L.attr[0], 4);
+                a.eps = eps;
+                a.g_off = ref(L, 0).st_off;
+                a.b_off = ref(L, 1).st_off;
+                if (so.dtype == FSW_DT_F32) {
+                    a.out_f32 = reinterpret_cast<float*>(sptr(L.out));
+                    a.out_bf16 = shadow(L.out);
+                } else {
+                    a.out_bf16 = reinterpret_cast<uint16_t*>(sptr(L.out));
+                }
+                break;
+            }
+            case FSW_OP_LINEAR: {
+                const TensorInfo& W = ref(L, 0);
+                const bool has_b = L.n_refs > 1;
+                if (!linear_is_gemm(m, L)) {
+                    x.kind = K_GEMV;
+                    GemvArgs& a = x.gemv;
+                    a.x = sptr(L.in0);
+                    a.x_bf16 = si.dtype == FSW_DT_BF16;
+                    a.ldx = slot_cols(si);
+                    a.r0 = (uint32_t)L.attr[1];
+                    a.rows = (uint32_t)linear_rows(m, L);
+                    a.K = W.t.shape[1];
+                    a.N = W.t.shape[0];
+                    a.w_off = W.st_off;
+                    a.has_bias = has_b;
+                    a.b_off = has_b ? ref(L, 1).st_off : 0;
+                    a.act = L.attr[0];
+                    a.res = sptr(L.in1);
+                    a.res_bf16 = L.in1 >= 0 && m.slots[L.in1].dtype == FSW_DT_BF16;
+                    a.out = sptr(L.out);
+                    a.out_bf16 = so.dtype == FSW_DT_BF16;
+                    a.out2 = shadow(L.out);
+                } else {
+                    x.kind = K_GEMM;
+                    GemmArgs& a = x.gemm;
+                    a.M = (uint32_t)slot_rows(si);
+                    a.N = W.rows;
+                    a.K = W.cols_pad;
+                    a.n_pad = W.rows_pad;
+                    a.w_off = W.st_off;
+                    a.has_bias = has_b;
+                    a.b_off = has_b ? ref(L, 1).st_off : 0;
+                    a.act = L.attr[0];
+                    a.res = sptr(L.in1);
+                    a.res_bf16 = L.in1 >= 0 && m.slots[L.in1].dtype == FSW_DT_BF16;
+                    a.ld_res = a.N;
+                    a.out = sptr(L.out);
+                    a.out_bf16 = so.dtype == FSW_DT_BF16;
+                    a.ld_out = a.N;
+                    a.out2 = shadow(L.out);
+                    a.bn = pick_bn(a.n_pad, (a.M + 127) / 128);
+                    const void* abase = si.dtype == FSW_DT_BF16 ? (const void*)sptr(L.in0) : (const void*)shadow(L.in0);
+                    if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si)))
+                        return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                }
+                break;
+            }
+            case FSW_OP_ATTENTION: {
+                x.kind = K_ATTN;
+                x.attn = {reinterpret_cast<const uint16_t*>(sptr(L.in0)), reinterpret_cast<uint16_t*>(sptr(L.out)),
+                          si.shape[0], (uint32_t)L.attr[0], (uint32_t)L.attr[1], L.attr[2]};
+                break;
+            }
+            case FSW_OP_CONV2D: {
+                const TensorInfo& W = ref(L, 0);
+                const uint32_t R = W.t.shape[1], S = W.t.shape[2], Cin = W.t.shape[3];
+                const bool direct = R == 1 && L.attr[1] == 1 && L.attr[2] == 0 && Cin % 64 == 0;
+                const uint32_t P = so.shape[0], Q = so.shape[1];
+                const void* abase = sptr(L.in0);
+                uint32_t acols = Cin;
+                if (!direct) {
+                    Launch y{};
+                    y.kind = K_IM2COL;
+                    y.layer = (int)li;
+                    y.im2col = {reinterpret_cast<const uint16_t*>(sptr(L.in0)), si.shape[0], si.shape[1], Cin,
+                                reinterpret_cast<uint16_t*>(g.ws + scratch_off), P, Q, R, S, (uint32_t)L.attr[1],
+                                (uint32_t)L.attr[2], R * S * Cin, W.cols_pad};
+                    p->launches.push_back(y);
+                    abase = g.ws + scratch_off;
+                    acols = W.cols_pad;
+                }
+                x.kind = K_GEMM;
+                GemmArgs& a = x.gemm;
+                a.M = P * Q;
+                a.N = W.rows;
+                a.K = W.cols_pad;
+                a.n_pad = W.rows_pad;
+                a.w_off = W.st_off;
+                a.has_bias = 1;
+                a.b_off = ref(L, 1).st_off;
+                a.act = L.attr[0];
+                a.res = sptr(L.in1);
+                a.res_bf16 = 1;
+                a.ld_res = a.N;
+                a.out = sptr(L.out);
+                a.out_bf16 = 1;
+                a.ld_out = a.N;
+                a.out2 = nullptr;
+                a.bn = pick_bn(a.n_pad, (a.M + 127) / 128);
+                if (!make_tmap_act(&x.tmap, abase, a.M, acols, acols))
+                    return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                break;
+            }
+            case FSW_OP_MAXPOOL:
+            case FSW_OP_AVGPOOL: {
+                x.kind = L.op == FSW_OP_MAXPOOL ? K_MAXPOOL : K_AVGPOOL;
+                PoolArgs& a = x.pool;
+                a.in = reinterpret_cast<const uint16_t*>(sptr(L.in0));
+                a.H = si.shape[0];
+                a.W = si.shape[1];
+                a.C = si.shape[2];
+                if (L.op == FSW_OP_MAXPOOL) {
+                    a.P = so.shape[0];
+                    a.Q = so.shape[1];
+                    a.k = L.attr[0];
+                    a.stride = L.attr[1];
+                    a.pad = L.attr[2];
+                    a.out = reinterpret_cast<uint16_t*>(sptr(L.out));
+                } else {
+                    a.out_f32 = reinterpret_cast<float*>(sptr(L.out));
+                }
+                break;
+            }
+        }
+        p->launches.push_back(x);
+    }
+    p->built = true;
+    m.plans[gi] = std::move(p);
+    return FSW_OK;
+}
+
+// Swap pieces for one chunk size / order: execution order, never straddling a layer region.
+static fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint32_t seed, PieceSet** out) {
+    auto key = std::make_tuple(chunk, order, seed);
+    auto it = p.pieces.find(key);
+    if (it != p.pieces.end()) {
+        *out = &it->second;
+        return FSW_OK;
+    }
+    PieceSet ps;
+    for (uint32_t li = 0; li < m.layers.size(); ++li)
+        for (uint64_t o = 0; o < m.region_bytes[li]; o += chunk)
+            ps.host.push_back({m.region_off[li] + o, (uint32_t)std::min<uint64_t>(chunk, m.region_bytes[li] - o), li});
+    if (order == FSW_ORDER_REVERSE) std::reverse(ps.host.begin(), ps.host.end());
+    if (order == FSW_ORDER_RANDOM) {
+        std::mt19937_64 rng(seed);
+        std::shuffle(ps.host.begin(), ps.host.end(), rng);
+    }
+    CU(cudaSetDevice(g.dev));
+    CU(cudaMalloc(&ps.dev, sizeof(Piece) * ps.host.size()));
+    CU(cudaMemcpy(ps.dev, ps.host.data(), sizeof(Piece) * ps.host.size(), cudaMemcpyHostToDevice));
+    auto res = p.pieces.emplace(key, std::move(ps));
+    *out = &res.first->second;
+    return FSW_OK;
+}
+
+static void enqueue_layers(Model& m, Plan& p, Gpu& g, bool cold, cudaStream_t s) {
+    const DevDesc* d = reinterpret_cast<const DevDesc*>(g.dstage);
+    for (const Launch& x : p.launches) {
+        Wait w{nullptr, 0, g.ctl, x.layer};
+        const bool has_weights = m.region_bytes[x.layer] > 0;
+        if (cold && has_weights) {
+            w.ready = g.ready + x.layer;
+            w.target = (uint32_t)m.region_bytes[x.layer];
+        }
+        switch (x.kind) {
+            case K_EMBED: launch_embed(s, d, w, x.embed); break;
+            case K_LN: launch_layernorm(s, d, w, x.ln); break;
+            case K_GEMV: launch_gemv(s, d, w, x.gemv); break;
+            case K_GEMM: launch_gemm(s, d, w, &x.tmap, x.gemm); break;
+            case K_ATTN: launch_attention(s, x.attn); break;
+            case K_IM2COL: launch_im2col(s, x.im2col); break;
+            case K_MAXPOOL: launch_maxpool(s, x.pool); break;
+            case K_AVGPOOL: launch_avgpool(s, x.pool); break;
+        }
+    }
+}
+
+struct InvokeCfg {
+    bool cold, dma, no_overlap;
+    uint64_t chunk;
+    int order;
+    uint32_t seed, ctas;
+    uint8_t* wbase;  // only used by DMA graphs (memcpy nodes need absolute addresses)
+};
+
+// Capture the invoke graph of (model, GPU, cfg).  Root: H2D of [desc | input]; cold adds the
+// ready/ctl reset, the swap kernel on its own stream (bracketed by external event nodes for
+// timing) and the gate; then the flag-gated layer kernels; then D2H of output and ctl.
+static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out) {
+    PieceSet* ps = nullptr;
+    if (ic.cold) {
+        fsw_status s = get_pieces(m, p, g, ic.chunk, ic.order, ic.seed, &ps);
+        if (s != FSW_OK) return s;
+        if (m.layers.size() > g.ready_cap) return fail(FSW_EINVAL, "too many layers");
+    }
+    CU(cudaSetDevice(g.dev));
+    cudaStream_t sx = g.sx, sc = g.sc;
+    CU(cudaStreamBeginCapture(sx, cudaStreamCaptureModeThreadLocal));
+    cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr + m.input_bytes, cudaMemcpyHostToDevice, sx);
+    cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
+    if (ic.cold) {
+        cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
+        cudaEventRecord(g.evfork, sx);
+        cudaStreamWaitEvent(sc, g.evfork, 0);
+        cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
+        if (!ic.dma) {
+            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, reinterpret_cast<const DevDesc*>(g.dstage),
+                        ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl);
+        } else {
+            for (size_t i = 0; i < ps->host.size(); ++i) {
+                const Piece& pc = ps->host[i];
+                cudaMemcpyAsync(ic.wbase + pc.off, m.store + pc.off, pc.bytes, cudaMemcpyHostToDevice, sc);
+                launch_signal(sc, g.ready, pc.layer, pc.bytes, g.ctl, i + 1 == ps->host.size());
+            }
+        }
+        cudaEventRecordWithFlags(g.evs1, sc, cudaEventRecordExternal);
+        cudaEventRecord(g.evjoin, sc);
+        if (ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
+        else if (!ic.dma) launch_gate(sx, g.ctl, ic.ctas);
+    }
+    enqueue_layers(m, p, g, ic.cold, sx);
+    launch_finish(sx, g.ctl);
+    if (ic.cold && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
+    cudaMemcpyAsync(g.hout, g.ws + p.slot_off[m.output_slot], m.output_bytes, cudaMemcpyDeviceToHost, sx);
+    cudaMemcpyAsync(g.hctl, g.ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, sx);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(sx, &graph);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FSW_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    }
+    e = cudaGraphInstantiate(out, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(FSW_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+    return FSW_OK;
+}
+
+// ==========================================================================================
+// pool residency
+// ==========================================================================================
+static void invalidate(fsw_ctx* c, Model& m, int gi) {
+    if (m.extent[gi] < 0) return;
+    fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.extent[gi]);
+    m.extent[gi] = -1;
+}
+
+// Allocate an extent for m on GPU gi, evicting idle LRU models there.
+static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
+    Gpu& g = c->gpus[gi];
+    for (;;) {
+        uint64_t off = 0;
+        if (fsw_arena_alloc(g.arena, m.store_bytes, &off) == FSW_OK) {
+            m.extent[gi] = (int64_t)off;
+            return FSW_OK;
+        }
+        Model* victim = nullptr;
+        for (auto& o : c->models)
+            if (o && o.get() != &m && o->extent[gi] >= 0 && o->inflight == 0 &&
+                (!victim || o->last_use[gi] < victim->last_use[gi]))
+                victim = o.get();
+        if (!victim)
+            return fail(FSW_ENOMEM, "pool on gpu %d cannot hold %llu bytes even after evicting every idle model", g.dev,
+                        (unsigned long long)m.store_bytes);
+        invalidate(c, *victim, gi);
+        g.n_evictions++;
+    }
+}
+
+extern "C" fsw_status fsw_evict(fsw_ctx* c, uint32_t id, int32_t gpu) {
+    if (!c) return fail(FSW_EINVAL, "NULL ctx");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (m->inflight) return fail(FSW_EBUSY, "model %u has an invoke in flight", id);
+    if (gpu >= (int)c->gpus.size() || gpu < -1) return fail(FSW_EINVAL, "bad gpu %d", gpu);
+    if (gpu >= 0) {
+        if (m->extent[gpu] < 0) return fail(FSW_ESTATE, "model %u is not resident on gpu %d", id, gpu);
+        invalidate(c, *m, gpu);
+        c->gpus[gpu].n_evictions++;
+        return FSW_OK;
+    }
+    for (size_t i = 0; i < c->gpus.size(); ++i)
+        if (m->extent[i] >= 0) {
+            invalidate(c, *m, (int)i);
+            c->gpus[i].n_evictions++;
+        }
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_unregister_model(fsw_ctx* c, uint32_t id) {
+    if (!c) return fail(FSW_EINVAL, "NULL ctx");
+    std::unique_ptr<Model> m;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        Model* mp = find_model(c, id);
+        if (!mp) return fail(FSW_ENOTFOUND, "model %u not found", id);
+        if (mp->inflight) return fail(FSW_EBUSY, "model %u has an invoke in flight", id);
+        for (size_t i = 0; i < c->gpus.size(); ++i) invalidate(c, *mp, (int)i);
+        m = std::move(c->models[id]);
+    }
+    for (size_t i = 0; i < c->gpus.size(); ++i)
+        if (m->plans[i]) free_plan(c->gpus[i], *m->plans[i]);
+    free_store(*m);
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_pool_stats_get(fsw_ctx* c, int32_t gpu, fsw_pool_stats* out) {
+    if (!c || !out || gpu < 0 || gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "pool_stats: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Gpu& g = c->gpus[gpu];
+    memset(out, 0, sizeof *out);
+    out->capacity = g.pool_bytes;
+    fsw_arena_stats(g.arena, &out->used, &out->largest_free, &out->n_extents);
+    for (auto& m : c->models)
+        if (m && m->extent[gpu] >= 0) out->n_resident++;
+    out->n_evictions = g.n_evictions;
+    out->bytes_swapped_total = g.bytes_swapped_total;
+    out->n_invokes_cold = g.n_cold;
+    out->n_invokes_warm = g.n_warm;
+    return FSW_OK;
+}
+
+// ==========================================================================================
+// invoke
+// ==========================================================================================
+static int pick_gpu(fsw_ctx* c, Model& m) {
+    for (size_t i = 0; i < c->gpus.size(); ++i)
+        if (!c->gpus[i].busy && m.extent[i] >= 0) return (int)i;  // resident and idle
+    for (size_t i = 0; i < c->gpus.size(); ++i)
+        if (!c->gpus[i].busy) return (int)i;  // lowest idle id
+    return -1;
+}
+
+extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_opts* opts, const void* input,
+                                    uint64_t input_bytes, void* output, uint64_t output_cap, fsw_invoke_stats* stats) {
+    const double t_entry = now_ms();
+    if (!c || !input || !output) return fail(FSW_EINVAL, "invoke: NULL argument");
+    fsw_invoke_opts o{};
+    o.gpu = -1;
+    if (opts) o = *opts;
+    Model* m = nullptr;
+    int gi = -1;
+    bool cold = false;
+    {
+        std::unique_lock<std::mutex> lk(c->mu);
+        m = find_model(c, id);
+        if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+        if (input_bytes != m->input_bytes) return fail(FSW_EINVAL, "invoke: input_bytes %llu != %llu", (unsigned long long)input_bytes, (unsigned long long)m->input_bytes);
+        if (output_cap < m->output_bytes) return fail(FSW_EINVAL, "invoke: output_cap too small (%llu < %llu)", (unsigned long long)output_cap, (unsigned long long)m->output_bytes);
+        if (o.gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "invoke: bad gpu %d", o.gpu);
+        for (;;) {
+            gi = o.gpu >= 0 ? (c->gpus[o.gpu].busy ? -1 : o.gpu) : pick_gpu(c, *m);
+            if (gi >= 0) break;
+            c->cv.wait(lk);
+        }
+        Gpu& g = c->gpus[gi];
+        g.busy = true;
+        m->inflight++;
+        cold = m->extent[gi] < 0;
+        if (cold) {
+            fsw_status s = ensure_extent(c, *m, gi);
+            if (s != FSW_OK) {
+                g.busy = false;
+                m->inflight--;
+                c->cv.notify_all();
+                return s;
+            }
+        }
+        m->last_use[gi] = ++c->clock;
+    }
+    Gpu& g = c->gpus[gi];
+    fsw_status st = FSW_OK;
+    auto finish = [&](fsw_status s) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (s != FSW_OK && cold) invalidate(c, *m, gi);  // failed swap: extent is not valid
+        g.busy = false;
+        m->inflight--;
+        c->cv.notify_all();
+        return s;
+    };
+    if (cudaSetDevice(g.dev) != cudaSuccess) return finish(fail(FSW_ECUDA, "cudaSetDevice"));
+    if (!m->plans[gi]) {
+        st = build_plan(c, *m, gi);
+        if (st != FSW_OK) return finish(st);
+    }
+    Plan& p = *m->plans[gi];
+    const uint32_t flags = o.flags | c->cfg.flags;
+    InvokeCfg ic{cold, (flags & FSW_DMA_BASELINE) != 0, (flags & FSW_NO_OVERLAP) != 0,
+                 o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
+                 o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, g.pool + (m->extent[gi] >= 0 ? m->extent[gi] : 0)};
+    if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
+    GraphKey key{cold, (int)(flags & (FSW_DMA_BASELINE | FSW_NO_OVERLAP)), cold ? ic.order : 0, cold ? ic.chunk : 0,
+                 cold ? ic.seed : 0, cold ? ic.ctas : 0, 0};
+    if (cold && ic.dma) key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);  // DMA graphs bake addresses
+    auto it = p.graphs.find(key);
+    cudaGraphExec_t exec = nullptr;
+    if (it == p.graphs.end()) {
+        st = build_graph(c, *m, p, g, ic, &exec);
+        if (st != FSW_OK) return finish(st);
+        p.graphs[key] = exec;
+    } else {
+        exec = it->second;
+    }
+    // stage: descriptor + input (pinned), one H2D node in the graph
+    DevDesc dd{g.pool + m->extent[gi], ++g.generation};
+    memcpy(g.hstage, &dd, sizeof dd);
+    memcpy(g.hstage + kStageHdr, input, input_bytes);
+    cudaEventRecord(g.ev0, g.sx);
+    cudaError_t e = cudaGraphLaunch(exec, g.sx);
+    cudaEventRecord(g.ev1, g.sx);
+    if (e == cudaSuccess) e = cudaEventSynchronize(g.ev1);
+    if (e != cudaSuccess) return finish(fail(FSW_ECUDA, "invoke: graph launch/sync: %s", cudaGetErrorString(e)));
+    const DevCtl ctl = *g.hctl;
+    if (ctl.err) {
+        const char* what = ctl.err == 1 ? "ready-flag watchdog" : ctl.err == 2 ? "swap-gate watchdog" : "embedding id out of range";
+        return finish(fail(ctl.err == 3 ? FSW_EINVAL : FSW_ETIMEOUT, "invoke: %s (layer %d)", what, ctl.err_layer));
+    }
+    memcpy(output, g.hout, m->output_bytes);
+    if (stats) {
+        memset(stats, 0, sizeof *stats);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, g.ev0, g.ev1);
+        stats->device_ms = ms;
+        stats->gpu = gi;
+        stats->n_sources = cold ? 1 : 0;
+        stats->swap_kind = cold ? FSW_SWAP_HOST : FSW_SWAP_RESIDENT;
+        stats->n_kernels = (uint32_t)p.launches.size() + 1 /*finish*/;
+        if (cold) {
+            float sm = 0;
+            cudaEventElapsedTime(&sm, g.evs0, g.evs1);
+            stats->swap_ms = sm;
+            stats->bytes_swapped = m->store_bytes;
+            stats->link_gbps = sm > 0 ? m->store_bytes / (sm * 1e6) : 0;
+            if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
+            if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
+            if (!ic.dma) stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)
+            else stats->n_kernels += (uint32_t)p.pieces.begin()->second.host.size();
+        }
+    }
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        if (cold) {
+            g.n_cold++;
+            g.bytes_swapped_total += m->store_bytes;
+        } else {
+            g.n_warm++;
+        }
+    }
+    finish(FSW_OK);
+    if (stats) stats->total_ms = now_ms() - t_entry;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_invoke(fsw_ctx* c, uint32_t id, const void* input, uint64_t input_bytes, void* output,
+                                 uint64_t output_cap, fsw_invoke_stats* stats) {
+    return fsw_invoke_ex(c, id, nullptr, input, input_bytes, output, output_cap, stats);
+}
+
+// ==========================================================================================
+// debug read-back
+// ==========================================================================================
+extern "C" fsw_status fsw_debug_read_resident(fsw_ctx* c, uint32_t id, int32_t gpu, void* dst, uint64_t cap) {
+    if (!c || !dst || gpu < 0 || gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "read_resident: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (m->extent[gpu] < 0) return fail(FSW_ESTATE, "model %u not resident on gpu %d", id, gpu);
+    if (cap < m->store_bytes) return fail(FSW_EINVAL, "read_resident: cap too small");
+    CU(cudaSetDevice(c->gpus[gpu].dev));
+    CU(cudaMemcpy(dst, c->gpus[gpu].pool + m->extent[gpu], m->store_bytes, cudaMemcpyDeviceToHost));
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_read_store(fsw_ctx* c, uint32_t id, void* dst, uint64_t cap) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!dst || cap < m->store_bytes) return fail(FSW_EINVAL, "read_store: cap too small");
+    memcpy(dst, m->store, m->store_bytes);
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_read_slot(fsw_ctx* c, uint32_t id, int32_t gpu, int32_t slot, void* dst, uint64_t cap) {
+    if (!c || !dst || gpu < 0 || gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "read_slot: bad argument");
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (slot < 0 || slot >= (int)m->slots.size()) return fail(FSW_EINVAL, "read_slot: bad slot");
+    if (!m->plans[gpu]) return fail(FSW_ESTATE, "read_slot: model never ran on gpu %d", gpu);
+    const uint64_t b = slot_bytes(m->slots[slot]);
+    if (cap < b) return fail(FSW_EINVAL, "read_slot: cap too small");
+    Gpu& g = c->gpus[gpu];
+    CU(cudaSetDevice(g.dev));
+    const uint8_t* src = slot == m->input_slot ? g.dstage + kStageHdr : g.ws + m->plans[gpu]->slot_off[slot];
+    CU(cudaMemcpy(dst, src, b, cudaMemcpyDeviceToHost));
+    return FSW_OK;
+}

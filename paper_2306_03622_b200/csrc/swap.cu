@@ -1,0 +1,86 @@
+// swap.cu — K1, the swap engine: host store (pinned, mapped) -> HBM extent, SM-driven.
+//
+// PAPER.md:579-583 moves models "from host to GPU through PCIe" with copy-engine DMA from
+// pinned memory; PAPER.md:588-590 overlaps "the transmission of subsequent layers with the
+// computation of previous layers".  Here the transfer is done by SMs instead of the copy
+// engine: persistent warps claim pieces in execution order from a global ticket, stream
+// them with 128-bit non-allocating loads from the mapped host store and 128-bit stores to
+// HBM, and publish each finished piece with a release-add of its byte count on the layer's
+// ready counter.  Layer kernels acquire that counter (device.cuh: wait_ready_*).
+// The DMA mechanism of the paper is kept as a baseline (launch_signal, FSW_DMA_BASELINE).
+#include "device.cuh"
+
+namespace fsw {
+
+template <int U>
+__global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, const DevDesc* __restrict__ desc,
+                                              const Piece* __restrict__ pieces, uint32_t n_pieces,
+                                              uint32_t* __restrict__ ready, DevCtl* __restrict__ ctl) {
+    if (threadIdx.x == 0) atomicAdd(&ctl->started, 1u);
+    uint8_t* const wbase = desc->wbase;
+    const uint32_t lane = threadIdx.x & 31u;
+    for (;;) {
+        uint32_t p = 0;
+        if (lane == 0) p = atomicAdd(&ctl->ticket, 1u);
+        p = __shfl_sync(0xffffffffu, p, 0);
+        if (p >= n_pieces) break;
+        if (p == 0 && lane == 0) ctl->t_first = globaltimer();
+        const Piece pc = pieces[p];
+        const uint4* src = reinterpret_cast<const uint4*>(host + pc.off);
+        uint4* dst = reinterpret_cast<uint4*>(wbase + pc.off);
+        const uint32_t n16 = pc.bytes >> 4;
+        uint32_t i = lane;
+        for (; i + (U - 1) * 32 < n16; i += U * 32) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = ld_stream_v4(src + i + u * 32);
+#pragma unroll
+            for (int u = 0; u < U; ++u) st_v4(dst + i + u * 32, v[u]);
+        }
+        for (; i < n16; i += 32) st_v4(dst + i, ld_stream_v4(src + i));
+        __threadfence();  // this lane's stores performed at gpu scope
+        __syncwarp();
+        if (lane == 0) {
+            red_release_gpu_add(&ready[pc.layer], pc.bytes);
+            atomicMax(&ctl->t_last, (unsigned long long)globaltimer());
+        }
+    }
+}
+
+void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, const DevDesc* desc,
+                 const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* ctl) {
+    k_swap<8><<<ctas, threads, 0, s>>>(host_mapped, desc, pieces, n_pieces, ready, ctl);
+}
+
+// Gate: the first node of the layer stream.  Holds the layer kernels back until every swap
+// CTA is resident, so spinning layer CTAs can never occupy the SMs the swap needs
+// (no deadlock whatever the block scheduler does).  One thread; costs one launch.
+__global__ void k_gate(DevCtl* ctl, uint32_t expected) {
+    const volatile uint32_t* st = &ctl->started;
+    const uint64_t t0 = globaltimer();
+    while (*st < expected) {
+        __nanosleep(256);
+        if (globaltimer() - t0 > kWatchdogNs) {
+            atomicExch(&ctl->err, 2);
+            break;
+        }
+    }
+}
+
+void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected) { k_gate<<<1, 1, 0, s>>>(ctl, expected); }
+
+// DMA baseline: after a copy-engine memcpy node of one piece, publish its bytes.
+__global__ void k_signal(uint32_t* ready, uint32_t layer, uint32_t bytes, DevCtl* ctl, int last) {
+    if (ctl->t_first == 0) ctl->t_first = globaltimer();
+    red_release_gpu_add(&ready[layer], bytes);
+    if (last) ctl->t_last = globaltimer();
+}
+
+void launch_signal(cudaStream_t s, uint32_t* ready, uint32_t layer, uint32_t bytes, DevCtl* ctl, int last) {
+    k_signal<<<1, 1, 0, s>>>(ready, layer, bytes, ctl, last);
+}
+
+__global__ void k_finish(DevCtl* ctl) { ctl->t_end = globaltimer(); }
+void launch_finish(cudaStream_t s, DevCtl* ctl) { k_finish<<<1, 1, 0, s>>>(ctl); }
+
+}  // namespace fsw

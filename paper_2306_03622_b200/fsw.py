@@ -1,0 +1,318 @@
+"""Thin ctypes binding of libfsw (include/fsw.h).  Argument marshalling only: every step of
+the swap-in-and-execute path runs in libfsw's C++ runtime and sm_100a kernels.
+
+There is no CPU fallback: if libfsw.so is missing or no CUDA device is present, the calls
+raise ``FswError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfsw.so")
+
+OK, EINVAL, ENOTFOUND, ENOMEM, EBUSY, ESTATE, ECUDA, ETIMEOUT, ETOPO = range(9)
+STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA", "ETIMEOUT", "ETOPO"]
+NO_OVERLAP, DMA_BASELINE, HOST_WC = 0x1, 0x2, 0x4
+ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
+SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
+
+u32, u64, i32, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
+
+
+class FswError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else status}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("n_gpus", u32), ("gpu_ids", ctypes.POINTER(i32)), ("pool_bytes_per_gpu", u64),
+                ("workspace_bytes_per_gpu", u64), ("copy_ctas", u32), ("copy_threads", u32),
+                ("chunk_bytes", u64), ("stripe_min_bytes", u64), ("flags", u32)]
+
+
+class Tensor(ctypes.Structure):
+    _fields_ = [("offset", u64), ("bytes", u64), ("dtype", u32), ("rank", u32), ("shape", u32 * 4)]
+
+
+class Slot(ctypes.Structure):
+    _fields_ = [("dtype", u32), ("rank", u32), ("shape", u32 * 4)]
+
+
+class Layer(ctypes.Structure):
+    _fields_ = [("op", u32), ("first_ref", u32), ("n_refs", u32), ("in0", i32), ("in1", i32), ("out", i32),
+                ("attr", i32 * 8)]
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("weights", vp), ("weight_bytes", u64),
+                ("tensors", ctypes.POINTER(Tensor)), ("n_tensors", u32),
+                ("refs", ctypes.POINTER(u32)), ("n_refs", u32),
+                ("slots", ctypes.POINTER(Slot)), ("n_slots", u32),
+                ("layers", ctypes.POINTER(Layer)), ("n_layers", u32),
+                ("input_slot", i32), ("output_slot", i32), ("flags", u32)]
+
+
+class ModelInfo(ctypes.Structure):
+    _fields_ = [("store_bytes", u64), ("algorithmic_bytes", u64), ("n_layers", u32), ("n_tensors", u32),
+                ("n_gemm_layers", u32), ("input_bytes", u64), ("output_bytes", u64), ("output_dtype", u32)]
+
+
+class StoreTensor(ctypes.Structure):
+    _fields_ = [("offset", u64), ("bytes", u64), ("layout", u32), ("rows", u32), ("cols", u32),
+                ("rows_pad", u32), ("cols_pad", u32), ("owner_layer", u32)]
+
+
+class InvokeStats(ctypes.Structure):
+    _fields_ = [("total_ms", dbl), ("device_ms", dbl), ("swap_ms", dbl), ("swap_span_ms", dbl),
+                ("compute_tail_ms", dbl), ("bytes_swapped", u64), ("link_gbps", dbl), ("gpu", i32),
+                ("swap_kind", u32), ("n_sources", u32), ("n_kernels", u32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class InvokeOpts(ctypes.Structure):
+    _fields_ = [("gpu", i32), ("stripe_mask", u32), ("chunk_bytes", u64), ("order", u32), ("order_seed", u32),
+                ("copy_ctas", u32), ("flags", u32)]
+
+
+class PoolStats(ctypes.Structure):
+    _fields_ = [("capacity", u64), ("used", u64), ("largest_free", u64), ("n_resident", u32), ("n_extents", u32),
+                ("n_evictions", u64), ("bytes_swapped_total", u64), ("n_invokes_cold", u64),
+                ("n_invokes_warm", u64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_register_model",
+           "fsw_unregister_model", "fsw_model_info_get", "fsw_store_tensor_get", "fsw_invoke", "fsw_invoke_ex",
+           "fsw_evict", "fsw_pool_stats_get", "fsw_n_gpus", "fsw_debug_read_resident", "fsw_debug_read_store",
+           "fsw_debug_read_slot", "fsw_arena_create", "fsw_arena_destroy", "fsw_arena_alloc", "fsw_arena_free",
+           "fsw_arena_stats"]
+
+_lib = None
+
+
+def lib():
+    """Load libfsw.so (fails loudly when it is missing — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FswError(ECUDA, f"{LIB_PATH} not built; run `python -m paper_2306_03622_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.fsw_last_error.restype = ctypes.c_char_p
+        L.fsw_version.restype = ctypes.c_char_p
+        L.fsw_init.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(vp)]
+        L.fsw_shutdown.argtypes = [vp]
+        L.fsw_shutdown.restype = None
+        L.fsw_register_model.argtypes = [vp, ctypes.POINTER(ModelDesc), ctypes.POINTER(u32)]
+        L.fsw_unregister_model.argtypes = [vp, u32]
+        L.fsw_model_info_get.argtypes = [vp, u32, ctypes.POINTER(ModelInfo)]
+        L.fsw_store_tensor_get.argtypes = [vp, u32, u32, ctypes.POINTER(StoreTensor)]
+        L.fsw_invoke.argtypes = [vp, u32, vp, u64, vp, u64, ctypes.POINTER(InvokeStats)]
+        L.fsw_invoke_ex.argtypes = [vp, u32, ctypes.POINTER(InvokeOpts), vp, u64, vp, u64, ctypes.POINTER(InvokeStats)]
+        L.fsw_evict.argtypes = [vp, u32, i32]
+        L.fsw_pool_stats_get.argtypes = [vp, i32, ctypes.POINTER(PoolStats)]
+        L.fsw_n_gpus.argtypes = [vp, ctypes.POINTER(u32)]
+        L.fsw_debug_read_resident.argtypes = [vp, u32, i32, vp, u64]
+        L.fsw_debug_read_store.argtypes = [vp, u32, vp, u64]
+        L.fsw_debug_read_slot.argtypes = [vp, u32, i32, i32, vp, u64]
+        L.fsw_arena_create.argtypes = [u64, u64]
+        L.fsw_arena_create.restype = vp
+        L.fsw_arena_destroy.argtypes = [vp]
+        L.fsw_arena_destroy.restype = None
+        L.fsw_arena_alloc.argtypes = [vp, u64, ctypes.POINTER(u64)]
+        L.fsw_arena_free.argtypes = [vp, u64]
+        L.fsw_arena_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u32)]
+        L.fsw_arena_stats.restype = None
+        for name in EXPORTS:
+            f = getattr(L, name)
+            if f.restype is ctypes.c_int:  # default
+                f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise FswError(rc, lib().fsw_last_error().decode(errors="replace"))
+
+
+class Arena:
+    """Host-only extent allocator of the weight pool (usable without a GPU)."""
+
+    def __init__(self, capacity: int, align: int = 64 << 10):
+        self.h = lib().fsw_arena_create(capacity, align)
+        if not self.h:
+            raise FswError(EINVAL, "bad arena parameters")
+
+    def alloc(self, nbytes: int) -> int:
+        off = u64()
+        _check(lib().fsw_arena_alloc(self.h, nbytes, ctypes.byref(off)))
+        return off.value
+
+    def free(self, off: int):
+        _check(lib().fsw_arena_free(self.h, off))
+
+    def stats(self):
+        u, lf, n = u64(), u64(), u32()
+        lib().fsw_arena_stats(self.h, ctypes.byref(u), ctypes.byref(lf), ctypes.byref(n))
+        return {"used": u.value, "largest_free": lf.value, "n_allocated": n.value}
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().fsw_arena_destroy(self.h)
+            self.h = None
+
+
+@dataclass
+class Result:
+    output: np.ndarray
+    stats: dict
+
+
+class Runtime:
+    """One libfsw context (one per process): pool, host stores, per-GPU executors."""
+
+    def __init__(self, n_gpus: int = 0, gpu_ids: Optional[Sequence[int]] = None, pool_bytes: int = 0,
+                 workspace_bytes: int = 0, copy_ctas: int = 0, copy_threads: int = 0, chunk_bytes: int = 0,
+                 flags: int = 0):
+        cfg = Config()
+        cfg.n_gpus = n_gpus or (len(gpu_ids) if gpu_ids else 0)
+        self._ids = (i32 * len(gpu_ids))(*gpu_ids) if gpu_ids else None
+        cfg.gpu_ids = self._ids
+        cfg.pool_bytes_per_gpu = pool_bytes
+        cfg.workspace_bytes_per_gpu = workspace_bytes
+        cfg.copy_ctas, cfg.copy_threads, cfg.chunk_bytes, cfg.flags = copy_ctas, copy_threads, chunk_bytes, flags
+        h = vp()
+        _check(lib().fsw_init(ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+        self._models = {}
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fsw_shutdown(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def n_gpus(self) -> int:
+        n = u32()
+        _check(lib().fsw_n_gpus(self.h, ctypes.byref(n)))
+        return n.value
+
+    # ---- registration -------------------------------------------------------------------
+    def register(self, name: str, weights: np.ndarray, tensors, refs, slots, layers, input_slot: int,
+                 output_slot: int) -> int:
+        """tensors: [(offset, bytes, dtype, shape)], slots: [(dtype, shape)],
+        layers: [(op, first_ref, n_refs, in0, in1, out, attr[8])], refs: [tensor index]."""
+        T = (Tensor * max(1, len(tensors)))()
+        for i, (off, nb, dt, shp) in enumerate(tensors):
+            T[i].offset, T[i].bytes, T[i].dtype, T[i].rank = off, nb, dt, len(shp)
+            for j, d in enumerate(shp):
+                T[i].shape[j] = d
+        S = (Slot * len(slots))()
+        for i, (dt, shp) in enumerate(slots):
+            S[i].dtype, S[i].rank = dt, len(shp)
+            for j, d in enumerate(shp):
+                S[i].shape[j] = d
+        Ls = (Layer * len(layers))()
+        for i, (op, fr, nr, a, b, o, attr) in enumerate(layers):
+            Ls[i].op, Ls[i].first_ref, Ls[i].n_refs, Ls[i].in0, Ls[i].in1, Ls[i].out = op, fr, nr, a, b, o
+            for j in range(8):
+                Ls[i].attr[j] = attr[j]
+        R = (u32 * max(1, len(refs)))(*refs)
+        w = np.ascontiguousarray(weights).view(np.uint8)
+        d = ModelDesc(name.encode(), w.ctypes.data, w.nbytes, T, len(tensors), R, len(refs), S, len(slots), Ls,
+                      len(layers), input_slot, output_slot, 0)
+        mid = u32()
+        _check(lib().fsw_register_model(self.h, ctypes.byref(d), ctypes.byref(mid)))
+        info = self.model_info(mid.value)
+        self._models[mid.value] = info
+        return mid.value
+
+    def register_spec(self, spec, weights: np.ndarray) -> int:
+        """Register a synth.ModelSpec-shaped description (duck-typed)."""
+        spec.assign_offsets()
+        tensors = [(t.offset, t.nbytes, t.dtype, t.shape) for t in spec.tensors]
+        slots = [(s.dtype, s.shape) for s in spec.slots]
+        refs, layers = [], []
+        for l in spec.layers:
+            layers.append((int(l.op), len(refs), len(l.refs), l.in0, l.in1, l.out, list(l.attr)))
+            refs += list(l.refs)
+        return self.register(spec.name, weights, tensors, refs, slots, layers, spec.input_slot, spec.output_slot)
+
+    def unregister(self, mid: int):
+        _check(lib().fsw_unregister_model(self.h, mid))
+        self._models.pop(mid, None)
+
+    def model_info(self, mid: int) -> dict:
+        i = ModelInfo()
+        _check(lib().fsw_model_info_get(self.h, mid, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in i._fields_}
+
+    def store_tensor(self, mid: int, t: int) -> dict:
+        s = StoreTensor()
+        _check(lib().fsw_store_tensor_get(self.h, mid, t, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    # ---- invoke -------------------------------------------------------------------------
+    def invoke(self, mid: int, inp: np.ndarray, out: Optional[np.ndarray] = None, gpu: int = -1,
+               chunk_bytes: int = 0, order: int = ORDER_EXEC, order_seed: int = 0, copy_ctas: int = 0,
+               flags: int = 0) -> Result:
+        info = self._models.get(mid) or self.model_info(mid)
+        inp = np.ascontiguousarray(inp)
+        if out is None:
+            out = np.empty(info["output_bytes"] // 4, dtype=np.float32 if info["output_dtype"] == 1 else np.int32) \
+                if info["output_dtype"] != 0 else np.empty(info["output_bytes"] // 2, dtype=np.uint16)
+        st = InvokeStats()
+        opts = InvokeOpts(gpu, 0, chunk_bytes, order, order_seed, copy_ctas, flags)
+        _check(lib().fsw_invoke_ex(self.h, mid, ctypes.byref(opts), inp.ctypes.data, inp.nbytes, out.ctypes.data,
+                                   out.nbytes, ctypes.byref(st)))
+        return Result(out, st.as_dict())
+
+    def invoke_plain(self, mid: int, inp: np.ndarray, out: np.ndarray) -> dict:
+        """fsw_invoke (scheduler's choice of GPU), the call a user makes."""
+        st = InvokeStats()
+        _check(lib().fsw_invoke(self.h, mid, inp.ctypes.data, inp.nbytes, out.ctypes.data, out.nbytes,
+                                ctypes.byref(st)))
+        return st.as_dict()
+
+    def evict(self, mid: int, gpu: int = -1):
+        _check(lib().fsw_evict(self.h, mid, gpu))
+
+    def pool_stats(self, gpu: int = 0) -> dict:
+        p = PoolStats()
+        _check(lib().fsw_pool_stats_get(self.h, gpu, ctypes.byref(p)))
+        return p.as_dict()
+
+    # ---- debug --------------------------------------------------------------------------
+    def read_resident(self, mid: int, gpu: int = 0) -> np.ndarray:
+        n = self.model_info(mid)["store_bytes"]
+        buf = np.empty(n, dtype=np.uint8)
+        _check(lib().fsw_debug_read_resident(self.h, mid, gpu, buf.ctypes.data, n))
+        return buf
+
+    def read_store(self, mid: int) -> np.ndarray:
+        n = self.model_info(mid)["store_bytes"]
+        buf = np.empty(n, dtype=np.uint8)
+        _check(lib().fsw_debug_read_store(self.h, mid, buf.ctypes.data, n))
+        return buf
+
+    def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:
+        buf = np.empty(nbytes, dtype=np.uint8)
+        _check(lib().fsw_debug_read_slot(self.h, mid, gpu, slot, buf.ctypes.data, nbytes))
+        return buf
