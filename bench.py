@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""bench.py — cold swap+infer latency of one inference function on B200 (BASELINE.json metric).
+
+One *step* = one cold invocation of the whole hot path: the model is resident on no
+GPU (``fsw_evict(m, -1)``), so the invoke swaps all of its weights from the pinned host store
+into the HBM pool with the SM swap kernel while the flag-gated layer kernels run as soon as each
+layer lands, then returns the output.  Default workload: BASELINE.json
+configs[1], BERT-base seq 128 batch 1 (~219 MB bf16).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--model bert-base] [--impl fsw|reference]
+
+``value``   = p50 device latency of the cold invoke (CUDA events around the invoke graph on its
+              launching stream), ms, lower is better.
+``e2e``     = the same metric through the public C-ABI call fsw_invoke with host buffers
+              (input copied host->device and the output device->host inside the timed region).
+``roofline``= the dominant kernel, the swap kernel: algorithmic bytes (the model's host-store
+              bytes) / its CUDA-event duration on its own stream, against the PCIe Gen5 x16 link.
+Under torchrun (N > 1) each rank serves its own replica (request-level data parallelism,
+PAPER.md:824; no data-path collective); max-over-ranks timing, rank 0 prints.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PCIE_GEN5_X16_GBS = 63.0  # 32 GT/s x 16 lanes x 128/130 / 8 (nominal, per direction)
+
+
+def percentile(xs, p):
+    """Nearest-rank percentile (SURVEY §8c reading #11)."""
+    s = sorted(xs)
+    k = max(1, int(np.ceil(p / 100.0 * len(s))))
+    return s[k - 1]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.lines, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def cpu_oracle_timing(spec, w, x, budget_s: float, max_reps: int = 50):
+    """Time the oracle (tests-only package) as it stands on the host cores: bounded sample."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    oracle.lib()
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < max_reps:
+        t0 = time.perf_counter()
+        oracle.output(spec, w, x)
+        times.append((time.perf_counter() - t0) * 1e3)
+        if time.perf_counter() - t_start > budget_s:
+            break
+    return times, cores
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (tier framing: no reference code exists)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    spec = synth.build_model(args.model)
+    w = spec.build_weights()
+    x = spec.make_input()
+    times, cores = cpu_oracle_timing(spec, w, x, budget_s=max(5.0, args.ref_budget_s), max_reps=args.warmup + args.steps)
+    timed = times[min(len(times) - 1, args.warmup):] if len(times) > args.warmup else times
+    v = statistics.median(timed)
+    line = {"impl": "reference", "metric": "cold swap+infer latency ms p50 (reference arm: CPU oracle forward)",
+            "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
+            "ms_per_step": round(statistics.mean(timed), 3), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.model} batch 1 forward (oracle, float64, host cores)"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": "oracle",
+                             "sample": f"{len(timed)} full {args.model} forwards (float64 oracle), OMP threads={cores}"},
+            "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def roofline_ms(bytes_, flops, fill_bytes, link_gbs, tflops):
+    return max(bytes_ / (link_gbs * 1e6), flops / (tflops * 1e9)) + fill_bytes / (link_gbs * 1e6)
+
+
+MODEL_FLOPS = {  # 2 FLOPs per MAC, batch 1
+    "bert-base": 22.35e9, "resnet50": 8.18e9, "gpt2-xl": 382.7e9, "mlp": 8.39e6,
+}
+
+
+def run_fsw(args):
+    import synth
+    from paper_2306_03622_b200 import Runtime, lib
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    gpu = local if world > 1 else 0
+    spec = synth.build_model(args.model)
+    w = spec.build_weights()
+    x = spec.make_input()
+    rt = Runtime(gpu_ids=[gpu], pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas, chunk_bytes=args.chunk_kb << 10)
+    mid = rt.register_spec(spec, w)
+    info = rt.model_info(mid)
+    out = np.empty(info["output_bytes"] // 4, dtype=np.float32)
+
+    def cold_step():
+        rt.evict(mid, -1)
+        return rt.invoke(mid, x, out=out, gpu=0).stats
+
+    for _ in range(args.warmup):
+        cold_step()
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(gpu) as clk:
+        t0 = time.perf_counter()
+        stats = [cold_step() for _ in range(args.steps)]
+        wall = time.perf_counter() - t0
+    if world > 1:
+        dist.barrier()
+    dev = [s["device_ms"] for s in stats]
+    swap = [s["swap_ms"] for s in stats]
+    tail = [s["compute_tail_ms"] for s in stats]
+    launches = sum(s["n_kernels"] for s in stats)
+    # e2e: the public fsw_invoke (scheduler picks the GPU), host buffers, H2D/D2H inside
+    e2e = []
+    for _ in range(max(3, args.steps // 2)):
+        rt.evict(mid, -1)
+        t1 = time.perf_counter()
+        rt.invoke_plain(mid, x, out)
+        e2e.append((time.perf_counter() - t1) * 1e3)
+    # resident (native) inference for comparison
+    warm = [rt.invoke(mid, x, out=out, gpu=0).stats["device_ms"] for _ in range(args.steps)]
+    # DMA ceiling of this box (copy-engine, pinned), for context
+    dma = None
+    try:
+        import torch
+        h = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+        d = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{gpu}")
+        for _ in range(2):
+            d.copy_(h, non_blocking=True)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        dma = (256 << 20) * 5 / (e0.elapsed_time(e1) * 1e6)
+        del h, d
+    except Exception:
+        dma = None
+    p50 = percentile(dev, 50)
+    local_res = {"p50": p50, "p99": percentile(dev, 99), "wall_s": wall}
+    if world > 1:
+        import torch.distributed as dist
+        g = [None] * world
+        dist.all_gather_object(g, local_res)
+        p50 = max(r["p50"] for r in g)
+        wall = max(r["wall_s"] for r in g)
+    if rank != 0:
+        rt.close()
+        return
+    store = info["store_bytes"]
+    swap_p50 = percentile(swap, 50)
+    achieved = store / (swap_p50 * 1e6)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "swap_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.model)
+        except Exception:
+            traffic = None
+    first = spec.layers[0]
+    fill = sum(spec.tensors[r].nbytes for r in first.refs)
+    flops = MODEL_FLOPS.get(args.model, 0.0)
+    t_roof = roofline_ms(info["algorithmic_bytes"], flops, fill, PCIE_GEN5_X16_GBS, 1645.1)
+    t_roof_dma = roofline_ms(info["algorithmic_bytes"], flops, fill, dma, 1645.1) if dma else None
+    cpu = None
+    if not args.no_cpu_baseline:
+        ct, cores = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
+        cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": cores, "kind": "oracle",
+               "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)"}
+    line = {
+        "metric": "cold swap+infer latency ms p50 (p99, resident, host->HBM GB/s in extra keys)",
+        "value": round(p50, 4), "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(statistics.mean(dev), 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded)",
+        "config": {"workload": f"{args.model} batch 1, cold invoke (model resident on no GPU)",
+                   "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"],
+                   "chunk_bytes": args.chunk_kb << 10, "copy_ctas": args.copy_ctas,
+                   "l2": "inputs larger than L2: every step streams all weights from host memory",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+        "p99_ms": round(percentile(dev, 99), 4), "mean_ms": round(statistics.mean(dev), 4),
+        "min_ms": round(min(dev), 4),
+        "resident_p50_ms": round(percentile(warm, 50), 4),
+        "swap_p50_ms": round(swap_p50, 4), "compute_tail_p50_ms": round(percentile(tail, 50), 4),
+        "host_to_hbm_gbs": round(achieved, 2), "dma_h2d_gbs_measured": round(dma, 2) if dma else None,
+        "pipelined_roofline_ms": round(t_roof, 4), "frac_of_pipelined_roofline": round(t_roof / p50, 4),
+        "pipelined_roofline_ms_at_measured_dma": round(t_roof_dma, 4) if t_roof_dma else None,
+        "roofline": {"bound": "pcie", "kernel": "k_swap", "achieved": round(achieved, 2),
+                     "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s", "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
+                     "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure)",
+                     "frac_of_measured_dma": round(achieved / dma, 4) if dma else None,
+                     "traffic": traffic},
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(percentile(e2e, 50), 4), "unit": "ms",
+                "h2d_bytes_per_step": int(info["input_bytes"]), "d2h_bytes_per_step": int(info["output_bytes"]),
+                "note": "fsw_invoke wall clock, host input/output buffers"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "paper_context": "Bert-qa (BERT-large fp32) Pipeline-PCIe 149 ms, Remote-Async 45 ms on V100/PCIe3 (PAPER.md:956); different model/hardware",
+    }
+    print(json.dumps(line), flush=True)
+    rt.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fsw", choices=["fsw", "reference"])
+    ap.add_argument("--model", default="bert-base")
+    ap.add_argument("--copy-ctas", type=int, default=32)
+    ap.add_argument("--chunk-kb", type=int, default=256)
+    ap.add_argument("--pool-gb", type=int, default=16)
+    ap.add_argument("--cpu-budget-s", type=float, default=10.0)
+    ap.add_argument("--ref-budget-s", type=float, default=60.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fsw(args)
+
+
+if __name__ == "__main__":
+    main()

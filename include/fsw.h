@@ -56,6 +56,8 @@ typedef enum {
 #define FSW_DMA_BASELINE 0x2u /* swap by copy-engine DMA (cudaMemcpyAsync from pinned memory,
                                  the paper's mechanism) instead of SM copy kernels */
 #define FSW_HOST_WC      0x4u /* back host stores with write-combined pinned pages            */
+#define FSW_HOST_ONLY    0x8u /* no GPU: registration / host-store / allocator logic only (tests);
+                                 invoke returns FSW_ECUDA                                       */
 
 typedef struct {
     uint32_t n_gpus;                  /* GPUs in the pool; 0 = all visible devices           */
@@ -75,7 +77,8 @@ typedef struct fsw_ctx fsw_ctx; /* opaque; one per process */
 
 /* Create the per-GPU runtime: one shared CUDA context per GPU with all kernels preloaded
  * (PAPER.md:551-555), the pre-allocated weight pool, workspace and streams.
- * cfg may be NULL (defaults).  Returns FSW_ECUDA when no CUDA device is present.            */
+ * cfg may be NULL (defaults).  Returns FSW_ECUDA when no CUDA device is present, unless
+ * cfg->flags has FSW_HOST_ONLY (then no GPU is touched and n_gpus is 0).                   */
 fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out);
 void fsw_shutdown(fsw_ctx* ctx);
 const char* fsw_last_error(void);

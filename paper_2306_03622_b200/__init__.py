@@ -5,6 +5,6 @@ flag-gated sm_100a layer kernels.  This package holds its sources (csrc/), the i
 build (build.py) and the ctypes binding (fsw.py).  It never imports the oracle.
 """
 from .fsw import (  # noqa: F401
-    Arena, FswError, Result, Runtime, lib, NO_OVERLAP, DMA_BASELINE, HOST_WC,
+    Arena, FswError, Result, Runtime, lib, NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY,
     ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM, SWAP_RESIDENT, SWAP_HOST,
 )

@@ -8,19 +8,29 @@
 // so each [BN x 64] weight tile is ONE contiguous cp.async.bulk of BN·128 bytes: no tensor
 // map is needed for weights and the graph stays valid whichever extent the model lands in.
 //
-// One CTA = one 128 x BN output tile; 4 warps.  Thread 0 is the TMA producer: it first
+// One CTA = one 128 x BN output tile; 4 warps.  Lane 0 of warp 0 is the producer: it first
 // spins on the layer's ready counter (the swap kernel's release, PAPER.md:588-590
-// pipelining), fences generic->async proxy, then streams the K loop through a 4-stage
-// mbarrier ring.  Thread 32 issues tcgen05.mma (M=128, N=BN, K=16) into TMEM and commits
-// each stage back to its empty barrier.  All 4 warps then drain TMEM (tcgen05.ld 32x32b)
-// through the fused bias / residual / activation epilogue.
+// pipelining), fences generic->async proxy, then streams the K loop through an mbarrier ring
+// whose stages are KSUB x 64 wide (4 x 64 for BN <= 64): at batch-1 M the MMA chain is
+// issue-bound (~47 cycles per tcgen05.mma for N <= 64, ~170 cycles per mbarrier wait, both
+// measured: tools/micro/umma_micro.cu), so wide stages amortise the waits.  Lane 0 of warp 1
+// issues tcgen05.mma (M=128, N=BN, K=16) into TMEM and commits each stage back to its empty
+// barrier.  All 4 warps then drain TMEM (tcgen05.ld 32x32b) into a shared tile and apply the
+// fused bias / residual / activation epilogue with 16-B coalesced global accesses.
 #include "device.cuh"
 
 namespace fsw {
 
+#ifdef FSW_GEMM_TIMING  // tools/gemm_bench.cu only: per-CTA phase stamps
+__device__ unsigned long long g_gemm_stamp[1024][6];
+#define STAMP(i) do { if (threadIdx.x == 0 || (i) == 2) g_gemm_stamp[(blockIdx.x * gridDim.y + blockIdx.y) & 1023][i] = globaltimer(); } while (0)
+#else
+#define STAMP(i) do { } while (0)
+#endif
+
 namespace {
 
-constexpr int kBM = 128, kBK = 64, kStages = 4;
+constexpr int kBM = 128, kBK = 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -88,34 +98,45 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 template <int BN>
-struct Smem {
-    static constexpr uint32_t kA = kBM * kBK * 2;  // 16 KiB
-    static constexpr uint32_t kB = BN * kBK * 2;   // BN x 128 B
-    static constexpr uint32_t kBytes = kStages * (kA + kB) + 1024 /*barriers*/ + 1024 /*align slack*/;
+struct Cfg {
+    static constexpr int kSub = BN <= 64 ? 4 : 2;            // 64-wide k sub-tiles per stage
+    static constexpr uint32_t kA = kBM * kBK * 2;            // one A sub-tile: 16 KiB
+    static constexpr uint32_t kB = BN * kBK * 2;             // one W sub-tile: BN x 128 B
+    static constexpr uint32_t kStage = kSub * (kA + kB);
+    static constexpr int kFit = (200 * 1024) / kStage;
+    static constexpr int kMaxStages = kFit > 8 ? 8 : kFit;
+    static constexpr int kLdc = BN + 4;                       // epilogue tile row stride (floats)
+    static constexpr uint32_t kCtile = kBM * kLdc * 4;
+    __host__ __device__ static uint32_t ring_bytes(int stages) {
+        uint32_t r = stages * kStage;
+        return r < kCtile ? (kCtile + 1023) / 1024 * 1024 : r;
+    }
+    __host__ __device__ static uint32_t smem_bytes(int stages) { return ring_bytes(stages) + 1024 /*barriers*/ + 1024 /*align*/; }
 };
 
 }  // namespace
 
 template <int BN>
 __global__ void __launch_bounds__(128, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const DevDesc* __restrict__ d, Wait w, GemmArgs a) {
-    using S = Smem<BN>;
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
+    using C = Cfg<BN>;
     constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + kStages * S::kA;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * S::kB);
-    uint64_t* empty = full + kStages;
-    uint64_t* done = empty + kStages;
+    // stage s: A sub-tiles at smem + s*kStage + j*kA, W sub-tiles after the A sub-tiles
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::ring_bytes(stages));
+    uint64_t* empty = full + stages;
+    uint64_t* done = empty + stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
-    const uint32_t nk = a.K / kBK;
+    const uint32_t nkt = a.K / kBK;                              // 64-wide k tiles
+    const uint32_t nst = (nkt + C::kSub - 1) / C::kSub;          // pipeline steps
+    STAMP(0);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
@@ -133,147 +154,165 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    STAMP(1);
 
-    if (threadIdx.x == 0) {
-        // ---------------- producer: ready flag -> proxy fence -> TMA(A) + bulk(W) ring ----------------
-        wait_ready_thread(w);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        const uint8_t* wt = d->wbase + a.w_off;
-        const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
-        for (uint32_t kb = 0; kb < nk; ++kb) {
-            const int s = kb % kStages;
-            if (kb >= (uint32_t)kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-            mbar_expect_tx(&full[s], S::kA + S::kB);
-            tma_load_2d(sA + s * S::kA, &tmA, (int)(kb * kBK), (int)m0, &full[s]);
-            bulk_load(sB + s * S::kB, wt + kb * ktile_stride + (uint64_t)(n0 / 8) * 1024, S::kB, &full[s]);
-        }
-    } else if (threadIdx.x == 32) {
-        // ---------------- MMA issuer: one thread drives the tensor core ----------------
-        constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
-        for (uint32_t kb = 0; kb < nk; ++kb) {
-            const int s = kb % kStages;
-            mbar_wait(&full[s], (kb / kStages) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-                const uint64_t ad = umma_desc_sw128(sA + s * S::kA + kk * 32);
-                const uint64_t bd = umma_desc_sw128(sB + s * S::kB + kk * 32);
-                umma_f16(tmem, ad, bd, idesc, (kb | kk) != 0);
+    // Role dispatch is warp-uniform: lane 0 of warp 0 (producer) / warp 1 (MMA issuer) works,
+    // the other lanes of those warps park at __syncwarp instead of spinning beside it.
+    if (warp == 0) {
+        if (lane == 0) {
+            wait_ready_thread(w);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint8_t* wt = d->wbase + a.w_off;
+            const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
+            for (uint32_t st = 0; st < nst; ++st) {
+                const int s = st % stages;
+                if (st >= (uint32_t)stages) mbar_wait(&empty[s], ((st / stages) - 1) & 1);
+                const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
+                uint8_t* sa = smem + s * C::kStage;
+                uint8_t* sb = sa + C::kSub * C::kA;
+                mbar_expect_tx(&full[s], nsub * (C::kA + C::kB));
+                for (uint32_t j = 0; j < nsub; ++j) {
+                    tma_load_2d(sa + j * C::kA, &tmA, (int)((kt0 + j) * kBK), (int)m0, &full[s]);
+                    bulk_load(sb + j * C::kB, wt + (kt0 + j) * ktile_stride + (uint64_t)(n0 / 8) * 1024, C::kB, &full[s]);
+                }
             }
-            umma_commit(&empty[s]);
         }
-        umma_commit(done);
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+            for (uint32_t st = 0; st < nst; ++st) {
+                const int s = st % stages;
+                mbar_wait(&full[s], (st / stages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
+                const uint8_t* sa = smem + s * C::kStage;
+                const uint8_t* sb = sa + C::kSub * C::kA;
+                const uint64_t ad0 = umma_desc_sw128(sa), bd0 = umma_desc_sw128(sb);
+                for (uint32_t j = 0; j < nsub; ++j) {
+#pragma unroll
+                    for (uint32_t kk = 0; kk < kBK / 16; ++kk) {
+                        // advance the start address: 16-B units; sub-tile j, 32 B per K=16 step
+                        const uint64_t ad = ad0 + ((j * C::kA + kk * 32) >> 4);
+                        const uint64_t bd = bd0 + ((j * C::kB + kk * 32) >> 4);
+                        umma_f16(tmem, ad, bd, idesc, (st | j | kk) != 0);
+                    }
+                }
+                umma_commit(&empty[s]);
+            }
+            umma_commit(done);
+        }
+        __syncwarp();
     }
 
-    // ---------------- epilogue: TMEM -> registers -> bias/residual/act -> global ----------------
+    // ---------------- epilogue ----------------
+    // 1) TMEM -> registers -> shared tile [128][BN+4] fp32 (all MMAs are complete at `done`,
+    //    so the stage buffers are free to reuse).
     mbar_wait(done, 0);
+    STAMP(3);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t row = m0 + warp * 32 + lane;
-    const uint16_t* bias = a.has_bias ? reinterpret_cast<const uint16_t*>(d->wbase + a.b_off) : nullptr;
-#pragma unroll 1
+    float* ct = reinterpret_cast<float*>(smem);
+#pragma unroll
     for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + ((warp * 32u) << 16) + (uint32_t)c0, r);
-        if (row >= a.M) continue;
-        const uint32_t nb = n0 + c0;
-        float v[32];
+        float4* dst = reinterpret_cast<float4*>(ct + (warp * 32 + lane) * C::kLdc + c0);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        const uint32_t ncols = min(32u, (uint32_t)(BN - c0));  // valid accumulator columns in this chunk
-        const bool full_vec = ncols == 32 && (nb + 32 <= a.N) && (a.ld_out % 8 == 0) && (a.res == nullptr || a.ld_res % 8 == 0);
-        if (full_vec) {
-            if (bias) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                    const uint4 bv = *reinterpret_cast<const uint4*>(bias + nb + j);
-                    const uint32_t bu[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        v[j + 2 * h] += __uint_as_float(bu[h] << 16);
-                        v[j + 2 * h + 1] += __uint_as_float(bu[h] & 0xffff0000u);
-                    }
-                }
-            }
-            if (a.res) {
-                if (a.res_bf16) {
-                    const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.res) +
-                                                                     (uint64_t)row * a.ld_res + nb);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint4 rv = rp[j];
-                        const uint32_t ru[4] = {rv.x, rv.y, rv.z, rv.w};
-#pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            v[8 * j + 2 * h] += __uint_as_float(ru[h] << 16);
-                            v[8 * j + 2 * h + 1] += __uint_as_float(ru[h] & 0xffff0000u);
-                        }
-                    }
-                } else {
-                    const float4* rp =
-                        reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + (uint64_t)row * a.ld_res + nb);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 rv = rp[j];
-                        v[4 * j] += rv.x;
-                        v[4 * j + 1] += rv.y;
-                        v[4 * j + 2] += rv.z;
-                        v[4 * j + 3] += rv.w;
-                    }
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = apply_act(a.act, v[j]);
-            if (a.out_bf16 || a.out2) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    pk[j] = (uint32_t)f32_to_bf16(v[2 * j]) | ((uint32_t)f32_to_bf16(v[2 * j + 1]) << 16);
-                uint16_t* dst = a.out_bf16 ? reinterpret_cast<uint16_t*>(a.out) : a.out2;
-                uint4* op = reinterpret_cast<uint4*>(dst + (uint64_t)row * a.ld_out + nb);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) op[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-            }
-            if (!a.out_bf16) {
-                float4* op = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (uint64_t)row * a.ld_out + nb);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) op[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t n = nb + j;
-                if (n >= a.N || (uint32_t)j >= ncols) break;
-                float x = v[j];
-                if (bias) x += bf16_to_f32(bias[n]);
-                if (a.res)
-                    x += a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[(uint64_t)row * a.ld_res + n])
-                                    : reinterpret_cast<const float*>(a.res)[(uint64_t)row * a.ld_res + n];
-                x = apply_act(a.act, x);
-                const uint64_t oi = (uint64_t)row * a.ld_out + n;
-                if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
-                else reinterpret_cast<float*>(a.out)[oi] = x;
-                if (a.out2) a.out2[oi] = f32_to_bf16(x);
-            }
-        }
+        for (int j = 0; j < 8; ++j)
+            if (c0 + 4 * j < BN)
+                dst[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                     __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+    STAMP(4);
+    // 2) row-major pass over 4-column units: consecutive threads take consecutive units, so the
+    //    bias / residual loads and the output stores are 8-16 B, coalesced and independent.
+    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(d->wbase + a.b_off) : nullptr;
+    const uint32_t rows = min((uint32_t)kBM, a.M - m0);
+    const uint32_t cols = min((uint32_t)BN, a.N - n0);
+    constexpr uint32_t upr = BN / 4;
+    const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (a.res == nullptr || a.ld_res % 4 == 0);
+    if (vec) {
+#pragma unroll 4
+        for (uint32_t u = threadIdx.x; u < rows * upr; u += blockDim.x) {
+            const uint32_t r = u / upr, c = (u - r * upr) * 4;
+            if (c >= cols) continue;
+            const uint32_t m = m0 + r, n = n0 + c;
+            float4 v = *reinterpret_cast<const float4*>(ct + r * C::kLdc + c);
+            if (bias) {
+                const uint2 bv = *reinterpret_cast<const uint2*>(bias + n);
+                v.x += __uint_as_float(bv.x << 16);
+                v.y += __uint_as_float(bv.x & 0xffff0000u);
+                v.z += __uint_as_float(bv.y << 16);
+                v.w += __uint_as_float(bv.y & 0xffff0000u);
+            }
+            if (a.res) {
+                const uint64_t ri = (uint64_t)m * a.ld_res + n;
+                if (a.res_bf16) {
+                    const uint2 rv = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.res) + ri);
+                    v.x += __uint_as_float(rv.x << 16);
+                    v.y += __uint_as_float(rv.x & 0xffff0000u);
+                    v.z += __uint_as_float(rv.y << 16);
+                    v.w += __uint_as_float(rv.y & 0xffff0000u);
+                } else {
+                    const float4 rv = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + ri);
+                    v.x += rv.x;
+                    v.y += rv.y;
+                    v.z += rv.z;
+                    v.w += rv.w;
+                }
+            }
+            v.x = apply_act(a.act, v.x);
+            v.y = apply_act(a.act, v.y);
+            v.z = apply_act(a.act, v.z);
+            v.w = apply_act(a.act, v.w);
+            const uint64_t oi = (uint64_t)m * a.ld_out + n;
+            const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
+                                        (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
+            if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
+            else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = v;
+            if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
+        }
+    } else {
+        for (uint32_t idx = threadIdx.x; idx < rows * BN; idx += blockDim.x) {
+            const uint32_t r = idx / BN, c = idx - r * BN;
+            if (c >= cols) continue;
+            const uint32_t m = m0 + r, n = n0 + c;
+            float x = ct[r * C::kLdc + c];
+            if (bias) x += bf16_to_f32(bias[n]);
+            if (a.res)
+                x += a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[(uint64_t)m * a.ld_res + n])
+                                : reinterpret_cast<const float*>(a.res)[(uint64_t)m * a.ld_res + n];
+            x = apply_act(a.act, x);
+            const uint64_t oi = (uint64_t)m * a.ld_out + n;
+            if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
+            else reinterpret_cast<float*>(a.out)[oi] = x;
+            if (a.out2) a.out2[oi] = f32_to_bf16(x);
+        }
+    }
+#ifdef FSW_GEMM_TIMING
+    __syncthreads();
+    STAMP(5);
+#endif
 }
 
 template <int BN>
 static void launch_bn(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {
-    const int smem = (int)Smem<BN>::kBytes;
+    using C = Cfg<BN>;
+    const int nst = (int)((a.K / kBK + C::kSub - 1) / C::kSub);
+    const int stages = nst < C::kMaxStages ? nst : C::kMaxStages;
     dim3 grid((a.M + kBM - 1) / kBM, a.n_pad / BN);
-    k_gemm<BN><<<grid, 128, smem, s>>>(*tmA, d, w, a);
+    k_gemm<BN><<<grid, 128, C::smem_bytes(stages), s>>>(*tmA, d, w, a, stages);
 }
 
 void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading)
-    cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<16>::kBytes);
-    cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<32>::kBytes);
-    cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<64>::kBytes);
-    cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Smem<128>::kBytes);
+    cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<16>::smem_bytes(Cfg<16>::kMaxStages));
+    cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<32>::smem_bytes(Cfg<32>::kMaxStages));
+    cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<64>::smem_bytes(Cfg<64>::kMaxStages));
+    cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::smem_bytes(Cfg<128>::kMaxStages));
 }
 
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {

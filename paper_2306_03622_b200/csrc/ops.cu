@@ -39,48 +39,66 @@ void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) 
 }
 
 // ------------------------------------------------------------------------------------------
-// LAYERNORM: one warp per row, row held in registers (C <= 2048), fp32 statistics.
+// LAYERNORM: one warp per row, the row held in registers as float4 (NV per lane, C <= 128·NV),
+// fp32 two-pass statistics (mean, then centred variance), 8-B vector loads of γ/β.
 // ------------------------------------------------------------------------------------------
-constexpr int kLnMaxPerLane = 64;
-
-__global__ void __launch_bounds__(256) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
+template <int NV>
+__global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
     wait_ready_cta(w);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp;
     if (r >= a.rows) return;
-    const float* x = a.in + (uint64_t)r * a.C;
-    float v[kLnMaxPerLane];
+    const uint32_t n4 = a.C >> 2;
+    const float4* x = reinterpret_cast<const float4*>(a.in + (uint64_t)r * a.C);
+    float4 v[NV];
     float s = 0.0f;
 #pragma unroll
-    for (int j = 0; j < kLnMaxPerLane; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const uint32_t c = lane + 32u * j;
-        v[j] = c < a.C ? x[c] : 0.0f;
-        s += v[j];
+        v[j] = c < n4 ? x[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
     }
     const float mu = warp_sum(s) / (float)a.C;
     float q = 0.0f;
 #pragma unroll
-    for (int j = 0; j < kLnMaxPerLane; ++j) {
-        const uint32_t c = lane + 32u * j;
-        const float dlt = c < a.C ? v[j] - mu : 0.0f;
-        q += dlt * dlt;
+    for (int j = 0; j < NV; ++j) {
+        if (lane + 32u * j < n4) {
+            const float d0 = v[j].x - mu, d1 = v[j].y - mu, d2 = v[j].z - mu, d3 = v[j].w - mu;
+            q += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+        }
     }
     const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
-    const uint16_t* g = reinterpret_cast<const uint16_t*>(d->wbase + a.g_off);
-    const uint16_t* b = reinterpret_cast<const uint16_t*>(d->wbase + a.b_off);
+    const uint2* g = reinterpret_cast<const uint2*>(d->wbase + a.g_off);
+    const uint2* b = reinterpret_cast<const uint2*>(d->wbase + a.b_off);
 #pragma unroll
-    for (int j = 0; j < kLnMaxPerLane; ++j) {
+    for (int j = 0; j < NV; ++j) {
         const uint32_t c = lane + 32u * j;
-        if (c < a.C) {
-            const float y = (v[j] - mu) * inv * bf16_to_f32(g[c]) + bf16_to_f32(b[c]);
-            if (a.out_f32) a.out_f32[(uint64_t)r * a.C + c] = y;
-            if (a.out_bf16) a.out_bf16[(uint64_t)r * a.C + c] = f32_to_bf16(y);
+        if (c < n4) {
+            const uint2 gv = g[c], bv = b[c];
+            float4 y;
+            y.x = (v[j].x - mu) * inv * __uint_as_float(gv.x << 16) + __uint_as_float(bv.x << 16);
+            y.y = (v[j].y - mu) * inv * __uint_as_float(gv.x & 0xffff0000u) + __uint_as_float(bv.x & 0xffff0000u);
+            y.z = (v[j].z - mu) * inv * __uint_as_float(gv.y << 16) + __uint_as_float(bv.y << 16);
+            y.w = (v[j].w - mu) * inv * __uint_as_float(gv.y & 0xffff0000u) + __uint_as_float(bv.y & 0xffff0000u);
+            if (a.out_f32) reinterpret_cast<float4*>(a.out_f32 + (uint64_t)r * a.C)[c] = y;
+            if (a.out_bf16) {
+                const uint32_t lo = (uint32_t)f32_to_bf16(y.x) | ((uint32_t)f32_to_bf16(y.y) << 16);
+                const uint32_t hi = (uint32_t)f32_to_bf16(y.z) | ((uint32_t)f32_to_bf16(y.w) << 16);
+                reinterpret_cast<uint2*>(a.out_bf16 + (uint64_t)r * a.C)[c] = make_uint2(lo, hi);
+            }
         }
     }
 }
 
 void launch_layernorm(cudaStream_t s, const DevDesc* d, Wait w, const LnArgs& a) {
-    k_layernorm<<<(a.rows + 7) / 8, 256, 0, s>>>(d, w, a);
+    const unsigned grid = (a.rows + 3) / 4;
+    const uint32_t nv = (a.C / 4 + 31) / 32;
+    if (nv <= 2) k_layernorm<2><<<grid, 128, 0, s>>>(d, w, a);
+    else if (nv <= 4) k_layernorm<4><<<grid, 128, 0, s>>>(d, w, a);
+    else if (nv <= 6) k_layernorm<6><<<grid, 128, 0, s>>>(d, w, a);
+    else if (nv <= 8) k_layernorm<8><<<grid, 128, 0, s>>>(d, w, a);
+    else if (nv <= 13) k_layernorm<13><<<grid, 128, 0, s>>>(d, w, a);
+    else k_layernorm<16><<<grid, 128, 0, s>>>(d, w, a);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -156,42 +174,55 @@ void launch_gemv(cudaStream_t s, const DevDesc* d, Wait w, const GemvArgs& a) {
 }
 
 // ------------------------------------------------------------------------------------------
-// ATTENTION core, one CTA per (head, 32 query rows); K/V of the head staged in shared memory
-// as fp32 (K rows padded by one float against bank conflicts); fp32 softmax.
+// ATTENTION core.  One CTA per (head, 16 query rows), 8 warps x 2 rows.  K and V of the head
+// are staged in shared memory as bf16 (K rows padded by 4 B: conflict-free column reads);
+// scores, softmax and the P·V accumulation are fp32 (SURVEY §8c reading #1).
 // ------------------------------------------------------------------------------------------
-constexpr int kAttnRows = 32;
+constexpr int kAttnRows = 16;
 
 __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
-    extern __shared__ float sm[];
+    extern __shared__ __align__(16) uint8_t sm_attn[];
     const uint32_t T = a.T, dh = a.dh, D = a.H * dh, W3 = 3 * D;
     const uint32_t h = blockIdx.x, t0 = blockIdx.y * kAttnRows;
     const uint32_t nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t kend = a.causal ? min(T, t0 + kAttnRows) : T;  // keys this CTA needs
-    float* Ks = sm;                          // [T][dh+1]
-    float* Vs = Ks + T * (dh + 1);           // [T][dh]
-    float* Ps = Vs + T * dh;                 // [nwarp][T]
-    float* Qs = Ps + nwarp * T;              // [nwarp][dh]
-    for (uint32_t i = threadIdx.x; i < kend * dh; i += blockDim.x) {
-        const uint32_t j = i / dh, c = i - j * dh;
-        const uint16_t* row = a.qkv + (uint64_t)j * W3 + h * dh + c;
-        Ks[j * (dh + 1) + c] = bf16_to_f32(row[D]);
-        Vs[j * dh + c] = bf16_to_f32(row[2 * D]);
+    const uint32_t tend = min(T, t0 + kAttnRows);
+    const uint32_t kend = a.causal ? tend : T;  // keys this CTA needs
+    const uint32_t kst = dh / 2 + 1;           // K row stride in 32-bit words (padded)
+    uint32_t* Ks = reinterpret_cast<uint32_t*>(sm_attn);     // [T][kst]   bf16x2
+    uint32_t* Vs = Ks + T * kst;                              // [T][dh/2]  bf16x2
+    float* Ps = reinterpret_cast<float*>(Vs + T * (dh / 2));  // [nwarp][T]
+    float* Qs = Ps + nwarp * T;                               // [nwarp][dh]
+    const uint32_t dh8 = dh / 8;
+    for (uint32_t i = threadIdx.x; i < kend * dh8; i += blockDim.x) {
+        const uint32_t j = i / dh8, c8 = i - j * dh8;
+        const uint16_t* row = a.qkv + (uint64_t)j * W3 + h * dh + c8 * 8;
+        const uint4 kv = *reinterpret_cast<const uint4*>(row + D);
+        const uint4 vv = *reinterpret_cast<const uint4*>(row + 2 * D);
+        uint32_t* kd = Ks + j * kst + c8 * 4;
+        kd[0] = kv.x; kd[1] = kv.y; kd[2] = kv.z; kd[3] = kv.w;
+        *reinterpret_cast<uint4*>(Vs + j * (dh / 2) + c8 * 4) = vv;
     }
     __syncthreads();
     const float scale = rsqrtf((float)dh);
     float* P = Ps + warp * T;
     float* q = Qs + warp * dh;
-    for (uint32_t t = t0 + warp; t < min(T, t0 + kAttnRows); t += nwarp) {
+    for (uint32_t t = t0 + warp; t < tend; t += nwarp) {
         for (uint32_t c = lane; c < dh; c += 32) q[c] = bf16_to_f32(a.qkv[(uint64_t)t * W3 + h * dh + c]) * scale;
         __syncwarp();
         const uint32_t jmax = a.causal ? t + 1 : T;
         float mx = -INFINITY;
         for (uint32_t j = lane; j < jmax; j += 32) {
-            const float* kr = Ks + j * (dh + 1);
-            float s = 0.0f;
-            for (uint32_t c = 0; c < dh; ++c) s = fmaf(q[c], kr[c], s);
-            P[j] = s;
-            mx = fmaxf(mx, s);
+            const uint32_t* kr = Ks + j * kst;
+            float s0 = 0.0f, s1 = 0.0f;
+            for (uint32_t c2 = 0; c2 < dh / 2; ++c2) {
+                const uint32_t k2 = kr[c2];
+                const float2 q2 = *reinterpret_cast<const float2*>(q + 2 * c2);
+                s0 = fmaf(q2.x, __uint_as_float(k2 << 16), s0);
+                s1 = fmaf(q2.y, __uint_as_float(k2 & 0xffff0000u), s1);
+            }
+            const float sc = s0 + s1;
+            P[j] = sc;
+            mx = fmaxf(mx, sc);
         }
         mx = warp_max(mx);
         float z = 0.0f;
@@ -203,10 +234,16 @@ __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
         z = warp_sum(z);
         __syncwarp();
         const float iz = 1.0f / z;
-        for (uint32_t c = lane; c < dh; c += 32) {
-            float acc = 0.0f;
-            for (uint32_t j = 0; j < jmax; ++j) acc = fmaf(P[j], Vs[j * dh + c], acc);
-            a.out[(uint64_t)t * D + h * dh + c] = f32_to_bf16(acc * iz);
+        for (uint32_t c2 = lane; c2 < dh / 2; c2 += 32) {
+            float o0 = 0.0f, o1 = 0.0f;
+            for (uint32_t j = 0; j < jmax; ++j) {
+                const float pj = P[j];
+                const uint32_t v2 = Vs[j * (dh / 2) + c2];
+                o0 = fmaf(pj, __uint_as_float(v2 << 16), o0);
+                o1 = fmaf(pj, __uint_as_float(v2 & 0xffff0000u), o1);
+            }
+            const uint32_t pk = (uint32_t)f32_to_bf16(o0 * iz) | ((uint32_t)f32_to_bf16(o1 * iz) << 16);
+            *reinterpret_cast<uint32_t*>(a.out + (uint64_t)t * D + h * dh + 2 * c2) = pk;
         }
         __syncwarp();
     }
@@ -214,7 +251,7 @@ __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
 
 void launch_attention(cudaStream_t s, const AttnArgs& a) {
     const int threads = 256, nwarp = threads / 32;
-    const size_t smem = sizeof(float) * (a.T * (a.dh + 1) + a.T * a.dh + nwarp * a.T + nwarp * a.dh);
+    const size_t smem = 4 * (a.T * (a.dh / 2 + 1) + a.T * (a.dh / 2)) + sizeof(float) * (nwarp * a.T + nwarp * a.dh);
     dim3 grid(a.H, (a.T + kAttnRows - 1) / kAttnRows);
     k_attention<<<grid, threads, smem, s>>>(a);
 }

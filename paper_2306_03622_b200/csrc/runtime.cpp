@@ -281,6 +281,14 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
 extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
     if (!out) return fail(FSW_EINVAL, "fsw_init: out is NULL");
     *out = nullptr;
+    if (cfg && (cfg->flags & FSW_HOST_ONLY)) {
+        auto c = std::make_unique<fsw_ctx>();
+        c->cfg = *cfg;
+        c->cfg.gpu_ids = nullptr;
+        if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 256 << 10;
+        *out = c.release();
+        return FSW_OK;
+    }
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0)
@@ -314,12 +322,12 @@ static void free_plan(Gpu& g, Plan& p) {
     p.pieces.clear();
 }
 
-static void free_store(Model& m) {
+static void free_store(Model& m, bool host_only) {
     if (!m.store) return;
     if (m.store_wc) {
         cudaFreeHost(m.store);
     } else {
-        cudaHostUnregister(m.store);
+        if (!host_only) cudaHostUnregister(m.store);
         munmap(m.store, m.store_alloc);
     }
     m.store = nullptr;
@@ -331,7 +339,7 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         if (!m) continue;
         for (size_t i = 0; i < c->gpus.size(); ++i)
             if (m->plans[i]) free_plan(c->gpus[i], *m->plans[i]);
-        free_store(*m);
+        free_store(*m, (c->cfg.flags & FSW_HOST_ONLY) != 0);
     }
     for (auto& g : c->gpus) {
         cudaSetDevice(g.dev);
@@ -442,7 +450,7 @@ static fsw_status check_layer(const Model& m, uint32_t li) {
         case FSW_OP_LAYERNORM:
             if (L.n_refs != 2 || si.dtype != FSW_DT_F32 || so.dtype == FSW_DT_I32 || slot_numel(si) != slot_numel(so))
                 return fail(FSW_EINVAL, "layer %u: LAYERNORM needs f32 input, 2 refs", li);
-            if (slot_cols(si) > 2048 || ref(0).shape[0] != slot_cols(si)) return fail(FSW_EINVAL, "layer %u: LAYERNORM width", li);
+            if (slot_cols(si) > 2048 || slot_cols(si) % 4 || ref(0).shape[0] != slot_cols(si)) return fail(FSW_EINVAL, "layer %u: LAYERNORM width", li);
             break;
         case FSW_OP_LINEAR: {
             if (L.n_refs < 1 || L.n_refs > 2) return fail(FSW_EINVAL, "layer %u: LINEAR refs", li);
@@ -468,7 +476,7 @@ static fsw_status check_layer(const Model& m, uint32_t li) {
             const int H = L.attr[0], dh = L.attr[1];
             if (si.dtype != FSW_DT_BF16 || so.dtype != FSW_DT_BF16 || si.rank != 2 || H <= 0 || dh <= 0 || dh > 256 ||
                 si.shape[1] != (uint32_t)(3 * H * dh) || so.shape[1] != (uint32_t)(H * dh) || so.shape[0] != si.shape[0] ||
-                si.shape[0] > 256 || dh > 128)
+                si.shape[0] > 256 || dh > 128 || dh % 8)
                 return fail(FSW_EINVAL, "layer %u: ATTENTION shapes/dtypes (bf16 qkv [T][3Hdh], T<=256, dh<=128)", li);
             break;
         }
@@ -571,7 +579,8 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
     if (m->store_bytes == 0) return fail(FSW_EINVAL, "register: model has no weights");
 
     // --- host store: pinned + mapped (cudaHostRegister of THP-backed mmap), or WC pinned ---
-    const bool wc = (c->cfg.flags & FSW_HOST_WC) != 0;
+    const bool host_only = (c->cfg.flags & FSW_HOST_ONLY) != 0;
+    const bool wc = !host_only && (c->cfg.flags & FSW_HOST_WC) != 0;
     m->store_alloc = align_up(m->store_bytes, 2 << 20);
     if (wc) {
         CU(cudaSetDevice(c->gpus[0].dev));
@@ -599,7 +608,7 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
                     memcpy(m->store + ti.st_off + tiled_off(n, k, ti.rows_pad), &w[n * ti.cols + k], 2);
         }
     }
-    if (!wc) {
+    if (!wc && !host_only) {
         CU(cudaSetDevice(c->gpus[0].dev));
         cudaError_t e = cudaHostRegister(m->store, m->store_alloc, cudaHostRegisterPortable | cudaHostRegisterMapped);
         if (e != cudaSuccess) {
@@ -933,6 +942,14 @@ struct InvokeCfg {
     uint8_t* wbase;  // only used by DMA graphs (memcpy nodes need absolute addresses)
 };
 
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_writeValue32 get_write_value32() {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess) return nullptr;
+    return reinterpret_cast<PFN_writeValue32>(p);
+}
+
 // Capture the invoke graph of (model, GPU, cfg).  Root: H2D of [desc | input]; cold adds the
 // ready/ctl reset, the swap kernel on its own stream (bracketed by external event nodes for
 // timing) and the gate; then the flag-gated layer kernels; then D2H of output and ctl.
@@ -957,10 +974,19 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
             launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, reinterpret_cast<const DevDesc*>(g.dstage),
                         ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl);
         } else {
-            for (size_t i = 0; i < ps->host.size(); ++i) {
-                const Piece& pc = ps->host[i];
-                cudaMemcpyAsync(ic.wbase + pc.off, m.store + pc.off, pc.bytes, cudaMemcpyHostToDevice, sc);
-                launch_signal(sc, g.ready, pc.layer, pc.bytes, g.ctl, i + 1 == ps->host.size());
+            // The paper's mechanism: copy-engine DMA from pinned memory in
+            // groups of >= 2 MB, layer by layer; after each layer a stream memory write (no kernel,
+            // so no SM is needed while layer kernels spin) publishes the layer's byte count.
+            static PFN_writeValue32 wv = get_write_value32();
+            if (!wv) return fail(FSW_ECUDA, "cuStreamWriteValue32 entry point unavailable");
+            const uint64_t grp = std::max<uint64_t>(ic.chunk, 2ull << 20);
+            for (uint32_t li = 0; li < m.layers.size(); ++li) {
+                if (!m.region_bytes[li]) continue;
+                for (uint64_t o = 0; o < m.region_bytes[li]; o += grp) {
+                    const uint64_t off = m.region_off[li] + o, nb = std::min<uint64_t>(grp, m.region_bytes[li] - o);
+                    cudaMemcpyAsync(ic.wbase + off, m.store + off, nb, cudaMemcpyHostToDevice, sc);
+                }
+                wv(sc, (CUdeviceptr)(g.ready + li), (cuuint32_t)m.region_bytes[li], 0);
             }
         }
         cudaEventRecordWithFlags(g.evs1, sc, cudaEventRecordExternal);
@@ -1050,7 +1076,7 @@ extern "C" fsw_status fsw_unregister_model(fsw_ctx* c, uint32_t id) {
     }
     for (size_t i = 0; i < c->gpus.size(); ++i)
         if (m->plans[i]) free_plan(c->gpus[i], *m->plans[i]);
-    free_store(*m);
+    free_store(*m, (c->cfg.flags & FSW_HOST_ONLY) != 0);
     return FSW_OK;
 }
 
@@ -1085,6 +1111,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                                     uint64_t input_bytes, void* output, uint64_t output_cap, fsw_invoke_stats* stats) {
     const double t_entry = now_ms();
     if (!c || !input || !output) return fail(FSW_EINVAL, "invoke: NULL argument");
+    if (c->gpus.empty()) return fail(FSW_ECUDA, "invoke: context has no GPU (FSW_HOST_ONLY)");
     fsw_invoke_opts o{};
     o.gpu = -1;
     if (opts) o = *opts;
@@ -1184,7 +1211,6 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
             if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
             if (!ic.dma) stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)
-            else stats->n_kernels += (uint32_t)p.pieces.begin()->second.host.size();
         }
     }
     {

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libfsw.so")
 
 OK, EINVAL, ENOTFOUND, ENOMEM, EBUSY, ESTATE, ECUDA, ETIMEOUT, ETOPO = range(9)
 STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA", "ETIMEOUT", "ETOPO"]
-NO_OVERLAP, DMA_BASELINE, HOST_WC = 0x1, 0x2, 0x4
+NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY = 0x1, 0x2, 0x4, 0x8
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
 

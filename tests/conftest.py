@@ -25,3 +25,31 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def rt():
+    """One libfsw context for the whole GPU session (the pool is pre-allocated once, like the
+    paper's GPU server)."""
+    from paper_2306_03622_b200 import Runtime
+    r = Runtime(gpu_ids=[0], pool_bytes=24 << 30)
+    yield r
+    r.close()
+
+
+_REG = {}
+
+
+@pytest.fixture(scope="session")
+def registered(rt):
+    """Register each synthetic model once per session: name -> (spec, weights, input, model id)."""
+    import synth
+
+    def get(name):
+        if name not in _REG:
+            spec = synth.build_model(name)
+            w = spec.build_weights()
+            x = spec.make_input()
+            _REG[name] = (spec, w, x, rt.register_spec(spec, w))
+        return _REG[name]
+    return get

@@ -1,0 +1,19 @@
+"""Small fixed workload for ncu: one cold invoke in no-overlap mode (ncu serialises kernels, so
+the overlapped pipeline would deadlock under it) and N warm invokes.  Never a bench number."""
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+import synth
+from paper_2306_03622_b200 import Runtime, NO_OVERLAP
+
+name = sys.argv[1] if len(sys.argv) > 1 else "bert-base"
+warm = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+rt = Runtime(pool_bytes=16 << 30)
+spec = synth.build_model(name)
+w = spec.build_weights()
+x = spec.make_input()
+mid = rt.register_spec(spec, w)
+rt.invoke(mid, x, flags=NO_OVERLAP)
+for _ in range(warm):
+    rt.invoke(mid, x)
+rt.close()
