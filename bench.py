@@ -225,11 +225,13 @@ def run_fsw(args):
     store = info["store_bytes"]
     swap_p50 = percentile(swap, 50)
     achieved = store / (swap_p50 * 1e6)
-    traffic = None
+    traffic = pcie_traffic = None
     tpath = os.path.join(ROOT, "profiles", "swap_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.model)
+            t = json.load(open(tpath)).get(args.model)
+            traffic = t and t["dram_bytes"]
+            pcie_traffic = t and t["pcie_read_bytes"]
         except Exception:
             traffic = None
     first = spec.layers[0]
@@ -263,7 +265,10 @@ def run_fsw(args):
                      "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s", "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
                      "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure)",
                      "frac_of_measured_dma": round(achieved / dma, 4) if dma else None,
-                     "traffic": traffic},
+                     "traffic": traffic,
+                     "traffic_note": "dram read+write bytes of one k_swap launch (ncu --set full, profiles/); "
+                                     "writes still resident in L2 at kernel end are not counted",
+                     "pcie_read_bytes": pcie_traffic},
         "cpu_baseline": cpu,
         "e2e": {"value": round(percentile(e2e, 50), 4), "unit": "ms",
                 "h2d_bytes_per_step": int(info["input_bytes"]), "d2h_bytes_per_step": int(info["output_bytes"]),
