@@ -150,7 +150,7 @@ MODEL_FLOPS = {  # 2 FLOPs per MAC, batch 1
 
 def run_fsw(args):
     import synth
-    from paper_2306_03622_b200 import Runtime, lib
+    from paper_2306_03622_b200 import DMA_BASELINE, ENGINE_DMA, ENGINE_SM, Runtime
 
     rank, world, local = dist_env()
     if world > 1:
@@ -160,14 +160,15 @@ def run_fsw(args):
     spec = synth.build_model(args.model)
     w = spec.build_weights()
     x = spec.make_input()
-    rt = Runtime(gpu_ids=[gpu], pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas, chunk_bytes=args.chunk_kb << 10)
+    rt = Runtime(gpu_ids=[gpu], pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas, chunk_bytes=args.chunk_kb << 10,
+                 engine=args.engine, dma_group_bytes=args.dma_group_mb << 20, dma_streams=args.dma_streams)
     mid = rt.register_spec(spec, w)
     info = rt.model_info(mid)
     out = np.empty(info["output_bytes"] // 4, dtype=np.float32)
 
-    def cold_step():
+    def cold_step(**kw):
         rt.evict(mid, -1)
-        return rt.invoke(mid, x, out=out, gpu=0).stats
+        return rt.invoke(mid, x, out=out, gpu=0, **kw).stats
 
     for _ in range(args.warmup):
         cold_step()
@@ -183,6 +184,7 @@ def run_fsw(args):
     swap = [s["swap_ms"] for s in stats]
     tail = [s["compute_tail_ms"] for s in stats]
     launches = sum(s["n_kernels"] for s in stats)
+    engine = {1: "sm", 2: "dma"}[stats[0]["engine"]]
     # e2e: the public fsw_invoke (scheduler picks the GPU), host buffers, H2D/D2H inside
     e2e = []
     for _ in range(max(3, args.steps // 2)):
@@ -192,7 +194,20 @@ def run_fsw(args):
         e2e.append((time.perf_counter() - t1) * 1e3)
     # resident (native) inference for comparison
     warm = [rt.invoke(mid, x, out=out, gpu=0).stats["device_ms"] for _ in range(args.steps)]
-    # DMA ceiling of this box (copy-engine, pinned), for context
+    # the other swap engines on the same workload (context: which engine wins and by how much)
+    variants = {}
+    for name, kw in (("sm", dict(engine=ENGINE_SM)), ("dma", dict(engine=ENGINE_DMA)),
+                     ("paper_dma_2MB_1stream", dict(flags=DMA_BASELINE))):
+        for _ in range(2):
+            cold_step(**kw)
+        st = [cold_step(**kw) for _ in range(max(5, args.steps // 2))]
+        sw = percentile([t["swap_ms"] for t in st], 50)
+        variants[name] = {"p50_ms": round(percentile([t["device_ms"] for t in st], 50), 4),
+                          "p99_ms": round(percentile([t["device_ms"] for t in st], 99), 4),
+                          "swap_p50_ms": round(sw, 4), "host_to_hbm_gbs": round(info["store_bytes"] / (sw * 1e6), 2),
+                          "compute_tail_p50_ms": round(percentile([t["compute_tail_ms"] for t in st], 50), 4),
+                          "copies": st[0]["n_copies"]}
+    # copy-engine ceiling of this box: one 256 MiB pinned H2D (torch), for context
     dma = None
     try:
         import torch
@@ -244,6 +259,23 @@ def run_fsw(args):
         ct, cores = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
         cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": cores, "kind": "oracle",
                "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)"}
+    if engine == "dma":
+        roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA groups (cudaMemcpyAsync, no SM kernel)",
+                "achieved": round(achieved, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
+                "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
+                "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure)",
+                "frac_of_measured_dma": round(achieved / dma, 4) if dma else None,
+                "traffic": None, "traffic_note": "copy-engine transfers are not kernels: ncu has no per-launch DRAM "
+                "counter for them; the SM engine's k_swap capture is in profiles/ (sm_engine_roofline)"}
+    else:
+        roof = {"bound": "pcie", "kernel": "k_swap", "achieved": round(achieved, 2), "peak": PCIE_GEN5_X16_GBS,
+                "unit": "GB/s", "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
+                "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure)",
+                "frac_of_measured_dma": round(achieved / dma, 4) if dma else None, "traffic": traffic,
+                "traffic_note": "dram read+write bytes of one k_swap launch (ncu --set full, profiles/); "
+                                "writes still resident in L2 at kernel end are not counted",
+                "pcie_read_bytes": pcie_traffic}
+    sm_gbs = variants["sm"]["host_to_hbm_gbs"]
     line = {
         "metric": "cold swap+infer latency ms p50 (p99, resident, host->HBM GB/s in extra keys)",
         "value": round(p50, 4), "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -251,7 +283,9 @@ def run_fsw(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded)",
         "config": {"workload": f"{args.model} batch 1, cold invoke (model resident on no GPU)",
                    "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"],
-                   "chunk_bytes": args.chunk_kb << 10, "copy_ctas": args.copy_ctas,
+                   "swap_engine": engine, "sm_chunk_bytes": (args.chunk_kb or 16) << 10,
+                   "sm_copy_ctas": args.copy_ctas or 16, "dma_group_bytes": (args.dma_group_mb or 64) << 20,
+                   "dma_streams": args.dma_streams or 1,
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
         "p99_ms": round(percentile(dev, 99), 4), "mean_ms": round(statistics.mean(dev), 4),
@@ -261,14 +295,11 @@ def run_fsw(args):
         "host_to_hbm_gbs": round(achieved, 2), "dma_h2d_gbs_measured": round(dma, 2) if dma else None,
         "pipelined_roofline_ms": round(t_roof, 4), "frac_of_pipelined_roofline": round(t_roof / p50, 4),
         "pipelined_roofline_ms_at_measured_dma": round(t_roof_dma, 4) if t_roof_dma else None,
-        "roofline": {"bound": "pcie", "kernel": "k_swap", "achieved": round(achieved, 2),
-                     "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s", "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
-                     "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure)",
-                     "frac_of_measured_dma": round(achieved / dma, 4) if dma else None,
-                     "traffic": traffic,
-                     "traffic_note": "dram read+write bytes of one k_swap launch (ncu --set full, profiles/); "
-                                     "writes still resident in L2 at kernel end are not counted",
-                     "pcie_read_bytes": pcie_traffic},
+        "roofline": roof,
+        "sm_engine_roofline": {"bound": "pcie", "kernel": "k_swap", "achieved": sm_gbs, "peak": PCIE_GEN5_X16_GBS,
+                               "unit": "GB/s", "frac": round(sm_gbs / PCIE_GEN5_X16_GBS, 4), "traffic": traffic,
+                               "pcie_read_bytes": pcie_traffic},
+        "engines": variants,
         "cpu_baseline": cpu,
         "e2e": {"value": round(percentile(e2e, 50), 4), "unit": "ms",
                 "h2d_bytes_per_step": int(info["input_bytes"]), "d2h_bytes_per_step": int(info["output_bytes"]),
@@ -288,9 +319,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fsw", choices=["fsw", "reference"])
     ap.add_argument("--model", default="bert-base")
-    ap.add_argument("--copy-ctas", type=int, default=32)
-    ap.add_argument("--chunk-kb", type=int, default=256)
+    ap.add_argument("--copy-ctas", type=int, default=0)
+    ap.add_argument("--chunk-kb", type=int, default=0)
     ap.add_argument("--pool-gb", type=int, default=16)
+    ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 SM swap kernel, 2 copy-engine DMA")
+    ap.add_argument("--dma-group-mb", type=int, default=0)
+    ap.add_argument("--dma-streams", type=int, default=0)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

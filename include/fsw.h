@@ -53,8 +53,9 @@ typedef enum {
 #define FSW_NO_OVERLAP   0x1u /* swap completes before the first layer kernel starts
                                  ("Non-pipeline" column of PAPER.md Table 4; also needed under
                                  ncu / compute-sanitizer, which serialise kernels)             */
-#define FSW_DMA_BASELINE 0x2u /* swap by copy-engine DMA (cudaMemcpyAsync from pinned memory,
-                                 the paper's mechanism) instead of SM copy kernels */
+#define FSW_DMA_BASELINE 0x2u /* the paper's transfer as a baseline: copy-engine DMA in ~2-MB
+                                 groups, one copy stream; overrides the
+                                 engine / group / stream settings                                */
 #define FSW_HOST_WC      0x4u /* back host stores with write-combined pinned pages            */
 #define FSW_HOST_ONLY    0x8u /* no GPU: registration / host-store / allocator logic only (tests);
                                  invoke returns FSW_ECUDA                                       */
@@ -65,13 +66,29 @@ typedef struct {
     uint64_t pool_bytes_per_gpu;      /* weight pool per GPU, pre-allocated at init; 0 = 64 GiB
                                          (capped at 60% of free memory)                       */
     uint64_t workspace_bytes_per_gpu; /* activation workspace per GPU; 0 = 512 MiB            */
-    uint32_t copy_ctas;               /* CTAs of the swap kernel; 0 = 32                      */
+    uint32_t copy_ctas;               /* CTAs of the SM swap kernel; 0 = 16                   */
     uint32_t copy_threads;            /* threads per swap CTA (multiple of 32); 0 = 256       */
     uint64_t chunk_bytes;             /* swap piece size (the paper's "group size",
-                                         PAPER.md:600-604); multiple of 256; 0 = 256 KiB       */
+                                         PAPER.md:600-604) of the SM engine; multiple of 256;
+                                         0 = 16 KiB (small pieces keep the swap in layer order) */
     uint64_t stripe_min_bytes;        /* reserved for striped swap; 0 = 256 MiB               */
     uint32_t flags;                   /* FSW_NO_OVERLAP | FSW_DMA_BASELINE | FSW_HOST_WC       */
+    uint32_t engine;                  /* FSW_ENGINE_*; 0 = AUTO                                */
+    uint64_t dma_min_bytes;           /* AUTO picks DMA for models with at least this many store
+                                         bytes, SM below; 0 = 32 MiB                           */
+    uint64_t dma_group_bytes;         /* DMA engine: target bytes per copy group (whole layers are
+                                         merged up to it, larger layers split, groups taper
+                                         towards the end of the store); 0 = 64 MiB             */
+    uint32_t dma_streams;             /* DMA engine: concurrent copy streams (1..4); 0 = 1      */
 } fsw_config;
+
+/* Swap engines.  Both move the host store into the extent in execution order and
+ * publish readiness in device memory that the layer kernels acquire:
+ *   SM : persistent CTAs stream pieces with 128-bit loads from mapped host memory; one release-add
+ *        of the piece's bytes on its layer's counter per piece (fine-grained, no per-copy setup);
+ *   DMA: copy-engine cudaMemcpyAsync of layer-aligned groups on `dma_streams` streams; after each
+ *        group a stream memory write (no SM) bumps that stream's group counter.               */
+enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2 };
 
 typedef struct fsw_ctx fsw_ctx; /* opaque; one per process */
 
@@ -161,14 +178,17 @@ typedef struct {
     double total_ms;        /* host wall clock: call entry -> output in the caller buffer   */
     double device_ms;       /* CUDA events around the invoke graph on the launching stream  */
     double swap_ms;         /* CUDA events around the swap kernel on its own stream         */
-    double swap_span_ms;    /* %globaltimer: first piece claimed -> last piece released     */
-    double compute_tail_ms; /* %globaltimer: last piece released -> last layer finished     */
+    double swap_span_ms;    /* SM: %globaltimer first piece claimed -> last released; DMA: = swap_ms */
+    double compute_tail_ms; /* last weight byte landed -> last layer finished (SM: %globaltimer;
+                               DMA: CUDA events, includes the output D2H)                     */
     uint64_t bytes_swapped;
     double link_gbps;       /* bytes_swapped / swap_ms                                       */
     int32_t gpu;
     uint32_t swap_kind;     /* FSW_SWAP_*                                                     */
     uint32_t n_sources;
     uint32_t n_kernels;     /* kernels launched by this invoke (incl. the swap kernel)       */
+    uint32_t engine;        /* FSW_ENGINE_SM / FSW_ENGINE_DMA for a cold invoke, else 0        */
+    uint32_t n_copies;      /* swap pieces (SM) or copy-engine groups (DMA) of this invoke      */
 } fsw_invoke_stats;
 
 /* Run one request: pick a GPU (resident and idle first, then the lowest idle id,
@@ -188,6 +208,9 @@ typedef struct {
     uint32_t order_seed;
     uint32_t copy_ctas;   /* 0 = ctx default                                                   */
     uint32_t flags;       /* FSW_NO_OVERLAP | FSW_DMA_BASELINE, OR-ed with the ctx flags       */
+    uint32_t engine;      /* FSW_ENGINE_*; 0 = ctx default                                     */
+    uint64_t dma_group_bytes; /* 0 = ctx default                                               */
+    uint32_t dma_streams;     /* 0 = ctx default                                               */
 } fsw_invoke_opts;
 fsw_status fsw_invoke_ex(fsw_ctx* ctx, uint32_t model_id, const fsw_invoke_opts* opts,
                          const void* input, uint64_t input_bytes, void* output, uint64_t output_cap,
@@ -210,6 +233,16 @@ fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu,
 fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
 /* Activation slot of the last invoke of `model_id` on `gpu` (valid until the next invoke). */
 fsw_status fsw_debug_read_slot(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, int32_t slot, void* dst, uint64_t cap);
+
+/* The DMA engine's copy plan for (group_bytes, streams), host logic only (usable with
+ * FSW_HOST_ONLY): n_groups copy groups [lo, hi) of the host store in execution order, each
+ * dealt to copy stream group_stream[i] = i mod streams; for every layer L, layer_targets[4L+j]
+ * = the number of stream-j groups that must have landed before L's weights are complete.
+ * group_lo_hi has 2·cap_groups entries; n_groups is set even when cap_groups is too small
+ * (then EINVAL).  Any output pointer may be NULL.                                          */
+fsw_status fsw_debug_dma_plan(fsw_ctx* ctx, uint32_t model_id, uint64_t group_bytes, uint32_t streams,
+                              uint64_t* group_lo_hi, uint32_t* group_stream, uint32_t cap_groups,
+                              uint32_t* n_groups, uint32_t* layer_targets);
 
 /* ---------------------------------------------------------------------------------------
  * Extent allocator of the weight pool (pure host logic, usable without a GPU; tests).

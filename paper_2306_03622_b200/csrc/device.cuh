@@ -42,23 +42,24 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
 // CTA barrier.  The acquire pairs with the swap kernel's red.release; the barrier extends
 // the ordering to the rest of the CTA.  A watchdog turns a lost release into an error word.
 __device__ __forceinline__ void wait_ready_thread(const Wait& w) {
-    if (w.ready == nullptr) return;
-    if (ld_acquire_gpu(w.ready) >= w.target) return;
-    const uint64_t t0 = globaltimer();
-    uint32_t ns = 64;
-    while (ld_acquire_gpu(w.ready) < w.target) {
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
-        if (globaltimer() - t0 > kWatchdogNs) {
-            atomicExch(&w.ctl->err, 1);
-            atomicExch(&w.ctl->err_layer, w.layer);
-            break;
+    for (uint32_t j = 0; j < w.n; ++j) {
+        if (ld_acquire_gpu(w.ready[j]) >= w.target[j]) continue;
+        const uint64_t t0 = globaltimer();
+        uint32_t ns = 64;
+        while (ld_acquire_gpu(w.ready[j]) < w.target[j]) {
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+            if (globaltimer() - t0 > kWatchdogNs) {
+                atomicExch(&w.ctl->err, 1);
+                atomicExch(&w.ctl->err_layer, w.layer);
+                return;
+            }
         }
     }
 }
 
 __device__ __forceinline__ void wait_ready_cta(const Wait& w) {
-    if (w.ready == nullptr) return;
+    if (w.n == 0) return;
     if (threadIdx.x == 0) wait_ready_thread(w);
     __syncthreads();
 }

@@ -36,10 +36,15 @@ struct Piece {
     uint32_t layer;   // ready counter to bump
 };
 
-// Readiness wait for a layer kernel: spin until ready[idx] >= target (bytes of the layer).
+// Readiness wait for a layer kernel: spin until ready[j][0] >= target[j] for every j < n.
+//   SM engine : n = 1, the layer's byte counter, target = the layer's region bytes.
+//   DMA engine: n = copy streams, each stream's group counter, target = groups of that stream
+//               up to the group holding the layer's last byte.
+constexpr int kMaxWaitSrc = 4;
 struct Wait {
-    const uint32_t* ready;  // nullptr = no wait (warm invoke / no weights)
-    uint32_t target;
+    const uint32_t* ready[kMaxWaitSrc];
+    uint32_t target[kMaxWaitSrc];
+    uint32_t n;  // 0 = no wait (warm invoke / no weights)
     DevCtl* ctl;
     int32_t layer;
 };

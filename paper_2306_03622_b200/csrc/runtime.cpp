@@ -14,6 +14,7 @@
 #include <sys/mman.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -162,13 +163,22 @@ struct Launch {  // one kernel of the layer graph (addresses resolved for one GP
 struct Gpu;
 
 struct GraphKey {
-    int cold, flags, order;
+    int cold, flags, order, engine;
     uint64_t chunk;
     uint32_t seed, ctas, extra;
     bool operator<(const GraphKey& o) const {
-        return std::tie(cold, flags, order, chunk, seed, ctas, extra) <
-               std::tie(o.cold, o.flags, o.order, o.chunk, o.seed, o.ctas, o.extra);
+        return std::tie(cold, flags, order, engine, chunk, seed, ctas, extra) <
+               std::tie(o.cold, o.flags, o.order, o.engine, o.chunk, o.seed, o.ctas, o.extra);
     }
+};
+
+// DMA engine plan: layer-aligned copy groups dealt round-robin to `streams` copy streams, and
+// for every layer the per-stream group count that covers the layer's last byte.
+struct DmaPlan {
+    struct Group { uint64_t lo, hi; uint32_t stream; };
+    std::vector<Group> groups;
+    std::vector<std::array<uint32_t, kMaxWaitSrc>> target;  // [layer][stream]
+    uint32_t streams = 1;
 };
 
 struct PieceSet {
@@ -184,6 +194,7 @@ struct Plan {  // one model on one GPU
     uint64_t ws_bytes = 0;
     std::map<GraphKey, cudaGraphExec_t> graphs;
     std::map<std::tuple<uint64_t, int, uint32_t>, PieceSet> pieces;  // (chunk, order, seed)
+    std::map<std::pair<uint64_t, uint32_t>, DmaPlan> dma;            // (group bytes, streams)
 };
 
 struct Model {
@@ -210,6 +221,9 @@ struct Model {
 struct Gpu {
     int dev = 0;
     cudaStream_t sx = nullptr, sc = nullptr;
+    cudaStream_t sd[kMaxWaitSrc] = {};  // DMA copy streams (sd[0] == sc)
+    cudaEvent_t evd[kMaxWaitSrc] = {};  // fork / join events of the DMA streams
+    uint32_t* progress = nullptr;       // DMA: one group counter per copy stream, 128 B apart
     uint8_t* pool = nullptr;
     uint64_t pool_bytes = 0;
     fsw_arena* arena = nullptr;
@@ -251,6 +265,11 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     init_ops_attrs();
     CU(cudaStreamCreateWithFlags(&g.sx, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&g.sc, cudaStreamNonBlocking));
+    g.sd[0] = g.sc;
+    for (int j = 1; j < kMaxWaitSrc; ++j) CU(cudaStreamCreateWithFlags(&g.sd[j], cudaStreamNonBlocking));
+    for (int j = 0; j < kMaxWaitSrc; ++j) CU(cudaEventCreateWithFlags(&g.evd[j], cudaEventDisableTiming));
+    CU(cudaMalloc(&g.progress, 128 * kMaxWaitSrc));
+    CU(cudaMemset(g.progress, 0, 128 * kMaxWaitSrc));
     size_t free_b = 0, total_b = 0;
     CU(cudaMemGetInfo(&free_b, &total_b));
     uint64_t want = c->cfg.pool_bytes_per_gpu ? c->cfg.pool_bytes_per_gpu : (64ull << 30);
@@ -295,10 +314,15 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
         return fail(FSW_ECUDA, "fsw_init: no CUDA device (%s)", e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
     auto c = std::make_unique<fsw_ctx>();
     if (cfg) c->cfg = *cfg;
-    if (c->cfg.copy_ctas == 0) c->cfg.copy_ctas = 32;
+    if (c->cfg.copy_ctas == 0) c->cfg.copy_ctas = 16;
     if (c->cfg.copy_threads == 0) c->cfg.copy_threads = 256;
-    if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 256 << 10;
+    if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 16 << 10;
     if (c->cfg.stripe_min_bytes == 0) c->cfg.stripe_min_bytes = 256ull << 20;
+    if (c->cfg.dma_min_bytes == 0) c->cfg.dma_min_bytes = 32ull << 20;
+    if (c->cfg.dma_group_bytes == 0) c->cfg.dma_group_bytes = 64ull << 20;
+    if (c->cfg.dma_streams == 0) c->cfg.dma_streams = 1;
+    if (c->cfg.engine > FSW_ENGINE_DMA || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
+        return fail(FSW_EINVAL, "fsw_init: engine, dma_streams (1..4) or dma_group_bytes (multiple of 256) invalid");
     if (c->cfg.chunk_bytes % 256 || c->cfg.copy_threads % 32 || c->cfg.copy_threads > 512)
         return fail(FSW_EINVAL, "fsw_init: chunk_bytes must be a multiple of 256, copy_threads a multiple of 32 <= 512");
     uint32_t n = c->cfg.n_gpus ? c->cfg.n_gpus : (uint32_t)ndev;
@@ -354,6 +378,9 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFreeHost(g.hout);
         cudaFreeHost(g.hctl);
         for (cudaEvent_t e : {g.ev0, g.ev1, g.evs0, g.evs1, g.evfork, g.evjoin}) cudaEventDestroy(e);
+        for (int j = 0; j < kMaxWaitSrc; ++j) cudaEventDestroy(g.evd[j]);
+        for (int j = 1; j < kMaxWaitSrc; ++j) cudaStreamDestroy(g.sd[j]);
+        cudaFree(g.progress);
         cudaStreamDestroy(g.sx);
         cudaStreamDestroy(g.sc);
         fsw_arena_destroy(g.arena);
@@ -912,14 +939,114 @@ static fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int orde
     return FSW_OK;
 }
 
-static void enqueue_layers(Model& m, Plan& p, Gpu& g, bool cold, cudaStream_t s) {
+// Copy groups of the DMA engine: whole layers are merged in execution order until a group holds
+// at least `grp` bytes; a layer region larger than 2·grp is split into ≈grp pieces (256-B
+// aligned).  Layer regions are contiguous in the store, so groups tile [0, store_bytes).
+static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams) {
+    DmaPlan d;
+    d.streams = streams;
+    const size_t nl = m.layers.size();
+    std::vector<uint32_t> last_group(nl, 0);
+    uint64_t lo = 0, hi = 0;  // open group [lo, hi)
+    auto close = [&]() {
+        if (hi > lo) {
+            d.groups.push_back({lo, hi, (uint32_t)(d.groups.size() % streams)});
+            lo = hi;
+        }
+    };
+    // Taper: a group starting at `lo` aims at min(grp, max(tail_min, remaining / 2)) bytes, so the
+    // groups shrink geometrically towards the end of the store.  The compute that trails the last
+    // byte is then only the last small group's layers (big groups amortise the ~8 us per-copy
+    // setup of the copy engine; small ones bound the tail).
+    const uint64_t total = m.store_bytes, tail_min = std::min<uint64_t>(grp, 1ull << 20);
+    auto want = [&](uint64_t at) { return std::min(grp, std::max(tail_min, align_up((total - at) / 2, 256))); };
+    for (size_t li = 0; li < nl; ++li) {
+        const uint64_t ro = m.region_off[li], rb = m.region_bytes[li];
+        if (!rb) continue;
+        if (rb > 2 * want(ro)) {
+            close();
+            for (uint64_t o = 0; o < rb;) {
+                const uint64_t w = want(ro + o);
+                const uint64_t step = rb - o <= 2 * w ? rb - o : w;
+                o += step;
+                hi = ro + o;
+                close();
+            }
+        } else {
+            hi = ro + rb;
+            if (hi - lo >= want(lo)) close();
+        }
+        last_group[li] = hi > lo ? (uint32_t)d.groups.size() : (uint32_t)d.groups.size() - 1;
+    }
+    close();
+    d.target.assign(nl, {});
+    for (size_t li = 0; li < nl; ++li) {
+        if (!m.region_bytes[li]) continue;
+        const uint32_t gl = last_group[li];
+        for (uint32_t j = 0; j < streams; ++j) d.target[li][j] = gl >= j ? (gl - j) / streams + 1 : 0;
+    }
+    return d;
+}
+
+static const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams) {
+    const auto key = std::make_pair(grp, streams);
+    auto it = p.dma.find(key);
+    if (it != p.dma.end()) return it->second;
+    return p.dma.emplace(key, make_dma_plan(m, grp, streams)).first->second;
+}
+
+// Host-only inspection of the DMA engine's copy plan (tests; no GPU needed).
+extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group_bytes, uint32_t streams,
+                                         uint64_t* group_lo_hi, uint32_t* group_stream, uint32_t cap_groups,
+                                         uint32_t* n_groups, uint32_t* layer_targets /* [n_layers][4] */) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!n_groups || group_bytes == 0 || group_bytes % 256 || streams == 0 || streams > (uint32_t)kMaxWaitSrc)
+        return fail(FSW_EINVAL, "dma_plan: bad argument");
+    const DmaPlan d = make_dma_plan(*m, group_bytes, streams);
+    *n_groups = (uint32_t)d.groups.size();
+    if (d.groups.size() > cap_groups) return fail(FSW_EINVAL, "dma_plan: %zu groups > cap %u", d.groups.size(), cap_groups);
+    for (size_t i = 0; i < d.groups.size(); ++i) {
+        if (group_lo_hi) {
+            group_lo_hi[2 * i] = d.groups[i].lo;
+            group_lo_hi[2 * i + 1] = d.groups[i].hi;
+        }
+        if (group_stream) group_stream[i] = d.groups[i].stream;
+    }
+    if (layer_targets)
+        for (size_t li = 0; li < m->layers.size(); ++li)
+            for (int j = 0; j < kMaxWaitSrc; ++j) layer_targets[4 * li + j] = d.target[li][j];
+    return FSW_OK;
+}
+
+struct InvokeCfg {
+    bool cold, no_overlap;
+    int engine;  // FSW_ENGINE_SM / FSW_ENGINE_DMA (resolved)
+    uint64_t chunk;
+    int order;
+    uint32_t seed, ctas;
+    uint8_t* wbase;              // only used by DMA graphs (memcpy nodes need absolute addresses)
+    const DmaPlan* dma_plan;     // DMA engine only
+};
+
+static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaStream_t s) {
     const DevDesc* d = reinterpret_cast<const DevDesc*>(g.dstage);
     for (const Launch& x : p.launches) {
-        Wait w{nullptr, 0, g.ctl, x.layer};
-        const bool has_weights = m.region_bytes[x.layer] > 0;
-        if (cold && has_weights) {
-            w.ready = g.ready + x.layer;
-            w.target = (uint32_t)m.region_bytes[x.layer];
+        Wait w{};
+        w.ctl = g.ctl;
+        w.layer = x.layer;
+        if (ic.cold && m.region_bytes[x.layer] > 0) {
+            if (ic.engine == FSW_ENGINE_SM) {
+                w.n = 1;
+                w.ready[0] = g.ready + x.layer;
+                w.target[0] = (uint32_t)m.region_bytes[x.layer];
+            } else {
+                w.n = ic.dma_plan->streams;
+                for (uint32_t j = 0; j < w.n; ++j) {
+                    w.ready[j] = g.progress + 32 * j;
+                    w.target[j] = ic.dma_plan->target[x.layer][j];
+                }
+            }
         }
         switch (x.kind) {
             case K_EMBED: launch_embed(s, d, w, x.embed); break;
@@ -934,14 +1061,6 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, bool cold, cudaStream_t s)
     }
 }
 
-struct InvokeCfg {
-    bool cold, dma, no_overlap;
-    uint64_t chunk;
-    int order;
-    uint32_t seed, ctas;
-    uint8_t* wbase;  // only used by DMA graphs (memcpy nodes need absolute addresses)
-};
-
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 static PFN_writeValue32 get_write_value32() {
     void* p = nullptr;
@@ -955,7 +1074,7 @@ static PFN_writeValue32 get_write_value32() {
 // timing) and the gate; then the flag-gated layer kernels; then D2H of output and ctl.
 static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out) {
     PieceSet* ps = nullptr;
-    if (ic.cold) {
+    if (ic.cold && ic.engine == FSW_ENGINE_SM) {
         fsw_status s = get_pieces(m, p, g, ic.chunk, ic.order, ic.seed, &ps);
         if (s != FSW_OK) return s;
         if (m.layers.size() > g.ready_cap) return fail(FSW_EINVAL, "too many layers");
@@ -966,35 +1085,42 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
     cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr + m.input_bytes, cudaMemcpyHostToDevice, sx);
     cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
     if (ic.cold) {
-        cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
+        if (ic.engine == FSW_ENGINE_SM) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
+        else cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
         cudaEventRecord(g.evfork, sx);
         cudaStreamWaitEvent(sc, g.evfork, 0);
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
-        if (!ic.dma) {
+        if (ic.engine == FSW_ENGINE_SM) {
             launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, reinterpret_cast<const DevDesc*>(g.dstage),
                         ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl);
         } else {
-            // The paper's mechanism: copy-engine DMA from pinned memory in
-            // groups of >= 2 MB, layer by layer; after each layer a stream memory write (no kernel,
-            // so no SM is needed while layer kernels spin) publishes the layer's byte count.
+            // Copy-engine DMA from the pinned store (the paper's transfer) in
+            // layer-aligned groups (its "group" pipelining unit), dealt round-robin
+            // to the copy streams so one engine's per-copy setup overlaps another's transfer.  After
+            // each group a stream memory write (no kernel, so no SM is needed while layer kernels
+            // spin) publishes that stream's group count; its default flags fence the copy first.
             static PFN_writeValue32 wv = get_write_value32();
             if (!wv) return fail(FSW_ECUDA, "cuStreamWriteValue32 entry point unavailable");
-            const uint64_t grp = std::max<uint64_t>(ic.chunk, 2ull << 20);
-            for (uint32_t li = 0; li < m.layers.size(); ++li) {
-                if (!m.region_bytes[li]) continue;
-                for (uint64_t o = 0; o < m.region_bytes[li]; o += grp) {
-                    const uint64_t off = m.region_off[li] + o, nb = std::min<uint64_t>(grp, m.region_bytes[li] - o);
-                    cudaMemcpyAsync(ic.wbase + off, m.store + off, nb, cudaMemcpyHostToDevice, sc);
-                }
-                wv(sc, (CUdeviceptr)(g.ready + li), (cuuint32_t)m.region_bytes[li], 0);
+            const DmaPlan& dp = *ic.dma_plan;
+            cudaEventRecord(g.evd[0], sc);
+            for (uint32_t j = 1; j < dp.streams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
+            uint32_t cnt[kMaxWaitSrc] = {};
+            for (const auto& gr : dp.groups) {
+                cudaStream_t sj = g.sd[gr.stream];
+                cudaMemcpyAsync(ic.wbase + gr.lo, m.store + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sj);
+                wv(sj, (CUdeviceptr)(g.progress + 32 * gr.stream), (cuuint32_t)(++cnt[gr.stream]), 0);
+            }
+            for (uint32_t j = 1; j < dp.streams; ++j) {
+                cudaEventRecord(g.evd[j], g.sd[j]);
+                cudaStreamWaitEvent(sc, g.evd[j], 0);
             }
         }
         cudaEventRecordWithFlags(g.evs1, sc, cudaEventRecordExternal);
         cudaEventRecord(g.evjoin, sc);
         if (ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
-        else if (!ic.dma) launch_gate(sx, g.ctl, ic.ctas);
+        else if (ic.engine == FSW_ENGINE_SM) launch_gate(sx, g.ctl, ic.ctas);
     }
-    enqueue_layers(m, p, g, ic.cold, sx);
+    enqueue_layers(m, p, g, ic, sx);
     launch_finish(sx, g.ctl);
     if (ic.cold && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
     cudaMemcpyAsync(g.hout, g.ws + p.slot_off[m.output_slot], m.output_bytes, cudaMemcpyDeviceToHost, sx);
@@ -1162,13 +1288,23 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     }
     Plan& p = *m->plans[gi];
     const uint32_t flags = o.flags | c->cfg.flags;
-    InvokeCfg ic{cold, (flags & FSW_DMA_BASELINE) != 0, (flags & FSW_NO_OVERLAP) != 0,
+    const bool baseline = (flags & FSW_DMA_BASELINE) != 0;
+    int engine = (int)(o.engine ? o.engine : c->cfg.engine);
+    if (baseline) engine = FSW_ENGINE_DMA;
+    if (engine == FSW_ENGINE_AUTO) engine = m->store_bytes >= c->cfg.dma_min_bytes ? FSW_ENGINE_DMA : FSW_ENGINE_SM;
+    const uint64_t dgrp = baseline ? (2ull << 20) : o.dma_group_bytes ? o.dma_group_bytes : c->cfg.dma_group_bytes;
+    const uint32_t dstr = baseline ? 1u : o.dma_streams ? o.dma_streams : c->cfg.dma_streams;
+    if (engine > FSW_ENGINE_DMA || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
+        return finish(fail(FSW_EINVAL, "invoke: bad engine / dma_group_bytes / dma_streams"));
+    InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
-                 o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, g.pool + (m->extent[gi] >= 0 ? m->extent[gi] : 0)};
+                 o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, g.pool + (m->extent[gi] >= 0 ? m->extent[gi] : 0), nullptr};
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
-    GraphKey key{cold, (int)(flags & (FSW_DMA_BASELINE | FSW_NO_OVERLAP)), cold ? ic.order : 0, cold ? ic.chunk : 0,
-                 cold ? ic.seed : 0, cold ? ic.ctas : 0, 0};
-    if (cold && ic.dma) key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);  // DMA graphs bake addresses
+    if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr);
+    const bool sm = engine == FSW_ENGINE_SM;
+    GraphKey key{cold, (int)(flags & FSW_NO_OVERLAP), cold && sm ? ic.order : 0, cold ? engine : 0,
+                 cold ? (sm ? ic.chunk : dgrp) : 0, cold && sm ? ic.seed : 0, cold ? (sm ? ic.ctas : dstr) : 0, 0};
+    if (cold && !sm) key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);  // DMA graphs bake addresses
     auto it = p.graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (it == p.graphs.end()) {
@@ -1203,14 +1339,25 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         stats->swap_kind = cold ? FSW_SWAP_HOST : FSW_SWAP_RESIDENT;
         stats->n_kernels = (uint32_t)p.launches.size() + 1 /*finish*/;
         if (cold) {
-            float sm = 0;
-            cudaEventElapsedTime(&sm, g.evs0, g.evs1);
-            stats->swap_ms = sm;
+            float swap_ms = 0;
+            cudaEventElapsedTime(&swap_ms, g.evs0, g.evs1);
+            stats->swap_ms = swap_ms;
             stats->bytes_swapped = m->store_bytes;
-            stats->link_gbps = sm > 0 ? m->store_bytes / (sm * 1e6) : 0;
-            if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
-            if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
-            if (!ic.dma) stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)
+            stats->link_gbps = swap_ms > 0 ? m->store_bytes / (swap_ms * 1e6) : 0;
+            stats->engine = (uint32_t)engine;
+            if (sm) {
+                if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
+                if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
+                stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)
+                PieceSet* ps = nullptr;
+                if (get_pieces(*m, p, g, ic.chunk, ic.order, ic.seed, &ps) == FSW_OK) stats->n_copies = (uint32_t)ps->host.size();
+            } else {
+                float tail = 0;
+                cudaEventElapsedTime(&tail, g.evs1, g.ev1);
+                stats->swap_span_ms = swap_ms;
+                stats->compute_tail_ms = tail > 0 ? tail : 0;
+                stats->n_copies = (uint32_t)ic.dma_plan->groups.size();
+            }
         }
     }
     {

@@ -21,6 +21,7 @@ STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA
 NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY = 0x1, 0x2, 0x4, 0x8
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
+ENGINE_AUTO, ENGINE_SM, ENGINE_DMA = 0, 1, 2
 
 u32, u64, i32, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -34,7 +35,8 @@ class FswError(RuntimeError):
 class Config(ctypes.Structure):
     _fields_ = [("n_gpus", u32), ("gpu_ids", ctypes.POINTER(i32)), ("pool_bytes_per_gpu", u64),
                 ("workspace_bytes_per_gpu", u64), ("copy_ctas", u32), ("copy_threads", u32),
-                ("chunk_bytes", u64), ("stripe_min_bytes", u64), ("flags", u32)]
+                ("chunk_bytes", u64), ("stripe_min_bytes", u64), ("flags", u32), ("engine", u32),
+                ("dma_min_bytes", u64), ("dma_group_bytes", u64), ("dma_streams", u32)]
 
 
 class Tensor(ctypes.Structure):
@@ -72,7 +74,7 @@ class StoreTensor(ctypes.Structure):
 class InvokeStats(ctypes.Structure):
     _fields_ = [("total_ms", dbl), ("device_ms", dbl), ("swap_ms", dbl), ("swap_span_ms", dbl),
                 ("compute_tail_ms", dbl), ("bytes_swapped", u64), ("link_gbps", dbl), ("gpu", i32),
-                ("swap_kind", u32), ("n_sources", u32), ("n_kernels", u32)]
+                ("swap_kind", u32), ("n_sources", u32), ("n_kernels", u32), ("engine", u32), ("n_copies", u32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -80,7 +82,7 @@ class InvokeStats(ctypes.Structure):
 
 class InvokeOpts(ctypes.Structure):
     _fields_ = [("gpu", i32), ("stripe_mask", u32), ("chunk_bytes", u64), ("order", u32), ("order_seed", u32),
-                ("copy_ctas", u32), ("flags", u32)]
+                ("copy_ctas", u32), ("flags", u32), ("engine", u32), ("dma_group_bytes", u64), ("dma_streams", u32)]
 
 
 class PoolStats(ctypes.Structure):
@@ -96,7 +98,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_unregister_model", "fsw_model_info_get", "fsw_store_tensor_get", "fsw_invoke", "fsw_invoke_ex",
            "fsw_evict", "fsw_pool_stats_get", "fsw_n_gpus", "fsw_debug_read_resident", "fsw_debug_read_store",
            "fsw_debug_read_slot", "fsw_arena_create", "fsw_arena_destroy", "fsw_arena_alloc", "fsw_arena_free",
-           "fsw_arena_stats"]
+           "fsw_arena_stats", "fsw_debug_dma_plan"]
 
 _lib = None
 
@@ -133,6 +135,7 @@ def lib():
         L.fsw_arena_free.argtypes = [vp, u64]
         L.fsw_arena_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u32)]
         L.fsw_arena_stats.restype = None
+        L.fsw_debug_dma_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
         for name in EXPORTS:
             f = getattr(L, name)
             if f.restype is ctypes.c_int:  # default
@@ -184,7 +187,8 @@ class Runtime:
 
     def __init__(self, n_gpus: int = 0, gpu_ids: Optional[Sequence[int]] = None, pool_bytes: int = 0,
                  workspace_bytes: int = 0, copy_ctas: int = 0, copy_threads: int = 0, chunk_bytes: int = 0,
-                 flags: int = 0):
+                 flags: int = 0, engine: int = ENGINE_AUTO, dma_min_bytes: int = 0, dma_group_bytes: int = 0,
+                 dma_streams: int = 0):
         cfg = Config()
         cfg.n_gpus = n_gpus or (len(gpu_ids) if gpu_ids else 0)
         self._ids = (i32 * len(gpu_ids))(*gpu_ids) if gpu_ids else None
@@ -192,6 +196,7 @@ class Runtime:
         cfg.pool_bytes_per_gpu = pool_bytes
         cfg.workspace_bytes_per_gpu = workspace_bytes
         cfg.copy_ctas, cfg.copy_threads, cfg.chunk_bytes, cfg.flags = copy_ctas, copy_threads, chunk_bytes, flags
+        cfg.engine, cfg.dma_min_bytes, cfg.dma_group_bytes, cfg.dma_streams = engine, dma_min_bytes, dma_group_bytes, dma_streams
         h = vp()
         _check(lib().fsw_init(ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
@@ -272,14 +277,14 @@ class Runtime:
     # ---- invoke -------------------------------------------------------------------------
     def invoke(self, mid: int, inp: np.ndarray, out: Optional[np.ndarray] = None, gpu: int = -1,
                chunk_bytes: int = 0, order: int = ORDER_EXEC, order_seed: int = 0, copy_ctas: int = 0,
-               flags: int = 0) -> Result:
+               flags: int = 0, engine: int = 0, dma_group_bytes: int = 0, dma_streams: int = 0) -> Result:
         info = self._models.get(mid) or self.model_info(mid)
         inp = np.ascontiguousarray(inp)
         if out is None:
             out = np.empty(info["output_bytes"] // 4, dtype=np.float32 if info["output_dtype"] == 1 else np.int32) \
                 if info["output_dtype"] != 0 else np.empty(info["output_bytes"] // 2, dtype=np.uint16)
         st = InvokeStats()
-        opts = InvokeOpts(gpu, 0, chunk_bytes, order, order_seed, copy_ctas, flags)
+        opts = InvokeOpts(gpu, 0, chunk_bytes, order, order_seed, copy_ctas, flags, engine, dma_group_bytes, dma_streams)
         _check(lib().fsw_invoke_ex(self.h, mid, ctypes.byref(opts), inp.ctypes.data, inp.nbytes, out.ctypes.data,
                                    out.nbytes, ctypes.byref(st)))
         return Result(out, st.as_dict())
@@ -300,6 +305,17 @@ class Runtime:
         return p.as_dict()
 
     # ---- debug --------------------------------------------------------------------------
+    def dma_plan(self, mid: int, group_bytes: int, streams: int):
+        """DMA engine copy plan: (groups [n][2] = [lo, hi), stream [n], layer targets [n_layers][4])."""
+        n = u32()
+        lib().fsw_debug_dma_plan(self.h, mid, group_bytes, streams, None, None, 0, ctypes.byref(n), None)
+        lohi = np.zeros((max(1, n.value), 2), np.uint64)
+        st = np.zeros(max(1, n.value), np.uint32)
+        tg = np.zeros((self.model_info(mid)["n_layers"], 4), np.uint32)
+        _check(lib().fsw_debug_dma_plan(self.h, mid, group_bytes, streams, lohi.ctypes.data, st.ctypes.data,
+                                        n.value, ctypes.byref(n), tg.ctypes.data))
+        return lohi[:n.value], st[:n.value], tg
+
     def read_resident(self, mid: int, gpu: int = 0) -> np.ndarray:
         n = self.model_info(mid)["store_bytes"]
         buf = np.empty(n, dtype=np.uint8)

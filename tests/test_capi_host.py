@@ -238,3 +238,44 @@ def test_synth_is_deterministic_and_seeded():
     assert not np.array_equal(a, s.build_weights())
     ids = synth.build_model("bert-base").make_input().view(np.int32)
     assert ids.min() >= 0 and ids.max() < 30522 and len(np.unique(ids)) > 100
+
+
+# ---------------------------------------------------------------------------------------------
+# DMA engine copy plan (host logic of the swap engine)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["bert-base", "resnet50", "mlp", "bert-tiny"])
+@pytest.mark.parametrize("grp,streams", [(8 << 20, 2), (2 << 20, 1), (1 << 20, 3), (16 << 20, 4), (256, 2)])
+def test_dma_plan_tiles_store_and_covers_each_layer(name, grp, streams):
+    spec = synth.build_model(name)
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, spec.build_weights())
+        info = rt.model_info(mid)
+        lohi, st, tg = rt.dma_plan(mid, grp, streams)
+        # groups tile [0, store_bytes) contiguously in execution order, 256-B aligned
+        assert lohi[0, 0] == 0 and lohi[-1, 1] == info["store_bytes"]
+        assert np.all(lohi[1:, 0] == lohi[:-1, 1]) and np.all(lohi[:, 1] > lohi[:, 0])
+        assert np.all(lohi % 256 == 0)
+        assert np.array_equal(st, np.arange(len(st)) % streams)
+        # no group exceeds a layer-merge bound: merged layers stop once >= grp, a split piece <= grp+255
+        regions = []
+        off = 0
+        for li in range(info["n_layers"]):
+            refs = [r for r in spec.layers[li].refs]
+            placed = [rt.store_tensor(mid, r) for r in refs]
+            mine = [p for p in placed if p["owner_layer"] == li]
+            hi = max((p["offset"] + p["bytes"] for p in mine), default=None)
+            regions.append(hi)
+        counts = np.zeros(streams, np.int64)
+        done = []   # done[g] = per-stream counts after group g landed
+        for g in range(len(st)):
+            counts[st[g]] += 1
+            done.append(counts.copy())
+        for li, hi in enumerate(regions):
+            if hi is None:
+                assert not tg[li].any()
+                continue
+            # the minimal group prefix holding the layer's last byte, expressed per stream
+            g = int(np.searchsorted(lohi[:, 1], hi, side="left"))
+            assert lohi[g, 0] < hi <= lohi[g, 1]
+            np.testing.assert_array_equal(tg[li, :streams], done[g])
+            assert not tg[li, streams:].any()

@@ -27,11 +27,15 @@ def test_evict_invalidates_without_copy_and_lru():
         st = rt.pool_stats(0)
         assert st["n_evictions"] == 1 and st["n_resident"] == 2
         assert rt.invoke(ids[0], x, gpu=0).stats["swap_kind"] == 0
-        assert rt.invoke(ids[1], x, gpu=0).stats["swap_kind"] == 1     # evicted -> cold again
+        assert rt.invoke(ids[1], x, gpu=0).stats["swap_kind"] == 1     # evicted -> cold again,
+        assert rt.pool_stats(0)["n_evictions"] == 2                    # evicting LRU model 2
         np.testing.assert_array_equal(outs[0].output, outs[1].output)
-        rt.evict(ids[2], 0)
         with pytest.raises(FswError) as e:
-            rt.evict(ids[2], 0)
+            rt.evict(ids[2], 0)                                        # not resident any more
+        assert e.value.status == F.ESTATE
+        rt.evict(ids[1], 0)
+        with pytest.raises(FswError) as e:
+            rt.evict(ids[1], 0)
         assert e.value.status == F.ESTATE
 
 

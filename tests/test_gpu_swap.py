@@ -4,35 +4,34 @@ import numpy as np
 import pytest
 
 import synth
-from paper_2306_03622_b200 import DMA_BASELINE, NO_OVERLAP, ORDER_RANDOM, ORDER_REVERSE
+from paper_2306_03622_b200 import DMA_BASELINE, ENGINE_DMA, ENGINE_SM, NO_OVERLAP, ORDER_RANDOM, ORDER_REVERSE
 from synth.models import DT_BF16, DT_F32, Act, ModelSpec, Op
 
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_DMA])
 @pytest.mark.parametrize("name", ["mlp", "bert-base", "resnet50", "gpt2-2L"])
-def test_swapped_bytes_bit_exact(rt, registered, name):
+def test_swapped_bytes_bit_exact(rt, registered, name, engine):
     spec, w, x, mid = registered(name)
     rt.evict(mid)
-    r = rt.invoke(mid, x, gpu=0)
+    r = rt.invoke(mid, x, gpu=0, engine=engine)
     assert r.stats["swap_kind"] == 1 and r.stats["bytes_swapped"] == rt.model_info(mid)["store_bytes"]
+    assert r.stats["engine"] == engine and r.stats["n_copies"] >= 1
     np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
 
 
 def _odd_model(sizes):
-    """One LINEAR per size; weights of odd byte counts (rows*K*2 with K=8) exercise piece tails."""
+    """One LINEAR per size, all reading the input; weight tensors of rows x 8 bf16 (16·rows bytes)
+    exercise piece / group tails that are not multiples of the piece or group size."""
     m = ModelSpec("odd", 31)
-    prev = m.slot("x", (1, 8), DT_F32)
-    m.input_slot = prev
+    x = m.slot("x", (1, 8), DT_F32)
+    m.input_slot = x
     for i, rows in enumerate(sizes):
         wt = m.tensor(f"w{i}", (rows, 8), init=("uniform", 0.1))
         out = m.slot(f"y{i}", (1, rows), DT_F32)
-        m.layer(Op.LINEAR, [wt], prev, -1, out, [Act.NONE])
-        nxt = m.slot(f"z{i}", (1, 8), DT_F32)
-        back = m.tensor(f"v{i}", (8, rows), init=("uniform", 0.1))
-        m.layer(Op.LINEAR, [back], out, -1, nxt, [Act.NONE])
-        prev = nxt
-    m.output_slot = prev
+        m.layer(Op.LINEAR, [wt], x, -1, out, [Act.NONE])
+    m.output_slot = out
     return m
 
 
@@ -45,7 +44,23 @@ def test_piece_size_and_cta_sweep_bit_exact(rt, chunk, ctas):
     try:
         for order in (0, ORDER_REVERSE, ORDER_RANDOM):
             rt.evict(mid)
-            rt.invoke(mid, spec.make_input(), gpu=0, chunk_bytes=chunk, copy_ctas=ctas, order=order, order_seed=chunk)
+            rt.invoke(mid, spec.make_input(), gpu=0, chunk_bytes=chunk, copy_ctas=ctas, order=order, order_seed=chunk,
+                      engine=ENGINE_SM)
+            np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    finally:
+        rt.unregister(mid)
+
+
+@pytest.mark.parametrize("grp,streams", [(256, 1), (4096, 2), (64 << 10, 4), (2 << 20, 3), (64 << 20, 2)])
+def test_dma_group_and_stream_sweep_bit_exact(rt, grp, streams):
+    spec = _odd_model([1, 256, 65537, 600_000])
+    mid = rt.register_spec(spec, spec.build_weights())
+    try:
+        for flags in (0, NO_OVERLAP):
+            rt.evict(mid)
+            r = rt.invoke(mid, spec.make_input(), gpu=0, engine=ENGINE_DMA, dma_group_bytes=grp, dma_streams=streams,
+                          flags=flags)
+            assert r.stats["engine"] == ENGINE_DMA
             np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
     finally:
         rt.unregister(mid)
@@ -60,11 +75,12 @@ def test_baseline_modes_bit_exact(rt, registered, flags):
     np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
 
 
-def test_swap_reaches_link_bandwidth(rt, registered):
-    """Sanity floor, not the bench: the SM swap kernel sustains > 40 GB/s on BERT-base."""
+@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_DMA])
+def test_swap_reaches_link_bandwidth(rt, registered, engine):
+    """Sanity floor, not the bench: either swap engine sustains > 40 GB/s on BERT-base."""
     spec, w, x, mid = registered("bert-base")
     gbs = []
     for _ in range(5):
         rt.evict(mid)
-        gbs.append(rt.invoke(mid, x, gpu=0).stats["link_gbps"])
+        gbs.append(rt.invoke(mid, x, gpu=0, engine=engine).stats["link_gbps"])
     assert np.median(gbs) > 40.0, gbs
