@@ -17,6 +17,19 @@
 // issues tcgen05.mma (M=128, N=BN, K=16) into TMEM and commits each stage back to its empty
 // barrier.  All 4 warps then drain TMEM (tcgen05.ld 32x32b) into a shared tile and apply the
 // fused bias / residual / activation epilogue with 16-B coalesced global accesses.
+//
+// Two generalisations for the batch-1 shapes of the paper's models:
+//   * split-K (gridDim.z > 1): small-M GEMMs (ResNet stages 3-4: M = 196 / 49, K up to 4608)
+//     would otherwise run a long serial K loop on a handful of CTAs.  Each split writes an fp32
+//     partial tile; the last CTA to arrive on the tile's counter sums the partials in split order
+//     (deterministic, bit-identical run to run) and runs the epilogue.
+//   * implicit-GEMM convolution (a.conv): the A tile of k-tile (r, s, c0) is Hb output rows x Q
+//     output columns x 64 input channels, gathered straight from the NHWC activation by ONE 4-D
+//     TMA load: start (c0, s − pad, p0·stride + r − pad), element strides = conv stride, and the
+//     out-of-bounds zero fill is the conv padding.  No im2col buffer, no extra kernel.
+// Every launch uses programmatic dependent launch (device.cuh): the prologue and the first
+// stages' WEIGHT loads overlap the previous kernel; activations are touched only after
+// griddepcontrol.wait.
 #include "device.cuh"
 
 namespace fsw {
@@ -57,6 +70,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
             smem_u32(dst)),
         "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -128,11 +149,15 @@ __global__ void __launch_bounds__(128, 1)
     uint64_t* empty = full + stages;
     uint64_t* done = empty + stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint32_t* last_flag = tmem_slot + 1;
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
-    const uint32_t nkt = a.K / kBK;                              // 64-wide k tiles
-    const uint32_t nst = (nkt + C::kSub - 1) / C::kSub;          // pipeline steps
+    const uint32_t tile = blockIdx.x * gridDim.y + blockIdx.y;
+    const uint32_t m0 = blockIdx.x * a.m_rows, n0 = blockIdx.y * BN;
+    const uint32_t kt_begin = blockIdx.z * a.kt_per;
+    const uint32_t nkt = min(a.K / kBK, kt_begin + a.kt_per) - kt_begin;  // >= 1 (host plan)
+    const uint32_t nst = (nkt + C::kSub - 1) / C::kSub;                   // pipeline steps
+    const uint32_t a_bytes = a.conv ? a.Hb * a.Q * (kBK * 2) : C::kA;    // TMA box bytes
     STAMP(0);
 
     if (threadIdx.x == 0) {
@@ -164,17 +189,41 @@ __global__ void __launch_bounds__(128, 1)
             asm volatile("fence.proxy.async.global;" ::: "memory");
             const uint8_t* wt = d->wbase + a.w_off;
             const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
-            for (uint32_t st = 0; st < nst; ++st) {
+            auto load_w = [&](uint32_t st) {
                 const int s = st % stages;
-                if (st >= (uint32_t)stages) mbar_wait(&empty[s], ((st / stages) - 1) & 1);
+                const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
+                uint8_t* sb = smem + s * C::kStage + C::kSub * C::kA;
+                mbar_expect_tx(&full[s], nsub * (a_bytes + C::kB));
+                for (uint32_t j = 0; j < nsub; ++j)
+                    bulk_load(sb + j * C::kB, wt + (kt_begin + kt0 + j) * ktile_stride + (uint64_t)(n0 / 8) * 1024, C::kB,
+                              &full[s]);
+            };
+            auto load_a = [&](uint32_t st) {
+                const int s = st % stages;
                 const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
                 uint8_t* sa = smem + s * C::kStage;
-                uint8_t* sb = sa + C::kSub * C::kA;
-                mbar_expect_tx(&full[s], nsub * (C::kA + C::kB));
                 for (uint32_t j = 0; j < nsub; ++j) {
-                    tma_load_2d(sa + j * C::kA, &tmA, (int)((kt0 + j) * kBK), (int)m0, &full[s]);
-                    bulk_load(sb + j * C::kB, wt + (kt0 + j) * ktile_stride + (uint64_t)(n0 / 8) * 1024, C::kB, &full[s]);
+                    const uint32_t kk = (kt_begin + kt0 + j) * kBK;
+                    if (a.conv) {
+                        const uint32_t tap = kk / a.Cin, c0 = kk - tap * a.Cin, r = tap / a.S, sx = tap - r * a.S;
+                        tma_load_4d(sa + j * C::kA, &tmA, (int)c0, (int)sx - (int)a.pad,
+                                    (int)(blockIdx.x * a.Hb * a.stride + r) - (int)a.pad, 0, &full[s]);
+                    } else {
+                        tma_load_2d(sa + j * C::kA, &tmA, (int)kk, (int)m0, &full[s]);
+                    }
                 }
+            };
+            // weights of the first stages stream while the previous kernel is still running
+            const uint32_t pre = min((uint32_t)stages, nst);
+            for (uint32_t st = 0; st < pre; ++st) load_w(st);
+            pdl_wait();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            for (uint32_t st = 0; st < pre; ++st) load_a(st);
+            for (uint32_t st = pre; st < nst; ++st) {
+                const int s = st % stages;
+                mbar_wait(&empty[s], ((st / stages) - 1) & 1);
+                load_w(st);
+                load_a(st);
             }
         }
         __syncwarp();
@@ -209,6 +258,7 @@ __global__ void __launch_bounds__(128, 1)
     // 1) TMEM -> registers -> shared tile [128][BN+4] fp32 (all MMAs are complete at `done`,
     //    so the stage buffers are free to reuse).
     mbar_wait(done, 0);
+    pdl_trigger();  // the successor's prologue and weight prefetch overlap this epilogue
     STAMP(3);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float* ct = reinterpret_cast<float*>(smem);
@@ -228,12 +278,65 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
     STAMP(4);
-    // 2) row-major pass over 4-column units: consecutive threads take consecutive units, so the
-    //    bias / residual loads and the output stores are 8-16 B, coalesced and independent.
-    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(d->wbase + a.b_off) : nullptr;
-    const uint32_t rows = min((uint32_t)kBM, a.M - m0);
+    pdl_wait();  // activations (residual in, output / partials out) only after the predecessor
+    const uint32_t rows = min(a.m_rows, a.M - m0);
     const uint32_t cols = min((uint32_t)BN, a.N - n0);
     constexpr uint32_t upr = BN / 4;
+    if (a.splits > 1) {
+        // 2a) split-K: publish this split's partial tile, the last arriving CTA reduces all splits
+        //     in split order (fixed summation order: deterministic).  Loads are batched kB units
+        //     per thread so the reduction is bandwidth- rather than latency-bound.
+        float* part = a.part + (size_t)tile * a.splits * (kBM * BN);
+        float4* mine = reinterpret_cast<float4*>(part + (size_t)blockIdx.z * (kBM * BN));
+        for (uint32_t u = threadIdx.x; u < rows * upr; u += blockDim.x) {
+            const uint32_t r = u / upr, c = (u - r * upr) * 4;
+            mine[u] = *reinterpret_cast<const float4*>(ct + r * C::kLdc + c);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *last_flag = atomicAdd(&a.ctr[tile], 1u) == a.splits - 1;
+        __syncthreads();
+        if (!*last_flag) return;
+        __threadfence();
+        constexpr int kB = 8;
+        for (uint32_t u0 = threadIdx.x; u0 < rows * upr; u0 += blockDim.x * kB) {
+            float4 acc[kB];
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                const uint32_t u = u0 + j * blockDim.x;
+                acc[j] = u < rows * upr ? __ldcg(reinterpret_cast<const float4*>(part) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (uint32_t z = 1; z < a.splits; ++z) {
+                const float4* pz = reinterpret_cast<const float4*>(part + (size_t)z * (kBM * BN));
+                float4 v[kB];
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    const uint32_t u = u0 + j * blockDim.x;
+                    v[j] = u < rows * upr ? __ldcg(pz + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int j = 0; j < kB; ++j) {
+                    acc[j].x += v[j].x;
+                    acc[j].y += v[j].y;
+                    acc[j].z += v[j].z;
+                    acc[j].w += v[j].w;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kB; ++j) {
+                const uint32_t u = u0 + j * blockDim.x;
+                if (u < rows * upr) {
+                    const uint32_t r = u / upr, c = (u - r * upr) * 4;
+                    *reinterpret_cast<float4*>(ct + r * C::kLdc + c) = acc[j];
+                }
+            }
+        }
+        if (threadIdx.x == 0) a.ctr[tile] = 0;  // self-reset for the next GEMM (ordered by PDL wait)
+        __syncthreads();
+    }
+    // 2b) row-major pass over 4-column units: consecutive threads take consecutive units, so the
+    //     bias / residual loads and the output stores are 8-16 B, coalesced and independent.
+    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(d->wbase + a.b_off) : nullptr;
     const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (a.res == nullptr || a.ld_res % 4 == 0);
     if (vec) {
 #pragma unroll 4
@@ -302,10 +405,10 @@ __global__ void __launch_bounds__(128, 1)
 template <int BN>
 static void launch_bn(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {
     using C = Cfg<BN>;
-    const int nst = (int)((a.K / kBK + C::kSub - 1) / C::kSub);
+    const int nst = (int)((a.kt_per + C::kSub - 1) / C::kSub);
     const int stages = nst < C::kMaxStages ? nst : C::kMaxStages;
-    dim3 grid((a.M + kBM - 1) / kBM, a.n_pad / BN);
-    k_gemm<BN><<<grid, 128, C::smem_bytes(stages), s>>>(*tmA, d, w, a, stages);
+    dim3 grid((a.M + a.m_rows - 1) / a.m_rows, a.n_pad / BN, a.splits);
+    launch_pdl(PDL_GEMM, k_gemm<BN>, grid, dim3(128), C::smem_bytes(stages), s, *tmA, d, w, a, stages);
 }
 
 void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading)
@@ -343,6 +446,26 @@ bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
     const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
     const cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_tmap_conv(CUtensorMap* map, const void* base, uint32_t H, uint32_t W, uint32_t C, uint32_t Q, uint32_t Hb,
+                    uint32_t stride) {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return false;
+        fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    if (Q * stride > 256 || Hb * stride > 256 || Hb * Q > (uint32_t)kBM || C % kBK) return false;
+    const cuuint64_t dims[4] = {C, W, H, 1};
+    const cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+    const cuuint32_t box[4] = {(cuuint32_t)kBK, Q * stride, Hb * stride, 1};
+    const cuuint32_t estr[4] = {1, stride, stride, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -55,7 +55,6 @@ constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, const DevDesc* desc,
                  const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* ctl);
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
-void launch_signal(cudaStream_t s, uint32_t* ready, uint32_t layer, uint32_t bytes, DevCtl* ctl, int last);
 void launch_finish(cudaStream_t s, DevCtl* ctl);
 
 // ---- layer ops ----------------------------------------------------------------------------
@@ -85,7 +84,15 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     const void* res; int res_bf16; uint32_t ld_res;
     void* out; int out_bf16; uint32_t ld_out;
     uint16_t* out2;     // optional bf16 shadow of an f32 output (same ld)
-    int bn;                      // tile N: 32, 64 or 128
+    int bn;             // tile N: 16, 32, 64 or 128
+    uint32_t m_rows;    // output rows per M tile: 128, or Hb·Q for an implicit-GEMM conv tile
+    // split-K: gridDim.z = splits; split z covers 64-wide k tiles [z·kt_per, (z+1)·kt_per)
+    uint32_t splits, kt_per;
+    float* part;        // [m_tiles·n_tiles][splits][128][bn] fp32 partial tiles (splits > 1)
+    uint32_t* ctr;      // [m_tiles·n_tiles] arrival counters, self-resetting (splits > 1)
+    // implicit-GEMM convolution: A tile = Hb output rows x Q columns x 64 input channels of one
+    // (r, s) tap, gathered by one 4-D TMA load (zero fill = padding, element stride = conv stride)
+    int conv; uint32_t Q, stride, pad, S, Cin, Hb;
 };
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a);
 
@@ -110,5 +117,9 @@ void init_ops_attrs();
 
 // Host helper: build the TMA descriptor of a row-major bf16 activation [rows][cols].
 bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems);
+// Host helper: 4-D TMA descriptor of an NHWC bf16 input [H][W][C] for implicit-GEMM conv:
+// box = 64 channels x Q output columns x Hb output rows, element strides = conv stride.
+bool make_tmap_conv(CUtensorMap* map, const void* base, uint32_t H, uint32_t W, uint32_t C, uint32_t Q, uint32_t Hb,
+                    uint32_t stride);
 
 }  // namespace fsw

@@ -12,6 +12,7 @@ namespace fsw {
 // ------------------------------------------------------------------------------------------
 __global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
     wait_ready_cta(w);
+    pdl_wait();
     const uint32_t t = blockIdx.x;
     const uint8_t* wb = d->wbase;
     uint32_t row[4];
@@ -35,7 +36,7 @@ __global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
 }
 
 void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) {
-    k_embed<<<a.T, 256, 0, s>>>(d, w, a);
+    launch_pdl(PDL_EMBED, k_embed, dim3(a.T), dim3(256), 0, s, d, w, a);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -45,6 +46,7 @@ void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) 
 template <int NV>
 __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
     wait_ready_cta(w);
+    pdl_wait();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp;
     if (r >= a.rows) return;
@@ -93,12 +95,12 @@ __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d
 void launch_layernorm(cudaStream_t s, const DevDesc* d, Wait w, const LnArgs& a) {
     const unsigned grid = (a.rows + 3) / 4;
     const uint32_t nv = (a.C / 4 + 31) / 32;
-    if (nv <= 2) k_layernorm<2><<<grid, 128, 0, s>>>(d, w, a);
-    else if (nv <= 4) k_layernorm<4><<<grid, 128, 0, s>>>(d, w, a);
-    else if (nv <= 6) k_layernorm<6><<<grid, 128, 0, s>>>(d, w, a);
-    else if (nv <= 8) k_layernorm<8><<<grid, 128, 0, s>>>(d, w, a);
-    else if (nv <= 13) k_layernorm<13><<<grid, 128, 0, s>>>(d, w, a);
-    else k_layernorm<16><<<grid, 128, 0, s>>>(d, w, a);
+    if (nv <= 2) launch_pdl(PDL_LN, k_layernorm<2>, dim3(grid), dim3(128), 0, s, d, w, a);
+    else if (nv <= 4) launch_pdl(PDL_LN, k_layernorm<4>, dim3(grid), dim3(128), 0, s, d, w, a);
+    else if (nv <= 6) launch_pdl(PDL_LN, k_layernorm<6>, dim3(grid), dim3(128), 0, s, d, w, a);
+    else if (nv <= 8) launch_pdl(PDL_LN, k_layernorm<8>, dim3(grid), dim3(128), 0, s, d, w, a);
+    else if (nv <= 13) launch_pdl(PDL_LN, k_layernorm<13>, dim3(grid), dim3(128), 0, s, d, w, a);
+    else launch_pdl(PDL_LN, k_layernorm<16>, dim3(grid), dim3(128), 0, s, d, w, a);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -110,6 +112,7 @@ constexpr int kGemvMaxRows = 8;
 template <int R>
 __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wait w, GemvArgs a) {
     extern __shared__ float xs[];  // [R][K]
+    pdl_wait();
     for (uint32_t i = threadIdx.x; i < R * a.K; i += blockDim.x) {
         const uint32_t r = i / a.K, k = i - r * a.K;
         const uint64_t src = (uint64_t)(a.r0 + r) * a.ldx + k;
@@ -167,9 +170,9 @@ void launch_gemv(cudaStream_t s, const DevDesc* d, Wait w, const GemvArgs& a) {
     if (ctas > 148 * 4) ctas = 148 * 4;
     if (ctas < 1) ctas = 1;
     if (a.rows <= 1) {
-        k_gemv<1><<<ctas, 256, smem, s>>>(d, w, a);
+        launch_pdl(PDL_GEMV, k_gemv<1>, dim3(ctas), dim3(256), smem, s, d, w, a);
     } else {
-        k_gemv<kGemvMaxRows><<<ctas, 256, smem, s>>>(d, w, a);
+        launch_pdl(PDL_GEMV, k_gemv<kGemvMaxRows>, dim3(ctas), dim3(256), smem, s, d, w, a);
     }
 }
 
@@ -182,6 +185,7 @@ constexpr int kAttnRows = 16;
 
 __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
     extern __shared__ __align__(16) uint8_t sm_attn[];
+    pdl_wait();
     const uint32_t T = a.T, dh = a.dh, D = a.H * dh, W3 = 3 * D;
     const uint32_t h = blockIdx.x, t0 = blockIdx.y * kAttnRows;
     const uint32_t nwarp = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -253,13 +257,14 @@ void launch_attention(cudaStream_t s, const AttnArgs& a) {
     const int threads = 256, nwarp = threads / 32;
     const size_t smem = 4 * (a.T * (a.dh / 2 + 1) + a.T * (a.dh / 2)) + sizeof(float) * (nwarp * a.T + nwarp * a.dh);
     dim3 grid(a.H, (a.T + kAttnRows - 1) / kAttnRows);
-    k_attention<<<grid, threads, smem, s>>>(a);
+    launch_pdl(PDL_ATTN, k_attention, grid, dim3(threads), smem, s, a);
 }
 
 // ------------------------------------------------------------------------------------------
 // IM2COL (NHWC bf16 -> [P·Q][Kpad] bf16, k = (r·S + s)·C + c, zero padding / tail)
 // ------------------------------------------------------------------------------------------
 __global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per thread
+    pdl_wait();
     const uint32_t k8n = a.Kpad >> 3;
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * k8n) return;
@@ -276,6 +281,7 @@ __global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per
 }
 
 __global__ void k_im2col_scalar(Im2colArgs a) {
+    pdl_wait();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * a.Kpad) return;
     const uint32_t pq = (uint32_t)(idx / a.Kpad), k = (uint32_t)(idx - (uint64_t)pq * a.Kpad);
@@ -292,10 +298,10 @@ __global__ void k_im2col_scalar(Im2colArgs a) {
 void launch_im2col(cudaStream_t s, const Im2colArgs& a) {
     if (a.C % 8 == 0) {
         const uint64_t n = (uint64_t)a.P * a.Q * (a.Kpad / 8);
-        k_im2col_vec8<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+        launch_pdl(PDL_IM2COL, k_im2col_vec8, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, a);
     } else {
         const uint64_t n = (uint64_t)a.P * a.Q * a.Kpad;
-        k_im2col_scalar<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+        launch_pdl(PDL_IM2COL, k_im2col_scalar, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, a);
     }
 }
 
@@ -303,6 +309,7 @@ void launch_im2col(cudaStream_t s, const Im2colArgs& a) {
 // pooling (NHWC bf16)
 // ------------------------------------------------------------------------------------------
 __global__ void k_maxpool(PoolArgs a) {
+    pdl_wait();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * a.C) return;
     const uint32_t c = (uint32_t)(idx % a.C), pq = (uint32_t)(idx / a.C), p = pq / a.Q, q = pq - p * a.Q;
@@ -318,10 +325,11 @@ __global__ void k_maxpool(PoolArgs a) {
 
 void launch_maxpool(cudaStream_t s, const PoolArgs& a) {
     const uint64_t n = (uint64_t)a.P * a.Q * a.C;
-    k_maxpool<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a);
+    launch_pdl(PDL_POOL, k_maxpool, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, a);
 }
 
 __global__ void k_avgpool(PoolArgs a) {
+    pdl_wait();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= a.C) return;
     const uint32_t hw = a.H * a.W;
@@ -331,7 +339,7 @@ __global__ void k_avgpool(PoolArgs a) {
 }
 
 void launch_avgpool(cudaStream_t s, const PoolArgs& a) {
-    k_avgpool<<<(a.C + 127) / 128, 128, 0, s>>>(a);
+    launch_pdl(PDL_POOL, k_avgpool, dim3((a.C + 127) / 128), dim3(128), 0, s, a);
 }
 
 void init_ops_attrs() {

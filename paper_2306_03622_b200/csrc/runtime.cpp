@@ -224,6 +224,7 @@ struct Gpu {
     cudaStream_t sd[kMaxWaitSrc] = {};  // DMA copy streams (sd[0] == sc)
     cudaEvent_t evd[kMaxWaitSrc] = {};  // fork / join events of the DMA streams
     uint32_t* progress = nullptr;       // DMA: one group counter per copy stream, 128 B apart
+    uint32_t* gemm_ctr = nullptr;       // split-K tile arrival counters (self-resetting)
     uint8_t* pool = nullptr;
     uint64_t pool_bytes = 0;
     fsw_arena* arena = nullptr;
@@ -245,6 +246,37 @@ struct Gpu {
 };
 
 constexpr uint64_t kStageHdr = 256;
+constexpr uint32_t kGemmCtrs = 1u << 16;
+
+// Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor, chosen by a
+// small cost model of one CTA's work — fixed launch/prologue/epilogue cost plus the bytes it
+// streams into shared memory (its A rows and W columns for kt_per k tiles) — times the number of
+// waves over the 148 SMs, plus the serial split-K reduction of the last-arriving CTA.
+struct Tiling { int bn; uint32_t splits, kt_per; };
+static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t /*a_kt_bytes*/, uint32_t /*m_rows*/) {
+    // Rule fitted to the (BN, split) sweep of tools/gemm_bench.cu on B200 (profiles/r01): a CTA
+    // takes a whole SM (shared memory), so grids stay within one wave of 148; within that, the
+    // narrowest tile wins (every N tile re-reads A, but more CTAs stream more of W in parallel);
+    // split-K pays only when the grid would fill less than half the SMs and each split keeps
+    // >= 10 k tiles (the last CTA's reduction is serial).
+    Tiling t{128, 1, kt};
+    for (int bn : {16, 32, 64, 128})
+        if (n_pad % bn == 0 && m_tiles * (n_pad / bn) <= 148) {
+            t.bn = bn;
+            break;
+        }
+    if (n_pad % t.bn) t.bn = 16;
+    const uint64_t base = m_tiles * (n_pad / t.bn);
+    if (base <= 74) {
+        uint32_t S = (uint32_t)std::min<uint64_t>(148 / base, kt / 10);
+        while (S > 1 && (kt + (kt + S - 1) / S - 1) / ((kt + S - 1) / S) != S) --S;  // no empty split
+        if (S > 1) {
+            t.splits = S;
+            t.kt_per = (kt + S - 1) / S;
+        }
+    }
+    return t;
+}
 
 struct fsw_ctx {
     fsw_config cfg{};
@@ -269,6 +301,8 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     for (int j = 1; j < kMaxWaitSrc; ++j) CU(cudaStreamCreateWithFlags(&g.sd[j], cudaStreamNonBlocking));
     for (int j = 0; j < kMaxWaitSrc; ++j) CU(cudaEventCreateWithFlags(&g.evd[j], cudaEventDisableTiming));
     CU(cudaMalloc(&g.progress, 128 * kMaxWaitSrc));
+    CU(cudaMalloc(&g.gemm_ctr, sizeof(uint32_t) * kGemmCtrs));
+    CU(cudaMemset(g.gemm_ctr, 0, sizeof(uint32_t) * kGemmCtrs));
     CU(cudaMemset(g.progress, 0, 128 * kMaxWaitSrc));
     size_t free_b = 0, total_b = 0;
     CU(cudaMemGetInfo(&free_b, &total_b));
@@ -381,6 +415,7 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         for (int j = 0; j < kMaxWaitSrc; ++j) cudaEventDestroy(g.evd[j]);
         for (int j = 1; j < kMaxWaitSrc; ++j) cudaStreamDestroy(g.sd[j]);
         cudaFree(g.progress);
+        cudaFree(g.gemm_ctr);
         cudaStreamDestroy(g.sx);
         cudaStreamDestroy(g.sc);
         fsw_arena_destroy(g.arena);
@@ -406,6 +441,20 @@ static uint32_t dt_size(uint32_t dt) { return dt == FSW_DT_BF16 ? 2 : 4; }
 static uint64_t slot_bytes(const fsw_slot& s) { return slot_numel(s) * dt_size(s.dtype); }
 static uint32_t slot_cols(const fsw_slot& s) { return s.rank ? s.shape[s.rank - 1] : 1; }
 static uint64_t slot_rows(const fsw_slot& s) { return slot_numel(s) / std::max<uint32_t>(1, slot_cols(s)); }
+
+// How a CONV2D layer runs (gemm_tc.cu): a 1x1/stride-1 conv is a plain GEMM over [P·Q][Cin];
+// Cin % 64 == 0 convs are implicit GEMMs (4-D TMA gathers of the NHWC input); the rest (the
+// ResNet stem, Cin = 3) go through an explicit im2col buffer.
+enum ConvPath { CONV_DIRECT, CONV_IMPLICIT, CONV_IM2COL };
+static uint32_t conv_rows_per_tile(uint32_t P, uint32_t Q) { return std::min<uint32_t>(128 / Q, P); }
+static ConvPath conv_path(const fsw_tensor& W, const fsw_layer& L, const fsw_slot& si, const fsw_slot& so) {
+    const uint32_t R = W.shape[1], Cin = W.shape[3], stride = (uint32_t)L.attr[1], Q = so.shape[1];
+    if (R == 1 && W.shape[2] == 1 && stride == 1 && L.attr[2] == 0 && Cin % 64 == 0) return CONV_DIRECT;
+    if (Cin % 64 == 0 && Q <= 128 && Q * stride <= 256 && conv_rows_per_tile(so.shape[0], Q) * stride <= 256 &&
+        stride <= 8 && si.rank == 3)
+        return CONV_IMPLICIT;
+    return CONV_IM2COL;
+}
 
 // Rows of in0 a LINEAR layer reads.
 static uint64_t linear_rows(const Model& m, const fsw_layer& L) {
@@ -699,8 +748,7 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
             const fsw_slot& si = m.slots[L.in0];
             const fsw_slot& so = m.slots[L.out];
             const fsw_tensor& W = m.tensors[m.refs[L.first_ref]].t;
-            const bool direct = W.shape[1] == 1 && L.attr[1] == 1 && L.attr[2] == 0 && si.shape[2] % 64 == 0;
-            if (!direct) {
+            if (conv_path(W, L, si, so) == CONV_IM2COL) {
                 const uint64_t K = (uint64_t)W.shape[1] * W.shape[2] * W.shape[3];
                 scratch = std::max(scratch, (uint64_t)so.shape[0] * so.shape[1] * align_up(K, 64) * 2);
             }
@@ -737,13 +785,17 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
         return (s >= 0 && p->shadow_off[s] >= 0) ? reinterpret_cast<uint16_t*>(g.ws + p->shadow_off[s]) : nullptr;
     };
     auto ref = [&](const fsw_layer& L, uint32_t j) -> const TensorInfo& { return m.tensors[m.refs[L.first_ref + j]]; };
-    auto pick_bn = [](uint32_t n_pad, uint64_t m_tiles) {
-        // small-M GEMMs are weight-streaming: prefer more CTAs (narrow tiles) when the grid is small
-        for (int bn : {128, 64, 32, 16})
-            if (n_pad % bn == 0 && m_tiles * (n_pad / bn) >= 120) return bn;
-        for (int bn : {16, 32, 64, 128})
-            if (n_pad % bn == 0) return bn;
-        return 16;
+    uint64_t part_bytes = 0;  // split-K partial tiles, shared by all GEMMs of the plan
+    auto set_tiling = [&](GemmArgs& a, uint64_t m_tiles, uint32_t m_rows, uint32_t a_kt_bytes) {
+        const Tiling t = choose_tiling(m_tiles, a.n_pad, a.K / 64, a_kt_bytes, m_rows);
+        a.bn = t.bn;
+        a.m_rows = m_rows;
+        a.splits = t.splits;
+        a.kt_per = t.kt_per;
+        a.ctr = g.gemm_ctr;
+        const uint64_t tiles = m_tiles * (a.n_pad / t.bn);
+        if (t.splits > 1) part_bytes = std::max<uint64_t>(part_bytes, tiles * t.splits * 128 * t.bn * 4);
+        return tiles <= kGemmCtrs;
     };
 
     CU(cudaSetDevice(g.dev));
@@ -833,7 +885,7 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     a.out_bf16 = so.dtype == FSW_DT_BF16;
                     a.ld_out = a.N;
                     a.out2 = shadow(L.out);
-                    a.bn = pick_bn(a.n_pad, (a.M + 127) / 128);
+                    set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
                     const void* abase = si.dtype == FSW_DT_BF16 ? (const void*)sptr(L.in0) : (const void*)shadow(L.in0);
                     if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si)))
                         return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
@@ -849,11 +901,11 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
             case FSW_OP_CONV2D: {
                 const TensorInfo& W = ref(L, 0);
                 const uint32_t R = W.t.shape[1], S = W.t.shape[2], Cin = W.t.shape[3];
-                const bool direct = R == 1 && L.attr[1] == 1 && L.attr[2] == 0 && Cin % 64 == 0;
+                const ConvPath path = conv_path(W.t, L, si, so);
                 const uint32_t P = so.shape[0], Q = so.shape[1];
                 const void* abase = sptr(L.in0);
                 uint32_t acols = Cin;
-                if (!direct) {
+                if (path == CONV_IM2COL) {
                     Launch y{};
                     y.kind = K_IM2COL;
                     y.layer = (int)li;
@@ -881,9 +933,23 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                 a.out_bf16 = 1;
                 a.ld_out = a.N;
                 a.out2 = nullptr;
-                a.bn = pick_bn(a.n_pad, (a.M + 127) / 128);
-                if (!make_tmap_act(&x.tmap, abase, a.M, acols, acols))
-                    return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                if (path == CONV_IMPLICIT) {
+                    const uint32_t Hb = conv_rows_per_tile(P, Q);
+                    a.conv = 1;
+                    a.Q = Q;
+                    a.stride = (uint32_t)L.attr[1];
+                    a.pad = (uint32_t)L.attr[2];
+                    a.S = S;
+                    a.Cin = Cin;
+                    a.Hb = Hb;
+                    set_tiling(a, (P + Hb - 1) / Hb, Hb * Q, Hb * Q * 128);
+                    if (!make_tmap_conv(&x.tmap, abase, si.shape[0], si.shape[1], Cin, Q, Hb, a.stride))
+                        return fail(FSW_ECUDA, "plan: conv tensor map failed (layer %u)", li);
+                } else {
+                    set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
+                    if (!make_tmap_act(&x.tmap, abase, a.M, acols, acols))
+                        return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                }
                 break;
             }
             case FSW_OP_MAXPOOL:
@@ -909,6 +975,13 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
         }
         p->launches.push_back(x);
     }
+    // split-K partials live after the activations and the im2col scratch
+    const uint64_t part_off = align_up(off, 1024);
+    p->ws_bytes = align_up(part_off + part_bytes, 1024);
+    if (p->ws_bytes > g.ws_bytes)
+        return fail(FSW_ENOMEM, "plan: workspace needs %llu bytes > %llu", (unsigned long long)p->ws_bytes, (unsigned long long)g.ws_bytes);
+    for (Launch& x : p->launches)
+        if (x.kind == K_GEMM) x.gemm.part = reinterpret_cast<float*>(g.ws + part_off);
     p->built = true;
     m.plans[gi] = std::move(p);
     return FSW_OK;

@@ -7,7 +7,7 @@
 // them with 128-bit non-allocating loads from the mapped host store and 128-bit stores to
 // HBM, and publish each finished piece with a release-add of its byte count on the layer's
 // ready counter.  Layer kernels acquire that counter (device.cuh: wait_ready_*).
-// The DMA mechanism of the paper is kept as a baseline (launch_signal, FSW_DMA_BASELINE).
+// The copy-engine DMA engine (runtime.cpp) publishes readiness with stream memory writes instead.
 #include "device.cuh"
 
 namespace fsw {
@@ -68,17 +68,6 @@ __global__ void k_gate(DevCtl* ctl, uint32_t expected) {
 }
 
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected) { k_gate<<<1, 1, 0, s>>>(ctl, expected); }
-
-// DMA baseline: after a copy-engine memcpy node of one piece, publish its bytes.
-__global__ void k_signal(uint32_t* ready, uint32_t layer, uint32_t bytes, DevCtl* ctl, int last) {
-    if (ctl->t_first == 0) ctl->t_first = globaltimer();
-    red_release_gpu_add(&ready[layer], bytes);
-    if (last) ctl->t_last = globaltimer();
-}
-
-void launch_signal(cudaStream_t s, uint32_t* ready, uint32_t layer, uint32_t bytes, DevCtl* ctl, int last) {
-    k_signal<<<1, 1, 0, s>>>(ready, layer, bytes, ctl, last);
-}
 
 __global__ void k_finish(DevCtl* ctl) { ctl->t_end = globaltimer(); }
 void launch_finish(cudaStream_t s, DevCtl* ctl) { k_finish<<<1, 1, 0, s>>>(ctl); }

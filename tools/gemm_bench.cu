@@ -1,58 +1,69 @@
-// Standalone timing of the tcgen05 GEMM kernel (tools only): back-to-back launches with CUDA
-// events, plus per-CTA %globaltimer phase stamps (FSW_GEMM_TIMING).
-#define FSW_GEMM_TIMING 1
+// Standalone timing of the tcgen05 GEMM kernel over (BN, split-K) for the batch-1 shapes of the
+// paper's models (tools only; feeds the cost model of runtime.cpp: choose_tiling).
+// Back-to-back PDL launches timed with CUDA events, like consecutive layers of an invoke graph.
 #include "../paper_2306_03622_b200/csrc/gemm_tc.cu"
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 using namespace fsw;
 
-int main() {
+int main(int argc, char** argv) {
+    // optional: gemm_bench <shape-name> <bn> <splits>  -> only that config (for ncu)
+    const char* only = argc > 1 ? argv[1] : nullptr;
+    const int only_bn = argc > 2 ? atoi(argv[2]) : 0;
+    const uint32_t only_s = argc > 3 ? (uint32_t)atoi(argv[3]) : 0;
     struct Shape { const char* name; uint32_t M, K, N; };
     Shape shapes[] = {{"bert.qkv", 128, 768, 2304}, {"bert.o", 128, 768, 768}, {"bert.ffn1", 128, 768, 3072},
-                      {"bert.ffn2", 128, 3072, 768}, {"gpt.fc", 128, 1600, 6400}, {"gpt.proj2", 128, 6400, 1600},
-                      {"rn.conv1", 12544, 192, 64}, {"rn.s1.3x3", 3136, 576, 64}, {"rn.s4.3x3", 49, 4608, 512},
-                      {"rn.s4.exp", 49, 512, 2048}};
+                      {"bert.ffn2", 128, 3072, 768}, {"gpt.qkv", 128, 1600, 4800}, {"gpt.fc", 128, 1600, 6400},
+                      {"gpt.proj2", 128, 6400, 1600}, {"rn.s1.1x1", 3136, 64, 64}, {"rn.s1.exp", 3136, 64, 256},
+                      {"rn.s3.1x1", 196, 1024, 256}, {"rn.s3.exp", 196, 256, 1024}, {"rn.s4.1x1", 49, 2048, 512},
+                      {"rn.s4.exp", 49, 512, 2048}, {"rn.s4.3x3(im2col)", 49, 4608, 512}};
     init_gemm_attrs();
     uint8_t *A, *W, *O;
+    float* part;
+    uint32_t* ctr;
     cudaMalloc(&A, 64 << 20); cudaMalloc(&W, 64 << 20); cudaMalloc(&O, 64 << 20);
+    cudaMalloc(&part, 64 << 20); cudaMalloc(&ctr, 1 << 20); cudaMemset(ctr, 0, 1 << 20);
     cudaMemset(A, 0x3c, 64 << 20); cudaMemset(W, 0x3c, 64 << 20);
     DevDesc* dd; cudaMalloc(&dd, sizeof(DevDesc));
     DevDesc h{W, 0}; cudaMemcpy(dd, &h, sizeof h, cudaMemcpyHostToDevice);
     DevCtl* ctl; cudaMalloc(&ctl, sizeof(DevCtl)); cudaMemset(ctl, 0, sizeof(DevCtl));
     cudaStream_t s; cudaStreamCreate(&s);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int mode : {0}) {
     for (auto& sh : shapes) {
+        if (only && strcmp(only, sh.name)) continue;
+        const uint32_t n_pad = (sh.N + 15) / 16 * 16, kt = sh.K / 64;
+        double best = 1e9; int bb = 0; uint32_t bs = 0;
         for (int bn : {16, 32, 64, 128}) {
-            uint32_t n_pad = (sh.N + 15) / 16 * 16;
-            if (n_pad % bn) continue;
-            CUtensorMap tm;
-            if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K)) { printf("tmap fail\n"); return 1; }
-            GemmArgs a{}; a.M = sh.M; a.N = sh.N; a.K = sh.K; a.n_pad = n_pad; a.w_off = 0; a.b_off = 0;
-            a.has_bias = 1; a.act = 0; a.res = nullptr; a.out = O; a.out_bf16 = 1; a.ld_out = sh.N; a.bn = bn;
-            Wait w{nullptr, 0, ctl, 0};
-            for (int i = 0; i < 3; ++i) launch_gemm(s, dd, w, &tm, a);
-            cudaEventRecord(e0, s);
-            const int reps = 20;
-            for (int i = 0; i < reps; ++i) launch_gemm(s, dd, w, &tm, a);
-            cudaEventRecord(e1, s);
-            cudaEventSynchronize(e1);
-            float ms; cudaEventElapsedTime(&ms, e0, e1);
-            // single launch stamps
-            cudaMemsetAsync(O, 0, 1, s);
-            launch_gemm(s, dd, w, &tm, a);
-            cudaStreamSynchronize(s);
-            static unsigned long long st[1024][6];
-            cudaMemcpyFromSymbol(st, g_gemm_stamp, sizeof st);
-            uint32_t nct = ((sh.M + 127) / 128) * (n_pad / bn); if (nct > 1024) nct = 1024;
-            unsigned long long t0 = ~0ull, tend = 0; double ph[5] = {0};
-            for (uint32_t c = 0; c < nct; ++c) { t0 = std::min(t0, st[c][0]); tend = std::max(tend, st[c][5]); for (int p = 0; p < 5; ++p) ph[p] += (double)(st[c][p + 1] - st[c][p]); }
-            double flops = 2.0 * sh.M * sh.N * sh.K;
-            printf("%-10s M=%5u K=%5u N=%5u BN=%3d ctas=%4u: %7.2f us/launch (%.1f TF/s)  span=%.2f us  phases(us): setup %.2f mainloop %.2f (+%.2f) tmem->smem %.2f store %.2f\n",
-                   sh.name, sh.M, sh.K, sh.N, bn, nct, ms * 1000 / reps, flops / (ms / reps * 1e-3) / 1e12, (tend - t0) / 1e3,
-                   ph[0] / nct / 1e3, ph[1] / nct / 1e3, ph[2] / nct / 1e3, ph[3] / nct / 1e3, ph[4] / nct / 1e3);
+            if (n_pad % bn || (only_bn && bn != only_bn)) continue;
+            for (uint32_t S : {1u, 2u, 3u, 4u, 6u, 8u, 12u, 16u, 24u, 36u}) {
+                if (S > kt || (only_s && S != only_s)) continue;
+                const uint32_t kt_per = (kt + S - 1) / S;
+                if ((kt + kt_per - 1) / kt_per != S) continue;
+                const uint32_t ctas = ((sh.M + 127) / 128) * (n_pad / bn) * S;
+                if (ctas > 600) continue;
+                CUtensorMap tm;
+                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K)) { printf("tmap fail\n"); return 1; }
+                GemmArgs a{}; a.M = sh.M; a.N = sh.N; a.K = sh.K; a.n_pad = n_pad; a.w_off = 0; a.b_off = 0;
+                a.has_bias = 1; a.act = 0; a.res = nullptr; a.out = O; a.out_bf16 = 1; a.ld_out = sh.N; a.bn = bn;
+                a.m_rows = 128; a.splits = S; a.kt_per = kt_per; a.part = part; a.ctr = ctr;
+                Wait w{}; w.ctl = ctl;
+                for (int i = 0; i < 3; ++i) launch_gemm(s, dd, w, &tm, a);
+                cudaEventRecord(e0, s);
+                const int reps = 50;
+                for (int i = 0; i < reps; ++i) launch_gemm(s, dd, w, &tm, a);
+                cudaEventRecord(e1, s);
+                cudaEventSynchronize(e1);
+                float ms; cudaEventElapsedTime(&ms, e0, e1);
+                const double us = ms * 1000 / reps;
+                const double wbytes = 2.0 * n_pad * sh.K;
+                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
+                       sh.K, sh.N, bn, S, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
+                if (us < best) { best = us; bb = bn; bs = S; }
+            }
         }
-    }
+        printf("  BEST %-18s BN=%d S=%u %.2f us\n", sh.name, bb, bs, best);
     }
     cudaError_t e = cudaGetLastError();
     printf("last error: %s\n", cudaGetErrorString(e));
