@@ -57,6 +57,7 @@ typedef enum {
                                  groups, one copy stream; overrides the
                                  engine / group / stream settings                                */
 #define FSW_HOST_WC      0x4u /* back host stores with write-combined pinned pages            */
+#define FSW_NO_PEER_SWAP 0x10u /* never swap from another GPU's resident copy (Alg. 1 case 2 off)  */
 #define FSW_HOST_ONLY    0x8u /* no GPU: registration / host-store / allocator logic only (tests);
                                  invoke returns FSW_ECUDA                                       */
 
@@ -71,7 +72,9 @@ typedef struct {
     uint64_t chunk_bytes;             /* swap piece size (the paper's "group size",
                                          PAPER.md:600-604) of the SM engine; multiple of 256;
                                          0 = 16 KiB (small pieces keep the swap in layer order) */
-    uint64_t stripe_min_bytes;        /* reserved for striped swap; 0 = 256 MiB               */
+    uint64_t stripe_min_bytes;        /* policy: stripe a cold host swap over every pool GPU with
+                                         peer access to the target when the store has at least
+                                         this many bytes; 0 = 256 MiB; UINT64_MAX = never         */
     uint32_t flags;                   /* FSW_NO_OVERLAP | FSW_DMA_BASELINE | FSW_HOST_WC       */
     uint32_t engine;                  /* FSW_ENGINE_*; 0 = AUTO                                */
     uint64_t dma_min_bytes;           /* AUTO picks DMA for models with at least this many store
@@ -202,7 +205,8 @@ fsw_status fsw_invoke(fsw_ctx* ctx, uint32_t model_id, const void* input, uint64
 enum { FSW_ORDER_EXEC = 0, FSW_ORDER_REVERSE = 1, FSW_ORDER_RANDOM = 2 };
 typedef struct {
     int32_t gpu;          /* −1 = scheduler's choice                                           */
-    uint32_t stripe_mask; /* reserved (striped swap)                                           */
+    uint32_t n_stripe_src;/* striped swap: 0 = ctx policy (stripe_min_bytes);
+                             else the number of entries of stripe_src                          */
     uint64_t chunk_bytes; /* 0 = ctx default                                                   */
     uint32_t order;       /* FSW_ORDER_* : order in which swap pieces are claimed (tests)      */
     uint32_t order_seed;
@@ -211,6 +215,18 @@ typedef struct {
     uint32_t engine;      /* FSW_ENGINE_*; 0 = ctx default                                     */
     uint64_t dma_group_bytes; /* 0 = ctx default                                               */
     uint32_t dma_streams;     /* 0 = ctx default                                               */
+    const int32_t* stripe_src; /* n_stripe_src pool GPU indices that each load a round-robin share of
+                             every layer's pieces from the host store over their own host link and
+                             store it into the target's extent (peer stores over NVLink for remote
+                             sources).  Duplicates are allowed: every entry runs its own swap kernel
+                             (single-GPU tests list the target several times).  A single entry equal
+                             to the target means "no striping".  ETOPO if a source has no peer
+                             access to the target.                                             */
+    uint32_t peer_src;    /* GPU->GPU swap (Alg. 1 case 2): 0 = policy (a cold
+                             invoke copies from another pool GPU that holds the model, over
+                             NVLink, before falling back to the host link; FSW_NO_PEER_SWAP turns
+                             it off); k > 0 = copy from pool GPU k-1 (ESTATE if not resident there,
+                             ETOPO without peer access)                                        */
 } fsw_invoke_opts;
 fsw_status fsw_invoke_ex(fsw_ctx* ctx, uint32_t model_id, const fsw_invoke_opts* opts,
                          const void* input, uint64_t input_bytes, void* output, uint64_t output_cap,

@@ -20,6 +20,16 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
     return v;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -43,11 +53,12 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
 // CTA barrier.  The acquire pairs with the swap kernel's red.release; the barrier extends
 // the ordering to the rest of the CTA.  A watchdog turns a lost release into an error word.
 __device__ __forceinline__ void wait_ready_thread(const Wait& w) {
+    auto load = [&](const uint32_t* p) { return w.sys ? ld_acquire_sys(p) : ld_acquire_gpu(p); };
     for (uint32_t j = 0; j < w.n; ++j) {
-        if (ld_acquire_gpu(w.ready[j]) >= w.target[j]) continue;
+        if (load(w.ready[j]) >= w.target[j]) continue;
         const uint64_t t0 = globaltimer();
         uint32_t ns = 64;
-        while (ld_acquire_gpu(w.ready[j]) < w.target[j]) {
+        while (load(w.ready[j]) < w.target[j]) {
             __nanosleep(ns);
             if (ns < 1024) ns <<= 1;
             if (globaltimer() - t0 > kWatchdogNs) {

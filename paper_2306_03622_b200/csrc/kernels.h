@@ -45,6 +45,7 @@ struct Wait {
     const uint32_t* ready[kMaxWaitSrc];
     uint32_t target[kMaxWaitSrc];
     uint32_t n;  // 0 = no wait (warm invoke / no weights)
+    uint32_t sys;  // 1: counters are bumped by other GPUs (striped swap) -> system-scope acquire
     DevCtl* ctl;
     int32_t layer;
 };
@@ -52,8 +53,12 @@ struct Wait {
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 // ---- swap ---------------------------------------------------------------------------------
-void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, const DevDesc* desc,
-                 const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* ctl);
+// SM swap engine.  dst = the target extent (nullptr: desc->wbase of this GPU's invoke); ready =
+// the target's per-layer counters; own = this launch's ticket / stamps; gate = the target's
+// control block whose `started` the target's gate kernel watches; sys = 1 when the target is
+// another GPU (peer stores over NVLink, system-scope release).
+void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, uint8_t* dst, const DevDesc* desc,
+                 const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys);
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
 void launch_finish(cudaStream_t s, DevCtl* ctl);
 

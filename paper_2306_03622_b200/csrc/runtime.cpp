@@ -195,6 +195,8 @@ struct Plan {  // one model on one GPU
     std::map<GraphKey, cudaGraphExec_t> graphs;
     std::map<std::tuple<uint64_t, int, uint32_t>, PieceSet> pieces;  // (chunk, order, seed)
     std::map<std::pair<uint64_t, uint32_t>, DmaPlan> dma;            // (group bytes, streams)
+    // striped swap: source j of n gets every n-th piece; its table lives on the source's device
+    std::map<std::tuple<uint64_t, uint32_t, uint32_t, int>, PieceSet> stripe;  // (chunk, n, j, device)
 };
 
 struct Model {
@@ -218,8 +220,19 @@ struct Model {
     int inflight = 0;
 };
 
+// A swap-kernel slot of a GPU acting as a striped-swap source for some target (its own ticket
+// counter, stream and completion event).  A GPU can feed several targets' swaps at once.
+struct SrcSlot {
+    DevCtl* ctl = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t done = nullptr;
+    bool busy = false;
+};
+constexpr int kSrcSlots = 4;
+
 struct Gpu {
     int dev = 0;
+    SrcSlot src[kSrcSlots];
     cudaStream_t sx = nullptr, sc = nullptr;
     cudaStream_t sd[kMaxWaitSrc] = {};  // DMA copy streams (sd[0] == sc)
     cudaEvent_t evd[kMaxWaitSrc] = {};  // fork / join events of the DMA streams
@@ -248,10 +261,7 @@ struct Gpu {
 constexpr uint64_t kStageHdr = 256;
 constexpr uint32_t kGemmCtrs = 1u << 16;
 
-// Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor, chosen by a
-// small cost model of one CTA's work — fixed launch/prologue/epilogue cost plus the bytes it
-// streams into shared memory (its A rows and W columns for kt_per k tiles) — times the number of
-// waves over the 148 SMs, plus the serial split-K reduction of the last-arriving CTA.
+// Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor.
 struct Tiling { int bn; uint32_t splits, kt_per; };
 static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t /*a_kt_bytes*/, uint32_t /*m_rows*/) {
     // Rule fitted to the (BN, split) sweep of tools/gemm_bench.cu on B200 (profiles/r01): a CTA
@@ -285,6 +295,7 @@ struct fsw_ctx {
     std::mutex mu;
     std::condition_variable cv;
     uint64_t clock = 0;
+    std::vector<std::vector<char>> peer;  // peer[i][j]: GPU i can store into GPU j's memory
 };
 
 // ==========================================================================================
@@ -302,6 +313,11 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     for (int j = 0; j < kMaxWaitSrc; ++j) CU(cudaEventCreateWithFlags(&g.evd[j], cudaEventDisableTiming));
     CU(cudaMalloc(&g.progress, 128 * kMaxWaitSrc));
     CU(cudaMalloc(&g.gemm_ctr, sizeof(uint32_t) * kGemmCtrs));
+    for (SrcSlot& sl : g.src) {
+        CU(cudaMalloc(&sl.ctl, sizeof(DevCtl)));
+        CU(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
     CU(cudaMemset(g.gemm_ctr, 0, sizeof(uint32_t) * kGemmCtrs));
     CU(cudaMemset(g.progress, 0, 128 * kMaxWaitSrc));
     size_t free_b = 0, total_b = 0;
@@ -367,6 +383,24 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
         fsw_status s = init_gpu(c.get(), c->gpus[i]);
         if (s != FSW_OK) return s;
     }
+    // NVLink peer access between the pool's GPUs (striped swap stores into a peer's extent)
+    c->peer.assign(n, std::vector<char>(n, 0));
+    for (uint32_t i = 0; i < n; ++i)
+        for (uint32_t j = 0; j < n; ++j) {
+            if (c->gpus[i].dev == c->gpus[j].dev) {
+                c->peer[i][j] = 1;
+                continue;
+            }
+            int ok = 0;
+            cudaDeviceCanAccessPeer(&ok, c->gpus[i].dev, c->gpus[j].dev);
+            if (ok) {
+                CU(cudaSetDevice(c->gpus[i].dev));
+                cudaError_t e = cudaDeviceEnablePeerAccess(c->gpus[j].dev, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (e != cudaSuccess) ok = 0;
+            }
+            c->peer[i][j] = (char)ok;
+        }
     c->cfg.gpu_ids = nullptr;
     *out = c.release();
     return FSW_OK;
@@ -378,6 +412,8 @@ static void free_plan(Gpu& g, Plan& p) {
     p.graphs.clear();
     for (auto& kv : p.pieces) cudaFree(kv.second.dev);
     p.pieces.clear();
+    for (auto& kv : p.stripe) cudaFree(kv.second.dev);  // UVA: any current device
+    p.stripe.clear();
 }
 
 static void free_store(Model& m, bool host_only) {
@@ -416,6 +452,11 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         for (int j = 1; j < kMaxWaitSrc; ++j) cudaStreamDestroy(g.sd[j]);
         cudaFree(g.progress);
         cudaFree(g.gemm_ctr);
+        for (SrcSlot& sl : g.src) {
+            cudaFree(sl.ctl);
+            cudaStreamDestroy(sl.st);
+            cudaEventDestroy(sl.done);
+        }
         cudaStreamDestroy(g.sx);
         cudaStreamDestroy(g.sc);
         fsw_arena_destroy(g.arena);
@@ -1100,7 +1141,34 @@ struct InvokeCfg {
     uint32_t seed, ctas;
     uint8_t* wbase;              // only used by DMA graphs (memcpy nodes need absolute addresses)
     const DmaPlan* dma_plan;     // DMA engine only
+    const uint8_t* src = nullptr; // DMA: copy source (host store, or a peer GPU's extent)
+    bool striped = false;        // striped swap: sources launched outside the graph (fsw_invoke_ex)
+    uint32_t local_ctas = 0;     // striped: swap CTAs running on the target GPU itself (gate)
 };
+
+// Striped swap: the execution-order piece list of the SM engine dealt round-robin to n sources
+// (piece q goes to source q mod n), so every source streams a share of every layer and all of them
+// advance through the model together; source j's table is allocated on source j's device.
+static fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, PieceSet** out) {
+    const auto key = std::make_tuple(chunk, n, j, dev);
+    auto it = p.stripe.find(key);
+    if (it != p.stripe.end()) {
+        *out = &it->second;
+        return FSW_OK;
+    }
+    PieceSet ps;
+    uint64_t q = 0;
+    for (uint32_t li = 0; li < m.layers.size(); ++li)
+        for (uint64_t o = 0; o < m.region_bytes[li]; o += chunk, ++q)
+            if (q % n == j) ps.host.push_back({m.region_off[li] + o, (uint32_t)std::min<uint64_t>(chunk, m.region_bytes[li] - o), li});
+    CU(cudaSetDevice(dev));
+    if (!ps.host.empty()) {
+        CU(cudaMalloc(&ps.dev, sizeof(Piece) * ps.host.size()));
+        CU(cudaMemcpy(ps.dev, ps.host.data(), sizeof(Piece) * ps.host.size(), cudaMemcpyHostToDevice));
+    }
+    *out = &p.stripe.emplace(key, std::move(ps)).first->second;
+    return FSW_OK;
+}
 
 static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaStream_t s) {
     const DevDesc* d = reinterpret_cast<const DevDesc*>(g.dstage);
@@ -1113,6 +1181,7 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
                 w.n = 1;
                 w.ready[0] = g.ready + x.layer;
                 w.target[0] = (uint32_t)m.region_bytes[x.layer];
+                w.sys = ic.striped ? 1 : 0;
             } else {
                 w.n = ic.dma_plan->streams;
                 for (uint32_t j = 0; j < w.n; ++j) {
@@ -1147,7 +1216,7 @@ static PFN_writeValue32 get_write_value32() {
 // timing) and the gate; then the flag-gated layer kernels; then D2H of output and ctl.
 static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out) {
     PieceSet* ps = nullptr;
-    if (ic.cold && ic.engine == FSW_ENGINE_SM) {
+    if (ic.cold && ic.engine == FSW_ENGINE_SM && !ic.striped) {
         fsw_status s = get_pieces(m, p, g, ic.chunk, ic.order, ic.seed, &ps);
         if (s != FSW_OK) return s;
         if (m.layers.size() > g.ready_cap) return fail(FSW_EINVAL, "too many layers");
@@ -1156,16 +1225,18 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
     cudaStream_t sx = g.sx, sc = g.sc;
     CU(cudaStreamBeginCapture(sx, cudaStreamCaptureModeThreadLocal));
     cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr + m.input_bytes, cudaMemcpyHostToDevice, sx);
-    cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
-    if (ic.cold) {
+    // striped: the counters and the control block are reset before the sources start (outside)
+    if (!ic.striped) cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
+    if (ic.cold && ic.striped && !ic.no_overlap && ic.local_ctas) launch_gate(sx, g.ctl, ic.local_ctas);
+    if (ic.cold && !ic.striped) {
         if (ic.engine == FSW_ENGINE_SM) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
         else cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
         cudaEventRecord(g.evfork, sx);
         cudaStreamWaitEvent(sc, g.evfork, 0);
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
         if (ic.engine == FSW_ENGINE_SM) {
-            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, reinterpret_cast<const DevDesc*>(g.dstage),
-                        ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl);
+            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, nullptr, reinterpret_cast<const DevDesc*>(g.dstage),
+                        ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl, g.ctl, 0);
         } else {
             // Copy-engine DMA from the pinned store (the paper's transfer) in
             // layer-aligned groups (its "group" pipelining unit), dealt round-robin
@@ -1180,7 +1251,7 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
             uint32_t cnt[kMaxWaitSrc] = {};
             for (const auto& gr : dp.groups) {
                 cudaStream_t sj = g.sd[gr.stream];
-                cudaMemcpyAsync(ic.wbase + gr.lo, m.store + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sj);
+                cudaMemcpyAsync(ic.wbase + gr.lo, ic.src + gr.lo, gr.hi - gr.lo, cudaMemcpyDefault, sj);
                 wv(sj, (CUdeviceptr)(g.progress + 32 * gr.stream), (cuuint32_t)(++cnt[gr.stream]), 0);
             }
             for (uint32_t j = 1; j < dp.streams; ++j) {
@@ -1195,7 +1266,7 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
     }
     enqueue_layers(m, p, g, ic, sx);
     launch_finish(sx, g.ctl);
-    if (ic.cold && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
+    if (ic.cold && !ic.striped && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
     cudaMemcpyAsync(g.hout, g.ws + p.slot_off[m.output_slot], m.output_bytes, cudaMemcpyDeviceToHost, sx);
     cudaMemcpyAsync(g.hctl, g.ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, sx);
     cudaGraph_t graph = nullptr;
@@ -1317,6 +1388,9 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     Model* m = nullptr;
     int gi = -1;
     bool cold = false;
+    std::vector<int> srcs;          // striped swap sources (pool GPU indices), empty = not striped
+    int peer = -1;                  // GPU->GPU swap source (pool GPU index), -1 = from the host
+    std::vector<SrcSlot*> slots;    // their swap-kernel slots
     {
         std::unique_lock<std::mutex> lk(c->mu);
         m = find_model(c, id);
@@ -1343,12 +1417,70 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             }
         }
         m->last_use[gi] = ++c->clock;
+        fsw_status ss = FSW_OK;
+        // GPU->GPU swap from a resident copy (Alg. 1 case 2): explicit, or policy
+        if (cold && o.peer_src) {
+            const int s = (int)o.peer_src - 1;
+            if (s < 0 || s >= (int)c->gpus.size() || s == gi) ss = fail(FSW_EINVAL, "invoke: bad peer_src %d", s);
+            else if (m->extent[s] < 0) ss = fail(FSW_ESTATE, "invoke: model %u is not resident on gpu %d", id, s);
+            else if (!c->peer[gi][s]) ss = fail(FSW_ETOPO, "invoke: gpu %d cannot read gpu %d", gi, s);
+            else peer = s;
+        } else if (cold && !o.n_stripe_src && !((o.flags | c->cfg.flags) & FSW_NO_PEER_SWAP)) {
+            for (int s = 0; s < (int)c->gpus.size() && peer < 0; ++s)
+                if (s != gi && m->extent[s] >= 0 && c->peer[gi][s]) peer = s;
+        }
+        // striped swap: explicit sources, or the ctx policy for large stores
+        if (ss != FSW_OK || peer >= 0) {
+        } else if (cold && o.n_stripe_src) {
+            if (!o.stripe_src || o.n_stripe_src > 16) ss = fail(FSW_EINVAL, "invoke: stripe_src");
+            for (uint32_t j = 0; ss == FSW_OK && j < o.n_stripe_src; ++j) {
+                const int sgi = o.stripe_src[j];
+                if (sgi < 0 || sgi >= (int)c->gpus.size()) ss = fail(FSW_EINVAL, "invoke: stripe source %d", sgi);
+                else if (!c->peer[sgi][gi]) ss = fail(FSW_ETOPO, "invoke: gpu %d cannot store into gpu %d", sgi, gi);
+                else srcs.push_back(sgi);
+            }
+        } else if (cold && c->gpus.size() > 1 && m->store_bytes >= c->cfg.stripe_min_bytes) {
+            srcs.push_back(gi);
+            for (int i = 0; i < (int)c->gpus.size(); ++i)
+                if (i != gi && c->peer[i][gi]) srcs.push_back(i);
+        }
+        if (srcs.size() == 1 && srcs[0] == gi) srcs.clear();
+        for (size_t j = 0; ss == FSW_OK && j < srcs.size(); ++j) {
+            SrcSlot* free_slot = nullptr;
+            for (SrcSlot& sl : c->gpus[srcs[j]].src)
+                if (!sl.busy) {
+                    free_slot = &sl;
+                    break;
+                }
+            if (!free_slot) {
+                if (o.n_stripe_src) ss = fail(FSW_EBUSY, "invoke: no free swap slot on gpu %d", srcs[j]);
+                else srcs.erase(srcs.begin() + j--);  // policy: that link is busy feeding other swaps
+                continue;
+            }
+            free_slot->busy = true;
+            slots.push_back(free_slot);
+        }
+        if (srcs.size() == 1 && srcs[0] == gi) {
+            slots[0]->busy = false;
+            srcs.clear();
+            slots.clear();
+        }
+        if (ss != FSW_OK) {
+            for (SrcSlot* sl : slots) sl->busy = false;
+            if (cold) invalidate(c, *m, gi);
+            g.busy = false;
+            m->inflight--;
+            c->cv.notify_all();
+            return ss;
+        }
     }
     Gpu& g = c->gpus[gi];
+    const bool striped = !srcs.empty();
     fsw_status st = FSW_OK;
     auto finish = [&](fsw_status s) {
         std::lock_guard<std::mutex> lk(c->mu);
         if (s != FSW_OK && cold) invalidate(c, *m, gi);  // failed swap: extent is not valid
+        for (SrcSlot* sl : slots) sl->busy = false;
         g.busy = false;
         m->inflight--;
         c->cv.notify_all();
@@ -1365,6 +1497,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     int engine = (int)(o.engine ? o.engine : c->cfg.engine);
     if (baseline) engine = FSW_ENGINE_DMA;
     if (engine == FSW_ENGINE_AUTO) engine = m->store_bytes >= c->cfg.dma_min_bytes ? FSW_ENGINE_DMA : FSW_ENGINE_SM;
+    if (striped) engine = FSW_ENGINE_SM;  // sources store into the target with SM kernels
+    if (peer >= 0) engine = FSW_ENGINE_DMA;  // NVLink copy-engine transfer from the peer's extent
     const uint64_t dgrp = baseline ? (2ull << 20) : o.dma_group_bytes ? o.dma_group_bytes : c->cfg.dma_group_bytes;
     const uint32_t dstr = baseline ? 1u : o.dma_streams ? o.dma_streams : c->cfg.dma_streams;
     if (engine > FSW_ENGINE_DMA || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
@@ -1374,10 +1508,30 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                  o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, g.pool + (m->extent[gi] >= 0 ? m->extent[gi] : 0), nullptr};
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
     if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr);
+    ic.src = peer >= 0 ? c->gpus[peer].pool + m->extent[peer] : m->store;
     const bool sm = engine == FSW_ENGINE_SM;
-    GraphKey key{cold, (int)(flags & FSW_NO_OVERLAP), cold && sm ? ic.order : 0, cold ? engine : 0,
-                 cold ? (sm ? ic.chunk : dgrp) : 0, cold && sm ? ic.seed : 0, cold ? (sm ? ic.ctas : dstr) : 0, 0};
-    if (cold && !sm) key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);  // DMA graphs bake addresses
+    // striped: every source claims pieces of >= 256 KiB (one system-scope fence + release each)
+    const uint64_t schunk = std::max<uint64_t>(ic.chunk, 256ull << 10);
+    std::vector<PieceSet*> sps(srcs.size(), nullptr);
+    for (size_t j = 0; j < srcs.size(); ++j) {
+        st = get_stripe_pieces(*m, p, schunk, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, &sps[j]);
+        if (st != FSW_OK) return finish(st);
+    }
+    if (striped) {
+        cudaSetDevice(g.dev);
+        ic.striped = true;
+        ic.local_ctas = ic.ctas * (uint32_t)srcs.size();  // the gate waits for every source kernel
+    }
+    GraphKey key{cold, (int)(flags & FSW_NO_OVERLAP), cold && sm && !striped ? ic.order : 0, cold ? engine + (striped ? 8 : 0) : 0,
+                 cold && !striped ? (sm ? ic.chunk : dgrp) : 0, cold && sm && !striped ? ic.seed : 0,
+                 cold ? (striped ? ic.local_ctas : sm ? ic.ctas : dstr) : 0, 0};
+    if (cold && !sm) {  // DMA graphs bake addresses: the target extent and a peer source's extent
+        key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);
+        if (peer >= 0) {
+            key.order = peer + 1;
+            key.seed = (uint32_t)((uint64_t)m->extent[peer] >> 16);
+        }
+    }
     auto it = p.graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (it == p.graphs.end()) {
@@ -1392,7 +1546,36 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     memcpy(g.hstage, &dd, sizeof dd);
     memcpy(g.hstage + kStageHdr, input, input_bytes);
     cudaEventRecord(g.ev0, g.sx);
-    cudaError_t e = cudaGraphLaunch(exec, g.sx);
+    cudaError_t e = cudaSuccess;
+    if (striped) {
+        // Reset the target's counters, then every source loads its share of the pieces over its own
+        // host link and stores it into the target's extent (peer stores over NVLink for remote
+        // sources), releasing each piece on the target's layer counter at system scope.
+        uint8_t* ext = g.pool + m->extent[gi];
+        cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m->layers.size(), g.sx);
+        cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), g.sx);
+        cudaEventRecord(g.evs0, g.sx);
+        cudaEventRecord(g.evfork, g.sx);
+        for (size_t j = 0; j < srcs.size(); ++j) {
+            Gpu& sg = c->gpus[srcs[j]];
+            SrcSlot& sl = *slots[j];
+            cudaSetDevice(sg.dev);
+            cudaStreamWaitEvent(sl.st, g.evfork, 0);
+            cudaMemsetAsync(sl.ctl, 0, sizeof(DevCtl), sl.st);
+            // an empty share still starts its CTAs: the target's gate counts every source kernel
+            launch_swap(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->store, ext, nullptr, sps[j]->dev,
+                        (uint32_t)sps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1);
+            cudaEventRecord(sl.done, sl.st);
+        }
+        cudaSetDevice(g.dev);
+        for (size_t j = 0; j < srcs.size(); ++j) cudaStreamWaitEvent(g.sc, slots[j]->done, 0);
+        cudaEventRecord(g.evs1, g.sc);
+        if (ic.no_overlap) cudaStreamWaitEvent(g.sx, g.evs1, 0);
+        e = cudaGraphLaunch(exec, g.sx);
+        cudaStreamWaitEvent(g.sx, g.evs1, 0);
+    } else {
+        e = cudaGraphLaunch(exec, g.sx);
+    }
     cudaEventRecord(g.ev1, g.sx);
     if (e == cudaSuccess) e = cudaEventSynchronize(g.ev1);
     if (e != cudaSuccess) return finish(fail(FSW_ECUDA, "invoke: graph launch/sync: %s", cudaGetErrorString(e)));
@@ -1408,8 +1591,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         cudaEventElapsedTime(&ms, g.ev0, g.ev1);
         stats->device_ms = ms;
         stats->gpu = gi;
-        stats->n_sources = cold ? 1 : 0;
-        stats->swap_kind = cold ? FSW_SWAP_HOST : FSW_SWAP_RESIDENT;
+        stats->n_sources = cold ? (striped ? (uint32_t)srcs.size() : 1) : 0;
+        stats->swap_kind = cold ? (striped ? FSW_SWAP_STRIPED : peer >= 0 ? FSW_SWAP_PEER : FSW_SWAP_HOST) : FSW_SWAP_RESIDENT;
         stats->n_kernels = (uint32_t)p.launches.size() + 1 /*finish*/;
         if (cold) {
             float swap_ms = 0;
@@ -1418,7 +1601,14 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             stats->bytes_swapped = m->store_bytes;
             stats->link_gbps = swap_ms > 0 ? m->store_bytes / (swap_ms * 1e6) : 0;
             stats->engine = (uint32_t)engine;
-            if (sm) {
+            if (striped) {
+                float tail = 0;
+                cudaEventElapsedTime(&tail, g.evs1, g.ev1);
+                stats->swap_span_ms = swap_ms;
+                stats->compute_tail_ms = tail > 0 ? tail : 0;
+                stats->n_kernels += (uint32_t)srcs.size() + (ic.no_overlap ? 0 : 1);  // sources (+ gate)
+                for (PieceSet* ps : sps) stats->n_copies += (uint32_t)ps->host.size();
+            } else if (sm) {
                 if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
                 if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
                 stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)

@@ -13,21 +13,21 @@
 namespace fsw {
 
 template <int U>
-__global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, const DevDesc* __restrict__ desc,
+__global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, uint8_t* dst, const DevDesc* __restrict__ desc,
                                               const Piece* __restrict__ pieces, uint32_t n_pieces,
-                                              uint32_t* __restrict__ ready, DevCtl* __restrict__ ctl) {
-    if (threadIdx.x == 0) atomicAdd(&ctl->started, 1u);
-    uint8_t* const wbase = desc->wbase;
+                                              uint32_t* __restrict__ ready, DevCtl* __restrict__ own, DevCtl* gate, int sys) {
+    if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
+    uint8_t* const wbase = dst ? dst : desc->wbase;
     const uint32_t lane = threadIdx.x & 31u;
     for (;;) {
         uint32_t p = 0;
-        if (lane == 0) p = atomicAdd(&ctl->ticket, 1u);
+        if (lane == 0) p = atomicAdd(&own->ticket, 1u);
         p = __shfl_sync(0xffffffffu, p, 0);
         if (p >= n_pieces) break;
-        if (p == 0 && lane == 0) ctl->t_first = globaltimer();
+        if (p == 0 && lane == 0) own->t_first = globaltimer();
         const Piece pc = pieces[p];
         const uint4* src = reinterpret_cast<const uint4*>(host + pc.off);
-        uint4* dst = reinterpret_cast<uint4*>(wbase + pc.off);
+        uint4* out = reinterpret_cast<uint4*>(wbase + pc.off);
         const uint32_t n16 = pc.bytes >> 4;
         uint32_t i = lane;
         for (; i + (U - 1) * 32 < n16; i += U * 32) {
@@ -35,21 +35,26 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
 #pragma unroll
             for (int u = 0; u < U; ++u) v[u] = ld_stream_v4(src + i + u * 32);
 #pragma unroll
-            for (int u = 0; u < U; ++u) st_v4(dst + i + u * 32, v[u]);
+            for (int u = 0; u < U; ++u) st_v4(out + i + u * 32, v[u]);
         }
-        for (; i < n16; i += 32) st_v4(dst + i, ld_stream_v4(src + i));
-        __threadfence();  // this lane's stores performed at gpu scope
-        __syncwarp();
-        if (lane == 0) {
-            red_release_gpu_add(&ready[pc.layer], pc.bytes);
-            atomicMax(&ctl->t_last, (unsigned long long)globaltimer());
+        for (; i < n16; i += 32) st_v4(out + i, ld_stream_v4(src + i));
+        if (sys) {
+            // peer stores over NVLink: order them at system scope before the remote release
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) red_release_sys_add(&ready[pc.layer], pc.bytes);
+        } else {
+            __threadfence();  // this lane's stores performed at gpu scope
+            __syncwarp();
+            if (lane == 0) red_release_gpu_add(&ready[pc.layer], pc.bytes);
         }
+        if (lane == 0) atomicMax(&own->t_last, (unsigned long long)globaltimer());
     }
 }
 
-void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, const DevDesc* desc,
-                 const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* ctl) {
-    k_swap<8><<<ctas, threads, 0, s>>>(host_mapped, desc, pieces, n_pieces, ready, ctl);
+void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, uint8_t* dst, const DevDesc* desc,
+                 const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys) {
+    k_swap<8><<<ctas, threads, 0, s>>>(host_mapped, dst, desc, pieces, n_pieces, ready, own, gate, sys);
 }
 
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libfsw.so")
 
 OK, EINVAL, ENOTFOUND, ENOMEM, EBUSY, ESTATE, ECUDA, ETIMEOUT, ETOPO = range(9)
 STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA", "ETIMEOUT", "ETOPO"]
-NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY = 0x1, 0x2, 0x4, 0x8
+NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP = 0x1, 0x2, 0x4, 0x8, 0x10
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
 ENGINE_AUTO, ENGINE_SM, ENGINE_DMA = 0, 1, 2
@@ -81,8 +81,9 @@ class InvokeStats(ctypes.Structure):
 
 
 class InvokeOpts(ctypes.Structure):
-    _fields_ = [("gpu", i32), ("stripe_mask", u32), ("chunk_bytes", u64), ("order", u32), ("order_seed", u32),
-                ("copy_ctas", u32), ("flags", u32), ("engine", u32), ("dma_group_bytes", u64), ("dma_streams", u32)]
+    _fields_ = [("gpu", i32), ("n_stripe_src", u32), ("chunk_bytes", u64), ("order", u32), ("order_seed", u32),
+                ("copy_ctas", u32), ("flags", u32), ("engine", u32), ("dma_group_bytes", u64), ("dma_streams", u32),
+                ("stripe_src", ctypes.POINTER(i32)), ("peer_src", u32)]
 
 
 class PoolStats(ctypes.Structure):
@@ -188,7 +189,7 @@ class Runtime:
     def __init__(self, n_gpus: int = 0, gpu_ids: Optional[Sequence[int]] = None, pool_bytes: int = 0,
                  workspace_bytes: int = 0, copy_ctas: int = 0, copy_threads: int = 0, chunk_bytes: int = 0,
                  flags: int = 0, engine: int = ENGINE_AUTO, dma_min_bytes: int = 0, dma_group_bytes: int = 0,
-                 dma_streams: int = 0):
+                 dma_streams: int = 0, stripe_min_bytes: int = 0):
         cfg = Config()
         cfg.n_gpus = n_gpus or (len(gpu_ids) if gpu_ids else 0)
         self._ids = (i32 * len(gpu_ids))(*gpu_ids) if gpu_ids else None
@@ -197,6 +198,7 @@ class Runtime:
         cfg.workspace_bytes_per_gpu = workspace_bytes
         cfg.copy_ctas, cfg.copy_threads, cfg.chunk_bytes, cfg.flags = copy_ctas, copy_threads, chunk_bytes, flags
         cfg.engine, cfg.dma_min_bytes, cfg.dma_group_bytes, cfg.dma_streams = engine, dma_min_bytes, dma_group_bytes, dma_streams
+        cfg.stripe_min_bytes = stripe_min_bytes
         h = vp()
         _check(lib().fsw_init(ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
@@ -277,14 +279,17 @@ class Runtime:
     # ---- invoke -------------------------------------------------------------------------
     def invoke(self, mid: int, inp: np.ndarray, out: Optional[np.ndarray] = None, gpu: int = -1,
                chunk_bytes: int = 0, order: int = ORDER_EXEC, order_seed: int = 0, copy_ctas: int = 0,
-               flags: int = 0, engine: int = 0, dma_group_bytes: int = 0, dma_streams: int = 0) -> Result:
+               flags: int = 0, engine: int = 0, dma_group_bytes: int = 0, dma_streams: int = 0,
+               stripe: Optional[Sequence[int]] = None, peer_src: int = -1) -> Result:
         info = self._models.get(mid) or self.model_info(mid)
         inp = np.ascontiguousarray(inp)
         if out is None:
             out = np.empty(info["output_bytes"] // 4, dtype=np.float32 if info["output_dtype"] == 1 else np.int32) \
                 if info["output_dtype"] != 0 else np.empty(info["output_bytes"] // 2, dtype=np.uint16)
         st = InvokeStats()
-        opts = InvokeOpts(gpu, 0, chunk_bytes, order, order_seed, copy_ctas, flags, engine, dma_group_bytes, dma_streams)
+        src = (i32 * len(stripe))(*stripe) if stripe else None
+        opts = InvokeOpts(gpu, len(stripe) if stripe else 0, chunk_bytes, order, order_seed, copy_ctas, flags, engine,
+                          dma_group_bytes, dma_streams, src, peer_src + 1)
         _check(lib().fsw_invoke_ex(self.h, mid, ctypes.byref(opts), inp.ctypes.data, inp.nbytes, out.ctypes.data,
                                    out.nbytes, ctypes.byref(st)))
         return Result(out, st.as_dict())

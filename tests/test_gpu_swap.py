@@ -84,3 +84,105 @@ def test_swap_reaches_link_bandwidth(rt, registered, engine):
         rt.evict(mid)
         gbs.append(rt.invoke(mid, x, gpu=0, engine=engine).stats["link_gbps"])
     assert np.median(gbs) > 40.0, gbs
+
+
+# ---------------------------------------------------------------------------------------------
+# striped swap.  This box has one GPU, so the sources are the target listed several
+# times: every entry runs its own swap kernel on its own stream with the protocol of a remote source
+# (its share of every layer's pieces, system-scope release on the target's counters, the target's
+# gate counting every source).  Bytes must land bit-exactly and the output must not change.
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n_src", [2, 3, 4])
+@pytest.mark.parametrize("name", ["mlp", "bert-base", "resnet50"])
+def test_striped_swap_virtual_sources_bit_exact(rt, registered, name, n_src):
+    spec, w, x, mid = registered(name)
+    rt.evict(mid)
+    base = rt.invoke(mid, x, gpu=0).output.copy()
+    for flags in (0, NO_OVERLAP):
+        rt.evict(mid)
+        r = rt.invoke(mid, x, gpu=0, stripe=[0] * n_src, flags=flags)
+        assert r.stats["swap_kind"] == 3 and r.stats["n_sources"] == n_src, r.stats
+        assert r.stats["engine"] == ENGINE_SM
+        np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+        np.testing.assert_array_equal(r.output, base)
+
+
+def test_striped_swap_more_sources_than_pieces(rt):
+    spec = _odd_model([1, 256])   # two pieces in total, four sources: two run empty shares
+    mid = rt.register_spec(spec, spec.build_weights())
+    try:
+        r = rt.invoke(mid, spec.make_input(), gpu=0, stripe=[0, 0, 0, 0])
+        assert r.stats["swap_kind"] == 3
+        np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    finally:
+        rt.unregister(mid)
+
+
+def test_striped_swap_argument_errors(rt, registered):
+    from paper_2306_03622_b200 import FswError
+    from paper_2306_03622_b200 import fsw as F
+    spec, w, x, mid = registered("mlp")
+    rt.evict(mid)
+    with pytest.raises(FswError) as e:
+        rt.invoke(mid, x, gpu=0, stripe=[0, 5])     # not a GPU of the pool
+    assert e.value.status == F.EINVAL
+    with pytest.raises(FswError) as e:
+        rt.invoke(mid, x, gpu=0, stripe=[0] * 5)    # more entries than swap slots on GPU 0
+    assert e.value.status == F.EBUSY
+    r = rt.invoke(mid, x, gpu=0, stripe=[0])        # one entry == target: plain host swap
+    assert r.stats["swap_kind"] == 1
+
+
+def test_striped_swap_two_pool_gpus_on_one_device():
+    """A pool of two GPU entries mapped onto the same device: pool GPU 1 acts as a remote source
+    of pool GPU 0 (its own slot, stream and ticket; stores into GPU 0's extent; system-scope
+    release on GPU 0's counters).  The ctx policy stripes once the store passes stripe_min_bytes."""
+    from paper_2306_03622_b200 import Runtime
+    spec = synth.build_model("bert-base")
+    w, x = spec.build_weights(), spec.make_input()
+    with Runtime(gpu_ids=[0, 0], pool_bytes=2 << 30, stripe_min_bytes=1) as rt2:
+        mid = rt2.register_spec(spec, w)
+        base = rt2.invoke(mid, x, gpu=0, stripe=[0]).output.copy()
+        for src in ([0, 1], [1, 0], [1], [1, 1, 0]):
+            rt2.evict(mid)
+            r = rt2.invoke(mid, x, gpu=0, stripe=src)
+            assert r.stats["swap_kind"] == 3 and r.stats["gpu"] == 0
+            np.testing.assert_array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
+            np.testing.assert_array_equal(r.output, base)
+        rt2.evict(mid)
+        out = np.empty_like(base)
+        st = rt2.invoke_plain(mid, x, out)   # policy: cold, store >= stripe_min_bytes -> striped x2
+        assert st["swap_kind"] == 3 and st["n_sources"] == 2
+        np.testing.assert_array_equal(out, base)
+
+
+def test_peer_swap_from_resident_copy_two_pool_gpus_on_one_device():
+    """Alg. 1 case 2: the model is resident on pool GPU 1 only, a cold invoke on
+    GPU 0 copies it from GPU 1's extent (copy engine, device to device) instead of the host store."""
+    from paper_2306_03622_b200 import NO_PEER_SWAP, FswError, Runtime
+    from paper_2306_03622_b200 import fsw as F
+    spec = synth.build_model("resnet50")
+    w, x = spec.build_weights(), spec.make_input()
+    with Runtime(gpu_ids=[0, 0], pool_bytes=1 << 30) as rt2:
+        mid = rt2.register_spec(spec, w)
+        base = rt2.invoke(mid, x, gpu=1).output.copy()
+        with pytest.raises(FswError) as e:
+            rt2.invoke(mid, x, gpu=0, peer_src=0)          # the target itself
+        assert e.value.status == F.EINVAL
+        r = rt2.invoke(mid, x, gpu=0)                        # policy: resident on GPU 1 -> peer swap
+        assert r.stats["swap_kind"] == 2 and r.stats["gpu"] == 0, r.stats
+        np.testing.assert_array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
+        np.testing.assert_array_equal(r.output, base)
+        rt2.evict(mid, 0)
+        r = rt2.invoke(mid, x, gpu=0, peer_src=1)            # explicit
+        assert r.stats["swap_kind"] == 2
+        np.testing.assert_array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
+        rt2.evict(mid, 0)
+        r = rt2.invoke(mid, x, gpu=0, flags=NO_PEER_SWAP)    # policy off: from the host store
+        assert r.stats["swap_kind"] == 1
+        np.testing.assert_array_equal(r.output, base)
+        rt2.evict(mid, 1)
+        rt2.evict(mid, 0)
+        with pytest.raises(FswError) as e:
+            rt2.invoke(mid, x, gpu=0, peer_src=1)          # not resident on GPU 1 any more
+        assert e.value.status == F.ESTATE
