@@ -83,6 +83,9 @@ typedef struct {
                                          merged up to it, larger layers split, groups taper
                                          towards the end of the store); 0 = 64 MiB             */
     uint32_t dma_streams;             /* DMA engine: concurrent copy streams (1..4); 0 = 1      */
+    const int32_t* pcie_neighbor;     /* n_gpus entries: the pool GPU sharing each GPU's PCIe
+                                         switch, −1 = none (Algorithm 1's "neighbor"); NULL = none
+                                         (HGX B200: one switch per GPU)                          */
 } fsw_config;
 
 /* Swap engines.  Both move the host store into the extent in execution order and
@@ -249,6 +252,76 @@ fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu,
 fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
 /* Activation slot of the last invoke of `model_id` on `gpu` (valid until the next invoke). */
 fsw_status fsw_debug_read_slot(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, int32_t slot, void* dst, uint64_t cap);
+
+/* ---------------------------------------------------------------------------------------
+ * Node policies (§5).  Pure host functions, no context: the
+ * runtime's placement (fsw_invoke) and eviction (weight pool) call the same code.
+ * ------------------------------------------------------------------------------------- */
+/* Required request count: (p·n − m)/(1 − p).  EINVAL unless 0 < p < 1, m <= n. */
+fsw_status fsw_policy_rrc(uint64_t n, uint64_t m, double p, double* out);
+/* α partition: with functions sorted by RRC (ties by index), high[i] = 1 for
+ * the first k, k the largest with Σ_{j<=k} max(RRC_j,0) <= α·Σ_i max(RRC_i,0).  EINVAL if α ∉ [0,1]. */
+fsw_status fsw_policy_partition(const double* rrc, uint32_t n, double alpha, uint8_t* high);
+/* Algorithm 2.  EINVAL unless scalar > 1. */
+fsw_status fsw_policy_alpha(double alpha, double last_ratio, double new_ratio, double scalar, double threshold,
+                            double* out);
+/* Algorithm 1.  Per GPU i of n: available[i] (idle), hosts[i] (target model
+ * resident), neighbor[i] (GPU sharing its PCIe switch, −1 none; NULL = none), loading[i] (0 none,
+ * 1 light, 2 heavy model being swapped in from the host; NULL = none), link[g·n+s] (NVLink GB/s
+ * from s into g, 0 = no link; NULL = uniform, as on NVSwitch).  kind: 0 run resident, 1 swap from
+ * the host, 2 swap from GPU src.  Ties: lowest GPU id / (target, source).  EBUSY: no GPU available. */
+typedef struct { int32_t gpu; uint32_t kind; int32_t src; } fsw_decision;
+fsw_status fsw_policy_schedule(uint32_t n, const uint8_t* available, const uint8_t* hosts, const int32_t* neighbor,
+                               const uint8_t* loading, const float* link, fsw_decision* out);
+/* Heaviness-aware LRU: eviction order of n resident models on one GPU — light
+ * models and heavy models with >= 2 copies first, then sole-copy heavy models, LRU within each;
+ * in-use models are skipped.  order has n entries; n_order = how many were emitted.            */
+fsw_status fsw_policy_eviction_order(uint32_t n, const uint8_t* heavy, const uint32_t* copies, const uint64_t* last_use,
+                                     const uint8_t* in_use, uint32_t* order, uint32_t* n_order);
+/* Heavy / light class of a model for placement and eviction: 1 heavy, 0 light, −1 auto (heavy
+ * while unmeasured; then heavy iff mean cold / mean resident device latency > 1.25, SPEC S:77's
+ * threshold on P:839's "pipelining significantly slows down the inference").                  */
+fsw_status fsw_model_set_heavy(fsw_ctx* ctx, uint32_t model_id, int32_t heavy);
+fsw_status fsw_model_is_heavy(fsw_ctx* ctx, uint32_t model_id, int32_t* heavy);
+
+/* ---------------------------------------------------------------------------------------
+ * Request scheduler: functions = (model, deadline, tail percentile p);
+ * requests queue in two priority classes by RRC and are dispatched onto the pool's GPUs
+ * through fsw_invoke (placement by Algorithm 1, at most max_inflight at once).  Input/output
+ * buffers of a submitted request stay caller-owned and must stay valid until fsw_wait.
+ * ------------------------------------------------------------------------------------- */
+typedef struct fsw_sched fsw_sched;
+typedef struct {
+    double alpha0;        /* initial α; 0 = 0.5                                               */
+    double scalar;        /* Algorithm 2 scale factor; 0 = 2                  */
+    double threshold;     /* Algorithm 2 threshold; 0 = 0.04                  */
+    double period_ms;     /* α re-configuration period; 0 = 10 000 ms                         */
+    uint32_t max_inflight;/* concurrent invokes; 0 = n_gpus (one request per GPU)      */
+} fsw_sched_config;
+fsw_status fsw_sched_create(fsw_ctx* ctx, const fsw_sched_config* cfg, fsw_sched** out);
+void fsw_sched_destroy(fsw_sched* s);  /* serves every queued request, then stops            */
+fsw_status fsw_function_register(fsw_sched* s, uint32_t model_id, double deadline_ms, double p, uint32_t* fid);
+fsw_status fsw_submit(fsw_sched* s, uint32_t fid, const void* input, uint64_t input_bytes, void* output,
+                      uint64_t output_cap, uint64_t* ticket);
+typedef struct {
+    double queue_ms, total_ms, device_ms; /* submit -> dispatch, submit -> output, invoke graph */
+    int32_t met_deadline, gpu;
+    uint32_t swap_kind;                   /* FSW_SWAP_*                                          */
+    fsw_status status;
+} fsw_request_stats;
+fsw_status fsw_wait(fsw_sched* s, uint64_t ticket, fsw_request_stats* out); /* returns its status */
+typedef struct {
+    uint64_t n, m;                        /* completed requests / within the deadline            */
+    double rrc, rrc_normalized, avg_latency_ms;
+    uint32_t high, queued;
+} fsw_function_stats;
+fsw_status fsw_function_stats_get(fsw_sched* s, uint32_t fid, fsw_function_stats* out);
+typedef struct {
+    double alpha;
+    uint32_t n_functions, n_high, active_functions, slo_compliant_functions;
+    uint64_t completed, met_deadline, n_resident, n_host_swaps, n_peer_swaps, n_striped_swaps;
+} fsw_sched_stats;
+fsw_status fsw_sched_stats_get(fsw_sched* s, fsw_sched_stats* out);
 
 /* The DMA engine's copy plan for (group_bytes, streams), host logic only (usable with
  * FSW_HOST_ONLY): n_groups copy groups [lo, hi) of the host store in execution order, each

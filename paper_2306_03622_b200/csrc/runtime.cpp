@@ -31,6 +31,7 @@
 
 #include "fsw.h"
 #include "kernels.h"
+#include "policy.h"
 
 using namespace fsw;
 
@@ -218,6 +219,10 @@ struct Model {
     std::vector<uint64_t> last_use;
     std::vector<std::unique_ptr<Plan>> plans;
     int inflight = 0;
+    // heavy / light class for placement and eviction: 1, 0, or -1 auto
+    int heavy = -1;
+    double cold_ms_sum = 0, warm_ms_sum = 0;
+    uint64_t n_cold_runs = 0, n_warm_runs = 0;
 };
 
 // A swap-kernel slot of a GPU acting as a striped-swap source for some target (its own ticket
@@ -253,6 +258,7 @@ struct Gpu {
     uint64_t stage_cap = 0, out_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr, evfork = nullptr, evjoin = nullptr;
     bool busy = false;
+    int loading = 0;  // 0, or 1 / 2 while a light / heavy model is being swapped in from the host
     uint64_t generation = 0;
     // stats
     uint64_t n_evictions = 0, bytes_swapped_total = 0, n_cold = 0, n_warm = 0;
@@ -296,6 +302,7 @@ struct fsw_ctx {
     std::condition_variable cv;
     uint64_t clock = 0;
     std::vector<std::vector<char>> peer;  // peer[i][j]: GPU i can store into GPU j's memory
+    std::vector<int> neighbor;            // GPU sharing a PCIe switch (-1 none), fsw_config.pcie_neighbor
 };
 
 // ==========================================================================================
@@ -383,6 +390,10 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
         fsw_status s = init_gpu(c.get(), c->gpus[i]);
         if (s != FSW_OK) return s;
     }
+    c->neighbor.assign(n, -1);
+    if (cfg && cfg->pcie_neighbor)
+        for (uint32_t i = 0; i < n; ++i) c->neighbor[i] = cfg->pcie_neighbor[i] < (int32_t)n ? cfg->pcie_neighbor[i] : -1;
+    c->cfg.pcie_neighbor = nullptr;
     // NVLink peer access between the pool's GPUs (striped swap stores into a peer's extent)
     c->peer.assign(n, std::vector<char>(n, 0));
     for (uint32_t i = 0; i < n; ++i)
@@ -1284,6 +1295,32 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
 // ==========================================================================================
 // pool residency
 // ==========================================================================================
+// Heavy / light: set by the caller, or measured — heavy iff pipelined swapping slows
+// the inference down by more than 1.25x — and heavy while unmeasured.
+static bool model_heavy(const Model& m) {
+    if (m.heavy >= 0) return m.heavy != 0;
+    if (!m.n_cold_runs || !m.n_warm_runs) return true;
+    return (m.cold_ms_sum / m.n_cold_runs) > 1.25 * (m.warm_ms_sum / m.n_warm_runs);
+}
+
+extern "C" fsw_status fsw_model_set_heavy(fsw_ctx* c, uint32_t id, int32_t heavy) {
+    if (!c || heavy < -1 || heavy > 1) return fail(FSW_EINVAL, "model_set_heavy: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Model* m = c->models.size() > id ? c->models[id].get() : nullptr;
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    m->heavy = heavy;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_model_is_heavy(fsw_ctx* c, uint32_t id, int32_t* heavy) {
+    if (!c || !heavy) return fail(FSW_EINVAL, "model_is_heavy: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Model* m = c->models.size() > id ? c->models[id].get() : nullptr;
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    *heavy = model_heavy(*m) ? 1 : 0;
+    return FSW_OK;
+}
+
 static void invalidate(fsw_ctx* c, Model& m, int gi) {
     if (m.extent[gi] < 0) return;
     fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.extent[gi]);
@@ -1299,11 +1336,24 @@ static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
             m.extent[gi] = (int64_t)off;
             return FSW_OK;
         }
-        Model* victim = nullptr;
-        for (auto& o : c->models)
-            if (o && o.get() != &m && o->extent[gi] >= 0 && o->inflight == 0 &&
-                (!victim || o->last_use[gi] < victim->last_use[gi]))
-                victim = o.get();
+        // heaviness-aware LRU: light models and heavy ones with copies on other
+        // GPUs go first, sole-copy heavy models last; LRU within each group
+        std::vector<Model*> cand;
+        std::vector<uint8_t> heavy, in_use;
+        std::vector<uint32_t> copies;
+        std::vector<uint64_t> last;
+        for (auto& o : c->models) {
+            if (!o || o.get() == &m || o->extent[gi] < 0) continue;
+            cand.push_back(o.get());
+            heavy.push_back(model_heavy(*o));
+            uint32_t k = 0;
+            for (int64_t e : o->extent) k += e >= 0;
+            copies.push_back(k);
+            last.push_back(o->last_use[gi]);
+            in_use.push_back(o->inflight != 0);
+        }
+        const std::vector<uint32_t> order = eviction_order(heavy, copies, last, in_use);
+        Model* victim = order.empty() ? nullptr : cand[order[0]];
         if (!victim)
             return fail(FSW_ENOMEM, "pool on gpu %d cannot hold %llu bytes even after evicting every idle model", g.dev,
                         (unsigned long long)m.store_bytes);
@@ -1369,12 +1419,19 @@ extern "C" fsw_status fsw_pool_stats_get(fsw_ctx* c, int32_t gpu, fsw_pool_stats
 // ==========================================================================================
 // invoke
 // ==========================================================================================
-static int pick_gpu(fsw_ctx* c, Model& m) {
-    for (size_t i = 0; i < c->gpus.size(); ++i)
-        if (!c->gpus[i].busy && m.extent[i] >= 0) return (int)i;  // resident and idle
-    for (size_t i = 0; i < c->gpus.size(); ++i)
-        if (!c->gpus[i].busy) return (int)i;  // lowest idle id
-    return -1;
+// Algorithm 1 over the pool's live state; NVLink through NVSwitch is uniform.
+static Decision pick_gpu(fsw_ctx* c, Model& m) {
+    const size_t n = c->gpus.size();
+    std::vector<uint8_t> avail(n), hosts(n), loading(n);
+    for (size_t i = 0; i < n; ++i) {
+        avail[i] = !c->gpus[i].busy;
+        hosts[i] = m.extent[i] >= 0;
+        loading[i] = (uint8_t)c->gpus[i].loading;
+    }
+    std::vector<float> link(n * n, 0.0f);
+    for (size_t g = 0; g < n; ++g)
+        for (size_t s = 0; s < n; ++s) link[g * n + s] = c->peer[g][s] ? 1.0f : 0.0f;
+    return schedule(avail, hosts, c->neighbor, loading, link);
 }
 
 extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_opts* opts, const void* input,
@@ -1398,8 +1455,10 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         if (input_bytes != m->input_bytes) return fail(FSW_EINVAL, "invoke: input_bytes %llu != %llu", (unsigned long long)input_bytes, (unsigned long long)m->input_bytes);
         if (output_cap < m->output_bytes) return fail(FSW_EINVAL, "invoke: output_cap too small (%llu < %llu)", (unsigned long long)output_cap, (unsigned long long)m->output_bytes);
         if (o.gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "invoke: bad gpu %d", o.gpu);
+        Decision dec;
         for (;;) {
-            gi = o.gpu >= 0 ? (c->gpus[o.gpu].busy ? -1 : o.gpu) : pick_gpu(c, *m);
+            if (o.gpu >= 0) gi = c->gpus[o.gpu].busy ? -1 : o.gpu;
+            else gi = (dec = pick_gpu(c, *m)).gpu;
             if (gi >= 0) break;
             c->cv.wait(lk);
         }
@@ -1426,6 +1485,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             else if (!c->peer[gi][s]) ss = fail(FSW_ETOPO, "invoke: gpu %d cannot read gpu %d", gi, s);
             else peer = s;
         } else if (cold && !o.n_stripe_src && !((o.flags | c->cfg.flags) & FSW_NO_PEER_SWAP)) {
+            if (o.gpu < 0 && dec.kind == 2) peer = dec.src;  // Algorithm 1, line 11
             for (int s = 0; s < (int)c->gpus.size() && peer < 0; ++s)
                 if (s != gi && m->extent[s] >= 0 && c->peer[gi][s]) peer = s;
         }
@@ -1465,6 +1525,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             srcs.clear();
             slots.clear();
         }
+        if (ss == FSW_OK && cold && peer < 0) g.loading = model_heavy(*m) ? 2 : 1;  // host link in use
         if (ss != FSW_OK) {
             for (SrcSlot* sl : slots) sl->busy = false;
             if (cold) invalidate(c, *m, gi);
@@ -1479,6 +1540,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     fsw_status st = FSW_OK;
     auto finish = [&](fsw_status s) {
         std::lock_guard<std::mutex> lk(c->mu);
+        g.loading = 0;
         if (s != FSW_OK && cold) invalidate(c, *m, gi);  // failed swap: extent is not valid
         for (SrcSlot* sl : slots) sl->busy = false;
         g.busy = false;
@@ -1625,11 +1687,19 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     }
     {
         std::lock_guard<std::mutex> lk(c->mu);
+        float dms = 0;
+        cudaEventElapsedTime(&dms, g.ev0, g.ev1);
         if (cold) {
             g.n_cold++;
             g.bytes_swapped_total += m->store_bytes;
+            if (peer < 0 && !striped) {
+                m->cold_ms_sum += dms;
+                m->n_cold_runs++;
+            }
         } else {
             g.n_warm++;
+            m->warm_ms_sum += dms;
+            m->n_warm_runs++;
         }
     }
     finish(FSW_OK);

@@ -36,7 +36,8 @@ class Config(ctypes.Structure):
     _fields_ = [("n_gpus", u32), ("gpu_ids", ctypes.POINTER(i32)), ("pool_bytes_per_gpu", u64),
                 ("workspace_bytes_per_gpu", u64), ("copy_ctas", u32), ("copy_threads", u32),
                 ("chunk_bytes", u64), ("stripe_min_bytes", u64), ("flags", u32), ("engine", u32),
-                ("dma_min_bytes", u64), ("dma_group_bytes", u64), ("dma_streams", u32)]
+                ("dma_min_bytes", u64), ("dma_group_bytes", u64), ("dma_streams", u32),
+                ("pcie_neighbor", ctypes.POINTER(i32))]
 
 
 class Tensor(ctypes.Structure):
@@ -95,11 +96,47 @@ class PoolStats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class Decision(ctypes.Structure):
+    _fields_ = [("gpu", i32), ("kind", u32), ("src", i32)]
+
+
+class SchedConfig(ctypes.Structure):
+    _fields_ = [("alpha0", dbl), ("scalar", dbl), ("threshold", dbl), ("period_ms", dbl), ("max_inflight", u32)]
+
+
+class RequestStats(ctypes.Structure):
+    _fields_ = [("queue_ms", dbl), ("total_ms", dbl), ("device_ms", dbl), ("met_deadline", i32), ("gpu", i32),
+                ("swap_kind", u32), ("status", ctypes.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class FunctionStats(ctypes.Structure):
+    _fields_ = [("n", u64), ("m", u64), ("rrc", dbl), ("rrc_normalized", dbl), ("avg_latency_ms", dbl), ("high", u32),
+                ("queued", u32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class SchedStats(ctypes.Structure):
+    _fields_ = [("alpha", dbl), ("n_functions", u32), ("n_high", u32), ("active_functions", u32),
+                ("slo_compliant_functions", u32), ("completed", u64), ("met_deadline", u64), ("n_resident", u64),
+                ("n_host_swaps", u64), ("n_peer_swaps", u64), ("n_striped_swaps", u64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_register_model",
            "fsw_unregister_model", "fsw_model_info_get", "fsw_store_tensor_get", "fsw_invoke", "fsw_invoke_ex",
            "fsw_evict", "fsw_pool_stats_get", "fsw_n_gpus", "fsw_debug_read_resident", "fsw_debug_read_store",
            "fsw_debug_read_slot", "fsw_arena_create", "fsw_arena_destroy", "fsw_arena_alloc", "fsw_arena_free",
-           "fsw_arena_stats", "fsw_debug_dma_plan"]
+           "fsw_arena_stats", "fsw_debug_dma_plan", "fsw_policy_rrc", "fsw_policy_partition", "fsw_policy_alpha",
+           "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
+           "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
+           "fsw_function_stats_get", "fsw_sched_stats_get"]
 
 _lib = None
 
@@ -137,6 +174,21 @@ def lib():
         L.fsw_arena_stats.argtypes = [vp, ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u32)]
         L.fsw_arena_stats.restype = None
         L.fsw_debug_dma_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
+        L.fsw_policy_rrc.argtypes = [u64, u64, dbl, ctypes.POINTER(dbl)]
+        L.fsw_policy_partition.argtypes = [vp, u32, dbl, vp]
+        L.fsw_policy_alpha.argtypes = [dbl, dbl, dbl, dbl, dbl, ctypes.POINTER(dbl)]
+        L.fsw_policy_schedule.argtypes = [u32, vp, vp, vp, vp, vp, ctypes.POINTER(Decision)]
+        L.fsw_policy_eviction_order.argtypes = [u32, vp, vp, vp, vp, vp, ctypes.POINTER(u32)]
+        L.fsw_model_set_heavy.argtypes = [vp, u32, i32]
+        L.fsw_model_is_heavy.argtypes = [vp, u32, ctypes.POINTER(i32)]
+        L.fsw_sched_create.argtypes = [vp, ctypes.POINTER(SchedConfig), ctypes.POINTER(vp)]
+        L.fsw_sched_destroy.argtypes = [vp]
+        L.fsw_sched_destroy.restype = None
+        L.fsw_function_register.argtypes = [vp, u32, dbl, dbl, ctypes.POINTER(u32)]
+        L.fsw_submit.argtypes = [vp, u32, vp, u64, vp, u64, ctypes.POINTER(u64)]
+        L.fsw_wait.argtypes = [vp, u64, ctypes.POINTER(RequestStats)]
+        L.fsw_function_stats_get.argtypes = [vp, u32, ctypes.POINTER(FunctionStats)]
+        L.fsw_sched_stats_get.argtypes = [vp, ctypes.POINTER(SchedStats)]
         for name in EXPORTS:
             f = getattr(L, name)
             if f.restype is ctypes.c_int:  # default
@@ -301,6 +353,14 @@ class Runtime:
                                 ctypes.byref(st)))
         return st.as_dict()
 
+    def set_heavy(self, mid: int, heavy: int):
+        _check(lib().fsw_model_set_heavy(self.h, mid, heavy))
+
+    def is_heavy(self, mid: int) -> bool:
+        h = i32()
+        _check(lib().fsw_model_is_heavy(self.h, mid, ctypes.byref(h)))
+        return bool(h.value)
+
     def evict(self, mid: int, gpu: int = -1):
         _check(lib().fsw_evict(self.h, mid, gpu))
 
@@ -337,3 +397,106 @@ class Runtime:
         buf = np.empty(nbytes, dtype=np.uint8)
         _check(lib().fsw_debug_read_slot(self.h, mid, gpu, slot, buf.ctypes.data, nbytes))
         return buf
+
+
+# ---- node policies (pure host functions; include/fsw.h "Node policies") ----------------------
+def policy_rrc(n: int, m: int, p: float) -> float:
+    out = dbl()
+    _check(lib().fsw_policy_rrc(n, m, p, ctypes.byref(out)))
+    return out.value
+
+
+def policy_partition(rrcs, alpha: float) -> np.ndarray:
+    r = np.ascontiguousarray(rrcs, dtype=np.float64)
+    high = np.zeros(len(r), np.uint8)
+    _check(lib().fsw_policy_partition(r.ctypes.data, len(r), alpha, high.ctypes.data))
+    return high
+
+
+def policy_alpha(alpha, last_ratio, new_ratio, scalar=2.0, threshold=0.04) -> float:
+    out = dbl()
+    _check(lib().fsw_policy_alpha(alpha, last_ratio, new_ratio, scalar, threshold, ctypes.byref(out)))
+    return out.value
+
+
+def policy_schedule(available, hosts, neighbor=None, loading=None, link=None):
+    """Algorithm 1: returns (gpu, kind, src) or None when no GPU is available (EBUSY)."""
+    n = len(available)
+    av = np.ascontiguousarray(available, np.uint8)
+    ho = np.ascontiguousarray(hosts, np.uint8)
+    nb = np.ascontiguousarray(neighbor, np.int32) if neighbor is not None else None
+    ld = np.ascontiguousarray(loading, np.uint8) if loading is not None else None
+    lk = np.ascontiguousarray(link, np.float32).reshape(-1) if link is not None else None
+    d = Decision()
+    rc = lib().fsw_policy_schedule(n, av.ctypes.data, ho.ctypes.data, nb.ctypes.data if nb is not None else None,
+                                   ld.ctypes.data if ld is not None else None, lk.ctypes.data if lk is not None else None,
+                                   ctypes.byref(d))
+    if rc == EBUSY:
+        return None
+    _check(rc)
+    return d.gpu, d.kind, d.src
+
+
+def policy_eviction_order(heavy, copies, last_use, in_use):
+    n = len(heavy)
+    h = np.ascontiguousarray(heavy, np.uint8)
+    c = np.ascontiguousarray(copies, np.uint32)
+    lu = np.ascontiguousarray(last_use, np.uint64)
+    iu = np.ascontiguousarray(in_use, np.uint8)
+    order = np.zeros(max(1, n), np.uint32)
+    k = u32()
+    _check(lib().fsw_policy_eviction_order(n, h.ctypes.data, c.ctypes.data, lu.ctypes.data, iu.ctypes.data,
+                                           order.ctypes.data, ctypes.byref(k)))
+    return list(order[:k.value])
+
+
+class Scheduler:
+    """Request scheduler over a Runtime (fsw_sched_*): functions, RRC queues, Algorithm 1 placement."""
+
+    def __init__(self, rt: "Runtime", alpha0=0.0, scalar=0.0, threshold=0.0, period_ms=0.0, max_inflight=0):
+        self.rt = rt
+        cfg = SchedConfig(alpha0, scalar, threshold, period_ms, max_inflight)
+        h = vp()
+        _check(lib().fsw_sched_create(rt.h, ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+        self._keep = {}
+
+    def register_function(self, model_id: int, deadline_ms: float, p: float = 0.98) -> int:
+        fid = u32()
+        _check(lib().fsw_function_register(self.h, model_id, deadline_ms, p, ctypes.byref(fid)))
+        return fid.value
+
+    def submit(self, fid: int, inp: np.ndarray, out: np.ndarray) -> int:
+        t = u64()
+        _check(lib().fsw_submit(self.h, fid, inp.ctypes.data, inp.nbytes, out.ctypes.data, out.nbytes, ctypes.byref(t)))
+        self._keep[t.value] = (inp, out)
+        return t.value
+
+    def wait(self, ticket: int) -> dict:
+        st = RequestStats()
+        rc = lib().fsw_wait(self.h, ticket, ctypes.byref(st))
+        self._keep.pop(ticket, None)
+        d = st.as_dict()
+        d["rc"] = rc
+        return d
+
+    def function_stats(self, fid: int) -> dict:
+        s = FunctionStats()
+        _check(lib().fsw_function_stats_get(self.h, fid, ctypes.byref(s)))
+        return s.as_dict()
+
+    def stats(self) -> dict:
+        s = SchedStats()
+        _check(lib().fsw_sched_stats_get(self.h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().fsw_sched_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

@@ -449,8 +449,13 @@ def resnet_tiny(seed=13, img=32) -> ModelSpec:
     return _resnet([1, 2, 1, 1], [16, 32, 64, 64], img, stem=16, n_classes=40, seed=seed, name=f"resnet_tiny{img}")
 
 
-def build_model(name: str) -> ModelSpec:
-    return CONFIGS[name]()
+def build_model(name: str, seed: Optional[int] = None) -> ModelSpec:
+    """A synthetic model of the named configuration; `seed` gives a distinct instance (weights and
+    input) of the same architecture, e.g. one per serverless function of a trace."""
+    spec = CONFIGS[name]()
+    if seed is not None:
+        spec.seed = seed
+    return spec
 
 
 CONFIGS: Dict[str, Callable[[], ModelSpec]] = {

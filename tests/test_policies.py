@@ -1,0 +1,182 @@
+"""CPU tests of FaaSwap's node policies in libfsw: RRC, α partition,
+α auto-configuration (Algorithm 2), interference-aware placement (Algorithm 1) and heaviness-aware
+eviction.  Pins: the paper's defining equations and worked statements, SPEC.md's example vectors
+(S:361-372), and an exhaustive brute-force ranking of Algorithm 1 over small nodes."""
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_2306_03622_b200 import build as B
+from paper_2306_03622_b200 import fsw as F
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    B.build()
+
+
+# ---------------------------------------------------------------------------------------------
+# RRC
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,m,p,want", [(0, 0, 0.98, 0.0), (100, 90, 0.98, 400.0), (100, 100, 0.98, -100.0)])
+def test_rrc_spec_vectors(n, m, p, want):
+    assert F.policy_rrc(n, m, p) == pytest.approx(want, abs=1e-9)
+
+
+@pytest.mark.parametrize("n,m,p", [(100, 90, 0.98), (7, 3, 0.9), (50, 49, 0.99), (10, 8, 0.5)])
+def test_rrc_solves_the_papers_equation(n, m, p):
+    """RRC is 'simply derived from the equation (m + RRC)/(n + RRC) = p'."""
+    r = F.policy_rrc(n, m, p)
+    assert (m + r) / (n + r) == pytest.approx(p, rel=1e-12)
+
+
+def test_rrc_monotone_and_errors():
+    assert F.policy_rrc(101, 90, 0.98) > F.policy_rrc(100, 90, 0.98)
+    assert F.policy_rrc(100, 91, 0.98) < F.policy_rrc(100, 90, 0.98)
+    for args in [(10, 5, 0.0), (10, 5, 1.0), (10, 11, 0.9)]:
+        with pytest.raises(F.FswError):
+            F.policy_rrc(*args)
+
+
+def test_serving_ceil_rrc_more_requests_in_deadline_reaches_compliance():
+    n, m, p = 100, 90, 0.98
+    k = int(np.ceil(F.policy_rrc(n, m, p)))
+    assert F.policy_rrc(n + k, m + k, p) <= 1e-9
+
+
+# ---------------------------------------------------------------------------------------------
+# α partition
+# ---------------------------------------------------------------------------------------------
+def test_partition_spec_vectors():
+    assert list(F.policy_partition([-5, 10, 30], 0.3)) == [1, 1, 0]          # budget 12: 0+10 <= 12 < 40
+    assert list(F.policy_partition([3, 1, 2, -1], 1.0)) == [1, 1, 1, 1]      # "when α is 1, all ... high"
+    assert list(F.policy_partition([3, 1, 2, -1, 0], 0.0)) == [0, 0, 0, 1, 1]  # only RRC <= 0 fit a zero budget
+
+
+def test_partition_is_monotone_in_alpha_and_scale_invariant():
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        r = rng.normal(0, 50, rng.integers(1, 12))
+        a1, a2 = sorted(rng.uniform(0, 1, 2))
+        h1, h2 = F.policy_partition(r, a1), F.policy_partition(r, a2)
+        assert np.all(h1 <= h2)
+        np.testing.assert_array_equal(F.policy_partition(r * 7.5, a1), h1)
+        # the high set is a prefix of the RRC order and satisfies the paper's inequality with max k
+        order = np.argsort(r, kind="stable")
+        k = int(h1.sum())
+        assert set(order[:k]) == set(np.flatnonzero(h1))
+        pos = np.maximum(r[order], 0)
+        assert pos[:k].sum() <= a1 * pos.sum() + 1e-9
+        if k < len(r):
+            assert pos[:k + 1].sum() > a1 * pos.sum()
+
+
+# ---------------------------------------------------------------------------------------------
+# Algorithm 2
+# ---------------------------------------------------------------------------------------------
+def test_alpha_autoconfig_spec_vectors():
+    assert F.policy_alpha(0.4, 0.80, 0.90) == pytest.approx(0.8)   # increase
+    assert F.policy_alpha(0.6, 0.90, 0.80) == pytest.approx(0.3)   # decrease
+    assert F.policy_alpha(0.5, 0.85, 0.87) == pytest.approx(0.5)   # within the threshold
+    assert F.policy_alpha(0.8, 0.1, 0.9) == pytest.approx(1.0)     # capped at 1
+    a = 0.01
+    for _ in range(20):
+        a = F.policy_alpha(a, 0.0, 1.0)
+    assert a == 1.0
+    with pytest.raises(F.FswError):
+        F.policy_alpha(0.5, 0.1, 0.2, scalar=1.0)
+
+
+# ---------------------------------------------------------------------------------------------
+# Algorithm 1
+# ---------------------------------------------------------------------------------------------
+FAST, SLOW = 50.0, 25.0
+
+
+def test_schedule_spec_examples():
+    # model on idle GPU 2 -> run there, no swap
+    assert F.policy_schedule([1, 1, 1, 1], [0, 0, 1, 0]) == (2, 0, -1)
+    # model only on busy GPU 0; GPU 1 idle with a fast link to 0, GPU 3 idle with a slow one
+    link = np.zeros((4, 4), np.float32)
+    link[1, 0], link[3, 0] = FAST, SLOW
+    assert F.policy_schedule([0, 1, 0, 1], [1, 0, 0, 0], link=link) == (1, 2, 0)
+    # model nowhere; GPU 0's neighbour GPU 1 loads a heavy model, GPU 2's neighbour GPU 3 is idle
+    assert F.policy_schedule([1, 0, 1, 0], [0, 0, 0, 0], neighbor=[1, 0, 3, 2], loading=[0, 2, 0, 0]) == (2, 1, -1)
+    # every GPU busy -> queued
+    assert F.policy_schedule([0, 0], [1, 0]) is None
+
+
+def _brute_force(avail, hosts, nb, loading, link):
+    """Enumerate every feasible (gpu, kind, src) and rank it by Algorithm 1's case order: run on an
+    available host; else the fastest NVLink pair (available target, hosting source); else a host
+    swap tiered by the neighbour's load (idle < light < heavy).  Ties: lowest ids."""
+    n = len(avail)
+    cands = []
+    for g in range(n):
+        if not avail[g]:
+            continue
+        if hosts[g]:
+            cands.append(((0, 0, g, 0), (g, 0, -1)))
+        for s in range(n):
+            if hosts[s] and s != g and link[g][s] > 0:
+                cands.append(((1, -link[g][s], g, s), (g, 2, s)))
+        if not any(hosts):
+            ld = loading[nb[g]] if nb[g] >= 0 else 0
+            tier = {0: 0, 1: 1, 2: 2}[ld]
+            cands.append(((2, tier, g, 0), (g, 1, -1)))
+    if any(hosts) and not any(c[1][1] in (0, 2) for c in cands):
+        # hosted only on busy GPUs with no NVLink path to an available GPU: fall back to the host
+        for g in range(n):
+            if avail[g]:
+                ld = loading[nb[g]] if nb[g] >= 0 else 0
+                cands.append(((2, ld, g, 0), (g, 1, -1)))
+    return min(cands)[1] if cands else None
+
+
+def test_schedule_matches_brute_force_exhaustively():
+    """all node states with <= 4 GPUs (pairs behind PCIe switches, two NVLink tiers)."""
+    checked = 0
+    for n in (1, 2, 3, 4):
+        nb = [i ^ 1 if (i ^ 1) < n else -1 for i in range(n)]
+        links = [np.where(np.eye(n) > 0, 0, FAST)]
+        if n >= 3:
+            l2 = np.full((n, n), SLOW, np.float32)
+            np.fill_diagonal(l2, 0)
+            l2[0, 1] = l2[1, 0] = FAST
+            l2[1, 2] = 0.0  # one missing path
+            links.append(l2)
+        for avail in itertools.product([0, 1], repeat=n):
+            for hosts in itertools.product([0, 1], repeat=n):
+                for loading in itertools.product([0, 1, 2], repeat=n):
+                    for link in links:
+                        got = F.policy_schedule(avail, hosts, neighbor=nb, loading=loading, link=link)
+                        assert got == _brute_force(avail, hosts, nb, loading, link), (avail, hosts, loading)
+                        if got is not None:
+                            assert avail[got[0]], "never a busy GPU"
+                        checked += 1
+    assert checked > 5000
+
+
+# ---------------------------------------------------------------------------------------------
+# heaviness-aware eviction
+# ---------------------------------------------------------------------------------------------
+def test_eviction_spec_examples():
+    # light A (lru t=1) before sole-copy heavy B (t=0), although B is older
+    assert F.policy_eviction_order(heavy=[0, 1], copies=[1, 1], last_use=[1, 0], in_use=[0, 0]) == [0, 1]
+    # heavy C with copies on two GPUs is low priority here
+    assert F.policy_eviction_order(heavy=[1, 1], copies=[2, 1], last_use=[9, 0], in_use=[0, 0]) == [0, 1]
+    # LRU within a group; in-use models are never candidates
+    assert F.policy_eviction_order(heavy=[0, 0, 0], copies=[1, 1, 1], last_use=[7, 3, 1], in_use=[0, 0, 1]) == [1, 0]
+
+
+def test_eviction_order_invariants():
+    rng = np.random.default_rng(3)
+    for _ in range(300):
+        n = int(rng.integers(0, 10))
+        heavy, copies = rng.integers(0, 2, n), rng.integers(1, 4, n)
+        last, used = rng.permutation(n), rng.integers(0, 2, n)
+        o = F.policy_eviction_order(heavy, copies, last, used)
+        assert sorted(o) == sorted(np.flatnonzero(used == 0).tolist())
+        prio = [(1 if heavy[i] and copies[i] == 1 else 0, last[i]) for i in o]
+        assert prio == sorted(prio)
