@@ -56,7 +56,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -196,8 +196,9 @@ def run_fsw(args):
     warm = [rt.invoke(mid, x, out=out, gpu=0).stats["device_ms"] for _ in range(args.steps)]
     # the other swap engines on the same workload (context: which engine wins and by how much)
     variants = {}
-    for name, kw in (("sm", dict(engine=ENGINE_SM)), ("dma", dict(engine=ENGINE_DMA)),
-                     ("paper_dma_2MB_1stream", dict(flags=DMA_BASELINE))):
+    for name, kw in (() if args.no_variants else
+                     (("sm", dict(engine=ENGINE_SM)), ("dma", dict(engine=ENGINE_DMA)),
+                      ("paper_dma_2MB_1stream", dict(flags=DMA_BASELINE)))):
         for _ in range(2):
             cold_step(**kw)
         st = [cold_step(**kw) for _ in range(max(5, args.steps // 2))]
@@ -275,7 +276,7 @@ def run_fsw(args):
                 "traffic_note": "dram read+write bytes of one k_swap launch (ncu --set full, profiles/); "
                                 "writes still resident in L2 at kernel end are not counted",
                 "pcie_read_bytes": pcie_traffic}
-    sm_gbs = variants["sm"]["host_to_hbm_gbs"]
+    sm_gbs = variants["sm"]["host_to_hbm_gbs"] if "sm" in variants else None
     line = {
         "metric": "cold swap+infer latency ms p50 (p99, resident, host->HBM GB/s in extra keys)",
         "value": round(p50, 4), "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -297,7 +298,7 @@ def run_fsw(args):
         "pipelined_roofline_ms_at_measured_dma": round(t_roof_dma, 4) if t_roof_dma else None,
         "roofline": roof,
         "sm_engine_roofline": {"bound": "pcie", "kernel": "k_swap", "achieved": sm_gbs, "peak": PCIE_GEN5_X16_GBS,
-                               "unit": "GB/s", "frac": round(sm_gbs / PCIE_GEN5_X16_GBS, 4), "traffic": traffic,
+                               "unit": "GB/s", "frac": round(sm_gbs / PCIE_GEN5_X16_GBS, 4) if sm_gbs else None, "traffic": traffic,
                                "pcie_read_bytes": pcie_traffic},
         "engines": variants,
         "cpu_baseline": cpu,
@@ -409,6 +410,8 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of striped swap")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the other-engine comparison runs (e.g. under ncu, which serialises kernels)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
