@@ -238,11 +238,22 @@ fsw_status fsw_invoke_ex(fsw_ctx* ctx, uint32_t model_id, const fsw_invoke_opts*
 /* Invalidate the model's extent on `gpu` (−1 = every GPU).  No device→host copy
  * (PAPER.md:611-614).  ESTATE if not resident there, EBUSY if an invoke is in flight.    */
 fsw_status fsw_evict(fsw_ctx* ctx, uint32_t model_id, int32_t gpu);
+#define FSW_EVICT_KEEP_PREFIX 0x1u /* invalidate only the part beyond the model's cached prefix     */
+fsw_status fsw_evict_ex(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint32_t flags);
+
+/* Partial-parameter caching (future work in PAPER.md:1209-1211): keep the
+ * first `bytes` of the host store (rounded down to a layer boundary, leaving at least one layer to
+ * swap) resident in a separate pool extent that survives the pool's evictions (and
+ * fsw_evict_ex(FSW_EVICT_KEEP_PREFIX)), so a cold invoke swaps only the rest: its layer kernels
+ * for cached layers start without waiting.  0 = no caching.  ESTATE while the model is resident
+ * anywhere (evict it first).  *actual = the prefix bytes chosen.                            */
+fsw_status fsw_model_set_cache_prefix(fsw_ctx* ctx, uint32_t model_id, uint64_t bytes, uint64_t* actual);
 
 typedef struct {
     uint64_t capacity, used, largest_free;
     uint32_t n_resident, n_extents;
     uint64_t n_evictions, bytes_swapped_total, n_invokes_cold, n_invokes_warm;
+    uint64_t prefix_bytes_cached;     /* valid cached prefixes held on this GPU (NEXT #4)     */
 } fsw_pool_stats;
 fsw_status fsw_pool_stats_get(fsw_ctx* ctx, int32_t gpu, fsw_pool_stats* out);
 fsw_status fsw_n_gpus(fsw_ctx* ctx, uint32_t* n);

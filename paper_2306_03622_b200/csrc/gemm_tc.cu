@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(128, 1)
         if (lane == 0) {
             wait_ready_thread(w);
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            const uint8_t* wt = d->wbase + a.w_off;
+            const uint8_t* wt = weight_ptr(*d, a.w_off);
             const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
             auto load_w = [&](uint32_t st) {
                 const int s = st % stages;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(128, 1)
     }
     // 2b) row-major pass over 4-column units: consecutive threads take consecutive units, so the
     //     bias / residual loads and the output stores are 8-16 B, coalesced and independent.
-    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(d->wbase + a.b_off) : nullptr;
+    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(*d, a.b_off)) : nullptr;
     const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (a.res == nullptr || a.ld_res % 4 == 0);
     if (vec) {
 #pragma unroll 4

@@ -12,10 +12,19 @@ namespace fsw {
 // Per-GPU device-side invoke descriptor, written by the first node of every invoke graph
 // (one small H2D from pinned staging).  Kernels find the model's extent through it, so a
 // graph built once per (model, GPU) stays valid whichever pool extent the model lands in.
+// Partial-parameter caching splits a resident model at a layer boundary
+// `split`: store bytes [0, split) live in a prefix extent that survives pool evictions, bytes
+// [split, B) in the suffix extent.  split = 0: the whole model is the one extent at sbase.
 struct DevDesc {
-    uint8_t* wbase;       // base of the model's extent in the weight pool (HBM)
+    uint8_t* wbase;       // prefix extent (store offsets [0, split))
+    uint8_t* sbase;       // suffix extent (store offsets [split, B))
+    uint64_t split;
     uint64_t generation;  // invoke counter (debug)
 };
+// HBM address of store offset `off` (tensors never straddle `split`).
+__host__ __device__ __forceinline__ uint8_t* weight_ptr(const DevDesc& d, uint64_t off) {
+    return off < d.split ? d.wbase + off : d.sbase + (off - d.split);
+}
 
 // Per-GPU device control block (zeroed at the root of each cold graph except `err`).
 struct DevCtl {
@@ -53,11 +62,12 @@ struct Wait {
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 
 // ---- swap ---------------------------------------------------------------------------------
-// SM swap engine.  dst = the target extent (nullptr: desc->wbase of this GPU's invoke); ready =
-// the target's per-layer counters; own = this launch's ticket / stamps; gate = the target's
-// control block whose `started` the target's gate kernel watches; sys = 1 when the target is
-// another GPU (peer stores over NVLink, system-scope release).
-void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, uint8_t* dst, const DevDesc* desc,
+// SM swap engine.  Destinations: the extents of `dst` (by value), or of *desc when desc is not
+// NULL (this GPU's invoke descriptor, written by the graph's first node); ready = the target's
+// per-layer counters; own = this launch's ticket / stamps; gate = the target's control block
+// whose `started` the target's gate kernel watches; sys = 1 when the target is another GPU
+// (peer stores over NVLink, system-scope release).
+void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, DevDesc dst, const DevDesc* desc,
                  const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys);
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
 void launch_finish(cudaStream_t s, DevCtl* ctl);

@@ -14,7 +14,7 @@ __global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
     wait_ready_cta(w);
     pdl_wait();
     const uint32_t t = blockIdx.x;
-    const uint8_t* wb = d->wbase;
+    const DevDesc dd = *d;
     uint32_t row[4];
     for (int j = 0; j < a.n_tables; ++j) {
         uint32_t r = a.rule[j] == FSW_RULE_IDS ? (uint32_t)a.ids[t] : (a.rule[j] == FSW_RULE_POSITION ? t : 0u);
@@ -27,7 +27,7 @@ __global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
     for (uint32_t c = threadIdx.x; c < a.C; c += blockDim.x) {
         float s = 0.0f;
         for (int j = 0; j < a.n_tables; ++j) {
-            const uint16_t* tab = reinterpret_cast<const uint16_t*>(wb + a.table_off[j]);
+            const uint16_t* tab = reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.table_off[j]));
             s += bf16_to_f32(tab[(uint64_t)row[j] * a.C + c]);
         }
         if (a.out) a.out[(uint64_t)t * a.C + c] = s;
@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d
         }
     }
     const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
-    const uint2* g = reinterpret_cast<const uint2*>(d->wbase + a.g_off);
-    const uint2* b = reinterpret_cast<const uint2*>(d->wbase + a.b_off);
+    const uint2* g = reinterpret_cast<const uint2*>(weight_ptr(*d, a.g_off));
+    const uint2* b = reinterpret_cast<const uint2*>(weight_ptr(*d, a.b_off));
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const uint32_t c = lane + 32u * j;
@@ -124,10 +124,11 @@ __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wai
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
-    const uint8_t* wb = d->wbase;
+    const uint8_t* wmat = weight_ptr(*d, a.w_off);
+    const uint16_t* bvec = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(*d, a.b_off)) : nullptr;
     const uint32_t k8n = a.K >> 3;
     for (uint32_t o = gwarp; o < a.N; o += nwarps) {
-        const uint4* wr = reinterpret_cast<const uint4*>(wb + a.w_off + (uint64_t)o * a.K * 2);
+        const uint4* wr = reinterpret_cast<const uint4*>(wmat + (uint64_t)o * a.K * 2);
         float acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0f;
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wai
 #pragma unroll
             for (int r = 0; r < R; ++r) v = (r == (int)lane) ? acc[r] : v;
             const uint64_t oi = (uint64_t)lane * a.N + o;
-            if (a.has_bias) v += bf16_to_f32(reinterpret_cast<const uint16_t*>(wb + a.b_off)[o]);
+            if (bvec) v += bf16_to_f32(bvec[o]);
             if (a.res) v += a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[oi])
                                        : reinterpret_cast<const float*>(a.res)[oi];
             v = apply_act(a.act, v);

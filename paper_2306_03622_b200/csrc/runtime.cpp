@@ -167,9 +167,11 @@ struct GraphKey {
     int cold, flags, order, engine;
     uint64_t chunk;
     uint32_t seed, ctas, extra;
+    uint64_t from = 0;   // first swapped store byte (partial caching: the cached prefix is skipped)
+    int64_t pext = -1;   // DMA graphs: prefix extent offset (baked address)
     bool operator<(const GraphKey& o) const {
-        return std::tie(cold, flags, order, engine, chunk, seed, ctas, extra) <
-               std::tie(o.cold, o.flags, o.order, o.engine, o.chunk, o.seed, o.ctas, o.extra);
+        return std::tie(cold, flags, order, engine, chunk, seed, ctas, extra, from, pext) <
+               std::tie(o.cold, o.flags, o.order, o.engine, o.chunk, o.seed, o.ctas, o.extra, o.from, o.pext);
     }
 };
 
@@ -194,10 +196,10 @@ struct Plan {  // one model on one GPU
     std::vector<int64_t> shadow_off;     // bf16 shadow of an f32 slot, or -1
     uint64_t ws_bytes = 0;
     std::map<GraphKey, cudaGraphExec_t> graphs;
-    std::map<std::tuple<uint64_t, int, uint32_t>, PieceSet> pieces;  // (chunk, order, seed)
-    std::map<std::pair<uint64_t, uint32_t>, DmaPlan> dma;            // (group bytes, streams)
+    std::map<std::tuple<uint64_t, int, uint32_t, uint64_t>, PieceSet> pieces;  // (chunk, order, seed, from)
+    std::map<std::tuple<uint64_t, uint32_t, uint64_t, uint64_t>, DmaPlan> dma;  // (group bytes, streams, from, split)
     // striped swap: source j of n gets every n-th piece; its table lives on the source's device
-    std::map<std::tuple<uint64_t, uint32_t, uint32_t, int>, PieceSet> stripe;  // (chunk, n, j, device)
+    std::map<std::tuple<uint64_t, uint32_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, n, j, device, from)
 };
 
 struct Model {
@@ -215,7 +217,12 @@ struct Model {
     uint64_t store_bytes = 0, store_alloc = 0;
     bool store_wc = false;
     // residency per GPU
-    std::vector<int64_t> extent;       // pool offset, or -1
+    std::vector<int64_t> extent;       // pool offset of the model (split = 0) or of its suffix, or -1
+    // partial-parameter caching: store bytes [0, split) — whole layers —
+    // live in a separate prefix extent that pool evictions keep (valid once its bytes landed)
+    uint64_t split = 0;
+    std::vector<int64_t> pextent;      // prefix extent per GPU, or -1
+    std::vector<uint8_t> pvalid;       // prefix bytes present
     std::vector<uint64_t> last_use;
     std::vector<std::unique_ptr<Plan>> plans;
     int inflight = 0;
@@ -746,6 +753,8 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
         }
     }
     m->extent.assign(c->gpus.size(), -1);
+    m->pextent.assign(c->gpus.size(), -1);
+    m->pvalid.assign(c->gpus.size(), 0);
     m->last_use.assign(c->gpus.size(), 0);
     m->plans.resize(c->gpus.size());
     std::lock_guard<std::mutex> lk(c->mu);
@@ -1040,17 +1049,20 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
 }
 
 // Swap pieces for one chunk size / order: execution order, never straddling a layer region.
-static fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint32_t seed, PieceSet** out) {
-    auto key = std::make_tuple(chunk, order, seed);
+static fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint32_t seed, uint64_t from,
+                             PieceSet** out) {
+    auto key = std::make_tuple(chunk, order, seed, from);
     auto it = p.pieces.find(key);
     if (it != p.pieces.end()) {
         *out = &it->second;
         return FSW_OK;
     }
     PieceSet ps;
-    for (uint32_t li = 0; li < m.layers.size(); ++li)
+    for (uint32_t li = 0; li < m.layers.size(); ++li) {
+        if (m.region_off[li] < from) continue;  // cached prefix
         for (uint64_t o = 0; o < m.region_bytes[li]; o += chunk)
             ps.host.push_back({m.region_off[li] + o, (uint32_t)std::min<uint64_t>(chunk, m.region_bytes[li] - o), li});
+    }
     if (order == FSW_ORDER_REVERSE) std::reverse(ps.host.begin(), ps.host.end());
     if (order == FSW_ORDER_RANDOM) {
         std::mt19937_64 rng(seed);
@@ -1067,12 +1079,12 @@ static fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int orde
 // Copy groups of the DMA engine: whole layers are merged in execution order until a group holds
 // at least `grp` bytes; a layer region larger than 2·grp is split into ≈grp pieces (256-B
 // aligned).  Layer regions are contiguous in the store, so groups tile [0, store_bytes).
-static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams) {
+static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams, uint64_t from, uint64_t split) {
     DmaPlan d;
     d.streams = streams;
     const size_t nl = m.layers.size();
     std::vector<uint32_t> last_group(nl, 0);
-    uint64_t lo = 0, hi = 0;  // open group [lo, hi)
+    uint64_t lo = from, hi = from;  // open group [lo, hi); groups tile [from, store_bytes)
     auto close = [&]() {
         if (hi > lo) {
             d.groups.push_back({lo, hi, (uint32_t)(d.groups.size() % streams)});
@@ -1087,7 +1099,8 @@ static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams) {
     auto want = [&](uint64_t at) { return std::min(grp, std::max(tail_min, align_up((total - at) / 2, 256))); };
     for (size_t li = 0; li < nl; ++li) {
         const uint64_t ro = m.region_off[li], rb = m.region_bytes[li];
-        if (!rb) continue;
+        if (!rb || ro < from) continue;
+        if (ro == split) close();  // a group never straddles the prefix / suffix extents
         if (rb > 2 * want(ro)) {
             close();
             for (uint64_t o = 0; o < rb;) {
@@ -1106,18 +1119,18 @@ static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams) {
     close();
     d.target.assign(nl, {});
     for (size_t li = 0; li < nl; ++li) {
-        if (!m.region_bytes[li]) continue;
+        if (!m.region_bytes[li] || m.region_off[li] < from) continue;
         const uint32_t gl = last_group[li];
         for (uint32_t j = 0; j < streams; ++j) d.target[li][j] = gl >= j ? (gl - j) / streams + 1 : 0;
     }
     return d;
 }
 
-static const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams) {
-    const auto key = std::make_pair(grp, streams);
+static const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams, uint64_t from) {
+    const auto key = std::make_tuple(grp, streams, from, m.split);
     auto it = p.dma.find(key);
     if (it != p.dma.end()) return it->second;
-    return p.dma.emplace(key, make_dma_plan(m, grp, streams)).first->second;
+    return p.dma.emplace(key, make_dma_plan(m, grp, streams, from, m.split)).first->second;
 }
 
 // Host-only inspection of the DMA engine's copy plan (tests; no GPU needed).
@@ -1128,7 +1141,7 @@ extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group
     if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
     if (!n_groups || group_bytes == 0 || group_bytes % 256 || streams == 0 || streams > (uint32_t)kMaxWaitSrc)
         return fail(FSW_EINVAL, "dma_plan: bad argument");
-    const DmaPlan d = make_dma_plan(*m, group_bytes, streams);
+    const DmaPlan d = make_dma_plan(*m, group_bytes, streams, 0, m->split);
     *n_groups = (uint32_t)d.groups.size();
     if (d.groups.size() > cap_groups) return fail(FSW_EINVAL, "dma_plan: %zu groups > cap %u", d.groups.size(), cap_groups);
     for (size_t i = 0; i < d.groups.size(); ++i) {
@@ -1150,9 +1163,11 @@ struct InvokeCfg {
     uint64_t chunk;
     int order;
     uint32_t seed, ctas;
-    uint8_t* wbase;              // only used by DMA graphs (memcpy nodes need absolute addresses)
+    DevDesc dst;                 // the target's extents (DMA graphs bake these addresses)
     const DmaPlan* dma_plan;     // DMA engine only
-    const uint8_t* src = nullptr; // DMA: copy source (host store, or a peer GPU's extent)
+    DevDesc src{};               // DMA: copy source extents (a peer GPU's), unless src_host
+    bool src_host = true;        // DMA: copy from the pinned host store
+    uint64_t from = 0;           // first swapped store byte (a cached prefix is skipped)
     bool striped = false;        // striped swap: sources launched outside the graph (fsw_invoke_ex)
     uint32_t local_ctas = 0;     // striped: swap CTAs running on the target GPU itself (gate)
 };
@@ -1160,8 +1175,9 @@ struct InvokeCfg {
 // Striped swap: the execution-order piece list of the SM engine dealt round-robin to n sources
 // (piece q goes to source q mod n), so every source streams a share of every layer and all of them
 // advance through the model together; source j's table is allocated on source j's device.
-static fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, PieceSet** out) {
-    const auto key = std::make_tuple(chunk, n, j, dev);
+static fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, uint64_t from,
+                                    PieceSet** out) {
+    const auto key = std::make_tuple(chunk, n, j, dev, from);
     auto it = p.stripe.find(key);
     if (it != p.stripe.end()) {
         *out = &it->second;
@@ -1170,7 +1186,7 @@ static fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t 
     PieceSet ps;
     uint64_t q = 0;
     for (uint32_t li = 0; li < m.layers.size(); ++li)
-        for (uint64_t o = 0; o < m.region_bytes[li]; o += chunk, ++q)
+        for (uint64_t o = 0; m.region_off[li] >= from && o < m.region_bytes[li]; o += chunk, ++q)
             if (q % n == j) ps.host.push_back({m.region_off[li] + o, (uint32_t)std::min<uint64_t>(chunk, m.region_bytes[li] - o), li});
     CU(cudaSetDevice(dev));
     if (!ps.host.empty()) {
@@ -1187,7 +1203,7 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
         Wait w{};
         w.ctl = g.ctl;
         w.layer = x.layer;
-        if (ic.cold && m.region_bytes[x.layer] > 0) {
+        if (ic.cold && m.region_bytes[x.layer] > 0 && m.region_off[x.layer] >= ic.from) {
             if (ic.engine == FSW_ENGINE_SM) {
                 w.n = 1;
                 w.ready[0] = g.ready + x.layer;
@@ -1228,7 +1244,7 @@ static PFN_writeValue32 get_write_value32() {
 static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out) {
     PieceSet* ps = nullptr;
     if (ic.cold && ic.engine == FSW_ENGINE_SM && !ic.striped) {
-        fsw_status s = get_pieces(m, p, g, ic.chunk, ic.order, ic.seed, &ps);
+        fsw_status s = get_pieces(m, p, g, ic.chunk, ic.order, ic.seed, ic.from, &ps);
         if (s != FSW_OK) return s;
         if (m.layers.size() > g.ready_cap) return fail(FSW_EINVAL, "too many layers");
     }
@@ -1246,7 +1262,7 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
         cudaStreamWaitEvent(sc, g.evfork, 0);
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
         if (ic.engine == FSW_ENGINE_SM) {
-            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, nullptr, reinterpret_cast<const DevDesc*>(g.dstage),
+            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, DevDesc{}, reinterpret_cast<const DevDesc*>(g.dstage),
                         ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl, g.ctl, 0);
         } else {
             // Copy-engine DMA from the pinned store (the paper's transfer) in
@@ -1262,7 +1278,8 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
             uint32_t cnt[kMaxWaitSrc] = {};
             for (const auto& gr : dp.groups) {
                 cudaStream_t sj = g.sd[gr.stream];
-                cudaMemcpyAsync(ic.wbase + gr.lo, ic.src + gr.lo, gr.hi - gr.lo, cudaMemcpyDefault, sj);
+                const uint8_t* from_ptr = ic.src_host ? m.store + gr.lo : weight_ptr(ic.src, gr.lo);
+                cudaMemcpyAsync(weight_ptr(ic.dst, gr.lo), from_ptr, gr.hi - gr.lo, cudaMemcpyDefault, sj);
                 wv(sj, (CUdeviceptr)(g.progress + 32 * gr.stream), (cuuint32_t)(++cnt[gr.stream]), 0);
             }
             for (uint32_t j = 1; j < dp.streams; ++j) {
@@ -1321,23 +1338,40 @@ extern "C" fsw_status fsw_model_is_heavy(fsw_ctx* c, uint32_t id, int32_t* heavy
     return FSW_OK;
 }
 
-static void invalidate(fsw_ctx* c, Model& m, int gi) {
-    if (m.extent[gi] < 0) return;
-    fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.extent[gi]);
-    m.extent[gi] = -1;
+// Eviction invalidates, it never copies back.  The suffix (or whole model)
+// extent goes; with keep_prefix a cached prefix stays (partial caching), else it goes too.
+static void invalidate(fsw_ctx* c, Model& m, int gi, bool keep_prefix = false) {
+    if (m.extent[gi] >= 0) {
+        fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.extent[gi]);
+        m.extent[gi] = -1;
+    }
+    if (!keep_prefix && m.pextent[gi] >= 0) {
+        fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.pextent[gi]);
+        m.pextent[gi] = -1;
+        m.pvalid[gi] = 0;
+    }
 }
 
-// Allocate an extent for m on GPU gi, evicting idle LRU models there.
+// Pool extents for a cold invoke of m on GPU gi: the suffix (or the whole model), plus the prefix
+// when m caches one that is not here yet.  Makes room by evicting idle models, heaviness-aware LRU
+// (PAPER.md:885-897): their suffixes / whole extents first (cached prefixes survive), and only
+// then cached prefixes, least recently used first.
 static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
     Gpu& g = c->gpus[gi];
+    const uint64_t need_p = m.split && m.pextent[gi] < 0 ? m.split : 0, need_s = m.store_bytes - m.split;
     for (;;) {
-        uint64_t off = 0;
-        if (fsw_arena_alloc(g.arena, m.store_bytes, &off) == FSW_OK) {
-            m.extent[gi] = (int64_t)off;
-            return FSW_OK;
+        uint64_t po = 0, so = 0;
+        if (need_p == 0 || fsw_arena_alloc(g.arena, need_p, &po) == FSW_OK) {
+            if (fsw_arena_alloc(g.arena, need_s, &so) == FSW_OK) {
+                if (need_p) {
+                    m.pextent[gi] = (int64_t)po;
+                    m.pvalid[gi] = 0;
+                }
+                m.extent[gi] = (int64_t)so;
+                return FSW_OK;
+            }
+            if (need_p) fsw_arena_free(g.arena, po);
         }
-        // heaviness-aware LRU: light models and heavy ones with copies on other
-        // GPUs go first, sole-copy heavy models last; LRU within each group
         std::vector<Model*> cand;
         std::vector<uint8_t> heavy, in_use;
         std::vector<uint32_t> copies;
@@ -1353,35 +1387,66 @@ static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
             in_use.push_back(o->inflight != 0);
         }
         const std::vector<uint32_t> order = eviction_order(heavy, copies, last, in_use);
-        Model* victim = order.empty() ? nullptr : cand[order[0]];
-        if (!victim)
+        if (!order.empty()) {
+            invalidate(c, *cand[order[0]], gi, /*keep_prefix=*/true);
+            g.n_evictions++;
+            continue;
+        }
+        Model* pv = nullptr;  // then the least recently used idle cached prefix
+        for (auto& o : c->models)
+            if (o && o.get() != &m && o->pextent[gi] >= 0 && o->extent[gi] < 0 && o->inflight == 0 &&
+                (!pv || o->last_use[gi] < pv->last_use[gi]))
+                pv = o.get();
+        if (!pv)
             return fail(FSW_ENOMEM, "pool on gpu %d cannot hold %llu bytes even after evicting every idle model", g.dev,
-                        (unsigned long long)m.store_bytes);
-        invalidate(c, *victim, gi);
+                        (unsigned long long)(need_p + need_s));
+        invalidate(c, *pv, gi);
         g.n_evictions++;
     }
 }
 
-extern "C" fsw_status fsw_evict(fsw_ctx* c, uint32_t id, int32_t gpu) {
+// Partial-parameter caching (the paper's future work).
+extern "C" fsw_status fsw_model_set_cache_prefix(fsw_ctx* c, uint32_t id, uint64_t bytes, uint64_t* actual) {
+    if (!c) return fail(FSW_EINVAL, "NULL ctx");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    for (size_t i = 0; i < m->extent.size(); ++i)
+        if (m->extent[i] >= 0 || m->pextent[i] >= 0)
+            return fail(FSW_ESTATE, "model %u is resident on gpu %zu: evict it before changing its cached prefix", id, i);
+    // the largest layer boundary <= bytes that leaves a non-empty suffix
+    uint64_t split = 0;
+    for (size_t li = 0; li < m->layers.size(); ++li)
+        if (m->region_off[li] <= bytes && m->region_off[li] < m->store_bytes) split = m->region_off[li];
+    m->split = split;  // graphs and copy plans are keyed by the swapped range and the split
+    if (actual) *actual = split;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_evict_ex(fsw_ctx* c, uint32_t id, int32_t gpu, uint32_t flags) {
     if (!c) return fail(FSW_EINVAL, "NULL ctx");
     std::lock_guard<std::mutex> lk(c->mu);
     Model* m = find_model(c, id);
     if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
     if (m->inflight) return fail(FSW_EBUSY, "model %u has an invoke in flight", id);
     if (gpu >= (int)c->gpus.size() || gpu < -1) return fail(FSW_EINVAL, "bad gpu %d", gpu);
+    const bool keep = (flags & FSW_EVICT_KEEP_PREFIX) != 0;
     if (gpu >= 0) {
-        if (m->extent[gpu] < 0) return fail(FSW_ESTATE, "model %u is not resident on gpu %d", id, gpu);
-        invalidate(c, *m, gpu);
+        if (m->extent[gpu] < 0 && (keep || m->pextent[gpu] < 0))
+            return fail(FSW_ESTATE, "model %u is not resident on gpu %d", id, gpu);
+        invalidate(c, *m, gpu, keep);
         c->gpus[gpu].n_evictions++;
         return FSW_OK;
     }
     for (size_t i = 0; i < c->gpus.size(); ++i)
-        if (m->extent[i] >= 0) {
-            invalidate(c, *m, (int)i);
+        if (m->extent[i] >= 0 || (!keep && m->pextent[i] >= 0)) {
+            invalidate(c, *m, (int)i, keep);
             c->gpus[i].n_evictions++;
         }
     return FSW_OK;
 }
+
+extern "C" fsw_status fsw_evict(fsw_ctx* c, uint32_t id, int32_t gpu) { return fsw_evict_ex(c, id, gpu, 0); }
 
 extern "C" fsw_status fsw_unregister_model(fsw_ctx* c, uint32_t id) {
     if (!c) return fail(FSW_EINVAL, "NULL ctx");
@@ -1407,8 +1472,10 @@ extern "C" fsw_status fsw_pool_stats_get(fsw_ctx* c, int32_t gpu, fsw_pool_stats
     memset(out, 0, sizeof *out);
     out->capacity = g.pool_bytes;
     fsw_arena_stats(g.arena, &out->used, &out->largest_free, &out->n_extents);
-    for (auto& m : c->models)
+    for (auto& m : c->models) {
         if (m && m->extent[gpu] >= 0) out->n_resident++;
+        if (m && m->pextent[gpu] >= 0 && m->pvalid[gpu]) out->prefix_bytes_cached += m->split;
+    }
     out->n_evictions = g.n_evictions;
     out->bytes_swapped_total = g.bytes_swapped_total;
     out->n_invokes_cold = g.n_cold;
@@ -1447,6 +1514,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     bool cold = false;
     std::vector<int> srcs;          // striped swap sources (pool GPU indices), empty = not striped
     int peer = -1;                  // GPU->GPU swap source (pool GPU index), -1 = from the host
+    bool pcached = false;           // the model's cached prefix is already on the target
     std::vector<SrcSlot*> slots;    // their swap-kernel slots
     {
         std::unique_lock<std::mutex> lk(c->mu);
@@ -1457,8 +1525,18 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         if (o.gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "invoke: bad gpu %d", o.gpu);
         Decision dec;
         for (;;) {
-            if (o.gpu >= 0) gi = c->gpus[o.gpu].busy ? -1 : o.gpu;
-            else gi = (dec = pick_gpu(c, *m)).gpu;
+            if (o.gpu >= 0) {
+                gi = c->gpus[o.gpu].busy ? -1 : o.gpu;
+            } else {
+                gi = (dec = pick_gpu(c, *m)).gpu;
+                // a host swap prefers an idle GPU that still caches the model's prefix (NEXT #4)
+                if (dec.kind == 1 && m->split)
+                    for (int i = 0; i < (int)c->gpus.size(); ++i)
+                        if (!c->gpus[i].busy && m->pvalid[i] && m->pextent[i] >= 0) {
+                            gi = i;
+                            break;
+                        }
+            }
             if (gi >= 0) break;
             c->cv.wait(lk);
         }
@@ -1466,6 +1544,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         g.busy = true;
         m->inflight++;
         cold = m->extent[gi] < 0;
+        pcached = cold && m->split && m->pextent[gi] >= 0 && m->pvalid[gi];
         if (cold) {
             fsw_status s = ensure_extent(c, *m, gi);
             if (s != FSW_OK) {
@@ -1565,18 +1644,25 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     const uint32_t dstr = baseline ? 1u : o.dma_streams ? o.dma_streams : c->cfg.dma_streams;
     if (engine > FSW_ENGINE_DMA || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
         return finish(fail(FSW_EINVAL, "invoke: bad engine / dma_group_bytes / dma_streams"));
+    auto extents = [&](int i) {  // the model's extents on pool GPU i
+        return DevDesc{c->gpus[i].pool + (m->pextent[i] >= 0 ? m->pextent[i] : 0), c->gpus[i].pool + m->extent[i], m->split, 0};
+    };
     InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
-                 o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, g.pool + (m->extent[gi] >= 0 ? m->extent[gi] : 0), nullptr};
+                 o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, extents(gi), nullptr};
+    ic.from = pcached ? m->split : 0;
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
-    if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr);
-    ic.src = peer >= 0 ? c->gpus[peer].pool + m->extent[peer] : m->store;
+    if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr, ic.from);
+    if (peer >= 0) {
+        ic.src = extents(peer);
+        ic.src_host = false;
+    }
     const bool sm = engine == FSW_ENGINE_SM;
     // striped: every source claims pieces of >= 256 KiB (one system-scope fence + release each)
     const uint64_t schunk = std::max<uint64_t>(ic.chunk, 256ull << 10);
     std::vector<PieceSet*> sps(srcs.size(), nullptr);
     for (size_t j = 0; j < srcs.size(); ++j) {
-        st = get_stripe_pieces(*m, p, schunk, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, &sps[j]);
+        st = get_stripe_pieces(*m, p, schunk, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &sps[j]);
         if (st != FSW_OK) return finish(st);
     }
     if (striped) {
@@ -1587,11 +1673,13 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     GraphKey key{cold, (int)(flags & FSW_NO_OVERLAP), cold && sm && !striped ? ic.order : 0, cold ? engine + (striped ? 8 : 0) : 0,
                  cold && !striped ? (sm ? ic.chunk : dgrp) : 0, cold && sm && !striped ? ic.seed : 0,
                  cold ? (striped ? ic.local_ctas : sm ? ic.ctas : dstr) : 0, 0};
-    if (cold && !sm) {  // DMA graphs bake addresses: the target extent and a peer source's extent
+    key.from = cold ? ic.from : 0;
+    if (cold && !sm) {  // DMA graphs bake addresses: the target extents and a peer source's extents
         key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);
+        key.pext = m->pextent[gi];
         if (peer >= 0) {
             key.order = peer + 1;
-            key.seed = (uint32_t)((uint64_t)m->extent[peer] >> 16);
+            key.seed = (uint32_t)((uint64_t)m->extent[peer] >> 16) ^ (uint32_t)((uint64_t)(m->pextent[peer] + 1) << 8);
         }
     }
     auto it = p.graphs.find(key);
@@ -1604,7 +1692,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         exec = it->second;
     }
     // stage: descriptor + input (pinned), one H2D node in the graph
-    DevDesc dd{g.pool + m->extent[gi], ++g.generation};
+    DevDesc dd = ic.dst;
+    dd.generation = ++g.generation;
     memcpy(g.hstage, &dd, sizeof dd);
     memcpy(g.hstage + kStageHdr, input, input_bytes);
     cudaEventRecord(g.ev0, g.sx);
@@ -1613,7 +1702,6 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         // Reset the target's counters, then every source loads its share of the pieces over its own
         // host link and stores it into the target's extent (peer stores over NVLink for remote
         // sources), releasing each piece on the target's layer counter at system scope.
-        uint8_t* ext = g.pool + m->extent[gi];
         cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m->layers.size(), g.sx);
         cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), g.sx);
         cudaEventRecord(g.evs0, g.sx);
@@ -1625,7 +1713,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             cudaStreamWaitEvent(sl.st, g.evfork, 0);
             cudaMemsetAsync(sl.ctl, 0, sizeof(DevCtl), sl.st);
             // an empty share still starts its CTAs: the target's gate counts every source kernel
-            launch_swap(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->store, ext, nullptr, sps[j]->dev,
+            launch_swap(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->store, ic.dst, nullptr, sps[j]->dev,
                         (uint32_t)sps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1);
             cudaEventRecord(sl.done, sl.st);
         }
@@ -1660,8 +1748,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             float swap_ms = 0;
             cudaEventElapsedTime(&swap_ms, g.evs0, g.evs1);
             stats->swap_ms = swap_ms;
-            stats->bytes_swapped = m->store_bytes;
-            stats->link_gbps = swap_ms > 0 ? m->store_bytes / (swap_ms * 1e6) : 0;
+            stats->bytes_swapped = m->store_bytes - ic.from;
+            stats->link_gbps = swap_ms > 0 ? stats->bytes_swapped / (swap_ms * 1e6) : 0;
             stats->engine = (uint32_t)engine;
             if (striped) {
                 float tail = 0;
@@ -1675,7 +1763,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                 if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
                 stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)
                 PieceSet* ps = nullptr;
-                if (get_pieces(*m, p, g, ic.chunk, ic.order, ic.seed, &ps) == FSW_OK) stats->n_copies = (uint32_t)ps->host.size();
+                if (get_pieces(*m, p, g, ic.chunk, ic.order, ic.seed, ic.from, &ps) == FSW_OK) stats->n_copies = (uint32_t)ps->host.size();
             } else {
                 float tail = 0;
                 cudaEventElapsedTime(&tail, g.evs1, g.ev1);
@@ -1691,7 +1779,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         cudaEventElapsedTime(&dms, g.ev0, g.ev1);
         if (cold) {
             g.n_cold++;
-            g.bytes_swapped_total += m->store_bytes;
+            g.bytes_swapped_total += m->store_bytes - ic.from;
+            if (m->split) m->pvalid[gi] = 1;  // the prefix bytes have landed
             if (peer < 0 && !striped) {
                 m->cold_ms_sum += dms;
                 m->n_cold_runs++;
@@ -1723,7 +1812,10 @@ extern "C" fsw_status fsw_debug_read_resident(fsw_ctx* c, uint32_t id, int32_t g
     if (m->extent[gpu] < 0) return fail(FSW_ESTATE, "model %u not resident on gpu %d", id, gpu);
     if (cap < m->store_bytes) return fail(FSW_EINVAL, "read_resident: cap too small");
     CU(cudaSetDevice(c->gpus[gpu].dev));
-    CU(cudaMemcpy(dst, c->gpus[gpu].pool + m->extent[gpu], m->store_bytes, cudaMemcpyDeviceToHost));
+    uint8_t* pool = c->gpus[gpu].pool;
+    if (m->split) CU(cudaMemcpy(dst, pool + m->pextent[gpu], m->split, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(static_cast<uint8_t*>(dst) + m->split, pool + m->extent[gpu], m->store_bytes - m->split,
+                  cudaMemcpyDeviceToHost));
     return FSW_OK;
 }
 

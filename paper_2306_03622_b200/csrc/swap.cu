@@ -13,11 +13,11 @@
 namespace fsw {
 
 template <int U>
-__global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, uint8_t* dst, const DevDesc* __restrict__ desc,
+__global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, DevDesc dst, const DevDesc* __restrict__ desc,
                                               const Piece* __restrict__ pieces, uint32_t n_pieces,
                                               uint32_t* __restrict__ ready, DevCtl* __restrict__ own, DevCtl* gate, int sys) {
     if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
-    uint8_t* const wbase = dst ? dst : desc->wbase;
+    const DevDesc dd = desc ? *desc : dst;
     const uint32_t lane = threadIdx.x & 31u;
     for (;;) {
         uint32_t p = 0;
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
         if (p == 0 && lane == 0) own->t_first = globaltimer();
         const Piece pc = pieces[p];
         const uint4* src = reinterpret_cast<const uint4*>(host + pc.off);
-        uint4* out = reinterpret_cast<uint4*>(wbase + pc.off);
+        uint4* out = reinterpret_cast<uint4*>(weight_ptr(dd, pc.off));
         const uint32_t n16 = pc.bytes >> 4;
         uint32_t i = lane;
         for (; i + (U - 1) * 32 < n16; i += U * 32) {
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
     }
 }
 
-void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, uint8_t* dst, const DevDesc* desc,
+void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, DevDesc dst, const DevDesc* desc,
                  const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys) {
     k_swap<8><<<ctas, threads, 0, s>>>(host_mapped, dst, desc, pieces, n_pieces, ready, own, gate, sys);
 }

@@ -22,6 +22,7 @@ NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP = 0x1, 0x2, 0x4, 0x8,
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
 ENGINE_AUTO, ENGINE_SM, ENGINE_DMA = 0, 1, 2
+EVICT_KEEP_PREFIX = 0x1
 
 u32, u64, i32, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -90,7 +91,7 @@ class InvokeOpts(ctypes.Structure):
 class PoolStats(ctypes.Structure):
     _fields_ = [("capacity", u64), ("used", u64), ("largest_free", u64), ("n_resident", u32), ("n_extents", u32),
                 ("n_evictions", u64), ("bytes_swapped_total", u64), ("n_invokes_cold", u64),
-                ("n_invokes_warm", u64)]
+                ("n_invokes_warm", u64), ("prefix_bytes_cached", u64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -136,7 +137,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_arena_stats", "fsw_debug_dma_plan", "fsw_policy_rrc", "fsw_policy_partition", "fsw_policy_alpha",
            "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
-           "fsw_function_stats_get", "fsw_sched_stats_get"]
+           "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix"]
 
 _lib = None
 
@@ -160,6 +161,8 @@ def lib():
         L.fsw_invoke.argtypes = [vp, u32, vp, u64, vp, u64, ctypes.POINTER(InvokeStats)]
         L.fsw_invoke_ex.argtypes = [vp, u32, ctypes.POINTER(InvokeOpts), vp, u64, vp, u64, ctypes.POINTER(InvokeStats)]
         L.fsw_evict.argtypes = [vp, u32, i32]
+        L.fsw_evict_ex.argtypes = [vp, u32, i32, u32]
+        L.fsw_model_set_cache_prefix.argtypes = [vp, u32, u64, ctypes.POINTER(u64)]
         L.fsw_pool_stats_get.argtypes = [vp, i32, ctypes.POINTER(PoolStats)]
         L.fsw_n_gpus.argtypes = [vp, ctypes.POINTER(u32)]
         L.fsw_debug_read_resident.argtypes = [vp, u32, i32, vp, u64]
@@ -361,8 +364,14 @@ class Runtime:
         _check(lib().fsw_model_is_heavy(self.h, mid, ctypes.byref(h)))
         return bool(h.value)
 
-    def evict(self, mid: int, gpu: int = -1):
-        _check(lib().fsw_evict(self.h, mid, gpu))
+    def evict(self, mid: int, gpu: int = -1, keep_prefix: bool = False):
+        _check(lib().fsw_evict_ex(self.h, mid, gpu, EVICT_KEEP_PREFIX if keep_prefix else 0))
+
+    def set_cache_prefix(self, mid: int, nbytes: int) -> int:
+        """Partial-parameter caching: returns the prefix bytes actually kept (a layer boundary)."""
+        a = u64()
+        _check(lib().fsw_model_set_cache_prefix(self.h, mid, nbytes, ctypes.byref(a)))
+        return a.value
 
     def pool_stats(self, gpu: int = 0) -> dict:
         p = PoolStats()
