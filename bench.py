@@ -100,6 +100,17 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def max_over_ranks(local: dict, world: int) -> dict:
+    """Every rank contributes its timings; all get the per-key maximum (the slowest rank decides a
+    latency; the driver's rule for multi-GPU numbers)."""
+    if world <= 1:
+        return dict(local)
+    import torch.distributed as dist
+    g = [None] * world
+    dist.all_gather_object(g, local)
+    return {k: max(r[k] for r in g) for k in local}
+
+
 def cpu_oracle_timing(spec, w, x, budget_s: float, max_reps: int = 50):
     """Time the oracle (tests-only package) as it stands on the host cores: bounded sample."""
     import oracle
@@ -247,13 +258,8 @@ def run_fsw(args):
     except Exception:
         dma = None
     p50 = percentile(dev, 50)
-    local_res = {"p50": p50, "p99": percentile(dev, 99), "wall_s": wall}
-    if world > 1:
-        import torch.distributed as dist
-        g = [None] * world
-        dist.all_gather_object(g, local_res)
-        p50 = max(r["p50"] for r in g)
-        wall = max(r["wall_s"] for r in g)
+    agg = max_over_ranks({"p50": p50, "p99": percentile(dev, 99), "wall_s": wall}, world)
+    p50, wall = agg["p50"], agg["wall_s"]
     if rank != 0:
         rt.close()
         return
@@ -332,6 +338,16 @@ def run_fsw(args):
     rt.close()
 
 
+STRIPED_BARRIERS = 3  # rank 0 of run_striped: after warm-up, after the timed steps, at exit
+
+
+def striped_follower():
+    """Ranks other than 0 in striped mode: no GPU work, only rank 0's barriers."""
+    import torch.distributed as dist
+    for _ in range(STRIPED_BARRIERS):
+        dist.barrier()
+
+
 def run_striped(args):
     """N > 1: one cold invoke of the workload striped over the host links of all N GPUs (SURVEY
     §8a a5): every GPU loads a round-robin share of each layer's pieces from the pinned store over
@@ -345,9 +361,7 @@ def run_striped(args):
     rank, world, _ = dist_env()
     dist.init_process_group("gloo")
     if rank != 0:
-        dist.barrier()
-        dist.barrier()
-        dist.barrier()
+        striped_follower()
         return
     spec = synth.build_model(args.model)
     w = spec.build_weights()

@@ -36,7 +36,7 @@ namespace fsw {
 
 #ifdef FSW_GEMM_TIMING  // tools/gemm_bench.cu only: per-CTA phase stamps
 __device__ unsigned long long g_gemm_stamp[1024][6];
-#define STAMP(i) do { if (threadIdx.x == 0 || (i) == 2) g_gemm_stamp[(blockIdx.x * gridDim.y + blockIdx.y) & 1023][i] = globaltimer(); } while (0)
+#define STAMP(i) do { if (threadIdx.x == 0) g_gemm_stamp[((blockIdx.z * gridDim.x + blockIdx.x) * gridDim.y + blockIdx.y) & 1023][i] = globaltimer(); } while (0)
 #else
 #define STAMP(i) do { } while (0)
 #endif
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(128, 1)
                 load_w(st);
                 load_a(st);
             }
+            STAMP(2);
         }
         __syncwarp();
     } else if (warp == 1) {

@@ -1,10 +1,14 @@
 // Standalone timing of the tcgen05 GEMM kernel over (BN, split-K) for the batch-1 shapes of the
 // paper's models (tools only; feeds the cost model of runtime.cpp: choose_tiling).
 // Back-to-back PDL launches timed with CUDA events, like consecutive layers of an invoke graph.
+#ifdef PHASES
+#define FSW_GEMM_TIMING 1
+#endif
 #include "../paper_2306_03622_b200/csrc/gemm_tc.cu"
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <vector>
 using namespace fsw;
 
@@ -61,6 +65,29 @@ int main(int argc, char** argv) {
                 printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
                        sh.K, sh.N, bn, S, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
                 if (us < best) { best = us; bb = bn; bs = S; }
+#ifdef PHASES
+                // one isolated launch: per-CTA %globaltimer stamps -> mean phase durations
+                cudaDeviceSynchronize();
+                launch_gemm(s, dd, w, &tm, a);
+                cudaDeviceSynchronize();
+                static unsigned long long st[1024][6];
+                cudaMemcpyFromSymbol(st, g_gemm_stamp, sizeof st);
+                uint32_t nct = ctas > 1024 ? 1024 : ctas;
+                unsigned long long t0 = ~0ull, t1 = 0;
+                double ph[5] = {0};
+                uint32_t nfull = 0;
+                for (uint32_t c = 0; c < nct; ++c) {
+                    t0 = std::min(t0, st[c][0]);
+                    t1 = std::max(t1, st[c][5]);
+                    if (st[c][5] == 0) continue;  // split-K CTAs that were not last skip stamp 5
+                    ++nfull;
+                    for (int p = 0; p < 5; ++p) ph[p] += (double)(st[c][p + 1] - st[c][p]);
+                }
+                if (nfull)
+                    printf("    phases (us, mean over %u CTAs): setup %.2f  mainloop-issue %.2f  mma-done %.2f  tmem->smem %.2f  epilogue %.2f  | span %.2f\n",
+                           nfull, ph[0] / nfull / 1e3, ph[1] / nfull / 1e3, ph[2] / nfull / 1e3, ph[3] / nfull / 1e3,
+                           ph[4] / nfull / 1e3, (t1 - t0) / 1e3);
+#endif
             }
         }
         printf("  BEST %-18s BN=%d S=%u %.2f us\n", sh.name, bb, bs, best);
