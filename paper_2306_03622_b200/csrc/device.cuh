@@ -4,6 +4,8 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <utility>
+
 #include "kernels.h"
 
 namespace fsw {
@@ -122,23 +124,34 @@ __device__ __forceinline__ float warp_max(float v) {
 // programmatic edge.
 enum PdlKind { PDL_GEMM = 1, PDL_LN = 2, PDL_ATTN = 4, PDL_EMBED = 8, PDL_GEMV = 16, PDL_IM2COL = 32, PDL_POOL = 64 };
 template <typename... KArgs, typename... Args>
-static void launch_pdl(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args&&... args) {
+static void launch_pdl_cluster(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                               dim3 cluster, Args&&... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cluster.x;
+    attr[1].val.clusterDim.y = cluster.y;
+    attr[1].val.clusterDim.z = cluster.z;
     cfg.attrs = attr;
     // FSW_PDL_MASK = kinds launched with PDL (A/B switch of tools/pdl_ab.sh).  Default: all but
     // attention — launched early behind the QKV GEMM it cost ~19 us per layer on BERT-base
     // (profiles/r01/pdl_ab.txt); every other kind gains or is neutral.
     static const int mask = getenv("FSW_PDL_MASK") ? atoi(getenv("FSW_PDL_MASK")) : (0x7f & ~PDL_ATTN);
-    cfg.numAttrs = (mask & kind) ? 1 : 0;
+    const bool pdl = (mask & kind) != 0, clustered = cluster.x * cluster.y * cluster.z > 1;
+    if (!pdl) cfg.attrs = attr + 1;
+    cfg.numAttrs = (pdl ? 1 : 0) + (clustered ? 1 : 0);
     cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    launch_pdl_cluster(kind, kernel, grid, block, smem, s, dim3(1, 1, 1), std::forward<Args>(args)...);
 }
 
 }  // namespace fsw

@@ -80,6 +80,28 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
+// A slice broadcast to every CTA of the cluster in `mask` (same smem offset, each CTA's barrier).
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(bar)),
+                 "h"(mask)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -137,8 +159,10 @@ struct Cfg {
 
 }  // namespace
 
+constexpr int kGemmThreads = 512;  // warp 0 TMA producer, warp 1 MMA issuer, all 16 in the epilogue
+
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
     using C = Cfg<BN>;
     constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
@@ -158,12 +182,18 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t nkt = min(a.K / kBK, kt_begin + a.kt_per) - kt_begin;  // >= 1 (host plan)
     const uint32_t nst = (nkt + C::kSub - 1) / C::kSub;                   // pipeline steps
     const uint32_t a_bytes = a.conv ? a.Hb * a.Q * (kBK * 2) : C::kA;    // TMA box bytes
+    // A multicast over a cluster of mc CTAs along N: CTA r loads rows [r·128/mc, (r+1)·128/mc) of
+    // every A sub-tile and broadcasts them to the whole cluster; a stage is free again only when
+    // all mc CTAs' MMAs have read it (empty barriers count mc multicast commits).
+    const uint32_t mc = a.mc > 1 ? a.mc : 1;
+    const uint32_t crank = mc > 1 ? cluster_ctarank() : 0;
+    const uint16_t cmask = (uint16_t)((1u << mc) - 1u);
     STAMP(0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], mc);
         }
         mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -176,7 +206,8 @@ __global__ void __launch_bounds__(128, 1)
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
+    if (mc > 1) cluster_sync();  // every CTA's barriers exist before any multicast lands
+    else __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     STAMP(1);
@@ -208,6 +239,10 @@ __global__ void __launch_bounds__(128, 1)
                         const uint32_t tap = kk / a.Cin, c0 = kk - tap * a.Cin, r = tap / a.S, sx = tap - r * a.S;
                         tma_load_4d(sa + j * C::kA, &tmA, (int)c0, (int)sx - (int)a.pad,
                                     (int)(blockIdx.x * a.Hb * a.stride + r) - (int)a.pad, 0, &full[s]);
+                    } else if (mc > 1) {
+                        const uint32_t rows = kBM / mc;
+                        tma_load_2d_mc(sa + j * C::kA + crank * rows * (kBK * 2), &tmA, (int)kk, (int)(m0 + crank * rows),
+                                       &full[s], cmask);
                     } else {
                         tma_load_2d(sa + j * C::kA, &tmA, (int)kk, (int)m0, &full[s]);
                     }
@@ -248,7 +283,8 @@ __global__ void __launch_bounds__(128, 1)
                         umma_f16(tmem, ad, bd, idesc, (st | j | kk) != 0);
                     }
                 }
-                umma_commit(&empty[s]);
+                if (mc > 1) umma_commit_mc(&empty[s], cmask);
+                else umma_commit(&empty[s]);
             }
             umma_commit(done);
         }
@@ -264,10 +300,11 @@ __global__ void __launch_bounds__(128, 1)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float* ct = reinterpret_cast<float*>(smem);
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    // warp w reads TMEM lanes 32·(w mod 4) (its lane quarter) and every (w / 4)-th 32-column block
+    for (int c0 = 32 * (int)(warp >> 2); c0 < BN; c0 += 32 * (kGemmThreads / 128)) {
         uint32_t r[32];
-        tmem_ld32(tmem + ((warp * 32u) << 16) + (uint32_t)c0, r);
-        float4* dst = reinterpret_cast<float4*>(ct + (warp * 32 + lane) * C::kLdc + c0);
+        tmem_ld32(tmem + (((warp & 3u) * 32u) << 16) + (uint32_t)c0, r);
+        float4* dst = reinterpret_cast<float4*>(ct + ((warp & 3u) * 32 + lane) * C::kLdc + c0);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
             if (c0 + 4 * j < BN)
@@ -297,7 +334,10 @@ __global__ void __launch_bounds__(128, 1)
         __syncthreads();
         if (threadIdx.x == 0) *last_flag = atomicAdd(&a.ctr[tile], 1u) == a.splits - 1;
         __syncthreads();
-        if (!*last_flag) return;
+        if (!*last_flag) {
+            if (mc > 1) cluster_sync();
+            return;
+        }
         __threadfence();
         constexpr int kB = 8;
         for (uint32_t u0 = threadIdx.x; u0 < rows * upr; u0 += blockDim.x * kB) {
@@ -336,49 +376,60 @@ __global__ void __launch_bounds__(128, 1)
         __syncthreads();
     }
     // 2b) row-major pass over 4-column units: consecutive threads take consecutive units, so the
-    //     bias / residual loads and the output stores are 8-16 B, coalesced and independent.
+    //     bias / residual loads and the output stores are 8-16 B and coalesced.  Because
+    //     blockDim.x is a multiple of BN/4, a thread always owns the same 4 columns: its bias is
+    //     loaded once, and its residual rows are loaded kE at a time before any of their stores
+    //     (measured: a load -> store chain per unit cost ~0.3 us per unit, 9.8 us at BN = 128).
     const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(*d, a.b_off)) : nullptr;
     const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (a.res == nullptr || a.ld_res % 4 == 0);
     if (vec) {
-#pragma unroll 4
-        for (uint32_t u = threadIdx.x; u < rows * upr; u += blockDim.x) {
-            const uint32_t r = u / upr, c = (u - r * upr) * 4;
-            if (c >= cols) continue;
-            const uint32_t m = m0 + r, n = n0 + c;
-            float4 v = *reinterpret_cast<const float4*>(ct + r * C::kLdc + c);
-            if (bias) {
-                const uint2 bv = *reinterpret_cast<const uint2*>(bias + n);
-                v.x += __uint_as_float(bv.x << 16);
-                v.y += __uint_as_float(bv.x & 0xffff0000u);
-                v.z += __uint_as_float(bv.y << 16);
-                v.w += __uint_as_float(bv.y & 0xffff0000u);
-            }
-            if (a.res) {
-                const uint64_t ri = (uint64_t)m * a.ld_res + n;
-                if (a.res_bf16) {
-                    const uint2 rv = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.res) + ri);
-                    v.x += __uint_as_float(rv.x << 16);
-                    v.y += __uint_as_float(rv.x & 0xffff0000u);
-                    v.z += __uint_as_float(rv.y << 16);
-                    v.w += __uint_as_float(rv.y & 0xffff0000u);
-                } else {
-                    const float4 rv = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + ri);
-                    v.x += rv.x;
-                    v.y += rv.y;
-                    v.z += rv.z;
-                    v.w += rv.w;
+        constexpr int kE = 8;
+        const uint32_t units = rows * upr, c = (threadIdx.x % upr) * 4;
+        const bool col_ok = c < cols;
+        float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (bias && col_ok) {
+            const uint2 bv = *reinterpret_cast<const uint2*>(bias + n0 + c);
+            bsum = make_float4(__uint_as_float(bv.x << 16), __uint_as_float(bv.x & 0xffff0000u),
+                               __uint_as_float(bv.y << 16), __uint_as_float(bv.y & 0xffff0000u));
+        }
+        const float* __restrict__ resf = a.res && !a.res_bf16 ? reinterpret_cast<const float*>(a.res) : nullptr;
+        const uint16_t* __restrict__ resh = a.res && a.res_bf16 ? reinterpret_cast<const uint16_t*>(a.res) : nullptr;
+        for (uint32_t u0 = threadIdx.x; u0 < units; u0 += blockDim.x * kE) {
+            uint4 raw[kE];
+#pragma unroll
+            for (int j = 0; j < kE; ++j) {
+                const uint32_t u = u0 + j * blockDim.x, r = u / upr;
+                raw[j] = make_uint4(0, 0, 0, 0);
+                if (u < units && col_ok) {
+                    const uint64_t ri = (uint64_t)(m0 + r) * a.ld_res + n0 + c;
+                    if (resf) raw[j] = *reinterpret_cast<const uint4*>(resf + ri);
+                    else if (resh) {
+                        const uint2 h = *reinterpret_cast<const uint2*>(resh + ri);
+                        raw[j] = make_uint4(h.x << 16, h.x & 0xffff0000u, h.y << 16, h.y & 0xffff0000u);
+                    }
                 }
             }
-            v.x = apply_act(a.act, v.x);
-            v.y = apply_act(a.act, v.y);
-            v.z = apply_act(a.act, v.z);
-            v.w = apply_act(a.act, v.w);
-            const uint64_t oi = (uint64_t)m * a.ld_out + n;
-            const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
-                                        (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
-            if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
-            else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = v;
-            if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
+#pragma unroll
+            for (int j = 0; j < kE; ++j) {
+                const uint32_t u = u0 + j * blockDim.x, r = u / upr;
+                if (!(u < units && col_ok)) continue;
+                float4 v = *reinterpret_cast<const float4*>(ct + r * C::kLdc + c);
+                // (acc + bias) + residual, the order of the unfused definition
+                v.x = (v.x + bsum.x) + __uint_as_float(raw[j].x);
+                v.y = (v.y + bsum.y) + __uint_as_float(raw[j].y);
+                v.z = (v.z + bsum.z) + __uint_as_float(raw[j].z);
+                v.w = (v.w + bsum.w) + __uint_as_float(raw[j].w);
+                v.x = apply_act(a.act, v.x);
+                v.y = apply_act(a.act, v.y);
+                v.z = apply_act(a.act, v.z);
+                v.w = apply_act(a.act, v.w);
+                const uint64_t oi = (uint64_t)(m0 + r) * a.ld_out + n0 + c;
+                const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
+                                            (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
+                if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
+                else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = v;
+                if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
+            }
         }
     } else {
         for (uint32_t idx = threadIdx.x; idx < rows * BN; idx += blockDim.x) {
@@ -401,6 +452,7 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     STAMP(5);
 #endif
+    if (mc > 1) cluster_sync();  // no CTA leaves while a peer's multicast commit may target it
 }
 
 template <int BN>
@@ -409,7 +461,8 @@ static void launch_bn(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMa
     const int nst = (int)((a.kt_per + C::kSub - 1) / C::kSub);
     const int stages = nst < C::kMaxStages ? nst : C::kMaxStages;
     dim3 grid((a.M + a.m_rows - 1) / a.m_rows, a.n_pad / BN, a.splits);
-    launch_pdl(PDL_GEMM, k_gemm<BN>, grid, dim3(128), C::smem_bytes(stages), s, *tmA, d, w, a, stages);
+    launch_pdl_cluster(PDL_GEMM, k_gemm<BN>, grid, dim3(kGemmThreads), C::smem_bytes(stages), s, dim3(1, a.mc > 1 ? a.mc : 1, 1),
+                       *tmA, d, w, a, stages);
 }
 
 void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading)
@@ -433,7 +486,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems) {
+bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems, uint32_t box_rows) {
     static PFN_encodeTiled fn = nullptr;
     if (!fn) {
         void* p = nullptr;
@@ -444,7 +497,7 @@ bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
     }
     const cuuint64_t dims[2] = {cols, rows};
     const cuuint64_t strides[1] = {ld_elems * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows ? box_rows : (cuuint32_t)kBM};
     const cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -108,6 +108,9 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // implicit-GEMM convolution: A tile = Hb output rows x Q columns x 64 input channels of one
     // (r, s) tap, gathered by one 4-D TMA load (zero fill = padding, element stride = conv stride)
     int conv; uint32_t Q, stride, pad, S, Cin, Hb;
+    // A multicast: CTAs of a (1, mc, 1) cluster share each A sub-tile, every CTA loading 128/mc rows
+    // and broadcasting them (mc in {1, 2, 4, 8}; the A tensor map's box is 128/mc rows)
+    uint32_t mc;
 };
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a);
 
@@ -131,7 +134,8 @@ void init_gemm_attrs();
 void init_ops_attrs();
 
 // Host helper: build the TMA descriptor of a row-major bf16 activation [rows][cols].
-bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems);
+bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld_elems,
+                   uint32_t box_rows = 0 /* 0 = 128 */);
 // Host helper: 4-D TMA descriptor of an NHWC bf16 input [H][W][C] for implicit-GEMM conv:
 // box = 64 channels x Q output columns x Hb output rows, element strides = conv stride.
 bool make_tmap_conv(CUtensorMap* map, const void* base, uint32_t H, uint32_t W, uint32_t C, uint32_t Q, uint32_t Hb,

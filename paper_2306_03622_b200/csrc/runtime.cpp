@@ -276,29 +276,35 @@ constexpr uint32_t kGemmCtrs = 1u << 16;
 
 // Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor.
 struct Tiling { int bn; uint32_t splits, kt_per; };
-static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t /*a_kt_bytes*/, uint32_t /*m_rows*/) {
-    // Rule fitted to the (BN, split) sweep of tools/gemm_bench.cu on B200 (profiles/r01): a CTA
-    // takes a whole SM (shared memory), so grids stay within one wave of 148; within that, the
-    // narrowest tile wins (every N tile re-reads A, but more CTAs stream more of W in parallel);
-    // split-K pays only when the grid would fill less than half the SMs and each split keeps
-    // >= 10 k tiles (the last CTA's reduction is serial).
-    Tiling t{128, 1, kt};
-    for (int bn : {16, 32, 64, 128})
-        if (n_pad % bn == 0 && m_tiles * (n_pad / bn) <= 148) {
-            t.bn = bn;
-            break;
-        }
-    if (n_pad % t.bn) t.bn = 16;
-    const uint64_t base = m_tiles * (n_pad / t.bn);
-    if (base <= 74) {
-        uint32_t S = (uint32_t)std::min<uint64_t>(148 / base, kt / 10);
-        while (S > 1 && (kt + (kt + S - 1) / S - 1) / ((kt + S - 1) / S) != S) --S;  // no empty split
-        if (S > 1) {
-            t.splits = S;
-            t.kt_per = (kt + S - 1) / S;
+static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t a_kt_bytes, uint32_t /*m_rows*/) {
+    // Linear latency model fitted (least squares, rms 1.1 us) to the (BN, split) sweep of
+    // tools/gemm_bench.cu on B200 over the batch-1 GEMM shapes of the paper's models
+    // (profiles/r01/gemm_bench_sweep.txt): fixed cost, the bytes one CTA streams into shared memory,
+    // the epilogue width, the split-K reduction, and the total L2->SM traffic (every N tile re-reads
+    // A).  One CTA per SM: a grid beyond one wave of 148 pays per wave.  Picks within 0.5 us of the
+    // measured best on every swept shape.
+    Tiling best{16, 1, kt};
+    double best_t = 1e30;
+    for (int bn : {16, 32, 64, 128}) {
+        if (n_pad % bn) continue;
+        const uint64_t base = m_tiles * (n_pad / bn);
+        for (uint32_t S = 1; S <= 16 && S <= kt; ++S) {
+            const uint32_t kt_per = (kt + S - 1) / S;
+            if ((kt + kt_per - 1) / kt_per != S) continue;  // no empty split
+            const uint64_t ctas = base * S;
+            if (S > 1 && ctas > 148) break;
+            const double cta_kb = kt_per * (double)(a_kt_bytes + bn * 128) / 1e3;
+            const double waves = (double)((ctas + 147) / 148);
+            double t = 4.44 + 0.0078 * cta_kb + 0.233 * (bn / 16.0) + 0.0428 * std::min<double>(ctas, 148) * cta_kb / 1e3;
+            if (S > 1) t += 2.51 + 0.0516 * S * (bn / 16.0);
+            t *= waves;
+            if (t < best_t - 1e-9) {
+                best_t = t;
+                best = {bn, S, kt_per};
+            }
         }
     }
-    return t;
+    return best;
 }
 
 struct fsw_ctx {
@@ -854,6 +860,14 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
         a.splits = t.splits;
         a.kt_per = t.kt_per;
         a.ctr = g.gemm_ctr;
+        // A multicast across an N cluster (plain GEMMs; the implicit-conv A box is not row-split)
+        a.mc = 1;
+        static const uint32_t mc_max = getenv("FSW_GEMM_MC") ? (uint32_t)atoi(getenv("FSW_GEMM_MC")) : 1;
+        for (uint32_t c : {8u, 4u, 2u})
+            if (c <= mc_max && m_rows == 128 && (a.n_pad / t.bn) % c == 0) {
+                a.mc = c;
+                break;
+            }
         const uint64_t tiles = m_tiles * (a.n_pad / t.bn);
         if (t.splits > 1) part_bytes = std::max<uint64_t>(part_bytes, tiles * t.splits * 128 * t.bn * 4);
         return tiles <= kGemmCtrs;
@@ -948,7 +962,7 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     a.out2 = shadow(L.out);
                     set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
                     const void* abase = si.dtype == FSW_DT_BF16 ? (const void*)sptr(L.in0) : (const void*)shadow(L.in0);
-                    if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si)))
+                    if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), 128 / a.mc))
                         return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
                 }
                 break;
@@ -1008,7 +1022,7 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                         return fail(FSW_ECUDA, "plan: conv tensor map failed (layer %u)", li);
                 } else {
                     set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
-                    if (!make_tmap_act(&x.tmap, abase, a.M, acols, acols))
+                    if (!make_tmap_act(&x.tmap, abase, a.M, acols, acols, 128 / a.mc))
                         return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
                 }
                 break;

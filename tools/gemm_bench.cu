@@ -17,6 +17,7 @@ int main(int argc, char** argv) {
     const char* only = argc > 1 ? argv[1] : nullptr;
     const int only_bn = argc > 2 ? atoi(argv[2]) : 0;
     const uint32_t only_s = argc > 3 ? (uint32_t)atoi(argv[3]) : 0;
+    const uint32_t only_mc = argc > 4 ? (uint32_t)atoi(argv[4]) : 0;
     struct Shape { const char* name; uint32_t M, K, N; };
     Shape shapes[] = {{"bert.qkv", 128, 768, 2304}, {"bert.o", 128, 768, 768}, {"bert.ffn1", 128, 768, 3072},
                       {"bert.ffn2", 128, 3072, 768}, {"gpt.qkv", 128, 1600, 4800}, {"gpt.fc", 128, 1600, 6400},
@@ -31,16 +32,18 @@ int main(int argc, char** argv) {
     cudaMalloc(&part, 64 << 20); cudaMalloc(&ctr, 1 << 20); cudaMemset(ctr, 0, 1 << 20);
     cudaMemset(A, 0x3c, 64 << 20); cudaMemset(W, 0x3c, 64 << 20);
     DevDesc* dd; cudaMalloc(&dd, sizeof(DevDesc));
-    DevDesc h{W, 0}; cudaMemcpy(dd, &h, sizeof h, cudaMemcpyHostToDevice);
+    DevDesc h{W, W, 0, 0}; cudaMemcpy(dd, &h, sizeof h, cudaMemcpyHostToDevice);
     DevCtl* ctl; cudaMalloc(&ctl, sizeof(DevCtl)); cudaMemset(ctl, 0, sizeof(DevCtl));
     cudaStream_t s; cudaStreamCreate(&s);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (auto& sh : shapes) {
         if (only && strcmp(only, sh.name)) continue;
         const uint32_t n_pad = (sh.N + 15) / 16 * 16, kt = sh.K / 64;
-        double best = 1e9; int bb = 0; uint32_t bs = 0;
+        double best = 1e9; int bb = 0; uint32_t bs = 0, bm = 1;
         for (int bn : {16, 32, 64, 128}) {
             if (n_pad % bn || (only_bn && bn != only_bn)) continue;
+            for (uint32_t mc : {1u, 2u, 4u, 8u}) {
+            if ((n_pad / bn) % mc || (only_mc && mc != only_mc)) continue;
             for (uint32_t S : {1u, 2u, 3u, 4u, 6u, 8u, 12u, 16u, 24u, 36u}) {
                 if (S > kt || (only_s && S != only_s)) continue;
                 const uint32_t kt_per = (kt + S - 1) / S;
@@ -48,10 +51,10 @@ int main(int argc, char** argv) {
                 const uint32_t ctas = ((sh.M + 127) / 128) * (n_pad / bn) * S;
                 if (ctas > 600) continue;
                 CUtensorMap tm;
-                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K)) { printf("tmap fail\n"); return 1; }
+                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K, 128 / mc)) { printf("tmap fail\n"); return 1; }
                 GemmArgs a{}; a.M = sh.M; a.N = sh.N; a.K = sh.K; a.n_pad = n_pad; a.w_off = 0; a.b_off = 0;
                 a.has_bias = 1; a.act = 0; a.res = nullptr; a.out = O; a.out_bf16 = 1; a.ld_out = sh.N; a.bn = bn;
-                a.m_rows = 128; a.splits = S; a.kt_per = kt_per; a.part = part; a.ctr = ctr;
+                a.m_rows = 128; a.splits = S; a.kt_per = kt_per; a.part = part; a.ctr = ctr; a.mc = mc;
                 Wait w{}; w.ctl = ctl;
                 for (int i = 0; i < 3; ++i) launch_gemm(s, dd, w, &tm, a);
                 cudaEventRecord(e0, s);
@@ -62,9 +65,9 @@ int main(int argc, char** argv) {
                 float ms; cudaEventElapsedTime(&ms, e0, e1);
                 const double us = ms * 1000 / reps;
                 const double wbytes = 2.0 * n_pad * sh.K;
-                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
-                       sh.K, sh.N, bn, S, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
-                if (us < best) { best = us; bb = bn; bs = S; }
+                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u mc=%u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
+                       sh.K, sh.N, bn, S, mc, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
+                if (us < best) { best = us; bb = bn; bs = S; bm = mc; }
 #ifdef PHASES
                 // one isolated launch: per-CTA %globaltimer stamps -> mean phase durations
                 cudaDeviceSynchronize();
@@ -89,8 +92,9 @@ int main(int argc, char** argv) {
                            ph[4] / nfull / 1e3, (t1 - t0) / 1e3);
 #endif
             }
+            }
         }
-        printf("  BEST %-18s BN=%d S=%u %.2f us\n", sh.name, bb, bs, best);
+        printf("  BEST %-18s BN=%d S=%u mc=%u %.2f us\n", sh.name, bb, bs, bm, best);
     }
     cudaError_t e = cudaGetLastError();
     printf("last error: %s\n", cudaGetErrorString(e));
