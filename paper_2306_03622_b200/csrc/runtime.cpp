@@ -1110,7 +1110,10 @@ static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams, uin
     // byte is then only the last small group's layers (big groups amortise the ~8 us per-copy
     // setup of the copy engine; small ones bound the tail).
     const uint64_t total = m.store_bytes, tail_min = std::min<uint64_t>(grp, 1ull << 20);
-    auto want = [&](uint64_t at) { return std::min(grp, std::max(tail_min, align_up((total - at) / 2, 256))); };
+    static const double frac = getenv("FSW_DMA_TAPER") ? atof(getenv("FSW_DMA_TAPER")) : 0.5;  // sweep hook
+    auto want = [&](uint64_t at) {
+        return std::min(grp, std::max(tail_min, align_up((uint64_t)((double)(total - at) * frac), 256)));
+    };
     for (size_t li = 0; li < nl; ++li) {
         const uint64_t ro = m.region_off[li], rb = m.region_bytes[li];
         if (!rb || ro < from) continue;
@@ -1265,13 +1268,17 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
     CU(cudaSetDevice(g.dev));
     cudaStream_t sx = g.sx, sc = g.sc;
     CU(cudaStreamBeginCapture(sx, cudaStreamCaptureModeThreadLocal));
-    cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr + m.input_bytes, cudaMemcpyHostToDevice, sx);
+    // The swap starts as early as possible: the DMA engine needs only its counters reset; the SM
+    // engine also reads the invoke descriptor and the control block.  The input (up to 300 KB for
+    // ResNet-50) is copied after the fork, overlapping the swap.
+    const bool dma_cold = ic.cold && !ic.striped && ic.engine != FSW_ENGINE_SM;
+    if (dma_cold) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
+    if (!dma_cold) cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr, cudaMemcpyHostToDevice, sx);
     // striped: the counters and the control block are reset before the sources start (outside)
-    if (!ic.striped) cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
+    if (!ic.striped && !dma_cold) cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
     if (ic.cold && ic.striped && !ic.no_overlap && ic.local_ctas) launch_gate(sx, g.ctl, ic.local_ctas);
     if (ic.cold && !ic.striped) {
         if (ic.engine == FSW_ENGINE_SM) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
-        else cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
         cudaEventRecord(g.evfork, sx);
         cudaStreamWaitEvent(sc, g.evfork, 0);
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
@@ -1303,6 +1310,13 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
         }
         cudaEventRecordWithFlags(g.evs1, sc, cudaEventRecordExternal);
         cudaEventRecord(g.evjoin, sc);
+    }
+    if (dma_cold) {
+        cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr, cudaMemcpyHostToDevice, sx);
+        cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
+    }
+    cudaMemcpyAsync(g.dstage + kStageHdr, g.hstage + kStageHdr, m.input_bytes, cudaMemcpyHostToDevice, sx);
+    if (ic.cold && !ic.striped) {
         if (ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
         else if (ic.engine == FSW_ENGINE_SM) launch_gate(sx, g.ctl, ic.ctas);
     }
