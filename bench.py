@@ -35,6 +35,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PCIE_GEN5_X16_GBS = 63.0  # 32 GT/s x 16 lanes x 128/130 / 8 (nominal, per direction)
+METRIC = "cold swap+infer latency ms p50 (p99, resident, host->HBM GB/s in extra keys)"  # every arm, every N
+
+
+def workload_name(model: str, world: int) -> str:
+    return f"{model} batch 1, cold invoke (model resident on no GPU)" + (
+        f", swap striped over {world} GPUs' host links" if world > 1 else "")
 
 
 def percentile(xs, p):
@@ -139,11 +145,14 @@ def run_reference(args):
     times, cores = cpu_oracle_timing(spec, w, x, budget_s=max(5.0, args.ref_budget_s), max_reps=args.warmup + args.steps)
     timed = times[min(len(times) - 1, args.warmup):] if len(times) > args.warmup else times
     v = statistics.median(timed)
-    line = {"impl": "reference", "metric": "cold swap+infer latency ms p50 (reference arm: CPU oracle forward)",
+    line = {"impl": "reference", "metric": METRIC,
             "value": round(v, 3), "unit": "ms", "n_gpus": args.gpus, "steps": len(timed), "warmup": args.warmup,
-            "ms_per_step": round(statistics.mean(timed), 3), "higher_is_better": False, "scaling": "weak",
+            "ms_per_step": round(statistics.mean(timed), 3), "higher_is_better": False,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.model} batch 1 forward (oracle, float64, host cores)"},
+            "config": {"workload": workload_name(args.model, world),
+                       "reference_arm": "the CPU oracle (float64 forward over the same bf16 weights, host cores): "
+                                        "no reference implementation of the paper exists"},
             "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": cores, "kind": "oracle",
                              "sample": f"{len(timed)} full {args.model} forwards (float64 oracle), OMP threads={cores}"},
             "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -303,11 +312,11 @@ def run_fsw(args):
                 "pcie_read_bytes": pcie_traffic}
     sm_gbs = variants["sm"]["host_to_hbm_gbs"] if "sm" in variants else None
     line = {
-        "metric": "cold swap+infer latency ms p50 (p99, resident, host->HBM GB/s in extra keys)",
+        "metric": METRIC,
         "value": round(p50, 4), "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(statistics.mean(dev), 4), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded)",
-        "config": {"workload": f"{args.model} batch 1, cold invoke (model resident on no GPU)",
+        "config": {"workload": workload_name(args.model, 1) + (f", {world} replicas" if world > 1 else ""),
                    "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"],
                    "swap_engine": engine, "sm_chunk_bytes": (args.chunk_kb or 16) << 10,
                    "sm_copy_ctas": args.copy_ctas or 16, "dma_group_bytes": (args.dma_group_mb or 64) << 20,
@@ -401,11 +410,11 @@ def run_striped(args):
     t_roof = roofline_ms(info["algorithmic_bytes"], MODEL_FLOPS.get(args.model, 0.0), fill, agg_peak, 1645.1)
     p50 = percentile(dev, 50)
     line = {
-        "metric": "cold swap+infer latency ms p50 (striped swap over N host links)",
+        "metric": METRIC,
         "value": round(p50, 4), "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(statistics.mean(dev), 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded)",
-        "config": {"workload": f"{args.model} batch 1, cold invoke striped over {world} GPUs' host links into GPU 0",
+        "config": {"workload": workload_name(args.model, world),
                    "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"], "swap_engine": "sm-striped",
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
                    "parallelism": f"striped swap x{world} (one process drives the pool)"},

@@ -4,16 +4,17 @@ import sys
 import numpy as np
 sys.path.insert(0, ".")
 import synth
-from paper_2306_03622_b200 import Runtime, NO_OVERLAP
+from paper_2306_03622_b200 import ENGINE_DMA, ENGINE_SM, NO_OVERLAP, Runtime
 
 name = sys.argv[1] if len(sys.argv) > 1 else "bert-base"
 warm = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+engine = {"sm": ENGINE_SM, "dma": ENGINE_DMA}.get(sys.argv[3] if len(sys.argv) > 3 else "", 0)
 rt = Runtime(pool_bytes=16 << 30)
 spec = synth.build_model(name)
 w = spec.build_weights()
 x = spec.make_input()
 mid = rt.register_spec(spec, w)
-rt.invoke(mid, x, flags=NO_OVERLAP)
+rt.invoke(mid, x, flags=NO_OVERLAP, engine=engine)
 for _ in range(warm):
     rt.invoke(mid, x)
 rt.close()
