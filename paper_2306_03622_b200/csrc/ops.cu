@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
     const uint32_t kend = a.causal ? tend : T;  // keys this CTA needs
     const uint32_t kst = dh / 2 + 1;           // K row stride in 32-bit words (padded)
     uint32_t* Ks = reinterpret_cast<uint32_t*>(sm_attn);     // [T][kst]   bf16x2
-    uint32_t* Vs = Ks + T * kst;                              // [T][dh/2]  bf16x2
+    uint32_t* Vs = Ks + ((T * kst + 3) & ~3u);                // [T][dh/2]  bf16x2, 16-B aligned (uint4 stores)
     float* Ps = reinterpret_cast<float*>(Vs + T * (dh / 2));  // [nwarp][T]
     float* Qs = Ps + nwarp * T;                               // [nwarp][dh]
     const uint32_t dh8 = dh / 8;
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
 
 void launch_attention(cudaStream_t s, const AttnArgs& a) {
     const int threads = 256, nwarp = threads / 32;
-    const size_t smem = 4 * (a.T * (a.dh / 2 + 1) + a.T * (a.dh / 2)) + sizeof(float) * (nwarp * a.T + nwarp * a.dh);
+    const size_t smem = 4 * (((a.T * (a.dh / 2 + 1) + 3) & ~3u) + a.T * (a.dh / 2)) + sizeof(float) * (nwarp * a.T + nwarp * a.dh);
     dim3 grid(a.H, (a.T + kAttnRows - 1) / kAttnRows);
     launch_pdl(PDL_ATTN, k_attention, grid, dim3(threads), smem, s, a);
 }
