@@ -70,7 +70,7 @@ constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, DevDesc dst, const DevDesc* desc,
                  const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys);
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
-void launch_finish(cudaStream_t s, DevCtl* ctl);
+void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl);
 
 // ---- layer ops ----------------------------------------------------------------------------
 struct EmbedArgs {

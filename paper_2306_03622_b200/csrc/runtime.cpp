@@ -260,8 +260,8 @@ struct Gpu {
     DevCtl* ctl = nullptr;
     uint8_t* dstage = nullptr;   // device: [DevDesc | pad | input]
     uint8_t* hstage = nullptr;   // pinned: same layout
-    uint8_t* hout = nullptr;     // pinned: output
-    DevCtl* hctl = nullptr;      // pinned: ctl copy
+    uint8_t* hout = nullptr;     // pinned, mapped: output (written by k_finish)
+    DevCtl* hctl = nullptr;      // pinned, mapped: ctl copy (written by k_finish)
     uint64_t stage_cap = 0, out_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr, evfork = nullptr, evjoin = nullptr;
     bool busy = false;
@@ -358,8 +358,8 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     g.out_cap = 16ull << 20;
     CU(cudaMalloc(&g.dstage, g.stage_cap));
     CU(cudaHostAlloc(&g.hstage, g.stage_cap, cudaHostAllocPortable));
-    CU(cudaHostAlloc(&g.hout, g.out_cap, cudaHostAllocPortable));
-    CU(cudaHostAlloc(reinterpret_cast<void**>(&g.hctl), sizeof(DevCtl), cudaHostAllocPortable));
+    CU(cudaHostAlloc(&g.hout, g.out_cap, cudaHostAllocPortable | cudaHostAllocMapped));
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&g.hctl), sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped));
     memset(g.hstage, 0, kStageHdr);
     for (cudaEvent_t* e : {&g.ev0, &g.ev1, &g.evs0, &g.evs1}) CU(cudaEventCreate(e));
     CU(cudaEventCreateWithFlags(&g.evfork, cudaEventDisableTiming));
@@ -1321,10 +1321,8 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
         else if (ic.engine == FSW_ENGINE_SM) launch_gate(sx, g.ctl, ic.ctas);
     }
     enqueue_layers(m, p, g, ic, sx);
-    launch_finish(sx, g.ctl);
-    if (ic.cold && !ic.striped && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
-    cudaMemcpyAsync(g.hout, g.ws + p.slot_off[m.output_slot], m.output_bytes, cudaMemcpyDeviceToHost, sx);
-    cudaMemcpyAsync(g.hctl, g.ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, sx);
+    if (ic.cold && !ic.striped && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);  // swap stamps final
+    launch_finish(sx, g.ctl, g.ws + p.slot_off[m.output_slot], m.output_bytes, g.hout, g.hctl);
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(sx, &graph);
     if (e != cudaSuccess) {

@@ -74,7 +74,23 @@ __global__ void k_gate(DevCtl* ctl, uint32_t expected) {
 
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected) { k_gate<<<1, 1, 0, s>>>(ctl, expected); }
 
-__global__ void k_finish(DevCtl* ctl) { ctl->t_end = globaltimer(); }
-void launch_finish(cudaStream_t s, DevCtl* ctl) { k_finish<<<1, 1, 0, s>>>(ctl); }
+// Last node of every invoke graph: stamp the end, then write the output slot and the control
+// block straight into mapped pinned host memory (zero-copy stores over PCIe), so the graph ends
+// without device-to-host copy nodes; the host reads them after the graph's completion event.
+__global__ void k_finish(DevCtl* ctl, const uint8_t* __restrict__ out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->t_end = globaltimer();
+        *host_ctl = *ctl;
+    }
+    const uint64_t n16 = bytes >> 4, stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint64_t i = t0; i < n16; i += stride)
+        reinterpret_cast<uint4*>(host_out)[i] = reinterpret_cast<const uint4*>(out)[i];
+    for (uint64_t i = (n16 << 4) + t0; i < bytes; i += stride) host_out[i] = out[i];
+}
+void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl) {
+    const uint64_t want = (bytes + 4095) / 4096;
+    k_finish<<<(unsigned)(want < 1 ? 1 : want > 148 ? 148 : want), 256, 0, s>>>(ctl, out, bytes, host_out, host_ctl);
+}
 
 }  // namespace fsw
