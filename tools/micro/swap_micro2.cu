@@ -119,15 +119,74 @@ int main() {
                bytes / (ms[ms.size() / 2] * 1e6), bytes / (ms[0] * 1e6));
         check(bytes, what);
     };
+    int wv_mode = 0;  // 0 default write-value (fenced), 1 no memory barrier, 2 no write-value
     auto grouped = [&](cudaStream_t s, uint64_t lo, uint64_t hi, uint64_t grp, uint32_t* word) {
         uint32_t k = 0;
         for (uint64_t o = lo; o < hi; o += grp) {
             const uint64_t nb = umin64(grp, hi - o);
             cudaMemcpyAsync(d + o, src + o, nb, cudaMemcpyHostToDevice, s);
-            cuStreamWriteValue32(s, (CUdeviceptr)word, (cuuint32_t)(++k), 0);
+            if (wv_mode == 0) cuStreamWriteValue32(s, (CUdeviceptr)word, (cuuint32_t)(++k), 0);
+            if (wv_mode == 1) cuStreamWriteValue32(s, (CUdeviceptr)word, (cuuint32_t)(++k), CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER);
         }
     };
+    // copies serialised across two streams by events, each stream's fenced write-value overlapping
+    // the other stream's next copy
+    cudaEvent_t evc[64];
+    for (int i = 0; i < 64; ++i) CK(cudaEventCreateWithFlags(&evc[i], cudaEventDisableTiming));
+    auto chained = [&](uint64_t bytes, uint64_t grp) {
+        cudaStream_t ss[2] = {st, st2};
+        cudaEventRecord(ef, st);
+        cudaStreamWaitEvent(st2, ef, 0);
+        uint32_t k[2] = {0, 0};
+        int i = 0;
+        for (uint64_t o = 0; o < bytes; o += grp, ++i) {
+            cudaStream_t s = ss[i & 1];
+            if (i > 0) cudaStreamWaitEvent(s, evc[(i - 1) % 64], 0);
+            cudaMemcpyAsync(d + o, src + o, umin64(grp, bytes - o), cudaMemcpyHostToDevice, s);
+            cudaEventRecord(evc[i % 64], s);
+            cuStreamWriteValue32(s, (CUdeviceptr)(prog + 32 * (i & 1)), (cuuint32_t)(++k[i & 1]), 0);
+        }
+        cudaEventRecord(ej, st2);
+        cudaStreamWaitEvent(st, ej, 0);
+    };
+    // copies back to back on one stream; the fenced write-values on a second "flag" stream, each
+    // after an event recorded behind its copy (the fence no longer stalls the copy stream)
+    auto flagged = [&](uint64_t bytes, uint64_t grp) {
+        cudaEventRecord(ef, st);
+        cudaStreamWaitEvent(st2, ef, 0);
+        uint32_t k = 0;
+        int i = 0;
+        for (uint64_t o = 0; o < bytes; o += grp, ++i) {
+            cudaMemcpyAsync(d + o, src + o, umin64(grp, bytes - o), cudaMemcpyHostToDevice, st);
+            cudaEventRecord(evc[i % 64], st);
+            cudaStreamWaitEvent(st2, evc[i % 64], 0);
+            cuStreamWriteValue32(st2, (CUdeviceptr)prog, (cuuint32_t)(++k), 0);
+        }
+        cudaEventRecord(ej, st2);
+        cudaStreamWaitEvent(st, ej, 0);
+    };
     char name[160];
+    if (getenv("GAP_ONLY")) {
+        for (uint64_t grp : {256ull << 10, 1ull << 20, 4ull << 20, 8ull << 20}) {
+            snprintf(name, sizeof name, "DMA back-to-back + flags on a 2nd stream %lluK", (unsigned long long)(grp >> 10));
+            timeit([&] { flagged(51ull << 20, grp); }, 51ull << 20, name);
+        }
+        for (uint64_t grp : {256ull << 10, 1ull << 20, 4ull << 20, 8ull << 20}) {
+            snprintf(name, sizeof name, "DMA chained over 2 streams %lluK, fenced write-values", (unsigned long long)(grp >> 10));
+            timeit([&] { chained(51ull << 20, grp); }, 51ull << 20, name);
+        }
+        for (uint64_t bytes : {51ull << 20}) {
+            for (int mode = 0; mode < 3; ++mode) {
+                wv_mode = mode;
+                for (uint64_t grp : {256ull << 10, 1ull << 20, 4ull << 20}) {
+                    snprintf(name, sizeof name, "DMA grouped %lluK, write-value mode %d (0 fenced, 1 no barrier, 2 none)",
+                             (unsigned long long)(grp >> 10), mode);
+                    timeit([&] { grouped(st, 0, bytes, grp, prog); }, bytes, name);
+                }
+            }
+        }
+        return 0;
+    }
     for (uint64_t bytes : {51ull << 20, 219ull << 20}) {
         for (int wc = 0; wc < 2; ++wc) {
             src = wc ? hwc : h;
