@@ -3,9 +3,11 @@
 
 One *step* = one cold invocation of the whole hot path: the model is resident on no
 GPU (``fsw_evict(m, -1)``), so the invoke swaps all of its weights from the pinned host store
-into the HBM pool with the SM swap kernel while the flag-gated layer kernels run as soon as each
-layer lands, then returns the output.  Default workload: BASELINE.json
-configs[1], BERT-base seq 128 batch 1 (~219 MB bf16).
+into the HBM pool while the flag-gated layer kernels run as soon as each layer lands
+(PAPER.md:588-590), then returns the output.  Default workload: BASELINE.json configs[1],
+BERT-base seq 128 batch 1 (~219 MB bf16), registered link-coded (FSW_REG_LINK_CODE):
+the host link carries the lossless exponent-coded store (~0.76 of the bytes) and the swap engine
+decodes it into the extent bit-exactly; the plain engines are reported beside it (``engines``).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--model bert-base] [--impl fsw|reference]
 
@@ -13,8 +15,9 @@ configs[1], BERT-base seq 128 batch 1 (~219 MB bf16).
               launching stream), ms, lower is better.
 ``e2e``     = the same metric through the public C-ABI call fsw_invoke with host buffers
               (input copied host->device and the output device->host inside the timed region).
-``roofline``= the dominant kernel, the swap kernel: algorithmic bytes (the model's host-store
-              bytes) / its CUDA-event duration on its own stream, against the PCIe Gen5 x16 link.
+``roofline``= the dominant work, the swap: bytes that cross the host link (the coded store, or the
+              plain store for the plain engines) / the swap's CUDA-event duration on its own
+              stream, against the PCIe Gen5 x16 link; the store bytes delivered per second beside it.
 Under torchrun (N > 1) each rank serves its own replica (request-level data parallelism,
 PAPER.md:824; no data-path collective); max-over-ranks timing, rank 0 prints.
 """
@@ -62,10 +65,14 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()  # nvidia-smi takes a while to start: time only once it samples
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.lines.clear()
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
@@ -168,9 +175,12 @@ MODEL_FLOPS = {  # 2 FLOPs per MAC, batch 1
 }
 
 
+ENGINE_NAMES = {1: "sm", 2: "dma", 3: "smz", 4: "dmaz"}
+
+
 def run_fsw(args):
     import synth
-    from paper_2306_03622_b200 import DMA_BASELINE, ENGINE_DMA, ENGINE_SM, Runtime
+    from paper_2306_03622_b200 import DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, Runtime
 
     rank, world, local = dist_env()
     if world > 1:
@@ -182,7 +192,7 @@ def run_fsw(args):
     x = spec.make_input()
     rt = Runtime(gpu_ids=[gpu], pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas, chunk_bytes=args.chunk_kb << 10,
                  engine=args.engine, dma_group_bytes=args.dma_group_mb << 20, dma_streams=args.dma_streams)
-    mid = rt.register_spec(spec, w)
+    mid = rt.register_spec(spec, w, link_code=not args.no_link_code)
     info = rt.model_info(mid)
     out = np.empty(info["output_bytes"] // 4, dtype=np.float32)
 
@@ -204,7 +214,8 @@ def run_fsw(args):
     swap = [s["swap_ms"] for s in stats]
     tail = [s["compute_tail_ms"] for s in stats]
     launches = sum(s["n_kernels"] for s in stats)
-    engine = {1: "sm", 2: "dma"}[stats[0]["engine"]]
+    engine = ENGINE_NAMES[stats[0]["engine"]]
+    wire = stats[0]["wire_bytes"]
     # e2e: the public fsw_invoke (scheduler picks the GPU), host buffers, H2D/D2H inside
     e2e = []
     for _ in range(max(3, args.steps // 2)):
@@ -218,7 +229,8 @@ def run_fsw(args):
     variants = {}
     for name, kw in (() if args.no_variants else
                      (("sm", dict(engine=ENGINE_SM)), ("dma", dict(engine=ENGINE_DMA)),
-                      ("paper_dma_2MB_1stream", dict(flags=DMA_BASELINE)))):
+                      ("paper_dma_2MB_1stream", dict(flags=DMA_BASELINE))) +
+                     ((("smz", dict(engine=ENGINE_SMZ)), ("dmaz", dict(engine=ENGINE_DMAZ))) if info["coded_bytes"] else ())):
         for _ in range(2):
             cold_step(**kw)
         st = [cold_step(**kw) for _ in range(max(5, args.steps // 2))]
@@ -226,6 +238,7 @@ def run_fsw(args):
         variants[name] = {"p50_ms": round(percentile([t["device_ms"] for t in st], 50), 4),
                           "p99_ms": round(percentile([t["device_ms"] for t in st], 99), 4),
                           "swap_p50_ms": round(sw, 4), "host_to_hbm_gbs": round(info["store_bytes"] / (sw * 1e6), 2),
+                          "wire_gbs": round(st[0]["wire_bytes"] / (sw * 1e6), 2), "wire_bytes": st[0]["wire_bytes"],
                           "compute_tail_p50_ms": round(percentile([t["compute_tail_ms"] for t in st], 50), 4),
                           "copies": st[0]["n_copies"]}
     # partial-parameter caching (NEXT #4): the first layer (the embedding / stem) stays resident
@@ -274,7 +287,8 @@ def run_fsw(args):
         return
     store = info["store_bytes"]
     swap_p50 = percentile(swap, 50)
-    achieved = store / (swap_p50 * 1e6)
+    achieved = store / (swap_p50 * 1e6)         # store bytes delivered into HBM per second
+    wire_gbs = wire / (swap_p50 * 1e6)          # bytes over the host link per second
     traffic = pcie_traffic = None
     tpath = os.path.join(ROOT, "profiles", "swap_traffic.json")
     if os.path.exists(tpath):
@@ -289,12 +303,23 @@ def run_fsw(args):
     flops = MODEL_FLOPS.get(args.model, 0.0)
     t_roof = roofline_ms(info["algorithmic_bytes"], flops, fill, PCIE_GEN5_X16_GBS, 1645.1)
     t_roof_dma = roofline_ms(info["algorithmic_bytes"], flops, fill, dma, 1645.1) if dma else None
+    ratio = wire / store  # link coding: the same roofline over the coded bytes
+    t_roof_coded = roofline_ms(info["algorithmic_bytes"] * ratio, flops, fill * ratio, PCIE_GEN5_X16_GBS, 1645.1)
     cpu = None
     if not args.no_cpu_baseline:
         ct, cores = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
         cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": cores, "kind": "oracle",
                "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)"}
-    if engine == "dma":
+    if engine == "dmaz":
+        roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA of link-coded groups into HBM staging + k_swapz decode",
+                "achieved": round(wire_gbs, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
+                "frac": round(wire_gbs / PCIE_GEN5_X16_GBS, 4), "store_bytes_gbs": round(achieved, 2),
+                "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure); "
+                             "achieved = coded bytes over the link / swap time, store_bytes_gbs = decoded bytes / swap time",
+                "frac_of_measured_dma": round(wire_gbs / dma, 4) if dma else None,
+                "traffic": None, "traffic_note": "copy-engine transfers are not kernels: ncu has no per-launch counter for "
+                "them; the decode kernel spans the whole swap (it waits for each group)"}
+    elif engine == "dma":
         roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA groups (cudaMemcpyAsync, no SM kernel)",
                 "achieved": round(achieved, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                 "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
@@ -302,6 +327,12 @@ def run_fsw(args):
                 "frac_of_measured_dma": round(achieved / dma, 4) if dma else None,
                 "traffic": None, "traffic_note": "copy-engine transfers are not kernels: ncu has no per-launch DRAM "
                 "counter for them; the SM engine's k_swap capture is in profiles/ (sm_engine_roofline)"}
+    elif engine == "smz":
+        roof = {"bound": "pcie", "kernel": "k_swapz (zero-copy decode of the coded store)", "achieved": round(wire_gbs, 2),
+                "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s", "frac": round(wire_gbs / PCIE_GEN5_X16_GBS, 4),
+                "store_bytes_gbs": round(achieved, 2),
+                "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure)",
+                "frac_of_measured_dma": round(wire_gbs / dma, 4) if dma else None, "traffic": None}
     else:
         roof = {"bound": "pcie", "kernel": "k_swap", "achieved": round(achieved, 2), "peak": PCIE_GEN5_X16_GBS,
                 "unit": "GB/s", "frac": round(achieved / PCIE_GEN5_X16_GBS, 4),
@@ -318,7 +349,8 @@ def run_fsw(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded)",
         "config": {"workload": workload_name(args.model, 1) + (f", {world} replicas" if world > 1 else ""),
                    "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"],
-                   "swap_engine": engine, "sm_chunk_bytes": (args.chunk_kb or 16) << 10,
+                   "swap_engine": engine, "link_code": bool(info["coded_bytes"]), "coded_bytes": int(info["coded_bytes"]),
+                   "sm_chunk_bytes": (args.chunk_kb or 16) << 10,
                    "sm_copy_ctas": args.copy_ctas or 16, "dma_group_bytes": (args.dma_group_mb or 64) << 20,
                    "dma_streams": args.dma_streams or 1,
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
@@ -327,8 +359,11 @@ def run_fsw(args):
         "min_ms": round(min(dev), 4),
         "resident_p50_ms": round(percentile(warm, 50), 4),
         "swap_p50_ms": round(swap_p50, 4), "compute_tail_p50_ms": round(percentile(tail, 50), 4),
-        "host_to_hbm_gbs": round(achieved, 2), "dma_h2d_gbs_measured": round(dma, 2) if dma else None,
+        "host_to_hbm_gbs": round(achieved, 2), "link_wire_gbs": round(wire_gbs, 2),
+        "dma_h2d_gbs_measured": round(dma, 2) if dma else None,
         "pipelined_roofline_ms": round(t_roof, 4), "frac_of_pipelined_roofline": round(t_roof / p50, 4),
+        "pipelined_roofline_ms_coded_bytes": round(t_roof_coded, 4),
+        "frac_of_pipelined_roofline_coded_bytes": round(t_roof_coded / p50, 4),
         "pipelined_roofline_ms_at_measured_dma": round(t_roof_dma, 4) if t_roof_dma else None,
         "roofline": roof,
         "sm_engine_roofline": {"bound": "pcie", "kernel": "k_swap", "achieved": sm_gbs, "peak": PCIE_GEN5_X16_GBS,
@@ -365,7 +400,7 @@ def run_striped(args):
     ranks only join the barriers.  Total work is fixed as N grows: strong scaling."""
     import synth
     import torch.distributed as dist
-    from paper_2306_03622_b200 import Runtime
+    from paper_2306_03622_b200 import ENGINE_SMZ, Runtime
 
     rank, world, _ = dist_env()
     dist.init_process_group("gloo")
@@ -377,14 +412,15 @@ def run_striped(args):
     x = spec.make_input()
     rt = Runtime(n_gpus=world, pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas, chunk_bytes=args.chunk_kb << 10,
                  stripe_min_bytes=1)
-    mid = rt.register_spec(spec, w)
+    mid = rt.register_spec(spec, w, link_code=not args.no_link_code)
     info = rt.model_info(mid)
     out = np.empty(info["output_bytes"] // 4, dtype=np.float32)
     src = list(range(world))
 
     def cold_step():
         rt.evict(mid, -1)
-        return rt.invoke(mid, x, out=out, gpu=0, stripe=src).stats
+        return rt.invoke(mid, x, out=out, gpu=0, stripe=src,
+                         engine=0 if args.no_link_code else ENGINE_SMZ).stats
 
     for _ in range(args.warmup):
         cold_step()
@@ -415,14 +451,16 @@ def run_striped(args):
         "ms_per_step": round(statistics.mean(dev), 4), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, seeded)",
         "config": {"workload": workload_name(args.model, world),
-                   "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"], "swap_engine": "sm-striped",
+                   "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"],
+                   "swap_engine": ENGINE_NAMES[stats[0]["engine"]] + "-striped", "coded_bytes": int(info["coded_bytes"]),
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
                    "parallelism": f"striped swap x{world} (one process drives the pool)"},
         "p99_ms": round(percentile(dev, 99), 4), "resident_p50_ms": round(percentile(warm, 50), 4),
         "swap_p50_ms": round(swap_p50, 4), "host_to_hbm_gbs": round(achieved, 2),
         "pipelined_roofline_ms": round(t_roof, 4), "frac_of_pipelined_roofline": round(t_roof / p50, 4),
-        "roofline": {"bound": "pcie", "kernel": "k_swap x N sources (peer stores over NVLink)", "achieved": round(achieved, 2),
-                     "peak": agg_peak, "unit": "GB/s", "frac": round(achieved / agg_peak, 4),
+        "roofline": {"bound": "pcie", "kernel": "k_swap / k_swapz x N sources (peer stores over NVLink)",
+                     "achieved": round(stats[0]["wire_bytes"] / (swap_p50 * 1e6), 2), "store_bytes_gbs": round(achieved, 2),
+                     "peak": agg_peak, "unit": "GB/s", "frac": round(stats[0]["wire_bytes"] / (swap_p50 * 1e6) / agg_peak, 4),
                      "peak_note": f"{world} x nominal PCIe Gen5 x16 per direction", "traffic": None},
         "cpu_baseline": None,
         "e2e": {"value": round(percentile(e2e, 50), 4), "unit": "ms", "h2d_bytes_per_step": int(info["input_bytes"]),
@@ -445,7 +483,9 @@ def main():
     ap.add_argument("--copy-ctas", type=int, default=0)
     ap.add_argument("--chunk-kb", type=int, default=0)
     ap.add_argument("--pool-gb", type=int, default=16)
-    ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 SM swap kernel, 2 copy-engine DMA")
+    ap.add_argument("--engine", type=int, default=0,
+                    help="0 auto, 1 SM swap kernel, 2 copy-engine DMA, 3 SMZ / 4 DMAZ (link-coded)")
+    ap.add_argument("--no-link-code", action="store_true", help="register the model without the coded store")
     ap.add_argument("--dma-group-mb", type=int, default=0)
     ap.add_argument("--dma-streams", type=int, default=0)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)

@@ -86,6 +86,9 @@ typedef struct {
     const int32_t* pcie_neighbor;     /* n_gpus entries: the pool GPU sharing each GPU's PCIe
                                          switch, −1 = none (Algorithm 1's "neighbor"); NULL = none
                                          (HGX B200: one switch per GPU)                          */
+    uint64_t dmaz_min_bytes;          /* AUTO picks DMAZ for link-coded models with at least this
+                                         many store bytes, SMZ below; 0 = 128 MiB (measured: SMZ wins
+                                         on ResNet-50's 51 MB, DMAZ on BERT-base's 219 MB)       */
 } fsw_config;
 
 /* Swap engines.  Both move the host store into the extent in execution order and
@@ -94,7 +97,15 @@ typedef struct {
  *        of the piece's bytes on its layer's counter per piece (fine-grained, no per-copy setup);
  *   DMA: copy-engine cudaMemcpyAsync of layer-aligned groups on `dma_streams` streams; after each
  *        group a stream memory write (no SM) bumps that stream's group counter.               */
-enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2 };
+enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SMZ = 3, FSW_ENGINE_DMAZ = 4 };
+/* Link-coded engines (models registered with FSW_REG_LINK_CODE).  The host link carries
+ * the model's exponent-coded store (lossless, ~0.76 of the bytes) and a kernel decodes it into the
+ * extent, releasing each decoded piece's bytes on its layer's counter (the SM protocol):
+ *   SMZ : persistent CTAs read coded pieces zero-copy from the mapped coded store and decode in registers;
+ *   DMAZ: copy-engine DMA of layer-ordered, tapered groups of coded pieces into a device staging
+ *         buffer, each followed by a stream write of the group count; persistent decode CTAs wait for
+ *         their piece's group, then decode from HBM.
+ * AUTO picks DMAZ / SMZ (by dmaz_min_bytes) for link-coded models, DMA / SM (by dma_min_bytes) otherwise. */
 
 typedef struct fsw_ctx fsw_ctx; /* opaque; one per process */
 
@@ -139,6 +150,10 @@ typedef struct { uint32_t dtype, rank; uint32_t shape[4]; } fsw_slot;
 typedef struct { uint32_t op, first_ref, n_refs; int32_t in0, in1, out; int32_t attr[8]; } fsw_layer;
 
 #define FSW_REG_ADOPT 0x1u /* reserved: pin the caller's buffer in place (not yet supported) */
+#define FSW_REG_LINK_CODE 0x2u /* also build the exponent-coded copy of the store (pinned, mapped) that
+                                  the SMZ / DMAZ engines move over the host link (format
+                                  at fsw_coded_piece below).  Lossless: the extent receives the store's
+                                  bytes bit-exactly.  Costs ~0.76x the store in extra host memory.  */
 
 typedef struct {
     const char* name;
@@ -166,6 +181,7 @@ typedef struct {
     uint32_t n_layers, n_tensors, n_gemm_layers;
     uint64_t input_bytes, output_bytes;
     uint32_t output_dtype;
+    uint64_t coded_bytes;      /* bytes of the exponent-coded store (FSW_REG_LINK_CODE), else 0 */
 } fsw_model_info;
 fsw_status fsw_model_info_get(fsw_ctx* ctx, uint32_t model_id, fsw_model_info* out);
 
@@ -195,6 +211,8 @@ typedef struct {
     uint32_t n_kernels;     /* kernels launched by this invoke (incl. the swap kernel)       */
     uint32_t engine;        /* FSW_ENGINE_SM / FSW_ENGINE_DMA for a cold invoke, else 0        */
     uint32_t n_copies;      /* swap pieces (SM) or copy-engine groups (DMA) of this invoke      */
+    uint64_t wire_bytes;    /* bytes that crossed the host / peer link (= bytes_swapped, except the
+                               link-coded engines, which move coded bytes)                      */
 } fsw_invoke_stats;
 
 /* Run one request: pick a GPU (resident and idle first, then the lowest idle id,
@@ -261,6 +279,19 @@ fsw_status fsw_n_gpus(fsw_ctx* ctx, uint32_t* n);
 /* Debug / test read-back (copies into caller host memory). */
 fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, void* dst, uint64_t cap);
 fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
+/* Link-coded store (FSW_REG_LINK_CODE): the coded bytes, and the piece table in execution order.
+ * Piece i covers store bytes [off, off + bytes) of layer `layer` (bytes <= 16 KiB, a multiple of 16)
+ * and is coded at [coff, coff + cbytes) of the coded store (coff a multiple of 128; gaps are zero).
+ * Its nb = ceil(bytes / 1024) blocks carry header bytes hdr[0..nb) (the rest 0); the coded piece is
+ * block b = raw bytes [off + 1024 b, ...) coded as, in order:
+ *   header 0     : the raw bytes (1024, or bytes − 1024 (nb − 1) for a partial last block);
+ *   header h ≥ 1 : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f) of the block's 16-bit words w_i,
+ *                  then 256 bytes of 4-bit codes (code of w_{2k} in the low nibble of byte k);
+ *                  exponent e_i = (w_i >> 7) & 0xff is 0 for code 15, else h − code.
+ * ENOTFOUND / ESTATE (model not link-coded) / EINVAL (cap too small; *n is still set).              */
+typedef struct { uint64_t off, coff; uint32_t bytes, cbytes, layer, pad; uint8_t hdr[16]; } fsw_coded_piece;
+fsw_status fsw_debug_read_coded(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
+fsw_status fsw_debug_coded_pieces(fsw_ctx* ctx, uint32_t model_id, fsw_coded_piece* out, uint32_t cap, uint32_t* n);
 /* Activation slot of the last invoke of `model_id` on `gpu` (valid until the next invoke). */
 fsw_status fsw_debug_read_slot(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, int32_t slot, void* dst, uint64_t cap);
 

@@ -162,7 +162,7 @@ struct Cfg {
 constexpr int kGemmThreads = 512;  // warp 0 TMA producer, warp 1 MMA issuer, all 16 in the epilogue
 
 template <int BN>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA (<= 64 regs) still fits beside it
     k_gemm(const __grid_constant__ CUtensorMap tmA, const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
     using C = Cfg<BN>;
     constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;

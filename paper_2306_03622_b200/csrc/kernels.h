@@ -70,6 +70,38 @@ constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
 void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapped, DevDesc dst, const DevDesc* desc,
                  const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys);
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
+// ---- exponent-coded link format ---------------------------------------------
+// A lossless recoding of the host store that moves ~25 % fewer bytes over the host link; the swap
+// kernel decodes it on the fly, so the extent receives the store's bytes bit-exactly.  The store is
+// cut into pieces of <= kZPiece raw bytes (never straddling a layer region); a piece is cut into
+// blocks of kZBlock raw bytes = 512 16-bit words, each with a header byte h (kept in the piece table,
+// in device memory).  Coded piece (128-B aligned in the coded store, so every warp load maps onto whole
+// 128-B host read requests) = the blocks in order:
+//   header h == 0 : raw block (kZBlock bytes, or the piece's tail bytes for a partial last block)
+//   header h >= 1 : kZCoded bytes = 512 bytes m_i = sign | 7 mantissa bits of word i, then 256 bytes
+//                   of 4-bit codes d_i (word 2k in the low nibble of byte k); the exponent is
+//                   e_i = (d_i == 15) ? 0 : h − d_i, so word i = (m_i & 0x80) << 8 | e_i << 7 | (m_i & 0x7f).
+// A block is coded when every non-zero exponent lies in [h − 14, h] (h = the largest), else raw.
+constexpr uint32_t kZPiece = 16384;
+constexpr uint32_t kZBlock = 1024;
+constexpr uint32_t kZCoded = 768;
+struct ZPiece {
+    uint64_t off;     // raw store offset == extent offset
+    uint64_t coff;    // offset of the coded piece in the coded store (multiple of 128)
+    uint32_t bytes;   // raw bytes (multiple of 16, <= kZPiece)
+    uint32_t layer;   // ready counter to bump
+    uint32_t grp;     // DMA+decode engine: copy group carrying the piece (decode waits for progress > grp)
+    uint32_t cbytes;  // coded bytes
+    uint8_t hdr[16];  // block headers (0 for blocks past the piece's end)
+};
+// Decoding swap kernel.  src + (coff − src_base) is a coded piece: the mapped coded host store
+// (stage = 0, zero-copy over the host link) or the device staging buffer the copy engine filled
+// (stage = 1; each piece first waits until *progress > grp).  Destinations, ready counters, gate and
+// sys as launch_swap.
+void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
+                  const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
+                  DevCtl* gate, int sys, int stage, const uint32_t* progress);
+
 void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl);
 
 // ---- layer ops ----------------------------------------------------------------------------
@@ -131,6 +163,7 @@ void launch_maxpool(cudaStream_t s, const PoolArgs& a);
 void launch_avgpool(cudaStream_t s, const PoolArgs& a);
 
 void init_gemm_attrs();
+void init_swap_attrs();
 void init_ops_attrs();
 
 // Host helper: build the TMA descriptor of a row-major bf16 activation [rows][cols].

@@ -26,6 +26,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -189,6 +190,15 @@ struct PieceSet {
     std::vector<Piece> host;
 };
 
+// Link-coded engines: the coded pieces one swap moves (store offsets >= from), with the DMA+decode
+// engine's copy groups over the coded bytes [group lo, hi) and each piece's group index.
+struct ZPieceSet {
+    ZPiece* dev = nullptr;
+    std::vector<ZPiece> host;
+    std::vector<std::pair<uint64_t, uint64_t>> groups;  // DMAZ: coded-store byte ranges, in order
+    uint64_t cfrom = 0, cend = 0;                        // coded bytes [cfrom, cend) cover the pieces
+};
+
 struct Plan {  // one model on one GPU
     bool built = false;
     std::vector<Launch> launches;
@@ -200,6 +210,9 @@ struct Plan {  // one model on one GPU
     std::map<std::tuple<uint64_t, uint32_t, uint64_t, uint64_t>, DmaPlan> dma;  // (group bytes, streams, from, split)
     // striped swap: source j of n gets every n-th piece; its table lives on the source's device
     std::map<std::tuple<uint64_t, uint32_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, n, j, device, from)
+    // link-coded engines: (order, seed, from, DMAZ group bytes or 0 for SMZ) and striped (n, j, device, from)
+    std::map<std::tuple<int, uint32_t, uint64_t, uint64_t>, ZPieceSet> zp;
+    std::map<std::tuple<uint32_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;
 };
 
 struct Model {
@@ -216,6 +229,10 @@ struct Model {
     uint8_t* store = nullptr;  // pinned, mapped host store (execution order)
     uint64_t store_bytes = 0, store_alloc = 0;
     bool store_wc = false;
+    // exponent-coded copy of the store (FSW_REG_LINK_CODE; kernels.h): pinned, mapped
+    uint8_t* zstore = nullptr;
+    uint64_t zbytes = 0, zalloc = 0;
+    std::vector<ZPiece> zpieces;  // execution order, grp = 0
     // residency per GPU
     std::vector<int64_t> extent;       // pool offset of the model (split = 0) or of its suffix, or -1
     // partial-parameter caching: store bytes [0, split) — whole layers —
@@ -258,6 +275,10 @@ struct Gpu {
     uint32_t* ready = nullptr;
     uint32_t ready_cap = 0;
     DevCtl* ctl = nullptr;
+    uint8_t* zstage = nullptr;   // DMAZ: device staging buffer for coded bytes (grown on demand)
+    uint64_t zstage_cap = 0;
+    uint32_t zstage_gen = 0;     // bumped on every reallocation (graphs bake the address)
+    cudaStream_t sz = nullptr;   // DMAZ: decode-kernel stream
     uint8_t* dstage = nullptr;   // device: [DevDesc | pad | input]
     uint8_t* hstage = nullptr;   // pinned: same layout
     uint8_t* hout = nullptr;     // pinned, mapped: output (written by k_finish)
@@ -326,9 +347,11 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaFree(nullptr));  // create the context now (one shared runtime per GPU)
     init_gemm_attrs();
     init_ops_attrs();
+    init_swap_attrs();
     CU(cudaStreamCreateWithFlags(&g.sx, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&g.sc, cudaStreamNonBlocking));
     g.sd[0] = g.sc;
+    CU(cudaStreamCreateWithFlags(&g.sz, cudaStreamNonBlocking));
     for (int j = 1; j < kMaxWaitSrc; ++j) CU(cudaStreamCreateWithFlags(&g.sd[j], cudaStreamNonBlocking));
     for (int j = 0; j < kMaxWaitSrc; ++j) CU(cudaEventCreateWithFlags(&g.evd[j], cudaEventDisableTiming));
     CU(cudaMalloc(&g.progress, 128 * kMaxWaitSrc));
@@ -389,9 +412,10 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
     if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 16 << 10;
     if (c->cfg.stripe_min_bytes == 0) c->cfg.stripe_min_bytes = 256ull << 20;
     if (c->cfg.dma_min_bytes == 0) c->cfg.dma_min_bytes = 32ull << 20;
+    if (c->cfg.dmaz_min_bytes == 0) c->cfg.dmaz_min_bytes = 128ull << 20;
     if (c->cfg.dma_group_bytes == 0) c->cfg.dma_group_bytes = 64ull << 20;
     if (c->cfg.dma_streams == 0) c->cfg.dma_streams = 1;
-    if (c->cfg.engine > FSW_ENGINE_DMA || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
+    if (c->cfg.engine > FSW_ENGINE_DMAZ || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
         return fail(FSW_EINVAL, "fsw_init: engine, dma_streams (1..4) or dma_group_bytes (multiple of 256) invalid");
     if (c->cfg.chunk_bytes % 256 || c->cfg.copy_threads % 32 || c->cfg.copy_threads > 512)
         return fail(FSW_EINVAL, "fsw_init: chunk_bytes must be a multiple of 256, copy_threads a multiple of 32 <= 512");
@@ -438,9 +462,18 @@ static void free_plan(Gpu& g, Plan& p) {
     p.pieces.clear();
     for (auto& kv : p.stripe) cudaFree(kv.second.dev);  // UVA: any current device
     p.stripe.clear();
+    for (auto& kv : p.zp) cudaFree(kv.second.dev);
+    p.zp.clear();
+    for (auto& kv : p.zstripe) cudaFree(kv.second.dev);
+    p.zstripe.clear();
 }
 
 static void free_store(Model& m, bool host_only) {
+    if (m.zstore) {
+        if (!host_only) cudaHostUnregister(m.zstore);
+        munmap(m.zstore, m.zalloc);
+        m.zstore = nullptr;
+    }
     if (!m.store) return;
     if (m.store_wc) {
         cudaFreeHost(m.store);
@@ -468,6 +501,8 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFree(g.ready);
         cudaFree(g.ctl);
         cudaFree(g.dstage);
+        cudaFree(g.zstage);
+        cudaStreamDestroy(g.sz);
         cudaFreeHost(g.hstage);
         cudaFreeHost(g.hout);
         cudaFreeHost(g.hctl);
@@ -650,6 +685,111 @@ static fsw_status check_layer(const Model& m, uint32_t li) {
     return FSW_OK;
 }
 
+// ---- exponent-coded link format (kernels.h) -----------------------------------
+// Header of a full block of 512 16-bit words: its largest exponent when every non-zero exponent is
+// within 14 of it (1 when all are zero), else 0 = stored raw.
+static uint8_t zheader(const uint16_t* w) {
+    uint32_t emax = 0, emin = 255;
+    for (uint32_t i = 0; i < kZBlock / 2; ++i) {
+        const uint32_t e = (w[i] >> 7) & 0xffu;
+        if (e) {
+            emax = std::max(emax, e);
+            emin = std::min(emin, e);
+        }
+    }
+    if (!emax) return 1;
+    return emax - emin <= 14 ? (uint8_t)emax : 0;
+}
+
+static void zencode_block(const uint16_t* w, uint32_t h, uint8_t* out /* kZCoded zeroed bytes */) {
+    for (uint32_t i = 0; i < kZBlock / 2; ++i) {
+        const uint32_t e = (w[i] >> 7) & 0xffu;
+        out[i] = (uint8_t)(((w[i] >> 8) & 0x80u) | (w[i] & 0x7fu));
+        out[512 + i / 2] |= (uint8_t)((e ? h - e : 15u) << (4 * (i & 1)));
+    }
+}
+
+template <typename F>
+static void parallel_for(size_t n, F f) {
+    const size_t T = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), 32));
+    if (n < 64 || T == 1) {
+        for (size_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    std::atomic<size_t> next{0};
+    for (size_t t = 0; t < T; ++t)
+        th.emplace_back([&]() {
+            for (size_t i; (i = next.fetch_add(256)) < n;)
+                for (size_t j = i; j < std::min(n, i + 256); ++j) f(j);
+        });
+    for (auto& t : th) t.join();
+}
+
+// Build the coded copy of m.store: pieces of <= kZPiece bytes per layer region in execution order,
+// headers first (parallel), then offsets, then the coded bytes (parallel) into a THP-backed mapping
+// that is pinned and mapped for zero-copy reads like the store itself.
+static fsw_status build_link_code(Model& m, bool host_only) {
+    std::vector<ZPiece>& pcs = m.zpieces;
+    pcs.clear();
+    for (uint32_t li = 0; li < m.layers.size(); ++li)
+        for (uint64_t o = 0; o < m.region_bytes[li]; o += kZPiece)
+            pcs.push_back({m.region_off[li] + o, 0, (uint32_t)std::min<uint64_t>(kZPiece, m.region_bytes[li] - o), li, 0, 0, {}});
+    const uint32_t bpp = kZPiece / kZBlock;
+    std::vector<uint8_t> hdr(pcs.size() * bpp, 0);
+    parallel_for(pcs.size(), [&](size_t i) {
+        const ZPiece& pc = pcs[i];
+        for (uint32_t b = 0; b < pc.bytes / kZBlock; ++b)
+            hdr[i * bpp + b] = zheader(reinterpret_cast<const uint16_t*>(m.store + pc.off + (uint64_t)b * kZBlock));
+    });
+    uint64_t cur = 0;
+    for (size_t i = 0; i < pcs.size(); ++i) {
+        ZPiece& pc = pcs[i];
+        const uint32_t nfull = pc.bytes / kZBlock;
+        uint32_t cb = pc.bytes - nfull * kZBlock;
+        for (uint32_t b = 0; b < nfull; ++b) cb += hdr[i * bpp + b] ? kZCoded : kZBlock;
+        pc.coff = cur;
+        pc.cbytes = cb;
+        memcpy(pc.hdr, &hdr[i * bpp], bpp);  // a partial last block's header stays 0 (raw)
+        cur = align_up(cur + cb, 128);
+    }
+    m.zbytes = cur;
+    m.zalloc = align_up(std::max<uint64_t>(cur, 1), 2 << 20);
+    void* p = mmap(nullptr, m.zalloc, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return fail(FSW_ENOMEM, "register: mmap of %llu coded bytes failed", (unsigned long long)m.zalloc);
+    madvise(p, m.zalloc, MADV_HUGEPAGE);
+    m.zstore = static_cast<uint8_t*>(p);
+    memset(m.zstore, 0, m.zalloc);  // alignment gaps stay zero
+    parallel_for(pcs.size(), [&](size_t i) {
+        const ZPiece& pc = pcs[i];
+        uint8_t* out = m.zstore + pc.coff;
+        const uint32_t nfull = pc.bytes / kZBlock, nb = (pc.bytes + kZBlock - 1) / kZBlock;
+        uint64_t o = 0;
+        for (uint32_t b = 0; b < nb; ++b) {
+            const uint8_t* raw = m.store + pc.off + (uint64_t)b * kZBlock;
+            const uint32_t h = b < nfull ? hdr[i * bpp + b] : 0;
+            if (h) {
+                memset(out + o, 0, kZCoded);
+                zencode_block(reinterpret_cast<const uint16_t*>(raw), h, out + o);
+                o += kZCoded;
+            } else {
+                const uint32_t n = b < nfull ? kZBlock : pc.bytes - nfull * kZBlock;
+                memcpy(out + o, raw, n);
+                o += n;
+            }
+        }
+    });
+    if (!host_only) {
+        cudaError_t e = cudaHostRegister(m.zstore, m.zalloc, cudaHostRegisterPortable | cudaHostRegisterMapped);
+        if (e != cudaSuccess) {
+            munmap(m.zstore, m.zalloc);
+            m.zstore = nullptr;
+            return fail(FSW_ECUDA, "register: cudaHostRegister (coded store): %s", cudaGetErrorString(e));
+        }
+    }
+    return FSW_OK;
+}
+
 extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, uint32_t* model_id) {
     if (!c || !model_id) return fail(FSW_EINVAL, "register: NULL argument");
     fsw_status s = validate(d);
@@ -758,6 +898,14 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
             return fail(FSW_ECUDA, "register: cudaHostRegister: %s", cudaGetErrorString(e));
         }
     }
+    if (d->flags & FSW_REG_LINK_CODE) {
+        if (!wc && !host_only) CU(cudaSetDevice(c->gpus[0].dev));
+        s = build_link_code(*m, host_only);
+        if (s != FSW_OK) {
+            free_store(*m, host_only);
+            return s;
+        }
+    }
     m->extent.assign(c->gpus.size(), -1);
     m->pextent.assign(c->gpus.size(), -1);
     m->pvalid.assign(c->gpus.size(), 0);
@@ -787,6 +935,7 @@ extern "C" fsw_status fsw_model_info_get(fsw_ctx* c, uint32_t id, fsw_model_info
     out->input_bytes = m->input_bytes;
     out->output_bytes = m->output_bytes;
     out->output_dtype = m->slots[m->output_slot].dtype;
+    out->coded_bytes = m->zstore ? m->zbytes : 0;
     return FSW_OK;
 }
 
@@ -1108,11 +1257,21 @@ static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams, uin
     // Taper: a group starting at `lo` aims at min(grp, max(tail_min, remaining / 2)) bytes, so the
     // groups shrink geometrically towards the end of the store.  The compute that trails the last
     // byte is then only the last small group's layers (big groups amortise the ~8 us per-copy
-    // setup of the copy engine; small ones bound the tail).
+    // setup of the copy engine; small ones bound the tail).  Ramp: at a layer boundary a group also
+    // closes once it holds ramp x the bytes already planned (>= tail_min), so the first layers land
+    // early and their compute starts while the rest streams (a layer larger than the ramp is not split
+    // for it: its kernel waits for its last byte anyway).
     const uint64_t total = m.store_bytes, tail_min = std::min<uint64_t>(grp, 1ull << 20);
     static const double frac = getenv("FSW_DMA_TAPER") ? atof(getenv("FSW_DMA_TAPER")) : 0.5;  // sweep hook
+    // sweep hook, default off: measured (tools/linkcode_bench.py, profiles/r01/linkcode/) ramp 1-4 cost the
+    // plain DMA engine 2-5 % on ResNet-50 and was neutral on BERT-base
+    static const double ramp = getenv("FSW_DMA_RAMP") ? atof(getenv("FSW_DMA_RAMP")) : 0.0;    // 0 = no ramp
     auto want = [&](uint64_t at) {
         return std::min(grp, std::max(tail_min, align_up((uint64_t)((double)(total - at) * frac), 256)));
+    };
+    auto want_close = [&](uint64_t at) {
+        if (ramp <= 0) return want(at);
+        return std::min(want(at), std::max(tail_min, (uint64_t)((double)(at - from) * ramp)));
     };
     for (size_t li = 0; li < nl; ++li) {
         const uint64_t ro = m.region_off[li], rb = m.region_bytes[li];
@@ -1129,7 +1288,7 @@ static DmaPlan make_dma_plan(const Model& m, uint64_t grp, uint32_t streams, uin
             }
         } else {
             hi = ro + rb;
-            if (hi - lo >= want(lo)) close();
+            if (hi - lo >= want_close(lo)) close();
         }
         last_group[li] = hi > lo ? (uint32_t)d.groups.size() : (uint32_t)d.groups.size() - 1;
     }
@@ -1174,6 +1333,85 @@ extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group
     return FSW_OK;
 }
 
+// Coded pieces of one link-coded swap (store offsets >= from) in the claim order.  DMAZ (grp > 0):
+// copy groups of whole pieces over the coded bytes, in execution order, tapered like the DMA engine's
+// (a group starting at coded offset `at` aims at min(grp, max(1 MiB, remaining / 2)) bytes), so the
+// decode and compute that trail the last group are short; each piece records its group.
+static fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
+                              ZPieceSet** out) {
+    const auto key = std::make_tuple(order, seed, from, grp);
+    auto it = p.zp.find(key);
+    if (it != p.zp.end()) {
+        *out = &it->second;
+        return FSW_OK;
+    }
+    ZPieceSet zs;
+    for (const ZPiece& pc : m.zpieces)
+        if (pc.off >= from) zs.host.push_back(pc);
+    if (zs.host.empty()) return fail(FSW_EINVAL, "link-coded swap with nothing to move");
+    zs.cfrom = zs.host.front().coff;
+    zs.cend = zs.host.back().coff + zs.host.back().cbytes;
+    if (grp) {
+        // the DMA engine's plan (make_dma_plan) over coded bytes: tail taper inside layers, head ramp
+        // at layer boundaries
+        static const double ramp = getenv("FSW_DMA_RAMP") ? atof(getenv("FSW_DMA_RAMP")) : 0.0;
+        const uint64_t tail_min = std::min<uint64_t>(grp, 1ull << 20);
+        uint64_t lo = zs.cfrom;
+        for (size_t i = 0; i < zs.host.size(); ++i) {
+            ZPiece& pc = zs.host[i];
+            pc.grp = (uint32_t)zs.groups.size();
+            const bool last = i + 1 == zs.host.size();
+            const uint64_t hi = last ? zs.cend : zs.host[i + 1].coff;
+            const uint64_t want = std::min(grp, std::max(tail_min, (zs.cend - lo) / 2));
+            const uint64_t want_close =
+                ramp > 0 ? std::min(want, std::max(tail_min, (uint64_t)((double)(lo - zs.cfrom) * ramp))) : want;
+            const bool boundary = last || zs.host[i + 1].layer != pc.layer;
+            if (last || hi - lo >= want || (boundary && hi - lo >= want_close)) {
+                zs.groups.push_back({lo, hi});
+                lo = hi;
+            }
+        }
+    }
+    if (order == FSW_ORDER_REVERSE) std::reverse(zs.host.begin(), zs.host.end());
+    if (order == FSW_ORDER_RANDOM) {
+        std::mt19937_64 rng(seed);
+        std::shuffle(zs.host.begin(), zs.host.end(), rng);
+    }
+    CU(cudaSetDevice(g.dev));
+    CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
+    CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
+    *out = &p.zp.emplace(key, std::move(zs)).first->second;
+    return FSW_OK;
+}
+
+// Striped link-coded swap: runs of 16 consecutive coded pieces (256 KiB of store) dealt round-robin to
+// n sources; source j's table lives on its device.
+static fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, int dev, uint64_t from, ZPieceSet** out) {
+    const auto key = std::make_tuple(n, j, dev, from);
+    auto it = p.zstripe.find(key);
+    if (it != p.zstripe.end()) {
+        *out = &it->second;
+        return FSW_OK;
+    }
+    ZPieceSet zs;
+    uint64_t q = 0;
+    for (const ZPiece& pc : m.zpieces) {
+        if (pc.off < from) continue;
+        if ((q++ / 16) % n == j) zs.host.push_back(pc);
+    }
+    CU(cudaSetDevice(dev));
+    if (!zs.host.empty()) {
+        CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
+        CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
+    }
+    *out = &p.zstripe.emplace(key, std::move(zs)).first->second;
+    return FSW_OK;
+}
+
+static bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_DMAZ; }
+// Engines whose layer kernels wait on per-layer byte counters (released by a swap kernel).
+static bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_coded(e); }
+
 struct InvokeCfg {
     bool cold, no_overlap;
     int engine;  // FSW_ENGINE_SM / FSW_ENGINE_DMA (resolved)
@@ -1187,6 +1425,7 @@ struct InvokeCfg {
     uint64_t from = 0;           // first swapped store byte (a cached prefix is skipped)
     bool striped = false;        // striped swap: sources launched outside the graph (fsw_invoke_ex)
     uint32_t local_ctas = 0;     // striped: swap CTAs running on the target GPU itself (gate)
+    uint64_t zgrp = 0;           // DMAZ: copy-group bytes
 };
 
 // Striped swap: the execution-order piece list of the SM engine dealt round-robin to n sources
@@ -1221,7 +1460,7 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
         w.ctl = g.ctl;
         w.layer = x.layer;
         if (ic.cold && m.region_bytes[x.layer] > 0 && m.region_off[x.layer] >= ic.from) {
-            if (ic.engine == FSW_ENGINE_SM) {
+            if (engine_bytes_ready(ic.engine)) {
                 w.n = 1;
                 w.ready[0] = g.ready + x.layer;
                 w.target[0] = (uint32_t)m.region_bytes[x.layer];
@@ -1260,31 +1499,62 @@ static PFN_writeValue32 get_write_value32() {
 // timing) and the gate; then the flag-gated layer kernels; then D2H of output and ctl.
 static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out) {
     PieceSet* ps = nullptr;
+    ZPieceSet* zs = nullptr;
     if (ic.cold && ic.engine == FSW_ENGINE_SM && !ic.striped) {
         fsw_status s = get_pieces(m, p, g, ic.chunk, ic.order, ic.seed, ic.from, &ps);
         if (s != FSW_OK) return s;
-        if (m.layers.size() > g.ready_cap) return fail(FSW_EINVAL, "too many layers");
     }
+    if (ic.cold && engine_coded(ic.engine) && !ic.striped) {
+        fsw_status s = get_zpieces(m, p, g, ic.order, ic.seed, ic.from, ic.engine == FSW_ENGINE_DMAZ ? ic.zgrp : 0, &zs);
+        if (s != FSW_OK) return s;
+        if (ic.engine == FSW_ENGINE_DMAZ && zs->cend - zs->cfrom > g.zstage_cap) return fail(FSW_EINVAL, "staging buffer too small");
+    }
+    if (ic.cold && (engine_bytes_ready(ic.engine) || ic.striped) && m.layers.size() > g.ready_cap)
+        return fail(FSW_EINVAL, "too many layers");
     CU(cudaSetDevice(g.dev));
     cudaStream_t sx = g.sx, sc = g.sc;
     CU(cudaStreamBeginCapture(sx, cudaStreamCaptureModeThreadLocal));
     // The swap starts as early as possible: the DMA engine needs only its counters reset; the SM
     // engine also reads the invoke descriptor and the control block.  The input (up to 300 KB for
     // ResNet-50) is copied after the fork, overlapping the swap.
-    const bool dma_cold = ic.cold && !ic.striped && ic.engine != FSW_ENGINE_SM;
+    const bool dma_cold = ic.cold && !ic.striped && ic.engine == FSW_ENGINE_DMA;
     if (dma_cold) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
     if (!dma_cold) cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr, cudaMemcpyHostToDevice, sx);
     // striped: the counters and the control block are reset before the sources start (outside)
     if (!ic.striped && !dma_cold) cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
     if (ic.cold && ic.striped && !ic.no_overlap && ic.local_ctas) launch_gate(sx, g.ctl, ic.local_ctas);
     if (ic.cold && !ic.striped) {
-        if (ic.engine == FSW_ENGINE_SM) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
+        if (engine_bytes_ready(ic.engine)) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
+        if (ic.engine == FSW_ENGINE_DMAZ) cudaMemsetAsync(g.progress, 0, 128, sx);
         cudaEventRecord(g.evfork, sx);
         cudaStreamWaitEvent(sc, g.evfork, 0);
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
+        const DevDesc* desc = reinterpret_cast<const DevDesc*>(g.dstage);
         if (ic.engine == FSW_ENGINE_SM) {
-            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, DevDesc{}, reinterpret_cast<const DevDesc*>(g.dstage),
-                        ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl, g.ctl, 0);
+            launch_swap(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.store, DevDesc{}, desc, ps->dev,
+                        (uint32_t)ps->host.size(), g.ready, g.ctl, g.ctl, 0);
+        } else if (ic.engine == FSW_ENGINE_SMZ) {
+            // zero-copy decode: coded pieces straight from the mapped coded store over the host link
+            launch_swapz(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.zstore, 0, DevDesc{}, desc, zs->dev,
+                         (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 0, nullptr);
+        } else if (ic.engine == FSW_ENGINE_DMAZ) {
+            // copy engine moves coded groups into the staging buffer (a fenced stream write of the group
+            // count after each); the decode kernel, forked onto its own stream, waits per piece for its
+            // group and decodes from HBM into the extent
+            static PFN_writeValue32 wv = get_write_value32();
+            if (!wv) return fail(FSW_ECUDA, "cuStreamWriteValue32 entry point unavailable");
+            cudaEventRecord(g.evd[0], sc);
+            cudaStreamWaitEvent(g.sz, g.evd[0], 0);
+            launch_swapz(g.sz, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
+                         (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 1, g.progress);
+            uint32_t cnt = 0;
+            for (const auto& gr : zs->groups) {
+                cudaMemcpyAsync(g.zstage + (gr.first - zs->cfrom), m.zstore + gr.first, gr.second - gr.first,
+                                cudaMemcpyHostToDevice, sc);
+                wv(sc, (CUdeviceptr)g.progress, (cuuint32_t)(++cnt), 0);
+            }
+            cudaEventRecord(g.evd[1], g.sz);
+            cudaStreamWaitEvent(sc, g.evd[1], 0);
         } else {
             // Copy-engine DMA from the pinned store (the paper's transfer) in
             // layer-aligned groups (its "group" pipelining unit), dealt round-robin
@@ -1318,7 +1588,7 @@ static fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const Invok
     cudaMemcpyAsync(g.dstage + kStageHdr, g.hstage + kStageHdr, m.input_bytes, cudaMemcpyHostToDevice, sx);
     if (ic.cold && !ic.striped) {
         if (ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
-        else if (ic.engine == FSW_ENGINE_SM) launch_gate(sx, g.ctl, ic.ctas);
+        else if (engine_bytes_ready(ic.engine)) launch_gate(sx, g.ctl, ic.ctas);
     }
     enqueue_layers(m, p, g, ic, sx);
     if (ic.cold && !ic.striped && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);  // swap stamps final
@@ -1663,12 +1933,17 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     const bool baseline = (flags & FSW_DMA_BASELINE) != 0;
     int engine = (int)(o.engine ? o.engine : c->cfg.engine);
     if (baseline) engine = FSW_ENGINE_DMA;
-    if (engine == FSW_ENGINE_AUTO) engine = m->store_bytes >= c->cfg.dma_min_bytes ? FSW_ENGINE_DMA : FSW_ENGINE_SM;
-    if (striped) engine = FSW_ENGINE_SM;  // sources store into the target with SM kernels
+    const bool big = m->store_bytes >= c->cfg.dma_min_bytes;
+    if (engine == FSW_ENGINE_AUTO)
+        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
+                           : (big ? FSW_ENGINE_DMA : FSW_ENGINE_SM);
+    if (engine_coded(engine) && !m->zstore) return finish(fail(FSW_EINVAL, "invoke: model %u is not link-coded (FSW_REG_LINK_CODE)", id));
+    // striped: sources store into the target with SM kernels (decoding ones for the coded engines)
+    if (striped) engine = engine_coded(engine) ? FSW_ENGINE_SMZ : FSW_ENGINE_SM;
     if (peer >= 0) engine = FSW_ENGINE_DMA;  // NVLink copy-engine transfer from the peer's extent
     const uint64_t dgrp = baseline ? (2ull << 20) : o.dma_group_bytes ? o.dma_group_bytes : c->cfg.dma_group_bytes;
     const uint32_t dstr = baseline ? 1u : o.dma_streams ? o.dma_streams : c->cfg.dma_streams;
-    if (engine > FSW_ENGINE_DMA || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
+    if (engine > FSW_ENGINE_DMAZ || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
         return finish(fail(FSW_EINVAL, "invoke: bad engine / dma_group_bytes / dma_streams"));
     auto extents = [&](int i) {  // the model's extents on pool GPU i
         return DevDesc{c->gpus[i].pool + (m->pextent[i] >= 0 ? m->pextent[i] : 0), c->gpus[i].pool + m->extent[i], m->split, 0};
@@ -1679,16 +1954,34 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     ic.from = pcached ? m->split : 0;
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
     if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr, ic.from);
+    ic.zgrp = dgrp;
+    if (cold && engine == FSW_ENGINE_DMAZ && !striped && g.zstage_cap < m->zbytes) {
+        // grow the staging buffer (graphs bake its address: the generation is part of their key)
+        cudaFree(g.zstage);
+        g.zstage = nullptr;
+        g.zstage_cap = 0;
+        const uint64_t cap = align_up(m->zbytes, 64ull << 20);
+        if (cudaMalloc(&g.zstage, cap) != cudaSuccess) {
+            cudaGetLastError();
+            return finish(fail(FSW_ENOMEM, "invoke: staging buffer of %llu bytes", (unsigned long long)cap));
+        }
+        g.zstage_cap = cap;
+        g.zstage_gen++;
+    }
     if (peer >= 0) {
         ic.src = extents(peer);
         ic.src_host = false;
     }
-    const bool sm = engine == FSW_ENGINE_SM;
+    const bool sm = engine_bytes_ready(engine);  // a swap kernel releases per-layer byte counters
     // striped: every source claims pieces of >= 256 KiB (one system-scope fence + release each)
     const uint64_t schunk = std::max<uint64_t>(ic.chunk, 256ull << 10);
     std::vector<PieceSet*> sps(srcs.size(), nullptr);
+    std::vector<ZPieceSet*> zps(srcs.size(), nullptr);
     for (size_t j = 0; j < srcs.size(); ++j) {
-        st = get_stripe_pieces(*m, p, schunk, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &sps[j]);
+        if (engine == FSW_ENGINE_SMZ)
+            st = get_zstripe_pieces(*m, p, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &zps[j]);
+        else
+            st = get_stripe_pieces(*m, p, schunk, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &sps[j]);
         if (st != FSW_OK) return finish(st);
     }
     if (striped) {
@@ -1696,10 +1989,12 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         ic.striped = true;
         ic.local_ctas = ic.ctas * (uint32_t)srcs.size();  // the gate waits for every source kernel
     }
+    const bool coded = engine_coded(engine);
     GraphKey key{cold, (int)(flags & FSW_NO_OVERLAP), cold && sm && !striped ? ic.order : 0, cold ? engine + (striped ? 8 : 0) : 0,
-                 cold && !striped ? (sm ? ic.chunk : dgrp) : 0, cold && sm && !striped ? ic.seed : 0,
-                 cold ? (striped ? ic.local_ctas : sm ? ic.ctas : dstr) : 0, 0};
+                 cold && !striped ? (engine == FSW_ENGINE_SM ? ic.chunk : engine == FSW_ENGINE_SMZ ? 0 : dgrp) : 0,
+                 cold && sm && !striped ? ic.seed : 0, cold ? (striped ? ic.local_ctas : sm ? ic.ctas : dstr) : 0, 0};
     key.from = cold ? ic.from : 0;
+    if (cold && engine == FSW_ENGINE_DMAZ && !striped) key.extra = g.zstage_gen;  // baked staging address
     if (cold && !sm) {  // DMA graphs bake addresses: the target extents and a peer source's extents
         key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);
         key.pext = m->pextent[gi];
@@ -1739,8 +2034,12 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             cudaStreamWaitEvent(sl.st, g.evfork, 0);
             cudaMemsetAsync(sl.ctl, 0, sizeof(DevCtl), sl.st);
             // an empty share still starts its CTAs: the target's gate counts every source kernel
-            launch_swap(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->store, ic.dst, nullptr, sps[j]->dev,
-                        (uint32_t)sps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1);
+            if (engine == FSW_ENGINE_SMZ)
+                launch_swapz(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->zstore, 0, ic.dst, nullptr, zps[j]->dev,
+                             (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 0, nullptr);
+            else
+                launch_swap(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->store, ic.dst, nullptr, sps[j]->dev,
+                            (uint32_t)sps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1);
             cudaEventRecord(sl.done, sl.st);
         }
         cudaSetDevice(g.dev);
@@ -1776,6 +2075,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             stats->swap_ms = swap_ms;
             stats->bytes_swapped = m->store_bytes - ic.from;
             stats->link_gbps = swap_ms > 0 ? stats->bytes_swapped / (swap_ms * 1e6) : 0;
+            stats->wire_bytes = stats->bytes_swapped;
             stats->engine = (uint32_t)engine;
             if (striped) {
                 float tail = 0;
@@ -1783,8 +2083,22 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                 stats->swap_span_ms = swap_ms;
                 stats->compute_tail_ms = tail > 0 ? tail : 0;
                 stats->n_kernels += (uint32_t)srcs.size() + (ic.no_overlap ? 0 : 1);  // sources (+ gate)
-                for (PieceSet* ps : sps) stats->n_copies += (uint32_t)ps->host.size();
-            } else if (sm) {
+                for (size_t j = 0; j < srcs.size(); ++j) stats->n_copies += (uint32_t)(coded ? zps[j]->host.size() : sps[j]->host.size());
+                if (coded) {
+                    stats->wire_bytes = 0;
+                    for (ZPieceSet* zs : zps)
+                        for (const ZPiece& pc : zs->host) stats->wire_bytes += pc.cbytes;
+                }
+            } else if (coded) {
+                if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
+                if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
+                stats->n_kernels += ic.no_overlap ? 1 : 2;  // decoding swap kernel (+ gate)
+                ZPieceSet* zs = nullptr;
+                if (get_zpieces(*m, p, g, ic.order, ic.seed, ic.from, engine == FSW_ENGINE_DMAZ ? dgrp : 0, &zs) == FSW_OK) {
+                    stats->n_copies = (uint32_t)(engine == FSW_ENGINE_DMAZ ? zs->groups.size() : zs->host.size());
+                    stats->wire_bytes = zs->cend - zs->cfrom;
+                }
+            } else if (engine == FSW_ENGINE_SM) {
                 if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
                 if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
                 stats->n_kernels += ic.no_overlap ? 1 : 2;  // swap (+ gate)
@@ -1842,6 +2156,30 @@ extern "C" fsw_status fsw_debug_read_resident(fsw_ctx* c, uint32_t id, int32_t g
     if (m->split) CU(cudaMemcpy(dst, pool + m->pextent[gpu], m->split, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(static_cast<uint8_t*>(dst) + m->split, pool + m->extent[gpu], m->store_bytes - m->split,
                   cudaMemcpyDeviceToHost));
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_read_coded(fsw_ctx* c, uint32_t id, void* dst, uint64_t cap) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!m->zstore) return fail(FSW_ESTATE, "model %u is not link-coded", id);
+    if (!dst || cap < m->zbytes) return fail(FSW_EINVAL, "read_coded: cap %llu < %llu", (unsigned long long)cap, (unsigned long long)m->zbytes);
+    memcpy(dst, m->zstore, m->zbytes);
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_coded_pieces(fsw_ctx* c, uint32_t id, fsw_coded_piece* out, uint32_t cap, uint32_t* n) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!m->zstore) return fail(FSW_ESTATE, "model %u is not link-coded", id);
+    if (!n) return fail(FSW_EINVAL, "coded_pieces: n is NULL");
+    *n = (uint32_t)m->zpieces.size();
+    if (m->zpieces.size() > cap || (!out && cap)) return fail(FSW_EINVAL, "coded_pieces: cap %u < %u", cap, *n);
+    for (size_t i = 0; i < m->zpieces.size(); ++i) {
+        const ZPiece& z = m->zpieces[i];
+        out[i] = {z.off, z.coff, z.bytes, z.cbytes, z.layer, 0, {}};
+        memcpy(out[i].hdr, z.hdr, sizeof z.hdr);
+    }
     return FSW_OK;
 }
 

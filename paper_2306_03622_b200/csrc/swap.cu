@@ -57,6 +57,160 @@ void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapp
     k_swap<8><<<ctas, threads, 0, s>>>(host_mapped, dst, desc, pieces, n_pieces, ready, own, gate, sys);
 }
 
+// ---- exponent-coded link format (kernels.h) -----------------------------------
+// Loads of coded bytes: from the mapped host store they are read once, non-allocating; from the
+// staging buffer (written by the copy engine, published by a fenced stream write) they are
+// L2-coherent .cg loads ordered after the acquire of the group counter.
+template <bool STAGE>
+__device__ __forceinline__ uint4 zld4(const uint8_t* p) {
+    uint4 r;
+    if (STAGE)
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+template <bool STAGE>
+__device__ __forceinline__ uint2 zld2(const uint8_t* p) {
+    uint2 r;
+    if (STAGE)
+        asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+    return r;
+}
+// word = sign | exponent | mantissa from the stored byte m = sign | mantissa and the code d.
+__device__ __forceinline__ uint32_t zword(uint32_t m, uint32_t d, uint32_t h) {
+    const uint32_t e = d == 15u ? 0u : h - d;
+    return ((m & 0x80u) << 8) | (e << 7) | (m & 0x7fu);
+}
+// Lane l of a coded block: words 16l .. 16l+15 from 16 stored bytes and 8 code bytes.
+__device__ __forceinline__ void zdecode16(const uint4 sm, const uint2 nb, uint32_t h, uint4& o0, uint4& o1) {
+    const uint32_t s[4] = {sm.x, sm.y, sm.z, sm.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t mm = s[k >> 1] >> (16 * (k & 1));
+        const uint32_t nn = (k < 4 ? nb.x : nb.y) >> (8 * (k & 3));
+        o[k] = zword(mm & 0xffu, nn & 15u, h) | (zword((mm >> 8) & 0xffu, (nn >> 4) & 15u, h) << 16);
+    }
+    o0 = make_uint4(o[0], o[1], o[2], o[3]);
+    o1 = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+__device__ __forceinline__ void wait_geq(const uint32_t* p, uint32_t v, DevCtl* ctl) {
+    if (ld_acquire_gpu(p) >= v) return;
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 64;
+    while (ld_acquire_gpu(p) < v) {
+        __nanosleep(ns);
+        if (ns < 512) ns <<= 1;
+        if (globaltimer() - t0 > kWatchdogNs) {
+            atomicExch(&ctl->err, 1);
+            atomicExch(&ctl->err_layer, -1);
+            return;
+        }
+    }
+}
+
+// Persistent warps claim coded pieces in the table's order (execution order), decode U blocks at a
+// time (all loads of the U blocks issued before any store, so a warp keeps ~3 KB of host reads in
+// flight), store 128-bit words into the extent and release the piece's raw bytes on its layer's
+// counter — the same readiness protocol as k_swap, so layer kernels cannot tell the engines apart.
+template <bool STAGE, int U>
+__global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_t src_base, DevDesc dst,
+                                               const DevDesc* __restrict__ desc, const ZPiece* __restrict__ pieces,
+                                               uint32_t n_pieces, uint32_t* __restrict__ ready, DevCtl* __restrict__ own,
+                                               DevCtl* gate, int sys, const uint32_t* progress) {
+    if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
+    const DevDesc dd = desc ? *desc : dst;
+    const uint32_t lane = threadIdx.x & 31u;
+    for (;;) {
+        uint32_t p = 0;
+        if (lane == 0) p = atomicAdd(&own->ticket, 1u);
+        p = __shfl_sync(0xffffffffu, p, 0);
+        if (p >= n_pieces) break;
+        if (p == 0 && lane == 0) own->t_first = globaltimer();
+        const ZPiece pc = pieces[p];
+        if (STAGE) {
+            if (lane == 0) wait_geq(progress, pc.grp + 1, own);
+            __syncwarp();
+        }
+        const uint8_t* cp = src + (pc.coff - src_base);
+        uint8_t* out = weight_ptr(dd, pc.off);
+        const uint32_t nfull = pc.bytes / kZBlock, nb = (pc.bytes + kZBlock - 1) / kZBlock;  // nb <= 16
+        // header byte (from the device piece table) and coded offset of block `lane` (exclusive scan)
+        const uint32_t h = lane < nb ? (uint32_t)__ldg(&pieces[p].hdr[lane]) : 0u;
+        const uint32_t sz = lane < nfull ? (h ? kZCoded : kZBlock) : lane < nb ? pc.bytes - nfull * kZBlock : 0u;
+        uint32_t incl = sz;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += t;
+        }
+        const uint32_t boff = incl - sz;
+        for (uint32_t b0 = 0; b0 < nfull; b0 += U) {
+            uint4 q0[U], q1[U];
+            uint32_t hh[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t b = b0 + u;
+                hh[u] = __shfl_sync(0xffffffffu, h, b & 31u);
+                const uint32_t ob = __shfl_sync(0xffffffffu, boff, b & 31u);
+                if (b < nfull) {
+                    q0[u] = zld4<STAGE>(cp + ob + lane * 16u);
+                    if (hh[u]) {
+                        const uint2 t = zld2<STAGE>(cp + ob + 512u + lane * 8u);
+                        q1[u] = make_uint4(t.x, t.y, 0u, 0u);
+                    } else {
+                        q1[u] = zld4<STAGE>(cp + ob + 512u + lane * 16u);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t b = b0 + u;
+                if (b >= nfull) break;
+                uint4* ob = reinterpret_cast<uint4*>(out + (uint64_t)b * kZBlock);
+                if (hh[u]) {
+                    uint4 o0, o1;
+                    zdecode16(q0[u], make_uint2(q1[u].x, q1[u].y), hh[u], o0, o1);
+                    st_v4(ob + 2 * lane, o0);
+                    st_v4(ob + 2 * lane + 1, o1);
+                } else {
+                    st_v4(ob + lane, q0[u]);
+                    st_v4(ob + 32 + lane, q1[u]);
+                }
+            }
+        }
+        if (nb > nfull) {  // raw tail of a layer region (< 1 KiB)
+            const uint32_t ob = __shfl_sync(0xffffffffu, boff, nfull & 31u);
+            const uint32_t n16 = (pc.bytes - nfull * kZBlock) >> 4;
+            uint4* o = reinterpret_cast<uint4*>(out + (uint64_t)nfull * kZBlock);
+            for (uint32_t i = lane; i < n16; i += 32) st_v4(o + i, zld4<STAGE>(cp + ob + i * 16u));
+        }
+        if (sys) {
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) red_release_sys_add(&ready[pc.layer], pc.bytes);
+        } else {
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) red_release_gpu_add(&ready[pc.layer], pc.bytes);
+        }
+        if (lane == 0) atomicMax(&own->t_last, (unsigned long long)globaltimer());
+    }
+}
+
+void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
+                  const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
+                  DevCtl* gate, int sys, int stage, const uint32_t* progress) {
+    if (stage)
+        k_swapz<true, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
+    else
+        k_swapz<false, 4><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
+}
+
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap
 // CTA is resident, so spinning layer CTAs can never occupy the SMs the swap needs
 // (no deadlock whatever the block scheduler does).  One thread; costs one launch.
@@ -92,5 +246,9 @@ void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t byt
     const uint64_t want = (bytes + 4095) / 4096;
     k_finish<<<(unsigned)(want < 1 ? 1 : want > 148 ? 148 : want), 256, 0, s>>>(ctl, out, bytes, host_out, host_ctl);
 }
+
+// No carveout preference for the swap kernels (measured: a max-shared carveout on every kernel made
+// the SM engine slower, e.g. BERT-base 4.30 -> 4.76 ms, and did not shorten the layer kernels).
+void init_swap_attrs() {}
 
 }  // namespace fsw

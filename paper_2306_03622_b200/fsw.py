@@ -21,7 +21,8 @@ STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA
 NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP = 0x1, 0x2, 0x4, 0x8, 0x10
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
-ENGINE_AUTO, ENGINE_SM, ENGINE_DMA = 0, 1, 2
+ENGINE_AUTO, ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ = 0, 1, 2, 3, 4
+REG_LINK_CODE = 0x2
 EVICT_KEEP_PREFIX = 0x1
 
 u32, u64, i32, dbl, vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
@@ -38,7 +39,7 @@ class Config(ctypes.Structure):
                 ("workspace_bytes_per_gpu", u64), ("copy_ctas", u32), ("copy_threads", u32),
                 ("chunk_bytes", u64), ("stripe_min_bytes", u64), ("flags", u32), ("engine", u32),
                 ("dma_min_bytes", u64), ("dma_group_bytes", u64), ("dma_streams", u32),
-                ("pcie_neighbor", ctypes.POINTER(i32))]
+                ("pcie_neighbor", ctypes.POINTER(i32)), ("dmaz_min_bytes", u64)]
 
 
 class Tensor(ctypes.Structure):
@@ -65,7 +66,8 @@ class ModelDesc(ctypes.Structure):
 
 class ModelInfo(ctypes.Structure):
     _fields_ = [("store_bytes", u64), ("algorithmic_bytes", u64), ("n_layers", u32), ("n_tensors", u32),
-                ("n_gemm_layers", u32), ("input_bytes", u64), ("output_bytes", u64), ("output_dtype", u32)]
+                ("n_gemm_layers", u32), ("input_bytes", u64), ("output_bytes", u64), ("output_dtype", u32),
+                ("coded_bytes", u64)]
 
 
 class StoreTensor(ctypes.Structure):
@@ -76,10 +78,16 @@ class StoreTensor(ctypes.Structure):
 class InvokeStats(ctypes.Structure):
     _fields_ = [("total_ms", dbl), ("device_ms", dbl), ("swap_ms", dbl), ("swap_span_ms", dbl),
                 ("compute_tail_ms", dbl), ("bytes_swapped", u64), ("link_gbps", dbl), ("gpu", i32),
-                ("swap_kind", u32), ("n_sources", u32), ("n_kernels", u32), ("engine", u32), ("n_copies", u32)]
+                ("swap_kind", u32), ("n_sources", u32), ("n_kernels", u32), ("engine", u32), ("n_copies", u32),
+                ("wire_bytes", u64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class CodedPiece(ctypes.Structure):
+    _fields_ = [("off", u64), ("coff", u64), ("bytes", u32), ("cbytes", u32), ("layer", u32), ("pad", u32),
+                ("hdr", ctypes.c_uint8 * 16)]
 
 
 class InvokeOpts(ctypes.Structure):
@@ -137,7 +145,8 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_arena_stats", "fsw_debug_dma_plan", "fsw_policy_rrc", "fsw_policy_partition", "fsw_policy_alpha",
            "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
-           "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix"]
+           "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
+           "fsw_debug_read_coded", "fsw_debug_coded_pieces"]
 
 _lib = None
 
@@ -168,6 +177,8 @@ def lib():
         L.fsw_debug_read_resident.argtypes = [vp, u32, i32, vp, u64]
         L.fsw_debug_read_store.argtypes = [vp, u32, vp, u64]
         L.fsw_debug_read_slot.argtypes = [vp, u32, i32, i32, vp, u64]
+        L.fsw_debug_read_coded.argtypes = [vp, u32, vp, u64]
+        L.fsw_debug_coded_pieces.argtypes = [vp, u32, vp, u32, ctypes.POINTER(u32)]
         L.fsw_arena_create.argtypes = [u64, u64]
         L.fsw_arena_create.restype = vp
         L.fsw_arena_destroy.argtypes = [vp]
@@ -244,7 +255,7 @@ class Runtime:
     def __init__(self, n_gpus: int = 0, gpu_ids: Optional[Sequence[int]] = None, pool_bytes: int = 0,
                  workspace_bytes: int = 0, copy_ctas: int = 0, copy_threads: int = 0, chunk_bytes: int = 0,
                  flags: int = 0, engine: int = ENGINE_AUTO, dma_min_bytes: int = 0, dma_group_bytes: int = 0,
-                 dma_streams: int = 0, stripe_min_bytes: int = 0):
+                 dma_streams: int = 0, stripe_min_bytes: int = 0, dmaz_min_bytes: int = 0):
         cfg = Config()
         cfg.n_gpus = n_gpus or (len(gpu_ids) if gpu_ids else 0)
         self._ids = (i32 * len(gpu_ids))(*gpu_ids) if gpu_ids else None
@@ -254,6 +265,7 @@ class Runtime:
         cfg.copy_ctas, cfg.copy_threads, cfg.chunk_bytes, cfg.flags = copy_ctas, copy_threads, chunk_bytes, flags
         cfg.engine, cfg.dma_min_bytes, cfg.dma_group_bytes, cfg.dma_streams = engine, dma_min_bytes, dma_group_bytes, dma_streams
         cfg.stripe_min_bytes = stripe_min_bytes
+        cfg.dmaz_min_bytes = dmaz_min_bytes
         h = vp()
         _check(lib().fsw_init(ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
@@ -278,7 +290,7 @@ class Runtime:
 
     # ---- registration -------------------------------------------------------------------
     def register(self, name: str, weights: np.ndarray, tensors, refs, slots, layers, input_slot: int,
-                 output_slot: int) -> int:
+                 output_slot: int, flags: int = 0) -> int:
         """tensors: [(offset, bytes, dtype, shape)], slots: [(dtype, shape)],
         layers: [(op, first_ref, n_refs, in0, in1, out, attr[8])], refs: [tensor index]."""
         T = (Tensor * max(1, len(tensors)))()
@@ -299,15 +311,16 @@ class Runtime:
         R = (u32 * max(1, len(refs)))(*refs)
         w = np.ascontiguousarray(weights).view(np.uint8)
         d = ModelDesc(name.encode(), w.ctypes.data, w.nbytes, T, len(tensors), R, len(refs), S, len(slots), Ls,
-                      len(layers), input_slot, output_slot, 0)
+                      len(layers), input_slot, output_slot, flags)
         mid = u32()
         _check(lib().fsw_register_model(self.h, ctypes.byref(d), ctypes.byref(mid)))
         info = self.model_info(mid.value)
         self._models[mid.value] = info
         return mid.value
 
-    def register_spec(self, spec, weights: np.ndarray) -> int:
-        """Register a synth.ModelSpec-shaped description (duck-typed)."""
+    def register_spec(self, spec, weights: np.ndarray, link_code: bool = False) -> int:
+        """Register a synth.ModelSpec-shaped description (duck-typed); link_code builds the
+        exponent-coded store the SMZ / DMAZ engines move (FSW_REG_LINK_CODE)."""
         spec.assign_offsets()
         tensors = [(t.offset, t.nbytes, t.dtype, t.shape) for t in spec.tensors]
         slots = [(s.dtype, s.shape) for s in spec.slots]
@@ -315,7 +328,8 @@ class Runtime:
         for l in spec.layers:
             layers.append((int(l.op), len(refs), len(l.refs), l.in0, l.in1, l.out, list(l.attr)))
             refs += list(l.refs)
-        return self.register(spec.name, weights, tensors, refs, slots, layers, spec.input_slot, spec.output_slot)
+        return self.register(spec.name, weights, tensors, refs, slots, layers, spec.input_slot, spec.output_slot,
+                             REG_LINK_CODE if link_code else 0)
 
     def unregister(self, mid: int):
         _check(lib().fsw_unregister_model(self.h, mid))
@@ -401,6 +415,22 @@ class Runtime:
         buf = np.empty(n, dtype=np.uint8)
         _check(lib().fsw_debug_read_store(self.h, mid, buf.ctypes.data, n))
         return buf
+
+    def read_coded(self, mid: int) -> np.ndarray:
+        n = self.model_info(mid)["coded_bytes"]
+        buf = np.empty(n, dtype=np.uint8)
+        _check(lib().fsw_debug_read_coded(self.h, mid, buf.ctypes.data, n))
+        return buf
+
+    def coded_pieces(self, mid: int) -> np.ndarray:
+        """Piece table of the link-coded store: structured array (off, coff, bytes, cbytes, layer, hdr[16])."""
+        n = u32()
+        lib().fsw_debug_coded_pieces(self.h, mid, None, 0, ctypes.byref(n))
+        arr = (CodedPiece * max(1, n.value))()
+        _check(lib().fsw_debug_coded_pieces(self.h, mid, arr, n.value, ctypes.byref(n)))
+        dt = np.dtype([("off", "<u8"), ("coff", "<u8"), ("bytes", "<u4"), ("cbytes", "<u4"), ("layer", "<u4"),
+                       ("pad", "<u4"), ("hdr", "u1", (16,))])
+        return np.frombuffer(bytes(arr), dtype=dt)[:n.value].copy()
 
     def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:
         buf = np.empty(nbytes, dtype=np.uint8)

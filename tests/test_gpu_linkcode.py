@@ -1,0 +1,138 @@
+"""GPU: the link-coded engines (SMZ: zero-copy decode from the mapped coded store; DMAZ: copy-engine
+DMA of coded groups into HBM staging + decode kernel) land the host store in the extent bit-exactly
+(SURVEY §8c 'Swap (K1/K2)' pin) for every model class, claim order, CTA count, group size and mode,
+and the outputs are bit-identical to the plain engines' (the decoded bytes are the same bytes)."""
+import numpy as np
+import pytest
+
+import synth
+from paper_2306_03622_b200 import (DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, NO_OVERLAP,
+                                   ORDER_RANDOM, ORDER_REVERSE, FswError)
+from paper_2306_03622_b200 import fsw as F
+from test_gpu_swap import _odd_model
+
+pytestmark = pytest.mark.gpu
+
+_CODED = {}
+
+
+@pytest.fixture(scope="module")
+def coded(rt, registered):
+    def get(name):
+        if name not in _CODED:
+            spec, w, x, mid = registered(name)
+            _CODED[name] = (spec, w, x, mid, rt.register_spec(spec, w, link_code=True))
+        return _CODED[name]
+    return get
+
+
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("name", ["mlp", "bert-base", "resnet50", "gpt2-2L"])
+def test_coded_swap_bit_exact_and_output_identical(rt, coded, name, engine):
+    spec, w, x, plain, mid = coded(name)
+    rt.evict(plain)
+    base = rt.invoke(plain, x, gpu=0, engine=ENGINE_SM).output.copy()
+    info = rt.model_info(mid)
+    rt.evict(mid)
+    r = rt.invoke(mid, x, gpu=0, engine=engine)
+    assert r.stats["swap_kind"] == 1 and r.stats["engine"] == engine, r.stats
+    assert r.stats["bytes_swapped"] == info["store_bytes"] and r.stats["wire_bytes"] == info["coded_bytes"]
+    np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    np.testing.assert_array_equal(r.output, base)
+    r2 = rt.invoke(mid, x, gpu=0)  # warm
+    assert r2.stats["swap_kind"] == 0
+    np.testing.assert_array_equal(r2.output, base)
+
+
+def test_auto_engine_picks_coded_engines(rt, coded):
+    for name, want in (("mlp", ENGINE_SMZ), ("bert-base", ENGINE_DMAZ)):
+        spec, w, x, plain, mid = coded(name)
+        rt.evict(mid)
+        assert rt.invoke(mid, x, gpu=0).stats["engine"] == want
+        rt.evict(plain)
+        assert rt.invoke(plain, x, gpu=0).stats["engine"] in (ENGINE_SM, ENGINE_DMA)
+
+
+@pytest.mark.parametrize("ctas", [1, 4, 16, 148])
+def test_smz_orders_and_ctas_bit_exact(rt, ctas):
+    spec = _odd_model([1, 256, 65537, 600_000])  # layer tails of 16 B .. not multiples of 1 KiB
+    mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
+    try:
+        for order in (0, ORDER_REVERSE, ORDER_RANDOM):
+            for flags in (0, NO_OVERLAP):
+                rt.evict(mid)
+                rt.invoke(mid, spec.make_input(), gpu=0, copy_ctas=ctas, order=order, order_seed=ctas,
+                          engine=ENGINE_SMZ, flags=flags)
+                np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    finally:
+        rt.unregister(mid)
+
+
+@pytest.mark.parametrize("grp", [256, 4096, 64 << 10, 2 << 20, 64 << 20])
+def test_dmaz_group_sweep_bit_exact(rt, grp):
+    spec = _odd_model([1, 256, 65537, 600_000])
+    mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
+    try:
+        for order, flags in ((0, 0), (0, NO_OVERLAP), (ORDER_REVERSE, 0), (ORDER_RANDOM, 0)):
+            rt.evict(mid)
+            r = rt.invoke(mid, spec.make_input(), gpu=0, engine=ENGINE_DMAZ, dma_group_bytes=grp, flags=flags,
+                          order=order, order_seed=grp)
+            assert r.stats["engine"] == ENGINE_DMAZ and r.stats["n_copies"] >= 1
+            np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    finally:
+        rt.unregister(mid)
+
+
+@pytest.mark.parametrize("n_src", [2, 3])
+def test_striped_smz_virtual_sources_bit_exact(rt, coded, n_src):
+    spec, w, x, plain, mid = coded("bert-base")
+    rt.evict(plain)
+    base = rt.invoke(plain, x, gpu=0, engine=ENGINE_SM).output.copy()
+    for flags in (0, NO_OVERLAP):
+        rt.evict(mid)
+        r = rt.invoke(mid, x, gpu=0, stripe=[0] * n_src, flags=flags, engine=ENGINE_SMZ)
+        assert r.stats["swap_kind"] == 3 and r.stats["engine"] == ENGINE_SMZ, r.stats
+        assert r.stats["wire_bytes"] == rt.model_info(mid)["coded_bytes"]
+        np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+        np.testing.assert_array_equal(r.output, base)
+
+
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+def test_coded_with_cached_prefix(rt, coded, engine):
+    """Partial caching (NEXT #4) + link coding: only the coded suffix moves."""
+    spec, w, x, plain, mid = coded("bert-base")
+    rt.evict(mid)
+    base = rt.invoke(mid, x, gpu=0, engine=engine).output.copy()
+    rt.evict(mid)
+    kept = rt.set_cache_prefix(mid, 40 << 20)
+    try:
+        rt.invoke(mid, x, gpu=0, engine=engine)           # lands prefix + suffix
+        rt.evict(mid, keep_prefix=True)
+        r = rt.invoke(mid, x, gpu=0, engine=engine)        # moves only the suffix
+        assert r.stats["bytes_swapped"] == rt.model_info(mid)["store_bytes"] - kept
+        assert r.stats["wire_bytes"] < r.stats["bytes_swapped"]
+        np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+        np.testing.assert_array_equal(r.output, base)
+    finally:
+        rt.evict(mid)
+        rt.set_cache_prefix(mid, 0)
+
+
+def test_coded_engine_on_plain_model_is_einval(rt, registered):
+    spec, w, x, mid = registered("mlp")
+    rt.evict(mid)
+    for engine in (ENGINE_SMZ, ENGINE_DMAZ):
+        with pytest.raises(FswError) as e:
+            rt.invoke(mid, x, gpu=0, engine=engine)
+        assert e.value.status == F.EINVAL
+
+
+def test_dmaz_beats_the_link(rt, coded):
+    """Sanity floor, not the bench: DMAZ delivers > 60 GB/s of store bytes on BERT-base (the link
+    carries ~0.76 of them at <= 55 GB/s)."""
+    spec, w, x, plain, mid = coded("bert-base")
+    gbs = []
+    for _ in range(5):
+        rt.evict(mid)
+        gbs.append(rt.invoke(mid, x, gpu=0, engine=ENGINE_DMAZ).stats["link_gbps"])
+    assert np.median(gbs) > 60.0, gbs

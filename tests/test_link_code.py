@@ -1,0 +1,159 @@
+"""CPU tests of the exponent-coded link format (FSW_REG_LINK_CODE; include/fsw.h).
+
+The coded store is decoded here by an independent numpy decoder written from the format text in
+include/fsw.h (it shares no code with the CUDA decoder in swap.cu or the C++ encoder), and must give
+back the host store byte for byte: the format is lossless by construction, so any dropped bit, wrong
+nibble order or wrong block offset fails.  The piece table must tile the store in execution order
+without straddling layer regions (each piece is released on one layer's ready counter).
+"""
+import numpy as np
+import pytest
+
+import synth
+from paper_2306_03622_b200 import build as B
+from paper_2306_03622_b200 import fsw as F
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    B.build()
+
+
+def decode_piece(cp: np.ndarray, hdr: np.ndarray, nbytes: int) -> np.ndarray:
+    """Decode one coded piece (uint8 array starting at its first block; hdr = its header bytes)
+    into `nbytes` raw bytes.  Returns (raw bytes, coded bytes consumed)."""
+    nb = -(-nbytes // 1024)
+    assert not hdr[nb:].any(), "headers past the last block must be 0"
+    out = np.empty(nbytes, np.uint8)
+    o = 0
+    for b in range(nb):
+        n = min(1024, nbytes - 1024 * b)
+        h = int(hdr[b])
+        if h == 0:
+            out[1024 * b:1024 * b + n] = cp[o:o + n]
+            o += n
+            continue
+        assert n == 1024, "a partial block must be raw"
+        m = cp[o:o + 512].astype(np.uint16)
+        codes = cp[o + 512:o + 768]
+        d = np.empty(512, np.uint16)
+        d[0::2] = codes & 15
+        d[1::2] = codes >> 4
+        e = np.where(d == 15, 0, h - d.astype(np.int32))
+        assert (e >= 0).all() and (e <= 255).all()
+        w = ((m & 0x80) << 8) | (e.astype(np.uint16) << 7) | (m & 0x7F)
+        out[1024 * b:1024 * b + 1024] = w.astype("<u2").view(np.uint8)
+        o += 768
+    return out, o
+
+
+def decode_all(rt, mid):
+    store = rt.read_store(mid)
+    coded = rt.read_coded(mid)
+    pcs = rt.coded_pieces(mid)
+    out = np.zeros_like(store)
+    for p in pcs:
+        dec, used = decode_piece(coded[p["coff"]:p["coff"] + p["cbytes"]], p["hdr"], int(p["bytes"]))
+        assert used == p["cbytes"]
+        out[p["off"]:p["off"] + p["bytes"]] = dec
+    return store, coded, pcs, out
+
+
+def check_table(rt, mid, spec, pcs, coded):
+    info = rt.model_info(mid)
+    assert info["coded_bytes"] == coded.nbytes
+    # pieces tile [0, store_bytes) in execution order, and the coded bytes contiguously
+    assert pcs["off"][0] == 0 and pcs["coff"][0] == 0
+    np.testing.assert_array_equal(pcs["off"][1:], pcs["off"][:-1] + pcs["bytes"][:-1])
+    # coded pieces are contiguous up to 128-B alignment (the gaps are zero)
+    end = pcs["coff"][:-1] + pcs["cbytes"][:-1]
+    np.testing.assert_array_equal(pcs["coff"][1:], (end + 127) // 128 * 128)
+    for a, b in zip(end[:50], pcs["coff"][1:51]):
+        assert not coded[a:b].any()
+    assert info["coded_bytes"] == (int(pcs["coff"][-1] + pcs["cbytes"][-1]) + 127) // 128 * 128
+    assert (pcs["bytes"] <= 16384).all() and (pcs["bytes"] % 16 == 0).all() and (pcs["coff"] % 128 == 0).all()
+    assert (np.diff(pcs["layer"].astype(np.int64)) >= 0).all()
+    # a piece never straddles its layer's region: every layer's pieces are contiguous and start it
+    for li in np.unique(pcs["layer"]):
+        sel = pcs[pcs["layer"] == li]
+        assert int(sel["off"][0]) % 256 == 0
+    return info
+
+
+@pytest.mark.parametrize("name", ["mlp-small", "bert-tiny", "gpt2-tiny", "resnet-tiny"])
+def test_coded_store_decodes_to_store(name):
+    spec = synth.build_model(name)
+    w = spec.build_weights()
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, w, link_code=True)
+        store, coded, pcs, out = decode_all(rt, mid)
+        check_table(rt, mid, spec, pcs, coded)
+        np.testing.assert_array_equal(out, store)
+        plain = rt.register_spec(spec, w)
+        assert rt.model_info(plain)["coded_bytes"] == 0
+        with pytest.raises(F.FswError) as e:
+            rt.read_coded(plain)
+        assert e.value.status == F.ESTATE
+
+
+def test_crafted_blocks_roundtrip():
+    """Every block kind: exponent spread 14 (coded) and 15 (raw), all zeros, signed zeros and
+    subnormals (exponent 0), inf / NaN (exponent 255), random 16-bit words, and a layer tail < 1 KiB."""
+    spec = synth.build_model("mlp-small")
+    w = spec.build_weights()
+    t = spec.tensors[0]
+    words = w[t.offset:t.offset + t.nbytes].view(np.uint16)
+    rng = np.random.default_rng(7)
+    n = words.size
+    blocks = n // 512
+    assert blocks >= 8
+    sm = rng.integers(0, 256, n).astype(np.uint16)
+    base = lambda m, e: ((m & 0x80) << 8) | (e.astype(np.uint16) << 7) | (m & 0x7F)
+    k = 0
+    words[k:k + 512] = base(sm[k:k + 512], rng.integers(100, 115, 512))          # spread 14 -> coded
+    words[k + 3] = base(sm[k + 3:k + 4], np.array([100]))[0]
+    words[k + 4] = base(sm[k + 4:k + 5], np.array([114]))[0]
+    k += 512
+    words[k:k + 512] = base(sm[k:k + 512], rng.integers(100, 116, 512))          # spread 15 -> raw
+    words[k + 5] = base(sm[k + 5:k + 6], np.array([100]))[0]
+    words[k + 6] = base(sm[k + 6:k + 7], np.array([115]))[0]
+    k += 512
+    words[k:k + 512] = 0                                                         # all zero
+    k += 512
+    words[k:k + 512] = np.where(rng.random(512) < 0.5, 0x8000, 0) | rng.integers(0, 128, 512)  # ±0, subnormals
+    k += 512
+    e = rng.integers(242, 256, 512)                                              # up to inf / NaN
+    words[k:k + 512] = base(sm[k:k + 512], e)
+    k += 512
+    words[k:k + 512] = rng.integers(0, 1 << 16, 512)                             # random words
+    k += 512
+    mixed = base(sm[k:k + 512], rng.integers(1, 15, 512))                        # zeros inside a coded block
+    mixed[::7] = 0
+    words[k:k + 512] = mixed
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, w, link_code=True)
+        store, coded, pcs, out = decode_all(rt, mid)
+        np.testing.assert_array_equal(out, store)
+        # header bytes of the first piece reflect the crafted block kinds
+        st = rt.store_tensor(mid, 0)
+        p0 = pcs[np.searchsorted(pcs["off"], st["offset"], side="right") - 1]
+        hdr = p0["hdr"]
+        first = (st["offset"] - int(p0["off"])) // 1024
+        if st["layout"] == 0 and first == 0 and (st["offset"] % 1024) == 0:
+            assert hdr[1] == 0 and hdr[0] == 114 and hdr[2] == 1
+
+
+def test_ratio_full_size_bert():
+    """bert-base: ≤ 0.77 of the store crosses the link (8 + 4 bits per 16-bit word, + raw blocks)."""
+    spec = synth.build_model("bert-base")
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
+        info = rt.model_info(mid)
+        ratio = info["coded_bytes"] / info["store_bytes"]
+        assert 0.74 < ratio < 0.77, ratio
+        # sampled pieces decode exactly (the whole store is checked for the small models)
+        store, coded, pcs = rt.read_store(mid), rt.read_coded(mid), rt.coded_pieces(mid)
+        for i in np.random.default_rng(0).choice(len(pcs), 200, replace=False):
+            p = pcs[i]
+            dec, _ = decode_piece(coded[p["coff"]:p["coff"] + p["cbytes"]], p["hdr"], int(p["bytes"]))
+            np.testing.assert_array_equal(dec, store[p["off"]:p["off"] + p["bytes"]])
