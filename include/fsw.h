@@ -282,14 +282,17 @@ fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint
 /* Link-coded store (FSW_REG_LINK_CODE): the coded bytes, and the piece table in execution order.
  * Piece i covers store bytes [off, off + bytes) of layer `layer` (bytes <= 16 KiB, a multiple of 16)
  * and is coded at [coff, coff + cbytes) of the coded store (coff a multiple of 128; gaps are zero).
- * Its nb = ceil(bytes / 1024) blocks carry header bytes hdr[0..nb) (the rest 0); the coded piece is
- * block b = raw bytes [off + 1024 b, ...) coded as, in order:
- *   header 0     : the raw bytes (1024, or bytes − 1024 (nb − 1) for a partial last block);
- *   header h ≥ 1 : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f) of the block's 16-bit words w_i,
- *                  then 256 bytes of 4-bit codes (code of w_{2k} in the low nibble of byte k);
- *                  exponent e_i = (w_i >> 7) & 0xff is 0 for code 15, else h − code.
+ * Its nb = ceil(bytes / 1024) blocks of 512 16-bit words w_i have 32-bit headers hdr[0..nb) (the rest
+ * 0): h = bits 0-7, b = bits 8-15, n = bits 16-31; the coded piece is its blocks in order, each:
+ *   b = 0xff : the raw bytes (1024, or bytes − 1024 (nb − 1) for a partial last block);
+ *   b = 0xfe : nothing (512 zero words);
+ *   b = 0..4 : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f); b bit-planes of 64 bytes (bit i of
+ *              plane p, byte i/8 bit i%8, = bit p of code c_i); n exceptions of 4 bytes (position in
+ *              bits 0-15, the whole word in bits 16-31), zero-padded to a multiple of 16 bytes.
+ *              w_i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then each exception's word
+ *              replaces w_position.
  * ENOTFOUND / ESTATE (model not link-coded) / EINVAL (cap too small; *n is still set).              */
-typedef struct { uint64_t off, coff; uint32_t bytes, cbytes, layer, pad; uint8_t hdr[16]; } fsw_coded_piece;
+typedef struct { uint64_t off, coff; uint32_t bytes, cbytes, layer, pad; uint32_t hdr[16]; } fsw_coded_piece;
 fsw_status fsw_debug_read_coded(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
 fsw_status fsw_debug_coded_pieces(fsw_ctx* ctx, uint32_t model_id, fsw_coded_piece* out, uint32_t cap, uint32_t* n);
 /* Activation slot of the last invoke of `model_id` on `gpu` (valid until the next invoke). */

@@ -71,20 +71,29 @@ void launch_swap(cudaStream_t s, int ctas, int threads, const uint8_t* host_mapp
                  const Piece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, int sys);
 void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
 // ---- exponent-coded link format ---------------------------------------------
-// A lossless recoding of the host store that moves ~25 % fewer bytes over the host link; the swap
+// A lossless recoding of the host store that moves ~30 % fewer bytes over the host link; the swap
 // kernel decodes it on the fly, so the extent receives the store's bytes bit-exactly.  The store is
 // cut into pieces of <= kZPiece raw bytes (never straddling a layer region); a piece is cut into
-// blocks of kZBlock raw bytes = 512 16-bit words, each with a header byte h (kept in the piece table,
-// in device memory).  Coded piece (128-B aligned in the coded store, so every warp load maps onto whole
-// 128-B host read requests) = the blocks in order:
-//   header h == 0 : raw block (kZBlock bytes, or the piece's tail bytes for a partial last block)
-//   header h >= 1 : kZCoded bytes = 512 bytes m_i = sign | 7 mantissa bits of word i, then 256 bytes
-//                   of 4-bit codes d_i (word 2k in the low nibble of byte k); the exponent is
-//                   e_i = (d_i == 15) ? 0 : h − d_i, so word i = (m_i & 0x80) << 8 | e_i << 7 | (m_i & 0x7f).
-// A block is coded when every non-zero exponent lies in [h − 14, h] (h = the largest), else raw.
+// blocks of kZBlock raw bytes = 512 16-bit words w_i, each described by a 32-bit header kept in the
+// piece table (device memory): h = bits 0-7, b = bits 8-15, n = bits 16-31.  Coded piece (128-B
+// aligned in the coded store, so every warp load maps onto whole 128-B host read requests) = its
+// blocks in order, each:
+//   b == kZRaw  : the raw bytes (kZBlock, or the piece's tail bytes for a partial last block)
+//   b == kZZero : nothing (all 512 words are 0)
+//   b in 0..4   : (patched frame of reference over the exponents e_i = w_i >> 7 & 0xff, h = max e_i)
+//                 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f); then b bit-planes of 64 bytes, bit i
+//                 of plane p (byte i/8, bit i%8) = bit p of c_i; then n exceptions of 4 bytes
+//                 (position i in bits 0-15, the whole word w_i in bits 16-31), zero-padded to 16 B.
+//                 Word i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then every exception
+//                 overwrites its word.  A word is an exception iff h − e_i >= 2^b (its code is then 0).
+// The encoder picks per block the b (or raw) with the fewest bytes.
 constexpr uint32_t kZPiece = 16384;
 constexpr uint32_t kZBlock = 1024;
-constexpr uint32_t kZCoded = 768;
+constexpr uint32_t kZRaw = 0xff, kZZero = 0xfe;
+__host__ __device__ __forceinline__ uint32_t zblock_bytes(uint32_t hdr, uint32_t raw_bytes) {
+    const uint32_t b = (hdr >> 8) & 0xffu, n = hdr >> 16;
+    return b == kZRaw ? raw_bytes : b == kZZero ? 0u : 512u + 64u * b + ((4u * n + 15u) & ~15u);
+}
 struct ZPiece {
     uint64_t off;     // raw store offset == extent offset
     uint64_t coff;    // offset of the coded piece in the coded store (multiple of 128)
@@ -92,7 +101,7 @@ struct ZPiece {
     uint32_t layer;   // ready counter to bump
     uint32_t grp;     // DMA+decode engine: copy group carrying the piece (decode waits for progress > grp)
     uint32_t cbytes;  // coded bytes
-    uint8_t hdr[16];  // block headers (0 for blocks past the piece's end)
+    uint32_t hdr[16]; // block headers (0 for blocks past the piece's end)
 };
 // Decoding swap kernel.  src + (coff − src_base) is a coded piece: the mapped coded host store
 // (stage = 0, zero-copy over the host link) or the device staging buffer the copy engine filled

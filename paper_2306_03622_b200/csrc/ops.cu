@@ -41,16 +41,29 @@ void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) 
 
 // ------------------------------------------------------------------------------------------
 // LAYERNORM: one warp per row, the row held in registers as float4 (NV per lane, C <= 128·NV),
-// fp32 two-pass statistics (mean, then centred variance), 8-B vector loads of γ/β.
+// fp32 two-pass statistics (mean, then centred variance), 8-B vector loads of γ/β.  γ/β are
+// weights (ordered by the ready counter, not by PDL): they are loaded before griddepcontrol.wait,
+// so their round trip overlaps the previous kernel instead of following the statistics.
 // ------------------------------------------------------------------------------------------
 template <int NV>
 __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
     wait_ready_cta(w);
-    pdl_wait();
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp;
-    if (r >= a.rows) return;
     const uint32_t n4 = a.C >> 2;
+    uint2 gv[NV], bv[NV];
+    {
+        const uint2* g = reinterpret_cast<const uint2*>(weight_ptr(*d, a.g_off));
+        const uint2* b = reinterpret_cast<const uint2*>(weight_ptr(*d, a.b_off));
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const uint32_t c = lane + 32u * j;
+            gv[j] = c < n4 ? g[c] : make_uint2(0u, 0u);
+            bv[j] = c < n4 ? b[c] : make_uint2(0u, 0u);
+        }
+    }
+    pdl_wait();
+    if (r >= a.rows) return;
     const float4* x = reinterpret_cast<const float4*>(a.in + (uint64_t)r * a.C);
     float4 v[NV];
     float s = 0.0f;
@@ -70,18 +83,15 @@ __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d
         }
     }
     const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
-    const uint2* g = reinterpret_cast<const uint2*>(weight_ptr(*d, a.g_off));
-    const uint2* b = reinterpret_cast<const uint2*>(weight_ptr(*d, a.b_off));
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const uint32_t c = lane + 32u * j;
         if (c < n4) {
-            const uint2 gv = g[c], bv = b[c];
             float4 y;
-            y.x = (v[j].x - mu) * inv * __uint_as_float(gv.x << 16) + __uint_as_float(bv.x << 16);
-            y.y = (v[j].y - mu) * inv * __uint_as_float(gv.x & 0xffff0000u) + __uint_as_float(bv.x & 0xffff0000u);
-            y.z = (v[j].z - mu) * inv * __uint_as_float(gv.y << 16) + __uint_as_float(bv.y << 16);
-            y.w = (v[j].w - mu) * inv * __uint_as_float(gv.y & 0xffff0000u) + __uint_as_float(bv.y & 0xffff0000u);
+            y.x = (v[j].x - mu) * inv * __uint_as_float(gv[j].x << 16) + __uint_as_float(bv[j].x << 16);
+            y.y = (v[j].y - mu) * inv * __uint_as_float(gv[j].x & 0xffff0000u) + __uint_as_float(bv[j].x & 0xffff0000u);
+            y.z = (v[j].z - mu) * inv * __uint_as_float(gv[j].y << 16) + __uint_as_float(bv[j].y << 16);
+            y.w = (v[j].w - mu) * inv * __uint_as_float(gv[j].y & 0xffff0000u) + __uint_as_float(bv[j].y & 0xffff0000u);
             if (a.out_f32) reinterpret_cast<float4*>(a.out_f32 + (uint64_t)r * a.C)[c] = y;
             if (a.out_bf16) {
                 const uint32_t lo = (uint32_t)f32_to_bf16(y.x) | ((uint32_t)f32_to_bf16(y.y) << 16);
@@ -254,7 +264,179 @@ __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// ATTENTION on the tensor cores for the batch-1 shapes of the paper's transformers (T <= 128,
+// dh in {16, 32, 64, 128}).  One CTA per (head, 64 query rows), 4 warps x 16 rows.  K and V of
+// the keys the CTA needs are staged in shared memory (rows padded to dh + 8 elements: the
+// 32-bit fragment loads and ldmatrix are bank-conflict free).  Per warp, everything stays in
+// registers: S = Q·Kᵀ by mma.sync m16n8k16 (bf16 in, fp32 accumulate; Q fragments loaded straight
+// from the qkv rows), the scale, causal / length mask and softmax in fp32 (row max and sum over
+// the lane quad), P rounded to bf16 and fed back as the A operand of O = P·V (V fragments by
+// ldmatrix.trans), O / Σ stored bf16.  At T = 128 the whole problem is ~10 µs of latency chains on
+// the old scalar kernel; the warp-level MMA keeps every dependent step in registers.  (tcgen05 would
+// need a TMEM allocation and mbarrier round trips per tile for a 16x128 problem: no gain here.)
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    return (uint32_t)f32_to_bf16(lo) | ((uint32_t)f32_to_bf16(hi) << 16);
+}
+
+constexpr int kAttnMmaRows = 64, kAttnMmaMaxT = 128;
+
+template <int DH>
+__global__ void __launch_bounds__(128) k_attention_mma(AttnArgs a) {
+    constexpr int KS = DH / 16;        // k-steps of Q·Kᵀ
+    constexpr int NO = DH / 8;         // n-tiles of O
+    constexpr int NS = kAttnMmaMaxT / 8;  // n-tiles of S (keys)
+    constexpr int LD = DH + 8;         // smem row stride (elements)
+    extern __shared__ __align__(16) uint16_t sm_kv[];
+    uint16_t* Ks = sm_kv;                           // [kpad][LD]
+    pdl_wait();
+    const uint32_t T = a.T, D = a.H * DH, W3 = 3 * D;
+    const uint32_t h = blockIdx.x, r0 = blockIdx.y * kAttnMmaRows;
+    const uint32_t kend = a.causal ? min(T, r0 + kAttnMmaRows) : T;
+    const uint32_t kpad = (kend + 15) & ~15u;
+    uint16_t* Vs = Ks + kpad * LD;                  // [kpad][LD]
+    // stage K and V rows [0, kpad) (rows >= T zero), 16-B chunks
+    constexpr uint32_t C8 = DH / 8;
+    for (uint32_t i = threadIdx.x; i < kpad * C8; i += blockDim.x) {
+        const uint32_t j = i / C8, c = (i - j * C8) * 8;
+        uint4 kv = make_uint4(0, 0, 0, 0), vv = kv;
+        if (j < kend) {
+            const uint16_t* row = a.qkv + (uint64_t)j * W3 + h * DH + c;
+            kv = *reinterpret_cast<const uint4*>(row + D);
+            vv = *reinterpret_cast<const uint4*>(row + 2 * D);
+        }
+        *reinterpret_cast<uint4*>(Ks + j * LD + c) = kv;
+        *reinterpret_cast<uint4*>(Vs + j * LD + c) = vv;
+    }
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const uint32_t q0 = r0 + warp * 16;
+    // Q fragments (A operand, row-major 16 x DH) straight from the qkv rows q0+g and q0+g+8
+    uint32_t qa[KS][4];
+    {
+        const uint32_t ra = q0 + g, rb = q0 + g + 8;
+        const uint16_t* pa = a.qkv + (uint64_t)ra * W3 + h * DH;
+        const uint16_t* pb = a.qkv + (uint64_t)rb * W3 + h * DH;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            const uint32_t c = kk * 16 + 2 * t;
+            qa[kk][0] = ra < T ? *reinterpret_cast<const uint32_t*>(pa + c) : 0u;
+            qa[kk][1] = rb < T ? *reinterpret_cast<const uint32_t*>(pb + c) : 0u;
+            qa[kk][2] = ra < T ? *reinterpret_cast<const uint32_t*>(pa + c + 8) : 0u;
+            qa[kk][3] = rb < T ? *reinterpret_cast<const uint32_t*>(pb + c + 8) : 0u;
+        }
+    }
+    __syncthreads();
+    if (q0 >= T) return;  // after the barrier: every thread helped stage
+    // keys this warp needs: all (non-causal) or up to its last row (causal)
+    const uint32_t kw = a.causal ? min(kend, q0 + 16) : kend;
+    const uint32_t nst = (kw + 7) / 8;
+    const float scale = rsqrtf((float)DH);
+    float s[NS][4];
+#pragma unroll
+    for (int n = 0; n < NS; ++n) {
+        s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.0f;
+        if ((uint32_t)n < nst) {
+            const uint16_t* kr = Ks + (n * 8 + g) * LD + 2 * t;
+#pragma unroll
+            for (int kk = 0; kk < KS; ++kk)
+                mma_bf16_16816(s[n], qa[kk], *reinterpret_cast<const uint32_t*>(kr + kk * 16),
+                               *reinterpret_cast<const uint32_t*>(kr + kk * 16 + 8));
+        }
+    }
+    // scale, mask, row max / sum (rows q0+g: elements 0,1; q0+g+8: elements 2,3)
+    const uint32_t ra = q0 + g, rb = ra + 8;
+    float mxa = -INFINITY, mxb = -INFINITY;
+#pragma unroll
+    for (int n = 0; n < NS; ++n) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint32_t j = n * 8 + 2 * t + (e & 1), r = e < 2 ? ra : rb;
+            const bool ok = (uint32_t)n < nst && j < T && (!a.causal || j <= r);
+            s[n][e] = ok ? s[n][e] * scale : -INFINITY;
+        }
+        mxa = fmaxf(mxa, fmaxf(s[n][0], s[n][1]));
+        mxb = fmaxf(mxb, fmaxf(s[n][2], s[n][3]));
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, o));
+        mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, o));
+    }
+    float za = 0.0f, zb = 0.0f;
+#pragma unroll
+    for (int n = 0; n < NS; ++n) {
+        s[n][0] = __expf(s[n][0] - mxa);
+        s[n][1] = __expf(s[n][1] - mxa);
+        s[n][2] = __expf(s[n][2] - mxb);
+        s[n][3] = __expf(s[n][3] - mxb);
+        za += s[n][0] + s[n][1];
+        zb += s[n][2] + s[n][3];
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        za += __shfl_xor_sync(0xffffffffu, za, o);
+        zb += __shfl_xor_sync(0xffffffffu, zb, o);
+    }
+    // O = P·V: the S accumulators of key tiles 2kk, 2kk+1 are the A fragment of k-step kk
+    float o[NO][4];
+#pragma unroll
+    for (int n = 0; n < NO; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0f;
+    const uint32_t nkk = (nst + 1) / 2;
+#pragma unroll
+    for (int kk = 0; kk < NS / 2; ++kk) {
+        if ((uint32_t)kk >= nkk) break;
+        const uint32_t pa[4] = {pack_bf16x2(s[2 * kk][0], s[2 * kk][1]), pack_bf16x2(s[2 * kk][2], s[2 * kk][3]),
+                                pack_bf16x2(s[2 * kk + 1][0], s[2 * kk + 1][1]),
+                                pack_bf16x2(s[2 * kk + 1][2], s[2 * kk + 1][3])};
+        // ldmatrix.x4.trans: matrices (keys kk·16 + 0..7 | 8..15) x (cols n·8 | (n+1)·8)
+        const uint32_t mi = lane >> 3, rr = lane & 7;
+#pragma unroll
+        for (int n = 0; n < NO; n += 2) {
+            const uint16_t* p = Vs + (kk * 16 + (mi & 1) * 8 + rr) * LD + (n + (mi >> 1)) * 8;
+            uint32_t b0, b1, b2, b3;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(b0), "=r"(b1), "=r"(b2), "=r"(b3)
+                         : "r"((uint32_t)__cvta_generic_to_shared(p)));
+            mma_bf16_16816(o[n], pa, b0, b1);
+            if (n + 1 < NO) mma_bf16_16816(o[n + 1], pa, b2, b3);
+        }
+    }
+    const float ia = 1.0f / za, ib = 1.0f / zb;
+#pragma unroll
+    for (int n = 0; n < NO; ++n) {
+        const uint32_t c = h * DH + n * 8 + 2 * t;
+        if (ra < T) *reinterpret_cast<uint32_t*>(a.out + (uint64_t)ra * D + c) = pack_bf16x2(o[n][0] * ia, o[n][1] * ia);
+        if (rb < T) *reinterpret_cast<uint32_t*>(a.out + (uint64_t)rb * D + c) = pack_bf16x2(o[n][2] * ib, o[n][3] * ib);
+    }
+}
+
+template <int DH>
+static void launch_attention_mma(cudaStream_t s, const AttnArgs& a) {
+    const uint32_t kmax = (a.T + 15) & ~15u;  // keys staged by the CTA that needs the most
+    const size_t smem = 2ull * kmax * (DH + 8) * sizeof(uint16_t);
+    dim3 grid(a.H, (a.T + kAttnMmaRows - 1) / kAttnMmaRows);
+    launch_pdl(PDL_ATTN, k_attention_mma<DH>, grid, dim3(128), smem, s, a);
+}
+
 void launch_attention(cudaStream_t s, const AttnArgs& a) {
+    static const bool scalar = getenv("FSW_ATTN_SCALAR") != nullptr;  // A/B hook: the scalar kernel
+    if (a.T <= (uint32_t)kAttnMmaMaxT && !scalar) {
+        switch (a.dh) {
+            case 16: return launch_attention_mma<16>(s, a);
+            case 32: return launch_attention_mma<32>(s, a);
+            case 64: return launch_attention_mma<64>(s, a);
+            case 128: return launch_attention_mma<128>(s, a);
+            default: break;
+        }
+    }
     const int threads = 256, nwarp = threads / 32;
     const size_t smem = 4 * (((a.T * (a.dh / 2 + 1) + 3) & ~3u) + a.T * (a.dh / 2)) + sizeof(float) * (nwarp * a.T + nwarp * a.dh);
     dim3 grid(a.H, (a.T + kAttnRows - 1) / kAttnRows);
@@ -347,6 +529,10 @@ void init_ops_attrs() {
     cudaFuncSetAttribute(k_gemv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_gemv<kGemvMaxRows>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_attention_mma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_attention_mma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_attention_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_attention_mma<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 }  // namespace fsw

@@ -686,26 +686,48 @@ static fsw_status check_layer(const Model& m, uint32_t li) {
 }
 
 // ---- exponent-coded link format (kernels.h) -----------------------------------
-// Header of a full block of 512 16-bit words: its largest exponent when every non-zero exponent is
-// within 14 of it (1 when all are zero), else 0 = stored raw.
-static uint8_t zheader(const uint16_t* w) {
-    uint32_t emax = 0, emin = 255;
+// Header of a full block of 512 16-bit words: all zero -> kZZero; else h = the largest exponent and
+// the code width b in 0..4 with the fewest bytes (words with h − e >= 2^b become exceptions), or raw
+// when no width beats the 1024 raw bytes.
+static uint32_t zheader(const uint16_t* w) {
+    uint32_t emax = 0, any = 0;
     for (uint32_t i = 0; i < kZBlock / 2; ++i) {
-        const uint32_t e = (w[i] >> 7) & 0xffu;
-        if (e) {
-            emax = std::max(emax, e);
-            emin = std::min(emin, e);
+        emax = std::max<uint32_t>(emax, (w[i] >> 7) & 0xffu);
+        any |= w[i];
+    }
+    if (!any) return kZZero << 8;
+    uint32_t hist[9] = {};  // hist[k] = words with h − e in [2^(k−1), 2^k) (k = 0: h − e = 0), k = 8: >= 128
+    for (uint32_t i = 0; i < kZBlock / 2; ++i) {
+        const uint32_t d = emax - ((w[i] >> 7) & 0xffu);
+        hist[d ? std::min<uint32_t>(8, 32 - __builtin_clz(d)) : 0]++;
+    }
+    uint32_t best = kZRaw, best_bytes = kZBlock, best_n = 0, n = kZBlock / 2;
+    for (uint32_t b = 0; b <= 4; ++b) {
+        n -= hist[b];  // words with h − e >= 2^b
+        const uint32_t bytes = zblock_bytes(emax | (b << 8) | (n << 16), kZBlock);
+        if (bytes < best_bytes) {
+            best = b;
+            best_bytes = bytes;
+            best_n = n;
         }
     }
-    if (!emax) return 1;
-    return emax - emin <= 14 ? (uint8_t)emax : 0;
+    return best == kZRaw ? kZRaw << 8 : emax | (best << 8) | (best_n << 16);
 }
 
-static void zencode_block(const uint16_t* w, uint32_t h, uint8_t* out /* kZCoded zeroed bytes */) {
+static void zencode_block(const uint16_t* w, uint32_t hdr, uint8_t* out /* zeroed, zblock_bytes(hdr) */) {
+    const uint32_t h = hdr & 0xffu, b = (hdr >> 8) & 0xffu;
+    uint32_t k = 0;
+    uint8_t* exc = out + 512 + 64 * b;
     for (uint32_t i = 0; i < kZBlock / 2; ++i) {
-        const uint32_t e = (w[i] >> 7) & 0xffu;
+        const uint32_t d = h - ((w[i] >> 7) & 0xffu);
         out[i] = (uint8_t)(((w[i] >> 8) & 0x80u) | (w[i] & 0x7fu));
-        out[512 + i / 2] |= (uint8_t)((e ? h - e : 15u) << (4 * (i & 1)));
+        if (d >> b) {  // exception: position and the whole word; code 0
+            const uint32_t e = i | ((uint32_t)w[i] << 16);
+            memcpy(exc + 4 * k++, &e, 4);
+            continue;
+        }
+        for (uint32_t p = 0; p < b; ++p)
+            if ((d >> p) & 1u) out[512 + 64 * p + i / 8] |= (uint8_t)(1u << (i % 8));
     }
 }
 
@@ -736,21 +758,23 @@ static fsw_status build_link_code(Model& m, bool host_only) {
         for (uint64_t o = 0; o < m.region_bytes[li]; o += kZPiece)
             pcs.push_back({m.region_off[li] + o, 0, (uint32_t)std::min<uint64_t>(kZPiece, m.region_bytes[li] - o), li, 0, 0, {}});
     const uint32_t bpp = kZPiece / kZBlock;
-    std::vector<uint8_t> hdr(pcs.size() * bpp, 0);
+    std::vector<uint32_t> hdr(pcs.size() * bpp, 0);
     parallel_for(pcs.size(), [&](size_t i) {
         const ZPiece& pc = pcs[i];
-        for (uint32_t b = 0; b < pc.bytes / kZBlock; ++b)
+        const uint32_t nfull = pc.bytes / kZBlock;
+        for (uint32_t b = 0; b < nfull; ++b)
             hdr[i * bpp + b] = zheader(reinterpret_cast<const uint16_t*>(m.store + pc.off + (uint64_t)b * kZBlock));
+        if (pc.bytes > nfull * kZBlock) hdr[i * bpp + nfull] = kZRaw << 8;  // partial tail block: raw
     });
     uint64_t cur = 0;
     for (size_t i = 0; i < pcs.size(); ++i) {
         ZPiece& pc = pcs[i];
-        const uint32_t nfull = pc.bytes / kZBlock;
-        uint32_t cb = pc.bytes - nfull * kZBlock;
-        for (uint32_t b = 0; b < nfull; ++b) cb += hdr[i * bpp + b] ? kZCoded : kZBlock;
+        const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
+        uint32_t cb = 0;
+        for (uint32_t b = 0; b < nb; ++b) cb += zblock_bytes(hdr[i * bpp + b], std::min(kZBlock, pc.bytes - b * kZBlock));
         pc.coff = cur;
         pc.cbytes = cb;
-        memcpy(pc.hdr, &hdr[i * bpp], bpp);  // a partial last block's header stays 0 (raw)
+        memcpy(pc.hdr, &hdr[i * bpp], sizeof pc.hdr);
         cur = align_up(cur + cb, 128);
     }
     m.zbytes = cur;
@@ -763,20 +787,15 @@ static fsw_status build_link_code(Model& m, bool host_only) {
     parallel_for(pcs.size(), [&](size_t i) {
         const ZPiece& pc = pcs[i];
         uint8_t* out = m.zstore + pc.coff;
-        const uint32_t nfull = pc.bytes / kZBlock, nb = (pc.bytes + kZBlock - 1) / kZBlock;
+        const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
         uint64_t o = 0;
         for (uint32_t b = 0; b < nb; ++b) {
             const uint8_t* raw = m.store + pc.off + (uint64_t)b * kZBlock;
-            const uint32_t h = b < nfull ? hdr[i * bpp + b] : 0;
-            if (h) {
-                memset(out + o, 0, kZCoded);
-                zencode_block(reinterpret_cast<const uint16_t*>(raw), h, out + o);
-                o += kZCoded;
-            } else {
-                const uint32_t n = b < nfull ? kZBlock : pc.bytes - nfull * kZBlock;
-                memcpy(out + o, raw, n);
-                o += n;
-            }
+            const uint32_t hd = hdr[i * bpp + b], n = std::min(kZBlock, pc.bytes - b * kZBlock);
+            const uint32_t kind = (hd >> 8) & 0xffu;
+            if (kind == kZRaw) memcpy(out + o, raw, n);
+            else if (kind != kZZero) zencode_block(reinterpret_cast<const uint16_t*>(raw), hd, out + o);  // zeroed above
+            o += zblock_bytes(hd, n);
         }
     });
     if (!host_only) {

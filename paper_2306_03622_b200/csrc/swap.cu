@@ -79,20 +79,38 @@ __device__ __forceinline__ uint2 zld2(const uint8_t* p) {
         asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
     return r;
 }
-// word = sign | exponent | mantissa from the stored byte m = sign | mantissa and the code d.
-__device__ __forceinline__ uint32_t zword(uint32_t m, uint32_t d, uint32_t h) {
-    const uint32_t e = d == 15u ? 0u : h - d;
-    return ((m & 0x80u) << 8) | (e << 7) | (m & 0x7fu);
+template <bool STAGE>
+__device__ __forceinline__ uint32_t zld16(const uint8_t* p) {
+    uint16_t r;
+    if (STAGE) asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(r) : "l"(p) : "memory");
+    else asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+    return r;
 }
-// Lane l of a coded block: words 16l .. 16l+15 from 16 stored bytes and 8 code bytes.
-__device__ __forceinline__ void zdecode16(const uint4 sm, const uint2 nb, uint32_t h, uint4& o0, uint4& o1) {
+template <bool STAGE>
+__device__ __forceinline__ uint32_t zld32(const uint8_t* p) {
+    uint32_t r;
+    if (STAGE) asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
+    else asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
+// Lane l of a coded block: words 16l .. 16l+15 from its 16 stored bytes, its 16 bits of each code
+// plane (plane p in bits 16p .. 16p+15 of pl) and the block's base exponent h.
+__device__ __forceinline__ void zdecode16(const uint4 sm, uint64_t pl, uint32_t h, uint4& o0, uint4& o1) {
     const uint32_t s[4] = {sm.x, sm.y, sm.z, sm.w};
     uint32_t o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const uint32_t mm = s[k >> 1] >> (16 * (k & 1));
-        const uint32_t nn = (k < 4 ? nb.x : nb.y) >> (8 * (k & 3));
-        o[k] = zword(mm & 0xffu, nn & 15u, h) | (zword((mm >> 8) & 0xffu, (nn >> 4) & 15u, h) << 16);
+        uint32_t w2 = 0;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int i = 2 * k + half;  // word i of the lane's 16
+            const uint32_t m = (s[i >> 2] >> (8 * (i & 3))) & 0xffu;
+            const uint32_t c = (uint32_t)((pl >> i) & 1u) | (uint32_t)(((pl >> (16 + i)) & 1u) << 1) |
+                               (uint32_t)(((pl >> (32 + i)) & 1u) << 2) | (uint32_t)(((pl >> (48 + i)) & 1u) << 3);
+            w2 |= (((m & 0x80u) << 8) | ((h - c) << 7) | (m & 0x7fu)) << (16 * half);
+        }
+        o[k] = w2;
     }
     o0 = make_uint4(o[0], o[1], o[2], o[3]);
     o1 = make_uint4(o[4], o[5], o[6], o[7]);
@@ -115,7 +133,7 @@ __device__ __forceinline__ void wait_geq(const uint32_t* p, uint32_t v, DevCtl* 
 
 // Persistent warps claim coded pieces in the table's order (execution order), decode U blocks at a
 // time (all loads of the U blocks issued before any store, so a warp keeps ~3 KB of host reads in
-// flight), store 128-bit words into the extent and release the piece's raw bytes on its layer's
+// flight), store 128-bit words into the extent, patch the exceptions and release the piece's raw bytes on its layer's
 // counter — the same readiness protocol as k_swap, so layer kernels cannot tell the engines apart.
 template <bool STAGE, int U>
 __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_t src_base, DevDesc dst,
@@ -138,10 +156,10 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
         }
         const uint8_t* cp = src + (pc.coff - src_base);
         uint8_t* out = weight_ptr(dd, pc.off);
-        const uint32_t nfull = pc.bytes / kZBlock, nb = (pc.bytes + kZBlock - 1) / kZBlock;  // nb <= 16
-        // header byte (from the device piece table) and coded offset of block `lane` (exclusive scan)
-        const uint32_t h = lane < nb ? (uint32_t)__ldg(&pieces[p].hdr[lane]) : 0u;
-        const uint32_t sz = lane < nfull ? (h ? kZCoded : kZBlock) : lane < nb ? pc.bytes - nfull * kZBlock : 0u;
+        const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;  // <= 16
+        // header (from the device piece table) and coded offset of block `lane` (exclusive scan)
+        const uint32_t hd = lane < nb ? __ldg(&pieces[p].hdr[lane]) : 0u;
+        const uint32_t sz = lane < nb ? zblock_bytes(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
         uint32_t incl = sz;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -149,45 +167,71 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
             if (lane >= (uint32_t)o) incl += t;
         }
         const uint32_t boff = incl - sz;
-        for (uint32_t b0 = 0; b0 < nfull; b0 += U) {
+        for (uint32_t b0 = 0; b0 < nb; b0 += U) {
+            // all loads of U blocks first (memory-level parallelism over the host link), then stores
             uint4 q0[U], q1[U];
-            uint32_t hh[U];
+            uint64_t pl[U];
+            uint32_t ex[U], hh[U], ob[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint32_t b = b0 + u;
-                hh[u] = __shfl_sync(0xffffffffu, h, b & 31u);
-                const uint32_t ob = __shfl_sync(0xffffffffu, boff, b & 31u);
-                if (b < nfull) {
-                    q0[u] = zld4<STAGE>(cp + ob + lane * 16u);
-                    if (hh[u]) {
-                        const uint2 t = zld2<STAGE>(cp + ob + 512u + lane * 8u);
-                        q1[u] = make_uint4(t.x, t.y, 0u, 0u);
-                    } else {
-                        q1[u] = zld4<STAGE>(cp + ob + 512u + lane * 16u);
+                hh[u] = __shfl_sync(0xffffffffu, hd, b & 31u);
+                ob[u] = __shfl_sync(0xffffffffu, boff, b & 31u);
+                const uint32_t kind = (hh[u] >> 8) & 0xffu, n = hh[u] >> 16;
+                const uint8_t* bp = cp + ob[u];
+                pl[u] = 0;
+                ex[u] = 0;
+                if (b >= nb || kind == kZZero) continue;
+                const bool full = b * kZBlock + kZBlock <= pc.bytes;
+                if (kind == kZRaw) {
+                    if (full) {
+                        q0[u] = zld4<STAGE>(bp + lane * 16u);
+                        q1[u] = zld4<STAGE>(bp + 512u + lane * 16u);
+                    }
+                    continue;
+                }
+                q0[u] = zld4<STAGE>(bp + lane * 16u);
+#pragma unroll
+                for (uint32_t pp = 0; pp < 4; ++pp)
+                    if (pp < kind) pl[u] |= (uint64_t)zld16<STAGE>(bp + 512u + 64u * pp + lane * 2u) << (16 * pp);
+                if (lane < n) ex[u] = zld32<STAGE>(bp + 512u + 64u * kind + lane * 4u);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t b = b0 + u;
+                if (b >= nb) break;
+                const uint32_t kind = (hh[u] >> 8) & 0xffu, n = hh[u] >> 16;
+                uint8_t* bo = out + (uint64_t)b * kZBlock;
+                uint4* o4 = reinterpret_cast<uint4*>(bo);
+                if (kind == kZZero) {
+                    st_v4(o4 + 2 * lane, make_uint4(0u, 0u, 0u, 0u));
+                    st_v4(o4 + 2 * lane + 1, make_uint4(0u, 0u, 0u, 0u));
+                } else if (kind == kZRaw) {
+                    if (b * kZBlock + kZBlock <= pc.bytes) {
+                        st_v4(o4 + lane, q0[u]);
+                        st_v4(o4 + 32 + lane, q1[u]);
+                    } else {  // the piece's partial tail (< 1 KiB, end of a layer region)
+                        const uint32_t n16 = (pc.bytes - b * kZBlock) >> 4;
+                        for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, zld4<STAGE>(cp + ob[u] + i * 16u));
+                    }
+                } else {
+                    uint4 o0, o1;
+                    zdecode16(q0[u], pl[u], hh[u] & 0xffu, o0, o1);
+                    st_v4(o4 + 2 * lane, o0);
+                    st_v4(o4 + 2 * lane + 1, o1);
+                    if (n) {
+                        // exceptions overwrite their words after the warp's block stores (__syncwarp
+                        // orders the warp's memory operations)
+                        __syncwarp();
+                        uint16_t* o16 = reinterpret_cast<uint16_t*>(bo);
+                        if (lane < n) o16[ex[u] & 0xffffu] = (uint16_t)(ex[u] >> 16);
+                        for (uint32_t j = 32 + lane; j < n; j += 32) {
+                            const uint32_t e = zld32<STAGE>(cp + ob[u] + 512u + 64u * kind + j * 4u);
+                            o16[e & 0xffffu] = (uint16_t)(e >> 16);
+                        }
                     }
                 }
             }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t b = b0 + u;
-                if (b >= nfull) break;
-                uint4* ob = reinterpret_cast<uint4*>(out + (uint64_t)b * kZBlock);
-                if (hh[u]) {
-                    uint4 o0, o1;
-                    zdecode16(q0[u], make_uint2(q1[u].x, q1[u].y), hh[u], o0, o1);
-                    st_v4(ob + 2 * lane, o0);
-                    st_v4(ob + 2 * lane + 1, o1);
-                } else {
-                    st_v4(ob + lane, q0[u]);
-                    st_v4(ob + 32 + lane, q1[u]);
-                }
-            }
-        }
-        if (nb > nfull) {  // raw tail of a layer region (< 1 KiB)
-            const uint32_t ob = __shfl_sync(0xffffffffu, boff, nfull & 31u);
-            const uint32_t n16 = (pc.bytes - nfull * kZBlock) >> 4;
-            uint4* o = reinterpret_cast<uint4*>(out + (uint64_t)nfull * kZBlock);
-            for (uint32_t i = lane; i < n16; i += 32) st_v4(o + i, zld4<STAGE>(cp + ob + i * 16u));
         }
         if (sys) {
             asm volatile("fence.acq_rel.sys;" ::: "memory");

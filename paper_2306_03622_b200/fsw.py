@@ -87,7 +87,7 @@ class InvokeStats(ctypes.Structure):
 
 class CodedPiece(ctypes.Structure):
     _fields_ = [("off", u64), ("coff", u64), ("bytes", u32), ("cbytes", u32), ("layer", u32), ("pad", u32),
-                ("hdr", ctypes.c_uint8 * 16)]
+                ("hdr", ctypes.c_uint32 * 16)]
 
 
 class InvokeOpts(ctypes.Structure):
@@ -429,7 +429,7 @@ class Runtime:
         arr = (CodedPiece * max(1, n.value))()
         _check(lib().fsw_debug_coded_pieces(self.h, mid, arr, n.value, ctypes.byref(n)))
         dt = np.dtype([("off", "<u8"), ("coff", "<u8"), ("bytes", "<u4"), ("cbytes", "<u4"), ("layer", "<u4"),
-                       ("pad", "<u4"), ("hdr", "u1", (16,))])
+                       ("pad", "<u4"), ("hdr", "<u4", (16,))])
         return np.frombuffer(bytes(arr), dtype=dt)[:n.value].copy()
 
     def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:

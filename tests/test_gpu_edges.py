@@ -110,8 +110,11 @@ def test_conv_paths_on_odd_sizes(rt, H, cin, cout, k, stride, pad):
     assert rel_err(got, ref) <= TOL
 
 
+# T <= 128 with dh in {16, 32, 64, 128} runs the tensor-core kernel (k_attention_mma), the rest the
+# scalar kernel: both against the float64 oracle
 @pytest.mark.parametrize("T,H,dh,causal", [(1, 2, 64, 0), (17, 3, 8, 1), (128, 12, 64, 0), (256, 2, 128, 1),
-                                           (200, 4, 32, 0)])
+                                           (200, 4, 32, 0), (128, 25, 64, 1), (100, 4, 32, 1), (64, 2, 128, 0),
+                                           (33, 3, 16, 1), (128, 2, 128, 1), (77, 2, 64, 0), (2, 1, 16, 1)])
 def test_attention_lengths_and_head_widths(rt, T, H, dh, causal):
     D = H * dh
     m = ModelSpec("attn", 59, input_kind=("uniform_bf16", 1.0))

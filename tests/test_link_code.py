@@ -20,30 +20,39 @@ def built():
 
 
 def decode_piece(cp: np.ndarray, hdr: np.ndarray, nbytes: int) -> np.ndarray:
-    """Decode one coded piece (uint8 array starting at its first block; hdr = its header bytes)
-    into `nbytes` raw bytes.  Returns (raw bytes, coded bytes consumed)."""
+    """Decode one coded piece (uint8 array starting at its first block; hdr = its 32-bit block
+    headers) into `nbytes` raw bytes, from the format text of include/fsw.h.
+    Returns (raw bytes, coded bytes consumed)."""
     nb = -(-nbytes // 1024)
     assert not hdr[nb:].any(), "headers past the last block must be 0"
     out = np.empty(nbytes, np.uint8)
     o = 0
-    for b in range(nb):
-        n = min(1024, nbytes - 1024 * b)
-        h = int(hdr[b])
-        if h == 0:
-            out[1024 * b:1024 * b + n] = cp[o:o + n]
-            o += n
+    for blk in range(nb):
+        n_raw = min(1024, nbytes - 1024 * blk)
+        hd = int(hdr[blk])
+        h, b, n = hd & 0xFF, (hd >> 8) & 0xFF, hd >> 16
+        dst = out[1024 * blk:1024 * blk + n_raw]
+        if b == 0xFF:
+            dst[:] = cp[o:o + n_raw]
+            o += n_raw
             continue
-        assert n == 1024, "a partial block must be raw"
+        assert n_raw == 1024, "a partial block must be raw"
+        if b == 0xFE:
+            dst[:] = 0
+            continue
+        assert b <= 4
         m = cp[o:o + 512].astype(np.uint16)
-        codes = cp[o + 512:o + 768]
-        d = np.empty(512, np.uint16)
-        d[0::2] = codes & 15
-        d[1::2] = codes >> 4
-        e = np.where(d == 15, 0, h - d.astype(np.int32))
-        assert (e >= 0).all() and (e <= 255).all()
+        c = np.zeros(512, np.int64)
+        for p in range(b):
+            bits = np.unpackbits(cp[o + 512 + 64 * p:o + 576 + 64 * p], bitorder="little")
+            c |= bits.astype(np.int64) << p
+        e = h - c
+        assert (e >= 0).all()
         w = ((m & 0x80) << 8) | (e.astype(np.uint16) << 7) | (m & 0x7F)
-        out[1024 * b:1024 * b + 1024] = w.astype("<u2").view(np.uint8)
-        o += 768
+        ex = cp[o + 512 + 64 * b:o + 512 + 64 * b + 4 * n].view("<u4")
+        w[(ex & 0xFFFF).astype(np.int64)] = (ex >> 16).astype(np.uint16)
+        dst[:] = w.astype("<u2").view(np.uint8)
+        o += 512 + 64 * b + (4 * n + 15) // 16 * 16
     return out, o
 
 
@@ -97,7 +106,7 @@ def test_coded_store_decodes_to_store(name):
 
 
 def test_crafted_blocks_roundtrip():
-    """Every block kind: exponent spread 14 (coded) and 15 (raw), all zeros, signed zeros and
+    """Every block kind: exponent spread 14 (4-bit codes) and 16 (an exception), all zeros, signed zeros and
     subnormals (exponent 0), inf / NaN (exponent 255), random 16-bit words, and a layer tail < 1 KiB."""
     spec = synth.build_model("mlp-small")
     w = spec.build_weights()
@@ -114,9 +123,9 @@ def test_crafted_blocks_roundtrip():
     words[k + 3] = base(sm[k + 3:k + 4], np.array([100]))[0]
     words[k + 4] = base(sm[k + 4:k + 5], np.array([114]))[0]
     k += 512
-    words[k:k + 512] = base(sm[k:k + 512], rng.integers(100, 116, 512))          # spread 15 -> raw
+    words[k:k + 512] = base(sm[k:k + 512], rng.integers(101, 117, 512))          # spread 16 -> one exception
     words[k + 5] = base(sm[k + 5:k + 6], np.array([100]))[0]
-    words[k + 6] = base(sm[k + 6:k + 7], np.array([115]))[0]
+    words[k + 6] = base(sm[k + 6:k + 7], np.array([116]))[0]
     k += 512
     words[k:k + 512] = 0                                                         # all zero
     k += 512
@@ -140,17 +149,21 @@ def test_crafted_blocks_roundtrip():
         hdr = p0["hdr"]
         first = (st["offset"] - int(p0["off"])) // 1024
         if st["layout"] == 0 and first == 0 and (st["offset"] % 1024) == 0:
-            assert hdr[1] == 0 and hdr[0] == 114 and hdr[2] == 1
+            kinds = [(int(x) >> 8) & 0xFF for x in hdr[:7]]
+        assert kinds[0] == 4 and int(hdr[0]) & 0xFF == 114 and int(hdr[0]) >> 16 == 0  # 4-bit codes
+        assert kinds[1] == 4 and int(hdr[1]) & 0xFF == 116 and int(hdr[1]) >> 16 == 1  # one exception
+        assert kinds[2] == 0xFE                                  # all zero
+        assert kinds[5] == 0xFF                                   # random words: raw
 
 
 def test_ratio_full_size_bert():
-    """bert-base: ≤ 0.77 of the store crosses the link (8 + 4 bits per 16-bit word, + raw blocks)."""
+    """bert-base: ≤ 0.72 of the store crosses the link (8 bits + b-bit codes + exceptions per word)."""
     spec = synth.build_model("bert-base")
     with F.Runtime(flags=F.HOST_ONLY) as rt:
         mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
         info = rt.model_info(mid)
         ratio = info["coded_bytes"] / info["store_bytes"]
-        assert 0.74 < ratio < 0.77, ratio
+        assert 0.68 < ratio < 0.72, ratio
         # sampled pieces decode exactly (the whole store is checked for the small models)
         store, coded, pcs = rt.read_store(mid), rt.read_coded(mid), rt.coded_pieces(mid)
         for i in np.random.default_rng(0).choice(len(pcs), 200, replace=False):
