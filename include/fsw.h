@@ -87,8 +87,7 @@ typedef struct {
                                          switch, −1 = none (Algorithm 1's "neighbor"); NULL = none
                                          (HGX B200: one switch per GPU)                          */
     uint64_t dmaz_min_bytes;          /* AUTO picks DMAZ for link-coded models with at least this
-                                         many store bytes, SMZ below; 0 = 128 MiB (measured: SMZ wins
-                                         on ResNet-50's 51 MB, DMAZ on BERT-base's 219 MB)       */
+                                         many store bytes, SMZ below; 0 = 32 MiB                  */
 } fsw_config;
 
 /* Swap engines.  Both move the host store into the extent in execution order and

@@ -412,7 +412,7 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
     if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 16 << 10;
     if (c->cfg.stripe_min_bytes == 0) c->cfg.stripe_min_bytes = 256ull << 20;
     if (c->cfg.dma_min_bytes == 0) c->cfg.dma_min_bytes = 32ull << 20;
-    if (c->cfg.dmaz_min_bytes == 0) c->cfg.dmaz_min_bytes = 128ull << 20;
+    if (c->cfg.dmaz_min_bytes == 0) c->cfg.dmaz_min_bytes = 32ull << 20;
     if (c->cfg.dma_group_bytes == 0) c->cfg.dma_group_bytes = 64ull << 20;
     if (c->cfg.dma_streams == 0) c->cfg.dma_streams = 1;
     if (c->cfg.engine > FSW_ENGINE_DMAZ || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
@@ -1369,11 +1369,13 @@ static fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t see
         if (pc.off >= from) zs.host.push_back(pc);
     if (zs.host.empty()) return fail(FSW_EINVAL, "link-coded swap with nothing to move");
     zs.cfrom = zs.host.front().coff;
-    zs.cend = zs.host.back().coff + zs.host.back().cbytes;
+    zs.cend = align_up(zs.host.back().coff + zs.host.back().cbytes, 128);  // the coded store is 128-B padded
     if (grp) {
         // the DMA engine's plan (make_dma_plan) over coded bytes: tail taper inside layers, head ramp
         // at layer boundaries
-        static const double ramp = getenv("FSW_DMA_RAMP") ? atof(getenv("FSW_DMA_RAMP")) : 0.0;
+        // head ramp on by default here (measured: DMAZ ResNet-50 0.890 -> 0.809 ms at ramp 4, BERT-base
+        // neutral); off for the plain DMA engine, where it cost ResNet-50 2-5 %
+        static const double ramp = getenv("FSW_DMAZ_RAMP") ? atof(getenv("FSW_DMAZ_RAMP")) : 4.0;
         const uint64_t tail_min = std::min<uint64_t>(grp, 1ull << 20);
         uint64_t lo = zs.cfrom;
         for (size_t i = 0; i < zs.host.size(); ++i) {
@@ -1430,6 +1432,10 @@ static fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, 
 static bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_DMAZ; }
 // Engines whose layer kernels wait on per-layer byte counters (released by a swap kernel).
 static bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_coded(e); }
+
+// DMAZ decode CTAs unless the invoke sets copy_ctas: measured, 16 CTAs make the decode the bottleneck
+// (BERT-base 3.60 ms), 32 keep up with the copy engine (2.94 ms) (profiles/r01/linkcode/).
+constexpr uint32_t kDmazCtas = 32;
 
 struct InvokeCfg {
     bool cold, no_overlap;
@@ -1969,7 +1975,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     };
     InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
-                 o.copy_ctas ? o.copy_ctas : c->cfg.copy_ctas, extents(gi), nullptr};
+                 o.copy_ctas ? o.copy_ctas : engine == FSW_ENGINE_DMAZ ? std::max(c->cfg.copy_ctas, kDmazCtas) : c->cfg.copy_ctas,
+                 extents(gi), nullptr};
     ic.from = pcached ? m->split : 0;
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
     if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr, ic.from);

@@ -95,8 +95,8 @@ __device__ __forceinline__ uint32_t zld32(const uint8_t* p) {
 }
 
 // Lane l of a coded block: words 16l .. 16l+15 from its 16 stored bytes, its 16 bits of each code
-// plane (plane p in bits 16p .. 16p+15 of pl) and the block's base exponent h.
-__device__ __forceinline__ void zdecode16(const uint4 sm, uint64_t pl, uint32_t h, uint4& o0, uint4& o1) {
+// plane (plane p in the low half of pl[p]) and the block's base exponent h.
+__device__ __forceinline__ void zdecode16(const uint4 sm, const uint32_t (&pl)[4], uint32_t h, uint4& o0, uint4& o1) {
     const uint32_t s[4] = {sm.x, sm.y, sm.z, sm.w};
     uint32_t o[8];
 #pragma unroll
@@ -106,14 +106,21 @@ __device__ __forceinline__ void zdecode16(const uint4 sm, uint64_t pl, uint32_t 
         for (int half = 0; half < 2; ++half) {
             const int i = 2 * k + half;  // word i of the lane's 16
             const uint32_t m = (s[i >> 2] >> (8 * (i & 3))) & 0xffu;
-            const uint32_t c = (uint32_t)((pl >> i) & 1u) | (uint32_t)(((pl >> (16 + i)) & 1u) << 1) |
-                               (uint32_t)(((pl >> (32 + i)) & 1u) << 2) | (uint32_t)(((pl >> (48 + i)) & 1u) << 3);
+            const uint32_t c = ((pl[0] >> i) & 1u) | (((pl[1] >> i) & 1u) << 1) | (((pl[2] >> i) & 1u) << 2) |
+                               (((pl[3] >> i) & 1u) << 3);
             w2 |= (((m & 0x80u) << 8) | ((h - c) << 7) | (m & 0x7fu)) << (16 * half);
         }
         o[k] = w2;
     }
     o0 = make_uint4(o[0], o[1], o[2], o[3]);
     o1 = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// 32-bit word `wi` (0..3) of lane `src`'s uint4 v, for every lane (four shuffles and a select).
+__device__ __forceinline__ uint32_t shfl_word(const uint4& v, uint32_t src, uint32_t wi) {
+    const uint32_t x = __shfl_sync(0xffffffffu, v.x, src), y = __shfl_sync(0xffffffffu, v.y, src);
+    const uint32_t z = __shfl_sync(0xffffffffu, v.z, src), w = __shfl_sync(0xffffffffu, v.w, src);
+    return wi == 0 ? x : wi == 1 ? y : wi == 2 ? z : w;
 }
 
 __device__ __forceinline__ void wait_geq(const uint32_t* p, uint32_t v, DevCtl* ctl) {
@@ -170,8 +177,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
         for (uint32_t b0 = 0; b0 < nb; b0 += U) {
             // all loads of U blocks first (memory-level parallelism over the host link), then stores
             uint4 q0[U], q1[U];
-            uint64_t pl[U];
-            uint32_t ex[U], hh[U], ob[U];
+            uint32_t hh[U], ob[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint32_t b = b0 + u;
@@ -179,8 +185,6 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                 ob[u] = __shfl_sync(0xffffffffu, boff, b & 31u);
                 const uint32_t kind = (hh[u] >> 8) & 0xffu, n = hh[u] >> 16;
                 const uint8_t* bp = cp + ob[u];
-                pl[u] = 0;
-                ex[u] = 0;
                 if (b >= nb || kind == kZZero) continue;
                 const bool full = b * kZBlock + kZBlock <= pc.bytes;
                 if (kind == kZRaw) {
@@ -190,11 +194,11 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                     }
                     continue;
                 }
+                // stored bytes, then the planes + exceptions region as whole 16-B chunks (every load of
+                // the block is a 16-B-per-lane load: whole 128-B host read requests)
                 q0[u] = zld4<STAGE>(bp + lane * 16u);
-#pragma unroll
-                for (uint32_t pp = 0; pp < 4; ++pp)
-                    if (pp < kind) pl[u] |= (uint64_t)zld16<STAGE>(bp + 512u + 64u * pp + lane * 2u) << (16 * pp);
-                if (lane < n) ex[u] = zld32<STAGE>(bp + 512u + 64u * kind + lane * 4u);
+                const uint32_t rb = 64u * kind + 4u * n;
+                if (lane * 16u < rb) q1[u] = zld4<STAGE>(bp + 512u + lane * 16u);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -215,17 +219,28 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                         for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, zld4<STAGE>(cp + ob[u] + i * 16u));
                     }
                 } else {
+                    // lane l's 16 code bits of plane p: bytes 64p + 2l .. +1 of the region, i.e. half
+                    // (l & 1) of word ((l & 7) >> 1) of chunk 4p + (l >> 3)
+                    uint32_t pl[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                    for (uint32_t pp = 0; pp < 4; ++pp)
+                        if (pp < kind)
+                            pl[pp] = (shfl_word(q1[u], 4u * pp + (lane >> 3), (lane & 7u) >> 1) >> (16u * (lane & 1u))) & 0xffffu;
+                    // exception j (lane j < 32): word (j & 3) of chunk 4b + (j >> 2)
+                    const uint32_t ex = n ? shfl_word(q1[u], (4u * kind + (lane >> 2)) & 31u, lane & 3u) : 0u;
                     uint4 o0, o1;
-                    zdecode16(q0[u], pl[u], hh[u] & 0xffu, o0, o1);
+                    zdecode16(q0[u], pl, hh[u] & 0xffu, o0, o1);
                     st_v4(o4 + 2 * lane, o0);
                     st_v4(o4 + 2 * lane + 1, o1);
                     if (n) {
                         // exceptions overwrite their words after the warp's block stores (__syncwarp
-                        // orders the warp's memory operations)
+                        // orders the warp's memory operations); those past the loaded 512-B region or
+                        // past the 32nd are read directly (rare: the chooser keeps n small)
                         __syncwarp();
                         uint16_t* o16 = reinterpret_cast<uint16_t*>(bo);
-                        if (lane < n) o16[ex[u] & 0xffffu] = (uint16_t)(ex[u] >> 16);
-                        for (uint32_t j = 32 + lane; j < n; j += 32) {
+                        const uint32_t in_reg = min(n, min(32u, (512u - 64u * kind) / 4u));
+                        if (lane < in_reg) o16[ex & 0xffffu] = (uint16_t)(ex >> 16);
+                        for (uint32_t j = in_reg + lane; j < n; j += 32) {
                             const uint32_t e = zld32<STAGE>(cp + ob[u] + 512u + 64u * kind + j * 4u);
                             o16[e & 0xffffu] = (uint16_t)(e >> 16);
                         }
@@ -252,7 +267,7 @@ void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uin
     if (stage)
         k_swapz<true, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
     else
-        k_swapz<false, 4><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
+        k_swapz<false, 3><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
 }
 
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap
