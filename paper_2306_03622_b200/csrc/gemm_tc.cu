@@ -99,6 +99,14 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// float4 at the same shared-memory offset in CTA `rank` of the cluster (distributed shared memory).
+__device__ __forceinline__ float4 ld_dsmem_f4(const void* local, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(local)), "r"(rank));
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra) : "memory");
+    return v;
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -317,10 +325,40 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
     STAMP(4);
     pdl_wait();  // activations (residual in, output / partials out) only after the predecessor
-    const uint32_t rows = min(a.m_rows, a.M - m0);
+    uint32_t rows = min(a.m_rows, a.M - m0);
     const uint32_t cols = min((uint32_t)BN, a.N - n0);
     constexpr uint32_t upr = BN / 4;
-    if (a.splits > 1) {
+    uint32_t rb = 0;  // first tile row this CTA's epilogue covers
+    if (a.cz > 1) {
+        // 2c) cluster split-K: the cz CTAs of a (1, 1, cz) cluster hold the partial tiles of one output
+        //     tile in their shared memory; CTA z sums rows [z·rows/cz, (z+1)·rows/cz) of all of them over
+        //     DSMEM in split order (deterministic) and runs the epilogue on those rows only.
+        cluster_sync();
+        const uint32_t z = blockIdx.z, per = (rows + a.cz - 1) / a.cz;
+        rb = min(rows, z * per);
+        const uint32_t re = min(rows, rb + per);
+        for (uint32_t u = threadIdx.x; u < (re - rb) * upr; u += blockDim.x) {
+            const uint32_t r = rb + u / upr, c = (u % upr) * 4;
+            const float* src = ct + r * C::kLdc + c;
+            float4 v[8];  // all peers' loads in flight at once, then the sum in split order
+#pragma unroll
+            for (uint32_t q = 0; q < 8; ++q)
+                if (q < a.cz) v[q] = ld_dsmem_f4(src, q);
+            float4 acc = v[0];
+#pragma unroll
+            for (uint32_t q = 1; q < 8; ++q) {
+                if (q >= a.cz) break;
+                acc.x += v[q].x;
+                acc.y += v[q].y;
+                acc.z += v[q].z;
+                acc.w += v[q].w;
+            }
+            // peers read only their own row slices: overwriting this slice of the local tile is safe
+            *reinterpret_cast<float4*>(const_cast<float*>(src)) = acc;
+        }
+        __syncthreads();
+        rows = re - rb;
+    } else if (a.splits > 1) {
         // 2a) split-K: publish this split's partial tile, the last arriving CTA reduces all splits
         //     in split order (fixed summation order: deterministic).  Loads are batched kB units
         //     per thread so the reduction is bandwidth- rather than latency-bound.
@@ -398,7 +436,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
             uint4 raw[kE];
 #pragma unroll
             for (int j = 0; j < kE; ++j) {
-                const uint32_t u = u0 + j * blockDim.x, r = u / upr;
+                const uint32_t u = u0 + j * blockDim.x, r = rb + u / upr;
                 raw[j] = make_uint4(0, 0, 0, 0);
                 if (u < units && col_ok) {
                     const uint64_t ri = (uint64_t)(m0 + r) * a.ld_res + n0 + c;
@@ -411,7 +449,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
             }
 #pragma unroll
             for (int j = 0; j < kE; ++j) {
-                const uint32_t u = u0 + j * blockDim.x, r = u / upr;
+                const uint32_t u = u0 + j * blockDim.x, r = rb + u / upr;
                 if (!(u < units && col_ok)) continue;
                 float4 v = *reinterpret_cast<const float4*>(ct + r * C::kLdc + c);
                 // (acc + bias) + residual, the order of the unfused definition
@@ -433,7 +471,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
         }
     } else {
         for (uint32_t idx = threadIdx.x; idx < rows * BN; idx += blockDim.x) {
-            const uint32_t r = idx / BN, c = idx - r * BN;
+            const uint32_t r = rb + idx / BN, c = idx - (idx / BN) * BN;
             if (c >= cols) continue;
             const uint32_t m = m0 + r, n = n0 + c;
             float x = ct[r * C::kLdc + c];
@@ -452,7 +490,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     __syncthreads();
     STAMP(5);
 #endif
-    if (mc > 1) cluster_sync();  // no CTA leaves while a peer's multicast commit may target it
+    if (mc > 1 || a.cz > 1) cluster_sync();  // no CTA leaves while a peer may still read / target its smem
 }
 
 template <int BN>
@@ -461,8 +499,8 @@ static void launch_bn(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMa
     const int nst = (int)((a.kt_per + C::kSub - 1) / C::kSub);
     const int stages = nst < C::kMaxStages ? nst : C::kMaxStages;
     dim3 grid((a.M + a.m_rows - 1) / a.m_rows, a.n_pad / BN, a.splits);
-    launch_pdl_cluster(PDL_GEMM, k_gemm<BN>, grid, dim3(kGemmThreads), C::smem_bytes(stages), s, dim3(1, a.mc > 1 ? a.mc : 1, 1),
-                       *tmA, d, w, a, stages);
+    launch_pdl_cluster(PDL_GEMM, k_gemm<BN>, grid, dim3(kGemmThreads), C::smem_bytes(stages), s,
+                       dim3(1, a.mc > 1 ? a.mc : 1, a.cz > 1 ? a.cz : 1), *tmA, d, w, a, stages);
 }
 
 void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading)

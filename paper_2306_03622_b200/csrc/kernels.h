@@ -152,6 +152,9 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // A multicast: CTAs of a (1, mc, 1) cluster share each A sub-tile, every CTA loading 128/mc rows
     // and broadcasting them (mc in {1, 2, 4, 8}; the A tensor map's box is 128/mc rows)
     uint32_t mc;
+    // cluster split-K: the `splits` CTAs of one output tile form a (1, 1, cz) cluster (cz == splits <= 8)
+    // and reduce their partial tiles over distributed shared memory instead of `part` / `ctr`
+    uint32_t cz;
 };
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a);
 

@@ -296,7 +296,7 @@ constexpr uint64_t kStageHdr = 256;
 constexpr uint32_t kGemmCtrs = 1u << 16;
 
 // Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor.
-struct Tiling { int bn; uint32_t splits, kt_per; };
+struct Tiling { int bn; uint32_t splits, kt_per; bool cluster; };
 static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t a_kt_bytes, uint32_t /*m_rows*/) {
     // Linear latency model fitted (least squares, rms 1.1 us) to the (BN, split) sweep of
     // tools/gemm_bench.cu on B200 over the batch-1 GEMM shapes of the paper's models
@@ -304,7 +304,7 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
     // the epilogue width, the split-K reduction, and the total L2->SM traffic (every N tile re-reads
     // A).  One CTA per SM: a grid beyond one wave of 148 pays per wave.  Picks within 0.5 us of the
     // measured best on every swept shape.
-    Tiling best{16, 1, kt};
+    Tiling best{16, 1, kt, false};
     double best_t = 1e30;
     for (int bn : {16, 32, 64, 128}) {
         if (n_pad % bn) continue;
@@ -321,7 +321,17 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
             t *= waves;
             if (t < best_t - 1e-9) {
                 best_t = t;
-                best = {bn, S, kt_per};
+                best = {bn, S, kt_per, false};
+            }
+            // cluster split-K (partials reduced over DSMEM, gemm_tc.cu 2c): a second linear model fitted
+            // to the single-wave cluster configurations of the same sweep (profiles/r01/gemm_sweep_cz2.txt,
+            // rms 1.9 us); with the first model it picks the measured best (or within 0.5 us) on every shape
+            if (S >= 2 && S <= 8 && ctas <= 148) {
+                const double tc = 6.2102 + 0.0051 * cta_kb + 0.0737 * (bn / 16.0) + 0.0766 * ctas * cta_kb / 1e3 + 0.2124 * S;
+                if (tc < best_t - 1e-9) {
+                    best_t = tc;
+                    best = {bn, S, kt_per, true};
+                }
             }
         }
     }
@@ -1028,11 +1038,13 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
         a.splits = t.splits;
         a.kt_per = t.kt_per;
         a.ctr = g.gemm_ctr;
+        static const bool no_cz = getenv("FSW_GEMM_NO_CLUSTER_SPLIT") != nullptr;  // A/B hook
+        a.cz = t.cluster && !no_cz ? t.splits : 0;
         // A multicast across an N cluster (plain GEMMs; the implicit-conv A box is not row-split)
         a.mc = 1;
         static const uint32_t mc_max = getenv("FSW_GEMM_MC") ? (uint32_t)atoi(getenv("FSW_GEMM_MC")) : 1;
         for (uint32_t c : {8u, 4u, 2u})
-            if (c <= mc_max && m_rows == 128 && (a.n_pad / t.bn) % c == 0) {
+            if (!a.cz && c <= mc_max && m_rows == 128 && (a.n_pad / t.bn) % c == 0) {
                 a.mc = c;
                 break;
             }

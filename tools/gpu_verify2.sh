@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_linkcode.py -x -q -k striped 2>&1 | grep -E "Error|assert|^E " | head -20
-timeout 900 python -m pytest tests/test_gpu_linkcode.py tests/test_gpu_edges.py tests/test_gpu_parity.py -q 2>&1 | tail -4
-timeout 600 python tools/linkcode_bench.py mlp resnet50 bert-base gpt2-xl --reps 15 2>&1 | tee gpurun_out/linkcode_v2c.txt | grep -E "smz|dmaz|\"dma\"" | cut -c1-230
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for v in 0 1; do echo "no_cluster_split=$v"; if [ $v = 1 ]; then export FSW_GEMM_NO_CLUSTER_SPLIT=1; fi; timeout 600 python tools/linkcode_bench.py resnet50 bert-base gpt2-xl --reps 5 2>&1 | grep dmaz | python -c "
+import sys,json
+for l in sys.stdin: d=json.loads(l); print(d['model'], 'resident', d['resident_ms'], 'cold dmaz', d['p50_ms'])"; done

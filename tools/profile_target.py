@@ -15,7 +15,7 @@ spec = synth.build_model(name)
 w = spec.build_weights()
 x = spec.make_input()
 mid = rt.register_spec(spec, w, link_code=coded)
-rt.invoke(mid, x, flags=NO_OVERLAP, engine=engine)
+rt.invoke(mid, x, flags=NO_OVERLAP, engine=engine if engine != ENGINE_DMAZ or "--dmaz-cold" in sys.argv else ENGINE_SMZ)
 for _ in range(warm):
     rt.invoke(mid, x)
 rt.close()
