@@ -98,7 +98,7 @@ typedef struct {
  *        group a stream memory write (no SM) bumps that stream's group counter.               */
 enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SMZ = 3, FSW_ENGINE_DMAZ = 4 };
 /* Link-coded engines (models registered with FSW_REG_LINK_CODE).  The host link carries
- * the model's exponent-coded store (lossless, ~0.76 of the bytes) and a kernel decodes it into the
+ * the model's exponent-coded store (lossless, ~0.71 of the bytes) and a kernel decodes it into the
  * extent, releasing each decoded piece's bytes on its layer's counter (the SM protocol):
  *   SMZ : persistent CTAs read coded pieces zero-copy from the mapped coded store and decode in registers;
  *   DMAZ: copy-engine DMA of layer-ordered, tapered groups of coded pieces into a device staging
@@ -152,7 +152,7 @@ typedef struct { uint32_t op, first_ref, n_refs; int32_t in0, in1, out; int32_t 
 #define FSW_REG_LINK_CODE 0x2u /* also build the exponent-coded copy of the store (pinned, mapped) that
                                   the SMZ / DMAZ engines move over the host link (format
                                   at fsw_coded_piece below).  Lossless: the extent receives the store's
-                                  bytes bit-exactly.  Costs ~0.76x the store in extra host memory.  */
+                                  bytes bit-exactly.  Costs ~0.71x the store in extra host memory.  */
 
 typedef struct {
     const char* name;
@@ -165,10 +165,10 @@ typedef struct {
     uint32_t flags;
 } fsw_model_desc;
 
-/* Validate the table, lay the weights out in the library's pinned, mapped host store in
- * execution order (each layer's tensors contiguous, 256-B aligned; GEMM weights re-laid in
- * the tensor-core tile order described in DESIGN.md §4), and register it for zero-copy
- * device access.  Untimed, one-time (the paper's model repository).
+/* Validate the table, lay the weights out in the library's pinned, mapped, THP-backed host store
+ * (pages bound to pool GPU 0's NUMA node before first touch) in execution order (each layer's
+ * tensors contiguous, 256-B aligned; GEMM weights re-laid in the tensor-core tile order described
+ * in DESIGN.md §4), and register it for zero-copy device access.  Untimed, one-time (the paper's model repository).
  * The caller may free `weights` on return.  Errors: EINVAL (bad table), ENOMEM, ECUDA.   */
 fsw_status fsw_register_model(fsw_ctx* ctx, const fsw_model_desc* desc, uint32_t* model_id);
 /* EBUSY while an invoke of the model is in flight; evicts it from every GPU first.        */
@@ -181,6 +181,8 @@ typedef struct {
     uint64_t input_bytes, output_bytes;
     uint32_t output_dtype;
     uint64_t coded_bytes;      /* bytes of the exponent-coded store (FSW_REG_LINK_CODE), else 0 */
+    int32_t numa_node;         /* NUMA node the host store's pages prefer (that of pool GPU 0's PCIe
+                                  root, from sysfs; bound before first touch), −1 if unknown / none */
 } fsw_model_info;
 fsw_status fsw_model_info_get(fsw_ctx* ctx, uint32_t model_id, fsw_model_info* out);
 

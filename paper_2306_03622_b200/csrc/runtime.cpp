@@ -12,8 +12,11 @@
 //   eviction by invalidation ................ evict()
 //   one request per GPU ..................... Gpu::busy
 #include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <array>
 #include <atomic>
 #include <chrono>
@@ -229,6 +232,7 @@ struct Model {
     uint8_t* store = nullptr;  // pinned, mapped host store (execution order)
     uint64_t store_bytes = 0, store_alloc = 0;
     bool store_wc = false;
+    int numa_node = -1;        // node the store's pages were bound to (mbind before first touch), or -1
     // exponent-coded copy of the store (FSW_REG_LINK_CODE; kernels.h): pinned, mapped
     uint8_t* zstore = nullptr;
     uint64_t zbytes = 0, zalloc = 0;
@@ -695,6 +699,30 @@ static fsw_status check_layer(const Model& m, uint32_t li) {
     return FSW_OK;
 }
 
+// ---- NUMA placement of host stores ---------------------------------------------
+// The NUMA node of a CUDA device, from sysfs (-1: unknown, or a single-node host).
+static int gpu_numa_node(int dev) {
+    char bus[64] = {};
+    if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return -1;
+    for (char* q = bus; *q; ++q) *q = (char)tolower(*q);
+    char path[128];
+    snprintf(path, sizeof path, "/sys/bus/pci/devices/%s/numa_node", bus);
+    FILE* f = fopen(path, "r");
+    if (!f) return -1;
+    int node = -1;
+    if (fscanf(f, "%d", &node) != 1) node = -1;
+    fclose(f);
+    return node;
+}
+// Prefer `node` for the pages of [p, p + len) before their first touch (MPOL_PREFERRED: the
+// allocation still succeeds when the node is full).  Returns the node bound, or -1.
+static int bind_pages(void* p, size_t len, int node) {
+    if (node < 0 || node >= 64) return -1;
+    const unsigned long mask = 1ul << node;
+    const long MPOL_PREFERRED_ = 1;
+    return syscall(SYS_mbind, p, len, MPOL_PREFERRED_, &mask, 64ul, 0u) == 0 ? node : -1;
+}
+
 // ---- exponent-coded link format (kernels.h) -----------------------------------
 // Header of a full block of 512 16-bit words: all zero -> kZZero; else h = the largest exponent and
 // the code width b in 0..4 with the fewest bytes (words with h − e >= 2^b become exceptions), or raw
@@ -792,6 +820,7 @@ static fsw_status build_link_code(Model& m, bool host_only) {
     void* p = mmap(nullptr, m.zalloc, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p == MAP_FAILED) return fail(FSW_ENOMEM, "register: mmap of %llu coded bytes failed", (unsigned long long)m.zalloc);
     madvise(p, m.zalloc, MADV_HUGEPAGE);
+    if (m.numa_node >= 0) bind_pages(p, m.zalloc, m.numa_node);
     m.zstore = static_cast<uint8_t*>(p);
     memset(m.zstore, 0, m.zalloc);  // alignment gaps stay zero
     parallel_for(pcs.size(), [&](size_t i) {
@@ -902,6 +931,8 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
         void* p = mmap(nullptr, m->store_alloc, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
         if (p == MAP_FAILED) return fail(FSW_ENOMEM, "register: mmap of %llu bytes failed", (unsigned long long)m->store_alloc);
         madvise(p, m->store_alloc, MADV_HUGEPAGE);
+        // the host link that reads the store is pool GPU 0's (striped swaps add the others)
+        if (!host_only) m->numa_node = bind_pages(p, m->store_alloc, gpu_numa_node(c->gpus[0].dev));
         m->store = static_cast<uint8_t*>(p);
     }
     // pack (zero padding everywhere; first touch happens here)
@@ -965,6 +996,7 @@ extern "C" fsw_status fsw_model_info_get(fsw_ctx* c, uint32_t id, fsw_model_info
     out->output_bytes = m->output_bytes;
     out->output_dtype = m->slots[m->output_slot].dtype;
     out->coded_bytes = m->zstore ? m->zbytes : 0;
+    out->numa_node = m->numa_node;
     return FSW_OK;
 }
 

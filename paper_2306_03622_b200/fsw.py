@@ -67,7 +67,7 @@ class ModelDesc(ctypes.Structure):
 class ModelInfo(ctypes.Structure):
     _fields_ = [("store_bytes", u64), ("algorithmic_bytes", u64), ("n_layers", u32), ("n_tensors", u32),
                 ("n_gemm_layers", u32), ("input_bytes", u64), ("output_bytes", u64), ("output_dtype", u32),
-                ("coded_bytes", u64)]
+                ("coded_bytes", u64), ("numa_node", i32)]
 
 
 class StoreTensor(ctypes.Structure):

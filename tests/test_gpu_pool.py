@@ -87,3 +87,16 @@ def test_public_invoke_picks_resident_gpu(rt, registered):
     out = np.empty(rt.model_info(mid)["output_bytes"] // 4, np.float32)
     st = rt.invoke_plain(mid, x, out)
     assert st["swap_kind"] == 0 and st["gpu"] == 0
+
+
+def test_host_store_numa_node_matches_gpu(rt, registered):
+    """the store's pages are bound (before first touch) to the NUMA node of the GPU
+    whose host link reads them; the node comes from sysfs (-1 on single-node hosts)."""
+    import os
+    import subprocess
+    spec, w, x, mid = registered("mlp")
+    bus = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=pci.bus_id", "--format=csv,noheader"],
+                         capture_output=True, text=True).stdout.strip().lower()  # 00000000:1b:00.0
+    path = f"/sys/bus/pci/devices/{bus[-12:]}/numa_node"
+    node = int(open(path).read()) if os.path.exists(path) else -1
+    assert rt.model_info(mid)["numa_node"] == (node if node >= 0 else -1), (bus, node)
