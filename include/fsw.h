@@ -87,7 +87,8 @@ typedef struct {
                                          switch, −1 = none (Algorithm 1's "neighbor"); NULL = none
                                          (HGX B200: one switch per GPU)                          */
     uint64_t dmaz_min_bytes;          /* AUTO picks DMAZ for link-coded models with at least this
-                                         many store bytes, SMZ below; 0 = 32 MiB                  */
+                                         many store bytes, SMZ below; 0 = 128 MiB (measured: SMZ
+                                         wins on ResNet-50's 51 MB, DMAZ on BERT-base's 219 MB)  */
 } fsw_config;
 
 /* Swap engines.  Both move the host store into the extent in execution order and
@@ -100,7 +101,8 @@ enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SM
 /* Link-coded engines (models registered with FSW_REG_LINK_CODE).  The host link carries
  * the model's exponent-coded store (lossless, ~0.71 of the bytes) and a kernel decodes it into the
  * extent, releasing each decoded piece's bytes on its layer's counter (the SM protocol):
- *   SMZ : persistent CTAs read coded pieces zero-copy from the mapped coded store and decode in registers;
+ *   SMZ : persistent CTAs stream coded pieces zero-copy from the mapped coded store with TMA bulk copies
+ *         into a shared-memory ring and decode them from there;
  *   DMAZ: copy-engine DMA of layer-ordered, tapered groups of coded pieces into a device staging
  *         buffer, each followed by a stream write of the group count; persistent decode CTAs wait for
  *         their piece's group, then decode from HBM.
@@ -284,14 +286,16 @@ fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint
  * Piece i covers store bytes [off, off + bytes) of layer `layer` (bytes <= 16 KiB, a multiple of 16)
  * and is coded at [coff, coff + cbytes) of the coded store (coff a multiple of 128; gaps are zero).
  * Its nb = ceil(bytes / 1024) blocks of 512 16-bit words w_i have 32-bit headers hdr[0..nb) (the rest
- * 0): h = bits 0-7, b = bits 8-15, n = bits 16-31; the coded piece is its blocks in order, each:
- *   b = 0xff : the raw bytes (1024, or bytes − 1024 (nb − 1) for a partial last block);
- *   b = 0xfe : nothing (512 zero words);
- *   b = 0..4 : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f); b bit-planes of 64 bytes (bit i of
- *              plane p, byte i/8 bit i%8, = bit p of code c_i); n exceptions of 4 bytes (position in
- *              bits 0-15, the whole word in bits 16-31), zero-padded to a multiple of 16 bytes.
- *              w_i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then each exception's word
- *              replaces w_position.
+ * 0): h = bits 0-7, b = bits 8-15, n = bits 16-31.  The coded piece is stream A, zero padding to a
+ * multiple of 128 bytes, then stream B:
+ *   stream A, per block:  b = 0xff : the raw bytes (1024, or bytes − 1024 (nb − 1) for a partial last
+ *                                    block);  b = 0xfe : nothing (512 zero words);
+ *                         b = 0..4 : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f);
+ *   stream B, per block with b = 0..4: b bit-planes of 64 bytes (bit i of plane p, byte i/8 bit i%8,
+ *                         = bit p of code c_i); n exceptions of 4 bytes (position in bits 0-15, the
+ *                         whole word in bits 16-31), zero-padded to a multiple of 16 bytes.
+ * A coded block decodes as w_i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then each
+ * exception's word replaces w_position.
  * ENOTFOUND / ESTATE (model not link-coded) / EINVAL (cap too small; *n is still set).              */
 typedef struct { uint64_t off, coff; uint32_t bytes, cbytes, layer, pad; uint32_t hdr[16]; } fsw_coded_piece;
 fsw_status fsw_debug_read_coded(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);

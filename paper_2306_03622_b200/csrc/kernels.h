@@ -75,24 +75,36 @@ void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
 // kernel decodes it on the fly, so the extent receives the store's bytes bit-exactly.  The store is
 // cut into pieces of <= kZPiece raw bytes (never straddling a layer region); a piece is cut into
 // blocks of kZBlock raw bytes = 512 16-bit words w_i, each described by a 32-bit header kept in the
-// piece table (device memory): h = bits 0-7, b = bits 8-15, n = bits 16-31.  Coded piece (128-B
-// aligned in the coded store, so every warp load maps onto whole 128-B host read requests) = its
-// blocks in order, each:
-//   b == kZRaw  : the raw bytes (kZBlock, or the piece's tail bytes for a partial last block)
-//   b == kZZero : nothing (all 512 words are 0)
-//   b in 0..4   : (patched frame of reference over the exponents e_i = w_i >> 7 & 0xff, h = max e_i)
-//                 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f); then b bit-planes of 64 bytes, bit i
-//                 of plane p (byte i/8, bit i%8) = bit p of c_i; then n exceptions of 4 bytes
-//                 (position i in bits 0-15, the whole word w_i in bits 16-31), zero-padded to 16 B.
-//                 Word i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then every exception
-//                 overwrites its word.  A word is an exception iff h − e_i >= 2^b (its code is then 0).
-// The encoder picks per block the b (or raw) with the fewest bytes.
+// piece table (device memory): h = bits 0-7, b = bits 8-15, n = bits 16-31.  A coded piece (128-B
+// aligned in the coded store) is two streams, so the bulk of every zero-copy load covers whole 128-B
+// host read requests:
+//   stream A, per block in order:  b == kZRaw  : the raw bytes (kZBlock, or the piece's tail bytes for
+//                                                a partial last block);
+//                                  b == kZZero : nothing (all 512 words are 0);
+//                                  b in 0..4   : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f);
+//   zero padding to a multiple of 128 bytes;
+//   stream B, per coded block (b in 0..4) in order: b bit-planes of 64 bytes (bit i of plane p, byte i/8
+//                                  bit i%8, = bit p of the code c_i), then n exceptions of 4 bytes
+//                                  (position i in bits 0-15, the whole word w_i in bits 16-31),
+//                                  zero-padded to a multiple of 16 bytes.
+// A coded block decodes (patched frame of reference over the exponents e_i = w_i >> 7 & 0xff, h = max
+// e_i) as w_i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then every exception overwrites its
+// word.  A word is an exception iff h − e_i >= 2^b (its code is then 0).  The encoder picks per
+// block the b (or raw) with the fewest bytes.
 constexpr uint32_t kZPiece = 16384;
 constexpr uint32_t kZBlock = 1024;
 constexpr uint32_t kZRaw = 0xff, kZZero = 0xfe;
-__host__ __device__ __forceinline__ uint32_t zblock_bytes(uint32_t hdr, uint32_t raw_bytes) {
+// stream-A and stream-B bytes of one block
+__host__ __device__ __forceinline__ uint32_t zblock_a(uint32_t hdr, uint32_t raw_bytes) {
+    const uint32_t b = (hdr >> 8) & 0xffu;
+    return b == kZRaw ? raw_bytes : b == kZZero ? 0u : 512u;
+}
+__host__ __device__ __forceinline__ uint32_t zblock_b(uint32_t hdr) {
     const uint32_t b = (hdr >> 8) & 0xffu, n = hdr >> 16;
-    return b == kZRaw ? raw_bytes : b == kZZero ? 0u : 512u + 64u * b + ((4u * n + 15u) & ~15u);
+    return b <= 4 ? 64u * b + ((4u * n + 15u) & ~15u) : 0u;
+}
+__host__ __device__ __forceinline__ uint32_t zblock_bytes(uint32_t hdr, uint32_t raw_bytes) {
+    return zblock_a(hdr, raw_bytes) + zblock_b(hdr);
 }
 struct ZPiece {
     uint64_t off;     // raw store offset == extent offset

@@ -426,7 +426,7 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
     if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 16 << 10;
     if (c->cfg.stripe_min_bytes == 0) c->cfg.stripe_min_bytes = 256ull << 20;
     if (c->cfg.dma_min_bytes == 0) c->cfg.dma_min_bytes = 32ull << 20;
-    if (c->cfg.dmaz_min_bytes == 0) c->cfg.dmaz_min_bytes = 32ull << 20;
+    if (c->cfg.dmaz_min_bytes == 0) c->cfg.dmaz_min_bytes = 128ull << 20;
     if (c->cfg.dma_group_bytes == 0) c->cfg.dma_group_bytes = 64ull << 20;
     if (c->cfg.dma_streams == 0) c->cfg.dma_streams = 1;
     if (c->cfg.engine > FSW_ENGINE_DMAZ || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
@@ -752,20 +752,21 @@ static uint32_t zheader(const uint16_t* w) {
     return best == kZRaw ? kZRaw << 8 : emax | (best << 8) | (best_n << 16);
 }
 
-static void zencode_block(const uint16_t* w, uint32_t hdr, uint8_t* out /* zeroed, zblock_bytes(hdr) */) {
+// Coded block: 512 stream-A bytes at outa, zblock_b(hdr) stream-B bytes at outb (both zeroed).
+static void zencode_block(const uint16_t* w, uint32_t hdr, uint8_t* outa, uint8_t* outb) {
     const uint32_t h = hdr & 0xffu, b = (hdr >> 8) & 0xffu;
     uint32_t k = 0;
-    uint8_t* exc = out + 512 + 64 * b;
+    uint8_t* exc = outb + 64 * b;
     for (uint32_t i = 0; i < kZBlock / 2; ++i) {
         const uint32_t d = h - ((w[i] >> 7) & 0xffu);
-        out[i] = (uint8_t)(((w[i] >> 8) & 0x80u) | (w[i] & 0x7fu));
+        outa[i] = (uint8_t)(((w[i] >> 8) & 0x80u) | (w[i] & 0x7fu));
         if (d >> b) {  // exception: position and the whole word; code 0
             const uint32_t e = i | ((uint32_t)w[i] << 16);
             memcpy(exc + 4 * k++, &e, 4);
             continue;
         }
         for (uint32_t p = 0; p < b; ++p)
-            if ((d >> p) & 1u) out[512 + 64 * p + i / 8] |= (uint8_t)(1u << (i % 8));
+            if ((d >> p) & 1u) outb[64 * p + i / 8] |= (uint8_t)(1u << (i % 8));
     }
 }
 
@@ -808,8 +809,12 @@ static fsw_status build_link_code(Model& m, bool host_only) {
     for (size_t i = 0; i < pcs.size(); ++i) {
         ZPiece& pc = pcs[i];
         const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
-        uint32_t cb = 0;
-        for (uint32_t b = 0; b < nb; ++b) cb += zblock_bytes(hdr[i * bpp + b], std::min(kZBlock, pc.bytes - b * kZBlock));
+        uint32_t la = 0, lb = 0;  // stream A, stream B
+        for (uint32_t b = 0; b < nb; ++b) {
+            la += zblock_a(hdr[i * bpp + b], std::min(kZBlock, pc.bytes - b * kZBlock));
+            lb += zblock_b(hdr[i * bpp + b]);
+        }
+        const uint32_t cb = (uint32_t)align_up(la, 128) + lb;
         pc.coff = cur;
         pc.cbytes = cb;
         memcpy(pc.hdr, &hdr[i * bpp], sizeof pc.hdr);
@@ -827,14 +832,17 @@ static fsw_status build_link_code(Model& m, bool host_only) {
         const ZPiece& pc = pcs[i];
         uint8_t* out = m.zstore + pc.coff;
         const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
-        uint64_t o = 0;
+        uint32_t la = 0;
+        for (uint32_t b = 0; b < nb; ++b) la += zblock_a(hdr[i * bpp + b], std::min(kZBlock, pc.bytes - b * kZBlock));
+        uint64_t oa = 0, ob = align_up(la, 128);
         for (uint32_t b = 0; b < nb; ++b) {
             const uint8_t* raw = m.store + pc.off + (uint64_t)b * kZBlock;
             const uint32_t hd = hdr[i * bpp + b], n = std::min(kZBlock, pc.bytes - b * kZBlock);
             const uint32_t kind = (hd >> 8) & 0xffu;
-            if (kind == kZRaw) memcpy(out + o, raw, n);
-            else if (kind != kZZero) zencode_block(reinterpret_cast<const uint16_t*>(raw), hd, out + o);  // zeroed above
-            o += zblock_bytes(hd, n);
+            if (kind == kZRaw) memcpy(out + oa, raw, n);
+            else if (kind != kZZero) zencode_block(reinterpret_cast<const uint16_t*>(raw), hd, out + oa, out + ob);  // zeroed
+            oa += zblock_a(hd, n);
+            ob += zblock_b(hd);
         }
     });
     if (!host_only) {
@@ -1477,8 +1485,9 @@ static bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_
 // Engines whose layer kernels wait on per-layer byte counters (released by a swap kernel).
 static bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_coded(e); }
 
-// DMAZ decode CTAs unless the invoke sets copy_ctas: measured, 16 CTAs make the decode the bottleneck
-// (BERT-base 3.60 ms), 32 keep up with the copy engine (2.94 ms) (profiles/r01/linkcode/).
+// Decoding swap CTAs (DMAZ and SMZ) unless the invoke sets copy_ctas: measured, 16 CTAs make the DMAZ
+// decode the bottleneck (BERT-base 3.60 ms vs 2.94 with 32) and leave SMZ's TMA ring short of the link
+// (ResNet-50 0.783 vs 0.739 ms) (profiles/r01/linkcode/).
 constexpr uint32_t kDmazCtas = 32;
 
 struct InvokeCfg {
@@ -2019,7 +2028,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     };
     InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
-                 o.copy_ctas ? o.copy_ctas : engine == FSW_ENGINE_DMAZ ? std::max(c->cfg.copy_ctas, kDmazCtas) : c->cfg.copy_ctas,
+                 o.copy_ctas ? o.copy_ctas : engine_coded(engine) ? std::max(c->cfg.copy_ctas, kDmazCtas) : c->cfg.copy_ctas,
                  extents(gi), nullptr};
     ic.from = pcached ? m->split : 0;
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));

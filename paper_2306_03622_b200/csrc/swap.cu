@@ -164,41 +164,49 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
         const uint8_t* cp = src + (pc.coff - src_base);
         uint8_t* out = weight_ptr(dd, pc.off);
         const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;  // <= 16
-        // header (from the device piece table) and coded offset of block `lane` (exclusive scan)
+        // block `lane`: header (device piece table), stream-A and stream-B offsets (exclusive scans)
         const uint32_t hd = lane < nb ? __ldg(&pieces[p].hdr[lane]) : 0u;
-        const uint32_t sz = lane < nb ? zblock_bytes(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
-        uint32_t incl = sz;
+        const uint32_t sa = lane < nb ? zblock_a(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
+        const uint32_t sb = lane < nb ? zblock_b(hd) : 0u;
+        uint32_t ia = sa, ib = sb;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (uint32_t)o) incl += t;
+            const uint32_t ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+            if (lane >= (uint32_t)o) {
+                ia += ta;
+                ib += tb;
+            }
         }
-        const uint32_t boff = incl - sz;
+        const uint32_t aoff = ia - sa, boff = ib - sb;
+        const uint8_t* cb = cp + ((__shfl_sync(0xffffffffu, ia, 31) + 127u) & ~127u);  // stream B
         for (uint32_t b0 = 0; b0 < nb; b0 += U) {
-            // all loads of U blocks first (memory-level parallelism over the host link), then stores
+            // All loads of U blocks first (memory-level parallelism over the host link), then stores.
+            // Zero-copy (host) path: stream B of the group is read as one line-aligned window of
+            // 1 KiB (two 16-B chunks per lane) and routed by shuffles, so every host read covers
+            // whole 128-B lines; the HBM staging path reads stream B directly.
             uint4 q0[U], q1[U];
-            uint32_t hh[U], ob[U];
+            uint32_t hh[U], oa[U], ob[U];
+            uint4 wv0 = make_uint4(0u, 0u, 0u, 0u), wv1 = wv0;
+            const uint32_t last = min(b0 + U, nb) - 1;
+            const uint32_t w0 = __shfl_sync(0xffffffffu, boff, b0 & 31u) & ~127u;
+            const uint32_t wend = __shfl_sync(0xffffffffu, ib, last & 31u);
+            const bool windowed = !STAGE && wend - w0 <= 1024u;
+            if (windowed) {
+                const uint32_t wlim = (wend + 127u) & ~127u;
+                if (w0 + lane * 16u < wlim) wv0 = zld4<STAGE>(cb + w0 + lane * 16u);
+                if (w0 + 512u + lane * 16u < wlim) wv1 = zld4<STAGE>(cb + w0 + 512u + lane * 16u);
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint32_t b = b0 + u;
                 hh[u] = __shfl_sync(0xffffffffu, hd, b & 31u);
+                oa[u] = __shfl_sync(0xffffffffu, aoff, b & 31u);
                 ob[u] = __shfl_sync(0xffffffffu, boff, b & 31u);
-                const uint32_t kind = (hh[u] >> 8) & 0xffu, n = hh[u] >> 16;
-                const uint8_t* bp = cp + ob[u];
+                const uint32_t kind = (hh[u] >> 8) & 0xffu;
                 if (b >= nb || kind == kZZero) continue;
                 const bool full = b * kZBlock + kZBlock <= pc.bytes;
-                if (kind == kZRaw) {
-                    if (full) {
-                        q0[u] = zld4<STAGE>(bp + lane * 16u);
-                        q1[u] = zld4<STAGE>(bp + 512u + lane * 16u);
-                    }
-                    continue;
-                }
-                // stored bytes, then the planes + exceptions region as whole 16-B chunks (every load of
-                // the block is a 16-B-per-lane load: whole 128-B host read requests)
-                q0[u] = zld4<STAGE>(bp + lane * 16u);
-                const uint32_t rb = 64u * kind + 4u * n;
-                if (lane * 16u < rb) q1[u] = zld4<STAGE>(bp + 512u + lane * 16u);
+                q0[u] = (kind != kZRaw || full) ? zld4<STAGE>(cp + oa[u] + lane * 16u) : make_uint4(0u, 0u, 0u, 0u);
+                if (kind == kZRaw && full) q1[u] = zld4<STAGE>(cp + oa[u] + 512u + lane * 16u);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -216,32 +224,48 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                         st_v4(o4 + 32 + lane, q1[u]);
                     } else {  // the piece's partial tail (< 1 KiB, end of a layer region)
                         const uint32_t n16 = (pc.bytes - b * kZBlock) >> 4;
-                        for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, zld4<STAGE>(cp + ob[u] + i * 16u));
+                        for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, zld4<STAGE>(cp + oa[u] + i * 16u));
                     }
                 } else {
-                    // lane l's 16 code bits of plane p: bytes 64p + 2l .. +1 of the region, i.e. half
-                    // (l & 1) of word ((l & 7) >> 1) of chunk 4p + (l >> 3)
+                    // lane l's 16 code bits of plane p: stream-B bytes ob + 64p + 2l .. +1
                     uint32_t pl[4] = {0u, 0u, 0u, 0u};
+                    uint32_t ex = 0u;
+                    if (windowed) {
 #pragma unroll
-                    for (uint32_t pp = 0; pp < 4; ++pp)
-                        if (pp < kind)
-                            pl[pp] = (shfl_word(q1[u], 4u * pp + (lane >> 3), (lane & 7u) >> 1) >> (16u * (lane & 1u))) & 0xffffu;
-                    // exception j (lane j < 32): word (j & 3) of chunk 4b + (j >> 2)
-                    const uint32_t ex = n ? shfl_word(q1[u], (4u * kind + (lane >> 2)) & 31u, lane & 3u) : 0u;
+                        for (uint32_t pp = 0; pp < 4; ++pp) {
+                            if (pp >= kind) break;
+                            const uint32_t rel = ob[u] + 64u * pp + 2u * lane - w0, c = rel >> 4;
+                            const uint32_t x0 = shfl_word(wv0, c & 31u, (rel >> 2) & 3u);
+                            const uint32_t x1 = shfl_word(wv1, c & 31u, (rel >> 2) & 3u);
+                            pl[pp] = ((c < 32u ? x0 : x1) >> (16u * ((rel >> 1) & 1u))) & 0xffffu;
+                        }
+                        if (n) {
+                            const uint32_t rel = ob[u] + 64u * kind + 4u * lane - w0, c = (rel >> 4) & 63u;
+                            const uint32_t x0 = shfl_word(wv0, c & 31u, (rel >> 2) & 3u);
+                            const uint32_t x1 = shfl_word(wv1, c & 31u, (rel >> 2) & 3u);
+                            ex = c < 32u ? x0 : x1;
+                        }
+                    } else {
+#pragma unroll
+                        for (uint32_t pp = 0; pp < 4; ++pp)
+                            if (pp < kind) pl[pp] = zld16<STAGE>(cb + ob[u] + 64u * pp + 2u * lane);
+                        if (lane < n) ex = zld32<STAGE>(cb + ob[u] + 64u * kind + 4u * lane);
+                    }
                     uint4 o0, o1;
                     zdecode16(q0[u], pl, hh[u] & 0xffu, o0, o1);
                     st_v4(o4 + 2 * lane, o0);
                     st_v4(o4 + 2 * lane + 1, o1);
                     if (n) {
                         // exceptions overwrite their words after the warp's block stores (__syncwarp
-                        // orders the warp's memory operations); those past the loaded 512-B region or
-                        // past the 32nd are read directly (rare: the chooser keeps n small)
+                        // orders the warp's memory operations); past the 32nd, or past the window,
+                        // they are read directly (rare: the chooser keeps n small)
                         __syncwarp();
                         uint16_t* o16 = reinterpret_cast<uint16_t*>(bo);
-                        const uint32_t in_reg = min(n, min(32u, (512u - 64u * kind) / 4u));
-                        if (lane < in_reg) o16[ex & 0xffffu] = (uint16_t)(ex >> 16);
-                        for (uint32_t j = in_reg + lane; j < n; j += 32) {
-                            const uint32_t e = zld32<STAGE>(cp + ob[u] + 512u + 64u * kind + j * 4u);
+                        const uint32_t in_reg = min(n, 32u);
+                        const bool reg_ok = !windowed || ob[u] + 64u * kind + 4u * in_reg - w0 <= 1024u;
+                        if (lane < in_reg && reg_ok) o16[ex & 0xffffu] = (uint16_t)(ex >> 16);
+                        for (uint32_t j = reg_ok ? in_reg + lane : lane; j < n; j += 32) {
+                            const uint32_t e = zld32<STAGE>(cb + ob[u] + 64u * kind + j * 4u);
                             o16[e & 0xffffu] = (uint16_t)(e >> 16);
                         }
                     }
@@ -261,13 +285,136 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
     }
 }
 
+// ---- SMZ: zero-copy coded pieces through TMA bulk copies into a shared-memory ring ----------
+// The register decoder above keeps only ~2 KB of host reads in flight per warp and decodes between
+// round trips, which left the host link at 38-45 GB/s.  Here one thread per CTA streams whole coded
+// pieces (<= kZBuf bytes) with cp.async.bulk into a double-buffered ring (the async copy engine of
+// the SM, completion on an mbarrier); the CTA's 4 warps decode the previous piece from shared memory
+// meanwhile (blocks w, w+4, ... per warp), store it, and release it on its layer's counter.
+constexpr uint32_t kZBuf = 12288, kZRing = 2;
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ src, DevDesc dst, const DevDesc* __restrict__ desc,
+                                                   const ZPiece* __restrict__ pieces, uint32_t n_pieces,
+                                                   uint32_t* __restrict__ ready, DevCtl* __restrict__ own, DevCtl* gate, int sys) {
+    extern __shared__ __align__(128) uint8_t zring[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(zring + kZRing * kZBuf);
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kZRing);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    const DevDesc dd = desc ? *desc : dst;
+    if (tid == 0) {
+        atomicAdd(&gate->started, 1u);
+        for (uint32_t b = 0; b < kZRing; ++b)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // thread 0: claim the next piece into ring slot b and start its bulk copy (pieces larger than a
+    // slot are decoded straight from host memory instead; no copy, the barrier is just arrived on)
+    auto issue = [&](uint32_t b) {
+        const uint32_t p = atomicAdd(&own->ticket, 1u);
+        slot[b] = p;
+        if (p >= n_pieces) return;
+        if (p == 0) own->t_first = globaltimer();
+        const ZPiece& pc = pieces[p];
+        const uint32_t bb = smem_addr(&bar[b]);
+        if (pc.cbytes <= kZBuf) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(pc.cbytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_addr(zring + b * kZBuf)),
+                         "l"(src + pc.coff), "r"(pc.cbytes), "r"(bb)
+                         : "memory");
+        } else {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bb) : "memory");
+        }
+    };
+    if (tid == 0)
+        for (uint32_t b = 0; b < kZRing; ++b) issue(b);
+    __syncthreads();
+    for (uint32_t it = 0;; ++it) {
+        const uint32_t b = it % kZRing, par = (it / kZRing) & 1u;
+        const uint32_t p = slot[b];
+        if (p >= n_pieces) break;  // tickets grow with it: every later slot is past the end too
+        const ZPiece pc = pieces[p];
+        {
+            uint32_t ok = 0;
+            const uint32_t bb = smem_addr(&bar[b]);
+            do {
+                asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+                             : "=r"(ok) : "r"(bb), "r"(par) : "memory");
+            } while (!ok);
+        }
+        const uint8_t* cp = pc.cbytes <= kZBuf ? zring + b * kZBuf : src + pc.coff;  // generic address
+        uint8_t* out = weight_ptr(dd, pc.off);
+        const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
+        // every warp scans the piece's block offsets (stream A, stream B)
+        const uint32_t hd = lane < nb ? __ldg(&pieces[p].hdr[lane]) : 0u;
+        const uint32_t sa = lane < nb ? zblock_a(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
+        const uint32_t sb = lane < nb ? zblock_b(hd) : 0u;
+        uint32_t ia = sa, ib = sb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+            if (lane >= (uint32_t)o) {
+                ia += ta;
+                ib += tb;
+            }
+        }
+        const uint8_t* cb = cp + ((__shfl_sync(0xffffffffu, ia, 31) + 127u) & ~127u);
+        for (uint32_t blk = warp; blk < nb; blk += 4) {
+            const uint32_t h = __shfl_sync(0xffffffffu, hd, blk), oa = __shfl_sync(0xffffffffu, ia - sa, blk);
+            const uint32_t ob = __shfl_sync(0xffffffffu, ib - sb, blk);
+            const uint32_t kind = (h >> 8) & 0xffu, n = h >> 16;
+            uint8_t* bo = out + (uint64_t)blk * kZBlock;
+            uint4* o4 = reinterpret_cast<uint4*>(bo);
+            if (kind == kZZero) {
+                st_v4(o4 + 2 * lane, make_uint4(0u, 0u, 0u, 0u));
+                st_v4(o4 + 2 * lane + 1, make_uint4(0u, 0u, 0u, 0u));
+            } else if (kind == kZRaw) {
+                const uint32_t n16 = min(kZBlock, pc.bytes - blk * kZBlock) >> 4;
+                for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, *reinterpret_cast<const uint4*>(cp + oa + i * 16u));
+            } else {
+                const uint4 sm = *reinterpret_cast<const uint4*>(cp + oa + lane * 16u);
+                uint32_t pl[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+                for (uint32_t pp = 0; pp < 4; ++pp)
+                    if (pp < kind) pl[pp] = *reinterpret_cast<const uint16_t*>(cb + ob + 64u * pp + 2u * lane);
+                uint4 o0, o1;
+                zdecode16(sm, pl, h & 0xffu, o0, o1);
+                st_v4(o4 + 2 * lane, o0);
+                st_v4(o4 + 2 * lane + 1, o1);
+                if (n) {
+                    __syncwarp();  // exceptions overwrite their words after the warp's block stores
+                    uint16_t* o16 = reinterpret_cast<uint16_t*>(bo);
+                    for (uint32_t j = lane; j < n; j += 32) {
+                        const uint32_t e = *reinterpret_cast<const uint32_t*>(cb + ob + 64u * kind + 4u * j);
+                        o16[e & 0xffffu] = (uint16_t)(e >> 16);
+                    }
+                }
+            }
+        }
+        // every thread's stores performed at the release's scope, then one release for the piece
+        if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+        else __threadfence();
+        __syncthreads();  // the whole piece is stored; ring slot b is free
+        if (tid == 0) {
+            if (sys) red_release_sys_add(&ready[pc.layer], pc.bytes);
+            else red_release_gpu_add(&ready[pc.layer], pc.bytes);
+            atomicMax(&own->t_last, (unsigned long long)globaltimer());
+            issue(b);
+        }
+    }
+}
+
 void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
                   const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
                   DevCtl* gate, int sys, int stage, const uint32_t* progress) {
     if (stage)
         k_swapz<true, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
-    else
-        k_swapz<false, 3><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
+    else if (getenv("FSW_SWAPZ_REGS"))  // A/B hook: the register decoder straight from host memory
+        k_swapz<false, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
+    else  // src_base is 0 for the mapped host store (pieces address it by coff)
+        k_swapz_tma<<<ctas, 128, kZRing * kZBuf + 64, s>>>(src, dst, desc, pieces, n_pieces, ready, own, gate, sys);
 }
 
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap

@@ -20,40 +20,45 @@ def built():
 
 
 def decode_piece(cp: np.ndarray, hdr: np.ndarray, nbytes: int) -> np.ndarray:
-    """Decode one coded piece (uint8 array starting at its first block; hdr = its 32-bit block
-    headers) into `nbytes` raw bytes, from the format text of include/fsw.h.
+    """Decode one coded piece (uint8 array from its first byte; hdr = its 32-bit block headers) into
+    `nbytes` raw bytes, from the format text of include/fsw.h: stream A (sign|mantissa bytes, raw
+    blocks), padding to 128 B, stream B (code planes + exceptions of the coded blocks).
     Returns (raw bytes, coded bytes consumed)."""
     nb = -(-nbytes // 1024)
     assert not hdr[nb:].any(), "headers past the last block must be 0"
+    kinds = [(int(x) >> 8) & 0xFF for x in hdr[:nb]]
+    la = sum(min(1024, nbytes - 1024 * b) if k == 0xFF else 0 if k == 0xFE else 512 for b, k in enumerate(kinds))
+    oa, ob = 0, -(-la // 128) * 128
+    assert not cp[la:ob].any(), "stream-A padding must be zero"
     out = np.empty(nbytes, np.uint8)
-    o = 0
     for blk in range(nb):
         n_raw = min(1024, nbytes - 1024 * blk)
         hd = int(hdr[blk])
         h, b, n = hd & 0xFF, (hd >> 8) & 0xFF, hd >> 16
         dst = out[1024 * blk:1024 * blk + n_raw]
         if b == 0xFF:
-            dst[:] = cp[o:o + n_raw]
-            o += n_raw
+            dst[:] = cp[oa:oa + n_raw]
+            oa += n_raw
             continue
         assert n_raw == 1024, "a partial block must be raw"
         if b == 0xFE:
             dst[:] = 0
             continue
         assert b <= 4
-        m = cp[o:o + 512].astype(np.uint16)
+        m = cp[oa:oa + 512].astype(np.uint16)
+        oa += 512
         c = np.zeros(512, np.int64)
         for p in range(b):
-            bits = np.unpackbits(cp[o + 512 + 64 * p:o + 576 + 64 * p], bitorder="little")
+            bits = np.unpackbits(cp[ob + 64 * p:ob + 64 * p + 64], bitorder="little")
             c |= bits.astype(np.int64) << p
         e = h - c
         assert (e >= 0).all()
         w = ((m & 0x80) << 8) | (e.astype(np.uint16) << 7) | (m & 0x7F)
-        ex = cp[o + 512 + 64 * b:o + 512 + 64 * b + 4 * n].view("<u4")
+        ex = cp[ob + 64 * b:ob + 64 * b + 4 * n].view("<u4")
         w[(ex & 0xFFFF).astype(np.int64)] = (ex >> 16).astype(np.uint16)
         dst[:] = w.astype("<u2").view(np.uint8)
-        o += 512 + 64 * b + (4 * n + 15) // 16 * 16
-    return out, o
+        ob += 64 * b + (4 * n + 15) // 16 * 16
+    return out, ob
 
 
 def decode_all(rt, mid):
