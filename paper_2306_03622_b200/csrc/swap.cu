@@ -71,15 +71,6 @@ __device__ __forceinline__ uint4 zld4(const uint8_t* p) {
     return r;
 }
 template <bool STAGE>
-__device__ __forceinline__ uint2 zld2(const uint8_t* p) {
-    uint2 r;
-    if (STAGE)
-        asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
-    else
-        asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-    return r;
-}
-template <bool STAGE>
 __device__ __forceinline__ uint32_t zld16(const uint8_t* p) {
     uint16_t r;
     if (STAGE) asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(r) : "l"(p) : "memory");
@@ -409,9 +400,10 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
 void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
                   const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
                   DevCtl* gate, int sys, int stage, const uint32_t* progress) {
+    static const bool swapz_regs = getenv("FSW_SWAPZ_REGS") != nullptr;
     if (stage)
         k_swapz<true, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
-    else if (getenv("FSW_SWAPZ_REGS"))  // A/B hook: the register decoder straight from host memory
+    else if (swapz_regs)  // A/B hook: the register decoder straight from host memory
         k_swapz<false, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
     else  // src_base is 0 for the mapped host store (pieces address it by coff)
         k_swapz_tma<<<ctas, 128, kZRing * kZBuf + 64, s>>>(src, dst, desc, pieces, n_pieces, ready, own, gate, sys);

@@ -138,3 +138,44 @@ def test_dmaz_beats_the_link(rt, coded):
         rt.evict(mid)
         gbs.append(rt.invoke(mid, x, gpu=0, engine=ENGINE_DMAZ).stats["link_gbps"])
     assert np.median(gbs) > 60.0, gbs
+
+
+def _crafted_weights(spec, w, seed=11):
+    """Overwrite the first weight tensor with every block kind the decoders special-case: 4-bit codes,
+    one exception, > 32 exceptions (words with tiny exponents), all-zero blocks, ±0 / subnormals,
+    inf / NaN exponents, and whole pieces of random 16-bit words (raw, larger than an SMZ ring slot)."""
+    t = spec.tensors[0]
+    words = w[t.offset:t.offset + t.nbytes].view(np.uint16)
+    rng = np.random.default_rng(seed)
+    sm = rng.integers(0, 256, words.size).astype(np.uint16)
+    base = lambda m, e: ((m & 0x80) << 8) | (np.asarray(e).astype(np.uint16) << 7) | (m & 0x7F)
+    k = 0
+    words[k:k + 512] = base(sm[k:k + 512], rng.integers(100, 115, 512)); k += 512
+    blk = base(sm[k:k + 512], rng.integers(101, 117, 512)); blk[5] = base(sm[k + 5], 100); words[k:k + 512] = blk; k += 512
+    blk = base(sm[k:k + 512], rng.integers(120, 128, 512)); blk[::7] = base(sm[k:k + 512:7], 3); words[k:k + 512] = blk; k += 512
+    words[k:k + 2048] = 0; k += 2048
+    words[k:k + 512] = np.where(rng.random(512) < 0.5, 0x8000, 0) | rng.integers(0, 128, 512); k += 512
+    words[k:k + 512] = base(sm[k:k + 512], rng.integers(242, 256, 512)); k += 512
+    k = (k + 8191) // 8192 * 8192  # next 16-KiB piece boundary of this tensor
+    words[k:k + 3 * 8192] = rng.integers(0, 1 << 16, 3 * 8192)          # three all-raw pieces
+    return w
+
+
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+def test_coded_rare_block_kinds_bit_exact(rt, engine):
+    spec = synth.build_model("mlp")
+    w = _crafted_weights(spec, spec.build_weights())
+    mid = rt.register_spec(spec, w, link_code=True)
+    try:
+        pcs = rt.coded_pieces(mid)
+        hdr = pcs["hdr"].reshape(-1)
+        kinds = (hdr >> 8) & 0xFF
+        assert (kinds == 0xFE).any() and (kinds == 0xFF).any() and ((hdr >> 16) > 32).any()
+        assert (pcs["cbytes"] > 12288).any()  # larger than an SMZ ring slot: the direct-read fallback
+        for order in (0, ORDER_REVERSE):
+            rt.evict(mid)
+            r = rt.invoke(mid, spec.make_input(), gpu=0, engine=engine, order=order)
+            assert r.stats["engine"] == engine
+            np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    finally:
+        rt.unregister(mid)
