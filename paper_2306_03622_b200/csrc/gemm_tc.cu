@@ -510,6 +510,38 @@ void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading, PAP
     cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::smem_bytes(Cfg<128>::kMaxStages));
 }
 
+template <int BN>
+static int max_clusters_bn(int cz) {
+    using C = Cfg<BN>;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1, 1, cz);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = C::smem_bytes(C::kMaxStages);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 1;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = cz;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm<BN>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// Clusters of cz GEMM CTAs that can be resident at once on the current device (one wave).
+int gemm_max_active_clusters(int bn, int cz) {
+    switch (bn) {
+        case 16: return max_clusters_bn<16>(cz);
+        case 32: return max_clusters_bn<32>(cz);
+        case 64: return max_clusters_bn<64>(cz);
+        default: return max_clusters_bn<128>(cz);
+    }
+}
+
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {
     switch (a.bn) {
         case 16: launch_bn<16>(s, d, w, tmA, a); break;

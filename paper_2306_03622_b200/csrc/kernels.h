@@ -187,6 +187,7 @@ void launch_maxpool(cudaStream_t s, const PoolArgs& a);
 void launch_avgpool(cudaStream_t s, const PoolArgs& a);
 
 void init_gemm_attrs();
+int gemm_max_active_clusters(int bn, int cz);  // clusters of cz GEMM CTAs resident at once (this device)
 void init_swap_attrs();
 void init_ops_attrs();
 

@@ -301,7 +301,11 @@ constexpr uint32_t kGemmCtrs = 1u << 16;
 
 // Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor.
 struct Tiling { int bn; uint32_t splits, kt_per; bool cluster; };
-static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t a_kt_bytes, uint32_t /*m_rows*/) {
+// max_cl[bn / 16][cz]: clusters of cz CTAs resident at once (cudaOccupancyMaxActiveClusters; B200 fits
+// fewer CTAs in clusters than singly, e.g. 132 in clusters of 4), or nullptr (no cluster configs).
+using ClusterCap = std::array<std::array<int, 9>, 9>;
+static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t a_kt_bytes, uint32_t /*m_rows*/,
+                            const ClusterCap* max_cl = nullptr) {
     // Linear latency model fitted (least squares, rms 1.1 us) to the (BN, split) sweep of
     // tools/gemm_bench.cu on B200 over the batch-1 GEMM shapes of the paper's models
     // (profiles/r01/gemm_bench_sweep.txt): fixed cost, the bytes one CTA streams into shared memory,
@@ -330,7 +334,7 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
             // cluster split-K (partials reduced over DSMEM, gemm_tc.cu 2c): a second linear model fitted
             // to the single-wave cluster configurations of the same sweep (profiles/r01/gemm_sweep_cz2.txt,
             // rms 1.9 us); with the first model it picks the measured best (or within 0.5 us) on every shape
-            if (S >= 2 && S <= 8 && ctas <= 148) {
+            if (S >= 2 && S <= 8 && max_cl && ctas <= (uint64_t)(*max_cl)[bn / 16][S] * S) {
                 const double tc = 6.2102 + 0.0051 * cta_kb + 0.0737 * (bn / 16.0) + 0.0766 * ctas * cta_kb / 1e3 + 0.2124 * S;
                 if (tc < best_t - 1e-9) {
                     best_t = tc;
@@ -1072,7 +1076,14 @@ static fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
     auto ref = [&](const fsw_layer& L, uint32_t j) -> const TensorInfo& { return m.tensors[m.refs[L.first_ref + j]]; };
     uint64_t part_bytes = 0;  // split-K partial tiles, shared by all GEMMs of the plan
     auto set_tiling = [&](GemmArgs& a, uint64_t m_tiles, uint32_t m_rows, uint32_t a_kt_bytes) {
-        const Tiling t = choose_tiling(m_tiles, a.n_pad, a.K / 64, a_kt_bytes, m_rows);
+        // one-wave cluster capacity for every (BN, cluster size), queried once (the pool's GPUs are alike)
+        static const ClusterCap max_cl = []() {
+            ClusterCap t{};
+            for (int bn : {16, 32, 64, 128})
+                for (int cz = 2; cz <= 8; ++cz) t[bn / 16][cz] = gemm_max_active_clusters(bn, cz);
+            return t;
+        }();
+        const Tiling t = choose_tiling(m_tiles, a.n_pad, a.K / 64, a_kt_bytes, m_rows, &max_cl);
         a.bn = t.bn;
         a.m_rows = m_rows;
         a.splits = t.splits;

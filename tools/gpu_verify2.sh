@@ -1,3 +1,6 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_linkcode.py -x -q 2>&1 | tail -3
-for c in 16 32; do echo "ctas=$c"; timeout 600 python tools/linkcode_bench.py mlp resnet50 bert-base --reps 15 --ctas $c 2>&1 | tee gpurun_out/linkcode_tma_c$c.txt | grep -E "smz|dmaz" | cut -c1-200; done
+python tools/cluster_cap.py
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py -x -q 2>&1 | tail -2
+timeout 600 python tools/linkcode_bench.py resnet50 bert-base gpt2-xl --reps 5 2>&1 | grep -E "dmaz|smz" | python -c "
+import sys,json
+for l in sys.stdin: d=json.loads(l); print(d['model'], d['engine'], 'resident', d['resident_ms'], 'cold', d['p50_ms'])"
