@@ -20,8 +20,8 @@ SO = os.path.join(PKG, "libfsw.so")
 BUILD = os.path.join(PKG, "_build")
 
 CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu"]
-CXX_SOURCES = ["runtime.cpp", "sched.cpp"]
-HEADERS = ["kernels.h", "device.cuh", "policy.h"]
+CXX_SOURCES = ["runtime.cpp", "store.cpp", "plan.cpp", "graph.cpp", "invoke.cpp", "sched.cpp"]
+HEADERS = ["kernels.h", "device.cuh", "policy.h", "rt_internal.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,4 +1,4 @@
-// kernels.h — launch interface between the host runtime (runtime.cpp) and the sm_100a
+// kernels.h — launch interface between the host runtime (rt_internal.h and its units) and the sm_100a
 // kernels (*.cu).  Plain C++ (no device code); included by both sides of libfsw.
 #pragma once
 #include <cuda.h>

@@ -1,0 +1,322 @@
+// plan.cpp — per-(model, GPU) execution plan: workspace layout and the kernel list, with the
+// tcgen05 GEMM tiling chosen by cost models fitted to B200 sweeps.
+#include "rt_internal.h"
+
+// Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN and split-K factor.
+// max_cl[bn / 16][cz]: clusters of cz CTAs resident at once (cudaOccupancyMaxActiveClusters; B200 fits
+// fewer CTAs in clusters than singly, e.g. 132 in clusters of 4), or nullptr (no cluster configs).
+using ClusterCap = std::array<std::array<int, 9>, 9>;
+static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint32_t a_kt_bytes, uint32_t /*m_rows*/,
+                            const ClusterCap* max_cl = nullptr) {
+    // Linear latency model fitted (least squares, rms 1.1 us) to the (BN, split) sweep of
+    // tools/gemm_bench.cu on B200 over the batch-1 GEMM shapes of the paper's models
+    // (profiles/r01/gemm_bench_sweep.txt): fixed cost, the bytes one CTA streams into shared memory,
+    // the epilogue width, the split-K reduction, and the total L2->SM traffic (every N tile re-reads
+    // A).  One CTA per SM: a grid beyond one wave of 148 pays per wave.  Picks within 0.5 us of the
+    // measured best on every swept shape.
+    Tiling best{16, 1, kt, false};
+    double best_t = 1e30;
+    for (int bn : {16, 32, 64, 128}) {
+        if (n_pad % bn) continue;
+        const uint64_t base = m_tiles * (n_pad / bn);
+        for (uint32_t S = 1; S <= 16 && S <= kt; ++S) {
+            const uint32_t kt_per = (kt + S - 1) / S;
+            if ((kt + kt_per - 1) / kt_per != S) continue;  // no empty split
+            const uint64_t ctas = base * S;
+            if (S > 1 && ctas > 148) break;
+            const double cta_kb = kt_per * (double)(a_kt_bytes + bn * 128) / 1e3;
+            const double waves = (double)((ctas + 147) / 148);
+            double t = 4.44 + 0.0078 * cta_kb + 0.233 * (bn / 16.0) + 0.0428 * std::min<double>(ctas, 148) * cta_kb / 1e3;
+            if (S > 1) t += 2.51 + 0.0516 * S * (bn / 16.0);
+            t *= waves;
+            if (t < best_t - 1e-9) {
+                best_t = t;
+                best = {bn, S, kt_per, false};
+            }
+            // cluster split-K (partials reduced over DSMEM, gemm_tc.cu 2c): a second linear model fitted
+            // to the single-wave cluster configurations of the same sweep (profiles/r01/gemm_sweep_cz2.txt,
+            // rms 1.9 us); with the first model it picks the measured best (or within 0.5 us) on every shape
+            if (S >= 2 && S <= 8 && max_cl && ctas <= (uint64_t)(*max_cl)[bn / 16][S] * S) {
+                const double tc = 6.2102 + 0.0051 * cta_kb + 0.0737 * (bn / 16.0) + 0.0766 * ctas * cta_kb / 1e3 + 0.2124 * S;
+                if (tc < best_t - 1e-9) {
+                    best_t = tc;
+                    best = {bn, S, kt_per, true};
+                }
+            }
+        }
+    }
+    return best;
+}
+
+// ==========================================================================================
+// plan: workspace layout + kernel list for one (model, GPU)
+// ==========================================================================================
+fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
+    Gpu& g = c->gpus[gi];
+    auto p = std::make_unique<Plan>();
+    const size_t ns = m.slots.size();
+    // which f32 slots feed a GEMM (need a bf16 shadow)
+    std::vector<bool> need_shadow(ns, false);
+    uint64_t scratch = 0;  // im2col scratch
+    for (auto& L : m.layers) {
+        if (L.op == FSW_OP_LINEAR && linear_is_gemm(m, L) && m.slots[L.in0].dtype == FSW_DT_F32) need_shadow[L.in0] = true;
+        if (L.op == FSW_OP_CONV2D) {
+            const fsw_slot& si = m.slots[L.in0];
+            const fsw_slot& so = m.slots[L.out];
+            const fsw_tensor& W = m.tensors[m.refs[L.first_ref]].t;
+            if (conv_path(W, L, si, so) == CONV_IM2COL) {
+                const uint64_t K = (uint64_t)W.shape[1] * W.shape[2] * W.shape[3];
+                scratch = std::max(scratch, (uint64_t)so.shape[0] * so.shape[1] * align_up(K, 64) * 2);
+            }
+        }
+    }
+    uint64_t off = 0;
+    p->slot_off.resize(ns);
+    p->shadow_off.assign(ns, -1);
+    const uint64_t stage_input_off = kStageHdr;  // input slot lives in the device stage
+    for (size_t i = 0; i < ns; ++i) {
+        if ((int)i == m.input_slot) {
+            p->slot_off[i] = UINT64_MAX;
+            continue;
+        }
+        p->slot_off[i] = off;
+        off = align_up(off + slot_bytes(m.slots[i]), 1024);
+        if (need_shadow[i]) {
+            p->shadow_off[i] = (int64_t)off;
+            off = align_up(off + slot_numel(m.slots[i]) * 2, 1024);
+        }
+    }
+    const uint64_t scratch_off = off;
+    off = align_up(off + scratch, 1024);
+    p->ws_bytes = off;
+    if (off > g.ws_bytes) return fail(FSW_ENOMEM, "plan: workspace needs %llu bytes > %llu", (unsigned long long)off, (unsigned long long)g.ws_bytes);
+    if (m.input_bytes + kStageHdr > g.stage_cap || m.output_bytes > g.out_cap) return fail(FSW_ENOMEM, "plan: input/output too large");
+
+    auto sptr = [&](int s) -> uint8_t* {
+        if (s < 0) return nullptr;
+        if (s == m.input_slot) return g.dstage + stage_input_off;
+        return g.ws + p->slot_off[s];
+    };
+    auto shadow = [&](int s) -> uint16_t* {
+        return (s >= 0 && p->shadow_off[s] >= 0) ? reinterpret_cast<uint16_t*>(g.ws + p->shadow_off[s]) : nullptr;
+    };
+    auto ref = [&](const fsw_layer& L, uint32_t j) -> const TensorInfo& { return m.tensors[m.refs[L.first_ref + j]]; };
+    uint64_t part_bytes = 0;  // split-K partial tiles, shared by all GEMMs of the plan
+    auto set_tiling = [&](GemmArgs& a, uint64_t m_tiles, uint32_t m_rows, uint32_t a_kt_bytes) {
+        // one-wave cluster capacity for every (BN, cluster size), queried once (the pool's GPUs are alike)
+        static const ClusterCap max_cl = []() {
+            ClusterCap t{};
+            for (int bn : {16, 32, 64, 128})
+                for (int cz = 2; cz <= 8; ++cz) t[bn / 16][cz] = gemm_max_active_clusters(bn, cz);
+            return t;
+        }();
+        const Tiling t = choose_tiling(m_tiles, a.n_pad, a.K / 64, a_kt_bytes, m_rows, &max_cl);
+        a.bn = t.bn;
+        a.m_rows = m_rows;
+        a.splits = t.splits;
+        a.kt_per = t.kt_per;
+        a.ctr = g.gemm_ctr;
+        static const bool no_cz = getenv("FSW_GEMM_NO_CLUSTER_SPLIT") != nullptr;  // A/B hook
+        a.cz = t.cluster && !no_cz ? t.splits : 0;
+        // A multicast across an N cluster (plain GEMMs; the implicit-conv A box is not row-split)
+        a.mc = 1;
+        static const uint32_t mc_max = getenv("FSW_GEMM_MC") ? (uint32_t)atoi(getenv("FSW_GEMM_MC")) : 1;
+        for (uint32_t c : {8u, 4u, 2u})
+            if (!a.cz && c <= mc_max && m_rows == 128 && (a.n_pad / t.bn) % c == 0) {
+                a.mc = c;
+                break;
+            }
+        const uint64_t tiles = m_tiles * (a.n_pad / t.bn);
+        if (t.splits > 1) part_bytes = std::max<uint64_t>(part_bytes, tiles * t.splits * 128 * t.bn * 4);
+        return tiles <= kGemmCtrs;
+    };
+
+    CU(cudaSetDevice(g.dev));
+    for (uint32_t li = 0; li < m.layers.size(); ++li) {
+        const fsw_layer& L = m.layers[li];
+        const fsw_slot& si = m.slots[L.in0];
+        const fsw_slot& so = m.slots[L.out];
+        Launch x{};
+        x.layer = (int)li;
+        switch (L.op) {
+            case FSW_OP_EMBED: {
+                x.kind = K_EMBED;
+                EmbedArgs& a = x.embed;
+                a.ids = reinterpret_cast<const int32_t*>(sptr(L.in0));
+                a.n_tables = L.attr[0];
+                for (int j = 0; j < a.n_tables; ++j) {
+                    a.table_off[j] = ref(L, j).st_off;
+                    a.table_rows[j] = ref(L, j).t.shape[0];
+                    a.rule[j] = L.attr[1 + j];
+                }
+                a.T = so.shape[0];
+                a.C = so.shape[1];
+                if (so.dtype == FSW_DT_F32) {
+                    a.out = reinterpret_cast<float*>(sptr(L.out));
+                    a.out_bf16 = shadow(L.out);
+                } else {
+                    a.out_bf16 = reinterpret_cast<uint16_t*>(sptr(L.out));
+                }
+                break;
+            }
+            case FSW_OP_LAYERNORM: {
+                x.kind = K_LN;
+                LnArgs& a = x.ln;
+                a.in = reinterpret_cast<const float*>(sptr(L.in0));
+                a.C = slot_cols(si);
+                a.rows = (uint32_t)slot_rows(si);
+                float eps;
+                memcpy(&eps, &L.attr[0], 4);
+                a.eps = eps;
+                a.g_off = ref(L, 0).st_off;
+                a.b_off = ref(L, 1).st_off;
+                if (so.dtype == FSW_DT_F32) {
+                    a.out_f32 = reinterpret_cast<float*>(sptr(L.out));
+                    a.out_bf16 = shadow(L.out);
+                } else {
+                    a.out_bf16 = reinterpret_cast<uint16_t*>(sptr(L.out));
+                }
+                break;
+            }
+            case FSW_OP_LINEAR: {
+                const TensorInfo& W = ref(L, 0);
+                const bool has_b = L.n_refs > 1;
+                if (!linear_is_gemm(m, L)) {
+                    x.kind = K_GEMV;
+                    GemvArgs& a = x.gemv;
+                    a.x = sptr(L.in0);
+                    a.x_bf16 = si.dtype == FSW_DT_BF16;
+                    a.ldx = slot_cols(si);
+                    a.r0 = (uint32_t)L.attr[1];
+                    a.rows = (uint32_t)linear_rows(m, L);
+                    a.K = W.t.shape[1];
+                    a.N = W.t.shape[0];
+                    a.w_off = W.st_off;
+                    a.has_bias = has_b;
+                    a.b_off = has_b ? ref(L, 1).st_off : 0;
+                    a.act = L.attr[0];
+                    a.res = sptr(L.in1);
+                    a.res_bf16 = L.in1 >= 0 && m.slots[L.in1].dtype == FSW_DT_BF16;
+                    a.out = sptr(L.out);
+                    a.out_bf16 = so.dtype == FSW_DT_BF16;
+                    a.out2 = shadow(L.out);
+                } else {
+                    x.kind = K_GEMM;
+                    GemmArgs& a = x.gemm;
+                    a.M = (uint32_t)slot_rows(si);
+                    a.N = W.rows;
+                    a.K = W.cols_pad;
+                    a.n_pad = W.rows_pad;
+                    a.w_off = W.st_off;
+                    a.has_bias = has_b;
+                    a.b_off = has_b ? ref(L, 1).st_off : 0;
+                    a.act = L.attr[0];
+                    a.res = sptr(L.in1);
+                    a.res_bf16 = L.in1 >= 0 && m.slots[L.in1].dtype == FSW_DT_BF16;
+                    a.ld_res = a.N;
+                    a.out = sptr(L.out);
+                    a.out_bf16 = so.dtype == FSW_DT_BF16;
+                    a.ld_out = a.N;
+                    a.out2 = shadow(L.out);
+                    set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
+                    const void* abase = si.dtype == FSW_DT_BF16 ? (const void*)sptr(L.in0) : (const void*)shadow(L.in0);
+                    if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), 128 / a.mc))
+                        return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                }
+                break;
+            }
+            case FSW_OP_ATTENTION: {
+                x.kind = K_ATTN;
+                x.attn = {reinterpret_cast<const uint16_t*>(sptr(L.in0)), reinterpret_cast<uint16_t*>(sptr(L.out)),
+                          si.shape[0], (uint32_t)L.attr[0], (uint32_t)L.attr[1], L.attr[2]};
+                break;
+            }
+            case FSW_OP_CONV2D: {
+                const TensorInfo& W = ref(L, 0);
+                const uint32_t R = W.t.shape[1], S = W.t.shape[2], Cin = W.t.shape[3];
+                const ConvPath path = conv_path(W.t, L, si, so);
+                const uint32_t P = so.shape[0], Q = so.shape[1];
+                const void* abase = sptr(L.in0);
+                uint32_t acols = Cin;
+                if (path == CONV_IM2COL) {
+                    Launch y{};
+                    y.kind = K_IM2COL;
+                    y.layer = (int)li;
+                    y.im2col = {reinterpret_cast<const uint16_t*>(sptr(L.in0)), si.shape[0], si.shape[1], Cin,
+                                reinterpret_cast<uint16_t*>(g.ws + scratch_off), P, Q, R, S, (uint32_t)L.attr[1],
+                                (uint32_t)L.attr[2], R * S * Cin, W.cols_pad};
+                    p->launches.push_back(y);
+                    abase = g.ws + scratch_off;
+                    acols = W.cols_pad;
+                }
+                x.kind = K_GEMM;
+                GemmArgs& a = x.gemm;
+                a.M = P * Q;
+                a.N = W.rows;
+                a.K = W.cols_pad;
+                a.n_pad = W.rows_pad;
+                a.w_off = W.st_off;
+                a.has_bias = 1;
+                a.b_off = ref(L, 1).st_off;
+                a.act = L.attr[0];
+                a.res = sptr(L.in1);
+                a.res_bf16 = 1;
+                a.ld_res = a.N;
+                a.out = sptr(L.out);
+                a.out_bf16 = 1;
+                a.ld_out = a.N;
+                a.out2 = nullptr;
+                if (path == CONV_IMPLICIT) {
+                    const uint32_t Hb = conv_rows_per_tile(P, Q);
+                    a.conv = 1;
+                    a.Q = Q;
+                    a.stride = (uint32_t)L.attr[1];
+                    a.pad = (uint32_t)L.attr[2];
+                    a.S = S;
+                    a.Cin = Cin;
+                    a.Hb = Hb;
+                    set_tiling(a, (P + Hb - 1) / Hb, Hb * Q, Hb * Q * 128);
+                    if (!make_tmap_conv(&x.tmap, abase, si.shape[0], si.shape[1], Cin, Q, Hb, a.stride))
+                        return fail(FSW_ECUDA, "plan: conv tensor map failed (layer %u)", li);
+                } else {
+                    set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
+                    if (!make_tmap_act(&x.tmap, abase, a.M, acols, acols, 128 / a.mc))
+                        return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                }
+                break;
+            }
+            case FSW_OP_MAXPOOL:
+            case FSW_OP_AVGPOOL: {
+                x.kind = L.op == FSW_OP_MAXPOOL ? K_MAXPOOL : K_AVGPOOL;
+                PoolArgs& a = x.pool;
+                a.in = reinterpret_cast<const uint16_t*>(sptr(L.in0));
+                a.H = si.shape[0];
+                a.W = si.shape[1];
+                a.C = si.shape[2];
+                if (L.op == FSW_OP_MAXPOOL) {
+                    a.P = so.shape[0];
+                    a.Q = so.shape[1];
+                    a.k = L.attr[0];
+                    a.stride = L.attr[1];
+                    a.pad = L.attr[2];
+                    a.out = reinterpret_cast<uint16_t*>(sptr(L.out));
+                } else {
+                    a.out_f32 = reinterpret_cast<float*>(sptr(L.out));
+                }
+                break;
+            }
+        }
+        p->launches.push_back(x);
+    }
+    // split-K partials live after the activations and the im2col scratch
+    const uint64_t part_off = align_up(off, 1024);
+    p->ws_bytes = align_up(part_off + part_bytes, 1024);
+    if (p->ws_bytes > g.ws_bytes)
+        return fail(FSW_ENOMEM, "plan: workspace needs %llu bytes > %llu", (unsigned long long)p->ws_bytes, (unsigned long long)g.ws_bytes);
+    for (Launch& x : p->launches)
+        if (x.kind == K_GEMM) x.gemm.part = reinterpret_cast<float*>(g.ws + part_off);
+    p->built = true;
+    m.plans[gi] = std::move(p);
+    return FSW_OK;
+}
+

@@ -1,0 +1,308 @@
+// rt_internal.h — declarations shared by the translation units of libfsw's host runtime
+// (runtime.cpp, store.cpp, plan.cpp, graph.cpp, invoke.cpp).  Not part of the C-ABI.
+#pragma once
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cctype>
+#include <array>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <random>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "fsw.h"
+#include "kernels.h"
+#include "policy.h"
+
+using namespace fsw;
+
+// errors (runtime.cpp): set the thread-local message for fsw_last_error and return s
+fsw_status fail(fsw_status s, const char* fmt, ...);
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) return fail(FSW_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                                           __FILE__, __LINE__);                                    \
+    } while (0)
+
+
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+inline double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// ==========================================================================================
+// Arena: best-fit extent allocator with coalescing (the pre-allocated pool)
+// ==========================================================================================
+// model + plans
+// ==========================================================================================
+enum { LAYOUT_ROWMAJOR = 0, LAYOUT_TILED = 1 };
+
+struct TensorInfo {
+    fsw_tensor t;
+    uint64_t st_off = 0, st_bytes = 0;
+    uint32_t layout = LAYOUT_ROWMAJOR, rows = 0, cols = 0, rows_pad = 0, cols_pad = 0;
+    int owner = -1;
+    bool placed = false;
+};
+
+enum KernelKind { K_EMBED, K_LN, K_GEMV, K_GEMM, K_ATTN, K_IM2COL, K_MAXPOOL, K_AVGPOOL };
+
+struct Launch {  // one kernel of the layer graph (addresses resolved for one GPU workspace)
+    KernelKind kind;
+    int layer;
+    EmbedArgs embed;
+    LnArgs ln;
+    GemvArgs gemv;
+    GemmArgs gemm;
+    CUtensorMap tmap;
+    AttnArgs attn;
+    Im2colArgs im2col;
+    PoolArgs pool;
+};
+
+struct Gpu;
+
+struct GraphKey {
+    int cold, flags, order, engine;
+    uint64_t chunk;
+    uint32_t seed, ctas, extra;
+    uint64_t from = 0;   // first swapped store byte (partial caching: the cached prefix is skipped)
+    int64_t pext = -1;   // DMA graphs: prefix extent offset (baked address)
+    bool operator<(const GraphKey& o) const {
+        return std::tie(cold, flags, order, engine, chunk, seed, ctas, extra, from, pext) <
+               std::tie(o.cold, o.flags, o.order, o.engine, o.chunk, o.seed, o.ctas, o.extra, o.from, o.pext);
+    }
+};
+
+// DMA engine plan: layer-aligned copy groups dealt round-robin to `streams` copy streams, and
+// for every layer the per-stream group count that covers the layer's last byte.
+struct DmaPlan {
+    struct Group { uint64_t lo, hi; uint32_t stream; };
+    std::vector<Group> groups;
+    std::vector<std::array<uint32_t, kMaxWaitSrc>> target;  // [layer][stream]
+    uint32_t streams = 1;
+};
+
+struct PieceSet {
+    Piece* dev = nullptr;
+    std::vector<Piece> host;
+};
+
+// Link-coded engines: the coded pieces one swap moves (store offsets >= from), with the DMA+decode
+// engine's copy groups over the coded bytes [group lo, hi) and each piece's group index.
+struct ZPieceSet {
+    ZPiece* dev = nullptr;
+    std::vector<ZPiece> host;
+    std::vector<std::pair<uint64_t, uint64_t>> groups;  // DMAZ: coded-store byte ranges, in order
+    uint64_t cfrom = 0, cend = 0;                        // coded bytes [cfrom, cend) cover the pieces
+};
+
+struct Plan {  // one model on one GPU
+    bool built = false;
+    std::vector<Launch> launches;
+    std::vector<uint64_t> slot_off;      // workspace offset of each slot
+    std::vector<int64_t> shadow_off;     // bf16 shadow of an f32 slot, or -1
+    uint64_t ws_bytes = 0;
+    std::map<GraphKey, cudaGraphExec_t> graphs;
+    std::map<std::tuple<uint64_t, int, uint32_t, uint64_t>, PieceSet> pieces;  // (chunk, order, seed, from)
+    std::map<std::tuple<uint64_t, uint32_t, uint64_t, uint64_t>, DmaPlan> dma;  // (group bytes, streams, from, split)
+    // striped swap: source j of n gets every n-th piece; its table lives on the source's device
+    std::map<std::tuple<uint64_t, uint32_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, n, j, device, from)
+    // link-coded engines: (order, seed, from, DMAZ group bytes or 0 for SMZ) and striped (n, j, device, from)
+    std::map<std::tuple<int, uint32_t, uint64_t, uint64_t>, ZPieceSet> zp;
+    std::map<std::tuple<uint32_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;
+};
+
+struct Model {
+    uint32_t id;
+    std::string name;
+    std::vector<TensorInfo> tensors;
+    std::vector<uint32_t> refs;
+    std::vector<fsw_slot> slots;
+    std::vector<fsw_layer> layers;
+    std::vector<uint64_t> region_off, region_bytes;
+    int32_t input_slot, output_slot;
+    uint64_t input_bytes = 0, output_bytes = 0, algorithmic_bytes = 0;
+    uint32_t n_gemm = 0;
+    uint8_t* store = nullptr;  // pinned, mapped host store (execution order)
+    uint64_t store_bytes = 0, store_alloc = 0;
+    bool store_wc = false;
+    int numa_node = -1;        // node the store's pages were bound to (mbind before first touch), or -1
+    // exponent-coded copy of the store (FSW_REG_LINK_CODE; kernels.h): pinned, mapped
+    uint8_t* zstore = nullptr;
+    uint64_t zbytes = 0, zalloc = 0;
+    std::vector<ZPiece> zpieces;  // execution order, grp = 0
+    // residency per GPU
+    std::vector<int64_t> extent;       // pool offset of the model (split = 0) or of its suffix, or -1
+    // partial-parameter caching: store bytes [0, split) — whole layers —
+    // live in a separate prefix extent that pool evictions keep (valid once its bytes landed)
+    uint64_t split = 0;
+    std::vector<int64_t> pextent;      // prefix extent per GPU, or -1
+    std::vector<uint8_t> pvalid;       // prefix bytes present
+    std::vector<uint64_t> last_use;
+    std::vector<std::unique_ptr<Plan>> plans;
+    int inflight = 0;
+    // heavy / light class for placement and eviction: 1, 0, or -1 auto
+    int heavy = -1;
+    double cold_ms_sum = 0, warm_ms_sum = 0;
+    uint64_t n_cold_runs = 0, n_warm_runs = 0;
+};
+
+// A swap-kernel slot of a GPU acting as a striped-swap source for some target (its own ticket
+// counter, stream and completion event).  A GPU can feed several targets' swaps at once.
+struct SrcSlot {
+    DevCtl* ctl = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t done = nullptr;
+    bool busy = false;
+};
+constexpr int kSrcSlots = 4;
+
+struct Gpu {
+    int dev = 0;
+    SrcSlot src[kSrcSlots];
+    cudaStream_t sx = nullptr, sc = nullptr;
+    cudaStream_t sd[kMaxWaitSrc] = {};  // DMA copy streams (sd[0] == sc)
+    cudaEvent_t evd[kMaxWaitSrc] = {};  // fork / join events of the DMA streams
+    uint32_t* progress = nullptr;       // DMA: one group counter per copy stream, 128 B apart
+    uint32_t* gemm_ctr = nullptr;       // split-K tile arrival counters (self-resetting)
+    uint8_t* pool = nullptr;
+    uint64_t pool_bytes = 0;
+    fsw_arena* arena = nullptr;
+    uint8_t* ws = nullptr;
+    uint64_t ws_bytes = 0;
+    uint32_t* ready = nullptr;
+    uint32_t ready_cap = 0;
+    DevCtl* ctl = nullptr;
+    uint8_t* zstage = nullptr;   // DMAZ: device staging buffer for coded bytes (grown on demand)
+    uint64_t zstage_cap = 0;
+    uint32_t zstage_gen = 0;     // bumped on every reallocation (graphs bake the address)
+    cudaStream_t sz = nullptr;   // DMAZ: decode-kernel stream
+    uint8_t* dstage = nullptr;   // device: [DevDesc | pad | input]
+    uint8_t* hstage = nullptr;   // pinned: same layout
+    uint8_t* hout = nullptr;     // pinned, mapped: output (written by k_finish)
+    DevCtl* hctl = nullptr;      // pinned, mapped: ctl copy (written by k_finish)
+    uint64_t stage_cap = 0, out_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr, evfork = nullptr, evjoin = nullptr;
+    bool busy = false;
+    int loading = 0;  // 0, or 1 / 2 while a light / heavy model is being swapped in from the host
+    uint64_t generation = 0;
+    // stats
+    uint64_t n_evictions = 0, bytes_swapped_total = 0, n_cold = 0, n_warm = 0;
+};
+
+constexpr uint64_t kStageHdr = 256;
+constexpr uint32_t kGemmCtrs = 1u << 16;
+
+// Tiling of one tcgen05 GEMM launch (gemm_tc.cu): tile width BN, split-K factor, cluster reduction.
+struct Tiling { int bn; uint32_t splits, kt_per; bool cluster; };
+
+struct fsw_ctx {
+    fsw_config cfg{};
+    std::vector<Gpu> gpus;
+    std::vector<std::unique_ptr<Model>> models;  // index = id (nullptr after unregister)
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t clock = 0;
+    std::vector<std::vector<char>> peer;  // peer[i][j]: GPU i can store into GPU j's memory
+    std::vector<int> neighbor;            // GPU sharing a PCIe switch (-1 none), fsw_config.pcie_neighbor
+};
+
+
+// ---- slot, layer and tile helpers (registration and plans) ---------------------------------
+inline uint64_t slot_numel(const fsw_slot& s) {
+    uint64_t n = 1;
+    for (uint32_t i = 0; i < s.rank; ++i) n *= s.shape[i];
+    return n;
+}
+inline uint32_t dt_size(uint32_t dt) { return dt == FSW_DT_BF16 ? 2 : 4; }
+inline uint64_t slot_bytes(const fsw_slot& s) { return slot_numel(s) * dt_size(s.dtype); }
+inline uint32_t slot_cols(const fsw_slot& s) { return s.rank ? s.shape[s.rank - 1] : 1; }
+inline uint64_t slot_rows(const fsw_slot& s) { return slot_numel(s) / std::max<uint32_t>(1, slot_cols(s)); }
+
+// How a CONV2D layer runs (gemm_tc.cu): a 1x1/stride-1 conv is a plain GEMM over [P·Q][Cin];
+// Cin % 64 == 0 convs are implicit GEMMs (4-D TMA gathers of the NHWC input); the rest (the
+// ResNet stem, Cin = 3) go through an explicit im2col buffer.
+enum ConvPath { CONV_DIRECT, CONV_IMPLICIT, CONV_IM2COL };
+inline uint32_t conv_rows_per_tile(uint32_t P, uint32_t Q) { return std::min<uint32_t>(128 / Q, P); }
+inline ConvPath conv_path(const fsw_tensor& W, const fsw_layer& L, const fsw_slot& si, const fsw_slot& so) {
+    const uint32_t R = W.shape[1], Cin = W.shape[3], stride = (uint32_t)L.attr[1], Q = so.shape[1];
+    if (R == 1 && W.shape[2] == 1 && stride == 1 && L.attr[2] == 0 && Cin % 64 == 0) return CONV_DIRECT;
+    if (Cin % 64 == 0 && Q <= 128 && Q * stride <= 256 && conv_rows_per_tile(so.shape[0], Q) * stride <= 256 &&
+        stride <= 8 && si.rank == 3)
+        return CONV_IMPLICIT;
+    return CONV_IM2COL;
+}
+
+// Rows of in0 a LINEAR layer reads.
+inline uint64_t linear_rows(const Model& m, const fsw_layer& L) {
+    const uint64_t rin = slot_rows(m.slots[L.in0]);
+    return L.attr[2] > 0 ? (uint64_t)L.attr[2] : rin;
+}
+inline bool linear_is_gemm(const Model& m, const fsw_layer& L) { return linear_rows(m, L) > 8; }
+
+// Tile order of a GEMM weight W[N][K]: 1024-B atoms of 8 rows x 64 bf16,
+// atoms ordered k-tile-major; inside an atom row r is 128 B at r·128 and its 16-B chunk c
+// sits at chunk position c ^ r (the UMMA/TMA SWIZZLE_128B pattern).  Padding is zero.
+inline uint64_t tiled_off(uint64_t n, uint64_t k, uint64_t n_pad) {
+    return ((k / 64) * (n_pad / 8) + n / 8) * 1024 + (n % 8) * 128 + ((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
+}
+
+// ---- swap engines ----------------------------------------------------------------------------
+inline bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_DMAZ; }
+// Engines whose layer kernels wait on per-layer byte counters (released by a swap kernel).
+inline bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_coded(e); }
+
+// Decoding swap CTAs (DMAZ and SMZ) unless the invoke sets copy_ctas: measured, 16 CTAs make the DMAZ
+// decode the bottleneck (BERT-base 3.60 ms vs 2.94 with 32) and leave SMZ's TMA ring short of the link
+// (ResNet-50 0.783 vs 0.739 ms) (profiles/r01/linkcode/).
+constexpr uint32_t kDmazCtas = 32;
+
+struct InvokeCfg {
+    bool cold, no_overlap;
+    int engine;  // FSW_ENGINE_SM / FSW_ENGINE_DMA (resolved)
+    uint64_t chunk;
+    int order;
+    uint32_t seed, ctas;
+    DevDesc dst;                 // the target's extents (DMA graphs bake these addresses)
+    const DmaPlan* dma_plan;     // DMA engine only
+    DevDesc src{};               // DMA: copy source extents (a peer GPU's), unless src_host
+    bool src_host = true;        // DMA: copy from the pinned host store
+    uint64_t from = 0;           // first swapped store byte (a cached prefix is skipped)
+    bool striped = false;        // striped swap: sources launched outside the graph (fsw_invoke_ex)
+    uint32_t local_ctas = 0;     // striped: swap CTAs running on the target GPU itself (gate)
+    uint64_t zgrp = 0;           // DMAZ: copy-group bytes
+};
+
+// ---- cross-unit functions ----------------------------------------------------------------
+Model* find_model(fsw_ctx* c, uint32_t id);                                      // runtime.cpp
+void free_plan(Gpu& g, Plan& p);                                                 // runtime.cpp
+void free_store(Model& m, bool host_only);                                       // runtime.cpp
+fsw_status build_link_code(Model& m, bool host_only);                            // store.cpp
+fsw_status build_plan(fsw_ctx* c, Model& m, int gi);                             // plan.cpp
+fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint32_t seed, uint64_t from,
+                      PieceSet** out);                                           // graph.cpp
+const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams, uint64_t from);
+fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
+                       ZPieceSet** out);
+fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, int dev, uint64_t from, ZPieceSet** out);
+fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, uint64_t from,
+                             PieceSet** out);
+fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out);
+bool model_heavy(const Model& m);                                                // invoke.cpp
+void invalidate(fsw_ctx* c, Model& m, int gi, bool keep_prefix = false);         // invoke.cpp

@@ -7,7 +7,7 @@
 // them with 128-bit non-allocating loads from the mapped host store and 128-bit stores to
 // HBM, and publish each finished piece with a release-add of its byte count on the layer's
 // ready counter.  Layer kernels acquire that counter (device.cuh: wait_ready_*).
-// The copy-engine DMA engine (runtime.cpp) publishes readiness with stream memory writes instead.
+// The copy-engine DMA engine (graph.cpp) publishes readiness with stream memory writes instead.
 #include "device.cuh"
 
 namespace fsw {
