@@ -127,8 +127,8 @@ def max_over_ranks(local: dict, world: int) -> dict:
 def cpu_oracle_timing(spec, w, x, budget_s: float, max_reps: int = 50):
     """Time the oracle (tests-only package) as it stands on the host cores: bounded sample."""
     import oracle
-    cores = len(os.sched_getaffinity(0))
-    oracle.lib()
+    # all the host cores this process may run on (torchrun sets OMP_NUM_THREADS=1 per rank)
+    cores = oracle.lib().oracle_set_threads(len(os.sched_getaffinity(0)))
     times = []
     t_start = time.perf_counter()
     while len(times) < max_reps:
@@ -186,7 +186,11 @@ def run_fsw(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    gpu = local if world > 1 else 0
+    if world > 1:
+        import torch
+        gpu = local % max(1, torch.cuda.device_count())  # replicas share devices on a smaller box
+    else:
+        gpu = 0
     spec = synth.build_model(args.model)
     w = spec.build_weights()
     x = spec.make_input()
@@ -410,8 +414,13 @@ def run_striped(args):
     spec = synth.build_model(args.model)
     w = spec.build_weights()
     x = spec.make_input()
-    rt = Runtime(n_gpus=world, pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas, chunk_bytes=args.chunk_kb << 10,
-                 stripe_min_bytes=1)
+    import torch
+    ndev = max(1, torch.cuda.device_count())
+    # one pool GPU per rank; on a box with fewer devices than ranks the pool GPUs share devices
+    # ("virtual" sources: same protocol, no extra host links — a plumbing check, not a scaling number)
+    gpu_ids = [i % ndev for i in range(world)]
+    rt = Runtime(gpu_ids=gpu_ids, pool_bytes=args.pool_gb << 30, copy_ctas=args.copy_ctas,
+                 chunk_bytes=args.chunk_kb << 10, stripe_min_bytes=1)
     mid = rt.register_spec(spec, w, link_code=not args.no_link_code)
     info = rt.model_info(mid)
     out = np.empty(info["output_bytes"] // 4, dtype=np.float32)
@@ -454,7 +463,8 @@ def run_striped(args):
                    "model_store_bytes": store, "algorithmic_bytes": info["algorithmic_bytes"],
                    "swap_engine": ENGINE_NAMES[stats[0]["engine"]] + "-striped", "coded_bytes": int(info["coded_bytes"]),
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
-                   "parallelism": f"striped swap x{world} (one process drives the pool)"},
+                   "parallelism": f"striped swap x{world} (one process drives the pool)",
+                   "devices": ndev, "virtual_sources": ndev < world},
         "p99_ms": round(percentile(dev, 99), 4), "resident_p50_ms": round(percentile(warm, 50), 4),
         "swap_p50_ms": round(swap_p50, 4), "host_to_hbm_gbs": round(achieved, 2),
         "pipelined_roofline_ms": round(t_roof, 4), "frac_of_pipelined_roofline": round(t_roof / p50, 4),

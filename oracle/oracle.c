@@ -27,6 +27,15 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <omp.h>
+
+/* Thread control for the timed CPU baseline (bench.py): torchrun pins OMP_NUM_THREADS=1 per rank, so
+ * the thread count is set explicitly; the result does not depend on it (each output element is
+ * accumulated sequentially by one thread). */
+int oracle_set_threads(int n) {
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+}
 
 /* ---- table vocabulary (restated; see synth/models.py and include/fsw.h) ---- */
 enum { OR_EMBED = 1, OR_LAYERNORM = 2, OR_LINEAR = 3, OR_ATTENTION = 4,
