@@ -185,6 +185,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
 
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t tile = blockIdx.x * gridDim.y + blockIdx.y;
+    const DevDesc dd = *d;  // the invoke descriptor: written by the graph's first node, before any kernel
     const uint32_t m0 = blockIdx.x * a.m_rows, n0 = blockIdx.y * BN;
     const uint32_t kt_begin = blockIdx.z * a.kt_per;
     const uint32_t nkt = min(a.K / kBK, kt_begin + a.kt_per) - kt_begin;  // >= 1 (host plan)
@@ -226,7 +227,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
         if (lane == 0) {
             wait_ready_thread(w);
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            const uint8_t* wt = weight_ptr(*d, a.w_off);
+            const uint8_t* wt = weight_ptr(dd, a.w_off);
             const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
             auto load_w = [&](uint32_t st) {
                 const int s = st % stages;
@@ -305,6 +306,13 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     mbar_wait(done, 0);
     pdl_trigger();  // the successor's prologue and weight prefetch overlap this epilogue
     STAMP(3);
+    // this thread's 4 bias columns (weights: acquired by the producer before the MMAs completed), loaded
+    // now so the round trip overlaps the TMEM drain
+    constexpr uint32_t upr = BN / 4;
+    const uint32_t c_own = (threadIdx.x % upr) * 4;
+    uint2 bias_raw = make_uint2(0u, 0u);
+    if (a.has_bias && n0 + c_own < a.N && a.N % 4 == 0)
+        bias_raw = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) + n0 + c_own);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float* ct = reinterpret_cast<float*>(smem);
 #pragma unroll
@@ -327,7 +335,6 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     pdl_wait();  // activations (residual in, output / partials out) only after the predecessor
     uint32_t rows = min(a.m_rows, a.M - m0);
     const uint32_t cols = min((uint32_t)BN, a.N - n0);
-    constexpr uint32_t upr = BN / 4;
     uint32_t rb = 0;  // first tile row this CTA's epilogue covers
     if (a.cz > 1) {
         // 2c) cluster split-K: the cz CTAs of a (1, 1, cz) cluster hold the partial tiles of one output
@@ -418,15 +425,15 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     //     blockDim.x is a multiple of BN/4, a thread always owns the same 4 columns: its bias is
     //     loaded once, and its residual rows are loaded kE at a time before any of their stores
     //     (measured: a load -> store chain per unit cost ~0.3 us per unit, 9.8 us at BN = 128).
-    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(*d, a.b_off)) : nullptr;
+    const uint16_t* __restrict__ bias = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
     const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (a.res == nullptr || a.ld_res % 4 == 0);
     if (vec) {
         constexpr int kE = 8;
         const uint32_t units = rows * upr, c = (threadIdx.x % upr) * 4;
         const bool col_ok = c < cols;
         float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (bias && col_ok) {
-            const uint2 bv = *reinterpret_cast<const uint2*>(bias + n0 + c);
+        if (bias && col_ok) {  // c == c_own: prefetched after the MMAs
+            const uint2 bv = bias_raw;
             bsum = make_float4(__uint_as_float(bv.x << 16), __uint_as_float(bv.x & 0xffff0000u),
                                __uint_as_float(bv.y << 16), __uint_as_float(bv.y & 0xffff0000u));
         }
