@@ -127,10 +127,11 @@ extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group
 // Coded pieces of one link-coded swap (store offsets >= from) in the claim order.  DMAZ (grp > 0):
 // copy groups of whole pieces over the coded bytes, in execution order, tapered like the DMA engine's
 // (a group starting at coded offset `at` aims at min(grp, max(1 MiB, remaining / 2)) bytes), so the
-// decode and compute that trail the last group are short; each piece records its group.
+// decode and compute that trail the last group are short.  Groups are dealt round-robin to `streams`
+// copy streams; each piece records its group as (stream << 24 | index of the group on its stream).
 fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
-                              ZPieceSet** out) {
-    const auto key = std::make_tuple(order, seed, from, grp);
+                       uint32_t streams, ZPieceSet** out) {
+    const auto key = std::make_tuple(order, seed, from, grp, streams);
     auto it = p.zp.find(key);
     if (it != p.zp.end()) {
         *out = &it->second;
@@ -152,7 +153,8 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
         uint64_t lo = zs.cfrom;
         for (size_t i = 0; i < zs.host.size(); ++i) {
             ZPiece& pc = zs.host[i];
-            pc.grp = (uint32_t)zs.groups.size();
+            const uint32_t gi = (uint32_t)zs.groups.size();
+            pc.grp = ((gi % streams) << 24) | (gi / streams);
             const bool last = i + 1 == zs.host.size();
             const uint64_t hi = last ? zs.cend : zs.host[i + 1].coff;
             const uint64_t want = std::min(grp, std::max(tail_min, (zs.cend - lo) / 2));
@@ -160,7 +162,7 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
                 ramp > 0 ? std::min(want, std::max(tail_min, (uint64_t)((double)(lo - zs.cfrom) * ramp))) : want;
             const bool boundary = last || zs.host[i + 1].layer != pc.layer;
             if (last || hi - lo >= want || (boundary && hi - lo >= want_close)) {
-                zs.groups.push_back({lo, hi});
+                zs.groups.push_back({lo, hi, gi % streams});
                 lo = hi;
             }
         }
@@ -278,7 +280,8 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
         if (s != FSW_OK) return s;
     }
     if (ic.cold && engine_coded(ic.engine) && !ic.striped) {
-        fsw_status s = get_zpieces(m, p, g, ic.order, ic.seed, ic.from, ic.engine == FSW_ENGINE_DMAZ ? ic.zgrp : 0, &zs);
+        fsw_status s = get_zpieces(m, p, g, ic.order, ic.seed, ic.from, ic.engine == FSW_ENGINE_DMAZ ? ic.zgrp : 0,
+                                   ic.engine == FSW_ENGINE_DMAZ ? ic.zstreams : 1, &zs);
         if (s != FSW_OK) return s;
         if (ic.engine == FSW_ENGINE_DMAZ && zs->cend - zs->cfrom > g.zstage_cap) return fail(FSW_EINVAL, "staging buffer too small");
     }
@@ -298,7 +301,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
     if (ic.cold && ic.striped && !ic.no_overlap && ic.local_ctas) launch_gate(sx, g.ctl, ic.local_ctas);
     if (ic.cold && !ic.striped) {
         if (engine_bytes_ready(ic.engine)) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
-        if (ic.engine == FSW_ENGINE_DMAZ) cudaMemsetAsync(g.progress, 0, 128, sx);
+        if (ic.engine == FSW_ENGINE_DMAZ) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
         cudaEventRecord(g.evfork, sx);
         cudaStreamWaitEvent(sc, g.evfork, 0);
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
@@ -318,16 +321,21 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             if (!wv) return fail(FSW_ECUDA, "cuStreamWriteValue32 entry point unavailable");
             cudaEventRecord(g.evd[0], sc);
             cudaStreamWaitEvent(g.sz, g.evd[0], 0);
+            for (uint32_t j = 1; j < ic.zstreams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
             launch_swapz(g.sz, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
                          (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 1, g.progress);
-            uint32_t cnt = 0;
+            uint32_t cnt[kMaxWaitSrc] = {};
             for (const auto& gr : zs->groups) {
-                cudaMemcpyAsync(g.zstage + (gr.first - zs->cfrom), m.zstore + gr.first, gr.second - gr.first,
-                                cudaMemcpyHostToDevice, sc);
-                wv(sc, (CUdeviceptr)g.progress, (cuuint32_t)(++cnt), 0);
+                cudaStream_t sj = g.sd[gr.stream];
+                cudaMemcpyAsync(g.zstage + (gr.lo - zs->cfrom), m.zstore + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sj);
+                wv(sj, (CUdeviceptr)(g.progress + 32 * gr.stream), (cuuint32_t)(++cnt[gr.stream]), 0);
             }
-            cudaEventRecord(g.evd[1], g.sz);
-            cudaStreamWaitEvent(sc, g.evd[1], 0);
+            for (uint32_t j = 1; j < ic.zstreams; ++j) {
+                cudaEventRecord(g.evd[j], g.sd[j]);
+                cudaStreamWaitEvent(sc, g.evd[j], 0);
+            }
+            cudaEventRecord(g.evz, g.sz);
+            cudaStreamWaitEvent(sc, g.evz, 0);
         } else {
             // Copy-engine DMA from the pinned store (the paper's transfer) in
             // layer-aligned groups (its "group" pipelining unit), dealt round-robin

@@ -318,6 +318,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));
     if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr, ic.from);
     ic.zgrp = dgrp;
+    ic.zstreams = dstr;
     if (cold && engine == FSW_ENGINE_DMAZ && !striped && g.zstage_cap < m->zbytes) {
         // grow the staging buffer (graphs bake its address: the generation is part of their key)
         cudaFree(g.zstage);
@@ -357,7 +358,10 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                  cold && !striped ? (engine == FSW_ENGINE_SM ? ic.chunk : engine == FSW_ENGINE_SMZ ? 0 : dgrp) : 0,
                  cold && sm && !striped ? ic.seed : 0, cold ? (striped ? ic.local_ctas : sm ? ic.ctas : dstr) : 0, 0};
     key.from = cold ? ic.from : 0;
-    if (cold && engine == FSW_ENGINE_DMAZ && !striped) key.extra = g.zstage_gen;  // baked staging address
+    if (cold && engine == FSW_ENGINE_DMAZ && !striped) {
+        key.extra = g.zstage_gen;  // baked staging address
+        key.pext = dstr;           // copy streams
+    }
     if (cold && !sm) {  // DMA graphs bake addresses: the target extents and a peer source's extents
         key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);
         key.pext = m->pextent[gi];
@@ -457,7 +461,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                 if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
                 stats->n_kernels += ic.no_overlap ? 1 : 2;  // decoding swap kernel (+ gate)
                 ZPieceSet* zs = nullptr;
-                if (get_zpieces(*m, p, g, ic.order, ic.seed, ic.from, engine == FSW_ENGINE_DMAZ ? dgrp : 0, &zs) == FSW_OK) {
+                if (get_zpieces(*m, p, g, ic.order, ic.seed, ic.from, engine == FSW_ENGINE_DMAZ ? dgrp : 0,
+                                engine == FSW_ENGINE_DMAZ ? dstr : 1, &zs) == FSW_OK) {
                     stats->n_copies = (uint32_t)(engine == FSW_ENGINE_DMAZ ? zs->groups.size() : zs->host.size());
                     stats->wire_bytes = zs->cend - zs->cfrom;
                 }

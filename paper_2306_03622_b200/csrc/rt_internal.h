@@ -108,7 +108,8 @@ struct PieceSet {
 struct ZPieceSet {
     ZPiece* dev = nullptr;
     std::vector<ZPiece> host;
-    std::vector<std::pair<uint64_t, uint64_t>> groups;  // DMAZ: coded-store byte ranges, in order
+    struct Group { uint64_t lo, hi; uint32_t stream; };
+    std::vector<Group> groups;                          // DMAZ: coded-store byte ranges, in order
     uint64_t cfrom = 0, cend = 0;                        // coded bytes [cfrom, cend) cover the pieces
 };
 
@@ -124,7 +125,7 @@ struct Plan {  // one model on one GPU
     // striped swap: source j of n gets every n-th piece; its table lives on the source's device
     std::map<std::tuple<uint64_t, uint32_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, n, j, device, from)
     // link-coded engines: (order, seed, from, DMAZ group bytes or 0 for SMZ) and striped (n, j, device, from)
-    std::map<std::tuple<int, uint32_t, uint64_t, uint64_t>, ZPieceSet> zp;
+    std::map<std::tuple<int, uint32_t, uint64_t, uint64_t, uint32_t>, ZPieceSet> zp;  // + DMAZ copy streams
     std::map<std::tuple<uint32_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;
 };
 
@@ -193,6 +194,7 @@ struct Gpu {
     uint64_t zstage_cap = 0;
     uint32_t zstage_gen = 0;     // bumped on every reallocation (graphs bake the address)
     cudaStream_t sz = nullptr;   // DMAZ: decode-kernel stream
+    cudaEvent_t evz = nullptr;   // DMAZ: join of the decode stream
     uint8_t* dstage = nullptr;   // device: [DevDesc | pad | input]
     uint8_t* hstage = nullptr;   // pinned: same layout
     uint8_t* hout = nullptr;     // pinned, mapped: output (written by k_finish)
@@ -287,6 +289,7 @@ struct InvokeCfg {
     bool striped = false;        // striped swap: sources launched outside the graph (fsw_invoke_ex)
     uint32_t local_ctas = 0;     // striped: swap CTAs running on the target GPU itself (gate)
     uint64_t zgrp = 0;           // DMAZ: copy-group bytes
+    uint32_t zstreams = 1;       // DMAZ: copy streams (groups dealt round-robin, one counter each)
 };
 
 // ---- cross-unit functions ----------------------------------------------------------------
@@ -299,7 +302,7 @@ fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint
                       PieceSet** out);                                           // graph.cpp
 const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams, uint64_t from);
 fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
-                       ZPieceSet** out);
+                       uint32_t streams, ZPieceSet** out);
 fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, int dev, uint64_t from, ZPieceSet** out);
 fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, uint64_t from,
                              PieceSet** out);

@@ -112,6 +112,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaStreamCreateWithFlags(&g.sc, cudaStreamNonBlocking));
     g.sd[0] = g.sc;
     CU(cudaStreamCreateWithFlags(&g.sz, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&g.evz, cudaEventDisableTiming));
     for (int j = 1; j < kMaxWaitSrc; ++j) CU(cudaStreamCreateWithFlags(&g.sd[j], cudaStreamNonBlocking));
     for (int j = 0; j < kMaxWaitSrc; ++j) CU(cudaEventCreateWithFlags(&g.evd[j], cudaEventDisableTiming));
     CU(cudaMalloc(&g.progress, 128 * kMaxWaitSrc));
@@ -263,6 +264,7 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFree(g.dstage);
         cudaFree(g.zstage);
         cudaStreamDestroy(g.sz);
+        cudaEventDestroy(g.evz);
         cudaFreeHost(g.hstage);
         cudaFreeHost(g.hout);
         cudaFreeHost(g.hctl);

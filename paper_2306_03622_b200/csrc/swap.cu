@@ -149,7 +149,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
         if (p == 0 && lane == 0) own->t_first = globaltimer();
         const ZPiece pc = pieces[p];
         if (STAGE) {
-            if (lane == 0) wait_geq(progress, pc.grp + 1, own);
+            if (lane == 0) wait_geq(progress + 32 * (pc.grp >> 24), (pc.grp & 0xffffffu) + 1, own);
             __syncwarp();
         }
         const uint8_t* cp = src + (pc.coff - src_base);
