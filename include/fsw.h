@@ -216,6 +216,8 @@ typedef struct {
     uint32_t n_copies;      /* swap pieces (SM) or copy-engine groups (DMA) of this invoke      */
     uint64_t wire_bytes;    /* bytes that crossed the host / peer link (= bytes_swapped, except the
                                link-coded engines, which move coded bytes)                      */
+    double host_setup_ms;   /* host: call entry -> graph launched (placement, extent, staging)   */
+    double host_wait_ms;    /* host: graph launched -> output in the caller buffer              */
 } fsw_invoke_stats;
 
 /* Run one request: pick a GPU (resident and idle first, then the lowest idle id,

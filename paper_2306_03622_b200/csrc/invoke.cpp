@@ -419,6 +419,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         e = cudaGraphLaunch(exec, g.sx);
     }
     cudaEventRecord(g.ev1, g.sx);
+    const double t_launched = now_ms();
     if (e == cudaSuccess) e = cudaEventSynchronize(g.ev1);
     if (e != cudaSuccess) return finish(fail(FSW_ECUDA, "invoke: graph launch/sync: %s", cudaGetErrorString(e)));
     const DevCtl ctl = *g.hctl;
@@ -427,8 +428,11 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         return finish(fail(ctl.err == 3 ? FSW_EINVAL : FSW_ETIMEOUT, "invoke: %s (layer %d)", what, ctl.err_layer));
     }
     memcpy(output, g.hout, m->output_bytes);
+    const double t_out = now_ms();
     if (stats) {
         memset(stats, 0, sizeof *stats);
+        stats->host_setup_ms = t_launched - t_entry;
+        stats->host_wait_ms = t_out - t_launched;
         float ms = 0;
         cudaEventElapsedTime(&ms, g.ev0, g.ev1);
         stats->device_ms = ms;

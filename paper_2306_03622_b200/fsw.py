@@ -79,7 +79,7 @@ class InvokeStats(ctypes.Structure):
     _fields_ = [("total_ms", dbl), ("device_ms", dbl), ("swap_ms", dbl), ("swap_span_ms", dbl),
                 ("compute_tail_ms", dbl), ("bytes_swapped", u64), ("link_gbps", dbl), ("gpu", i32),
                 ("swap_kind", u32), ("n_sources", u32), ("n_kernels", u32), ("engine", u32), ("n_copies", u32),
-                ("wire_bytes", u64)]
+                ("wire_bytes", u64), ("host_setup_ms", dbl), ("host_wait_ms", dbl)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
