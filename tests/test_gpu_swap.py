@@ -79,6 +79,9 @@ def test_baseline_modes_bit_exact(rt, registered, flags):
 def test_swap_reaches_link_bandwidth(rt, registered, engine):
     """Sanity floor, not the bench: either swap engine sustains > 40 GB/s on BERT-base."""
     spec, w, x, mid = registered("bert-base")
+    for _ in range(3):  # untimed warm-up
+        rt.evict(mid)
+        rt.invoke(mid, x, gpu=0, engine=engine)
     gbs = []
     for _ in range(5):
         rt.evict(mid)
