@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--period-ms", type=float, default=2000.0)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
+    ap.add_argument("--link-code", action="store_true", help="register every model link-coded (DESIGN.md §5b)")
     args = ap.parse_args()
     counts = [int(c) for c in args.mix.split(",")]
     kinds = ["resnet50"] * counts[0] + ["bert-base"] * counts[1] + ["gpt2-xl"] * counts[2]
@@ -66,7 +67,7 @@ def main():
     mids, inputs, outs = [], [], []
     for i, k in enumerate(kinds):
         spec = synth.build_model(k, seed=1000 + i)
-        mids.append(rt.register_spec(spec, spec.build_weights()))
+        mids.append(rt.register_spec(spec, spec.build_weights(), link_code=args.link_code))
         inputs.append(spec.make_input())
         outs.append(rt.model_info(mids[-1])["output_bytes"])
     print(f"registered {len(kinds)} functions in {time.time() - t0:.1f}s", flush=True)
@@ -92,6 +93,7 @@ def main():
         per_class.setdefault(kinds[fid], []).append(r["total_ms"])
     summary = {
         "functions": len(kinds), "mix": dict(zip(["resnet50", "bert-base", "gpt2-xl"], counts)),
+        "link_code": args.link_code, "rates_per_min": [args.rate_lo, args.rate_hi],
         "requests": len(res), "duration_s": args.duration_s, "wall_s": round(wall, 2), "pool_gb": args.pool_gb,
         "slo_compliant_function_ratio": round(st["slo_compliant_functions"] / max(1, st["active_functions"]), 4),
         "request_deadline_ratio": round(st["met_deadline"] / max(1, st["completed"]), 4),
