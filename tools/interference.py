@@ -26,13 +26,14 @@ def main():
     ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--models", default="mlp,resnet50,bert-base,gpt2-2L")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "interference.json"))
+    ap.add_argument("--link-code", action="store_true", help="register the models link-coded (SMZ / DMAZ engines)")
     args = ap.parse_args()
     names = args.models.split(",")
     rt = Runtime(gpu_ids=[0, 0], pool_bytes=3 << 30)
     mids, xs = {}, {}
     for n in names:
         sp = synth.build_model(n)
-        mids[n] = rt.register_spec(sp, sp.build_weights())
+        mids[n] = rt.register_spec(sp, sp.build_weights(), link_code=args.link_code)
         xs[n] = sp.make_input()
 
     def cold(n, gpu):
