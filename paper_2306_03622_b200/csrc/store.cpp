@@ -177,19 +177,25 @@ static uint32_t zheader(const uint16_t* w) {
 // Coded block: 512 stream-A bytes at outa, zblock_b(hdr) stream-B bytes at outb (both zeroed).
 static void zencode_block(const uint16_t* w, uint32_t hdr, uint8_t* outa, uint8_t* outb) {
     const uint32_t h = hdr & 0xffu, b = (hdr >> 8) & 0xffu;
+    uint8_t code[kZBlock / 2];
     uint32_t k = 0;
     uint8_t* exc = outb + 64 * b;
     for (uint32_t i = 0; i < kZBlock / 2; ++i) {
         const uint32_t d = h - ((w[i] >> 7) & 0xffu);
         outa[i] = (uint8_t)(((w[i] >> 8) & 0x80u) | (w[i] & 0x7fu));
-        if (d >> b) {  // exception: position and the whole word; code 0
+        const bool ex = (d >> b) != 0;  // exception: position and the whole word; code 0
+        code[i] = ex ? 0 : (uint8_t)d;
+        if (ex) {
             const uint32_t e = i | ((uint32_t)w[i] << 16);
             memcpy(exc + 4 * k++, &e, 4);
-            continue;
         }
-        for (uint32_t p = 0; p < b; ++p)
-            if ((d >> p) & 1u) outb[64 * p + i / 8] |= (uint8_t)(1u << (i % 8));
     }
+    for (uint32_t p = 0; p < b; ++p)  // plane p, 64 words per 64-bit lane word (bit i % 64 = word i)
+        for (uint32_t q = 0; q < 8; ++q) {
+            uint64_t v = 0;
+            for (uint32_t i = 0; i < 64; ++i) v |= (uint64_t)((code[64 * q + i] >> p) & 1u) << i;
+            memcpy(outb + 64 * p + 8 * q, &v, 8);
+        }
 }
 
 template <typename F>
@@ -249,7 +255,9 @@ fsw_status build_link_code(Model& m, bool host_only) {
     madvise(p, m.zalloc, MADV_HUGEPAGE);
     if (m.numa_node >= 0) bind_pages(p, m.zalloc, m.numa_node);
     m.zstore = static_cast<uint8_t*>(p);
-    memset(m.zstore, 0, m.zalloc);  // alignment gaps stay zero
+    parallel_for((m.zalloc + (2u << 20) - 1) / (2u << 20), [&](size_t i) {  // alignment gaps stay zero
+        memset(m.zstore + i * (2u << 20), 0, std::min<uint64_t>(2u << 20, m.zalloc - i * (2u << 20)));
+    });
     parallel_for(pcs.size(), [&](size_t i) {
         const ZPiece& pc = pcs[i];
         uint8_t* out = m.zstore + pc.coff;
@@ -367,16 +375,23 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
     }
     // pack (zero padding everywhere; first touch happens here)
     const uint8_t* src = static_cast<const uint8_t*>(d->weights);
-    memset(m->store, 0, m->store_alloc);
+    // zero fill (first touch, 2-MiB chunks in parallel), then the tensors: row-major copies, and GEMM
+    // weights re-laid in tile order one source row per task (16-bit stores; tiled_off keeps rows apart)
+    const size_t kChunk = 2u << 20;
+    parallel_for((m->store_alloc + kChunk - 1) / kChunk, [&](size_t i) {
+        memset(m->store + i * kChunk, 0, std::min<uint64_t>(kChunk, m->store_alloc - i * kChunk));
+    });
     for (auto& ti : m->tensors) {
         if (ti.owner < 0) continue;
         if (ti.layout == LAYOUT_ROWMAJOR) {
             memcpy(m->store + ti.st_off, src + ti.t.offset, ti.t.bytes);
         } else {
             const uint16_t* w = reinterpret_cast<const uint16_t*>(src + ti.t.offset);
-            for (uint64_t n = 0; n < ti.rows; ++n)
+            uint8_t* base = m->store + ti.st_off;
+            parallel_for(ti.rows, [&](size_t n) {
                 for (uint64_t k = 0; k < ti.cols; ++k)
-                    memcpy(m->store + ti.st_off + tiled_off(n, k, ti.rows_pad), &w[n * ti.cols + k], 2);
+                    *reinterpret_cast<uint16_t*>(base + tiled_off(n, k, ti.rows_pad)) = w[n * ti.cols + k];
+            });
         }
     }
     if (!wc && !host_only) {
