@@ -109,6 +109,45 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def gpu_local_core(gpu: int):
+    """A host core on the NUMA node of `gpu`'s PCIe root (sysfs), for pinning the timing thread
+    (host noise); the last core the process may run on when the node is unknown."""
+    allowed = sorted(os.sched_getaffinity(0))
+    try:
+        bus = subprocess.run(["nvidia-smi", "-i", str(gpu), "--query-gpu=pci.bus_id", "--format=csv,noheader"],
+                             capture_output=True, text=True, timeout=10).stdout.strip().lower()[-12:]
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read())
+        cores = []
+        for part in open(f"/sys/devices/system/node/node{max(node, 0)}/cpulist").read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cores += list(range(int(lo), int(hi or lo) + 1))
+        local = [c for c in cores if c in allowed]
+        if local:
+            return local[-1]
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    return allowed[-1]
+
+
+class PinnedThread:
+    """Pin the calling thread to one core for the timed region, then restore its affinity."""
+
+    def __init__(self, core):
+        self.core, self.saved = core, None
+
+    def __enter__(self):
+        try:
+            self.saved = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {self.core})
+        except OSError:
+            self.saved = None
+        return self
+
+    def __exit__(self, *a):
+        if self.saved:
+            os.sched_setaffinity(0, self.saved)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -208,7 +247,8 @@ def run_fsw(args):
         cold_step()
     if world > 1:
         dist.barrier()
-    with ClockSampler(gpu) as clk:
+    core = gpu_local_core(gpu)
+    with ClockSampler(gpu) as clk, PinnedThread(core):  # sampler started first: it is not pinned
         t0 = time.perf_counter()
         stats = [cold_step() for _ in range(args.steps)]
         wall = time.perf_counter() - t0
@@ -222,11 +262,12 @@ def run_fsw(args):
     wire = stats[0]["wire_bytes"]
     # e2e: the public fsw_invoke (scheduler picks the GPU), host buffers, H2D/D2H inside
     e2e = []
-    for _ in range(max(3, args.steps // 2)):
-        rt.evict(mid, -1)
-        t1 = time.perf_counter()
-        rt.invoke_plain(mid, x, out)
-        e2e.append((time.perf_counter() - t1) * 1e3)
+    with PinnedThread(core):
+        for _ in range(max(3, args.steps // 2)):
+            rt.evict(mid, -1)
+            t1 = time.perf_counter()
+            rt.invoke_plain(mid, x, out)
+            e2e.append((time.perf_counter() - t1) * 1e3)
     # resident (native) inference for comparison
     warm = [rt.invoke(mid, x, out=out, gpu=0).stats["device_ms"] for _ in range(args.steps)]
     # the other swap engines on the same workload (context: which engine wins and by how much)
@@ -358,6 +399,7 @@ def run_fsw(args):
                    "sm_copy_ctas": args.copy_ctas or 16, "dma_group_bytes": (args.dma_group_mb or 64) << 20,
                    "dma_streams": args.dma_streams or 1,
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
+                   "timing_thread_core": core,
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
         "p99_ms": round(percentile(dev, 99), 4), "mean_ms": round(statistics.mean(dev), 4),
         "min_ms": round(min(dev), 4),
