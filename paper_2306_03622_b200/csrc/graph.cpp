@@ -149,6 +149,7 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
         // head ramp on by default here (measured: DMAZ ResNet-50 0.890 -> 0.809 ms at ramp 4, BERT-base
         // neutral); off for the plain DMA engine, where it cost ResNet-50 2-5 %
         static const double ramp = getenv("FSW_DMAZ_RAMP") ? atof(getenv("FSW_DMAZ_RAMP")) : 4.0;
+        static const double taper = getenv("FSW_DMAZ_TAPER") ? atof(getenv("FSW_DMAZ_TAPER")) : 0.5;  // sweep hook
         const uint64_t tail_min = std::min<uint64_t>(grp, 1ull << 20);
         uint64_t lo = zs.cfrom;
         for (size_t i = 0; i < zs.host.size(); ++i) {
@@ -157,7 +158,7 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
             pc.grp = ((gi % streams) << 24) | (gi / streams);
             const bool last = i + 1 == zs.host.size();
             const uint64_t hi = last ? zs.cend : zs.host[i + 1].coff;
-            const uint64_t want = std::min(grp, std::max(tail_min, (zs.cend - lo) / 2));
+            const uint64_t want = std::min(grp, std::max(tail_min, (uint64_t)((double)(zs.cend - lo) * taper)));
             const uint64_t want_close =
                 ramp > 0 ? std::min(want, std::max(tail_min, (uint64_t)((double)(lo - zs.cfrom) * ramp))) : want;
             const bool boundary = last || zs.host[i + 1].layer != pc.layer;
