@@ -385,6 +385,16 @@ fsw_status fsw_debug_dma_plan(fsw_ctx* ctx, uint32_t model_id, uint64_t group_by
                               uint64_t* group_lo_hi, uint32_t* group_stream, uint32_t cap_groups,
                               uint32_t* n_groups, uint32_t* layer_targets);
 
+/* The DMAZ engine's copy plan of a link-coded model (host logic only, usable with FSW_HOST_ONLY):
+ * n_groups copy groups [lo, hi) of the coded store, in order, tiling it; group i goes to copy
+ * stream group_stream[i] = i mod streams; piece_group[p] (one entry per coded piece, see
+ * fsw_debug_coded_pieces) = (stream << 24) | (index of the piece's group among its stream's groups).
+ * ESTATE if the model is not link-coded; EINVAL for a bad argument or cap_groups too small (n_groups
+ * is still set).  Any output pointer except n_groups may be NULL.                              */
+fsw_status fsw_debug_dmaz_plan(fsw_ctx* ctx, uint32_t model_id, uint64_t group_bytes, uint32_t streams,
+                               uint64_t* group_lo_hi, uint32_t* group_stream, uint32_t cap_groups,
+                               uint32_t* n_groups, uint32_t* piece_group);
+
 /* ---------------------------------------------------------------------------------------
  * Extent allocator of the weight pool (pure host logic, usable without a GPU; tests).
  * Best-fit over a free list of [offset, size) extents with coalescing on free.

@@ -129,15 +129,9 @@ extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group
 // (a group starting at coded offset `at` aims at min(grp, max(1 MiB, remaining / 2)) bytes), so the
 // decode and compute that trail the last group are short.  Groups are dealt round-robin to `streams`
 // copy streams; each piece records its group as (stream << 24 | index of the group on its stream).
-fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
-                       uint32_t streams, ZPieceSet** out) {
-    const auto key = std::make_tuple(order, seed, from, grp, streams);
-    auto it = p.zp.find(key);
-    if (it != p.zp.end()) {
-        *out = &it->second;
-        return FSW_OK;
-    }
-    ZPieceSet zs;
+// Host part of a link-coded swap plan (no device memory): the pieces >= from in execution order, and
+// for DMAZ (grp > 0) the copy groups.  Used by get_zpieces and by the host-only debug export.
+static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32_t streams, ZPieceSet& zs) {
     for (const ZPiece& pc : m.zpieces)
         if (pc.off >= from) zs.host.push_back(pc);
     if (zs.host.empty()) return fail(FSW_EINVAL, "link-coded swap with nothing to move");
@@ -168,6 +162,20 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
             }
         }
     }
+    return FSW_OK;
+}
+
+fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
+                       uint32_t streams, ZPieceSet** out) {
+    const auto key = std::make_tuple(order, seed, from, grp, streams);
+    auto it = p.zp.find(key);
+    if (it != p.zp.end()) {
+        *out = &it->second;
+        return FSW_OK;
+    }
+    ZPieceSet zs;
+    fsw_status st = make_zplan(m, from, grp, streams, zs);
+    if (st != FSW_OK) return st;
     if (order == FSW_ORDER_REVERSE) std::reverse(zs.host.begin(), zs.host.end());
     if (order == FSW_ORDER_RANDOM) {
         std::mt19937_64 rng(seed);
@@ -177,6 +185,32 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
     CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
     CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
     *out = &p.zp.emplace(key, std::move(zs)).first->second;
+    return FSW_OK;
+}
+
+// Host-only inspection of the DMAZ copy plan (tests; no GPU needed).
+extern "C" fsw_status fsw_debug_dmaz_plan(fsw_ctx* c, uint32_t id, uint64_t group_bytes, uint32_t streams,
+                                          uint64_t* group_lo_hi, uint32_t* group_stream, uint32_t cap_groups,
+                                          uint32_t* n_groups, uint32_t* piece_group) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!m->zstore) return fail(FSW_ESTATE, "model %u is not link-coded", id);
+    if (!n_groups || group_bytes == 0 || streams == 0 || streams > (uint32_t)kMaxWaitSrc)
+        return fail(FSW_EINVAL, "dmaz_plan: bad argument");
+    ZPieceSet zs;
+    fsw_status st = make_zplan(*m, 0, group_bytes, streams, zs);
+    if (st != FSW_OK) return st;
+    *n_groups = (uint32_t)zs.groups.size();
+    if (zs.groups.size() > cap_groups) return fail(FSW_EINVAL, "dmaz_plan: %zu groups > cap %u", zs.groups.size(), cap_groups);
+    for (size_t i = 0; i < zs.groups.size(); ++i) {
+        if (group_lo_hi) {
+            group_lo_hi[2 * i] = zs.groups[i].lo;
+            group_lo_hi[2 * i + 1] = zs.groups[i].hi;
+        }
+        if (group_stream) group_stream[i] = zs.groups[i].stream;
+    }
+    if (piece_group)
+        for (size_t i = 0; i < zs.host.size(); ++i) piece_group[i] = zs.host[i].grp;
     return FSW_OK;
 }
 

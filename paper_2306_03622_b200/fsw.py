@@ -146,7 +146,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
-           "fsw_debug_read_coded", "fsw_debug_coded_pieces"]
+           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan"]
 
 _lib = None
 
@@ -179,6 +179,7 @@ def lib():
         L.fsw_debug_read_slot.argtypes = [vp, u32, i32, i32, vp, u64]
         L.fsw_debug_read_coded.argtypes = [vp, u32, vp, u64]
         L.fsw_debug_coded_pieces.argtypes = [vp, u32, vp, u32, ctypes.POINTER(u32)]
+        L.fsw_debug_dmaz_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
         L.fsw_arena_create.argtypes = [u64, u64]
         L.fsw_arena_create.restype = vp
         L.fsw_arena_destroy.argtypes = [vp]
@@ -431,6 +432,17 @@ class Runtime:
         dt = np.dtype([("off", "<u8"), ("coff", "<u8"), ("bytes", "<u4"), ("cbytes", "<u4"), ("layer", "<u4"),
                        ("pad", "<u4"), ("hdr", "<u4", (16,))])
         return np.frombuffer(bytes(arr), dtype=dt)[:n.value].copy()
+
+    def dmaz_plan(self, mid: int, group_bytes: int, streams: int = 1):
+        """DMAZ copy plan: (groups [n][2] coded [lo, hi), stream [n], piece_group [n_pieces])."""
+        n = u32()
+        lib().fsw_debug_dmaz_plan(self.h, mid, group_bytes, streams, None, None, 0, ctypes.byref(n), None)
+        lohi = np.zeros((max(1, n.value), 2), np.uint64)
+        st = np.zeros(max(1, n.value), np.uint32)
+        pg = np.zeros(max(1, len(self.coded_pieces(mid))), np.uint32)
+        _check(lib().fsw_debug_dmaz_plan(self.h, mid, group_bytes, streams, lohi.ctypes.data, st.ctypes.data,
+                                         n.value, ctypes.byref(n), pg.ctypes.data))
+        return lohi[:n.value], st[:n.value], pg
 
     def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:
         buf = np.empty(nbytes, dtype=np.uint8)

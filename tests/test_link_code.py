@@ -175,3 +175,35 @@ def test_ratio_full_size_bert():
             p = pcs[i]
             dec, _ = decode_piece(coded[p["coff"]:p["coff"] + p["cbytes"]], p["hdr"], int(p["bytes"]))
             np.testing.assert_array_equal(dec, store[p["off"]:p["off"] + p["bytes"]])
+
+
+@pytest.mark.parametrize("name", ["bert-tiny", "resnet-tiny", "mlp-small"])
+@pytest.mark.parametrize("grp,streams", [(4096, 1), (64 << 10, 2), (1 << 20, 1), (64 << 20, 3)])
+def test_dmaz_plan_tiles_coded_store(name, grp, streams):
+    """DMAZ copy groups tile the coded store in order (no gap, no overlap), are dealt round-robin to
+    the streams, and every piece's recorded group is the group holding its coded bytes."""
+    spec = synth.build_model(name)
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
+        lohi, st, pg = rt.dmaz_plan(mid, grp, streams)
+        pcs = rt.coded_pieces(mid)
+        info = rt.model_info(mid)
+        assert lohi[0, 0] == 0 and lohi[-1, 1] == info["coded_bytes"]
+        np.testing.assert_array_equal(lohi[1:, 0], lohi[:-1, 1])
+        assert (lohi[:, 1] > lohi[:, 0]).all()
+        np.testing.assert_array_equal(st, np.arange(len(st)) % streams)
+        for p, g in zip(pcs, pg):
+            gi = (int(g) & 0xFFFFFF) * streams + (int(g) >> 24)
+            assert int(g) >> 24 == gi % streams
+            assert lohi[gi, 0] <= p["coff"] and p["coff"] + p["cbytes"] <= lohi[gi, 1], (p, gi, lohi[gi])
+        # groups never exceed the cap by more than one piece
+        assert ((lohi[:, 1] - lohi[:, 0]) <= grp + 16384 + 128).all()
+
+
+def test_dmaz_plan_needs_link_code():
+    spec = synth.build_model("mlp-small")
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, spec.build_weights())
+        with pytest.raises(F.FswError) as e:
+            rt.dmaz_plan(mid, 1 << 20)
+        assert e.value.status == F.ESTATE
