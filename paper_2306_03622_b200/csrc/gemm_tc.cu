@@ -153,16 +153,24 @@ struct Cfg {
     static constexpr int kSub = BN <= 64 ? 4 : 2;            // 64-wide k sub-tiles per stage
     static constexpr uint32_t kA = kBM * kBK * 2;            // one A sub-tile: 16 KiB
     static constexpr uint32_t kB = BN * kBK * 2;             // one W sub-tile: BN x 128 B
-    static constexpr uint32_t kStage = kSub * (kA + kB);
-    static constexpr int kFit = (200 * 1024) / kStage;
-    static constexpr int kMaxStages = kFit > 8 ? 8 : kFit;
     static constexpr int kLdc = BN + 4;                       // epilogue tile row stride (floats)
     static constexpr uint32_t kCtile = kBM * kLdc * 4;
-    __host__ __device__ static uint32_t ring_bytes(int stages) {
-        uint32_t r = stages * kStage;
+    // runtime stage geometry: the A sub-tile occupies a_sub bytes of shared memory (16 KiB, or 8 KiB for
+    // 64-row activation tiles, whose 16-KiB UMMA read then runs into the following sub-tile: rows whose
+    // accumulators are never read), so 64-row tiles fit twice the k-tiles in flight
+    __host__ __device__ static uint32_t a_sub(uint32_t m_rows, int conv) { return !conv && m_rows <= 64 ? kA / 2 : kA; }
+    __host__ __device__ static uint32_t stage_bytes(uint32_t asub) { return kSub * (asub + kB); }
+    __host__ __device__ static uint32_t ring_bytes(int stages, uint32_t asub = kA) {
+        uint32_t r = stages * stage_bytes(asub);
         return r < kCtile ? (kCtile + 1023) / 1024 * 1024 : r;
     }
-    __host__ __device__ static uint32_t smem_bytes(int stages) { return ring_bytes(stages) + 1024 /*barriers*/ + 1024 /*align*/; }
+    __host__ __device__ static uint32_t smem_bytes(int stages, uint32_t asub = kA) {
+        return ring_bytes(stages, asub) + 1024 /*barriers*/ + 1024 /*align*/;
+    }
+    __host__ static int max_stages(uint32_t asub) {
+        const int fit = (int)((200 * 1024) / stage_bytes(asub));
+        return fit > 8 ? 8 : fit;
+    }
 };
 
 }  // namespace
@@ -176,8 +184,9 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    // stage s: A sub-tiles at smem + s*kStage + j*kA, W sub-tiles after the A sub-tiles
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::ring_bytes(stages));
+    // stage s: A sub-tiles at smem + s*sstride + j*asub, W sub-tiles after the A sub-tiles
+    const uint32_t asub = C::a_sub(a.m_rows, a.conv), sstride = C::stage_bytes(asub);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::ring_bytes(stages, asub));
     uint64_t* empty = full + stages;
     uint64_t* done = empty + stages;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
@@ -190,7 +199,10 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     const uint32_t kt_begin = blockIdx.z * a.kt_per;
     const uint32_t nkt = min(a.K / kBK, kt_begin + a.kt_per) - kt_begin;  // >= 1 (host plan)
     const uint32_t nst = (nkt + C::kSub - 1) / C::kSub;                   // pipeline steps
-    const uint32_t a_bytes = a.conv ? a.Hb * a.Q * (kBK * 2) : C::kA;    // TMA box bytes
+    // TMA box bytes of one A sub-tile: Hb x Q conv rows, or m_rows activation rows (m_rows = 64 halves the
+    // A bytes a CTA streams: the upper 64 rows of the 128-row UMMA tile then hold stale data whose
+    // accumulator rows the epilogue never reads)
+    const uint32_t a_bytes = a.conv ? a.Hb * a.Q * (kBK * 2) : a.m_rows * (kBK * 2);
     // A multicast over a cluster of mc CTAs along N: CTA r loads rows [r·128/mc, (r+1)·128/mc) of
     // every A sub-tile and broadcasts them to the whole cluster; a stage is free again only when
     // all mc CTAs' MMAs have read it (empty barriers count mc multicast commits).
@@ -221,56 +233,58 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     const uint32_t tmem = *tmem_slot;
     STAMP(1);
 
-    // Role dispatch is warp-uniform: lane 0 of warp 0 (producer) / warp 1 (MMA issuer) works,
-    // the other lanes of those warps park at __syncwarp instead of spinning beside it.
+    // Role dispatch is warp-uniform: warp 0 produces (lane 0 arms each stage's barrier, then lane j issues
+    // the copies of the stage's sub-tile j: one thread issuing every TMA / bulk copy back to back was the
+    // producer's critical path), lane 0 of warp 1 issues the MMAs; the other lanes of warp 1 park.
     if (warp == 0) {
-        if (lane == 0) {
-            wait_ready_thread(w);
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            const uint8_t* wt = weight_ptr(dd, a.w_off);
-            const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
-            auto load_w = [&](uint32_t st) {
-                const int s = st % stages;
-                const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
-                uint8_t* sb = smem + s * C::kStage + C::kSub * C::kA;
-                mbar_expect_tx(&full[s], nsub * (a_bytes + C::kB));
-                for (uint32_t j = 0; j < nsub; ++j)
-                    bulk_load(sb + j * C::kB, wt + (kt_begin + kt0 + j) * ktile_stride + (uint64_t)(n0 / 8) * 1024, C::kB,
-                              &full[s]);
-            };
-            auto load_a = [&](uint32_t st) {
-                const int s = st % stages;
-                const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
-                uint8_t* sa = smem + s * C::kStage;
-                for (uint32_t j = 0; j < nsub; ++j) {
-                    const uint32_t kk = (kt_begin + kt0 + j) * kBK;
-                    if (a.conv) {
-                        const uint32_t tap = kk / a.Cin, c0 = kk - tap * a.Cin, r = tap / a.S, sx = tap - r * a.S;
-                        tma_load_4d(sa + j * C::kA, &tmA, (int)c0, (int)sx - (int)a.pad,
-                                    (int)(blockIdx.x * a.Hb * a.stride + r) - (int)a.pad, 0, &full[s]);
-                    } else if (mc > 1) {
-                        const uint32_t rows = kBM / mc;
-                        tma_load_2d_mc(sa + j * C::kA + crank * rows * (kBK * 2), &tmA, (int)kk, (int)(m0 + crank * rows),
-                                       &full[s], cmask);
-                    } else {
-                        tma_load_2d(sa + j * C::kA, &tmA, (int)kk, (int)m0, &full[s]);
-                    }
+        if (lane == 0) wait_ready_thread(w);
+        __syncwarp();  // the weights lane 0 acquired are visible to the warp
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const uint8_t* wt = weight_ptr(dd, a.w_off);
+        const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
+        auto load_w = [&](uint32_t st) {
+            const int s = st % stages;
+            const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
+            uint8_t* sb = smem + s * sstride + C::kSub * asub;
+            if (lane == 0) mbar_expect_tx(&full[s], nsub * (a_bytes + C::kB));
+            __syncwarp();
+            if (lane < nsub)
+                bulk_load(sb + lane * C::kB, wt + (kt_begin + kt0 + lane) * ktile_stride + (uint64_t)(n0 / 8) * 1024, C::kB,
+                          &full[s]);
+        };
+        auto load_a = [&](uint32_t st) {
+            const int s = st % stages;
+            const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
+            uint8_t* sa = smem + s * sstride;
+            if (lane < nsub) {
+                const uint32_t j = lane, kk = (kt_begin + kt0 + j) * kBK;
+                if (a.conv) {
+                    const uint32_t tap = kk / a.Cin, c0 = kk - tap * a.Cin, r = tap / a.S, sx = tap - r * a.S;
+                    tma_load_4d(sa + j * asub, &tmA, (int)c0, (int)sx - (int)a.pad,
+                                (int)(blockIdx.x * a.Hb * a.stride + r) - (int)a.pad, 0, &full[s]);
+                } else if (mc > 1) {
+                    const uint32_t rows = kBM / mc;
+                    tma_load_2d_mc(sa + j * asub + crank * rows * (kBK * 2), &tmA, (int)kk, (int)(m0 + crank * rows),
+                                   &full[s], cmask);
+                } else {
+                    tma_load_2d(sa + j * asub, &tmA, (int)kk, (int)m0, &full[s]);
                 }
-            };
-            // weights of the first stages stream while the previous kernel is still running
-            const uint32_t pre = min((uint32_t)stages, nst);
-            for (uint32_t st = 0; st < pre; ++st) load_w(st);
-            pdl_wait();
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            for (uint32_t st = 0; st < pre; ++st) load_a(st);
-            for (uint32_t st = pre; st < nst; ++st) {
-                const int s = st % stages;
-                mbar_wait(&empty[s], ((st / stages) - 1) & 1);
-                load_w(st);
-                load_a(st);
             }
-            STAMP(2);
+        };
+        // weights of the first stages stream while the previous kernel is still running
+        const uint32_t pre = min((uint32_t)stages, nst);
+        for (uint32_t st = 0; st < pre; ++st) load_w(st);
+        pdl_wait();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (uint32_t st = 0; st < pre; ++st) load_a(st);
+        for (uint32_t st = pre; st < nst; ++st) {
+            const int s = st % stages;
+            if (lane == 0) mbar_wait(&empty[s], ((st / stages) - 1) & 1);
+            __syncwarp();
+            load_w(st);
+            load_a(st);
         }
+        STAMP(2);
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {
@@ -280,14 +294,14 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
                 mbar_wait(&full[s], (st / stages) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t kt0 = st * C::kSub, nsub = min((uint32_t)C::kSub, nkt - kt0);
-                const uint8_t* sa = smem + s * C::kStage;
-                const uint8_t* sb = sa + C::kSub * C::kA;
+                const uint8_t* sa = smem + s * sstride;
+                const uint8_t* sb = sa + C::kSub * asub;
                 const uint64_t ad0 = umma_desc_sw128(sa), bd0 = umma_desc_sw128(sb);
                 for (uint32_t j = 0; j < nsub; ++j) {
 #pragma unroll
                     for (uint32_t kk = 0; kk < kBK / 16; ++kk) {
                         // advance the start address: 16-B units; sub-tile j, 32 B per K=16 step
-                        const uint64_t ad = ad0 + ((j * C::kA + kk * 32) >> 4);
+                        const uint64_t ad = ad0 + ((j * asub + kk * 32) >> 4);
                         const uint64_t bd = bd0 + ((j * C::kB + kk * 32) >> 4);
                         umma_f16(tmem, ad, bd, idesc, (st | j | kk) != 0);
                     }
@@ -318,6 +332,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
 #pragma unroll
     // warp w reads TMEM lanes 32·(w mod 4) (its lane quarter) and every (w / 4)-th 32-column block
     for (int c0 = 32 * (int)(warp >> 2); c0 < BN; c0 += 32 * (kGemmThreads / 128)) {
+        if ((warp & 3u) * 32u >= a.m_rows) break;  // TMEM lanes past the tile's rows (m_rows = 64)
         uint32_t r[32];
         tmem_ld32(tmem + (((warp & 3u) * 32u) << 16) + (uint32_t)c0, r);
         float4* dst = reinterpret_cast<float4*>(ct + ((warp & 3u) * 32 + lane) * C::kLdc + c0);
@@ -504,17 +519,19 @@ template <int BN>
 static void launch_bn(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {
     using C = Cfg<BN>;
     const int nst = (int)((a.kt_per + C::kSub - 1) / C::kSub);
-    const int stages = nst < C::kMaxStages ? nst : C::kMaxStages;
+    const uint32_t asub = C::a_sub(a.m_rows, a.conv);
+    const int ms = C::max_stages(asub);
+    const int stages = nst < ms ? nst : ms;
     dim3 grid((a.M + a.m_rows - 1) / a.m_rows, a.n_pad / BN, a.splits);
-    launch_pdl_cluster(PDL_GEMM, k_gemm<BN>, grid, dim3(kGemmThreads), C::smem_bytes(stages), s,
+    launch_pdl_cluster(PDL_GEMM, k_gemm<BN>, grid, dim3(kGemmThreads), C::smem_bytes(stages, asub), s,
                        dim3(1, a.mc > 1 ? a.mc : 1, a.cz > 1 ? a.cz : 1), *tmA, d, w, a, stages);
 }
 
 void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading)
-    cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<16>::smem_bytes(Cfg<16>::kMaxStages));
-    cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<32>::smem_bytes(Cfg<32>::kMaxStages));
-    cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<64>::smem_bytes(Cfg<64>::kMaxStages));
-    cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg<128>::smem_bytes(Cfg<128>::kMaxStages));
+    cudaFuncSetAttribute(k_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 template <int BN>
@@ -523,7 +540,7 @@ static int max_clusters_bn(int cz) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(1, 1, cz);
     cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = C::smem_bytes(C::kMaxStages);
+    cfg.dynamicSmemBytes = C::smem_bytes(C::max_stages(C::kA));
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 1;

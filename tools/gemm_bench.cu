@@ -39,26 +39,29 @@ int main(int argc, char** argv) {
     for (auto& sh : shapes) {
         if (only && strcmp(only, sh.name)) continue;
         const uint32_t n_pad = (sh.N + 15) / 16 * 16, kt = sh.K / 64;
-        double best = 1e9; int bb = 0; uint32_t bs = 0, bm = 1, bz = 0;
+        double best = 1e9; int bb = 0; uint32_t bs = 0, bm = 1, bz = 0, bmr = 128;
         for (int bn : {16, 32, 64, 128}) {
             if (n_pad % bn || (only_bn && bn != only_bn)) continue;
             for (uint32_t mc : {1u, 2u, 4u, 8u}) {
             if ((n_pad / bn) % mc || (only_mc && mc != only_mc)) continue;
             for (uint32_t S : {1u, 2u, 3u, 4u, 6u, 8u, 12u, 16u, 24u, 36u}) {
             for (uint32_t cl : {0u, 1u}) {  // split-K reduction: global partials (0) / cluster DSMEM (1)
+            for (uint32_t mr : {128u, 64u}) {  // activation rows per M tile
                 if (S > kt || (only_s && S != only_s)) continue;
                 if (cl && (S < 2 || S > 8 || mc > 1)) continue;
                 if (getenv("CZ_ONLY") && !cl && S > 1) continue;
                 if (getenv("NO_MC") && mc > 1) continue;
                 const uint32_t kt_per = (kt + S - 1) / S;
                 if ((kt + kt_per - 1) / kt_per != S) continue;
-                const uint32_t ctas = ((sh.M + 127) / 128) * (n_pad / bn) * S;
+                if (mr == 64 && mc > 1) continue;
+                if (getenv("MR") && (uint32_t)atoi(getenv("MR")) != mr) continue;
+                const uint32_t ctas = ((sh.M + mr - 1) / mr) * (n_pad / bn) * S;
                 if (ctas > 600) continue;
                 CUtensorMap tm;
-                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K, 128 / mc)) { printf("tmap fail\n"); return 1; }
+                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K, mr == 64 ? 64 : 128 / mc)) { printf("tmap fail\n"); return 1; }
                 GemmArgs a{}; a.M = sh.M; a.N = sh.N; a.K = sh.K; a.n_pad = n_pad; a.w_off = 0; a.b_off = 0;
                 a.has_bias = 1; a.act = 0; a.res = nullptr; a.out = O; a.out_bf16 = 1; a.ld_out = sh.N; a.bn = bn;
-                a.m_rows = 128; a.splits = S; a.kt_per = kt_per; a.part = part; a.ctr = ctr; a.mc = mc; a.cz = cl ? S : 0;
+                a.m_rows = mr; a.splits = S; a.kt_per = kt_per; a.part = part; a.ctr = ctr; a.mc = mc; a.cz = cl ? S : 0;
                 Wait w{}; w.ctl = ctl;
                 for (int i = 0; i < 3; ++i) launch_gemm(s, dd, w, &tm, a);
                 cudaEventRecord(e0, s);
@@ -69,9 +72,9 @@ int main(int argc, char** argv) {
                 float ms; cudaEventElapsedTime(&ms, e0, e1);
                 const double us = ms * 1000 / reps;
                 const double wbytes = 2.0 * n_pad * sh.K;
-                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u%s mc=%u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
-                       sh.K, sh.N, bn, S, cl ? "c" : " ", mc, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
-                if (us < best) { best = us; bb = bn; bs = S; bm = mc; bz = cl; }
+                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u%s mc=%u mr=%3u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
+                       sh.K, sh.N, bn, S, cl ? "c" : " ", mc, mr, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
+                if (us < best) { best = us; bb = bn; bs = S; bm = mc; bz = cl; bmr = mr; }
 #ifdef PHASES
                 // one isolated launch: per-CTA %globaltimer stamps -> mean phase durations
                 cudaDeviceSynchronize();
@@ -98,8 +101,9 @@ int main(int argc, char** argv) {
             }
             }
             }
+            }
         }
-        printf("  BEST %-18s BN=%d S=%u%s mc=%u %.2f us\n", sh.name, bb, bs, bz ? "c" : "", bm, best);
+        printf("  BEST %-18s BN=%d S=%u%s mc=%u mr=%u %.2f us\n", sh.name, bb, bs, bz ? "c" : "", bm, bmr, best);
     }
     cudaError_t e = cudaGetLastError();
     printf("last error: %s\n", cudaGetErrorString(e));
