@@ -444,6 +444,16 @@ def resnet50(seed=3) -> ModelSpec:
     return _resnet([3, 4, 6, 3], [64, 128, 256, 512], 224, seed=seed, name="resnet50")
 
 
+def resnet101(seed=5) -> ModelSpec:
+    """ResNet-101 v1.5 (tab:eval_remote_swap)."""
+    return _resnet([3, 4, 23, 3], [64, 128, 256, 512], 224, seed=seed, name="resnet101")
+
+
+def resnet152(seed=6) -> ModelSpec:
+    """ResNet-152 v1.5."""
+    return _resnet([3, 8, 36, 3], [64, 128, 256, 512], 224, seed=seed, name="resnet152")
+
+
 def resnet_tiny(seed=13, img=32) -> ModelSpec:
     """A small ResNet with the same structure (all op kinds, projections, strides) for fast parity."""
     return _resnet([1, 2, 1, 1], [16, 32, 64, 64], img, stem=16, n_classes=40, seed=seed, name=f"resnet_tiny{img}")
@@ -463,6 +473,10 @@ CONFIGS: Dict[str, Callable[[], ModelSpec]] = {
     "bert-base": lambda: bert(),
     "resnet50": lambda: resnet50(),
     "gpt2-xl": lambda: gpt2(),
+    # the paper's other swap-evaluation models (tab:eval_remote_swap)
+    "resnet101": lambda: resnet101(),
+    "resnet152": lambda: resnet152(),
+    "bert-large": lambda: bert(n_layers=24, hidden=1024, heads=16, inter=4096, seed=7, name="bert-large"),
     # small members of the same families (parity tests at oracle-friendly sizes)
     "mlp-small": lambda: mlp(width=256, n_layers=3, seed=11),
     "bert-tiny": lambda: bert(n_layers=2, hidden=128, heads=2, inter=256, vocab=1000, max_pos=64, seq=64,

@@ -20,7 +20,8 @@ def rel_err(got, ref):
 
 
 @pytest.mark.parametrize("name", ["mlp-small", "mlp", "bert-tiny", "gpt2-tiny", "resnet-tiny",
-                                  "bert-base", "resnet50", "gpt2-2L"])
+                                  "bert-base", "resnet50", "gpt2-2L",
+                                  "resnet101", "resnet152", "bert-large"])  # + the paper's other models
 def test_cold_invoke_matches_oracle(rt, registered, name):
     spec, w, x, mid = registered(name)
     rt.evict(mid)
