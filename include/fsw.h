@@ -184,7 +184,10 @@ typedef struct {
     uint32_t output_dtype;
     uint64_t coded_bytes;      /* bytes of the exponent-coded store (FSW_REG_LINK_CODE), else 0 */
     int32_t numa_node;         /* NUMA node the host store's pages prefer (that of pool GPU 0's PCIe
-                                  root, from sysfs; bound before first touch), −1 if unknown / none */
+                                  root, from sysfs; bound before first touch), −1 if unknown / none,
+                                  −2 when the pool spans several nodes: 2-MiB chunks are then bound
+                                  round-robin across the pool's nodes and striped swaps deal each
+                                  chunk's data to a source on its node (fsw_policy_stripe_deal)  */
 } fsw_model_info;
 fsw_status fsw_model_info_get(fsw_ctx* ctx, uint32_t model_id, fsw_model_info* out);
 
@@ -330,6 +333,12 @@ fsw_status fsw_policy_schedule(uint32_t n, const uint8_t* available, const uint8
  * in-use models are skipped.  order has n entries; n_order = how many were emitted.            */
 fsw_status fsw_policy_eviction_order(uint32_t n, const uint8_t* heavy, const uint32_t* copies, const uint64_t* last_use,
                                      const uint8_t* in_use, uint32_t* order, uint32_t* n_order);
+/* Striped swap: the source of each of n_units units (pieces, or runs of coded
+ * pieces, in execution order) — a unit goes to the sources whose NUMA node equals unit_node[u],
+ * round-robin among them; a unit whose node has no source (or is −1) goes round-robin over all n_src
+ * sources.  The runtime deals its striped swaps with this function.  EINVAL on NULL / n_src == 0. */
+fsw_status fsw_policy_stripe_deal(uint32_t n_units, const int32_t* unit_node, uint32_t n_src, const int32_t* src_node,
+                                  uint32_t* out);
 /* Heavy / light class of a model for placement and eviction: 1 heavy, 0 light, −1 auto (heavy
  * while unmeasured; then heavy iff mean cold / mean resident device latency > 1.25, SPEC S:77's
  * threshold on P:839's "pipelining significantly slows down the inference").                  */

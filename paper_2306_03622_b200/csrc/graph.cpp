@@ -216,19 +216,31 @@ extern "C" fsw_status fsw_debug_dmaz_plan(fsw_ctx* c, uint32_t id, uint64_t grou
 
 // Striped link-coded swap: runs of 16 consecutive coded pieces (256 KiB of store) dealt round-robin to
 // n sources; source j's table lives on its device.
-fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, int dev, uint64_t from, ZPieceSet** out) {
-    const auto key = std::make_tuple(n, j, dev, from);
+static uint64_t nodes_key(const std::vector<int>& src_node) {  // FNV-1a of the sources' nodes
+    uint64_t h = 1469598103934665603ull;
+    for (int v : src_node) h = (h ^ (uint64_t)(uint32_t)(v + 7)) * 1099511628211ull;
+    return h ^ src_node.size();
+}
+
+fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_node, uint32_t j, int dev, uint64_t from,
+                              ZPieceSet** out) {
+    const auto key = std::make_tuple(nodes_key(src_node), j, dev, from);
     auto it = p.zstripe.find(key);
     if (it != p.zstripe.end()) {
         *out = &it->second;
         return FSW_OK;
     }
+    // units = runs of 16 coded pieces (256 KiB of store); each goes to a source on the NUMA node of its
+    // first coded byte (stripe_deal: round-robin among them; over all sources on a single-node host)
+    std::vector<const ZPiece*> sel;
+    for (const ZPiece& pc : m.zpieces)
+        if (pc.off >= from) sel.push_back(&pc);
+    std::vector<int> unit_node;
+    for (size_t q = 0; q < sel.size(); q += 16) unit_node.push_back(chunk_node(m.zstore_node, sel[q]->coff));
+    const std::vector<uint32_t> owner = stripe_deal(unit_node, src_node);
     ZPieceSet zs;
-    uint64_t q = 0;
-    for (const ZPiece& pc : m.zpieces) {
-        if (pc.off < from) continue;
-        if ((q++ / 16) % n == j) zs.host.push_back(pc);
-    }
+    for (size_t q = 0; q < sel.size(); ++q)
+        if (owner[q / 16] == j) zs.host.push_back(*sel[q]);
     CU(cudaSetDevice(dev));
     if (!zs.host.empty()) {
         CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
@@ -241,19 +253,26 @@ fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, int dev
 // Striped swap: the execution-order piece list of the SM engine dealt round-robin to n sources
 // (piece q goes to source q mod n), so every source streams a share of every layer and all of them
 // advance through the model together; source j's table is allocated on source j's device.
-fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, uint64_t from,
-                                    PieceSet** out) {
-    const auto key = std::make_tuple(chunk, n, j, dev, from);
+fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vector<int>& src_node, uint32_t j, int dev,
+                             uint64_t from, PieceSet** out) {
+    const auto key = std::make_tuple(chunk, nodes_key(src_node), j, dev, from);
     auto it = p.stripe.find(key);
     if (it != p.stripe.end()) {
         *out = &it->second;
         return FSW_OK;
     }
-    PieceSet ps;
-    uint64_t q = 0;
+    // units = pieces; each goes to a source on the NUMA node of its first byte (stripe_deal)
+    std::vector<Piece> all;
+    std::vector<int> unit_node;
     for (uint32_t li = 0; li < m.layers.size(); ++li)
-        for (uint64_t o = 0; m.region_off[li] >= from && o < m.region_bytes[li]; o += chunk, ++q)
-            if (q % n == j) ps.host.push_back({m.region_off[li] + o, (uint32_t)std::min<uint64_t>(chunk, m.region_bytes[li] - o), li});
+        for (uint64_t o = 0; m.region_off[li] >= from && o < m.region_bytes[li]; o += chunk) {
+            all.push_back({m.region_off[li] + o, (uint32_t)std::min<uint64_t>(chunk, m.region_bytes[li] - o), li});
+            unit_node.push_back(chunk_node(m.store_node, m.region_off[li] + o));
+        }
+    const std::vector<uint32_t> owner = stripe_deal(unit_node, src_node);
+    PieceSet ps;
+    for (size_t q = 0; q < all.size(); ++q)
+        if (owner[q] == j) ps.host.push_back(all[q]);
     CU(cudaSetDevice(dev));
     if (!ps.host.empty()) {
         CU(cudaMalloc(&ps.dev, sizeof(Piece) * ps.host.size()));

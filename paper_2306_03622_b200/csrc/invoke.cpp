@@ -341,11 +341,13 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     const uint64_t schunk = std::max<uint64_t>(ic.chunk, 256ull << 10);
     std::vector<PieceSet*> sps(srcs.size(), nullptr);
     std::vector<ZPieceSet*> zps(srcs.size(), nullptr);
+    std::vector<int> src_node;
+    for (int sgi : srcs) src_node.push_back(c->gpu_node[sgi]);
     for (size_t j = 0; j < srcs.size(); ++j) {
         if (engine == FSW_ENGINE_SMZ)
-            st = get_zstripe_pieces(*m, p, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &zps[j]);
+            st = get_zstripe_pieces(*m, p, src_node, (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &zps[j]);
         else
-            st = get_stripe_pieces(*m, p, schunk, (uint32_t)srcs.size(), (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &sps[j]);
+            st = get_stripe_pieces(*m, p, schunk, src_node, (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &sps[j]);
         if (st != FSW_OK) return finish(st);
     }
     if (striped) {

@@ -38,4 +38,10 @@ Decision schedule(const std::vector<uint8_t>& available, const std::vector<uint8
 std::vector<uint32_t> eviction_order(const std::vector<uint8_t>& heavy, const std::vector<uint32_t>& copies,
                                      const std::vector<uint64_t>& last_use, const std::vector<uint8_t>& in_use);
 
+// Striped swap: deal units (pieces, or runs of coded pieces) in execution order to
+// the sources so each unit is read by a source on the NUMA node holding its host pages: unit u goes to
+// the sources whose node equals unit_node[u], round-robin among them (a counter per node); a unit whose
+// node has no source (or is -1) goes round-robin over all sources.  Returns the source of every unit.
+std::vector<uint32_t> stripe_deal(const std::vector<int>& unit_node, const std::vector<int>& src_node);
+
 }  // namespace fsw

@@ -123,10 +123,10 @@ struct Plan {  // one model on one GPU
     std::map<std::tuple<uint64_t, int, uint32_t, uint64_t>, PieceSet> pieces;  // (chunk, order, seed, from)
     std::map<std::tuple<uint64_t, uint32_t, uint64_t, uint64_t>, DmaPlan> dma;  // (group bytes, streams, from, split)
     // striped swap: source j of n gets every n-th piece; its table lives on the source's device
-    std::map<std::tuple<uint64_t, uint32_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, n, j, device, from)
+    std::map<std::tuple<uint64_t, uint64_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, sources' nodes, j, device, from)
     // link-coded engines: (order, seed, from, DMAZ group bytes or 0 for SMZ) and striped (n, j, device, from)
     std::map<std::tuple<int, uint32_t, uint64_t, uint64_t, uint32_t>, ZPieceSet> zp;  // + DMAZ copy streams
-    std::map<std::tuple<uint32_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;
+    std::map<std::tuple<uint64_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;  // (sources' nodes, j, device, from)
 };
 
 struct Model {
@@ -143,7 +143,9 @@ struct Model {
     uint8_t* store = nullptr;  // pinned, mapped host store (execution order)
     uint64_t store_bytes = 0, store_alloc = 0;
     bool store_wc = false;
-    int numa_node = -1;        // node the store's pages were bound to (mbind before first touch), or -1
+    int numa_node = -1;        // node the store's pages were bound to (mbind before first touch), -1 none,
+                               // -2 bound chunk-wise across the pool's nodes (store_node / zstore_node)
+    std::vector<int> store_node, zstore_node;  // node of each 2-MiB chunk of the store / coded store (empty: one node)
     // exponent-coded copy of the store (FSW_REG_LINK_CODE; kernels.h): pinned, mapped
     uint8_t* zstore = nullptr;
     uint64_t zbytes = 0, zalloc = 0;
@@ -223,6 +225,10 @@ struct fsw_ctx {
     uint64_t clock = 0;
     std::vector<std::vector<char>> peer;  // peer[i][j]: GPU i can store into GPU j's memory
     std::vector<int> neighbor;            // GPU sharing a PCIe switch (-1 none), fsw_config.pcie_neighbor
+    // NUMA node of each pool GPU's PCIe root (sysfs; -1 unknown) and the distinct nodes.  With more than
+    // one node the host stores are bound chunk-wise across them and striped swaps read node-locally.
+    std::vector<int> gpu_node, nodes;
+    bool fake_numa = false;               // FSW_FAKE_NUMA=k: pretend pool GPU i is on node i % k (no mbind)
 };
 
 
@@ -296,16 +302,20 @@ struct InvokeCfg {
 Model* find_model(fsw_ctx* c, uint32_t id);                                      // runtime.cpp
 void free_plan(Gpu& g, Plan& p);                                                 // runtime.cpp
 void free_store(Model& m, bool host_only);                                       // runtime.cpp
-fsw_status build_link_code(Model& m, bool host_only);                            // store.cpp
+fsw_status build_link_code(fsw_ctx* c, Model& m, bool host_only);               // store.cpp
+int gpu_numa_node(int dev);                                                      // store.cpp
+constexpr uint64_t kNumaChunk = 2ull << 20;  // NUMA binding unit of the host stores (one THP page)
+inline int chunk_node(const std::vector<int>& map, uint64_t off) { return map.empty() ? -1 : map[off / kNumaChunk]; }
 fsw_status build_plan(fsw_ctx* c, Model& m, int gi);                             // plan.cpp
 fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint32_t seed, uint64_t from,
                       PieceSet** out);                                           // graph.cpp
 const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams, uint64_t from);
 fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
                        uint32_t streams, ZPieceSet** out);
-fsw_status get_zstripe_pieces(Model& m, Plan& p, uint32_t n, uint32_t j, int dev, uint64_t from, ZPieceSet** out);
-fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, uint32_t n, uint32_t j, int dev, uint64_t from,
-                             PieceSet** out);
+fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_node, uint32_t j, int dev, uint64_t from,
+                              ZPieceSet** out);
+fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vector<int>& src_node, uint32_t j, int dev,
+                             uint64_t from, PieceSet** out);
 fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out);
 bool model_heavy(const Model& m);                                                // invoke.cpp
 void invalidate(fsw_ctx* c, Model& m, int gi, bool keep_prefix = false);         // invoke.cpp

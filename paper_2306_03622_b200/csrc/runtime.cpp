@@ -189,6 +189,15 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
         if (s != FSW_OK) return s;
     }
     c->neighbor.assign(n, -1);
+    {
+        const char* fk = getenv("FSW_FAKE_NUMA");
+        c->fake_numa = fk && atoi(fk) > 1;
+        for (uint32_t i = 0; i < n; ++i)
+            c->gpu_node.push_back(c->fake_numa ? (int)(i % (uint32_t)atoi(fk)) : gpu_numa_node(c->gpus[i].dev));
+        for (int v : c->gpu_node)
+            if (v >= 0 && std::find(c->nodes.begin(), c->nodes.end(), v) == c->nodes.end()) c->nodes.push_back(v);
+        std::sort(c->nodes.begin(), c->nodes.end());
+    }
     if (cfg && cfg->pcie_neighbor)
         for (uint32_t i = 0; i < n; ++i) c->neighbor[i] = cfg->pcie_neighbor[i] < (int32_t)n ? cfg->pcie_neighbor[i] : -1;
     c->cfg.pcie_neighbor = nullptr;

@@ -164,6 +164,32 @@ extern "C" fsw_status fsw_policy_schedule(uint32_t n, const uint8_t* available, 
     return d.gpu < 0 ? FSW_EBUSY : FSW_OK;
 }
 
+std::vector<uint32_t> fsw::stripe_deal(const std::vector<int>& unit_node, const std::vector<int>& src_node) {
+    const uint32_t n = (uint32_t)src_node.size();
+    std::map<int, std::vector<uint32_t>> by_node;
+    for (uint32_t j = 0; j < n; ++j)
+        if (src_node[j] >= 0) by_node[src_node[j]].push_back(j);
+    std::map<int, uint64_t> ctr;
+    uint64_t any = 0;
+    std::vector<uint32_t> out(unit_node.size(), 0);
+    for (size_t u = 0; u < unit_node.size(); ++u) {
+        auto it = unit_node[u] >= 0 ? by_node.find(unit_node[u]) : by_node.end();
+        if (it == by_node.end()) out[u] = n ? (uint32_t)(any++ % n) : 0;
+        else out[u] = it->second[ctr[unit_node[u]]++ % it->second.size()];
+    }
+    return out;
+}
+
+extern "C" fsw_status fsw_policy_stripe_deal(uint32_t n_units, const int32_t* unit_node, uint32_t n_src,
+                                             const int32_t* src_node, uint32_t* out) {
+    if ((n_units && (!unit_node || !out)) || n_src == 0 || !src_node)
+        return FSW_EINVAL;
+    const std::vector<uint32_t> r = fsw::stripe_deal(std::vector<int>(unit_node, unit_node + n_units),
+                                                     std::vector<int>(src_node, src_node + n_src));
+    std::copy(r.begin(), r.end(), out);
+    return FSW_OK;
+}
+
 extern "C" fsw_status fsw_policy_eviction_order(uint32_t n, const uint8_t* heavy, const uint32_t* copies,
                                                 const uint64_t* last_use, const uint8_t* in_use, uint32_t* order,
                                                 uint32_t* n_order) {

@@ -123,7 +123,7 @@ static fsw_status check_layer(const Model& m, uint32_t li) {
 
 // ---- NUMA placement of host stores ---------------------------------------------
 // The NUMA node of a CUDA device, from sysfs (-1: unknown, or a single-node host).
-static int gpu_numa_node(int dev) {
+int gpu_numa_node(int dev) {
     char bus[64] = {};
     if (cudaDeviceGetPCIBusId(bus, sizeof bus, dev) != cudaSuccess) return -1;
     for (char* q = bus; *q; ++q) *q = (char)tolower(*q);
@@ -218,7 +218,23 @@ static void parallel_for(size_t n, F f) {
 // Build the coded copy of m.store: pieces of <= kZPiece bytes per layer region in execution order,
 // headers first (parallel), then offsets, then the coded bytes (parallel) into a THP-backed mapping
 // that is pinned and mapped for zero-copy reads like the store itself.
-fsw_status build_link_code(Model& m, bool host_only) {
+// Bind [p, p + len) before first touch: to `node`, or — when the pool's GPUs span several NUMA nodes —
+// 2-MiB chunk i to nodes[i % n] (striped swaps then deal each chunk's data to a source on its node).
+// Returns the model's numa_node value and fills the chunk map.
+static int bind_store(fsw_ctx* c, uint8_t* p, uint64_t len, int node, std::vector<int>& map) {
+    map.clear();
+    if (c->nodes.size() > 1) {
+        for (uint64_t i = 0; i * kNumaChunk < len; ++i) {
+            const int nd = c->nodes[i % c->nodes.size()];
+            if (!c->fake_numa) bind_pages(p + i * kNumaChunk, std::min<uint64_t>(kNumaChunk, len - i * kNumaChunk), nd);
+            map.push_back(nd);
+        }
+        return -2;
+    }
+    return bind_pages(p, len, node);
+}
+
+fsw_status build_link_code(fsw_ctx* c, Model& m, bool host_only) {
     std::vector<ZPiece>& pcs = m.zpieces;
     pcs.clear();
     for (uint32_t li = 0; li < m.layers.size(); ++li)
@@ -253,7 +269,7 @@ fsw_status build_link_code(Model& m, bool host_only) {
     void* p = mmap(nullptr, m.zalloc, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p == MAP_FAILED) return fail(FSW_ENOMEM, "register: mmap of %llu coded bytes failed", (unsigned long long)m.zalloc);
     madvise(p, m.zalloc, MADV_HUGEPAGE);
-    if (m.numa_node >= 0) bind_pages(p, m.zalloc, m.numa_node);
+    if (!host_only) bind_store(c, static_cast<uint8_t*>(p), m.zalloc, m.numa_node, m.zstore_node);
     m.zstore = static_cast<uint8_t*>(p);
     parallel_for((m.zalloc + (2u << 20) - 1) / (2u << 20), [&](size_t i) {  // alignment gaps stay zero
         memset(m.zstore + i * (2u << 20), 0, std::min<uint64_t>(2u << 20, m.zalloc - i * (2u << 20)));
@@ -370,7 +386,8 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
         if (p == MAP_FAILED) return fail(FSW_ENOMEM, "register: mmap of %llu bytes failed", (unsigned long long)m->store_alloc);
         madvise(p, m->store_alloc, MADV_HUGEPAGE);
         // the host link that reads the store is pool GPU 0's (striped swaps add the others)
-        if (!host_only) m->numa_node = bind_pages(p, m->store_alloc, gpu_numa_node(c->gpus[0].dev));
+        if (!host_only)
+            m->numa_node = bind_store(c, static_cast<uint8_t*>(p), m->store_alloc, gpu_numa_node(c->gpus[0].dev), m->store_node);
         m->store = static_cast<uint8_t*>(p);
     }
     // pack (zero padding everywhere; first touch happens here)
@@ -405,7 +422,7 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
     }
     if (d->flags & FSW_REG_LINK_CODE) {
         if (!wc && !host_only) CU(cudaSetDevice(c->gpus[0].dev));
-        s = build_link_code(*m, host_only);
+        s = build_link_code(c, *m, host_only);
         if (s != FSW_OK) {
             free_store(*m, host_only);
             return s;

@@ -146,7 +146,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
-           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan"]
+           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal"]
 
 _lib = None
 
@@ -194,6 +194,7 @@ def lib():
         L.fsw_policy_alpha.argtypes = [dbl, dbl, dbl, dbl, dbl, ctypes.POINTER(dbl)]
         L.fsw_policy_schedule.argtypes = [u32, vp, vp, vp, vp, vp, ctypes.POINTER(Decision)]
         L.fsw_policy_eviction_order.argtypes = [u32, vp, vp, vp, vp, vp, ctypes.POINTER(u32)]
+        L.fsw_policy_stripe_deal.argtypes = [u32, vp, u32, vp, vp]
         L.fsw_model_set_heavy.argtypes = [vp, u32, i32]
         L.fsw_model_is_heavy.argtypes = [vp, u32, ctypes.POINTER(i32)]
         L.fsw_sched_create.argtypes = [vp, ctypes.POINTER(SchedConfig), ctypes.POINTER(vp)]
@@ -499,6 +500,15 @@ def policy_eviction_order(heavy, copies, last_use, in_use):
     _check(lib().fsw_policy_eviction_order(n, h.ctypes.data, c.ctypes.data, lu.ctypes.data, iu.ctypes.data,
                                            order.ctypes.data, ctypes.byref(k)))
     return list(order[:k.value])
+
+
+def policy_stripe_deal(unit_node, src_node):
+    """Striped swap: the source of every unit (node-local first, round-robin; fsw_policy_stripe_deal)."""
+    un = np.ascontiguousarray(unit_node, np.int32)
+    sn = np.ascontiguousarray(src_node, np.int32)
+    out = np.zeros(max(1, len(un)), np.uint32)
+    _check(lib().fsw_policy_stripe_deal(len(un), un.ctypes.data, len(sn), sn.ctypes.data, out.ctypes.data))
+    return out[:len(un)]
 
 
 class Scheduler:

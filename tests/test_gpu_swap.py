@@ -189,3 +189,25 @@ def test_peer_swap_from_resident_copy_two_pool_gpus_on_one_device():
         with pytest.raises(FswError) as e:
             rt2.invoke(mid, x, gpu=0, peer_src=1)          # not resident on GPU 1 any more
         assert e.value.status == F.ESTATE
+
+
+def test_striped_swap_numa_dealing_two_fake_nodes(monkeypatch):
+    """FSW_FAKE_NUMA=2: pool GPU i pretends to sit on NUMA node i % 2, so the host stores are mapped
+    chunk-wise across two nodes and striped swaps deal each chunk to a source on its node (no mbind on
+    this single-node box).  Bytes and outputs must not change, plain and link-coded."""
+    from paper_2306_03622_b200 import ENGINE_SMZ, Runtime
+    monkeypatch.setenv("FSW_FAKE_NUMA", "2")
+    spec = synth.build_model("bert-base")
+    w, x = spec.build_weights(), spec.make_input()
+    with Runtime(gpu_ids=[0, 0], pool_bytes=2 << 30, stripe_min_bytes=1) as rt2:
+        plain = rt2.register_spec(spec, w)
+        coded = rt2.register_spec(spec, w, link_code=True)
+        assert rt2.model_info(plain)["numa_node"] == -2
+        base = rt2.invoke(plain, x, gpu=0, stripe=[0]).output.copy()
+        for mid, eng in ((plain, 0), (coded, ENGINE_SMZ)):
+            for src in ([0, 1], [1, 0], [0, 1, 1]):
+                rt2.evict(mid)
+                r = rt2.invoke(mid, x, gpu=0, stripe=src, engine=eng)
+                assert r.stats["swap_kind"] == 3
+                np.testing.assert_array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
+                np.testing.assert_array_equal(r.output, base)

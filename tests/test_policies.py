@@ -180,3 +180,32 @@ def test_eviction_order_invariants():
         assert sorted(o) == sorted(np.flatnonzero(used == 0).tolist())
         prio = [(1 if heavy[i] and copies[i] == 1 else 0, last[i]) for i in o]
         assert prio == sorted(prio)
+
+
+def test_stripe_deal_node_local_round_robin():
+    """a unit is read by a source on its NUMA node, round-robin among them."""
+    from paper_2306_03622_b200.fsw import policy_stripe_deal
+    # sources 0, 1 on node 0; 2, 3 on node 1; units alternate nodes
+    out = policy_stripe_deal([0, 1, 0, 1, 0, 1, 0, 1], [0, 0, 1, 1])
+    assert list(out) == [0, 2, 1, 3, 0, 2, 1, 3]
+    # a node without sources, and unknown nodes, fall back to round-robin over every source
+    out = policy_stripe_deal([2, 2, -1, 0], [0, 0, 1])
+    assert list(out[:3]) == [0, 1, 2] and out[3] in (0, 1)
+    # single-node hosts: plain round-robin (the runtime's behaviour before NUMA dealing)
+    out = policy_stripe_deal([-1] * 7, [0, 0, 0])
+    assert list(out) == [0, 1, 2, 0, 1, 2, 0]
+
+
+def test_stripe_deal_balance_property():
+    """Every source of a node gets the same number of that node's units (± 1)."""
+    import numpy as np
+    from paper_2306_03622_b200.fsw import policy_stripe_deal
+    rng = np.random.default_rng(3)
+    units = rng.integers(0, 2, 1000)
+    src = [0, 1, 0, 1, 1]
+    out = policy_stripe_deal(units, src)
+    for node in (0, 1):
+        mine = [j for j, s in enumerate(src) if s == node]
+        counts = [int(np.sum(out[units == node] == j)) for j in mine]
+        assert max(counts) - min(counts) <= 1
+        assert set(np.unique(out[units == node])) <= set(mine)
