@@ -159,6 +159,21 @@ static Decision pick_gpu(fsw_ctx* c, Model& m) {
     return schedule(avail, hosts, c->neighbor, loading, link);
 }
 
+// A CUDA profiling / checking tool is attached: ncu's libcuda-injection or compute-sanitizer's
+// interceptor is mapped into the process (or FSW_PROFILER_SAFE=1 asks for the same behaviour).
+static bool profiler_attached() {
+    if (getenv("FSW_PROFILER_SAFE") && atoi(getenv("FSW_PROFILER_SAFE")) != 0) return true;
+    if (getenv("CUDA_INJECTION64_PATH")) return true;
+    FILE* f = fopen("/proc/self/maps", "r");
+    if (!f) return false;
+    char line[4096];
+    bool found = false;
+    while (!found && fgets(line, sizeof line, f))
+        found = strstr(line, "libcuda-injection") || strstr(line, "InterceptorInjectionTarget");
+    fclose(f);
+    return found;
+}
+
 extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_opts* opts, const void* input,
                                     uint64_t input_bytes, void* output, uint64_t output_cap, fsw_invoke_stats* stats) {
     const double t_entry = now_ms();
@@ -291,13 +306,17 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         if (st != FSW_OK) return finish(st);
     }
     Plan& p = *m->plans[gi];
-    const uint32_t flags = o.flags | c->cfg.flags;
+    // Profiler-safe mode: under ncu / compute-sanitizer (a CUDA injection library is attached) kernels
+    // run serialised, so nothing may wait on work the tool orders after it: every invoke runs no-overlap
+    // and link-coded models use SMZ (DMAZ's decode kernel waits on copy-engine groups).
+    static const bool profiled = profiler_attached();
+    const uint32_t flags = o.flags | c->cfg.flags | (profiled ? FSW_NO_OVERLAP : 0u);
     const bool baseline = (flags & FSW_DMA_BASELINE) != 0;
     int engine = (int)(o.engine ? o.engine : c->cfg.engine);
     if (baseline) engine = FSW_ENGINE_DMA;
     const bool big = m->store_bytes >= c->cfg.dma_min_bytes;
     if (engine == FSW_ENGINE_AUTO)
-        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
+        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes && !profiled ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
                            : (big ? FSW_ENGINE_DMA : FSW_ENGINE_SM);
     if (engine_coded(engine) && !m->zstore) return finish(fail(FSW_EINVAL, "invoke: model %u is not link-coded (FSW_REG_LINK_CODE)", id));
     // striped: sources store into the target with SM kernels (decoding ones for the coded engines)
