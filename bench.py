@@ -357,6 +357,11 @@ def run_fsw(args):
         ct, cores = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
         cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": cores, "kind": "oracle",
                "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)"}
+    dec = None
+    try:
+        dec = json.load(open(tpath)).get(args.model + "-dmaz-decode") if os.path.exists(tpath) else None
+    except Exception:
+        dec = None
     if engine == "dmaz":
         roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA of link-coded groups into HBM staging + k_swapz decode",
                 "achieved": round(wire_gbs, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
@@ -364,8 +369,11 @@ def run_fsw(args):
                 "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure); "
                              "achieved = coded bytes over the link / swap time, store_bytes_gbs = decoded bytes / swap time",
                 "frac_of_measured_dma": round(wire_gbs / dma, 4) if dma else None,
-                "traffic": None, "traffic_note": "copy-engine transfers are not kernels: ncu has no per-launch counter for "
-                "them; the decode kernel spans the whole swap (it waits for each group)"}
+                "traffic": dec["dram_bytes"] if dec else None,
+                "traffic_note": "DRAM read+write bytes of the decode kernel k_swapz per cold invoke (ncu --set full, "
+                "profiles/swap_traffic.json): it reads the staged coded bytes once and writes the store bytes (the "
+                "rest still in L2 at kernel end); the copy-engine transfer itself is not a kernel",
+                "decode_kernel_alone_ms": dec["duration_ms"] if dec else None}
     elif engine == "dma":
         roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA groups (cudaMemcpyAsync, no SM kernel)",
                 "achieved": round(achieved, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",

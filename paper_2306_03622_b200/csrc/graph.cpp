@@ -373,11 +373,18 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             // group and decodes from HBM into the extent
             static PFN_writeValue32 wv = get_write_value32();
             if (!wv) return fail(FSW_ECUDA, "cuStreamWriteValue32 entry point unavailable");
+            // no-overlap: the decode kernel follows the copies on the copy stream (it then waits on nothing,
+            // which also keeps the graph safe under tools that serialise kernels)
+            const bool serial = ic.no_overlap;
+            cudaStream_t sdec = serial ? sc : g.sz;
             cudaEventRecord(g.evd[0], sc);
-            cudaStreamWaitEvent(g.sz, g.evd[0], 0);
+            if (!serial) cudaStreamWaitEvent(g.sz, g.evd[0], 0);
             for (uint32_t j = 1; j < ic.zstreams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
-            launch_swapz(g.sz, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
-                         (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 1, g.progress);
+            auto decode = [&]() {
+                launch_swapz(sdec, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
+                             (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 1, g.progress);
+            };
+            if (!serial) decode();
             uint32_t cnt[kMaxWaitSrc] = {};
             for (const auto& gr : zs->groups) {
                 cudaStream_t sj = g.sd[gr.stream];
@@ -388,8 +395,12 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
                 cudaEventRecord(g.evd[j], g.sd[j]);
                 cudaStreamWaitEvent(sc, g.evd[j], 0);
             }
-            cudaEventRecord(g.evz, g.sz);
-            cudaStreamWaitEvent(sc, g.evz, 0);
+            if (serial) {
+                decode();
+            } else {
+                cudaEventRecord(g.evz, g.sz);
+                cudaStreamWaitEvent(sc, g.evz, 0);
+            }
         } else {
             // Copy-engine DMA from the pinned store (the paper's transfer) in
             // layer-aligned groups (its "group" pipelining unit), dealt round-robin

@@ -308,7 +308,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     Plan& p = *m->plans[gi];
     // Profiler-safe mode: under ncu / compute-sanitizer (a CUDA injection library is attached) kernels
     // run serialised, so nothing may wait on work the tool orders after it: every invoke runs no-overlap
-    // and link-coded models use SMZ (DMAZ's decode kernel waits on copy-engine groups).
+    // (DMAZ then decodes after its last copy group, on the copy stream).
     static const bool profiled = profiler_attached();
     const uint32_t flags = o.flags | c->cfg.flags | (profiled ? FSW_NO_OVERLAP : 0u);
     const bool baseline = (flags & FSW_DMA_BASELINE) != 0;
@@ -316,7 +316,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     if (baseline) engine = FSW_ENGINE_DMA;
     const bool big = m->store_bytes >= c->cfg.dma_min_bytes;
     if (engine == FSW_ENGINE_AUTO)
-        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes && !profiled ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
+        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
                            : (big ? FSW_ENGINE_DMA : FSW_ENGINE_SM);
     if (engine_coded(engine) && !m->zstore) return finish(fail(FSW_EINVAL, "invoke: model %u is not link-coded (FSW_REG_LINK_CODE)", id));
     // striped: sources store into the target with SM kernels (decoding ones for the coded engines)
