@@ -249,8 +249,8 @@ def run_fsw(args):
         cold_step()
     if world > 1:
         dist.barrier()
-    cores = gpu_local_cores(gpu)
-    with ClockSampler(gpu) as clk, PinnedThread(cores):  # sampler started first: it is not bound
+    numa_cores = gpu_local_cores(gpu)
+    with ClockSampler(gpu) as clk, PinnedThread(numa_cores):  # sampler started first: it is not bound
         t0 = time.perf_counter()
         stats = [cold_step() for _ in range(args.steps)]
         wall = time.perf_counter() - t0
@@ -264,7 +264,7 @@ def run_fsw(args):
     wire = stats[0]["wire_bytes"]
     # e2e: the public fsw_invoke (scheduler picks the GPU), host buffers, H2D/D2H inside
     e2e = []
-    with PinnedThread(cores):
+    with PinnedThread(numa_cores):
         for _ in range(max(3, args.steps // 2)):
             rt.evict(mid, -1)
             t1 = time.perf_counter()
@@ -354,8 +354,8 @@ def run_fsw(args):
     t_roof_coded = roofline_ms(info["algorithmic_bytes"] * ratio, flops, fill * ratio, PCIE_GEN5_X16_GBS, 1645.1)
     cpu = None
     if not args.no_cpu_baseline:
-        ct, cores = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
-        cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": cores, "kind": "oracle",
+        ct, omp_threads = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
+        cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": omp_threads, "kind": "oracle",
                "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)"}
     dec = None
     try:
@@ -409,7 +409,7 @@ def run_fsw(args):
                    "sm_copy_ctas": args.copy_ctas or 16, "dma_group_bytes": (args.dma_group_mb or 64) << 20,
                    "dma_streams": args.dma_streams or 1,
                    "l2": "inputs larger than L2: every step streams all weights from host memory",
-                   "timing_thread_cores": f"{len(cores)} cores of the GPU's NUMA node",
+                   "timing_thread_cores": f"{len(numa_cores)} cores of the GPU's NUMA node",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
         "p99_ms": round(percentile(dev, 99), 4), "mean_ms": round(statistics.mean(dev), 4),
         "min_ms": round(min(dev), 4),
