@@ -67,7 +67,8 @@ typedef struct {
     uint64_t pool_bytes_per_gpu;      /* weight pool per GPU, pre-allocated at init; 0 = 64 GiB
                                          (capped at 60% of free memory)                       */
     uint64_t workspace_bytes_per_gpu; /* activation workspace per GPU; 0 = 512 MiB            */
-    uint32_t copy_ctas;               /* CTAs of the SM swap kernel; 0 = 16                   */
+    uint32_t copy_ctas;               /* CTAs of the SM swap kernel; 0 = 16 (the link-coded engines'
+                                         decode kernels use at least 32)                        */
     uint32_t copy_threads;            /* threads per swap CTA (multiple of 32); 0 = 256       */
     uint64_t chunk_bytes;             /* swap piece size (the paper's "group size",
                                          PAPER.md:600-604) of the SM engine; multiple of 256;
@@ -79,10 +80,11 @@ typedef struct {
     uint32_t engine;                  /* FSW_ENGINE_*; 0 = AUTO                                */
     uint64_t dma_min_bytes;           /* AUTO picks DMA for models with at least this many store
                                          bytes, SM below; 0 = 32 MiB                           */
-    uint64_t dma_group_bytes;         /* DMA engine: target bytes per copy group (whole layers are
-                                         merged up to it, larger layers split, groups taper
+    uint64_t dma_group_bytes;         /* DMA / DMAZ engines: target bytes per copy group (whole layers
+                                         are merged up to it, larger layers split, groups taper
                                          towards the end of the store); 0 = 64 MiB             */
-    uint32_t dma_streams;             /* DMA engine: concurrent copy streams (1..4); 0 = 1      */
+    uint32_t dma_streams;             /* DMA / DMAZ engines: concurrent copy streams (1..4); 0 = 1
+                                         (measured: more streams contend for the one host link)  */
     const int32_t* pcie_neighbor;     /* n_gpus entries: the pool GPU sharing each GPU's PCIe
                                          switch, −1 = none (Algorithm 1's "neighbor"); NULL = none
                                          (HGX B200: one switch per GPU)                          */
@@ -91,7 +93,7 @@ typedef struct {
                                          wins on ResNet-50's 51 MB, DMAZ on BERT-base's 219 MB)  */
 } fsw_config;
 
-/* Swap engines.  Both move the host store into the extent in execution order and
+/* Swap engines.  All move the host store into the extent in execution order and
  * publish readiness in device memory that the layer kernels acquire:
  *   SM : persistent CTAs stream pieces with 128-bit loads from mapped host memory; one release-add
  *        of the piece's bytes on its layer's counter per piece (fine-grained, no per-copy setup);
