@@ -68,7 +68,7 @@ typedef struct {
                                          (capped at 60% of free memory)                       */
     uint64_t workspace_bytes_per_gpu; /* activation workspace per GPU; 0 = 512 MiB            */
     uint32_t copy_ctas;               /* CTAs of the SM swap kernel; 0 = 16 (the link-coded engines'
-                                         decode kernels use at least 32)                        */
+                                         decode kernels use at least 32 (SMZ) / 48 (DMAZ))      */
     uint32_t copy_threads;            /* threads per swap CTA (multiple of 32); 0 = 256       */
     uint64_t chunk_bytes;             /* swap piece size (the paper's "group size",
                                          PAPER.md:600-604) of the SM engine; multiple of 256;
@@ -298,11 +298,17 @@ fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint
  *   stream A, per block:  b = 0xff : the raw bytes (1024, or bytes − 1024 (nb − 1) for a partial last
  *                                    block);  b = 0xfe : nothing (512 zero words);
  *                         b = 0..4 : 512 bytes m_i = (w_i >> 8 & 0x80) | (w_i & 0x7f);
+ *                         b = 0x10..0x13 : the same 512 bytes m_i;
  *   stream B, per block with b = 0..4: b bit-planes of 64 bytes (bit i of plane p, byte i/8 bit i%8,
  *                         = bit p of code c_i); n exceptions of 4 bytes (position in bits 0-15, the
- *                         whole word in bits 16-31), zero-padded to a multiple of 16 bytes.
+ *                         whole word in bits 16-31), zero-padded to a multiple of 16 bytes;
+ *             per block with b = 0x10 + o (two-tier, o = 0..3; n = n_e | n_x << 10): 2 tier-1 planes
+ *                         of 64 bytes (2-bit t_i), 3 tier-2 planes of 4·ceil(n_e / 32) bytes (3-bit s_j of
+ *                         the j-th word with t_i = 3, bit j of plane q = bit q of s_j), n_x exceptions,
+ *                         zero-padded to a multiple of 16 bytes.
  * A coded block decodes as w_i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then each
- * exception's word replaces w_position.
+ * exception's word replaces w_position.  c_i = the b-bit code (b = 0..4), or (two-tier) o + t_i when
+ * t_i < 3, else s_j < o ? s_j : s_j + 3.
  * ENOTFOUND / ESTATE (model not link-coded) / EINVAL (cap too small; *n is still set).              */
 typedef struct { uint64_t off, coff; uint32_t bytes, cbytes, layer, pad; uint32_t hdr[16]; } fsw_coded_piece;
 fsw_status fsw_debug_read_coded(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);

@@ -331,7 +331,10 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     };
     InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
-                 o.copy_ctas ? o.copy_ctas : engine_coded(engine) ? std::max(c->cfg.copy_ctas, kDmazCtas) : c->cfg.copy_ctas,
+                 o.copy_ctas                     ? o.copy_ctas
+                 : engine == FSW_ENGINE_DMAZ     ? std::max(c->cfg.copy_ctas, kDmazCtas)
+                 : engine == FSW_ENGINE_SMZ      ? std::max(c->cfg.copy_ctas, kSmzCtas)
+                                                 : c->cfg.copy_ctas,
                  extents(gi), nullptr};
     ic.from = pcached ? m->split : 0;
     if (ic.chunk % 256 || ic.chunk == 0 || ic.chunk >= (1ull << 32)) return finish(fail(FSW_EINVAL, "invoke: bad chunk_bytes"));

@@ -89,11 +89,17 @@ void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
 //                                  zero-padded to a multiple of 16 bytes.
 // A coded block decodes (patched frame of reference over the exponents e_i = w_i >> 7 & 0xff, h = max
 // e_i) as w_i = (m_i & 0x80) << 8 | (h − c_i) << 7 | (m_i & 0x7f), then every exception overwrites its
-// word.  A word is an exception iff h − e_i >= 2^b (its code is then 0).  The encoder picks per
-// block the b (or raw) with the fewest bytes.
+// word.  A word is an exception iff h − e_i >= 2^b (its code is then 0).
+// Two-tier blocks (b = kZTier + o, o in 0..3; v4) code d_i = h − e_i closer to its entropy: bits 16-25
+// of the header are the escape count n_e, bits 26-31 the exception count n_x.  Stream B is two tier-1
+// bit-planes of 64 bytes (2-bit codes t_i: t_i < 3 means d_i = o + t_i, t_i = 3 means escaped), then
+// three tier-2 bit-planes of 4·ceil(n_e / 32) bytes each holding one 3-bit code s_j per escaped word
+// in word order (bit j of plane q = bit q of s_j; d = s_j < o ? s_j : s_j + 3, so escapes cover
+// d in [0, o) and [o + 3, 10]), then n_x exceptions as above (escaped words with d >= 11, s_j = 0),
+// zero-padded to a multiple of 16 bytes.  The encoder picks per block the kind with the fewest bytes.
 constexpr uint32_t kZPiece = 16384;
 constexpr uint32_t kZBlock = 1024;
-constexpr uint32_t kZRaw = 0xff, kZZero = 0xfe;
+constexpr uint32_t kZRaw = 0xff, kZZero = 0xfe, kZTier = 0x10;
 // stream-A and stream-B bytes of one block
 __host__ __device__ __forceinline__ uint32_t zblock_a(uint32_t hdr, uint32_t raw_bytes) {
     const uint32_t b = (hdr >> 8) & 0xffu;
@@ -101,7 +107,16 @@ __host__ __device__ __forceinline__ uint32_t zblock_a(uint32_t hdr, uint32_t raw
 }
 __host__ __device__ __forceinline__ uint32_t zblock_b(uint32_t hdr) {
     const uint32_t b = (hdr >> 8) & 0xffu, n = hdr >> 16;
+    if ((b & ~3u) == kZTier) return (128u + 12u * (((n & 0x3ffu) + 31u) / 32u) + 4u * (n >> 10) + 15u) & ~15u;
     return b <= 4 ? 64u * b + ((4u * n + 15u) & ~15u) : 0u;
+}
+// coded blocks (FOR or two-tier): tier-1 code planes, tier-2 plane bytes, exception count and offset
+__host__ __device__ __forceinline__ bool ztier(uint32_t hdr) { return (((hdr >> 8) & 0xffu) & ~3u) == kZTier; }
+__host__ __device__ __forceinline__ uint32_t zplanes(uint32_t hdr) { return ztier(hdr) ? 2u : (hdr >> 8) & 0xffu; }
+__host__ __device__ __forceinline__ uint32_t zt2_bytes(uint32_t hdr) { return 4u * ((((hdr >> 16) & 0x3ffu) + 31u) / 32u); }
+__host__ __device__ __forceinline__ uint32_t zexc_n(uint32_t hdr) { return ztier(hdr) ? hdr >> 26 : hdr >> 16; }
+__host__ __device__ __forceinline__ uint32_t zexc_off(uint32_t hdr) {
+    return ztier(hdr) ? 128u + 3u * zt2_bytes(hdr) : 64u * ((hdr >> 8) & 0xffu);
 }
 __host__ __device__ __forceinline__ uint32_t zblock_bytes(uint32_t hdr, uint32_t raw_bytes) {
     return zblock_a(hdr, raw_bytes) + zblock_b(hdr);

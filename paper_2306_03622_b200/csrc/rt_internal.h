@@ -276,10 +276,12 @@ inline bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_
 // Engines whose layer kernels wait on per-layer byte counters (released by a swap kernel).
 inline bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_coded(e); }
 
-// Decoding swap CTAs (DMAZ and SMZ) unless the invoke sets copy_ctas: measured, 16 CTAs make the DMAZ
-// decode the bottleneck (BERT-base 3.60 ms vs 2.94 with 32) and leave SMZ's TMA ring short of the link
-// (ResNet-50 0.783 vs 0.739 ms) (profiles/r01/linkcode/).
-constexpr uint32_t kDmazCtas = 32;
+// Decoding swap CTAs unless the invoke sets copy_ctas (profiles/r01/linkcode/).  SMZ: 16 CTAs leave
+// the TMA ring short of the link (ResNet-50 0.783 vs 0.739 ms), 32 reach it.  DMAZ (register decoder,
+// 256 threads): the two-tier codes of link format v4 decode at 117 GB/s of store bytes on 32 CTAs and
+// 168 GB/s on 48 (measured alone, tools/dmaz_probe.py); beside the layer kernels 32 CTAs fall behind
+// the copy engine (BERT-base 3.10 ms), 48 do not (2.82 ms, as 64 and 96).
+constexpr uint32_t kSmzCtas = 32, kDmazCtas = 48;
 
 struct InvokeCfg {
     bool cold, no_overlap;

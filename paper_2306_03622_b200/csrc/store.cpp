@@ -147,8 +147,9 @@ static int bind_pages(void* p, size_t len, int node) {
 
 // ---- exponent-coded link format (kernels.h) -----------------------------------
 // Header of a full block of 512 16-bit words: all zero -> kZZero; else h = the largest exponent and
-// the code width b in 0..4 with the fewest bytes (words with h − e >= 2^b become exceptions), or raw
-// when no width beats the 1024 raw bytes.
+// the kind with the fewest bytes: a code width b in 0..4 (words with h − e >= 2^b become exceptions),
+// a two-tier code with tier-1 offset o in 0..3 (at most 63 exceptions), or raw when nothing beats the
+// 1024 raw bytes.
 static uint32_t zheader(const uint16_t* w) {
     uint32_t emax = 0, any = 0;
     for (uint32_t i = 0; i < kZBlock / 2; ++i) {
@@ -161,21 +162,52 @@ static uint32_t zheader(const uint16_t* w) {
         const uint32_t d = emax - ((w[i] >> 7) & 0xffu);
         hist[d ? std::min<uint32_t>(8, 32 - __builtin_clz(d)) : 0]++;
     }
-    uint32_t best = kZRaw, best_bytes = kZBlock, best_n = 0, n = kZBlock / 2;
+    uint32_t best = kZRaw << 8, best_bytes = kZBlock, n = kZBlock / 2;
     for (uint32_t b = 0; b <= 4; ++b) {
         n -= hist[b];  // words with h − e >= 2^b
-        const uint32_t bytes = zblock_bytes(emax | (b << 8) | (n << 16), kZBlock);
-        if (bytes < best_bytes) {
-            best = b;
-            best_bytes = bytes;
-            best_n = n;
-        }
+        const uint32_t hd = emax | (b << 8) | (n << 16), bytes = zblock_bytes(hd, kZBlock);
+        if (bytes < best_bytes) best = hd, best_bytes = bytes;
     }
-    return best == kZRaw ? kZRaw << 8 : emax | (best << 8) | (best_n << 16);
+    // two-tier kinds: tier 1 holds d in [o, o + 3), tier 2 d in [0, o) and [o + 3, 10], exceptions d >= 11
+    uint32_t cnt[12] = {};  // cnt[d] for d <= 10, cnt[11] = words with d >= 11
+    for (uint32_t i = 0; i < kZBlock / 2; ++i) cnt[std::min<uint32_t>(11, emax - ((w[i] >> 7) & 0xffu))]++;
+    for (uint32_t o = 0; o < 4; ++o) {
+        const uint32_t nx = cnt[11], ne = kZBlock / 2 - cnt[o] - cnt[o + 1] - cnt[o + 2];
+        if (nx > 63) break;
+        const uint32_t hd = emax | ((kZTier + o) << 8) | (ne << 16) | (nx << 26), bytes = zblock_bytes(hd, kZBlock);
+        if (bytes < best_bytes) best = hd, best_bytes = bytes;
+    }
+    return best;
 }
 
 // Coded block: 512 stream-A bytes at outa, zblock_b(hdr) stream-B bytes at outb (both zeroed).
+static void zencode_tier(const uint16_t* w, uint32_t hdr, uint8_t* outa, uint8_t* outb) {
+    const uint32_t h = hdr & 0xffu, o = ((hdr >> 8) & 0xffu) - kZTier, ne = (hdr >> 16) & 0x3ffu;
+    const uint32_t pw = 4 * ((ne + 31) / 32);  // bytes per tier-2 plane
+    uint8_t* t2 = outb + 128;
+    uint8_t* exc = t2 + 3 * pw;
+    uint32_t j = 0, k = 0;
+    for (uint32_t i = 0; i < kZBlock / 2; ++i) {
+        const uint32_t d = h - ((w[i] >> 7) & 0xffu);
+        outa[i] = (uint8_t)(((w[i] >> 8) & 0x80u) | (w[i] & 0x7fu));
+        uint32_t t = 3;
+        if (d >= o && d < o + 3) t = d - o;
+        outb[(i >> 3)] |= (uint8_t)((t & 1u) << (i & 7));
+        outb[64 + (i >> 3)] |= (uint8_t)((t >> 1) << (i & 7));
+        if (t != 3) continue;
+        uint32_t sj = d < o ? d : d - 3;  // escaped word j = this word's rank among the escapes
+        if (d >= 11) {
+            sj = 0;
+            const uint32_t e = i | ((uint32_t)w[i] << 16);
+            memcpy(exc + 4 * k++, &e, 4);
+        }
+        for (uint32_t q = 0; q < 3; ++q) t2[q * pw + (j >> 3)] |= (uint8_t)(((sj >> q) & 1u) << (j & 7));
+        ++j;
+    }
+}
+
 static void zencode_block(const uint16_t* w, uint32_t hdr, uint8_t* outa, uint8_t* outb) {
+    if ((((hdr >> 8) & 0xffu) & ~3u) == kZTier) return zencode_tier(w, hdr, outa, outb);
     const uint32_t h = hdr & 0xffu, b = (hdr >> 8) & 0xffu;
     uint8_t code[kZBlock / 2];
     uint32_t k = 0;

@@ -85,9 +85,19 @@ __device__ __forceinline__ uint32_t zld32(const uint8_t* p) {
     return r;
 }
 
-// Lane l of a coded block: words 16l .. 16l+15 from its 16 stored bytes, its 16 bits of each code
-// plane (plane p in the low half of pl[p]) and the block's base exponent h.
-__device__ __forceinline__ void zdecode16(const uint4 sm, const uint32_t (&pl)[4], uint32_t h, uint4& o0, uint4& o1) {
+// Bit i of the low 16 bits of x -> bit 4i (one code bit per 4-bit lane of a 64-bit word).
+__device__ __forceinline__ uint64_t spread4(uint32_t x) {
+    uint64_t v = x & 0xffffu;
+    v = (v | (v << 24)) & 0x000000ff000000ffull;
+    v = (v | (v << 12)) & 0x000f000f000f000full;
+    v = (v | (v << 6)) & 0x0303030303030303ull;
+    v = (v | (v << 3)) & 0x1111111111111111ull;
+    return v;
+}
+
+// Lane l of a coded block: words 16l .. 16l+15 from its 16 stored bytes m_i, the offsets d_i = h − e_i
+// (4 bits each, word i in bits 4i..4i+3 of dp) and the block's base exponent h.
+__device__ __forceinline__ void zdecode16(const uint4 sm, uint64_t dp, uint32_t h, uint4& o0, uint4& o1) {
     const uint32_t s[4] = {sm.x, sm.y, sm.z, sm.w};
     uint32_t o[8];
 #pragma unroll
@@ -97,14 +107,62 @@ __device__ __forceinline__ void zdecode16(const uint4 sm, const uint32_t (&pl)[4
         for (int half = 0; half < 2; ++half) {
             const int i = 2 * k + half;  // word i of the lane's 16
             const uint32_t m = (s[i >> 2] >> (8 * (i & 3))) & 0xffu;
-            const uint32_t c = ((pl[0] >> i) & 1u) | (((pl[1] >> i) & 1u) << 1) | (((pl[2] >> i) & 1u) << 2) |
-                               (((pl[3] >> i) & 1u) << 3);
-            w2 |= (((m & 0x80u) << 8) | ((h - c) << 7) | (m & 0x7fu)) << (16 * half);
+            const uint32_t d = (uint32_t)(dp >> (4 * i)) & 0xfu;
+            w2 |= (((m & 0x80u) << 8) | (((h - d) & 0xffu) << 7) | (m & 0x7fu)) << (16 * half);
         }
         o[k] = w2;
     }
     o0 = make_uint4(o[0], o[1], o[2], o[3]);
     o1 = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// The lane's 16 offsets d_i of a coded block.  rd32(off, valid) reads the 32-bit word at byte `off`
+// of the block's stream B (it is called by every lane of the warp: `valid` says whether the value is
+// used, so loaders may skip the read, and shuffle-based loaders stay warp-collective).
+//   FOR (b = 0..4): d_i = c_i from the lane's 16 bits of each of the b planes;
+//   two-tier (b = kZTier + o): tier-1 code t_i from two planes; the lane's escaped words (t_i = 3) take
+//   the tier-2 codes s_j, j = r, r+1, ..., where r is the number of escaped words of lower lanes.
+template <typename RD32>
+__device__ __forceinline__ uint64_t zcodes(uint32_t hdr, uint32_t lane, RD32 rd32) {
+    auto rd16 = [&](uint32_t off) { return (rd32(off & ~3u, true) >> (16u * ((off >> 1) & 1u))) & 0xffffu; };
+    if (!ztier(hdr)) {
+        const uint32_t np = zplanes(hdr);
+        uint64_t dp = 0;
+#pragma unroll
+        for (uint32_t p = 0; p < 4; ++p)
+            if (p < np) dp |= spread4(rd16(64u * p + 2u * lane)) << p;
+        return dp;
+    }
+    const uint32_t o = ((hdr >> 8) & 0xffu) - kZTier;
+    const uint32_t t0 = rd16(2u * lane), t1 = rd16(64u + 2u * lane), esc = t0 & t1;
+    const uint32_t cnt = __popc(esc);
+    uint32_t r = cnt;  // inclusive scan over the warp, then exclusive
+#pragma unroll
+    for (int sft = 1; sft < 32; sft <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, r, sft);
+        if (lane >= (uint32_t)sft) r += t;
+    }
+    r -= cnt;
+    const uint32_t pw = zt2_bytes(hdr), wo = 128u + 4u * (r >> 5);
+    const bool need1 = cnt != 0, need2 = (r & 31u) + cnt > 32u;
+    uint32_t x[3];
+#pragma unroll
+    for (uint32_t q = 0; q < 3; ++q) {
+        const uint32_t lo = rd32(wo + q * pw, need1), hi = rd32(wo + q * pw + 4u, need2);
+        x[q] = __funnelshift_r(need1 ? lo : 0u, need2 ? hi : 0u, r & 31u);
+    }
+    uint64_t dp = spread4(t0) | (spread4(t1) << 1);
+    dp += 0x1111111111111111ull * o;  // d = o + t: tier-1 words; escaped nibbles hold o + 3 so far
+    for (uint32_t e = esc; e; e &= e - 1u) {  // escaped words in order, consuming s_r, s_r+1, ...
+        const uint32_t i = __ffs(e) - 1u;
+        const uint32_t sj = (x[0] & 1u) | ((x[1] & 1u) << 1) | ((x[2] & 1u) << 2);
+        x[0] >>= 1;
+        x[1] >>= 1;
+        x[2] >>= 1;
+        const int delta = (int)(sj < o ? sj : sj + 3u) - (int)(o + 3u);  // nibble o + 3 -> d (no borrow: d >= 0)
+        dp += (uint64_t)(int64_t)delta << (4u * i);
+    }
+    return dp;
 }
 
 // 32-bit word `wi` (0..3) of lane `src`'s uint4 v, for every lane (four shuffles and a select).
@@ -203,7 +261,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
             for (int u = 0; u < U; ++u) {
                 const uint32_t b = b0 + u;
                 if (b >= nb) break;
-                const uint32_t kind = (hh[u] >> 8) & 0xffu, n = hh[u] >> 16;
+                const uint32_t kind = (hh[u] >> 8) & 0xffu;
                 uint8_t* bo = out + (uint64_t)b * kZBlock;
                 uint4* o4 = reinterpret_cast<uint4*>(bo);
                 if (kind == kZZero) {
@@ -218,32 +276,22 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                         for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, zld4<STAGE>(cp + oa[u] + i * 16u));
                     }
                 } else {
-                    // lane l's 16 code bits of plane p: stream-B bytes ob + 64p + 2l .. +1
-                    uint32_t pl[4] = {0u, 0u, 0u, 0u};
+                    // stream-B words of this block: routed out of the window by shuffles, or read directly
+                    const uint32_t hdr = hh[u], n = zexc_n(hdr), xo = zexc_off(hdr);
+                    auto rd32 = [&](uint32_t off, bool valid) -> uint32_t {
+                        if (windowed) {
+                            const uint32_t rel = ob[u] + off - w0, c = (rel >> 4) & 63u;
+                            const uint32_t x0 = shfl_word(wv0, c & 31u, (rel >> 2) & 3u);
+                            const uint32_t x1 = shfl_word(wv1, c & 31u, (rel >> 2) & 3u);
+                            return c < 32u ? x0 : x1;
+                        }
+                        return valid ? zld32<STAGE>(cb + ob[u] + off) : 0u;
+                    };
+                    const uint64_t dp = zcodes(hdr, lane, rd32);
                     uint32_t ex = 0u;
-                    if (windowed) {
-#pragma unroll
-                        for (uint32_t pp = 0; pp < 4; ++pp) {
-                            if (pp >= kind) break;
-                            const uint32_t rel = ob[u] + 64u * pp + 2u * lane - w0, c = rel >> 4;
-                            const uint32_t x0 = shfl_word(wv0, c & 31u, (rel >> 2) & 3u);
-                            const uint32_t x1 = shfl_word(wv1, c & 31u, (rel >> 2) & 3u);
-                            pl[pp] = ((c < 32u ? x0 : x1) >> (16u * ((rel >> 1) & 1u))) & 0xffffu;
-                        }
-                        if (n) {
-                            const uint32_t rel = ob[u] + 64u * kind + 4u * lane - w0, c = (rel >> 4) & 63u;
-                            const uint32_t x0 = shfl_word(wv0, c & 31u, (rel >> 2) & 3u);
-                            const uint32_t x1 = shfl_word(wv1, c & 31u, (rel >> 2) & 3u);
-                            ex = c < 32u ? x0 : x1;
-                        }
-                    } else {
-#pragma unroll
-                        for (uint32_t pp = 0; pp < 4; ++pp)
-                            if (pp < kind) pl[pp] = zld16<STAGE>(cb + ob[u] + 64u * pp + 2u * lane);
-                        if (lane < n) ex = zld32<STAGE>(cb + ob[u] + 64u * kind + 4u * lane);
-                    }
+                    if (n) ex = rd32(xo + 4u * lane, lane < n);
                     uint4 o0, o1;
-                    zdecode16(q0[u], pl, hh[u] & 0xffu, o0, o1);
+                    zdecode16(q0[u], dp, hdr & 0xffu, o0, o1);
                     st_v4(o4 + 2 * lane, o0);
                     st_v4(o4 + 2 * lane + 1, o1);
                     if (n) {
@@ -253,10 +301,10 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                         __syncwarp();
                         uint16_t* o16 = reinterpret_cast<uint16_t*>(bo);
                         const uint32_t in_reg = min(n, 32u);
-                        const bool reg_ok = !windowed || ob[u] + 64u * kind + 4u * in_reg - w0 <= 1024u;
+                        const bool reg_ok = !windowed || ob[u] + xo + 4u * in_reg - w0 <= 1024u;
                         if (lane < in_reg && reg_ok) o16[ex & 0xffffu] = (uint16_t)(ex >> 16);
                         for (uint32_t j = reg_ok ? in_reg + lane : lane; j < n; j += 32) {
-                            const uint32_t e = zld32<STAGE>(cb + ob[u] + 64u * kind + j * 4u);
+                            const uint32_t e = zld32<STAGE>(cb + ob[u] + xo + j * 4u);
                             o16[e & 0xffffu] = (uint16_t)(e >> 16);
                         }
                     }
@@ -285,9 +333,13 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
 constexpr uint32_t kZBuf = 12288, kZRing = 2;
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ src, DevDesc dst, const DevDesc* __restrict__ desc,
-                                                   const ZPiece* __restrict__ pieces, uint32_t n_pieces,
-                                                   uint32_t* __restrict__ ready, DevCtl* __restrict__ own, DevCtl* gate, int sys) {
+// STAGE: the same kernel decodes the DMAZ staging buffer (src + coff − src_base): thread 0 first waits
+// until the copy group carrying the piece has landed (*progress > grp), then bulk-copies it from HBM.
+template <bool STAGE>
+__global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ src, uint64_t src_base, DevDesc dst,
+                                                   const DevDesc* __restrict__ desc, const ZPiece* __restrict__ pieces,
+                                                   uint32_t n_pieces, uint32_t* __restrict__ ready, DevCtl* __restrict__ own,
+                                                   DevCtl* gate, int sys, const uint32_t* progress) {
     extern __shared__ __align__(128) uint8_t zring[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(zring + kZRing * kZBuf);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kZRing);
@@ -309,11 +361,15 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         if (p == 0) own->t_first = globaltimer();
         const ZPiece& pc = pieces[p];
         const uint32_t bb = smem_addr(&bar[b]);
+        if (STAGE) {
+            wait_geq(progress + 32 * (pc.grp >> 24), (pc.grp & 0xffffffu) + 1, own);
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // the landed bytes, to the bulk copy
+        }
         if (pc.cbytes <= kZBuf) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(pc.cbytes) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              smem_addr(zring + b * kZBuf)),
-                         "l"(src + pc.coff), "r"(pc.cbytes), "r"(bb)
+                         "l"(src + (pc.coff - src_base)), "r"(pc.cbytes), "r"(bb)
                          : "memory");
         } else {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bb) : "memory");
@@ -335,7 +391,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
                              : "=r"(ok) : "r"(bb), "r"(par) : "memory");
             } while (!ok);
         }
-        const uint8_t* cp = pc.cbytes <= kZBuf ? zring + b * kZBuf : src + pc.coff;  // generic address
+        const uint8_t* cp = pc.cbytes <= kZBuf ? zring + b * kZBuf : src + (pc.coff - src_base);  // generic address
         uint8_t* out = weight_ptr(dd, pc.off);
         const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
         // every warp scans the piece's block offsets (stream A, stream B)
@@ -355,7 +411,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         for (uint32_t blk = warp; blk < nb; blk += 4) {
             const uint32_t h = __shfl_sync(0xffffffffu, hd, blk), oa = __shfl_sync(0xffffffffu, ia - sa, blk);
             const uint32_t ob = __shfl_sync(0xffffffffu, ib - sb, blk);
-            const uint32_t kind = (h >> 8) & 0xffu, n = h >> 16;
+            const uint32_t kind = (h >> 8) & 0xffu;
             uint8_t* bo = out + (uint64_t)blk * kZBlock;
             uint4* o4 = reinterpret_cast<uint4*>(bo);
             if (kind == kZZero) {
@@ -366,19 +422,19 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
                 for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, *reinterpret_cast<const uint4*>(cp + oa + i * 16u));
             } else {
                 const uint4 sm = *reinterpret_cast<const uint4*>(cp + oa + lane * 16u);
-                uint32_t pl[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-                for (uint32_t pp = 0; pp < 4; ++pp)
-                    if (pp < kind) pl[pp] = *reinterpret_cast<const uint16_t*>(cb + ob + 64u * pp + 2u * lane);
+                const uint32_t n = zexc_n(h), xo = zexc_off(h);
+                const uint64_t dp = zcodes(h, lane, [&](uint32_t off, bool valid) -> uint32_t {
+                    return valid ? *reinterpret_cast<const uint32_t*>(cb + ob + off) : 0u;
+                });
                 uint4 o0, o1;
-                zdecode16(sm, pl, h & 0xffu, o0, o1);
+                zdecode16(sm, dp, h & 0xffu, o0, o1);
                 st_v4(o4 + 2 * lane, o0);
                 st_v4(o4 + 2 * lane + 1, o1);
                 if (n) {
                     __syncwarp();  // exceptions overwrite their words after the warp's block stores
                     uint16_t* o16 = reinterpret_cast<uint16_t*>(bo);
                     for (uint32_t j = lane; j < n; j += 32) {
-                        const uint32_t e = *reinterpret_cast<const uint32_t*>(cb + ob + 64u * kind + 4u * j);
+                        const uint32_t e = *reinterpret_cast<const uint32_t*>(cb + ob + xo + 4u * j);
                         o16[e & 0xffffu] = (uint16_t)(e >> 16);
                     }
                 }
@@ -400,13 +456,19 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
 void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
                   const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
                   DevCtl* gate, int sys, int stage, const uint32_t* progress) {
-    static const bool swapz_regs = getenv("FSW_SWAPZ_REGS") != nullptr;
-    if (stage)
+    // A/B hooks: FSW_SWAPZ_REGS = the register decoder from host memory too, FSW_DMAZ_TMA = the TMA
+    // ring decoder on the staging buffer (measured slower there: 128 threads per CTA decode 86 GB/s of
+    // store bytes on 32 CTAs, the 256-thread register decoder 117; tools/dmaz_probe.py)
+    static const bool swapz_regs = getenv("FSW_SWAPZ_REGS") != nullptr, dmaz_tma = getenv("FSW_DMAZ_TMA") != nullptr;
+    const size_t smem = kZRing * kZBuf + 64;
+    if (stage && !dmaz_tma)
         k_swapz<true, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
-    else if (swapz_regs)  // A/B hook: the register decoder straight from host memory
+    else if (stage)
+        k_swapz_tma<true><<<ctas, 128, smem, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
+    else if (swapz_regs)
         k_swapz<false, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
     else  // src_base is 0 for the mapped host store (pieces address it by coff)
-        k_swapz_tma<<<ctas, 128, kZRing * kZBuf + 64, s>>>(src, dst, desc, pieces, n_pieces, ready, own, gate, sys);
+        k_swapz_tma<false><<<ctas, 128, smem, s>>>(src, 0, dst, desc, pieces, n_pieces, ready, own, gate, sys, nullptr);
 }
 
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap

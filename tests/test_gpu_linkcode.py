@@ -9,6 +9,7 @@ import synth
 from paper_2306_03622_b200 import (DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, NO_OVERLAP,
                                    ORDER_RANDOM, ORDER_REVERSE, FswError)
 from paper_2306_03622_b200 import fsw as F
+from crafted import tier_offsets
 from test_gpu_swap import _odd_model
 
 pytestmark = pytest.mark.gpu
@@ -159,6 +160,8 @@ def _crafted_weights(spec, w, seed=11):
     words[k:k + 2048] = 0; k += 2048
     words[k:k + 512] = np.where(rng.random(512) < 0.5, 0x8000, 0) | rng.integers(0, 128, 512); k += 512
     words[k:k + 512] = base(sm[k:k + 512], rng.integers(242, 256, 512)); k += 512
+    for o in range(4):  # two-tier blocks, tier-1 offset o, with escapes on both sides and exceptions
+        words[k:k + 512] = base(sm[k:k + 512], 120 - tier_offsets(rng, o, n_exc=5 + 15 * o)); k += 512
     k = (k + 8191) // 8192 * 8192  # next 16-KiB piece boundary of this tensor
     words[k:k + 3 * 8192] = rng.integers(0, 1 << 16, 3 * 8192)          # three all-raw pieces
     return w
@@ -174,6 +177,9 @@ def test_coded_rare_block_kinds_bit_exact(rt, engine):
         hdr = pcs["hdr"].reshape(-1)
         kinds = (hdr >> 8) & 0xFF
         assert (kinds == 0xFE).any() and (kinds == 0xFF).any() and ((hdr >> 16) > 32).any()
+        for o in range(4):
+            assert (kinds == 0x10 + o).any()
+        assert ((kinds >= 0x10) & (kinds <= 0x13) & ((hdr >> 26) > 32)).any()  # > 32 exceptions, two-tier
         assert (pcs["cbytes"] > 12288).any()  # larger than an SMZ ring slot: the direct-read fallback
         for order in (0, ORDER_REVERSE):
             rt.evict(mid)
