@@ -9,7 +9,7 @@ import synth
 from paper_2306_03622_b200 import (DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, NO_OVERLAP,
                                    ORDER_RANDOM, ORDER_REVERSE, FswError)
 from paper_2306_03622_b200 import fsw as F
-from crafted import tier_offsets
+from crafted import random_block_mixture, tier_offsets
 from test_gpu_swap import _odd_model
 
 pytestmark = pytest.mark.gpu
@@ -181,6 +181,24 @@ def test_coded_rare_block_kinds_bit_exact(rt, engine):
             assert (kinds == 0x10 + o).any()
         assert ((kinds >= 0x10) & (kinds <= 0x13) & ((hdr >> 26) > 32)).any()  # > 32 exceptions, two-tier
         assert (pcs["cbytes"] > 12288).any()  # larger than an SMZ ring slot: the direct-read fallback
+        for order in (0, ORDER_REVERSE):
+            rt.evict(mid)
+            r = rt.invoke(mid, spec.make_input(), gpu=0, engine=engine, order=order)
+            assert r.stats["engine"] == engine
+            np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+    finally:
+        rt.unregister(mid)
+
+
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_coded_random_block_mixture_bit_exact(rt, engine, seed):
+    """Every block of the MLP drawn from a random mixture of block kinds (tests/crafted.py): the coded
+    engines land the store bit-exactly, in execution and in reverse piece order."""
+    spec = synth.build_model("mlp")
+    w = random_block_mixture(spec, spec.build_weights(), seed)
+    mid = rt.register_spec(spec, w, link_code=True)
+    try:
         for order in (0, ORDER_REVERSE):
             rt.evict(mid)
             r = rt.invoke(mid, spec.make_input(), gpu=0, engine=engine, order=order)

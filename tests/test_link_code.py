@@ -11,7 +11,7 @@ import pytest
 
 import synth
 from paper_2306_03622_b200 import build as B
-from crafted import tier_offsets
+from crafted import random_block_mixture, tier_offsets
 from paper_2306_03622_b200 import fsw as F
 
 
@@ -250,3 +250,58 @@ def test_dmaz_plan_needs_link_code():
         with pytest.raises(F.FswError) as e:
             rt.dmaz_plan(mid, 1 << 20)
         assert e.value.status == F.ESTATE
+
+
+def _block_costs(words):
+    """Coded bytes of one 512-word block under every kind of the format (include/fsw.h), from the
+    block's exponents alone: FOR widths 0..4, two-tier offsets 0..3 (at most 63 exceptions), raw."""
+    pad16 = lambda x: -(-x // 16) * 16
+    if not words.any():
+        return 0
+    e = ((words >> 7) & 0xFF).astype(np.int64)
+    d = e.max() - e
+    costs = [1024]
+    for b in range(5):
+        costs.append(512 + pad16(64 * b + 4 * int((d >= (1 << b)).sum())))
+    nx = int((d >= 11).sum())
+    if nx <= 63:
+        for o in range(4):
+            ne = int(((d < o) | (d >= o + 3)).sum())
+            costs.append(512 + pad16(128 + 12 * -(-ne // 32) + 4 * nx))
+    return min(costs)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_block_mixture_roundtrip_and_cheapest_kind(seed):
+    """Every weight block drawn from a random mixture (geometric exponent offsets with random ratio and
+    base, two-tier patterns, tiny-value outliers, zeros, inf/NaN exponents, random words): the coded
+    store decodes to the store byte for byte, every block kind occurs, and each block's coded size is
+    the cheapest the format allows for it (the encoder's chooser)."""
+    spec = synth.build_model("mlp-small")
+    w = random_block_mixture(spec, spec.build_weights(), seed)
+    with F.Runtime(flags=F.HOST_ONLY) as rt:
+        mid = rt.register_spec(spec, w, link_code=True)
+        store, coded, pcs, out = decode_all(rt, mid)
+        np.testing.assert_array_equal(out, store)
+        kinds = set()
+        sw = store.view(np.uint16)
+        for p in pcs:
+            nb = -(-int(p["bytes"]) // 1024)
+            for b in range(nb):
+                hd = int(p["hdr"][b])
+                kinds.add((hd >> 8) & 0xFF)
+                if (b + 1) * 1024 > int(p["bytes"]):
+                    continue  # a partial tail block is always raw
+                blk = sw[(int(p["off"]) + 1024 * b) // 2:(int(p["off"]) + 1024 * b) // 2 + 512]
+                kd = (hd >> 8) & 0xFF
+                if kd == 0xFE:
+                    size = 0
+                elif kd == 0xFF:
+                    size = 1024
+                elif kd >= 0x10:
+                    ne, nx = (hd >> 16) & 0x3FF, hd >> 26
+                    size = 512 + -(-(128 + 12 * -(-ne // 32) + 4 * nx) // 16) * 16
+                else:
+                    size = 512 + -(-(64 * kd + 4 * (hd >> 16)) // 16) * 16
+                assert size == _block_costs(blk), (hex(hd), size, _block_costs(blk))
+        assert {0xFE, 0xFF, 0x10, 0x11, 0x12, 0x13} <= kinds and len(kinds & {0, 1, 2, 3, 4}) >= 3, sorted(kinds)
