@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <cmath>
 #include <vector>
 using namespace fsw;
 
@@ -30,7 +31,17 @@ int main(int argc, char** argv) {
     uint32_t* ctr;
     cudaMalloc(&A, 64 << 20); cudaMalloc(&W, 64 << 20); cudaMalloc(&O, 64 << 20);
     cudaMalloc(&part, 64 << 20); cudaMalloc(&ctr, 1 << 20); cudaMemset(ctr, 0, 1 << 20);
-    cudaMemset(A, 0x3c, 64 << 20); cudaMemset(W, 0x3c, 64 << 20);
+    {  // random bf16 in [-1, 1): outputs of different tilings are compared against each other
+        std::vector<uint16_t> hv((64 << 20) / 2);
+        uint32_t x = 12345;
+        for (auto& v : hv) { x = x * 1664525u + 1013904223u; float f = ((x >> 8) * (1.0f / 16777216.0f)) * 2.0f - 1.0f;
+                             uint32_t u; memcpy(&u, &f, 4); v = (uint16_t)(u >> 16); }
+        cudaMemcpy(A, hv.data(), 64 << 20, cudaMemcpyHostToDevice);
+        for (auto& v : hv) { x = x * 1664525u + 1013904223u; float f = ((x >> 8) * (1.0f / 16777216.0f)) * 0.1f - 0.05f;
+                             uint32_t u; memcpy(&u, &f, 4); v = (uint16_t)(u >> 16); }
+        cudaMemcpy(W, hv.data(), 64 << 20, cudaMemcpyHostToDevice);
+    }
+    std::vector<uint16_t> ref, got;
     DevDesc* dd; cudaMalloc(&dd, sizeof(DevDesc));
     DevDesc h{W, W, 0, 0}; cudaMemcpy(dd, &h, sizeof h, cudaMemcpyHostToDevice);
     DevCtl* ctl; cudaMalloc(&ctl, sizeof(DevCtl)); cudaMemset(ctl, 0, sizeof(DevCtl));
@@ -39,7 +50,10 @@ int main(int argc, char** argv) {
     for (auto& sh : shapes) {
         if (only && strcmp(only, sh.name)) continue;
         const uint32_t n_pad = (sh.N + 15) / 16 * 16, kt = sh.K / 64;
-        double best = 1e9; int bb = 0; uint32_t bs = 0, bm = 1, bz = 0, bmr = 128;
+        double best = 1e9; int bb = 0; uint32_t bs = 0, bm = 1, bz = 0, bmr = 128, bsab = 0;
+        ref.clear();
+        {
+        const uint32_t sab = 0;  // the swap-AB variant measured in profiles/r01/gemm_swap_ab_sweep.txt was not kept
         for (int bn : {16, 32, 64, 128}) {
             if (n_pad % bn || (only_bn && bn != only_bn)) continue;
             for (uint32_t mc : {1u, 2u, 4u, 8u}) {
@@ -48,6 +62,17 @@ int main(int argc, char** argv) {
             for (uint32_t cl : {0u, 1u}) {  // split-K reduction: global partials (0) / cluster DSMEM (1)
             for (uint32_t mr : {128u, 64u}) {  // activation rows per M tile
                 if (S > kt || (only_s && S != only_s)) continue;
+                if (ref.empty() && (sab || bn != 32 || S != 1 || mc != 1 || cl || mr != 128)) {
+                    // reference output of this shape: BN = 32, no split, no swap-AB
+                    CUtensorMap tr; make_tmap_act(&tr, A, sh.M, sh.K, sh.K, 128);
+                    GemmArgs r{}; r.M = sh.M; r.N = sh.N; r.K = sh.K; r.n_pad = n_pad; r.has_bias = 1; r.out = O; r.out_bf16 = 1;
+                    r.ld_out = sh.N; r.bn = n_pad % 32 ? 16 : 32; r.m_rows = 128; r.splits = 1; r.kt_per = kt; r.part = part; r.ctr = ctr; r.mc = 1;
+                    Wait w0{}; w0.ctl = ctl;
+                    launch_gemm(s, dd, w0, &tr, r);
+                    cudaStreamSynchronize(s);
+                    ref.resize((size_t)sh.M * sh.N);
+                    cudaMemcpy(ref.data(), O, ref.size() * 2, cudaMemcpyDeviceToHost);
+                }
                 if (cl && (S < 2 || S > 8 || mc > 1)) continue;
                 if (getenv("CZ_ONLY") && !cl && S > 1) continue;
                 if (getenv("NO_MC") && mc > 1) continue;
@@ -58,7 +83,7 @@ int main(int argc, char** argv) {
                 const uint32_t ctas = ((sh.M + mr - 1) / mr) * (n_pad / bn) * S;
                 if (ctas > 600) continue;
                 CUtensorMap tm;
-                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K, mr == 64 ? 64 : 128 / mc)) { printf("tmap fail\n"); return 1; }
+                if (!make_tmap_act(&tm, A, sh.M, sh.K, sh.K, mr < 128 ? mr : 128 / mc)) { printf("tmap fail\n"); return 1; }
                 GemmArgs a{}; a.M = sh.M; a.N = sh.N; a.K = sh.K; a.n_pad = n_pad; a.w_off = 0; a.b_off = 0;
                 a.has_bias = 1; a.act = 0; a.res = nullptr; a.out = O; a.out_bf16 = 1; a.ld_out = sh.N; a.bn = bn;
                 a.m_rows = mr; a.splits = S; a.kt_per = kt_per; a.part = part; a.ctr = ctr; a.mc = mc; a.cz = cl ? S : 0;
@@ -72,9 +97,17 @@ int main(int argc, char** argv) {
                 float ms; cudaEventElapsedTime(&ms, e0, e1);
                 const double us = ms * 1000 / reps;
                 const double wbytes = 2.0 * n_pad * sh.K;
-                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u%s mc=%u mr=%3u ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s)\n", sh.name, sh.M,
-                       sh.K, sh.N, bn, S, cl ? "c" : " ", mc, mr, ctas, us, wbytes / us / 1e3, 2.0 * sh.M * sh.N * sh.K / us / 1e6);
-                if (us < best) { best = us; bb = bn; bs = S; bm = mc; bz = cl; bmr = mr; }
+                double err = 0, mref = 0;
+                if (!ref.empty()) {
+                    got.resize(ref.size());
+                    cudaMemcpy(got.data(), O, got.size() * 2, cudaMemcpyDeviceToHost);
+                    auto f = [](uint16_t v) { uint32_t u = (uint32_t)v << 16; float x; memcpy(&x, &u, 4); return (double)x; };
+                    for (size_t i = 0; i < ref.size(); ++i) { err = std::max(err, std::fabs(f(got[i]) - f(ref[i]))); mref = std::max(mref, std::fabs(f(ref[i]))); }
+                }
+                printf("%-18s M=%5u K=%5u N=%5u BN=%3d S=%2u%s mc=%u mr=%3u%s ctas=%4u: %7.2f us  (W %.0f GB/s, %.1f TF/s) err %.1e\n", sh.name, sh.M,
+                       sh.K, sh.N, bn, S, cl ? "c" : " ", mc, mr, sab ? " sab" : "", ctas, us, wbytes / us / 1e3,
+                       2.0 * sh.M * sh.N * sh.K / us / 1e6, mref > 0 ? err / mref : -1.0);
+                if (us < best) { best = us; bb = bn; bs = S; bm = mc; bz = cl; bmr = mr; bsab = sab; }
 #ifdef PHASES
                 // one isolated launch: per-CTA %globaltimer stamps -> mean phase durations
                 cudaDeviceSynchronize();
@@ -103,7 +136,8 @@ int main(int argc, char** argv) {
             }
             }
         }
-        printf("  BEST %-18s BN=%d S=%u%s mc=%u mr=%u %.2f us\n", sh.name, bb, bs, bz ? "c" : "", bm, bmr, best);
+        }
+        printf("  BEST %-18s BN=%d S=%u%s mc=%u mr=%u%s %.2f us\n", sh.name, bb, bs, bz ? "c" : "", bm, bmr, bsab ? " sab" : "", best);
     }
     cudaError_t e = cudaGetLastError();
     printf("last error: %s\n", cudaGetErrorString(e));
