@@ -1,0 +1,280 @@
+// Prototype (tools only, not in libfsw): batch-1 GEMM on the 2-CTA UMMA (tcgen05.mma.cta_group::2),
+// in the swap-AB form cuBLAS uses for these shapes: a CTA pair computes 128 weight rows x 32 tokens,
+// each CTA holding 64 weight rows and 16 tokens of every K sub-tile in its shared memory, so an SM
+// receives half the operand bytes of a 1-CTA tile (k_gemm vs cuBLAS).
+//   Y[t][n] = sum_k X[t][k] * W[n][k] + b[n]      (bf16 in, fp32 accumulate, bf16 out)
+// Weights use libfsw's pre-tiled K-major SWIZZLE_128B layout (one bulk copy per 64-row sub-tile).
+// The peer CTA relays "my half of stage s landed" to the leader's barrier; the leader issues the
+// MMAs and commits each stage to both CTAs' empty barriers (multicast).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/gemm2cta_proto tools/micro/gemm2cta_proto.cu -lcuda
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+constexpr int T = 32, TH = T / 2, WR = 64, KSUB = 4;
+constexpr uint32_t WSUB = WR * 128, XSUB = TH * 128, STAGE = KSUB * (WSUB + XSUB);
+
+struct Args {
+    const uint8_t* w;
+    const uint16_t* bias;
+    uint16_t* out;
+    uint32_t M, N, K, n_pad;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
+    uint32_t ok = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(su32(b)), "r"(par) : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ uint64_t desc_sw128(const void* p) {
+    return ((uint64_t)(su32(p) >> 4) & 0x3FFF) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __grid_constant__ CUtensorMap tmX, Args a, int stages) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* lfull = (uint64_t*)(smem + stages * STAGE);
+    uint64_t* pfull = lfull + stages;
+    uint64_t* empty = pfull + stages;
+    uint64_t* done = empty + stages;
+    uint32_t* tslot = (uint32_t*)(done + 1);
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x >> 1) * 128 + rank * WR;  // this CTA's weight rows
+    const uint32_t tb = blockIdx.y * T;                       // the pair's tokens
+    const uint32_t nkt = a.K / 64, nst = (nkt + KSUB - 1) / KSUB;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&lfull[s], 1);
+            mbar_init(&pfull[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(tslot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0 && lane == 0) {  // producer (both CTAs): this CTA's 64 weight rows and 16 tokens
+        const uint64_t kstride = (uint64_t)(a.n_pad / 8) * 1024;
+        auto load_w = [&](uint32_t st) {
+            const uint32_t s = st % stages, nsub = min((uint32_t)KSUB, nkt - st * KSUB);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&lfull[s])), "r"(nsub * (WSUB + XSUB)) : "memory");
+            for (uint32_t j = 0; j < nsub; ++j) {
+                const uint32_t kt = st * KSUB + j;
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 su32(smem + s * STAGE + j * WSUB)), "l"(a.w + kt * kstride + (uint64_t)(w0 / 8) * 1024), "r"(WSUB),
+                             "r"(su32(&lfull[s])) : "memory");
+            }
+        };
+        auto load_x = [&](uint32_t st) {
+            const uint32_t s = st % stages, nsub = min((uint32_t)KSUB, nkt - st * KSUB);
+            for (uint32_t j = 0; j < nsub; ++j) {
+                const uint32_t kt = st * KSUB + j;
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                                 su32(smem + s * STAGE + KSUB * WSUB + j * XSUB)), "l"(&tmX), "r"((int)(kt * 64)), "r"((int)(tb + rank * TH)),
+                             "r"(su32(&lfull[s])) : "memory");
+            }
+        };
+        // weights of the stages in flight first (they do not depend on the predecessor), then the tokens
+        const uint32_t pre = min((uint32_t)stages, nst);
+        for (uint32_t st = 0; st < pre; ++st) load_w(st);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (uint32_t st = 0; st < pre; ++st) load_x(st);
+        for (uint32_t st = pre; st < nst; ++st) {
+            mbar_wait(&empty[st % stages], ((st / stages) - 1) & 1);
+            load_w(st);
+            load_x(st);
+        }
+    } else if (warp == 1 && lane == 0 && rank == 1) {  // relay: my half of stage s has landed
+        for (uint32_t st = 0; st < nst; ++st) {
+            const uint32_t s = st % stages;
+            mbar_wait(&lfull[s], (st / stages) & 1);
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(&pfull[s])));
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer: M = 128 (64 per CTA), N = 32 (16 per CTA)
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        for (uint32_t st = 0; st < nst; ++st) {
+            const uint32_t s = st % stages, nsub = min((uint32_t)KSUB, nkt - st * KSUB);
+            mbar_wait(&lfull[s], (st / stages) & 1);
+            mbar_wait(&pfull[s], (st / stages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad0 = desc_sw128(smem + s * STAGE), bd0 = desc_sw128(smem + s * STAGE + KSUB * WSUB);
+            for (uint32_t j = 0; j < nsub; ++j)
+                for (uint32_t kk = 0; kk < 4; ++kk) {
+                    const uint64_t ad = ad0 + ((j * WSUB + kk * 32) >> 4), bd = bd0 + ((j * XSUB + kk * 32) >> 4);
+                    const uint32_t acc = (st | j | kk) != 0;
+                    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem),
+                                 "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                }
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                             su32(&empty[s])), "h"((uint16_t)3) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(su32(done)),
+                     "h"((uint16_t)3) : "memory");
+    }
+    __syncwarp();
+    // epilogue: this CTA's 64 weight rows x all 32 tokens; TMEM lane = m + 64·(token >= 16), column = token mod 16
+    mbar_wait(done, 0);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+                   "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                 : "r"(tmem + ((warp * 32u) << 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const uint32_t m = (warp & 1) * 32 + lane, n = w0 + m, tok0 = tb + (warp >> 1) * 16;
+    if (n < a.N) {
+        const float bias = __uint_as_float((uint32_t)a.bias[n] << 16);
+        for (int c = 0; c < 16; ++c) {
+            const uint32_t t = tok0 + c;
+            if (t < a.M) {
+                const float v = __uint_as_float(r[c]) + bias;
+                const uint32_t u = __float_as_uint(v);
+                a.out[(uint64_t)t * a.N + n] = (uint16_t)((u + 0x7FFF + ((u >> 16) & 1)) >> 16);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync();  // no CTA frees TMEM while its peer's MMAs could still target it
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static uint16_t f2bf(float f) { uint32_t u; memcpy(&u, &f, 4); return (uint16_t)((u + 0x7FFF + ((u >> 16) & 1)) >> 16); }
+static float bf2f(uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(&f, &u, 4); return f; }
+
+int main(int argc, char** argv) {
+    setvbuf(stdout, nullptr, _IONBF, 0);
+    struct Shape { const char* name; uint32_t M, K, N; } shapes[] = {
+        {"bert.qkv", 128, 768, 2304}, {"bert.o", 128, 768, 768}, {"bert.ffn1", 128, 768, 3072}, {"bert.ffn2", 128, 3072, 768},
+        {"gpt.qkv", 128, 1600, 4800}, {"gpt.fc", 128, 1600, 6400}, {"gpt.proj2", 128, 6400, 1600}};
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+    EncFn enc = (EncFn)fp;
+    cudaFuncSetAttribute(k_g2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaStream_t s;
+    cudaStreamCreate(&s);
+    for (auto& sh : shapes) {
+        if (argc > 1 && strcmp(argv[1], sh.name)) continue;
+        const uint32_t n_pad = (sh.N + 127) / 128 * 128, nkt = sh.K / 64;
+        std::vector<uint16_t> X((size_t)sh.M * sh.K), Wl((size_t)sh.N * sh.K), B(sh.N);
+        uint32_t x = 7;
+        auto rnd = [&]() { x = x * 1664525u + 1013904223u; return ((x >> 8) * (1.0f / 16777216.0f)) * 2.0f - 1.0f; };
+        for (auto& v : X) v = f2bf(rnd());
+        for (auto& v : Wl) v = f2bf(rnd() * 0.05f);
+        for (auto& v : B) v = f2bf(rnd() * 0.1f);
+        // pre-tiled weights: k tile kt, 8-row group g = n / 8: 1024 B at (kt·n_pad/8 + g)·1024, row n%8 at
+        // +128·(n%8), its 16-B chunk c at chunk c ^ (n % 8)  (K-major SWIZZLE_128B)
+        std::vector<uint16_t> Wt((size_t)nkt * n_pad * 64, 0);
+        for (uint32_t n = 0; n < sh.N; ++n)
+            for (uint32_t k = 0; k < sh.K; ++k) {
+                const uint32_t kt = k / 64, kk = k % 64, c = kk / 8, e = kk % 8;
+                const size_t byte = ((size_t)kt * (n_pad / 8) + n / 8) * 1024 + (n % 8) * 128 + ((c ^ (n % 8)) * 16) + e * 2;
+                Wt[byte / 2] = Wl[(size_t)n * sh.K + k];
+            }
+        uint16_t *dX, *dB, *dO;
+        uint8_t* dW;
+        cudaMalloc(&dX, X.size() * 2);
+        cudaMalloc(&dW, Wt.size() * 2);
+        cudaMalloc(&dB, B.size() * 2);
+        cudaMalloc(&dO, (size_t)sh.M * sh.N * 2);
+        cudaMemcpy(dX, X.data(), X.size() * 2, cudaMemcpyHostToDevice);
+        cudaMemcpy(dW, Wt.data(), Wt.size() * 2, cudaMemcpyHostToDevice);
+        cudaMemcpy(dB, B.data(), B.size() * 2, cudaMemcpyHostToDevice);
+        cudaMemset(dO, 0, (size_t)sh.M * sh.N * 2);
+        CUtensorMap tm;
+        const cuuint64_t dims[2] = {sh.K, sh.M}, strides[1] = {(cuuint64_t)sh.K * 2};
+        const cuuint32_t box[2] = {64, TH}, es[2] = {1, 1};
+        if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dX, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            printf("tensor map failed\n");
+            return 1;
+        }
+        Args a{dW, dB, dO, sh.M, sh.N, sh.K, n_pad};
+        const int nst = (int)((nkt + KSUB - 1) / KSUB), stages = nst < 5 ? nst : 5;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(n_pad / 128 * 2, (sh.M + T - 1) / T);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = stages * STAGE + 1024 + 256;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages);
+        cudaError_t e2 = cudaStreamSynchronize(s);
+        if (e != cudaSuccess || e2 != cudaSuccess) {
+            printf("%s: launch %s / %s\n", sh.name, cudaGetErrorString(e), cudaGetErrorString(e2));
+            return 1;
+        }
+        std::vector<uint16_t> O((size_t)sh.M * sh.N);
+        cudaMemcpy(O.data(), dO, O.size() * 2, cudaMemcpyDeviceToHost);
+        double err = 0, mx = 0;
+        for (uint32_t t = 0; t < sh.M; t += 7)
+            for (uint32_t n = 0; n < sh.N; ++n) {
+                double ref = bf2f(B[n]);
+                for (uint32_t k = 0; k < sh.K; ++k) ref += (double)bf2f(X[(size_t)t * sh.K + k]) * bf2f(Wl[(size_t)n * sh.K + k]);
+                err = std::max(err, std::fabs(ref - bf2f(O[(size_t)t * sh.N + n])));
+                mx = std::max(mx, std::fabs(ref));
+            }
+        // timing: back-to-back launches captured in a graph, with and without PDL
+        for (int pdl = 1; pdl >= 0; --pdl) {
+        cfg.numAttrs = pdl;
+        const int reps = 50;
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
+        for (int i = 0; i < reps; ++i) cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages);
+        cudaStreamEndCapture(s, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphLaunch(ge, s);
+        cudaStreamSynchronize(s);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        cudaGraphLaunch(ge, s);
+        cudaEventRecord(e1, s);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("%-10s M=%4u K=%5u N=%5u ctas=%4u stages=%d: %6.2f us per GEMM (graph, %s)  max err %.2e of max |ref| %.2f  %s\n",
+               sh.name, sh.M, sh.K, sh.N, cfg.gridDim.x * cfg.gridDim.y, stages, ms * 1000 / reps, pdl ? "PDL chain" : "no PDL   ",
+               err, mx, err <= 1e-2 * mx ? "OK" : "MISMATCH");
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        }
+        cudaFree(dX); cudaFree(dW); cudaFree(dB); cudaFree(dO);
+    }
+    printf("last error: %s\n", cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
