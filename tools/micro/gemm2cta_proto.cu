@@ -13,9 +13,20 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <algorithm>
 #include <vector>
 
-constexpr int T = 32, TH = T / 2, WR = 64, KSUB = 4;
+#ifndef KSUB_
+#define KSUB_ 4
+#endif
+#ifndef MAXST_
+#define MAXST_ 5
+#endif
+constexpr int T = 32, TH = T / 2, WR = 64, KSUB = KSUB_;
+__device__ unsigned long long g_stamp[512][6];  // per-CTA %globaltimer phase stamps (isolated launch)
+__device__ __forceinline__ unsigned long long gtime() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
+#define STAMP(i) do { if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 512) g_stamp[blockIdx.x + gridDim.x * blockIdx.y][i] = gtime(); } while (0)
 constexpr uint32_t WSUB = WR * 128, XSUB = TH * 128, STAGE = KSUB * (WSUB + XSUB);
 
 struct Args {
@@ -43,8 +54,9 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __grid_constant__ CUtensorMap tmX, Args a, int stages) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __grid_constant__ CUtensorMap tmX, Args a, int stages, int teardown_sync) {
     extern __shared__ uint8_t raw[];
+    STAMP(0);
     uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
     uint64_t* lfull = (uint64_t*)(smem + stages * STAGE);
     uint64_t* pfull = lfull + stages;
@@ -66,7 +78,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
         mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncthreads();
+    const uint64_t kstride = (uint64_t)(a.n_pad / 8) * 1024;
+    // warp 0 issues the copies lane-parallel: lane 0 arms the stages' barriers, then lane l issues copy l
+    // of the stages in [st0, st1) (one thread issuing every copy back to back was the critical path)
+    auto arm = [&](uint32_t st0, uint32_t st1) {
+        if (lane == 0)
+            for (uint32_t st = st0; st < st1; ++st) {
+                const uint32_t nsub = min((uint32_t)KSUB, nkt - st * KSUB);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&lfull[st % stages])), "r"(nsub * (WSUB + XSUB)) : "memory");
+            }
+        __syncwarp();
+    };
+    auto load_w = [&](uint32_t st0, uint32_t st1) {
+        for (uint32_t i = lane; i < (st1 - st0) * KSUB; i += 32) {
+            const uint32_t st = st0 + i / KSUB, j = i % KSUB, kt = st * KSUB + j, s = st % stages;
+            if (kt >= nkt) continue;
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             su32(smem + s * STAGE + j * WSUB)), "l"(a.w + kt * kstride + (uint64_t)(w0 / 8) * 1024), "r"(WSUB),
+                         "r"(su32(&lfull[s])) : "memory");
+        }
+    };
+    auto load_x = [&](uint32_t st0, uint32_t st1) {
+        for (uint32_t i = lane; i < (st1 - st0) * KSUB; i += 32) {
+            const uint32_t st = st0 + i / KSUB, j = i % KSUB, kt = st * KSUB + j, s = st % stages;
+            if (kt >= nkt) continue;
+            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                             su32(smem + s * STAGE + KSUB * WSUB + j * XSUB)), "l"(&tmX), "r"((int)(kt * 64)), "r"((int)(tb + rank * TH)),
+                         "r"(su32(&lfull[s])) : "memory");
+        }
+    };
+    // the weights of the stages in flight are requested before anything else (they depend on nothing),
+    // while warp 1 allocates the pair's TMEM
+    const uint32_t pre = min((uint32_t)stages, nst);
     if (warp == 0) {
+        if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+        arm(0, pre);
+        load_w(0, pre);
+    }
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(tslot)) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
@@ -74,38 +124,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
     cluster_sync();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tslot;
+    STAMP(1);
 
-    if (warp == 0 && lane == 0) {  // producer (both CTAs): this CTA's 64 weight rows and 16 tokens
-        const uint64_t kstride = (uint64_t)(a.n_pad / 8) * 1024;
-        auto load_w = [&](uint32_t st) {
-            const uint32_t s = st % stages, nsub = min((uint32_t)KSUB, nkt - st * KSUB);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&lfull[s])), "r"(nsub * (WSUB + XSUB)) : "memory");
-            for (uint32_t j = 0; j < nsub; ++j) {
-                const uint32_t kt = st * KSUB + j;
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                                 su32(smem + s * STAGE + j * WSUB)), "l"(a.w + kt * kstride + (uint64_t)(w0 / 8) * 1024), "r"(WSUB),
-                             "r"(su32(&lfull[s])) : "memory");
-            }
-        };
-        auto load_x = [&](uint32_t st) {
-            const uint32_t s = st % stages, nsub = min((uint32_t)KSUB, nkt - st * KSUB);
-            for (uint32_t j = 0; j < nsub; ++j) {
-                const uint32_t kt = st * KSUB + j;
-                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                                 su32(smem + s * STAGE + KSUB * WSUB + j * XSUB)), "l"(&tmX), "r"((int)(kt * 64)), "r"((int)(tb + rank * TH)),
-                             "r"(su32(&lfull[s])) : "memory");
-            }
-        };
-        // weights of the stages in flight first (they do not depend on the predecessor), then the tokens
-        const uint32_t pre = min((uint32_t)stages, nst);
-        for (uint32_t st = 0; st < pre; ++st) load_w(st);
+    if (warp == 0) {  // producer (both CTAs): the tokens, then the rest of the ring
         asm volatile("griddepcontrol.wait;" ::: "memory");
-        for (uint32_t st = 0; st < pre; ++st) load_x(st);
+        load_x(0, pre);
         for (uint32_t st = pre; st < nst; ++st) {
-            mbar_wait(&empty[st % stages], ((st / stages) - 1) & 1);
-            load_w(st);
-            load_x(st);
+            if (lane == 0) mbar_wait(&empty[st % stages], ((st / stages) - 1) & 1);
+            __syncwarp();
+            arm(st, st + 1);
+            load_w(st, st + 1);
+            load_x(st, st + 1);
         }
+        STAMP(2);
     } else if (warp == 1 && lane == 0 && rank == 1) {  // relay: my half of stage s has landed
         for (uint32_t st = 0; st < nst; ++st) {
             const uint32_t s = st % stages;
@@ -138,6 +169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
     __syncwarp();
     // epilogue: this CTA's 64 weight rows x all 32 tokens; TMEM lane = m + 64·(token >= 16), column = token mod 16
     mbar_wait(done, 0);
+    STAMP(3);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     uint32_t r[16];
@@ -158,9 +190,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
             }
         }
     }
+    __syncthreads();
+    STAMP(4);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    cluster_sync();  // no CTA frees TMEM while its peer's MMAs could still target it
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    if (teardown_sync) cluster_sync();  // (both CTAs have seen `done`: no MMA can still target either TMEM)
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    STAMP(5);
 }
 
 typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -172,6 +207,7 @@ static float bf2f(uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(
 
 int main(int argc, char** argv) {
     setvbuf(stdout, nullptr, _IONBF, 0);
+    const int tsync = getenv("NO_TEARDOWN_SYNC") ? 0 : 1;
     struct Shape { const char* name; uint32_t M, K, N; } shapes[] = {
         {"bert.qkv", 128, 768, 2304}, {"bert.o", 128, 768, 768}, {"bert.ffn1", 128, 768, 3072}, {"bert.ffn2", 128, 3072, 768},
         {"gpt.qkv", 128, 1600, 4800}, {"gpt.fc", 128, 1600, 6400}, {"gpt.proj2", 128, 6400, 1600}};
@@ -219,7 +255,7 @@ int main(int argc, char** argv) {
             return 1;
         }
         Args a{dW, dB, dO, sh.M, sh.N, sh.K, n_pad};
-        const int nst = (int)((nkt + KSUB - 1) / KSUB), stages = nst < 5 ? nst : 5;
+        const int nst = (int)((nkt + KSUB - 1) / KSUB), stages = nst < MAXST_ ? nst : MAXST_;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(n_pad / 128 * 2, (sh.M + T - 1) / T);
         cfg.blockDim = dim3(128);
@@ -230,11 +266,27 @@ int main(int argc, char** argv) {
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages, tsync);
         cudaError_t e2 = cudaStreamSynchronize(s);
         if (e != cudaSuccess || e2 != cudaSuccess) {
             printf("%s: launch %s / %s\n", sh.name, cudaGetErrorString(e), cudaGetErrorString(e2));
             return 1;
+        }
+        {  // phases of one isolated launch
+            cudaDeviceSynchronize();
+            cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages, tsync);
+            cudaDeviceSynchronize();
+            static unsigned long long st[512][6];
+            cudaMemcpyFromSymbol(st, g_stamp, sizeof st);
+            const uint32_t nct = std::min(512u, cfg.gridDim.x * cfg.gridDim.y);
+            double ph[5] = {0};
+            unsigned long long t0 = ~0ull, t1 = 0;
+            for (uint32_t c = 0; c < nct; ++c) {
+                t0 = std::min(t0, st[c][0]); t1 = std::max(t1, st[c][5]);
+                for (int p = 0; p < 5; ++p) ph[p] += (double)(st[c][p + 1] - st[c][p]);
+            }
+            printf("%-10s phases (us, mean over %u CTAs): setup %.2f  loads-issued %.2f  mma-done %.2f  epilogue %.2f  teardown %.2f | span %.2f\n",
+                   sh.name, nct, ph[0] / nct / 1e3, ph[1] / nct / 1e3, ph[2] / nct / 1e3, ph[3] / nct / 1e3, ph[4] / nct / 1e3, (t1 - t0) / 1e3);
         }
         std::vector<uint16_t> O((size_t)sh.M * sh.N);
         cudaMemcpy(O.data(), dO, O.size() * 2, cudaMemcpyDeviceToHost);
@@ -253,7 +305,7 @@ int main(int argc, char** argv) {
         cudaGraph_t g;
         cudaGraphExec_t ge;
         cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
-        for (int i = 0; i < reps; ++i) cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages);
+        for (int i = 0; i < reps; ++i) cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages, tsync);
         cudaStreamEndCapture(s, &g);
         cudaGraphInstantiate(&ge, g, 0);
         cudaGraphLaunch(ge, s);
