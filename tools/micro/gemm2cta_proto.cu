@@ -54,7 +54,7 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __grid_constant__ CUtensorMap tmX, Args a, int stages, int teardown_sync) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, Args a, int stages, int teardown_sync) {
     extern __shared__ uint8_t raw[];
     STAMP(0);
     uint8_t* smem = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -82,30 +82,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
     const uint64_t kstride = (uint64_t)(a.n_pad / 8) * 1024;
     // warp 0 issues the copies lane-parallel: lane 0 arms the stages' barriers, then lane l issues copy l
     // of the stages in [st0, st1) (one thread issuing every copy back to back was the critical path)
+#ifdef DIRECT
+    // DIRECT: both CTAs' copies complete on the LEADER's barrier (cta_group::2 TMA), which expects the
+    // bytes of both halves; no relay
+    constexpr uint32_t kArmMul = 2;
+    const bool arms = rank == 0;
+#else
+    constexpr uint32_t kArmMul = 1;
+    const bool arms = true;
+#endif
     auto arm = [&](uint32_t st0, uint32_t st1) {
-        if (lane == 0)
+        if (lane == 0 && arms)
             for (uint32_t st = st0; st < st1; ++st) {
                 const uint32_t nsub = min((uint32_t)KSUB, nkt - st * KSUB);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&lfull[st % stages])), "r"(nsub * (WSUB + XSUB)) : "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&lfull[st % stages])), "r"(kArmMul * nsub * (WSUB + XSUB)) : "memory");
             }
         __syncwarp();
+    };
+    auto bar_of = [&](uint32_t s) -> uint32_t {
+#ifdef DIRECT
+        uint32_t r;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(su32(&lfull[s])));
+        return r;
+#else
+        return su32(&lfull[s]);
+#endif
     };
     auto load_w = [&](uint32_t st0, uint32_t st1) {
         for (uint32_t i = lane; i < (st1 - st0) * KSUB; i += 32) {
             const uint32_t st = st0 + i / KSUB, j = i % KSUB, kt = st * KSUB + j, s = st % stages;
             if (kt >= nkt) continue;
+#ifdef DIRECT
+            asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                             su32(smem + s * STAGE + j * WSUB)), "l"(&tmW), "r"(0), "r"((int)(kt * a.n_pad + w0)), "r"(bar_of(s)) : "memory");
+#else
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              su32(smem + s * STAGE + j * WSUB)), "l"(a.w + kt * kstride + (uint64_t)(w0 / 8) * 1024), "r"(WSUB),
                          "r"(su32(&lfull[s])) : "memory");
+#endif
         }
     };
     auto load_x = [&](uint32_t st0, uint32_t st1) {
         for (uint32_t i = lane; i < (st1 - st0) * KSUB; i += 32) {
             const uint32_t st = st0 + i / KSUB, j = i % KSUB, kt = st * KSUB + j, s = st % stages;
             if (kt >= nkt) continue;
+#ifdef DIRECT
+            asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                             su32(smem + s * STAGE + KSUB * WSUB + j * XSUB)), "l"(&tmX), "r"((int)(kt * 64)), "r"((int)(tb + rank * TH)),
+                         "r"(bar_of(s)) : "memory");
+#else
             asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
                              su32(smem + s * STAGE + KSUB * WSUB + j * XSUB)), "l"(&tmX), "r"((int)(kt * 64)), "r"((int)(tb + rank * TH)),
                          "r"(su32(&lfull[s])) : "memory");
+#endif
         }
     };
     // the weights of the stages in flight are requested before anything else (they depend on nothing),
@@ -114,7 +143,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
     if (warp == 0) {
         if (lane == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
         arm(0, pre);
-        load_w(0, pre);
+#ifndef DIRECT
+        load_w(0, pre);  // DIRECT: the peer may only signal the leader's barrier after the cluster barrier
+#endif
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(tslot)) : "memory");
@@ -127,6 +158,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
     STAMP(1);
 
     if (warp == 0) {  // producer (both CTAs): the tokens, then the rest of the ring
+#ifdef DIRECT
+        load_w(0, pre);
+#endif
         asm volatile("griddepcontrol.wait;" ::: "memory");
         load_x(0, pre);
         for (uint32_t st = pre; st < nst; ++st) {
@@ -137,6 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
             load_x(st, st + 1);
         }
         STAMP(2);
+#ifndef DIRECT
     } else if (warp == 1 && lane == 0 && rank == 1) {  // relay: my half of stage s has landed
         for (uint32_t st = 0; st < nst; ++st) {
             const uint32_t s = st % stages;
@@ -145,12 +180,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(&pfull[s])));
             asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
         }
+#endif
     } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer: M = 128 (64 per CTA), N = 32 (16 per CTA)
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(T >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         for (uint32_t st = 0; st < nst; ++st) {
             const uint32_t s = st % stages, nsub = min((uint32_t)KSUB, nkt - st * KSUB);
             mbar_wait(&lfull[s], (st / stages) & 1);
+#ifndef DIRECT
             mbar_wait(&pfull[s], (st / stages) & 1);
+#endif
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint64_t ad0 = desc_sw128(smem + s * STAGE), bd0 = desc_sw128(smem + s * STAGE + KSUB * WSUB);
             for (uint32_t j = 0; j < nsub; ++j)
@@ -254,6 +292,14 @@ int main(int argc, char** argv) {
             printf("tensor map failed\n");
             return 1;
         }
+        CUtensorMap tw;  // the pre-tiled weights as rows of 128 B (already swizzled: copied verbatim)
+        const cuuint64_t wd[2] = {64, (cuuint64_t)nkt * n_pad}, wsd[1] = {128};
+        const cuuint32_t wbox[2] = {64, (cuuint32_t)WR};
+        if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dW, wd, wsd, wbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            printf("weight tensor map failed\n");
+            return 1;
+        }
         Args a{dW, dB, dO, sh.M, sh.N, sh.K, n_pad};
         const int nst = (int)((nkt + KSUB - 1) / KSUB), stages = nst < MAXST_ ? nst : MAXST_;
         cudaLaunchConfig_t cfg{};
@@ -266,7 +312,7 @@ int main(int argc, char** argv) {
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages, tsync);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_g2, tm, tw, a, stages, tsync);
         cudaError_t e2 = cudaStreamSynchronize(s);
         if (e != cudaSuccess || e2 != cudaSuccess) {
             printf("%s: launch %s / %s\n", sh.name, cudaGetErrorString(e), cudaGetErrorString(e2));
@@ -274,7 +320,7 @@ int main(int argc, char** argv) {
         }
         {  // phases of one isolated launch
             cudaDeviceSynchronize();
-            cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages, tsync);
+            cudaLaunchKernelEx(&cfg, k_g2, tm, tw, a, stages, tsync);
             cudaDeviceSynchronize();
             static unsigned long long st[512][6];
             cudaMemcpyFromSymbol(st, g_stamp, sizeof st);
@@ -305,7 +351,7 @@ int main(int argc, char** argv) {
         cudaGraph_t g;
         cudaGraphExec_t ge;
         cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal);
-        for (int i = 0; i < reps; ++i) cudaLaunchKernelEx(&cfg, k_g2, tm, a, stages, tsync);
+        for (int i = 0; i < reps; ++i) cudaLaunchKernelEx(&cfg, k_g2, tm, tw, a, stages, tsync);
         cudaStreamEndCapture(s, &g);
         cudaGraphInstantiate(&ge, g, 0);
         cudaGraphLaunch(ge, s);
