@@ -112,6 +112,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
         for (uint32_t i = lane; i < (st1 - st0) * KSUB; i += 32) {
             const uint32_t st = st0 + i / KSUB, j = i % KSUB, kt = st * KSUB + j, s = st % stages;
             if (kt >= nkt) continue;
+// (measured: a plain cp.async.bulk whose mbarrier operand is the LEADER's barrier never completes it
+//  (the kernel hangs), so the weights need a tensor map, or the relay, in the 2-CTA design)
 #ifdef DIRECT
             asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
                              su32(smem + s * STAGE + j * WSUB)), "l"(&tmW), "r"(0), "r"((int)(kt * a.n_pad + w0)), "r"(bar_of(s)) : "memory");
