@@ -11,7 +11,7 @@ with Runtime(gpu_ids=[0], pool_bytes=8 << 30) as rt:
         spec = synth.build_model("bert-base", seed=200 + trial)
         mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
         x = spec.make_input()
-        time.sleep(1.0)  # let the GPU go idle
+        time.sleep(5.0)  # let the GPU go idle
         if warm:
             a = torch.randn(4096, 4096, device="cuda")
             t0 = time.time()
@@ -20,8 +20,8 @@ with Runtime(gpu_ids=[0], pool_bytes=8 << 30) as rt:
                 a = a / a.norm()
             torch.cuda.synchronize()
         d = []
-        for i in range(8):
+        for i in range(12):
             rt.evict(mid)
             d.append(rt.invoke(mid, x, gpu=0).stats["device_ms"])
-        print(f"trial {trial} warm_gpu={warm}: first 8 cold invokes {np.round(d, 3).tolist()}", flush=True)
+        print(f"trial {trial} warm_gpu={warm}: first 12 cold invokes {np.round(d, 3).tolist()}", flush=True)
         rt.unregister(mid)
