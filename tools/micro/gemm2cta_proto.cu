@@ -23,7 +23,11 @@
 #ifndef MAXST_
 #define MAXST_ 5
 #endif
-constexpr int T = 32, TH = T / 2, WR = 64, KSUB = KSUB_;
+#ifndef T_
+#define T_ 32
+#endif
+constexpr int T = T_, TH = T / 2, WR = 64, KSUB = KSUB_;  // T tokens per pair tile (16 .. 128)
+constexpr int TCOLS = TH < 32 ? 32 : TH;                   // TMEM columns (accumulator: T/2 per lane half)
 __device__ unsigned long long g_stamp[512][6];  // per-CTA %globaltimer phase stamps (isolated launch)
 __device__ __forceinline__ unsigned long long gtime() { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 #define STAMP(i) do { if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 512) g_stamp[blockIdx.x + gridDim.x * blockIdx.y][i] = gtime(); } while (0)
@@ -150,7 +154,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
 #endif
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(tslot)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "n"(TCOLS) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -212,29 +216,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
     STAMP(3);
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    uint32_t r[16];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-                   "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                 : "r"(tmem + ((warp * 32u) << 16)));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const uint32_t m = (warp & 1) * 32 + lane, n = w0 + m, tok0 = tb + (warp >> 1) * 16;
-    if (n < a.N) {
-        const float bias = __uint_as_float((uint32_t)a.bias[n] << 16);
-        for (int c = 0; c < 16; ++c) {
-            const uint32_t t = tok0 + c;
-            if (t < a.M) {
-                const float v = __uint_as_float(r[c]) + bias;
-                const uint32_t u = __float_as_uint(v);
-                a.out[(uint64_t)t * a.N + n] = (uint16_t)((u + 0x7FFF + ((u >> 16) & 1)) >> 16);
+    const uint32_t m = (warp & 1) * 32 + lane, n = w0 + m, tok0 = tb + (warp >> 1) * TH;
+    const float bias = n < a.N ? __uint_as_float((uint32_t)a.bias[n] << 16) : 0.0f;
+#pragma unroll
+    for (int c0 = 0; c0 < TH; c0 += 16) {
+        uint32_t r[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+                       "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                     : "r"(tmem + ((warp * 32u) << 16) + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (n < a.N)
+            for (int c = 0; c < 16 && c0 + c < TH; ++c) {
+                const uint32_t t = tok0 + c0 + c;
+                if (t < a.M) {
+                    const float v = __uint_as_float(r[c]) + bias;
+                    const uint32_t u = __float_as_uint(v);
+                    a.out[(uint64_t)t * a.N + n] = (uint16_t)((u + 0x7FFF + ((u >> 16) & 1)) >> 16);
+                }
             }
-        }
     }
     __syncthreads();
     STAMP(4);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (teardown_sync) cluster_sync();  // (both CTAs have seen `done`: no MMA can still target either TMEM)
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS) : "memory");
     STAMP(5);
 }
 
