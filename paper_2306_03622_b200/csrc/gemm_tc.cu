@@ -515,6 +515,188 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     if (mc > 1 || a.cz > 1) cluster_sync();  // no CTA leaves while a peer may still read / target its smem
 }
 
+// ---- K3b: the 2-CTA (cta_group::2) swap-AB GEMM for batch-1 transformer linears ---------------
+// out[t][n] = act(Σ_k A[t][k]·W[n][k] + b[n] + res[t][n]) over a CTA PAIR: the pair owns 128 weight rows
+// (the UMMA M operand, 64 per CTA) and T tokens (the N operand, T/2 per CTA); each CTA holds only its
+// halves of every K sub-tile in shared memory and the leader's tcgen05.mma.cta_group::2 reads the
+// peer's, so an SM receives half the operand bytes of a 1-CTA tile (per-SM operand
+// bytes set the batch-1 GEMM time).  Both CTAs' TMA loads complete on the LEADER's full barrier
+// (cp.async.bulk.tensor.cta_group::2), which expects both halves' bytes; the weights come through one
+// tensor map over the GPU's whole weight pool (rows of 128 B of the pre-tiled layout, copied verbatim),
+// addressed by the row of the layer's extent, so no per-extent map is needed.  The leader commits each
+// stage to both CTAs' empty barriers (multicast).  TMEM layout of the pair's M=128 accumulator in each
+// CTA: lane m + 64·(token ≥ T/2), column token mod T/2 (CUTLASS's 2SM "2x2" atom).
+constexpr int kG2WR = 64, kG2KSub = 4;
+template <int TT>
+struct G2Cfg {
+    static constexpr int TH = TT / 2;
+    static constexpr uint32_t kW = kG2WR * 128, kX = TH * 128, kStage = kG2KSub * (kW + kX);
+    static constexpr int kTmemCols = TH < 32 ? 32 : TH;
+    __host__ static int max_stages() { const int f = (int)((200 * 1024) / kStage); return f > 5 ? 5 : f; }
+};
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t par) {
+    uint32_t ok = 0;
+    do {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(smem_u32(b)), "r"(par) : "memory");
+    } while (!ok);
+}
+
+template <int TT>
+__global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
+                                               const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
+    using C = G2Cfg<TT>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * C::kStage);
+    uint64_t* empty = full + stages;
+    uint64_t* done = empty + stages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    const uint32_t rank = cluster_ctarank(), warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t w0 = (blockIdx.x >> 1) * 128 + rank * kG2WR;  // this CTA's weight rows (tile columns)
+    const uint32_t tb = blockIdx.y * TT;                          // the pair's tokens (tile rows)
+    const uint32_t nkt = a.K / kBK, nst = (nkt + kG2KSub - 1) / kG2KSub;
+    const DevDesc dd = *d;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(C::kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cluster_sync();  // both CTAs' barriers exist before any copy completes on the leader's
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        // producer (both CTAs), lane-parallel: lane 0 of the LEADER arms a stage for both halves' bytes
+        uint32_t lead[8];  // the leader's full barriers, in the cluster window
+        for (int s = 0; s < stages && s < 8; ++s)
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead[s]) : "r"(smem_u32(&full[s])));
+        if (lane == 0) wait_ready_thread(w);
+        __syncwarp();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        // row of this CTA's first weight row of k tile 0 in the pool-wide map (128-B rows)
+        const uint64_t wrow = (uint64_t)(weight_ptr(dd, a.w_off) - reinterpret_cast<const uint8_t*>(a.wpool)) / 128 + w0;
+        auto arm = [&](uint32_t st0, uint32_t st1) {
+            if (lane == 0 && rank == 0)
+                for (uint32_t st = st0; st < st1; ++st) {
+                    const uint32_t nsub = min((uint32_t)kG2KSub, nkt - st * kG2KSub);
+                    mbar_expect_tx(&full[st % stages], 2 * nsub * (C::kW + C::kX));
+                }
+            __syncwarp();
+        };
+        auto load = [&](uint32_t st0, uint32_t st1, bool wts) {
+            for (uint32_t i = lane; i < (st1 - st0) * kG2KSub; i += 32) {
+                const uint32_t st = st0 + i / kG2KSub, j = i % kG2KSub, kt = st * kG2KSub + j, s = st % stages;
+                if (kt >= nkt) continue;
+                if (wts)
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                        "%3}], [%4];" ::"r"(smem_u32(smem + s * C::kStage + j * C::kW)),
+                        "l"(&tmW), "r"(0), "r"((int)(wrow + (uint64_t)kt * a.n_pad)), "r"(lead[s])
+                        : "memory");
+                else
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                        "%3}], [%4];" ::"r"(smem_u32(smem + s * C::kStage + kG2KSub * C::kW + j * C::kX)),
+                        "l"(&tmA), "r"((int)(kt * kBK)), "r"((int)(tb + rank * C::TH)), "r"(lead[s])
+                        : "memory");
+            }
+        };
+        const uint32_t pre = min((uint32_t)stages, nst);
+        arm(0, pre);
+        load(0, pre, true);  // weights first: they do not depend on the predecessor
+        pdl_wait();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        load(0, pre, false);
+        for (uint32_t st = pre; st < nst; ++st) {
+            if (lane == 0) mbar_wait_cluster(&empty[st % stages], ((st / stages) - 1) & 1);
+            __syncwarp();
+            arm(st, st + 1);
+            load(st, st + 1, true);
+            load(st, st + 1, false);
+        }
+    } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer: M = 128 (64 per CTA), N = TT (TT/2 per CTA)
+        constexpr uint32_t idesc = umma_idesc_bf16(128, TT);
+        for (uint32_t st = 0; st < nst; ++st) {
+            const uint32_t s = st % stages, nsub = min((uint32_t)kG2KSub, nkt - st * kG2KSub);
+            mbar_wait_cluster(&full[s], (st / stages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad0 = umma_desc_sw128(smem + s * C::kStage), bd0 = umma_desc_sw128(smem + s * C::kStage + kG2KSub * C::kW);
+            for (uint32_t j = 0; j < nsub; ++j)
+#pragma unroll
+                for (uint32_t kk = 0; kk < kBK / 16; ++kk) {
+                    const uint64_t ad = ad0 + ((j * C::kW + kk * 32) >> 4), bd = bd0 + ((j * C::kX + kk * 32) >> 4);
+                    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem),
+                                 "l"(ad), "l"(bd), "r"(idesc), "r"((uint32_t)((st | j | kk) != 0)));
+                }
+            asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                             smem_u32(&empty[s])), "h"((uint16_t)3) : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         smem_u32(done)), "h"((uint16_t)3) : "memory");
+    }
+    __syncwarp();
+    // epilogue: this CTA's 64 weight rows x the pair's TT tokens, straight from TMEM
+    mbar_wait_cluster(done, 0);
+    pdl_trigger();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pdl_wait();  // activations (residual in, output out) only after the predecessor
+    const uint32_t n = w0 + (warp & 1) * 32 + lane, tok0 = tb + (warp >> 1) * C::TH;
+    const float bias = a.has_bias && n < a.N ? bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off))[n]) : 0.0f;
+#pragma unroll
+    for (int c0 = 0; c0 < C::TH; c0 += 16) {
+        uint32_t r[16];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+                       "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                     : "r"(tmem + ((warp * 32u) << 16) + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (n < a.N)
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const uint32_t t = tok0 + c0 + c;
+                if (c0 + c >= C::TH || t >= a.M) break;
+                float v = __uint_as_float(r[c]) + bias;
+                if (a.res)
+                    v += a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[(uint64_t)t * a.ld_res + n])
+                                    : reinterpret_cast<const float*>(a.res)[(uint64_t)t * a.ld_res + n];
+                v = apply_act(a.act, v);
+                const uint64_t oi = (uint64_t)t * a.ld_out + n;
+                if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
+                else reinterpret_cast<float*>(a.out)[oi] = v;
+                if (a.out2) a.out2[oi] = f32_to_bf16(v);
+            }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    // both CTAs saw `done`: no MMA can still target either TMEM, and no copy or MMA touches the peer's
+    // shared memory any more
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols) : "memory");
+}
+
+template <int TT>
+static void launch_g2(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const CUtensorMap* tmW, const GemmArgs& a) {
+    using C = G2Cfg<TT>;
+    const int nst = (int)((a.K / kBK + kG2KSub - 1) / kG2KSub), ms = C::max_stages();
+    const int stages = nst < ms ? nst : ms;
+    const dim3 grid((a.n_pad + 127) / 128 * 2, (a.M + TT - 1) / TT);
+    launch_pdl_cluster(PDL_GEMM, k_gemm2<TT>, grid, dim3(128), stages * C::kStage + 2048, s, dim3(2, 1, 1), *tmA, *tmW, d, w, a,
+                       stages);
+}
+
 template <int BN>
 static void launch_bn(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {
     using C = Cfg<BN>;
@@ -532,6 +714,10 @@ void init_gemm_attrs() {  // once per device at fsw_init (kernel preloading, PAP
     cudaFuncSetAttribute(k_gemm<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_gemm<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm2<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm2<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
 template <int BN>
@@ -566,7 +752,16 @@ int gemm_max_active_clusters(int bn, int cz) {
     }
 }
 
-void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a) {
+void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a, const CUtensorMap* tmW) {
+    if (a.pair_t) {
+        switch (a.pair_t) {
+            case 16: launch_g2<16>(s, d, w, tmA, tmW, a); break;
+            case 32: launch_g2<32>(s, d, w, tmA, tmW, a); break;
+            case 64: launch_g2<64>(s, d, w, tmA, tmW, a); break;
+            default: launch_g2<128>(s, d, w, tmA, tmW, a); break;
+        }
+        return;
+    }
     switch (a.bn) {
         case 16: launch_bn<16>(s, d, w, tmA, a); break;
         case 32: launch_bn<32>(s, d, w, tmA, a); break;
@@ -595,6 +790,27 @@ bool make_tmap_act(CUtensorMap* map, const void* base, uint64_t rows, uint64_t c
     const cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The GPU's whole weight pool as rows of 128 B (the pre-tiled weight layout, copied verbatim by the
+// 2-CTA GEMM: no swizzle on the copy, the bytes already are in SWIZZLE_128B order), 64-row boxes.
+bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes) {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            return false;
+        fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    if (bytes / 128 >= (1ull << 31)) return false;  // TMA row coordinates are int32
+    const cuuint64_t dims[2] = {64, bytes / 128};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kG2WR};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -306,7 +306,7 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
             case K_EMBED: launch_embed(s, d, w, x.embed); break;
             case K_LN: launch_layernorm(s, d, w, x.ln); break;
             case K_GEMV: launch_gemv(s, d, w, x.gemv); break;
-            case K_GEMM: launch_gemm(s, d, w, &x.tmap, x.gemm); break;
+            case K_GEMM: launch_gemm(s, d, w, &x.tmap, x.gemm, &g.wmap); break;
             case K_ATTN: launch_attention(s, x.attn); break;
             case K_IM2COL: launch_im2col(s, x.im2col); break;
             case K_MAXPOOL: launch_maxpool(s, x.pool); break;

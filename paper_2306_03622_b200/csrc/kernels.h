@@ -182,8 +182,15 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // cluster split-K: the `splits` CTAs of one output tile form a (1, 1, cz) cluster (cz == splits <= 8)
     // and reduce their partial tiles over distributed shared memory instead of `part` / `ctr`
     uint32_t cz;
+    // 2-CTA swap-AB GEMM (k_gemm2): pair_t = tokens per CTA pair (16, 32, 64 or 128), 0 = k_gemm.  The
+    // A tensor map's box is then pair_t / 2 rows; weights come through the pool-wide map (wpool = the
+    // GPU's pool base, the map's origin)
+    uint32_t pair_t;
+    const void* wpool;
 };
-void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a);
+void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a,
+                 const CUtensorMap* tmW = nullptr);
+bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes);
 
 struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; };
 void launch_attention(cudaStream_t s, const AttnArgs& a);

@@ -218,10 +218,39 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     a.out_bf16 = so.dtype == FSW_DT_BF16;
                     a.ld_out = a.N;
                     a.out2 = shadow(L.out);
-                    set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
                     const void* abase = si.dtype == FSW_DT_BF16 ? (const void*)sptr(L.in0) : (const void*)shadow(L.in0);
-                    if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), 128 / a.mc))
-                        return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                    // Opt-in (FSW_GEMM_2CTA=1): the 2-CTA swap-AB GEMM for the wide batch-1 transformer linears
+                    // (<= 128 tokens, K <= 1600, N >= 768), the token tile putting the number of CTA pairs
+                    // nearest 40.  Back to back on L2-resident weights it beat k_gemm by 14-20 %
+                    // (profiles/r01/gemm2cta_proto_tokens.txt), but inside the invoke graph, weights from
+                    // HBM, it is slower (resident BERT-base 0.702 vs 0.586 ms, profiles/r01/gemm2cta_in_graph.txt),
+                    // so k_gemm stays the default.
+                    static const bool use2 = getenv("FSW_GEMM_2CTA") != nullptr;
+                    uint32_t pt = 0;
+                    if (use2 && g.wmap_ok && a.M <= 128 && a.K / 64 <= 25 && a.N >= 768) {
+                        const uint32_t ntile = (a.n_pad + 127) / 128;
+                        long best = 1 << 30;
+                        for (uint32_t t : {16u, 32u, 64u, 128u}) {
+                            const long pairs = (long)ntile * ((a.M + t - 1) / t), dist = pairs > 40 ? pairs - 40 : 40 - pairs;
+                            if (dist < best) best = dist, pt = t;
+                        }
+                    }
+                    if (pt) {
+                        a.pair_t = pt;
+                        a.wpool = g.pool;
+                        a.bn = 128;
+                        a.m_rows = pt;
+                        a.splits = 1;
+                        a.kt_per = a.K / 64;
+                        a.mc = 1;
+                        a.cz = 0;
+                        if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), pt / 2))
+                            return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                    } else {
+                        set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
+                        if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), 128 / a.mc))
+                            return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                    }
                 }
                 break;
             }

@@ -186,6 +186,8 @@ struct Gpu {
     uint32_t* gemm_ctr = nullptr;       // split-K tile arrival counters (self-resetting)
     uint8_t* pool = nullptr;
     uint64_t pool_bytes = 0;
+    CUtensorMap wmap;            // the pool as 128-B rows: the 2-CTA GEMM's weight map (k_gemm2)
+    bool wmap_ok = false;
     fsw_arena* arena = nullptr;
     uint8_t* ws = nullptr;
     uint64_t ws_bytes = 0;

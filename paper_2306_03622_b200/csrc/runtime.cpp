@@ -130,6 +130,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     want = std::min<uint64_t>(want, (uint64_t)(free_b * 0.6));
     g.pool_bytes = want / (64 << 10) * (64 << 10);
     CU(cudaMalloc(&g.pool, g.pool_bytes));
+    g.wmap_ok = make_tmap_pool(&g.wmap, g.pool, g.pool_bytes);
     g.arena = fsw_arena_create(g.pool_bytes, 64 << 10);
     g.ws_bytes = c->cfg.workspace_bytes_per_gpu ? c->cfg.workspace_bytes_per_gpu : (512ull << 20);
     CU(cudaMalloc(&g.ws, g.ws_bytes));
