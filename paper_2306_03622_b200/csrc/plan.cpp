@@ -230,8 +230,9 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     if (use2 && g.wmap_ok && a.M <= 128 && a.K / 64 <= 25 && a.N >= 768) {
                         const uint32_t ntile = (a.n_pad + 127) / 128;
                         long best = 1 << 30;
+                        static const long target = getenv("FSW_GEMM_2CTA_PAIRS") ? atol(getenv("FSW_GEMM_2CTA_PAIRS")) : 40;
                         for (uint32_t t : {16u, 32u, 64u, 128u}) {
-                            const long pairs = (long)ntile * ((a.M + t - 1) / t), dist = pairs > 40 ? pairs - 40 : 40 - pairs;
+                            const long pairs = (long)ntile * ((a.M + t - 1) / t), dist = pairs > target ? pairs - target : target - pairs;
                             if (dist < best) best = dist, pt = t;
                         }
                     }
