@@ -535,13 +535,6 @@ struct G2Cfg {
     __host__ static int max_stages() { const int f = (int)((200 * 1024) / kStage); return f > 5 ? 5 : f; }
 };
 
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t par) {
-    uint32_t ok = 0;
-    do {
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(ok) : "r"(smem_u32(b)), "r"(par) : "memory");
-    } while (!ok);
-}
 
 template <int TT>
 __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
@@ -621,7 +614,7 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
         asm volatile("fence.proxy.async.global;" ::: "memory");
         load(0, pre, false);
         for (uint32_t st = pre; st < nst; ++st) {
-            if (lane == 0) mbar_wait_cluster(&empty[st % stages], ((st / stages) - 1) & 1);
+            if (lane == 0) mbar_wait(&empty[st % stages], ((st / stages) - 1) & 1);
             __syncwarp();
             arm(st, st + 1);
             load(st, st + 1, true);
@@ -631,7 +624,7 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
         constexpr uint32_t idesc = umma_idesc_bf16(128, TT);
         for (uint32_t st = 0; st < nst; ++st) {
             const uint32_t s = st % stages, nsub = min((uint32_t)kG2KSub, nkt - st * kG2KSub);
-            mbar_wait_cluster(&full[s], (st / stages) & 1);
+            mbar_wait(&full[s], (st / stages) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint64_t ad0 = umma_desc_sw128(smem + s * C::kStage), bd0 = umma_desc_sw128(smem + s * C::kStage + kG2KSub * C::kW);
             for (uint32_t j = 0; j < nsub; ++j)
@@ -648,8 +641,10 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
                          smem_u32(done)), "h"((uint16_t)3) : "memory");
     }
     __syncwarp();
-    // epilogue: this CTA's 64 weight rows x the pair's TT tokens, straight from TMEM
-    mbar_wait_cluster(done, 0);
+    // epilogue: this CTA's 64 weight rows x the pair's TT tokens, straight from TMEM.  (Barrier waits
+    // are cta-scope, as for the 1-CTA kernel: an .acquire.cluster poll executes CCTL.IVALL, an L1
+    // invalidate, on every try; it was the top warp stall of the first in-graph ncu capture.)
+    mbar_wait(done, 0);
     pdl_trigger();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     pdl_wait();  // activations (residual in, output out) only after the predecessor

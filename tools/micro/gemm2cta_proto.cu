@@ -38,6 +38,7 @@ struct Args {
     const uint16_t* bias;
     uint16_t* out;
     uint32_t M, N, K, n_pad;
+    uint32_t wrow0;  // row of the weights in the weight map (0 unless POOL_GB places them in a big buffer)
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -120,7 +121,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128) k_g2(const __gr
 //  (the kernel hangs), so the weights need a tensor map, or the relay, in the 2-CTA design)
 #ifdef DIRECT
             asm volatile("cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                             su32(smem + s * STAGE + j * WSUB)), "l"(&tmW), "r"(0), "r"((int)(kt * a.n_pad + w0)), "r"(bar_of(s)) : "memory");
+                             su32(smem + s * STAGE + j * WSUB)), "l"(&tmW), "r"(0), "r"((int)(a.wrow0 + kt * a.n_pad + w0)), "r"(bar_of(s)) : "memory");
 #else
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              su32(smem + s * STAGE + j * WSUB)), "l"(a.w + kt * kstride + (uint64_t)(w0 / 8) * 1024), "r"(WSUB),
@@ -285,7 +286,14 @@ int main(int argc, char** argv) {
         uint16_t *dX, *dB, *dO;
         uint8_t* dW;
         cudaMalloc(&dX, X.size() * 2);
-        cudaMalloc(&dW, Wt.size() * 2);
+        uint8_t* big = nullptr;
+        const uint64_t big_bytes = getenv("POOL_GB") ? (uint64_t)atoi(getenv("POOL_GB")) << 30 : 0;
+        if (big_bytes) {  // weights deep inside a pool-sized allocation, the map spanning all of it (libfsw's layout)
+            cudaMalloc(&big, big_bytes);
+            dW = big + big_bytes / 2 / 1024 * 1024;
+        } else {
+            cudaMalloc(&dW, Wt.size() * 2);
+        }
         cudaMalloc(&dB, B.size() * 2);
         cudaMalloc(&dO, (size_t)sh.M * sh.N * 2);
         cudaMemcpy(dX, X.data(), X.size() * 2, cudaMemcpyHostToDevice);
@@ -301,14 +309,15 @@ int main(int argc, char** argv) {
             return 1;
         }
         CUtensorMap tw;  // the pre-tiled weights as rows of 128 B (already swizzled: copied verbatim)
-        const cuuint64_t wd[2] = {64, (cuuint64_t)nkt * n_pad}, wsd[1] = {128};
+        const uint64_t wrow0 = big_bytes ? (uint64_t)(dW - big) / 128 : 0;
+        const cuuint64_t wd[2] = {64, big_bytes ? big_bytes / 128 : (cuuint64_t)nkt * n_pad}, wsd[1] = {128};
         const cuuint32_t wbox[2] = {64, (cuuint32_t)WR};
-        if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dW, wd, wsd, wbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, big_bytes ? (void*)big : (void*)dW, wd, wsd, wbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
             printf("weight tensor map failed\n");
             return 1;
         }
-        Args a{dW, dB, dO, sh.M, sh.N, sh.K, n_pad};
+        Args a{dW, dB, dO, sh.M, sh.N, sh.K, n_pad, (uint32_t)wrow0};
         const int nst = (int)((nkt + KSUB - 1) / KSUB), stages = nst < MAXST_ ? nst : MAXST_;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(n_pad / 128 * 2, (sh.M + T - 1) / T);
@@ -379,7 +388,7 @@ int main(int argc, char** argv) {
         cudaGraphExecDestroy(ge);
         cudaGraphDestroy(g);
         }
-        cudaFree(dX); cudaFree(dW); cudaFree(dB); cudaFree(dO);
+        cudaFree(dX); cudaFree(big ? (void*)big : (void*)dW); cudaFree(dB); cudaFree(dO);
     }
     printf("last error: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
