@@ -551,6 +551,10 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
     const uint32_t tb = blockIdx.y * TT;                          // the pair's tokens (tile rows)
     const uint32_t nkt = a.K / kBK, nst = (nkt + kG2KSub - 1) / kG2KSub;
     const DevDesc dd = *d;
+    // issued now so their latency hides under the setup: the weight row of this CTA in the pool map, the
+    // bias of this thread's epilogue row
+    const uint64_t wrow = (uint64_t)(weight_ptr(dd, a.w_off) - reinterpret_cast<const uint8_t*>(a.wpool)) / 128 + w0;
+    const uint32_t n_ep = w0 + (warp & 1) * 32 + lane;
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
@@ -579,8 +583,6 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
         if (lane == 0) wait_ready_thread(w);
         __syncwarp();
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        // row of this CTA's first weight row of k tile 0 in the pool-wide map (128-B rows)
-        const uint64_t wrow = (uint64_t)(weight_ptr(dd, a.w_off) - reinterpret_cast<const uint8_t*>(a.wpool)) / 128 + w0;
         auto arm = [&](uint32_t st0, uint32_t st1) {
             if (lane == 0 && rank == 0)
                 for (uint32_t st = st0; st < st1; ++st) {
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
     pdl_trigger();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     pdl_wait();  // activations (residual in, output out) only after the predecessor
-    const uint32_t n = w0 + (warp & 1) * 32 + lane, tok0 = tb + (warp >> 1) * C::TH;
+    const uint32_t n = n_ep, tok0 = tb + (warp >> 1) * C::TH;
     const float bias = a.has_bias && n < a.N ? bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off))[n]) : 0.0f;
 #pragma unroll
     for (int c0 = 0; c0 < C::TH; c0 += 16) {
