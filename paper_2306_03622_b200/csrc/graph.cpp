@@ -348,16 +348,26 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
     // engine also reads the invoke descriptor and the control block.  The input (up to 300 KB for
     // ResNet-50) is copied after the fork, overlapping the swap.
     const bool dma_cold = ic.cold && !ic.striped && ic.engine == FSW_ENGINE_DMA;
-    if (dma_cold) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
+    // DMAZ: the copy engine also needs only its group counters reset; the decode kernel waits for the
+    // rest of the setup (descriptor, control block, ready counters) through evset
+    const bool dmaz_cold = ic.cold && !ic.striped && ic.engine == FSW_ENGINE_DMAZ;
+    if (dma_cold || dmaz_cold) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
+    if (dmaz_cold) {
+        cudaEventRecord(g.evfork, sx);
+        cudaStreamWaitEvent(sc, g.evfork, 0);
+    }
     if (!dma_cold) cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr, cudaMemcpyHostToDevice, sx);
     // striped: the counters and the control block are reset before the sources start (outside)
     if (!ic.striped && !dma_cold) cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
     if (ic.cold && ic.striped && !ic.no_overlap && ic.local_ctas) launch_gate(sx, g.ctl, ic.local_ctas);
     if (ic.cold && !ic.striped) {
         if (engine_bytes_ready(ic.engine)) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
-        if (ic.engine == FSW_ENGINE_DMAZ) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
-        cudaEventRecord(g.evfork, sx);
-        cudaStreamWaitEvent(sc, g.evfork, 0);
+        if (dmaz_cold) {
+            cudaEventRecord(g.evset, sx);
+        } else {
+            cudaEventRecord(g.evfork, sx);
+            cudaStreamWaitEvent(sc, g.evfork, 0);
+        }
         cudaEventRecordWithFlags(g.evs0, sc, cudaEventRecordExternal);
         const DevDesc* desc = reinterpret_cast<const DevDesc*>(g.dstage);
         if (ic.engine == FSW_ENGINE_SM) {
@@ -378,7 +388,10 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             const bool serial = ic.no_overlap;
             cudaStream_t sdec = serial ? sc : g.sz;
             cudaEventRecord(g.evd[0], sc);
-            if (!serial) cudaStreamWaitEvent(g.sz, g.evd[0], 0);
+            if (!serial) {
+                cudaStreamWaitEvent(g.sz, g.evd[0], 0);
+                cudaStreamWaitEvent(g.sz, g.evset, 0);
+            }
             for (uint32_t j = 1; j < ic.zstreams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
             auto decode = [&]() {
                 launch_swapz(sdec, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
@@ -396,6 +409,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
                 cudaStreamWaitEvent(sc, g.evd[j], 0);
             }
             if (serial) {
+                cudaStreamWaitEvent(sc, g.evset, 0);  // the decode reads the descriptor and ready counters
                 decode();
             } else {
                 cudaEventRecord(g.evz, g.sz);

@@ -199,6 +199,7 @@ struct Gpu {
     uint32_t zstage_gen = 0;     // bumped on every reallocation (graphs bake the address)
     cudaStream_t sz = nullptr;   // DMAZ: decode-kernel stream
     cudaEvent_t evz = nullptr;   // DMAZ: join of the decode stream
+    cudaEvent_t evset = nullptr; // DMAZ: the layer stream's setup (descriptor, counters) is done
     uint8_t* dstage = nullptr;   // device: [DevDesc | pad | input]
     uint8_t* hstage = nullptr;   // pinned: same layout
     uint8_t* hout = nullptr;     // pinned, mapped: output (written by k_finish)

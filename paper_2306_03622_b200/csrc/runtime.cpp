@@ -113,6 +113,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     g.sd[0] = g.sc;
     CU(cudaStreamCreateWithFlags(&g.sz, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&g.evz, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&g.evset, cudaEventDisableTiming));
     for (int j = 1; j < kMaxWaitSrc; ++j) CU(cudaStreamCreateWithFlags(&g.sd[j], cudaStreamNonBlocking));
     for (int j = 0; j < kMaxWaitSrc; ++j) CU(cudaEventCreateWithFlags(&g.evd[j], cudaEventDisableTiming));
     CU(cudaMalloc(&g.progress, 128 * kMaxWaitSrc));
@@ -275,6 +276,7 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFree(g.zstage);
         cudaStreamDestroy(g.sz);
         cudaEventDestroy(g.evz);
+        cudaEventDestroy(g.evset);
         cudaFreeHost(g.hstage);
         cudaFreeHost(g.hout);
         cudaFreeHost(g.hctl);
