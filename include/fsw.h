@@ -60,6 +60,13 @@ typedef enum {
 #define FSW_NO_PEER_SWAP 0x10u /* never swap from another GPU's resident copy (Alg. 1 case 2 off)  */
 #define FSW_HOST_ONLY    0x8u /* no GPU: registration / host-store / allocator logic only (tests);
                                  invoke returns FSW_ECUDA                                       */
+#define FSW_DEBUG_POISON 0x20u /* test mode (also set by the environment variable FSW_DEBUG_POISON=1 at
+                                 fsw_init): before every cold invoke, fill the extents the swap will
+                                 write (prefix + suffix) and the DMAZ staging buffer with a per-invoke
+                                 32-bit pattern, and before every invoke the model's activation
+                                 workspace, so a byte the swap (or a layer kernel) fails to write can
+                                 never pass as the stale correct byte of an earlier invoke.  Costs one
+                                 HBM fill per invoke; off in the bench.                         */
 
 typedef struct {
     uint32_t n_gpus;                  /* GPUs in the pool; 0 = all visible devices           */
@@ -101,7 +108,7 @@ typedef struct {
  *        group a stream memory write (no SM) bumps that stream's group counter.               */
 enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SMZ = 3, FSW_ENGINE_DMAZ = 4 };
 /* Link-coded engines (models registered with FSW_REG_LINK_CODE).  The host link carries
- * the model's exponent-coded store (lossless, ~0.71 of the bytes) and a kernel decodes it into the
+ * the model's exponent-coded store (lossless, 0.68 of the bytes with format v4 on the synthetic weights) and a kernel decodes it into the
  * extent, releasing each decoded piece's bytes on its layer's counter (the SM protocol):
  *   SMZ : persistent CTAs stream coded pieces zero-copy from the mapped coded store with TMA bulk copies
  *         into a shared-memory ring and decode them from there;
@@ -156,7 +163,7 @@ typedef struct { uint32_t op, first_ref, n_refs; int32_t in0, in1, out; int32_t 
 #define FSW_REG_LINK_CODE 0x2u /* also build the exponent-coded copy of the store (pinned, mapped) that
                                   the SMZ / DMAZ engines move over the host link (format
                                   at fsw_coded_piece below).  Lossless: the extent receives the store's
-                                  bytes bit-exactly.  Costs ~0.71x the store in extra host memory.  */
+                                  bytes bit-exactly.  Costs ~0.68x the store in extra host memory.  */
 
 typedef struct {
     const char* name;
@@ -285,6 +292,34 @@ typedef struct {
 } fsw_pool_stats;
 fsw_status fsw_pool_stats_get(fsw_ctx* ctx, int32_t gpu, fsw_pool_stats* out);
 fsw_status fsw_n_gpus(fsw_ctx* ctx, uint32_t* n);
+
+/* Fault injection (tests: negative controls of the bit-exact and litmus checks).  kind:
+ *   FSW_FAULT_NONE       : clear;
+ *   FSW_FAULT_DROP_PIECE : the swap kernels (SM, SMZ, DMAZ decode; every source of a striped swap)
+ *                          skip the stores of the piece they claim as number `index` but still
+ *                          release its bytes on the layer counter;
+ *   FSW_FAULT_DROP_GROUP : the copy-engine engines (DMA, DMAZ) skip copy group `index` but still
+ *                          publish its completion.
+ * Process-wide on the device side (every pool GPU); cached invoke graphs are rebuilt.  EINVAL on
+ * an unknown kind.                                                                            */
+enum { FSW_FAULT_NONE = 0, FSW_FAULT_DROP_PIECE = 1, FSW_FAULT_DROP_GROUP = 2 };
+fsw_status fsw_debug_set_fault(fsw_ctx* ctx, uint32_t kind, uint32_t index);
+
+/* Readiness-protocol litmus test (DESIGN.md §5 "Memory ordering"; the correctness claim of
+ * PAPER.md:519 under the layer overlap of PAPER.md:588-590).  Runs `iters` iterations on pool GPU
+ * `gpu` of: poison a scratch extent (and the DMAZ staging buffer), reset the counters, then run the
+ * swap engine `engine` (FSW_ENGINE_SM / DMA / SMZ / DMAZ; `ctas` swap CTAs for the kernel engines)
+ * as the producer of model `model_id`'s store into that extent, CONCURRENTLY with `ctas` consumer
+ * CTAs that take the layers round-robin and, per layer, do exactly what a layer kernel does before
+ * reading weights — one thread acquires the layer's counter(s) (wait_ready), executes
+ * fence.proxy.async.global and issues cp.async.bulk copies of the layer region into shared memory —
+ * and compare every 16-byte word with the store.  *bad_words = words that differed (summed over all
+ * iterations), *checked_bytes = bytes compared (= iters x store bytes when nothing timed out).
+ * The model must have no invoke in flight (EBUSY); ENOMEM if the pool has no room for the scratch
+ * extent; ETIMEOUT if a consumer's spin hit the watchdog; EINVAL for a bad engine / ctas (1..1024)
+ * or a coded engine on a model that is not link-coded.                                          */
+fsw_status fsw_debug_litmus(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint32_t engine, uint32_t ctas, uint32_t iters,
+                            uint64_t* bad_words, uint64_t* checked_bytes);
 
 /* Debug / test read-back (copies into caller host memory). */
 fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, void* dst, uint64_t cap);

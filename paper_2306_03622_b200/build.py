@@ -20,7 +20,7 @@ SO = os.path.join(PKG, "libfsw.so")
 BUILD = os.path.join(PKG, "_build")
 
 CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu"]
-CXX_SOURCES = ["runtime.cpp", "store.cpp", "plan.cpp", "graph.cpp", "invoke.cpp", "sched.cpp"]
+CXX_SOURCES = ["runtime.cpp", "store.cpp", "plan.cpp", "graph.cpp", "invoke.cpp", "sched.cpp", "litmus.cpp"]
 HEADERS = ["kernels.h", "device.cuh", "policy.h", "rt_internal.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -315,8 +315,7 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
     }
 }
 
-typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-static PFN_writeValue32 get_write_value32() {
+PFN_writeValue32 get_write_value32() {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess) return nullptr;
@@ -399,9 +398,11 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             };
             if (!serial) decode();
             uint32_t cnt[kMaxWaitSrc] = {};
-            for (const auto& gr : zs->groups) {
+            for (size_t gi = 0; gi < zs->groups.size(); ++gi) {
+                const auto& gr = zs->groups[gi];
                 cudaStream_t sj = g.sd[gr.stream];
-                cudaMemcpyAsync(g.zstage + (gr.lo - zs->cfrom), m.zstore + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sj);
+                if (!(c->fault_kind == FSW_FAULT_DROP_GROUP && c->fault_index == gi))  // fault injection (tests)
+                    cudaMemcpyAsync(g.zstage + (gr.lo - zs->cfrom), m.zstore + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sj);
                 wv(sj, (CUdeviceptr)(g.progress + 32 * gr.stream), (cuuint32_t)(++cnt[gr.stream]), 0);
             }
             for (uint32_t j = 1; j < ic.zstreams; ++j) {
@@ -427,10 +428,12 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             cudaEventRecord(g.evd[0], sc);
             for (uint32_t j = 1; j < dp.streams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
             uint32_t cnt[kMaxWaitSrc] = {};
-            for (const auto& gr : dp.groups) {
+            for (size_t gi = 0; gi < dp.groups.size(); ++gi) {
+                const auto& gr = dp.groups[gi];
                 cudaStream_t sj = g.sd[gr.stream];
                 const uint8_t* from_ptr = ic.src_host ? m.store + gr.lo : weight_ptr(ic.src, gr.lo);
-                cudaMemcpyAsync(weight_ptr(ic.dst, gr.lo), from_ptr, gr.hi - gr.lo, cudaMemcpyDefault, sj);
+                if (!(c->fault_kind == FSW_FAULT_DROP_GROUP && c->fault_index == gi))  // fault injection (tests)
+                    cudaMemcpyAsync(weight_ptr(ic.dst, gr.lo), from_ptr, gr.hi - gr.lo, cudaMemcpyDefault, sj);
                 wv(sj, (CUdeviceptr)(g.progress + 32 * gr.stream), (cuuint32_t)(++cnt[gr.stream]), 0);
             }
             for (uint32_t j = 1; j < dp.streams; ++j) {

@@ -38,6 +38,7 @@ void invalidate(fsw_ctx* c, Model& m, int gi, bool keep_prefix) {
         fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.extent[gi]);
         m.extent[gi] = -1;
     }
+    m.complete[gi] = 0;
     if (!keep_prefix && m.pextent[gi] >= 0) {
         fsw_arena_free(c->gpus[gi].arena, (uint64_t)m.pextent[gi]);
         m.pextent[gi] = -1;
@@ -61,6 +62,7 @@ static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
                     m.pvalid[gi] = 0;
                 }
                 m.extent[gi] = (int64_t)so;
+                m.complete[gi] = 0;  // a resident copy only once the cold invoke succeeded
                 return FSW_OK;
             }
             if (need_p) fsw_arena_free(g.arena, po);
@@ -74,7 +76,7 @@ static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
             cand.push_back(o.get());
             heavy.push_back(model_heavy(*o));
             uint32_t k = 0;
-            for (int64_t e : o->extent) k += e >= 0;
+            for (size_t i = 0; i < o->extent.size(); ++i) k += o->extent[i] >= 0 && o->complete[i];
             copies.push_back(k);
             last.push_back(o->last_use[gi]);
             in_use.push_back(o->inflight != 0);
@@ -150,7 +152,7 @@ static Decision pick_gpu(fsw_ctx* c, Model& m) {
     std::vector<uint8_t> avail(n), hosts(n), loading(n);
     for (size_t i = 0; i < n; ++i) {
         avail[i] = !c->gpus[i].busy;
-        hosts[i] = m.extent[i] >= 0;
+        hosts[i] = m.extent[i] >= 0 && m.complete[i];  // an extent still being swapped in is no copy
         loading[i] = (uint8_t)c->gpus[i].loading;
     }
     std::vector<float> link(n * n, 0.0f);
@@ -233,13 +235,13 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         if (cold && o.peer_src) {
             const int s = (int)o.peer_src - 1;
             if (s < 0 || s >= (int)c->gpus.size() || s == gi) ss = fail(FSW_EINVAL, "invoke: bad peer_src %d", s);
-            else if (m->extent[s] < 0) ss = fail(FSW_ESTATE, "invoke: model %u is not resident on gpu %d", id, s);
+            else if (m->extent[s] < 0 || !m->complete[s]) ss = fail(FSW_ESTATE, "invoke: model %u is not resident on gpu %d", id, s);
             else if (!c->peer[gi][s]) ss = fail(FSW_ETOPO, "invoke: gpu %d cannot read gpu %d", gi, s);
             else peer = s;
         } else if (cold && !o.n_stripe_src && !((o.flags | c->cfg.flags) & FSW_NO_PEER_SWAP)) {
             if (o.gpu < 0 && dec.kind == 2) peer = dec.src;  // Algorithm 1, line 11
             for (int s = 0; s < (int)c->gpus.size() && peer < 0; ++s)
-                if (s != gi && m->extent[s] >= 0 && c->peer[gi][s]) peer = s;
+                if (s != gi && m->extent[s] >= 0 && m->complete[s] && c->peer[gi][s]) peer = s;
         }
         // striped swap: explicit sources, or the ctx policy for large stores
         if (ss != FSW_OK || peer >= 0) {
@@ -387,21 +389,49 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         key.pext = dstr;           // copy streams
     }
     if (cold && !sm) {  // DMA graphs bake addresses: the target extents and a peer source's extents
-        key.extra = (uint32_t)((uint64_t)m->extent[gi] >> 16);
+        key.ext = m->extent[gi];
         key.pext = m->pextent[gi];
         if (peer >= 0) {
             key.order = peer + 1;
-            key.seed = (uint32_t)((uint64_t)m->extent[peer] >> 16) ^ (uint32_t)((uint64_t)(m->pextent[peer] + 1) << 8);
+            key.src_ext = m->extent[peer];
+            key.src_pext = m->pextent[peer];
         }
     }
+    key.fault = c->fault_gen;
     auto it = p.graphs.find(key);
     cudaGraphExec_t exec = nullptr;
     if (it == p.graphs.end()) {
+        if (key.baked()) {
+            // graphs baked for other placements: keep the kMaxBakedGraphs - 1 most recently used (the
+            // placement changes under eviction churn; none of them is executing: this GPU is ours)
+            std::vector<std::pair<uint64_t, GraphKey>> baked;
+            for (auto& kv : p.graphs)
+                if (kv.first.baked()) baked.push_back({kv.second.last_use, kv.first});
+            std::sort(baked.begin(), baked.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+            for (size_t i = 0; i + kMaxBakedGraphs <= baked.size(); ++i) {
+                cudaGraphExecDestroy(p.graphs[baked[i].second].exec);
+                p.graphs.erase(baked[i].second);
+            }
+        }
         st = build_graph(c, *m, p, g, ic, &exec);
         if (st != FSW_OK) return finish(st);
-        p.graphs[key] = exec;
+        p.graphs[key] = GraphEntry{exec, ++p.graph_clock};
     } else {
-        exec = it->second;
+        exec = it->second.exec;
+        it->second.last_use = ++p.graph_clock;
+    }
+    // Test mode (FSW_DEBUG_POISON): every byte this invoke's swap must write, the DMAZ staging buffer
+    // and the model's activation workspace start as a per-invoke pattern, so an omitted store can never
+    // pass as the stale correct byte an earlier invoke left (the allocator hands back the same extent).
+    // Ordered before the graph on the launching stream, outside the timed events.
+    if (c->cfg.flags & FSW_DEBUG_POISON) {
+        const uint32_t pat = 0xA5C30000u ^ (uint32_t)((g.generation + 1) * 2654435761u);
+        launch_poison(g.sx, g.ws, p.ws_bytes, pat ^ 0x10u);
+        if (cold) {
+            launch_poison(g.sx, g.pool + m->extent[gi], m->store_bytes - m->split, pat);
+            if (m->split && !pcached) launch_poison(g.sx, g.pool + m->pextent[gi], m->split, pat);
+            if (engine == FSW_ENGINE_DMAZ && !striped && g.zstage) launch_poison(g.sx, g.zstage, g.zstage_cap, pat ^ 0x20u);
+        }
     }
     // stage: descriptor + input (pinned), one H2D node in the graph
     DevDesc dd = ic.dst;
@@ -517,6 +547,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             g.n_cold++;
             g.bytes_swapped_total += m->store_bytes - ic.from;
             if (m->split) m->pvalid[gi] = 1;  // the prefix bytes have landed
+            m->complete[gi] = 1;              // now a resident copy (peer swaps may read it)
             if (peer < 0 && !striped) {
                 m->cold_ms_sum += dms;
                 m->n_cold_runs++;
@@ -529,6 +560,21 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     }
     finish(FSW_OK);
     if (stats) stats->total_ms = now_ms() - t_entry;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_set_fault(fsw_ctx* c, uint32_t kind, uint32_t index) {
+    if (!c || kind > FSW_FAULT_DROP_GROUP) return fail(FSW_EINVAL, "set_fault: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (Gpu& g : c->gpus) {
+        if (g.busy) return fail(FSW_EBUSY, "set_fault: an invoke is in flight on gpu %d", g.dev);
+        CU(cudaSetDevice(g.dev));
+        set_drop_piece(kind == FSW_FAULT_DROP_PIECE ? index : 0xffffffffu);
+        CU(cudaDeviceSynchronize());
+    }
+    c->fault_kind = kind;
+    c->fault_index = index;
+    c->fault_gen++;  // cached graphs (DMA groups are baked into them) are keyed by it
     return FSW_OK;
 }
 

@@ -140,6 +140,18 @@ void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uin
 
 void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl);
 
+// ---- test mode (FSW_DEBUG_POISON, fsw_debug_set_fault, fsw_debug_litmus) ---------------------
+void launch_poison(cudaStream_t s, void* p, uint64_t bytes, uint32_t pattern);
+void set_drop_piece(uint32_t index);  // current device; ~0 = no fault
+// One layer region of a litmus run: store offset, bytes, and the per-counter targets of its Wait.
+struct LitmusLayer { uint64_t off; uint32_t bytes, layer; uint32_t target[kMaxWaitSrc]; };
+// `ctas` consumer CTAs (layer regions round-robin); wbase.ready[j] = the counters (per_layer_counter:
+// the base of the per-layer byte counters, indexed by LitmusLayer::layer), n, sys, ctl as a layer
+// kernel's Wait.
+void launch_litmus_check(cudaStream_t s, int ctas, DevDesc dst, const uint8_t* golden, const LitmusLayer* layers,
+                         uint32_t n_layers, Wait wbase, int per_layer_counter, DevCtl* gate, uint32_t gate_expected,
+                         unsigned long long* bad, unsigned long long* checked);
+
 // ---- layer ops ----------------------------------------------------------------------------
 struct EmbedArgs {
     const int32_t* ids; int n_tables; uint64_t table_off[4]; uint32_t table_rows[4]; int rule[4];

@@ -83,11 +83,24 @@ struct GraphKey {
     uint32_t seed, ctas, extra;
     uint64_t from = 0;   // first swapped store byte (partial caching: the cached prefix is skipped)
     int64_t pext = -1;   // DMA graphs: prefix extent offset (baked address)
+    int64_t ext = -1;    // DMA graphs: target extent offset (baked address)
+    int64_t src_ext = -1, src_pext = -1;  // peer DMA graphs: the source GPU's extents (baked addresses)
+    uint32_t fault = 0;  // debug fault injection generation (fsw_debug_set_fault)
     bool operator<(const GraphKey& o) const {
-        return std::tie(cold, flags, order, engine, chunk, seed, ctas, extra, from, pext) <
-               std::tie(o.cold, o.flags, o.order, o.engine, o.chunk, o.seed, o.ctas, o.extra, o.from, o.pext);
+        return std::tie(cold, flags, order, engine, chunk, seed, ctas, extra, from, pext, ext, src_ext, src_pext, fault) <
+               std::tie(o.cold, o.flags, o.order, o.engine, o.chunk, o.seed, o.ctas, o.extra, o.from, o.pext, o.ext,
+                        o.src_ext, o.src_pext, o.fault);
     }
+    bool baked() const { return ext >= 0; }  // addresses of one placement: bounded LRU cache
 };
+
+// An instantiated invoke graph and when it was last launched (graphs that bake one placement's
+// addresses are destroyed least recently used first beyond kMaxBakedGraphs per plan).
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    uint64_t last_use = 0;
+};
+constexpr size_t kMaxBakedGraphs = 8;
 
 // DMA engine plan: layer-aligned copy groups dealt round-robin to `streams` copy streams, and
 // for every layer the per-stream group count that covers the layer's last byte.
@@ -119,7 +132,8 @@ struct Plan {  // one model on one GPU
     std::vector<uint64_t> slot_off;      // workspace offset of each slot
     std::vector<int64_t> shadow_off;     // bf16 shadow of an f32 slot, or -1
     uint64_t ws_bytes = 0;
-    std::map<GraphKey, cudaGraphExec_t> graphs;
+    std::map<GraphKey, GraphEntry> graphs;
+    uint64_t graph_clock = 0;
     std::map<std::tuple<uint64_t, int, uint32_t, uint64_t>, PieceSet> pieces;  // (chunk, order, seed, from)
     std::map<std::tuple<uint64_t, uint32_t, uint64_t, uint64_t>, DmaPlan> dma;  // (group bytes, streams, from, split)
     // striped swap: source j of n gets every n-th piece; its table lives on the source's device
@@ -157,6 +171,9 @@ struct Model {
     uint64_t split = 0;
     std::vector<int64_t> pextent;      // prefix extent per GPU, or -1
     std::vector<uint8_t> pvalid;       // prefix bytes present
+    // extent[i] holds every swapped byte: set under c->mu only after a cold invoke on GPU i succeeded.
+    // A GPU->GPU swap reads only complete extents (an extent being swapped in is not a resident copy).
+    std::vector<uint8_t> complete;
     std::vector<uint64_t> last_use;
     std::vector<std::unique_ptr<Plan>> plans;
     int inflight = 0;
@@ -232,6 +249,7 @@ struct fsw_ctx {
     // one node the host stores are bound chunk-wise across them and striped swaps read node-locally.
     std::vector<int> gpu_node, nodes;
     bool fake_numa = false;               // FSW_FAKE_NUMA=k: pretend pool GPU i is on node i % k (no mbind)
+    uint32_t fault_kind = 0, fault_index = 0, fault_gen = 0;  // fsw_debug_set_fault (tests)
 };
 
 
@@ -322,5 +340,7 @@ fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_nod
 fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vector<int>& src_node, uint32_t j, int dev,
                              uint64_t from, PieceSet** out);
 fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out);
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_writeValue32 get_write_value32();                                           // graph.cpp: cuStreamWriteValue32
 bool model_heavy(const Model& m);                                                // invoke.cpp
 void invalidate(fsw_ctx* c, Model& m, int gi, bool keep_prefix = false);         // invoke.cpp

@@ -170,6 +170,7 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
         return fail(FSW_ECUDA, "fsw_init: no CUDA device (%s)", e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
     auto c = std::make_unique<fsw_ctx>();
     if (cfg) c->cfg = *cfg;
+    if (getenv("FSW_DEBUG_POISON") && atoi(getenv("FSW_DEBUG_POISON")) != 0) c->cfg.flags |= FSW_DEBUG_POISON;
     if (c->cfg.copy_ctas == 0) c->cfg.copy_ctas = 16;
     if (c->cfg.copy_threads == 0) c->cfg.copy_threads = 256;
     if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 16 << 10;
@@ -228,7 +229,7 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
 
 void free_plan(Gpu& g, Plan& p) {
     cudaSetDevice(g.dev);
-    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second.exec);
     p.graphs.clear();
     for (auto& kv : p.pieces) cudaFree(kv.second.dev);
     p.pieces.clear();

@@ -33,10 +33,16 @@ std::vector<uint8_t> partition_high(const std::vector<double>& rrcs, double alph
     std::vector<uint32_t> idx(n);
     std::iota(idx.begin(), idx.end(), 0u);
     std::stable_sort(idx.begin(), idx.end(), [&](uint32_t a, uint32_t b) { return rrcs[a] < rrcs[b]; });
+    // the total is summed in the same (sorted) order as the prefixes, so the last prefix equals it
+    // bit for bit and α = 1 puts every function in the high group
     double total = 0.0;
-    for (double r : rrcs) total += std::max(r, 0.0);
+    for (uint32_t i : idx) total += std::max(rrcs[i], 0.0);
     const double budget = alpha * total;
     std::vector<uint8_t> high(n, 0);
+    if (alpha >= 1.0) {
+        std::fill(high.begin(), high.end(), 1);
+        return high;
+    }
     double prefix = 0.0;
     for (uint32_t i : idx) {  // k = the largest prefix whose positive part fits the budget
         prefix += std::max(rrcs[i], 0.0);
@@ -214,6 +220,7 @@ double now_ms() {
 
 struct Req {
     uint32_t fid;
+    uint32_t model;  // copied at submit: workers never touch s->funcs outside the lock
     uint64_t ticket;
     const void* in;
     uint64_t in_bytes;
@@ -333,9 +340,8 @@ static void worker_main(fsw_sched* s) {
             s->work.pop_front();
             r->t_start = now_ms();
         }
-        const uint32_t model = s->funcs[r->fid].model;
         fsw_invoke_stats st{};
-        const fsw_status rc = fsw_invoke(s->ctx, model, r->in, r->in_bytes, r->out, r->out_cap, &st);
+        const fsw_status rc = fsw_invoke(s->ctx, r->model, r->in, r->in_bytes, r->out, r->out_cap, &st);
         const double t_end = now_ms();
         std::lock_guard<std::mutex> lk(s->mu);
         Func& f = s->funcs[r->fid];
@@ -420,7 +426,7 @@ extern "C" fsw_status fsw_submit(fsw_sched* s, uint32_t fid, const void* input, 
     std::lock_guard<std::mutex> lk(s->mu);
     if (fid >= s->funcs.size()) return FSW_ENOTFOUND;
     if (s->stop) return FSW_ESTATE;
-    Req* r = new Req{fid, s->next_ticket++, input, in_bytes, output, out_cap, now_ms()};
+    Req* r = new Req{fid, s->funcs[fid].model, s->next_ticket++, input, in_bytes, output, out_cap, now_ms()};
     s->reqs[r->ticket] = r;
     s->funcs[fid].q.push_back(r);
     *ticket = r->ticket;

@@ -463,6 +463,7 @@ extern "C" fsw_status fsw_register_model(fsw_ctx* c, const fsw_model_desc* d, ui
     m->extent.assign(c->gpus.size(), -1);
     m->pextent.assign(c->gpus.size(), -1);
     m->pvalid.assign(c->gpus.size(), 0);
+    m->complete.assign(c->gpus.size(), 0);
     m->last_use.assign(c->gpus.size(), 0);
     m->plans.resize(c->gpus.size());
     std::lock_guard<std::mutex> lk(c->mu);

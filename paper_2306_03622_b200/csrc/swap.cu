@@ -12,13 +12,19 @@
 
 namespace fsw {
 
+// Fault injection (fsw_debug_set_fault, tests only): the claim index of the piece whose stores every
+// swap kernel skips while still releasing its bytes, or ~0 = none.  Read once per kernel.
+__device__ uint32_t g_drop_piece = 0xffffffffu;
+
+void set_drop_piece(uint32_t index) { cudaMemcpyToSymbol(g_drop_piece, &index, sizeof index); }
+
 template <int U>
 __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, DevDesc dst, const DevDesc* __restrict__ desc,
                                               const Piece* __restrict__ pieces, uint32_t n_pieces,
                                               uint32_t* __restrict__ ready, DevCtl* __restrict__ own, DevCtl* gate, int sys) {
     if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
     const DevDesc dd = desc ? *desc : dst;
-    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lane = threadIdx.x & 31u, drop = g_drop_piece;
     for (;;) {
         uint32_t p = 0;
         if (lane == 0) p = atomicAdd(&own->ticket, 1u);
@@ -28,7 +34,7 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
         const Piece pc = pieces[p];
         const uint4* src = reinterpret_cast<const uint4*>(host + pc.off);
         uint4* out = reinterpret_cast<uint4*>(weight_ptr(dd, pc.off));
-        const uint32_t n16 = pc.bytes >> 4;
+        const uint32_t n16 = p == drop ? 0u : pc.bytes >> 4;  // fault injection: no stores, still released
         uint32_t i = lane;
         for (; i + (U - 1) * 32 < n16; i += U * 32) {
             uint4 v[U];
@@ -198,7 +204,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                                                DevCtl* gate, int sys, const uint32_t* progress) {
     if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
     const DevDesc dd = desc ? *desc : dst;
-    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lane = threadIdx.x & 31u, drop = g_drop_piece;
     for (;;) {
         uint32_t p = 0;
         if (lane == 0) p = atomicAdd(&own->ticket, 1u);
@@ -212,7 +218,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
         }
         const uint8_t* cp = src + (pc.coff - src_base);
         uint8_t* out = weight_ptr(dd, pc.off);
-        const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;  // <= 16
+        const uint32_t nb = p == drop ? 0u : (pc.bytes + kZBlock - 1) / kZBlock;  // <= 16; fault: none
         // block `lane`: header (device piece table), stream-A and stream-B offsets (exclusive scans)
         const uint32_t hd = lane < nb ? __ldg(&pieces[p].hdr[lane]) : 0u;
         const uint32_t sa = lane < nb ? zblock_a(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
     extern __shared__ __align__(128) uint8_t zring[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(zring + kZRing * kZBuf);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kZRing);
-    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, drop = g_drop_piece;
     const DevDesc dd = desc ? *desc : dst;
     if (tid == 0) {
         atomicAdd(&gate->started, 1u);
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         }
         const uint8_t* cp = pc.cbytes <= kZBuf ? zring + b * kZBuf : src + (pc.coff - src_base);  // generic address
         uint8_t* out = weight_ptr(dd, pc.off);
-        const uint32_t nb = (pc.bytes + kZBlock - 1) / kZBlock;
+        const uint32_t nb = p == drop ? 0u : (pc.bytes + kZBlock - 1) / kZBlock;  // fault injection: none
         // every warp scans the piece's block offsets (stream A, stream B)
         const uint32_t hd = lane < nb ? __ldg(&pieces[p].hdr[lane]) : 0u;
         const uint32_t sa = lane < nb ? zblock_a(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
@@ -505,6 +511,105 @@ __global__ void k_finish(DevCtl* ctl, const uint8_t* __restrict__ out, uint64_t 
 void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl) {
     const uint64_t want = (bytes + 4095) / 4096;
     k_finish<<<(unsigned)(want < 1 ? 1 : want > 148 ? 148 : want), 256, 0, s>>>(ctl, out, bytes, host_out, host_ctl);
+}
+
+// ---- test mode: poison fills and the readiness litmus consumer -------------------------------
+// Fill [p, p + bytes) with a 32-bit pattern (FSW_DEBUG_POISON): four distinct words per 16 bytes.
+__global__ void k_poison(uint8_t* __restrict__ p, uint64_t bytes, uint32_t pattern) {
+    const uint64_t n16 = bytes >> 4, stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint4 v = make_uint4(pattern, pattern ^ 0x01010101u, pattern ^ 0x02020202u, pattern ^ 0x03030303u);
+    for (uint64_t i = t0; i < n16; i += stride) st_v4(reinterpret_cast<uint4*>(p) + i, v);
+    for (uint64_t i = (n16 << 4) + t0; i < bytes; i += stride) p[i] = (uint8_t)(pattern >> (8 * (i & 3)));
+}
+void launch_poison(cudaStream_t s, void* p, uint64_t bytes, uint32_t pattern) {
+    if (!bytes) return;
+    k_poison<<<296, 512, 0, s>>>(static_cast<uint8_t*>(p), bytes, pattern);
+}
+
+// Litmus consumer (fsw_debug_litmus).  Exactly the weight-reading path of a layer kernel: one thread
+// acquires the layer's counter(s) (wait_ready_thread, the same code the layer kernels run), executes
+// fence.proxy.async.global (the GEMM producer's fence: the bytes were written through the generic proxy
+// or by the copy engine and are read through the async proxy) and bulk-copies the region into shared
+// memory in kLitChunk pieces; the CTA compares every 16-byte word with the golden copy.
+constexpr uint32_t kLitChunk = 16384;
+__global__ void __launch_bounds__(256) k_litmus_check(DevDesc dst, const uint8_t* __restrict__ golden,
+                                                      const LitmusLayer* __restrict__ layers, uint32_t n_layers,
+                                                      Wait wbase, int per_layer_counter, DevCtl* gate, uint32_t gate_expected,
+                                                      unsigned long long* bad, unsigned long long* checked) {
+    __shared__ __align__(128) uint8_t buf[kLitChunk];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t nbad;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        nbad = 0;
+        // as the invoke graph's k_gate: spin only once every producer CTA is resident
+        const volatile uint32_t* st = &gate->started;
+        const uint64_t t0 = globaltimer();
+        while (gate_expected && *st < gate_expected) {
+            __nanosleep(128);
+            if (globaltimer() - t0 > kWatchdogNs) {
+                atomicExch(&gate->err, 2);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    unsigned long long nchk = 0;
+    for (uint32_t L = blockIdx.x; L < n_layers; L += gridDim.x) {
+        const LitmusLayer ly = layers[L];
+        Wait w = wbase;
+        w.layer = (int32_t)ly.layer;
+        for (uint32_t j = 0; j < w.n; ++j) {
+            if (per_layer_counter) w.ready[j] = wbase.ready[j] + ly.layer;
+            w.target[j] = ly.target[j];
+        }
+        if (tid == 0) {
+            wait_ready_thread(w);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        for (uint32_t o = 0; o < ly.bytes; o += kLitChunk) {
+            const uint32_t nbytes = min(kLitChunk, ly.bytes - o);
+            if (tid == 0) {
+                const uint32_t bb = smem_addr(&bar);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(nbytes) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_addr(buf)),
+                             "l"(weight_ptr(dst, ly.off + o)), "r"(nbytes), "r"(bb)
+                             : "memory");
+            }
+            {
+                uint32_t ok = 0;
+                do {
+                    asm volatile("{ .reg .pred q; mbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2; selp.u32 %0, 1, 0, q; }"
+                                 : "=r"(ok) : "r"(smem_addr(&bar)), "r"(phase) : "memory");
+                } while (!ok);
+            }
+            phase ^= 1u;
+            uint32_t my = 0;
+            for (uint32_t i = tid; i < nbytes / 16; i += blockDim.x) {
+                const uint4 a = reinterpret_cast<const uint4*>(buf)[i];
+                const uint4 g = __ldg(reinterpret_cast<const uint4*>(golden + ly.off + o) + i);
+                my += (a.x != g.x || a.y != g.y || a.z != g.z || a.w != g.w);
+            }
+            if (my) atomicAdd(&nbad, my);
+            nchk += nbytes;
+            __syncthreads();  // buf is read by every thread before the next copy overwrites it
+        }
+    }
+    if (tid == 0) {
+        if (nbad) atomicAdd(bad, (unsigned long long)nbad);
+        atomicAdd(checked, nchk);
+    }
+}
+void launch_litmus_check(cudaStream_t s, int ctas, DevDesc dst, const uint8_t* golden, const LitmusLayer* layers,
+                         uint32_t n_layers, Wait wbase, int per_layer_counter, DevCtl* gate, uint32_t gate_expected,
+                         unsigned long long* bad, unsigned long long* checked) {
+    k_litmus_check<<<ctas, 256, 0, s>>>(dst, golden, layers, n_layers, wbase, per_layer_counter, gate, gate_expected, bad,
+                                        checked);
 }
 
 // No carveout preference for the swap kernels (measured: a max-shared carveout on every kernel made

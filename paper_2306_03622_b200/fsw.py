@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_HERE, "libfsw.so")
 
 OK, EINVAL, ENOTFOUND, ENOMEM, EBUSY, ESTATE, ECUDA, ETIMEOUT, ETOPO = range(9)
 STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA", "ETIMEOUT", "ETOPO"]
-NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP = 0x1, 0x2, 0x4, 0x8, 0x10
+NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP, DEBUG_POISON = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+FAULT_NONE, FAULT_DROP_PIECE, FAULT_DROP_GROUP = 0, 1, 2
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
 ENGINE_AUTO, ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ = 0, 1, 2, 3, 4
@@ -146,7 +147,8 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
-           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal"]
+           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal",
+           "fsw_debug_set_fault", "fsw_debug_litmus"]
 
 _lib = None
 
@@ -180,6 +182,8 @@ def lib():
         L.fsw_debug_read_coded.argtypes = [vp, u32, vp, u64]
         L.fsw_debug_coded_pieces.argtypes = [vp, u32, vp, u32, ctypes.POINTER(u32)]
         L.fsw_debug_dmaz_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
+        L.fsw_debug_set_fault.argtypes = [vp, u32, u32]
+        L.fsw_debug_litmus.argtypes = [vp, u32, i32, u32, u32, u32, ctypes.POINTER(u64), ctypes.POINTER(u64)]
         L.fsw_arena_create.argtypes = [u64, u64]
         L.fsw_arena_create.restype = vp
         L.fsw_arena_destroy.argtypes = [vp]
@@ -444,6 +448,16 @@ class Runtime:
         _check(lib().fsw_debug_dmaz_plan(self.h, mid, group_bytes, streams, lohi.ctypes.data, st.ctypes.data,
                                          n.value, ctypes.byref(n), pg.ctypes.data))
         return lohi[:n.value], st[:n.value], pg
+
+    def set_fault(self, kind: int, index: int = 0):
+        """Fault injection (negative controls): FAULT_DROP_PIECE / FAULT_DROP_GROUP / FAULT_NONE."""
+        _check(lib().fsw_debug_set_fault(self.h, kind, index))
+
+    def litmus(self, mid: int, engine: int, ctas: int, iters: int, gpu: int = 0):
+        """Readiness litmus (fsw_debug_litmus): (bad 16-byte words, bytes checked) over `iters` runs."""
+        bad, chk = u64(), u64()
+        _check(lib().fsw_debug_litmus(self.h, mid, gpu, engine, ctas, iters, ctypes.byref(bad), ctypes.byref(chk)))
+        return bad.value, chk.value
 
     def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:
         buf = np.empty(nbytes, dtype=np.uint8)

@@ -4,6 +4,13 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# Every libfsw context the test session creates runs in poison mode (FSW_DEBUG_POISON, include/fsw.h):
+# before each cold invoke the extents the swap must fill and the DMAZ staging buffer are overwritten
+# with a per-invoke pattern, and before each invoke the activation workspace, so a store the swap (or a
+# layer kernel) omits can never pass as a stale correct byte left by an earlier invoke of the same
+# model in the same extent (the allocator hands the same offset back).
+os.environ.setdefault("FSW_DEBUG_POISON", "1")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

@@ -211,3 +211,33 @@ def test_striped_swap_numa_dealing_two_fake_nodes(monkeypatch):
                 assert r.stats["swap_kind"] == 3
                 np.testing.assert_array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
                 np.testing.assert_array_equal(r.output, base)
+
+
+def test_peer_swap_never_reads_an_extent_still_being_swapped_in():
+    """while thread A cold-loads a model onto pool GPU 0, a concurrent invoke on pool
+    GPU 1 must not treat GPU 0's half-written extent as a resident copy (Algorithm 1 case 2 needs a
+    complete copy): it swaps from the host, and both copies end up bit-exact."""
+    import threading
+    import time
+    from paper_2306_03622_b200 import ENGINE_SM, Runtime
+    spec = synth.build_model("bert-base")
+    w, x = spec.build_weights(), spec.make_input()
+    with Runtime(gpu_ids=[0, 0], pool_bytes=2 << 30) as rt2:
+        mid = rt2.register_spec(spec, w)
+        base = rt2.invoke(mid, x, gpu=0).output.copy()
+        for _ in range(5):
+            rt2.evict(mid)
+            res = {}
+
+            def run(gpu, delay):
+                time.sleep(delay)
+                res[gpu] = rt2.invoke(mid, x, gpu=gpu, engine=ENGINE_SM, chunk_bytes=16 << 10)
+
+            ta = threading.Thread(target=run, args=(0, 0.0))
+            tb = threading.Thread(target=run, args=(1, 0.001))  # A's swap takes ~4 ms
+            ta.start(); tb.start(); ta.join(); tb.join()
+            assert res[0].stats["swap_kind"] == 1
+            assert res[1].stats["swap_kind"] in (1, 2)  # peer only if A had completed first
+            for g in (0, 1):
+                np.testing.assert_array_equal(rt2.read_resident(mid, g), rt2.read_store(mid))
+                np.testing.assert_array_equal(res[g].output, base)
