@@ -208,7 +208,63 @@ def run_reference(args):
 
 
 def roofline_ms(bytes_, flops, fill_bytes, link_gbs, tflops):
+    """BASELINE.json north_star's pipelined roofline: max(total bytes / aggregate link bandwidth, total
+    compute at peak) plus the first-layer fill (bytes of the first layer in execution order / bandwidth)."""
     return max(bytes_ / (link_gbs * 1e6), flops / (tflops * 1e9)) + fill_bytes / (link_gbs * 1e6)
+
+
+def flowshop_ms(x_ms, c_ms):
+    """SURVEY §8(d)'s tight bound: the two-machine flow shop (link, then GPU) over layers in execution order,
+    transfer of layer k taking x_k and its compute c_k: makespan = max_k (Σ_{j<=k} x_j + Σ_{j>=k} c_j)."""
+    x, c = np.asarray(x_ms, dtype=np.float64), np.asarray(c_ms, dtype=np.float64)
+    if x.size == 0:
+        return 0.0
+    return float(np.max(np.cumsum(x) + np.cumsum(c[::-1])[::-1]))
+
+
+def pipeline_latency(t_transfer_ms, t_compute_ms, n_groups):
+    """SPEC.md's two-stage pipeline of n equal groups (SPEC [OP] pipeline_latency, §4.3):
+    t_x + (n − 1)·max(t_x, t_c) + t_c with t_x, t_c the per-group times — the flow shop of equal stages."""
+    tx, tc = t_transfer_ms / n_groups, t_compute_ms / n_groups
+    return tx + (n_groups - 1) * max(tx, tc) + tc
+
+
+def layer_flops(spec, layer):
+    """FLOPs (2 per MAC) of one layer at batch 1: linear / conv as dense GEMMs, attention 4·T²·dh per head."""
+    from synth.models import Op
+    if layer.op == Op.LINEAR:
+        n, k = spec.tensors[layer.refs[0]].shape[:2]
+        rows = layer.attr[2] if layer.attr[2] > 0 else int(np.prod(spec.slots[layer.in0].shape)) // k
+        return 2.0 * rows * n * k
+    if layer.op == Op.CONV2D:
+        cout, r, s_, cin = spec.tensors[layer.refs[0]].shape[:4]
+        p, q = spec.slots[layer.out].shape[:2]
+        return 2.0 * p * q * cout * r * s_ * cin
+    if layer.op == Op.ATTENTION:
+        t = spec.slots[layer.in0].shape[0]
+        return 4.0 * t * t * layer.attr[1] * layer.attr[0]
+    return 0.0
+
+
+def model_flops(spec):
+    return sum(layer_flops(spec, l) for l in spec.layers)
+
+
+def layer_bytes(spec):
+    """Algorithmic weight bytes per layer in execution order (a tied tensor counts at its first user)."""
+    seen, out = set(), []
+    for l in spec.layers:
+        out.append(sum(spec.tensors[r].nbytes for r in l.refs if r not in seen))
+        seen.update(l.refs)
+    return out
+
+
+def bf16_peak_tflops():
+    """Dense bf16 peak: MEASURED_PEAKS.json (driver-measured cuBLAS, burst), else the nominal 2250."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except (OSError, ValueError, KeyError):
+        return 2250.0
 
 
 MODEL_FLOPS = {  # 2 FLOPs per MAC, batch 1 (SURVEY Appendix A)

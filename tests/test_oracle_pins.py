@@ -538,3 +538,92 @@ def test_resnet_tiny_vs_torch_functional_float64():
                          torch.tensor(_t(w, spec, spec.tensors[l.refs[1]].name)))
         vals[l.out] = o
     np.testing.assert_allclose(y, vals[spec.output_slot].numpy(), rtol=1e-11, atol=1e-11)
+
+
+# ---------------------------------------------------------------------------------------------
+# ResNet-50 v1.5 against torchvision (SURVEY §8(c) reading #5: BN folded, stride on the 3x3)
+# ---------------------------------------------------------------------------------------------
+def _tv_resnet50_folded(spec, seed=0):
+    """torchvision's resnet50 (float64, eval) with random BatchNorm statistics; every conv+BN pair folded
+    into (W', b') in float64, written into the synth table's tensors (bf16), and the rounded values
+    loaded back into the torchvision model with each BN reduced to `+ b'` (var 1, mean 0,
+    gamma 1; eps 1e-300 leaves sqrt(var + eps) == 1), so both sides compute with the same weights."""
+    import torchvision
+    torch.manual_seed(seed)
+    tv = torchvision.models.resnet50(weights=None).double().eval()
+    for m in tv.modules():
+        if isinstance(m, torch.nn.BatchNorm2d):
+            m.running_mean.uniform_(-0.1, 0.1)
+            m.running_var.uniform_(0.5, 1.5)
+            m.weight.data.uniform_(0.3, 0.6)
+            m.bias.data.uniform_(-0.1, 0.1)
+    pairs = [("conv1", tv.conv1, tv.bn1)]
+    for si in range(4):
+        for bi, blk in enumerate(getattr(tv, f"layer{si + 1}")):
+            p = f"layer{si + 1}.{bi}"
+            pairs += [(p + ".conv1", blk.conv1, blk.bn1), (p + ".conv2", blk.conv2, blk.bn2),
+                      (p + ".conv3", blk.conv3, blk.bn3)]
+            if blk.downsample is not None:
+                pairs.append((p + ".downsample", blk.downsample[0], blk.downsample[1]))
+    ov = {}
+    with torch.no_grad():
+        for name, conv, bn in pairs:
+            s = bn.weight / torch.sqrt(bn.running_var + bn.eps)
+            ov[name + ".weight"] = (conv.weight * s[:, None, None, None]).permute(0, 2, 3, 1).numpy()
+            ov[name + ".bias"] = (bn.bias - bn.running_mean * s).numpy()
+        ov["fc.weight"], ov["fc.bias"] = tv.fc.weight.numpy(), tv.fc.bias.numpy()
+    w = spec.build_weights(ov)
+    with torch.no_grad():
+        for name, conv, bn in pairs:
+            conv.weight.copy_(torch.tensor(_t(w, spec, name + ".weight")).permute(0, 3, 1, 2))
+            bn.running_mean.zero_()
+            bn.running_var.fill_(1.0)
+            bn.eps = 1e-300  # sqrt(1 + eps) == 1 in float64
+            bn.weight.fill_(1.0)
+            bn.bias.copy_(torch.tensor(_t(w, spec, name + ".bias")))
+        tv.fc.weight.copy_(torch.tensor(_t(w, spec, "fc.weight")))
+        tv.fc.bias.copy_(torch.tensor(_t(w, spec, "fc.bias")))
+    return tv, w
+
+
+def _tv_input(spec, img):
+    return torch.tensor(bf16_bits_to_f64(img.view(np.uint16)).reshape(spec.slots[spec.input_slot].shape)).permute(2, 0, 1)[None]
+
+
+def test_resnet50_v15_table_vs_torchvision_float64():
+    """The synth ResNet-50 table (reduced to a 64x64 image, full widths and depths) run by the oracle equals
+    torchvision.models.resnet50 (v1.5) in float64 with the same folded weights.  Negative controls: the v1
+    block (stride on the first 1x1) and ReLU before the residual add must NOT match."""
+    spec = synth.models._resnet([3, 4, 6, 3], [64, 128, 256, 512], 64, name="resnet50-64px")
+    tv, w = _tv_resnet50_folded(spec)
+    img = spec.make_input()
+    y = oracle.output(spec, w, img).reshape(-1)
+    with torch.no_grad():
+        ref = tv(_tv_input(spec, img))[0].numpy()
+    assert np.max(np.abs(y - ref)) <= 1e-9 * np.max(np.abs(ref)), np.max(np.abs(y - ref))
+    # v1: stride moved to the first 1x1 of each stage's first block
+    with torch.no_grad():
+        for si in (2, 3, 4):
+            blk = getattr(tv, f"layer{si}")[0]
+            blk.conv1.stride, blk.conv2.stride = (2, 2), (1, 1)
+        v1 = tv(_tv_input(spec, img))[0].numpy()
+        for si in (2, 3, 4):
+            blk = getattr(tv, f"layer{si}")[0]
+            blk.conv1.stride, blk.conv2.stride = (1, 1), (2, 2)
+    assert np.max(np.abs(y - v1)) > 1e-3 * np.max(np.abs(ref))
+    # ReLU applied to the conv3 branch before the residual add (instead of after the add)
+    from torchvision.models.resnet import Bottleneck
+
+    def relu_before_add(self, x):
+        idt = x if self.downsample is None else self.downsample(x)
+        o = self.relu(self.bn1(self.conv1(x)))
+        o = self.relu(self.bn2(self.conv2(o)))
+        return self.relu(self.bn3(self.conv3(o))) + idt
+    orig = Bottleneck.forward
+    Bottleneck.forward = relu_before_add
+    try:
+        with torch.no_grad():
+            rb = tv(_tv_input(spec, img))[0].numpy()
+    finally:
+        Bottleneck.forward = orig
+    assert np.max(np.abs(y - rb)) > 1e-3 * np.max(np.abs(ref))
