@@ -165,11 +165,11 @@ def max_over_ranks(local: dict, world: int) -> dict:
     return {k: max(r[k] for r in g) for k in local}
 
 
-def cpu_oracle_timing(spec, w, x, budget_s: float, max_reps: int = 50):
+def cpu_oracle_timing(spec, w, x, budget_s: float, max_reps: int = 50, threads: int = 0):
     """Time the oracle (tests-only package) as it stands on the host cores: bounded sample."""
     import oracle
     # all the host cores this process may run on (torchrun sets OMP_NUM_THREADS=1 per rank)
-    cores = oracle.lib().oracle_set_threads(len(os.sched_getaffinity(0)))
+    cores = oracle.lib().oracle_set_threads(threads or len(os.sched_getaffinity(0)))
     times = []
     t_start = time.perf_counter()
     while len(times) < max_reps:
@@ -267,12 +267,130 @@ def bf16_peak_tflops():
         return 2250.0
 
 
-MODEL_FLOPS = {  # 2 FLOPs per MAC, batch 1
-    "bert-base": 22.35e9, "resnet50": 8.18e9, "gpt2-xl": 382.7e9, "mlp": 8.39e6,
-}
 
 
 ENGINE_NAMES = {1: "sm", 2: "dma", 3: "smz", 4: "dmaz"}
+
+
+def host_cpu_info():
+    """lscpu model name, nproc and the cores this process may run on."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return {"lscpu_model": model, "nproc": os.cpu_count(), "affinity_cores": len(os.sched_getaffinity(0))}
+
+
+def coded_layer_bytes(rt, mid, n_layers):
+    """Coded (link) bytes of each layer region of a link-coded model, from its piece table."""
+    out = np.zeros(n_layers, dtype=np.float64)
+    for pc in rt.coded_pieces(mid):
+        out[int(pc["layer"])] += int(pc["cbytes"])
+    return out
+
+
+def roofline_report(spec, p50_ms, link_gbs, peak_tf, coded=None):
+    """Both of SURVEY §8(d)'s fractions for one measured cold latency: the north_star fill roofline and
+    the tight flow-shop bound, over the plain store bytes and (link-coded model) over the coded bytes."""
+    lb = np.array(layer_bytes(spec), dtype=np.float64)
+    c = np.array([layer_flops(spec, l) for l in spec.layers]) / (peak_tf * 1e9)
+    flops = float(sum(layer_flops(spec, l) for l in spec.layers))
+    r = {}
+    for kind, b in (("plain_bytes", lb), ("coded_bytes", coded)):
+        if b is None:
+            continue
+        t_roof = roofline_ms(b.sum(), flops, b[0], link_gbs, peak_tf)
+        t_fs = flowshop_ms(b / (link_gbs * 1e6), c)
+        r[kind] = {"bytes": int(b.sum()), "roofline_ms": round(t_roof, 4), "frac_roofline": round(t_roof / p50_ms, 4),
+                   "flowshop_ms": round(t_fs, 4), "frac_flowshop": round(t_fs / p50_ms, 4),
+                   "ratio_to_roofline": round(p50_ms / t_roof, 4)}
+    return r
+
+
+def measure_cold(rt, mid, x, out, reps, warm, **kw):
+    """`warm` untimed then `reps` cold invokes (evict everywhere first, SURVEY §8c reading #10)."""
+    st = []
+    for i in range(warm + reps):
+        rt.evict(mid, -1)
+        s = rt.invoke(mid, x, out=out, gpu=0, **kw).stats
+        if i >= warm:
+            st.append(s)
+    return st
+
+
+def cold_summary(st, store_bytes):
+    dev = [t["device_ms"] for t in st]
+    sw = percentile([t["swap_ms"] for t in st], 50)
+    return {"p50_ms": round(percentile(dev, 50), 4), "p99_ms": round(percentile(dev, 99), 4),
+            "mean_ms": round(statistics.mean(dev), 4), "reps": len(dev), "swap_p50_ms": round(sw, 4),
+            "compute_tail_p50_ms": round(percentile([t["compute_tail_ms"] for t in st], 50), 4),
+            "wire_bytes": int(st[0]["wire_bytes"]), "wire_gbs": round(st[0]["wire_bytes"] / (sw * 1e6), 2),
+            "store_bytes_gbs": round(store_bytes / (sw * 1e6), 2), "engine": ENGINE_NAMES.get(st[0]["engine"])}
+
+
+# The other single-GPU configs of BASELINE.json (configs[0], [2], [3] at 1 GPU), measured beside the
+# headline in the same run: (model, timed cold reps, untimed warm-up reps)
+EXTRA_CONFIGS = (("mlp", 100, 20), ("resnet50", 100, 20), ("gpt2-xl", 10, 3))
+
+
+def measure_extra_config(rt, name, reps, warm, link_gbs, peak_tf):
+    import synth
+    from paper_2306_03622_b200 import ENGINE_DMA, ENGINE_SM
+    spec = synth.build_model(name)
+    w = spec.build_weights()
+    x = spec.make_input()
+    mid = rt.register_spec(spec, w, link_code=True)
+    del w
+    try:
+        info = rt.model_info(mid)
+        out = np.empty(max(1, info["output_bytes"] // 4), dtype=np.float32)
+        st = measure_cold(rt, mid, x, out, reps, warm)
+        r = cold_summary(st, info["store_bytes"])
+        rt.invoke(mid, x, out=out, gpu=0)
+        warm_ms = [rt.invoke(mid, x, out=out, gpu=0).stats["device_ms"] for _ in range(max(10, reps // 2))]
+        r["resident_p50_ms"] = round(percentile(warm_ms, 50), 4)
+        r["store_bytes"], r["coded_bytes"] = int(info["store_bytes"]), int(info["coded_bytes"])
+        r["coded_ratio"] = round(info["coded_bytes"] / info["store_bytes"], 4)
+        r["roofline"] = roofline_report(spec, r["p50_ms"], link_gbs, peak_tf,
+                                        coded_layer_bytes(rt, mid, len(spec.layers)))
+        plain_engine = ENGINE_DMA if info["store_bytes"] >= (32 << 20) else ENGINE_SM
+        sp = measure_cold(rt, mid, x, out, max(5, reps // 2), max(2, warm // 2), engine=plain_engine)
+        r["plain_store"] = cold_summary(sp, info["store_bytes"])
+        r["plain_store"]["roofline"] = roofline_report(spec, r["plain_store"]["p50_ms"], link_gbs, peak_tf)
+        return r
+    finally:
+        rt.evict(mid, -1)
+        rt.unregister(mid)
+
+
+def measure_weight_distributions(rt, name, reps, warm, link_gbs, peak_tf):
+    """Link coding on bell-shaped and heavy-tailed weights of the same σ (the uniform init
+    is a favourable case): coded/plain byte ratio and cold latency of the default (coded) engine."""
+    import synth
+    res = {}
+    for dist in ("gaussian", "laplace"):
+        spec = synth.build_model(name)
+        spec.dist = dist
+        w = spec.build_weights()
+        x = spec.make_input()
+        mid = rt.register_spec(spec, w, link_code=True)
+        del w
+        try:
+            info = rt.model_info(mid)
+            out = np.empty(max(1, info["output_bytes"] // 4), dtype=np.float32)
+            r = cold_summary(measure_cold(rt, mid, x, out, reps, warm), info["store_bytes"])
+            r["coded_ratio"] = round(info["coded_bytes"] / info["store_bytes"], 4)
+            r["roofline"] = roofline_report(spec, r["p50_ms"], link_gbs, peak_tf,
+                                            coded_layer_bytes(rt, mid, len(spec.layers)))
+            res[dist] = r
+        finally:
+            rt.evict(mid, -1)
+            rt.unregister(mid)
+    return res
 
 
 def run_fsw(args):
@@ -403,16 +521,33 @@ def run_fsw(args):
             traffic = None
     first = spec.layers[0]
     fill = sum(spec.tensors[r].nbytes for r in first.refs)
-    flops = MODEL_FLOPS.get(args.model, 0.0)
-    t_roof = roofline_ms(info["algorithmic_bytes"], flops, fill, PCIE_GEN5_X16_GBS, 1645.1)
-    t_roof_dma = roofline_ms(info["algorithmic_bytes"], flops, fill, dma, 1645.1) if dma else None
-    ratio = wire / store  # link coding: the same roofline over the coded bytes
-    t_roof_coded = roofline_ms(info["algorithmic_bytes"] * ratio, flops, fill * ratio, PCIE_GEN5_X16_GBS, 1645.1)
+    flops = model_flops(spec)
+    peak_tf = bf16_peak_tflops()
+    t_roof = roofline_ms(info["algorithmic_bytes"], flops, fill, PCIE_GEN5_X16_GBS, peak_tf)
+    t_roof_dma = roofline_ms(info["algorithmic_bytes"], flops, fill, dma, peak_tf) if dma else None
+    coded_lb = coded_layer_bytes(rt, mid, len(spec.layers)) if info["coded_bytes"] else None
+    # link coding: the same roofline over the coded bytes (first-layer fill = its coded bytes)
+    t_roof_coded = (roofline_ms(coded_lb.sum(), flops, coded_lb[0], PCIE_GEN5_X16_GBS, peak_tf) if coded_lb is not None
+                    else t_roof)
+    fractions = roofline_report(spec, p50, PCIE_GEN5_X16_GBS, peak_tf, coded_lb)
+    extras, dists = {}, {}
+    if not args.no_extras and args.model == "bert-base" and world == 1:
+        for name, reps, warm_n in EXTRA_CONFIGS:
+            try:
+                extras[name] = measure_extra_config(rt, name, reps, warm_n, PCIE_GEN5_X16_GBS, peak_tf)
+            except Exception as e:  # report, never hide: a config that fails shows up in the line
+                extras[name] = {"error": repr(e)}
+        try:
+            dists = measure_weight_distributions(rt, "bert-base", 20, 5, PCIE_GEN5_X16_GBS, peak_tf)
+        except Exception as e:
+            dists = {"error": repr(e)}
     cpu = None
     if not args.no_cpu_baseline:
         ct, omp_threads = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
+        ct1, _ = cpu_oracle_timing(spec, w, x, budget_s=0.0, max_reps=1, threads=1)
         cpu = {"value": round(statistics.median(ct), 3), "unit": "ms", "cores": omp_threads, "kind": "oracle",
-               "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)"}
+               "sample": f"{len(ct)} full {args.model} forwards (float64 oracle over the same bf16 weights)",
+               "single_thread_ms": round(ct1[0], 1), **host_cpu_info()}
     dec = None
     try:
         dec = json.load(open(tpath)).get(args.model + "-dmaz-decode") if os.path.exists(tpath) else None
@@ -477,11 +612,15 @@ def run_fsw(args):
         "pipelined_roofline_ms_coded_bytes": round(t_roof_coded, 4),
         "frac_of_pipelined_roofline_coded_bytes": round(t_roof_coded / p50, 4),
         "pipelined_roofline_ms_at_measured_dma": round(t_roof_dma, 4) if t_roof_dma else None,
+        "roofline_fractions": fractions,
+        "bf16_peak_tflops": peak_tf,
         "roofline": roof,
         "sm_engine_roofline": {"bound": "pcie", "kernel": "k_swap", "achieved": sm_gbs, "peak": PCIE_GEN5_X16_GBS,
                                "unit": "GB/s", "frac": round(sm_gbs / PCIE_GEN5_X16_GBS, 4) if sm_gbs else None, "traffic": traffic,
                                "pcie_read_bytes": pcie_traffic},
         "engines": variants,
+        "configs_1gpu": extras,
+        "weight_distributions": dists,
         "cpu_baseline": cpu,
         "e2e": {"value": round(percentile(e2e, 50), 4), "unit": "ms",
                 "h2d_bytes_per_step": int(info["input_bytes"]), "d2h_bytes_per_step": int(info["output_bytes"]),
@@ -560,7 +699,7 @@ def run_striped(args):
     agg_peak = PCIE_GEN5_X16_GBS * world
     first = spec.layers[0]
     fill = sum(spec.tensors[r].nbytes for r in first.refs)
-    t_roof = roofline_ms(info["algorithmic_bytes"], MODEL_FLOPS.get(args.model, 0.0), fill, agg_peak, 1645.1)
+    t_roof = roofline_ms(info["algorithmic_bytes"], model_flops(spec), fill, agg_peak, bf16_peak_tflops())
     p50 = percentile(dev, 50)
     line = {
         "metric": METRIC,
@@ -610,6 +749,8 @@ def main():
     ap.add_argument("--ref-budget-s", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of striped swap")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the other 1-GPU configs (MLP, ResNet-50, GPT-2-XL) and the weight-distribution runs")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the other-engine comparison runs (e.g. under ncu, which serialises kernels)")
     args = ap.parse_args()

@@ -14,6 +14,7 @@
  * generated independently and in parallel with identical results.
  */
 #include <stdint.h>
+#include <math.h>
 #include <string.h>
 
 static inline uint64_t splitmix64(uint64_t x) {
@@ -72,5 +73,30 @@ void synth_int_bf16(uint16_t* out, uint64_t n, uint64_t seed, uint64_t stream, i
         int32_t v = lo + (int32_t)(unit(key, i) * span);
         if (v > hi) v = hi;
         out[i] = f32_to_bf16_rne((float)v);
+    }
+}
+
+/* Other weight distributions with a chosen standard deviation (bench: link-code ratio on bell-shaped
+ * and heavy-tailed weights).  Normal: Box-Muller over the pair (u(2i), u(2i+1));
+ * Laplace: inverse CDF of u(i) with scale b = sigma / sqrt(2).  Random numbers only. */
+void synth_normal_bf16(uint16_t* out, uint64_t n, uint64_t seed, uint64_t stream, double sigma) {
+    const uint64_t key = synth_key(seed, stream);
+    const double two_pi = 6.283185307179586476925286766559;
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)n; ++i) {
+        const double u1 = unit(key, 2 * (uint64_t)i), u2 = unit(key, 2 * (uint64_t)i + 1);
+        const double z = sqrt(-2.0 * log(1.0 - u1)) * cos(two_pi * u2);
+        out[i] = f32_to_bf16_rne((float)(sigma * z));
+    }
+}
+
+void synth_laplace_bf16(uint16_t* out, uint64_t n, uint64_t seed, uint64_t stream, double sigma) {
+    const uint64_t key = synth_key(seed, stream);
+    const double b = sigma / sqrt(2.0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < (int64_t)n; ++i) {
+        const double u = unit(key, (uint64_t)i) - 0.5;
+        const double x = u < 0 ? b * log(1.0 + 2.0 * u) : -b * log(1.0 - 2.0 * u);
+        out[i] = f32_to_bf16_rne((float)x);
     }
 }

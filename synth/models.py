@@ -34,7 +34,7 @@ _SO = os.path.join(_HERE, "libsynth.so")
 def build_lib(force: bool = False) -> str:
     src = os.path.join(_HERE, "csrc", "synth.c")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _SO, src])
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _SO, src, "-lm"])
     return _SO
 
 
@@ -51,7 +51,10 @@ def lib():
         _lib.synth_uniform_f32.argtypes = [vp, u64, u64, u64, dbl, dbl]
         _lib.synth_ids_i32.argtypes = [vp, u64, u64, u64, i32]
         _lib.synth_int_bf16.argtypes = [vp, u64, u64, u64, i32, i32]
-        for f in (_lib.synth_uniform_bf16, _lib.synth_uniform_f32, _lib.synth_ids_i32, _lib.synth_int_bf16):
+        _lib.synth_normal_bf16.argtypes = [vp, u64, u64, u64, dbl]
+        _lib.synth_laplace_bf16.argtypes = [vp, u64, u64, u64, dbl]
+        for f in (_lib.synth_uniform_bf16, _lib.synth_uniform_f32, _lib.synth_ids_i32, _lib.synth_int_bf16,
+                  _lib.synth_normal_bf16, _lib.synth_laplace_bf16):
             f.restype = None
     return _lib
 
@@ -142,6 +145,9 @@ class ModelSpec:
     input_slot: int = 0
     output_slot: int = -1
     input_kind: tuple = ("uniform_f32", 1.0)
+    # distribution of the ("uniform", a) bf16 tensors: "uniform" (U(±a), the default), or "gaussian" /
+    # "laplace" with the same standard deviation a/√3 (bench: link coding on bell-shaped weights)
+    dist: str = "uniform"
 
     # -- construction helpers ------------------------------------------------
     def tensor(self, name, shape, dtype=DT_BF16, init=("uniform", 0.02)) -> int:
@@ -214,7 +220,11 @@ class ModelSpec:
             else:
                 raise ValueError(kind)
             ptr = view.ctypes.data
-            if t.dtype == DT_BF16:
+            if t.dtype == DT_BF16 and kind == "uniform" and self.dist != "uniform":
+                sigma = t.init[1] / math.sqrt(3.0)
+                gen = {"gaussian": L.synth_normal_bf16, "laplace": L.synth_laplace_bf16}[self.dist]
+                gen(ptr, t.numel, self.seed, tid + 1, sigma)
+            elif t.dtype == DT_BF16:
                 L.synth_uniform_bf16(ptr, t.numel, self.seed, tid + 1, lo, hi)
             elif t.dtype == DT_F32:
                 L.synth_uniform_f32(ptr, t.numel, self.seed, tid + 1, lo, hi)

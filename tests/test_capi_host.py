@@ -240,6 +240,21 @@ def test_synth_is_deterministic_and_seeded():
     assert ids.min() >= 0 and ids.max() < 30522 and len(np.unique(ids)) > 100
 
 
+@pytest.mark.parametrize("dist,kurt", [("uniform", -1.2), ("gaussian", 0.0), ("laplace", 3.0)])
+def test_synth_weight_distributions_have_the_stated_sigma_and_shape(dist, kurt):
+    """bench.py's link-code runs on bell-shaped / heavy-tailed weights: same σ (0.02 for BERT's linears),
+    excess kurtosis of U / N / Laplace (−1.2, 0, 3)."""
+    from scipy import stats
+    from synth.models import bf16_bits_to_f64
+    s = synth.build_model("bert-tiny")
+    s.dist = dist
+    w = s.build_weights()
+    t = s.tensors[s.tensor_index("embeddings.word")]
+    v = bf16_bits_to_f64(w[t.offset:t.offset + t.nbytes].view(np.uint16))
+    assert v.std() == pytest.approx(0.02, rel=0.02)
+    assert stats.kurtosis(v) == pytest.approx(kurt, abs=0.15)
+
+
 # ---------------------------------------------------------------------------------------------
 # DMA engine copy plan (host logic of the swap engine, DESIGN.md §5)
 # ---------------------------------------------------------------------------------------------
