@@ -311,14 +311,21 @@ def roofline_report(spec, p50_ms, link_gbs, peak_tf, coded=None):
     return r
 
 
-def measure_cold(rt, mid, x, out, reps, warm, **kw):
-    """`warm` untimed then `reps` cold invokes (evict everywhere first, SURVEY §8c reading #10)."""
-    st = []
-    for i in range(warm + reps):
+def measure_cold(rt, mid, x, out, reps, warm, warm_s=0.5, **kw):
+    """At least `warm` untimed cold invokes and `warm_s` seconds of them (a small model's invokes are too
+    short to bring the SM clock up from idle: MLP measured 0.20-0.23 ms right after a registration, 0.140 ms
+    once the GPU is loaded; tools/probe_mlp_order.py), then `reps` timed cold invokes (evicted everywhere
+    first, SURVEY §8c reading #10)."""
+    t0 = time.perf_counter()
+    i = 0
+    while i < warm or time.perf_counter() - t0 < warm_s:
         rt.evict(mid, -1)
-        s = rt.invoke(mid, x, out=out, gpu=0, **kw).stats
-        if i >= warm:
-            st.append(s)
+        rt.invoke(mid, x, out=out, gpu=0, **kw)
+        i += 1
+    st = []
+    for _ in range(reps):
+        rt.evict(mid, -1)
+        st.append(rt.invoke(mid, x, out=out, gpu=0, **kw).stats)
     return st
 
 

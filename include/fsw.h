@@ -289,6 +289,7 @@ typedef struct {
     uint32_t n_resident, n_extents;
     uint64_t n_evictions, bytes_swapped_total, n_invokes_cold, n_invokes_warm;
     uint64_t prefix_bytes_cached;     /* valid cached prefixes held on this GPU (NEXT #4)     */
+    uint64_t n_evictions_heavy;       /* of n_evictions: models in the heavy class when evicted */
 } fsw_pool_stats;
 fsw_status fsw_pool_stats_get(fsw_ctx* ctx, int32_t gpu, fsw_pool_stats* out);
 fsw_status fsw_n_gpus(fsw_ctx* ctx, uint32_t* n);
@@ -382,11 +383,24 @@ fsw_status fsw_policy_eviction_order(uint32_t n, const uint8_t* heavy, const uin
  * sources.  The runtime deals its striped swaps with this function.  EINVAL on NULL / n_src == 0. */
 fsw_status fsw_policy_stripe_deal(uint32_t n_units, const int32_t* unit_node, uint32_t n_src, const int32_t* src_node,
                                   uint32_t* out);
-/* Heavy / light class of a model for placement and eviction: 1 heavy, 0 light, −1 auto (heavy
- * while unmeasured; then heavy iff mean cold / mean resident device latency > 1.25, SPEC S:77's
- * threshold on P:839's "pipelining significantly slows down the inference").                  */
+/* Heavy / light (heavy when "model pipelining significantly slows down the inference
+ * execution"; the class drives Algorithm 1's neighbour test and the eviction groups).
+ * Re-derived for B200: with swap = the swap's added latency (cold − resident), the
+ * model's SLO deadline and a queueing budget,
+ *     slack = deadline − resident − queue_budget;   heavy  iff  slack <= 0  or  swap > theta · slack;
+ * without a deadline (deadline <= 0) SPEC S:43-51's execution-relative rule: heavy iff
+ * resident + swap > 1.25 · resident.  EINVAL on a negative time, theta <= 0.                   */
+fsw_status fsw_policy_heavy(double swap_ms, double resident_ms, double deadline_ms, double queue_budget_ms, double theta,
+                            int32_t* heavy);
+/* A model's class: 1 heavy, 0 light, −1 auto = fsw_policy_heavy on its measured mean cold and resident
+ * device latencies (before both are measured: swap ≈ link bytes / 55 GB/s, resident 0), its tightest
+ * SLO (fsw_model_set_slo; fsw_function_register sets it) and the context's theta / queue budget
+ * (fsw_set_heavy_policy; defaults 0.05 and 0 ms).                                              */
 fsw_status fsw_model_set_heavy(fsw_ctx* ctx, uint32_t model_id, int32_t heavy);
 fsw_status fsw_model_is_heavy(fsw_ctx* ctx, uint32_t model_id, int32_t* heavy);
+/* Record a deadline of a function served by the model (the tightest one is kept).  EINVAL if <= 0. */
+fsw_status fsw_model_set_slo(fsw_ctx* ctx, uint32_t model_id, double deadline_ms);
+fsw_status fsw_set_heavy_policy(fsw_ctx* ctx, double theta, double queue_budget_ms);
 
 /* ---------------------------------------------------------------------------------------
  * Request scheduler: functions = (model, deadline, tail percentile p);

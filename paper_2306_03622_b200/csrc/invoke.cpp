@@ -5,12 +5,37 @@
 // ==========================================================================================
 // pool residency
 // ==========================================================================================
-// Heavy / light: set by the caller, or measured — heavy iff pipelined swapping slows
-// the inference down by more than 1.25x — and heavy while unmeasured.
-bool model_heavy(const Model& m) {
+// Heavy / light: set by the caller, else heavy_by_slo (policy.h) on the
+// swap's added latency = mean cold − mean resident device time, measured; before both were measured
+// the swap time is estimated from the bytes that cross the link (the coded store for a link-coded model)
+// at 55 GB/s (the copy engine's measured PCIe rate) and the resident time as 0.
+bool model_heavy(const fsw_ctx* c, const Model& m) {
     if (m.heavy >= 0) return m.heavy != 0;
-    if (!m.n_cold_runs || !m.n_warm_runs) return true;
-    return (m.cold_ms_sum / m.n_cold_runs) > 1.25 * (m.warm_ms_sum / m.n_warm_runs);
+    double swap_ms, res_ms = 0.0;
+    if (m.n_cold_runs && m.n_warm_runs) {
+        res_ms = m.warm_ms_sum / (double)m.n_warm_runs;
+        swap_ms = std::max(0.0, m.cold_ms_sum / (double)m.n_cold_runs - res_ms);
+    } else {
+        swap_ms = (double)(m.zstore ? m.zbytes : m.store_bytes) / 55e6;
+    }
+    return heavy_by_slo(swap_ms, res_ms, m.slo_ms, c->queue_budget_ms, c->heavy_theta);
+}
+
+extern "C" fsw_status fsw_model_set_slo(fsw_ctx* c, uint32_t id, double deadline_ms) {
+    if (!c || !(deadline_ms > 0.0)) return fail(FSW_EINVAL, "model_set_slo: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    Model* m = c->models.size() > id ? c->models[id].get() : nullptr;
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    m->slo_ms = m->slo_ms > 0.0 ? std::min(m->slo_ms, deadline_ms) : deadline_ms;
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_set_heavy_policy(fsw_ctx* c, double theta, double queue_budget_ms) {
+    if (!c || !(theta > 0.0) || !(queue_budget_ms >= 0.0)) return fail(FSW_EINVAL, "set_heavy_policy: bad argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->heavy_theta = theta;
+    c->queue_budget_ms = queue_budget_ms;
+    return FSW_OK;
 }
 
 extern "C" fsw_status fsw_model_set_heavy(fsw_ctx* c, uint32_t id, int32_t heavy) {
@@ -27,7 +52,7 @@ extern "C" fsw_status fsw_model_is_heavy(fsw_ctx* c, uint32_t id, int32_t* heavy
     std::lock_guard<std::mutex> lk(c->mu);
     Model* m = c->models.size() > id ? c->models[id].get() : nullptr;
     if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
-    *heavy = model_heavy(*m) ? 1 : 0;
+    *heavy = model_heavy(c, *m) ? 1 : 0;
     return FSW_OK;
 }
 
@@ -74,7 +99,7 @@ static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
         for (auto& o : c->models) {
             if (!o || o.get() == &m || o->extent[gi] < 0) continue;
             cand.push_back(o.get());
-            heavy.push_back(model_heavy(*o));
+            heavy.push_back(model_heavy(c, *o));
             uint32_t k = 0;
             for (size_t i = 0; i < o->extent.size(); ++i) k += o->extent[i] >= 0 && o->complete[i];
             copies.push_back(k);
@@ -85,6 +110,7 @@ static fsw_status ensure_extent(fsw_ctx* c, Model& m, int gi) {
         if (!order.empty()) {
             invalidate(c, *cand[order[0]], gi, /*keep_prefix=*/true);
             g.n_evictions++;
+            g.n_evictions_heavy += heavy[order[0]];
             continue;
         }
         Model* pv = nullptr;  // then the least recently used idle cached prefix
@@ -279,7 +305,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             srcs.clear();
             slots.clear();
         }
-        if (ss == FSW_OK && cold && peer < 0) g.loading = model_heavy(*m) ? 2 : 1;  // host link in use
+        if (ss == FSW_OK && cold && peer < 0) g.loading = model_heavy(c, *m) ? 2 : 1;  // host link in use
         if (ss != FSW_OK) {
             for (SrcSlot* sl : slots) sl->busy = false;
             if (cold) invalidate(c, *m, gi);

@@ -38,6 +38,16 @@ Decision schedule(const std::vector<uint8_t>& available, const std::vector<uint8
 std::vector<uint32_t> eviction_order(const std::vector<uint8_t>& heavy, const std::vector<uint32_t>& copies,
                                      const std::vector<uint64_t>& last_use, const std::vector<uint8_t>& in_use);
 
+// Heavy / light (a model is heavy when "model pipelining significantly slows down the
+// inference", i.e. its swap is the bottleneck; used by Algorithm 1 and the eviction policy).
+// Re-derived for B200: at batch 1 every model's swap is many times its
+// sub-millisecond execution, so the paper's execution-relative test (cold / resident >
+// 1.25) calls every model heavy.  With an SLO the test is against the request's latency budget instead:
+//   slack = deadline − resident − queue_budget;  heavy  iff  slack <= 0  or  swap > theta · slack,
+// swap = the swap's added latency (cold − resident).  Without an SLO (deadline <= 0) SPEC's rule:
+// heavy iff resident + swap > 1.25 · resident (strict).  Monotone: more swap time never turns heavy light.
+bool heavy_by_slo(double swap_ms, double resident_ms, double deadline_ms, double queue_budget_ms, double theta);
+
 // Striped swap: deal units (pieces, or runs of coded pieces) in execution order to
 // the sources so each unit is read by a source on the NUMA node holding its host pages: unit u goes to
 // the sources whose node equals unit_node[u], round-robin among them (a counter per node); a unit whose

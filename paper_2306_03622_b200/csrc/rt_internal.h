@@ -179,6 +179,7 @@ struct Model {
     int inflight = 0;
     // heavy / light class for placement and eviction: 1, 0, or -1 auto
     int heavy = -1;
+    double slo_ms = 0;  // tightest deadline of the functions serving this model (0 = none)
     double cold_ms_sum = 0, warm_ms_sum = 0;
     uint64_t n_cold_runs = 0, n_warm_runs = 0;
 };
@@ -228,6 +229,7 @@ struct Gpu {
     uint64_t generation = 0;
     // stats
     uint64_t n_evictions = 0, bytes_swapped_total = 0, n_cold = 0, n_warm = 0;
+    uint64_t n_evictions_heavy = 0;  // evictions of a model in the heavy class at the time
 };
 
 constexpr uint64_t kStageHdr = 256;
@@ -250,6 +252,7 @@ struct fsw_ctx {
     std::vector<int> gpu_node, nodes;
     bool fake_numa = false;               // FSW_FAKE_NUMA=k: pretend pool GPU i is on node i % k (no mbind)
     uint32_t fault_kind = 0, fault_index = 0, fault_gen = 0;  // fsw_debug_set_fault (tests)
+    double heavy_theta = 0.05, queue_budget_ms = 0.0;          // heavy / light policy (fsw_set_heavy_policy)
 };
 
 
@@ -342,5 +345,5 @@ fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vecto
 fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out);
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 PFN_writeValue32 get_write_value32();                                           // graph.cpp: cuStreamWriteValue32
-bool model_heavy(const Model& m);                                                // invoke.cpp
+bool model_heavy(const fsw_ctx* c, const Model& m);                              // invoke.cpp
 void invalidate(fsw_ctx* c, Model& m, int gi, bool keep_prefix = false);         // invoke.cpp

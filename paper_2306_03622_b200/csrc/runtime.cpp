@@ -321,6 +321,7 @@ extern "C" fsw_status fsw_pool_stats_get(fsw_ctx* c, int32_t gpu, fsw_pool_stats
         if (m && m->pextent[gpu] >= 0 && m->pvalid[gpu]) out->prefix_bytes_cached += m->split;
     }
     out->n_evictions = g.n_evictions;
+    out->n_evictions_heavy = g.n_evictions_heavy;
     out->bytes_swapped_total = g.bytes_swapped_total;
     out->n_invokes_cold = g.n_cold;
     out->n_invokes_warm = g.n_warm;

@@ -113,6 +113,12 @@ Decision schedule(const std::vector<uint8_t>& available, const std::vector<uint8
     return d;
 }
 
+bool heavy_by_slo(double swap_ms, double resident_ms, double deadline_ms, double queue_budget_ms, double theta) {
+    if (deadline_ms <= 0.0) return resident_ms + swap_ms > 1.25 * resident_ms;
+    const double slack = deadline_ms - resident_ms - queue_budget_ms;
+    return slack <= 0.0 || swap_ms > theta * slack;
+}
+
 std::vector<uint32_t> eviction_order(const std::vector<uint8_t>& heavy, const std::vector<uint32_t>& copies,
                                      const std::vector<uint64_t>& last_use, const std::vector<uint8_t>& in_use) {
     std::vector<uint32_t> low, high;
@@ -193,6 +199,14 @@ extern "C" fsw_status fsw_policy_stripe_deal(uint32_t n_units, const int32_t* un
     const std::vector<uint32_t> r = fsw::stripe_deal(std::vector<int>(unit_node, unit_node + n_units),
                                                      std::vector<int>(src_node, src_node + n_src));
     std::copy(r.begin(), r.end(), out);
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_policy_heavy(double swap_ms, double resident_ms, double deadline_ms, double queue_budget_ms,
+                                       double theta, int32_t* heavy) {
+    if (!heavy || !(swap_ms >= 0.0) || !(resident_ms >= 0.0) || !(theta > 0.0) || !(queue_budget_ms >= 0.0))
+        return FSW_EINVAL;
+    *heavy = heavy_by_slo(swap_ms, resident_ms, deadline_ms, queue_budget_ms, theta) ? 1 : 0;
     return FSW_OK;
 }
 
@@ -410,6 +424,8 @@ extern "C" fsw_status fsw_function_register(fsw_sched* s, uint32_t model_id, dou
     if (!s || !fid || !(deadline_ms > 0) || !(p > 0 && p < 1)) return FSW_EINVAL;
     fsw_model_info mi;
     if (fsw_model_info_get(s->ctx, model_id, &mi) != FSW_OK) return FSW_ENOTFOUND;
+    // the model's class is judged against its tightest deadline
+    if (fsw_model_set_slo(s->ctx, model_id, deadline_ms) != FSW_OK) return FSW_ENOTFOUND;
     std::lock_guard<std::mutex> lk(s->mu);
     Func f;
     f.model = model_id;

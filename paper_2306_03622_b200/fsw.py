@@ -100,7 +100,7 @@ class InvokeOpts(ctypes.Structure):
 class PoolStats(ctypes.Structure):
     _fields_ = [("capacity", u64), ("used", u64), ("largest_free", u64), ("n_resident", u32), ("n_extents", u32),
                 ("n_evictions", u64), ("bytes_swapped_total", u64), ("n_invokes_cold", u64),
-                ("n_invokes_warm", u64), ("prefix_bytes_cached", u64)]
+                ("n_invokes_warm", u64), ("prefix_bytes_cached", u64), ("n_evictions_heavy", u64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -148,7 +148,8 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
            "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal",
-           "fsw_debug_set_fault", "fsw_debug_litmus"]
+           "fsw_debug_set_fault", "fsw_debug_litmus", "fsw_policy_heavy", "fsw_model_set_slo",
+           "fsw_set_heavy_policy"]
 
 _lib = None
 
@@ -183,6 +184,9 @@ def lib():
         L.fsw_debug_coded_pieces.argtypes = [vp, u32, vp, u32, ctypes.POINTER(u32)]
         L.fsw_debug_dmaz_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
         L.fsw_debug_set_fault.argtypes = [vp, u32, u32]
+        L.fsw_policy_heavy.argtypes = [dbl, dbl, dbl, dbl, dbl, ctypes.POINTER(i32)]
+        L.fsw_model_set_slo.argtypes = [vp, u32, dbl]
+        L.fsw_set_heavy_policy.argtypes = [vp, dbl, dbl]
         L.fsw_debug_litmus.argtypes = [vp, u32, i32, u32, u32, u32, ctypes.POINTER(u64), ctypes.POINTER(u64)]
         L.fsw_arena_create.argtypes = [u64, u64]
         L.fsw_arena_create.restype = vp
@@ -384,6 +388,12 @@ class Runtime:
         _check(lib().fsw_model_is_heavy(self.h, mid, ctypes.byref(h)))
         return bool(h.value)
 
+    def set_slo(self, mid: int, deadline_ms: float):
+        _check(lib().fsw_model_set_slo(self.h, mid, deadline_ms))
+
+    def set_heavy_policy(self, theta: float = 0.05, queue_budget_ms: float = 0.0):
+        _check(lib().fsw_set_heavy_policy(self.h, theta, queue_budget_ms))
+
     def evict(self, mid: int, gpu: int = -1, keep_prefix: bool = False):
         _check(lib().fsw_evict_ex(self.h, mid, gpu, EVICT_KEEP_PREFIX if keep_prefix else 0))
 
@@ -501,6 +511,13 @@ def policy_schedule(available, hosts, neighbor=None, loading=None, link=None):
         return None
     _check(rc)
     return d.gpu, d.kind, d.src
+
+
+def policy_heavy(swap_ms: float, resident_ms: float, deadline_ms: float = 0.0, queue_budget_ms: float = 0.0,
+                 theta: float = 0.05) -> bool:
+    h = i32()
+    _check(lib().fsw_policy_heavy(swap_ms, resident_ms, deadline_ms, queue_budget_ms, theta, ctypes.byref(h)))
+    return bool(h.value)
 
 
 def policy_eviction_order(heavy, copies, last_use, in_use):

@@ -219,3 +219,47 @@ def test_stripe_deal_balance_property():
         counts = [int(np.sum(out[units == node] == j)) for j in mine]
         assert max(counts) - min(counts) <= 1
         assert set(np.unique(out[units == node])) <= set(mine)
+
+
+# ---------------------------------------------------------------------------------------------
+# heavy / light (re-derived for B200 against the SLO slack)
+# ---------------------------------------------------------------------------------------------
+def test_heavy_spec_vectors_without_slo():
+    # SPEC S:43-51 examples (Table 4): pipeline / exec > 1.25 strictly
+    assert F.policy_heavy(29.0 - 19.0, 19.0)          # ResNet-152: 29 vs 19 -> 1.53 -> heavy
+    assert not F.policy_heavy(27.0 - 25.0, 25.0)      # DenseNet-169: 27 vs 25 -> 1.08 -> light
+    assert not F.policy_heavy(2.5, 10.0)              # exactly 1.25 -> light (strict)
+    assert F.policy_heavy(2.5 + 1e-9, 10.0)
+
+
+def test_heavy_by_slo_slack_hand_computed():
+    # B200 measurements (bench r2): swap added latency = cold - resident; deadlines of the trace
+    # GPT-2-XL: slack = 500 - 3.19 = 496.81, 0.05 * slack = 24.84 < 35.27 -> heavy
+    assert F.policy_heavy(38.46 - 3.19, 3.19, 500.0)
+    # BERT-base: slack = 200 - 0.59 = 199.41 -> budget 9.97 > 2.24 -> light
+    assert not F.policy_heavy(2.83 - 0.59, 0.59, 200.0)
+    # ResNet-50: slack = 80 - 0.44 = 79.56 -> budget 3.98 > 0.28 -> light
+    assert not F.policy_heavy(0.72 - 0.44, 0.44, 80.0)
+    # a queueing budget shrinks the slack: 200 - 0.59 - 150 = 49.41 -> 2.47 > 2.24 -> still light; 160 -> heavy
+    assert not F.policy_heavy(2.24, 0.59, 200.0, queue_budget_ms=150.0)
+    assert F.policy_heavy(2.24, 0.59, 200.0, queue_budget_ms=160.0)   # slack 39.41 -> 1.97 < 2.24
+    assert F.policy_heavy(0.0, 90.0, 80.0)            # no slack at all: any swap misses the deadline
+    assert F.policy_heavy(10.0, 1.0, 100.0, theta=0.1)    # 0.1 * 99 = 9.9 < 10
+    assert not F.policy_heavy(9.8, 1.0, 100.0, theta=0.1)
+
+
+def test_heavy_is_monotone_in_swap_time():
+    # SPEC invariant: more transfer never flips heavy -> light
+    rng = np.random.default_rng(9)
+    for _ in range(300):
+        res, dl, qb = rng.uniform(0, 5), rng.choice([0.0, rng.uniform(1, 500)]), rng.uniform(0, 50)
+        s = np.sort(rng.uniform(0, 100, 6))
+        h = [F.policy_heavy(float(x), float(res), float(dl), float(qb)) for x in s]
+        assert h == sorted(h)
+
+
+def test_heavy_rejects_bad_arguments():
+    with pytest.raises(F.FswError):
+        F.policy_heavy(-1.0, 1.0)
+    with pytest.raises(F.FswError):
+        F.policy_heavy(1.0, 1.0, 10.0, theta=0.0)

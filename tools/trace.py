@@ -56,6 +56,10 @@ def main():
     ap.add_argument("--period-ms", type=float, default=2000.0)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "trace.json"))
     ap.add_argument("--link-code", action="store_true", help="register every model link-coded (DESIGN.md §5b)")
+    ap.add_argument("--theta", type=float, default=0.05, help="heavy iff swap > theta x SLO slack (DESIGN.md §7c)")
+    ap.add_argument("--queue-budget-ms", type=float, default=0.0)
+    ap.add_argument("--all-heavy", action="store_true",
+                    help="force every model heavy (the paper's execution-relative rule at batch 1 on B200)")
     args = ap.parse_args()
     counts = [int(c) for c in args.mix.split(",")]
     kinds = ["resnet50"] * counts[0] + ["bert-base"] * counts[1] + ["gpt2-xl"] * counts[2]
@@ -72,8 +76,13 @@ def main():
         outs.append(rt.model_info(mids[-1])["output_bytes"])
     print(f"registered {len(kinds)} functions in {time.time() - t0:.1f}s", flush=True)
 
+    rt.set_heavy_policy(args.theta, args.queue_budget_ms)
+    if args.all_heavy:
+        for m in mids:
+            rt.set_heavy(m, 1)
     sched = Scheduler(rt, period_ms=args.period_ms)
     fids = [sched.register_function(m, DEADLINE_MS[k], args.p) for m, k in zip(mids, kinds)]
+    heavy0 = {k: sum(rt.is_heavy(m) for m, kk in zip(mids, kinds) if kk == k) for k in set(kinds)}
     trace = poisson_trace(rates, args.duration_s * 1000.0, args.seed)
     print(f"trace: {len(trace)} requests over {args.duration_s:.0f}s ({len(trace) / args.duration_s:.1f} req/s)", flush=True)
 
@@ -103,7 +112,15 @@ def main():
         "latency_ms": {k: {"p50": round(float(np.percentile(v, 50)), 3), "p98": round(float(np.percentile(v, 98)), 3),
                            "deadline": DEADLINE_MS[k], "n": len(v)} for k, v in per_class.items()},
         "pool": rt.pool_stats(0),
+        # heavy / light split: models per class before the run (estimated swap time) and
+        # after it (measured), and how many evictions hit heavy models
+        "heavy_policy": {"theta": args.theta, "queue_budget_ms": args.queue_budget_ms, "all_heavy": args.all_heavy},
+        "heavy_models_before": heavy0,
+        "heavy_models_after": {k: sum(rt.is_heavy(m) for m, kk in zip(mids, kinds) if kk == k) for k in set(kinds)},
+        "models_per_kind": {k: kinds.count(k) for k in set(kinds)},
     }
+    summary["eviction_mix"] = {"total": summary["pool"]["n_evictions"], "heavy": summary["pool"]["n_evictions_heavy"],
+                               "light": summary["pool"]["n_evictions"] - summary["pool"]["n_evictions_heavy"]}
     print(json.dumps(summary), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(summary, open(args.out, "w"), indent=1)
