@@ -658,7 +658,7 @@ def run_striped(args):
     ranks only join the barriers.  Total work is fixed as N grows: strong scaling."""
     import synth
     import torch.distributed as dist
-    from paper_2306_03622_b200 import ENGINE_SMZ, Runtime
+    from paper_2306_03622_b200 import Runtime
 
     rank, world, _ = dist_env()
     dist.init_process_group("gloo")
@@ -682,8 +682,7 @@ def run_striped(args):
 
     def cold_step():
         rt.evict(mid, -1)
-        return rt.invoke(mid, x, out=out, gpu=0, stripe=src,
-                         engine=0 if args.no_link_code else ENGINE_SMZ).stats
+        return rt.invoke(mid, x, out=out, gpu=0, stripe=src, engine=args.engine).stats
 
     for _ in range(args.warmup):
         cold_step()

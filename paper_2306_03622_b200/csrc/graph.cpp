@@ -250,6 +250,61 @@ fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_nod
     return FSW_OK;
 }
 
+// DMAZ striped swap: the coded pieces >= from cut into runs of ~run_bytes contiguous coded bytes (whole
+// pieces, execution order), each run dealt to a source on the NUMA node of its first byte (stripe_deal).
+// Source j copies its runs with its copy engine, back to back, into its own staging buffer (run k at
+// staging offset Σ earlier runs), publishing the run count after each, and its decode kernel decodes the
+// run's pieces from there into the target.  groups = the runs [lo, hi) of the coded store; each piece's
+// coff is rewritten to its staging offset and grp to its run's index (stream 0).
+fsw_status get_zstripe_dma(Model& m, Plan& p, const std::vector<int>& src_node, uint32_t j, int dev, uint64_t from,
+                           uint64_t run_bytes, ZPieceSet** out) {
+    const auto key = std::make_tuple(nodes_key(src_node), j, dev, from, run_bytes);
+    auto it = p.zstripe_dma.find(key);
+    if (it != p.zstripe_dma.end()) {
+        *out = &it->second;
+        return FSW_OK;
+    }
+    std::vector<const ZPiece*> sel;
+    for (const ZPiece& pc : m.zpieces)
+        if (pc.off >= from) sel.push_back(&pc);
+    if (sel.empty()) return fail(FSW_EINVAL, "link-coded swap with nothing to move");
+    const uint64_t cend = align_up(sel.back()->coff + sel.back()->cbytes, 128);
+    std::vector<std::pair<size_t, size_t>> runs;  // [first, last) piece index
+    for (size_t a = 0; a < sel.size();) {
+        size_t b = a + 1;
+        while (b < sel.size() && sel[b]->coff - sel[a]->coff < run_bytes) ++b;
+        runs.push_back({a, b});
+        a = b;
+    }
+    std::vector<int> unit_node;
+    for (auto& r : runs) unit_node.push_back(chunk_node(m.zstore_node, sel[r.first]->coff));
+    const std::vector<uint32_t> owner = stripe_deal(unit_node, src_node);
+    ZPieceSet zs;
+    uint64_t soff = 0;
+    for (size_t k = 0; k < runs.size(); ++k) {
+        if (owner[k] != j) continue;
+        const uint64_t lo = sel[runs[k].first]->coff, hi = runs[k].second < sel.size() ? sel[runs[k].second]->coff : cend;
+        const uint32_t gi = (uint32_t)zs.groups.size();
+        zs.groups.push_back({lo, hi, 0});
+        for (size_t q = runs[k].first; q < runs[k].second; ++q) {
+            ZPiece pc = *sel[q];
+            pc.coff = soff + (pc.coff - lo);
+            pc.grp = gi;
+            zs.host.push_back(pc);
+        }
+        soff += hi - lo;
+    }
+    zs.cfrom = 0;
+    zs.cend = soff;  // staging bytes this source needs
+    CU(cudaSetDevice(dev));
+    if (!zs.host.empty()) {
+        CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
+        CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
+    }
+    *out = &p.zstripe_dma.emplace(key, std::move(zs)).first->second;
+    return FSW_OK;
+}
+
 // Striped swap: the execution-order piece list of the SM engine dealt round-robin to n sources
 // (piece q goes to source q mod n), so every source streams a share of every layer and all of them
 // advance through the model together; source j's table is allocated on source j's device.

@@ -347,8 +347,11 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
                            : (big ? FSW_ENGINE_DMA : FSW_ENGINE_SM);
     if (engine_coded(engine) && !m->zstore) return finish(fail(FSW_EINVAL, "invoke: model %u is not link-coded (FSW_REG_LINK_CODE)", id));
-    // striped: sources store into the target with SM kernels (decoding ones for the coded engines)
-    if (striped) engine = engine_coded(engine) ? FSW_ENGINE_SMZ : FSW_ENGINE_SM;
+    // striped: sources store into the target with SM kernels (decoding ones for the coded engines):
+    // DMAZ sources copy their runs into their own staging buffer with their copy engine and decode from
+    // there (the copy engine's larger PCIe read requests: 55 vs 51.3 GB/s per link), SMZ
+    // sources read the coded store zero-copy, plain stores use k_swap
+    if (striped) engine = engine_coded(engine) ? (engine == FSW_ENGINE_DMAZ ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ) : FSW_ENGINE_SM;
     if (peer >= 0) engine = FSW_ENGINE_DMA;  // NVLink copy-engine transfer from the peer's extent
     const uint64_t dgrp = baseline ? (2ull << 20) : o.dma_group_bytes ? o.dma_group_bytes : c->cfg.dma_group_bytes;
     const uint32_t dstr = baseline ? 1u : o.dma_streams ? o.dma_streams : c->cfg.dma_streams;
@@ -396,9 +399,26 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     for (size_t j = 0; j < srcs.size(); ++j) {
         if (engine == FSW_ENGINE_SMZ)
             st = get_zstripe_pieces(*m, p, src_node, (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &zps[j]);
+        else if (engine == FSW_ENGINE_DMAZ)
+            st = get_zstripe_dma(*m, p, src_node, (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, kStripeRunBytes, &zps[j]);
         else
             st = get_stripe_pieces(*m, p, schunk, src_node, (uint32_t)j, c->gpus[srcs[j]].dev, ic.from, &sps[j]);
         if (st != FSW_OK) return finish(st);
+    }
+    for (size_t j = 0; striped && engine == FSW_ENGINE_DMAZ && j < srcs.size(); ++j) {
+        SrcSlot& sl = *slots[j];  // grow the source's staging buffer to its share of the coded bytes
+        if (sl.stage_cap >= zps[j]->cend) continue;
+        cudaSetDevice(c->gpus[srcs[j]].dev);
+        cudaFree(sl.stage);
+        sl.stage = nullptr;
+        sl.stage_cap = 0;
+        const uint64_t cap = align_up(std::max<uint64_t>(zps[j]->cend, 1), 64ull << 20);
+        if (cudaMalloc(&sl.stage, cap) != cudaSuccess) {
+            cudaGetLastError();
+            return finish(fail(FSW_ENOMEM, "invoke: striped staging buffer of %llu bytes on gpu %d", (unsigned long long)cap,
+                               c->gpus[srcs[j]].dev));
+        }
+        sl.stage_cap = cap;
     }
     if (striped) {
         cudaSetDevice(g.dev);
@@ -481,7 +501,28 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             cudaStreamWaitEvent(sl.st, g.evfork, 0);
             cudaMemsetAsync(sl.ctl, 0, sizeof(DevCtl), sl.st);
             // an empty share still starts its CTAs: the target's gate counts every source kernel
-            if (engine == FSW_ENGINE_SMZ)
+            if (engine == FSW_ENGINE_DMAZ) {
+                // copy engine: the source's runs, back to back, into its staging buffer, a fenced write of
+                // the run count after each; the decode kernel (own stream) waits per piece for its run
+                static PFN_writeValue32 wv = get_write_value32();
+                cudaMemsetAsync(sl.progress, 0, 128, sl.st);
+                if (c->cfg.flags & FSW_DEBUG_POISON) launch_poison(sl.st, sl.stage, sl.stage_cap, 0x5A5A0000u ^ (uint32_t)j);
+                cudaEventRecord(sl.evfork, sl.st);
+                cudaStreamWaitEvent(sl.sdec, sl.evfork, 0);
+                launch_swapz(sl.sdec, (int)ic.ctas, (int)c->cfg.copy_threads, sl.stage, 0, ic.dst, nullptr, zps[j]->dev,
+                             (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 1, sl.progress);
+                uint32_t cnt = 0;
+                uint64_t soff = 0;  // run k sits at the sum of the earlier runs' bytes (get_zstripe_dma)
+                for (size_t gi2 = 0; gi2 < zps[j]->groups.size(); ++gi2) {
+                    const auto& gr = zps[j]->groups[gi2];
+                    if (!(c->fault_kind == FSW_FAULT_DROP_GROUP && c->fault_index == gi2))
+                        cudaMemcpyAsync(sl.stage + soff, m->zstore + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sl.st);
+                    wv(sl.st, (CUdeviceptr)sl.progress, (cuuint32_t)(++cnt), 0);
+                    soff += gr.hi - gr.lo;
+                }
+                cudaEventRecord(sl.evjoin, sl.sdec);
+                cudaStreamWaitEvent(sl.st, sl.evjoin, 0);
+            } else if (engine == FSW_ENGINE_SMZ)
                 launch_swapz(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->zstore, 0, ic.dst, nullptr, zps[j]->dev,
                              (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 0, nullptr);
             else
@@ -534,7 +575,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                 stats->swap_span_ms = swap_ms;
                 stats->compute_tail_ms = tail > 0 ? tail : 0;
                 stats->n_kernels += (uint32_t)srcs.size() + (ic.no_overlap ? 0 : 1);  // sources (+ gate)
-                for (size_t j = 0; j < srcs.size(); ++j) stats->n_copies += (uint32_t)(coded ? zps[j]->host.size() : sps[j]->host.size());
+                for (size_t j = 0; j < srcs.size(); ++j) stats->n_copies += (uint32_t)(engine == FSW_ENGINE_DMAZ ? zps[j]->groups.size() : coded ? zps[j]->host.size() : sps[j]->host.size());
                 if (coded) {
                     stats->wire_bytes = 0;
                     for (ZPieceSet* zs : zps)

@@ -141,6 +141,8 @@ struct Plan {  // one model on one GPU
     // link-coded engines: (order, seed, from, DMAZ group bytes or 0 for SMZ) and striped (n, j, device, from)
     std::map<std::tuple<int, uint32_t, uint64_t, uint64_t, uint32_t>, ZPieceSet> zp;  // + DMAZ copy streams
     std::map<std::tuple<uint64_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;  // (sources' nodes, j, device, from)
+    // DMAZ striped: source j's runs of coded pieces (copy groups) and its pieces with coff = staging offset
+    std::map<std::tuple<uint64_t, uint32_t, int, uint64_t, uint64_t>, ZPieceSet> zstripe_dma;  // + run bytes
 };
 
 struct Model {
@@ -191,6 +193,13 @@ struct SrcSlot {
     cudaStream_t st = nullptr;
     cudaEvent_t done = nullptr;
     bool busy = false;
+    // DMAZ striped source (copy engine over this GPU's own host link into `stage`, then a decode kernel
+    // storing into the target): staging buffer, run counter, decode stream and its fork / join events
+    uint8_t* stage = nullptr;
+    uint64_t stage_cap = 0;
+    uint32_t* progress = nullptr;
+    cudaStream_t sdec = nullptr;
+    cudaEvent_t evfork = nullptr, evjoin = nullptr;
 };
 constexpr int kSrcSlots = 4;
 
@@ -342,6 +351,9 @@ fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_nod
                               ZPieceSet** out);
 fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vector<int>& src_node, uint32_t j, int dev,
                              uint64_t from, PieceSet** out);
+fsw_status get_zstripe_dma(Model& m, Plan& p, const std::vector<int>& src_node, uint32_t j, int dev, uint64_t from,
+                           uint64_t run_bytes, ZPieceSet** out);
+constexpr uint64_t kStripeRunBytes = 4ull << 20;  // DMAZ striped: coded bytes per copy run (>= ~8 us copy setup x 55 GB/s x 10)
 fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaGraphExec_t* out);
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 PFN_writeValue32 get_write_value32();                                           // graph.cpp: cuStreamWriteValue32

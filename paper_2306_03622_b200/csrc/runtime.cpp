@@ -120,8 +120,12 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaMalloc(&g.gemm_ctr, sizeof(uint32_t) * kGemmCtrs));
     for (SrcSlot& sl : g.src) {
         CU(cudaMalloc(&sl.ctl, sizeof(DevCtl)));
+        CU(cudaMalloc(&sl.progress, 128));
         CU(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&sl.sdec, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&sl.evfork, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&sl.evjoin, cudaEventDisableTiming));
     }
     CU(cudaMemset(g.gemm_ctr, 0, sizeof(uint32_t) * kGemmCtrs));
     CU(cudaMemset(g.progress, 0, 128 * kMaxWaitSrc));
@@ -239,6 +243,8 @@ void free_plan(Gpu& g, Plan& p) {
     p.zp.clear();
     for (auto& kv : p.zstripe) cudaFree(kv.second.dev);
     p.zstripe.clear();
+    for (auto& kv : p.zstripe_dma) cudaFree(kv.second.dev);
+    p.zstripe_dma.clear();
 }
 
 void free_store(Model& m, bool host_only) {
@@ -288,8 +294,13 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFree(g.gemm_ctr);
         for (SrcSlot& sl : g.src) {
             cudaFree(sl.ctl);
+            cudaFree(sl.progress);
+            cudaFree(sl.stage);
             cudaStreamDestroy(sl.st);
+            cudaStreamDestroy(sl.sdec);
             cudaEventDestroy(sl.done);
+            cudaEventDestroy(sl.evfork);
+            cudaEventDestroy(sl.evjoin);
         }
         cudaStreamDestroy(g.sx);
         cudaStreamDestroy(g.sc);

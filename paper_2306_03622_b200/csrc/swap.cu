@@ -18,11 +18,18 @@ __device__ uint32_t g_drop_piece = 0xffffffffu;
 
 void set_drop_piece(uint32_t index) { cudaMemcpyToSymbol(g_drop_piece, &index, sizeof index); }
 
+// A swap CTA has started: count it on the target's gate.  A remote source (sys) increments the target
+// GPU's counter over NVLink at system scope (the target's k_gate reads it with ld.acquire.sys).
+__device__ __forceinline__ void gate_arrive(DevCtl* gate, int sys) {
+    if (sys) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(&gate->started) : "memory");
+    else atomicAdd(&gate->started, 1u);
+}
+
 template <int U>
 __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, DevDesc dst, const DevDesc* __restrict__ desc,
                                               const Piece* __restrict__ pieces, uint32_t n_pieces,
                                               uint32_t* __restrict__ ready, DevCtl* __restrict__ own, DevCtl* gate, int sys) {
-    if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
+    if (threadIdx.x == 0) gate_arrive(gate, sys);
     const DevDesc dd = desc ? *desc : dst;
     const uint32_t lane = threadIdx.x & 31u, drop = g_drop_piece;
     for (;;) {
@@ -202,7 +209,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
                                                const DevDesc* __restrict__ desc, const ZPiece* __restrict__ pieces,
                                                uint32_t n_pieces, uint32_t* __restrict__ ready, DevCtl* __restrict__ own,
                                                DevCtl* gate, int sys, const uint32_t* progress) {
-    if (threadIdx.x == 0) atomicAdd(&gate->started, 1u);
+    if (threadIdx.x == 0) gate_arrive(gate, sys);
     const DevDesc dd = desc ? *desc : dst;
     const uint32_t lane = threadIdx.x & 31u, drop = g_drop_piece;
     for (;;) {
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, drop = g_drop_piece;
     const DevDesc dd = desc ? *desc : dst;
     if (tid == 0) {
-        atomicAdd(&gate->started, 1u);
+        gate_arrive(gate, sys);
         for (uint32_t b = 0; b < kZRing; ++b)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[b])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -481,9 +488,9 @@ void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uin
 // CTA is resident, so spinning layer CTAs can never occupy the SMs the swap needs
 // (no deadlock whatever the block scheduler does).  One thread; costs one launch.
 __global__ void k_gate(DevCtl* ctl, uint32_t expected) {
-    const volatile uint32_t* st = &ctl->started;
+    const uint32_t* st = &ctl->started;
     const uint64_t t0 = globaltimer();
-    while (*st < expected) {
+    while (ld_acquire_sys(st) < expected) {
         __nanosleep(256);
         if (globaltimer() - t0 > kWatchdogNs) {
             atomicExch(&ctl->err, 2);

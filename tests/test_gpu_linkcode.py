@@ -100,6 +100,47 @@ def test_striped_smz_virtual_sources_bit_exact(rt, coded, n_src):
         np.testing.assert_array_equal(r.output, base)
 
 
+@pytest.mark.parametrize("n_src", [1, 2, 3, 4])
+def test_striped_dmaz_virtual_sources_bit_exact(rt, coded, n_src):
+    """DMAZ striped sources: each source copies its 4-MiB runs of the coded store with its
+    copy engine into its own staging buffer and decodes them into the target (system-scope releases)."""
+    spec, w, x, plain, mid = coded("bert-base")
+    rt.evict(plain)
+    base = rt.invoke(plain, x, gpu=0, engine=ENGINE_SM).output.copy()
+    for flags in (0, NO_OVERLAP):
+        rt.evict(mid)
+        r = rt.invoke(mid, x, gpu=0, stripe=[0] * n_src, flags=flags, engine=ENGINE_DMAZ)
+        if n_src > 1:
+            assert r.stats["swap_kind"] == 3 and r.stats["engine"] == ENGINE_DMAZ, r.stats
+            assert r.stats["wire_bytes"] == int(rt.coded_pieces(mid)["cbytes"].sum())
+        np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+        np.testing.assert_array_equal(r.output, base)
+
+
+def test_striped_dmaz_two_pool_gpus_and_dropped_run(rt):
+    """Two pool GPUs on one device: pool GPU 1 is a DMAZ source of pool GPU 0.  A skipped copy run (fault
+    injection, still published) must show up as wrong bytes under poison mode (negative control)."""
+    from paper_2306_03622_b200 import FAULT_DROP_GROUP, FAULT_NONE, Runtime
+    spec = synth.build_model("bert-base")
+    w, x = spec.build_weights(), spec.make_input()
+    with Runtime(gpu_ids=[0, 0], pool_bytes=2 << 30) as rt2:
+        mid = rt2.register_spec(spec, w, link_code=True)
+        base = rt2.invoke(mid, x, gpu=0, engine=ENGINE_SM).output.copy()
+        for src in ([0, 1], [1, 0], [1]):
+            rt2.evict(mid)
+            r = rt2.invoke(mid, x, gpu=0, stripe=src, engine=ENGINE_DMAZ)
+            assert r.stats["swap_kind"] == 3
+            np.testing.assert_array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
+            np.testing.assert_array_equal(r.output, base)
+        rt2.evict(mid)
+        rt2.set_fault(FAULT_DROP_GROUP, 3)
+        try:
+            rt2.invoke(mid, x, gpu=0, stripe=[0, 1], engine=ENGINE_DMAZ)
+            assert not np.array_equal(rt2.read_resident(mid, 0), rt2.read_store(mid))
+        finally:
+            rt2.set_fault(FAULT_NONE)
+
+
 @pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
 def test_coded_with_cached_prefix(rt, coded, engine):
     """Partial caching (NEXT #4) + link coding: only the coded suffix moves."""
