@@ -60,6 +60,11 @@ typedef enum {
 #define FSW_NO_PEER_SWAP 0x10u /* never swap from another GPU's resident copy (Alg. 1 case 2 off)  */
 #define FSW_HOST_ONLY    0x8u /* no GPU: registration / host-store / allocator logic only (tests);
                                  invoke returns FSW_ECUDA                                       */
+#define FSW_TRACE        0x40u /* device timeline (also FSW_TRACE=1 in the environment at fsw_init): every
+                                 kernel records per layer its first CTA entry, last weight-wait completion
+                                 and last CTA exit, and the swap kernels the first / last release of the
+                                 layer's pieces (%globaltimer ns); read with fsw_debug_trace_read.  A
+                                 few atomics per CTA; off in the bench.                          */
 #define FSW_DEBUG_POISON 0x20u /* test mode (also set by the environment variable FSW_DEBUG_POISON=1 at
                                  fsw_init): before every cold invoke, fill the extents the swap will
                                  write (prefix + suffix) and the DMAZ staging buffer with a per-invoke
@@ -321,6 +326,15 @@ fsw_status fsw_debug_set_fault(fsw_ctx* ctx, uint32_t kind, uint32_t index);
  * or a coded engine on a model that is not link-coded.                                          */
 fsw_status fsw_debug_litmus(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint32_t engine, uint32_t ctas, uint32_t iters,
                             uint64_t* bad_words, uint64_t* checked_bytes);
+
+/* The device timeline of the last invoke of `model_id` on `gpu` (FSW_TRACE): out[5·L + i] for every layer
+ * L of the model = %globaltimer ns of i = 0 the first kernel CTA entry, 1 the last weight-wait completion,
+ * 2 the last CTA exit, 3 the first and 4 the last release of one of the layer's swap pieces (kernel
+ * engines; the copy engine records nothing); 0 = no event.  t_invoke (nullable, 3 entries): the
+ * invoke's first piece claimed, last piece released, graph end.  ESTATE without FSW_TRACE; EINVAL if
+ * cap_layers < the model's layers.                                                                   */
+fsw_status fsw_debug_trace_read(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint64_t* out, uint32_t cap_layers,
+                                uint64_t* t_invoke);
 
 /* Debug / test read-back (copies into caller host memory). */
 fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, void* dst, uint64_t cap);

@@ -50,6 +50,25 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
                  : "memory");
 }
 
+// Device timeline (kernels.h kTraceStride): g_trace is this translation unit's copy of the per-GPU trace
+// buffer (nullptr unless FSW_TRACE); one thread per CTA records, with atomicMax (min fields complemented).
+static __device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ void trace_max(int32_t layer, int field, unsigned long long v) {
+    unsigned long long* t = g_trace;
+    if (t && layer >= 0) atomicMax(t + (uint64_t)layer * kTraceStride + field, v);
+}
+__device__ __forceinline__ void trace_entry(int32_t layer) {
+    if (threadIdx.x == 0) trace_max(layer, 0, ~globaltimer());
+}
+// Records the CTA's exit when it goes out of scope (every return path); thread 0 of the CTA.
+struct TraceExit {
+    int32_t layer;
+    __device__ __forceinline__ explicit TraceExit(int32_t l) : layer(l) { trace_entry(l); }
+    __device__ __forceinline__ ~TraceExit() {
+        if (threadIdx.x == 0) trace_max(layer, 2, globaltimer());
+    }
+};
+
 // Layer-kernel side of the ready-flag protocol: one thread spins with
 // back-off until the layer's byte counter reaches its region size, then the caller does a
 // CTA barrier.  The acquire pairs with the swap kernel's red.release; the barrier extends
@@ -74,7 +93,10 @@ __device__ __forceinline__ void wait_ready_thread(const Wait& w) {
 
 __device__ __forceinline__ void wait_ready_cta(const Wait& w) {
     if (w.n == 0) return;
-    if (threadIdx.x == 0) wait_ready_thread(w);
+    if (threadIdx.x == 0) {
+        wait_ready_thread(w);
+        trace_max(w.layer, 1, globaltimer());
+    }
     __syncthreads();
 }
 

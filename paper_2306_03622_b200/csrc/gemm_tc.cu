@@ -180,6 +180,7 @@ constexpr int kGemmThreads = 512;  // warp 0 TMA producer, warp 1 MMA issuer, al
 template <int BN>
 __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA (<= 64 regs) still fits beside it
     k_gemm(const __grid_constant__ CUtensorMap tmA, const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
+    TraceExit tx(w.layer);
     using C = Cfg<BN>;
     constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
     extern __shared__ uint8_t smem_raw[];
@@ -237,7 +238,10 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     // the copies of the stage's sub-tile j: one thread issuing every TMA / bulk copy back to back was the
     // producer's critical path), lane 0 of warp 1 issues the MMAs; the other lanes of warp 1 park.
     if (warp == 0) {
-        if (lane == 0) wait_ready_thread(w);
+        if (lane == 0) {
+            wait_ready_thread(w);
+            trace_max(w.layer, 1, globaltimer());
+        }
         __syncwarp();  // the weights lane 0 acquired are visible to the warp
         asm volatile("fence.proxy.async.global;" ::: "memory");
         const uint8_t* wt = weight_ptr(dd, a.w_off);
@@ -539,6 +543,7 @@ struct G2Cfg {
 template <int TT>
 __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                                                const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
+    TraceExit tx(w.layer);
     using C = G2Cfg<TT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -580,7 +585,10 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
         uint32_t lead[8];  // the leader's full barriers, in the cluster window
         for (int s = 0; s < stages && s < 8; ++s)
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead[s]) : "r"(smem_u32(&full[s])));
-        if (lane == 0) wait_ready_thread(w);
+        if (lane == 0) {
+            wait_ready_thread(w);
+            trace_max(w.layer, 1, globaltimer());
+        }
         __syncwarp();
         asm volatile("fence.proxy.async.global;" ::: "memory");
         auto arm = [&](uint32_t st0, uint32_t st1) {
@@ -830,5 +838,7 @@ bool make_tmap_conv(CUtensorMap* map, const void* base, uint32_t H, uint32_t W, 
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+
+void set_trace_gemm(unsigned long long* t) { cudaMemcpyToSymbol(g_trace, &t, sizeof t); }
 
 }  // namespace fsw

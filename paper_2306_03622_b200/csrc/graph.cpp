@@ -362,10 +362,26 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
             case K_LN: launch_layernorm(s, d, w, x.ln); break;
             case K_GEMV: launch_gemv(s, d, w, x.gemv); break;
             case K_GEMM: launch_gemm(s, d, w, &x.tmap, x.gemm, &g.wmap); break;
-            case K_ATTN: launch_attention(s, x.attn); break;
-            case K_IM2COL: launch_im2col(s, x.im2col); break;
-            case K_MAXPOOL: launch_maxpool(s, x.pool); break;
-            case K_AVGPOOL: launch_avgpool(s, x.pool); break;
+            case K_ATTN: {
+                AttnArgs a = x.attn;
+                a.layer = x.layer;
+                launch_attention(s, a);
+                break;
+            }
+            case K_IM2COL: {
+                Im2colArgs a = x.im2col;
+                a.layer = x.layer;
+                launch_im2col(s, a);
+                break;
+            }
+            case K_MAXPOOL:
+            case K_AVGPOOL: {
+                PoolArgs a = x.pool;
+                a.layer = x.layer;
+                if (x.kind == K_MAXPOOL) launch_maxpool(s, a);
+                else launch_avgpool(s, a);
+                break;
+            }
         }
     }
 }

@@ -479,6 +479,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             if (engine == FSW_ENGINE_DMAZ && !striped && g.zstage) launch_poison(g.sx, g.zstage, g.zstage_cap, pat ^ 0x20u);
         }
     }
+    if (g.trace)  // device timeline of this invoke (FSW_TRACE): every field starts at 0
+        cudaMemsetAsync(g.trace, 0, sizeof(unsigned long long) * kTraceStride * m->layers.size(), g.sx);
     // stage: descriptor + input (pinned), one H2D node in the graph
     DevDesc dd = ic.dst;
     dd.generation = ++g.generation;

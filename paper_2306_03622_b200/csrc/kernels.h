@@ -204,22 +204,32 @@ void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tm
                  const CUtensorMap* tmW = nullptr);
 bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes);
 
-struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; };
+struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; int32_t layer; };
 void launch_attention(cudaStream_t s, const AttnArgs& a);
 
 struct Im2colArgs {
     const uint16_t* in; uint32_t H, W, C;
     uint16_t* out; uint32_t P, Q, R, S, stride, pad, K, Kpad;
+    int32_t layer;
 };
 void launch_im2col(cudaStream_t s, const Im2colArgs& a);
 
 struct PoolArgs {
     const uint16_t* in; uint32_t H, W, C; uint32_t P, Q, k, stride, pad;
     uint16_t* out; float* out_f32;
+    int32_t layer;
 };
 void launch_maxpool(cudaStream_t s, const PoolArgs& a);
 void launch_avgpool(cudaStream_t s, const PoolArgs& a);
 
+// Device timeline (FSW_TRACE, fsw_debug_trace_read; DESIGN.md §5 "Overlap timeline"): per layer L,
+// kTraceStride u64 at trace + L·kTraceStride: [0] ~(first kernel CTA entry), [1] last weight-wait done,
+// [2] last kernel CTA exit, [3] ~(first piece of L released by a swap kernel), [4] last piece released.
+// Min fields are stored complemented so that one memset to 0 resets every field (atomicMax for all).
+constexpr uint32_t kTraceStride = 8;
+void set_trace_swap(unsigned long long* t);  // current device; nullptr = off (swap.cu)
+void set_trace_ops(unsigned long long* t);   // ops.cu
+void set_trace_gemm(unsigned long long* t);  // gemm_tc.cu
 void init_gemm_attrs();
 int gemm_max_active_clusters(int bn, int cz);  // clusters of cz GEMM CTAs resident at once (this device)
 void init_swap_attrs();

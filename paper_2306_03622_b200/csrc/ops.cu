@@ -11,6 +11,7 @@ namespace fsw {
 // EMBED: out[t][c] = Σ_j table_j[row_j(t)][c]   (fp32 sum of bf16 rows)
 // ------------------------------------------------------------------------------------------
 __global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
+    TraceExit tx(w.layer);
     wait_ready_cta(w);
     pdl_wait();
     const uint32_t t = blockIdx.x;
@@ -47,6 +48,7 @@ void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) 
 // ------------------------------------------------------------------------------------------
 template <int NV>
 __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
+    TraceExit tx(w.layer);
     wait_ready_cta(w);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -121,6 +123,7 @@ constexpr int kGemvMaxRows = 8;
 
 template <int R>
 __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wait w, GemvArgs a) {
+    TraceExit tx(w.layer);
     extern __shared__ float xs[];  // [R][K]
     pdl_wait();
     for (uint32_t i = threadIdx.x; i < R * a.K; i += blockDim.x) {
@@ -129,7 +132,10 @@ __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wai
         xs[i] = r >= a.rows ? 0.0f : a.x_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.x)[src])
                          : reinterpret_cast<const float*>(a.x)[src];
     }
-    if (threadIdx.x == 0) wait_ready_thread(w);
+    if (threadIdx.x == 0) {
+        wait_ready_thread(w);
+        trace_max(w.layer, 1, globaltimer());
+    }
     __syncthreads();  // publishes xs and the acquired weights to the CTA
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t gwarp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -195,6 +201,7 @@ void launch_gemv(cudaStream_t s, const DevDesc* d, Wait w, const GemvArgs& a) {
 constexpr int kAttnRows = 16;
 
 __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
+    TraceExit tx(a.layer);
     extern __shared__ __align__(16) uint8_t sm_attn[];
     pdl_wait();
     const uint32_t T = a.T, dh = a.dh, D = a.H * dh, W3 = 3 * D;
@@ -291,6 +298,7 @@ constexpr int kAttnMmaRows = 64, kAttnMmaMaxT = 128;
 
 template <int DH>
 __global__ void __launch_bounds__(128) k_attention_mma(AttnArgs a) {
+    TraceExit tx(a.layer);
     constexpr int KS = DH / 16;        // k-steps of Q·Kᵀ
     constexpr int NO = DH / 8;         // n-tiles of O
     constexpr int NS = kAttnMmaMaxT / 8;  // n-tiles of S (keys)
@@ -426,6 +434,7 @@ constexpr int kAttnSplitRows = 16, kAttnSplitWarps = 4;
 
 template <int DH>
 __global__ void __launch_bounds__(128) k_attention_mma2(AttnArgs a) {
+    TraceExit tx(a.layer);
     constexpr int KS = DH / 16, NO = DH / 8, LD = DH + 8;
     constexpr int NSW = kAttnMmaMaxT / 8 / kAttnSplitWarps;  // key n-tiles per warp (4 at T <= 128)
     extern __shared__ __align__(16) uint16_t sm_kv2[];
@@ -635,6 +644,7 @@ void launch_attention(cudaStream_t s, const AttnArgs& a) {
 // IM2COL (NHWC bf16 -> [P·Q][Kpad] bf16, k = (r·S + s)·C + c, zero padding / tail)
 // ------------------------------------------------------------------------------------------
 __global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per thread
+    TraceExit tx(a.layer);
     pdl_wait();
     const uint32_t k8n = a.Kpad >> 3;
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -652,6 +662,7 @@ __global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per
 }
 
 __global__ void k_im2col_scalar(Im2colArgs a) {
+    TraceExit tx(a.layer);
     pdl_wait();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * a.Kpad) return;
@@ -680,6 +691,7 @@ void launch_im2col(cudaStream_t s, const Im2colArgs& a) {
 // pooling (NHWC bf16)
 // ------------------------------------------------------------------------------------------
 __global__ void k_maxpool(PoolArgs a) {
+    TraceExit tx(a.layer);
     pdl_wait();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * a.C) return;
@@ -700,6 +712,7 @@ void launch_maxpool(cudaStream_t s, const PoolArgs& a) {
 }
 
 __global__ void k_avgpool(PoolArgs a) {
+    TraceExit tx(a.layer);
     pdl_wait();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= a.C) return;
@@ -726,5 +739,7 @@ void init_ops_attrs() {
     cudaFuncSetAttribute(k_attention_mma2<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_attention_mma2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
+
+void set_trace_ops(unsigned long long* t) { cudaMemcpyToSymbol(g_trace, &t, sizeof t); }
 
 }  // namespace fsw

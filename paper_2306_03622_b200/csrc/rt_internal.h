@@ -239,6 +239,7 @@ struct Gpu {
     // stats
     uint64_t n_evictions = 0, bytes_swapped_total = 0, n_cold = 0, n_warm = 0;
     uint64_t n_evictions_heavy = 0;  // evictions of a model in the heavy class at the time
+    unsigned long long* trace = nullptr;  // device timeline (FSW_TRACE): kTraceStride u64 per layer
 };
 
 constexpr uint64_t kStageHdr = 256;

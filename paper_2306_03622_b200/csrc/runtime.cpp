@@ -152,6 +152,13 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaHostAlloc(reinterpret_cast<void**>(&g.hctl), sizeof(DevCtl), cudaHostAllocPortable | cudaHostAllocMapped));
     memset(g.hstage, 0, kStageHdr);
     for (cudaEvent_t* e : {&g.ev0, &g.ev1, &g.evs0, &g.evs1}) CU(cudaEventCreate(e));
+    if (c->cfg.flags & FSW_TRACE) {  // device timeline: every kernel of this device records into it
+        CU(cudaMalloc(&g.trace, sizeof(unsigned long long) * kTraceStride * g.ready_cap));
+        CU(cudaMemset(g.trace, 0, sizeof(unsigned long long) * kTraceStride * g.ready_cap));
+        set_trace_swap(g.trace);
+        set_trace_ops(g.trace);
+        set_trace_gemm(g.trace);
+    }
     CU(cudaEventCreateWithFlags(&g.evfork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&g.evjoin, cudaEventDisableTiming));
     return FSW_OK;
@@ -175,6 +182,7 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
     auto c = std::make_unique<fsw_ctx>();
     if (cfg) c->cfg = *cfg;
     if (getenv("FSW_DEBUG_POISON") && atoi(getenv("FSW_DEBUG_POISON")) != 0) c->cfg.flags |= FSW_DEBUG_POISON;
+    if (getenv("FSW_TRACE") && atoi(getenv("FSW_TRACE")) != 0) c->cfg.flags |= FSW_TRACE;
     if (c->cfg.copy_ctas == 0) c->cfg.copy_ctas = 16;
     if (c->cfg.copy_threads == 0) c->cfg.copy_threads = 256;
     if (c->cfg.chunk_bytes == 0) c->cfg.chunk_bytes = 16 << 10;
@@ -278,6 +286,7 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFree(g.pool);
         cudaFree(g.ws);
         cudaFree(g.ready);
+        cudaFree(g.trace);
         cudaFree(g.ctl);
         cudaFree(g.dstage);
         cudaFree(g.zstage);
@@ -354,6 +363,36 @@ extern "C" fsw_status fsw_debug_read_resident(fsw_ctx* c, uint32_t id, int32_t g
     if (m->split) CU(cudaMemcpy(dst, pool + m->pextent[gpu], m->split, cudaMemcpyDeviceToHost));
     CU(cudaMemcpy(static_cast<uint8_t*>(dst) + m->split, pool + m->extent[gpu], m->store_bytes - m->split,
                   cudaMemcpyDeviceToHost));
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_trace_read(fsw_ctx* c, uint32_t id, int32_t gpu, uint64_t* out, uint32_t cap_layers,
+                                           uint64_t* t_invoke) {
+    if (!c || !out || gpu < 0 || gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "trace_read: bad argument");
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    Gpu& g = c->gpus[gpu];
+    if (!g.trace) return fail(FSW_ESTATE, "trace_read: context not created with FSW_TRACE");
+    const size_t nl = m->layers.size();
+    if (cap_layers < nl) return fail(FSW_EINVAL, "trace_read: cap %u < %zu layers", cap_layers, nl);
+    CU(cudaSetDevice(g.dev));
+    std::vector<unsigned long long> raw(nl * kTraceStride);
+    CU(cudaMemcpy(raw.data(), g.trace, sizeof(unsigned long long) * raw.size(), cudaMemcpyDeviceToHost));
+    for (size_t l = 0; l < nl; ++l) {  // [entry, wait done, exit, first release, last release]; 0 = none
+        const unsigned long long* r = &raw[l * kTraceStride];
+        out[5 * l + 0] = r[0] ? ~r[0] : 0;
+        out[5 * l + 1] = r[1];
+        out[5 * l + 2] = r[2];
+        out[5 * l + 3] = r[3] ? ~r[3] : 0;
+        out[5 * l + 4] = r[4];
+    }
+    if (t_invoke) {  // the last invoke's control block: first piece claimed, last released, graph end
+        DevCtl ctl{};
+        CU(cudaMemcpy(&ctl, g.ctl, sizeof ctl, cudaMemcpyDeviceToHost));
+        t_invoke[0] = ctl.t_first;
+        t_invoke[1] = ctl.t_last;
+        t_invoke[2] = ctl.t_end;
+    }
     return FSW_OK;
 }
 

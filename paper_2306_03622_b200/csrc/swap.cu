@@ -17,6 +17,7 @@ namespace fsw {
 __device__ uint32_t g_drop_piece = 0xffffffffu;
 
 void set_drop_piece(uint32_t index) { cudaMemcpyToSymbol(g_drop_piece, &index, sizeof index); }
+void set_trace_swap(unsigned long long* t) { cudaMemcpyToSymbol(g_trace, &t, sizeof t); }
 
 // A swap CTA has started: count it on the target's gate.  A remote source (sys) increments the target
 // GPU's counter over NVLink at system scope (the target's k_gate reads it with ld.acquire.sys).
@@ -61,7 +62,12 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
             __syncwarp();
             if (lane == 0) red_release_gpu_add(&ready[pc.layer], pc.bytes);
         }
-        if (lane == 0) atomicMax(&own->t_last, (unsigned long long)globaltimer());
+        if (lane == 0) {
+            const unsigned long long now = globaltimer();
+            atomicMax(&own->t_last, now);
+            trace_max((int32_t)pc.layer, 3, ~now);
+            trace_max((int32_t)pc.layer, 4, now);
+        }
     }
 }
 
@@ -333,7 +339,12 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
             __syncwarp();
             if (lane == 0) red_release_gpu_add(&ready[pc.layer], pc.bytes);
         }
-        if (lane == 0) atomicMax(&own->t_last, (unsigned long long)globaltimer());
+        if (lane == 0) {
+            const unsigned long long now = globaltimer();
+            atomicMax(&own->t_last, now);
+            trace_max((int32_t)pc.layer, 3, ~now);
+            trace_max((int32_t)pc.layer, 4, now);
+        }
     }
 }
 
@@ -460,7 +471,10 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         if (tid == 0) {
             if (sys) red_release_sys_add(&ready[pc.layer], pc.bytes);
             else red_release_gpu_add(&ready[pc.layer], pc.bytes);
-            atomicMax(&own->t_last, (unsigned long long)globaltimer());
+            const unsigned long long now = globaltimer();
+            atomicMax(&own->t_last, now);
+            trace_max((int32_t)pc.layer, 3, ~now);
+            trace_max((int32_t)pc.layer, 4, now);
             issue(b);
         }
     }

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libfsw.so")
 
 OK, EINVAL, ENOTFOUND, ENOMEM, EBUSY, ESTATE, ECUDA, ETIMEOUT, ETOPO = range(9)
 STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA", "ETIMEOUT", "ETOPO"]
-NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP, DEBUG_POISON = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP, DEBUG_POISON, TRACE = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40
 FAULT_NONE, FAULT_DROP_PIECE, FAULT_DROP_GROUP = 0, 1, 2
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
@@ -149,7 +149,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
            "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal",
            "fsw_debug_set_fault", "fsw_debug_litmus", "fsw_policy_heavy", "fsw_model_set_slo",
-           "fsw_set_heavy_policy"]
+           "fsw_set_heavy_policy", "fsw_debug_trace_read"]
 
 _lib = None
 
@@ -184,6 +184,7 @@ def lib():
         L.fsw_debug_coded_pieces.argtypes = [vp, u32, vp, u32, ctypes.POINTER(u32)]
         L.fsw_debug_dmaz_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
         L.fsw_debug_set_fault.argtypes = [vp, u32, u32]
+        L.fsw_debug_trace_read.argtypes = [vp, u32, i32, vp, u32, vp]
         L.fsw_policy_heavy.argtypes = [dbl, dbl, dbl, dbl, dbl, ctypes.POINTER(i32)]
         L.fsw_model_set_slo.argtypes = [vp, u32, dbl]
         L.fsw_set_heavy_policy.argtypes = [vp, dbl, dbl]
@@ -468,6 +469,15 @@ class Runtime:
         bad, chk = u64(), u64()
         _check(lib().fsw_debug_litmus(self.h, mid, gpu, engine, ctas, iters, ctypes.byref(bad), ctypes.byref(chk)))
         return bad.value, chk.value
+
+    def trace(self, mid: int, gpu: int = 0):
+        """Device timeline of the last invoke (FSW_TRACE): ([n_layers][5] ns: entry, wait done, exit, first /
+        last piece released; 0 = none), [first piece claimed, last released, graph end] ns)."""
+        n = self.model_info(mid)["n_layers"]
+        out = np.zeros((n, 5), np.uint64)
+        ti = np.zeros(3, np.uint64)
+        _check(lib().fsw_debug_trace_read(self.h, mid, gpu, out.ctypes.data, n, ti.ctypes.data))
+        return out, ti
 
     def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:
         buf = np.empty(nbytes, dtype=np.uint8)
