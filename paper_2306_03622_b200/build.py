@@ -19,9 +19,9 @@ INCLUDE = os.path.join(ROOT, "include")
 SO = os.path.join(PKG, "libfsw.so")
 BUILD = os.path.join(PKG, "_build")
 
-CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu"]
+CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu", "mega.cu"]
 CXX_SOURCES = ["runtime.cpp", "store.cpp", "plan.cpp", "graph.cpp", "invoke.cpp", "sched.cpp", "litmus.cpp"]
-HEADERS = ["kernels.h", "device.cuh", "policy.h", "rt_internal.h"]
+HEADERS = ["kernels.h", "device.cuh", "policy.h", "rt_internal.h", "umma.cuh", "attn_core.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

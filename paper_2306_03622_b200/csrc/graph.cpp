@@ -337,26 +337,40 @@ fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vecto
     return FSW_OK;
 }
 
-static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaStream_t s) {
-    const DevDesc* d = reinterpret_cast<const DevDesc*>(g.dstage);
-    for (const Launch& x : p.launches) {
-        Wait w{};
-        w.ctl = g.ctl;
-        w.layer = x.layer;
-        if (ic.cold && m.region_bytes[x.layer] > 0 && m.region_off[x.layer] >= ic.from) {
-            if (engine_bytes_ready(ic.engine)) {
-                w.n = 1;
-                w.ready[0] = g.ready + x.layer;
-                w.target[0] = (uint32_t)m.region_bytes[x.layer];
-                w.sys = ic.striped ? 1 : 0;
-            } else {
-                w.n = ic.dma_plan->streams;
-                for (uint32_t j = 0; j < w.n; ++j) {
-                    w.ready[j] = g.progress + 32 * j;
-                    w.target[j] = ic.dma_plan->target[x.layer][j];
-                }
+// The readiness wait of a kernel of layer `layer` for this invoke configuration.
+static Wait layer_wait(Model& m, Gpu& g, const InvokeCfg& ic, int layer) {
+    Wait w{};
+    w.ctl = g.ctl;
+    w.layer = layer;
+    if (ic.cold && m.region_bytes[layer] > 0 && m.region_off[layer] >= ic.from) {
+        if (engine_bytes_ready(ic.engine)) {
+            w.n = 1;
+            w.ready[0] = g.ready + layer;
+            w.target[0] = (uint32_t)m.region_bytes[layer];
+            w.sys = ic.striped ? 1 : 0;
+        } else {
+            w.n = ic.dma_plan->streams;
+            for (uint32_t j = 0; j < w.n; ++j) {
+                w.ready[j] = g.progress + 32 * j;
+                w.target[j] = ic.dma_plan->target[layer][j];
             }
         }
+    }
+    return w;
+}
+
+static fsw_status enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaStream_t s) {
+    const DevDesc* d = reinterpret_cast<const DevDesc*>(g.dstage);
+    if (p.mega.on) {
+        // the persistent transformer kernel: one launch; its op table (this invoke configuration's waits)
+        // was written to device memory by build_graph before the capture began
+        cudaMemsetAsync(p.mega.op_cnt, 0, sizeof(uint32_t) * p.mega.ops.size(), s);
+        launch_mega(s, p.mega.ctas, d, reinterpret_cast<const MkOp*>(p.last_mk_ops), (uint32_t)p.mega.ops.size(),
+                    p.mega.op_cnt, p.mega.tmaps, g.gemm_ctr, p.mega.part);
+        return FSW_OK;
+    }
+    for (const Launch& x : p.launches) {
+        const Wait w = layer_wait(m, g, ic, x.layer);
         switch (x.kind) {
             case K_EMBED: launch_embed(s, d, w, x.embed); break;
             case K_LN: launch_layernorm(s, d, w, x.ln); break;
@@ -384,6 +398,7 @@ static void enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic, cudaS
             }
         }
     }
+    return FSW_OK;
 }
 
 PFN_writeValue32 get_write_value32() {
@@ -412,6 +427,14 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
     if (ic.cold && (engine_bytes_ready(ic.engine) || ic.striped) && m.layers.size() > g.ready_cap)
         return fail(FSW_EINVAL, "too many layers");
     CU(cudaSetDevice(g.dev));
+    if (p.mega.on) {  // the persistent kernel's op table with this configuration's waits (no allocation in a capture)
+        std::vector<MkOp> ops = p.mega.ops;
+        for (MkOp& op : ops) op.w = layer_wait(m, g, ic, op.layer);
+        void* dev = nullptr;
+        CU(cudaMalloc(&dev, sizeof(MkOp) * ops.size()));
+        p.last_mk_ops = dev;
+        CU(cudaMemcpy(dev, ops.data(), sizeof(MkOp) * ops.size(), cudaMemcpyHostToDevice));
+    }
     cudaStream_t sx = g.sx, sc = g.sc;
     CU(cudaStreamBeginCapture(sx, cudaStreamCaptureModeThreadLocal));
     // The swap starts as early as possible: the DMA engine needs only its counters reset; the SM
@@ -524,7 +547,14 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
         if (ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
         else if (engine_bytes_ready(ic.engine)) launch_gate(sx, g.ctl, ic.ctas);
     }
-    enqueue_layers(m, p, g, ic, sx);
+    const fsw_status lst = enqueue_layers(m, p, g, ic, sx);
+    if (lst != FSW_OK) {
+        cudaGraph_t dead = nullptr;
+        cudaStreamEndCapture(sx, &dead);
+        if (dead) cudaGraphDestroy(dead);
+        cudaGetLastError();
+        return lst;
+    }
     if (ic.cold && !ic.striped && !ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);  // swap stamps final
     launch_finish(sx, g.ctl, g.ws + p.slot_off[m.output_slot], m.output_bytes, g.hout, g.hctl);
     cudaGraph_t graph = nullptr;

@@ -456,12 +456,18 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             std::sort(baked.begin(), baked.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
             for (size_t i = 0; i + kMaxBakedGraphs <= baked.size(); ++i) {
                 cudaGraphExecDestroy(p.graphs[baked[i].second].exec);
+                cudaFree(p.graphs[baked[i].second].mk_ops);
                 p.graphs.erase(baked[i].second);
             }
         }
+        p.last_mk_ops = nullptr;
         st = build_graph(c, *m, p, g, ic, &exec);
-        if (st != FSW_OK) return finish(st);
-        p.graphs[key] = GraphEntry{exec, ++p.graph_clock};
+        if (st != FSW_OK) {
+            cudaFree(p.last_mk_ops);
+            p.last_mk_ops = nullptr;
+            return finish(st);
+        }
+        p.graphs[key] = GraphEntry{exec, ++p.graph_clock, p.last_mk_ops};
     } else {
         exec = it->second.exec;
         it->second.last_use = ++p.graph_clock;

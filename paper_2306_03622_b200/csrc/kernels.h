@@ -230,6 +230,37 @@ constexpr uint32_t kTraceStride = 8;
 void set_trace_swap(unsigned long long* t);  // current device; nullptr = off (swap.cu)
 void set_trace_ops(unsigned long long* t);   // ops.cu
 void set_trace_gemm(unsigned long long* t);  // gemm_tc.cu
+void set_trace_mega(unsigned long long* t);  // mega.cu
+// ---- persistent transformer kernel (mega.cu; DESIGN.md §5 "k_mega") ---------------------------------
+// One launch runs every layer of a transformer (EMBED, LAYERNORM, LINEAR, ATTENTION) on one CTA per SM.
+// Op i is a list of n_tasks tasks; CTA c takes tasks c, c + grid, ... of every op in order.  A task of
+// op i reads activations only after op `dep` (i − 1) has counted all its tasks done (release / acquire
+// on a per-op counter); weights need only the layer's readiness (Wait), so a CTA's producer warp
+// streams the next op's weight tiles while the previous op still runs.  GEMMs are swap-AB tcgen05
+// tiles: 128 weight rows (UMMA M) x tt tokens (UMMA N) x a K range (split-K, partials reduced by the
+// last split in split order).
+enum MkKind : uint32_t { MK_GEMM = 1, MK_LN = 2, MK_ATTN = 3, MK_EMBED = 4, MK_GEMV = 5 };
+struct MkOp {
+    uint32_t kind, n_tasks;
+    int32_t dep;                       // op whose completion the activations need (-1: none)
+    int32_t layer;
+    Wait w;                            // weights' readiness (n = 0: resident / no weights)
+    uint32_t tt, n_rt, n_tt, splits, kt_per, tmap;  // GEMM tiling; tmap = index into the tensor-map array
+    union {
+        GemmArgs gemm;
+        LnArgs ln;
+        AttnArgs attn;
+        EmbedArgs embed;
+        GemvArgs gemv;
+    };
+};
+constexpr uint32_t kMkTT = 64;  // largest token tile
+// ops / counters / tensor maps in device memory; grid = one CTA per SM (ctas)
+void launch_mega(cudaStream_t s, int ctas, const DevDesc* d, const MkOp* ops, uint32_t n_ops, uint32_t* op_cnt,
+                 const CUtensorMap* tmaps, uint32_t* tile_ctr, float* part);
+size_t mega_smem_bytes();
+void init_mega_attrs();
+
 void init_gemm_attrs();
 int gemm_max_active_clusters(int bn, int cz);  // clusters of cz GEMM CTAs resident at once (this device)
 void init_swap_attrs();

@@ -1,0 +1,456 @@
+// mega.cu — k_mega: the persistent transformer kernel.  ONE launch runs every layer of a BERT / GPT-2
+// style layer table (EMBED, LAYERNORM, LINEAR, ATTENTION) on one CTA per SM, instead of one kernel
+// per layer op (~86 launches for BERT-base, each paying its setup, first-data latency and epilogue
+// tail: resident BERT-base measured 52 us per encoder layer against ~2 us of weight bytes at HBM rate,
+// profiles/r02/timeline_*).  It is the same flag-gated pipelined execution: every op
+// waits for its layer's ready counter before it touches weights, so on a cold invoke it runs behind
+// the swap exactly like the per-op kernels.
+//
+// Work: op i of the table is n_tasks tasks; CTA c takes tasks c, c + grid, ... of every op, in op
+// order.  Dependencies are op-level: a task reads activations only after op i − 1 has counted all of
+// its tasks done (red.release on a per-op counter, ld.acquire by the consumer; chained, so every
+// earlier op is done too).  Weights are not activations: the producer warp streams the weight tiles
+// of a CTA's next GEMM task into the shared-memory ring BEFORE that dependency resolves, so the HBM
+// weight stream of op i overlaps the tail of op i − 1.
+//
+// Warp roles (192 threads): warp 0 = producer (one thread: weight bulk copies of the pre-tiled layout,
+// DESIGN.md §4, and TMA loads of the activation tile), warp 1 = tcgen05.mma issuer (one thread),
+// warps 2-5 = epilogue of GEMM tasks (TMEM lane quarter = warp mod 4) and the CUDA-core tasks
+// (embedding gather, LayerNorm, attention core, small-M GEMV) with named barrier 1.
+//
+// GEMM tiles are swap-AB: the UMMA M operand is 128 weight rows, N is tt tokens (16 / 32 / 64), so a
+// task streams 128·K_range·2 weight bytes and tt·K_range·2 activation bytes; D = [weight row][token]
+// sits in one of two TMEM buffers (the MMA of the next task overlaps this task's epilogue).  Split-K
+// tasks write fp32 partials; the last split to arrive sums them in split order (deterministic).
+#include "attn_core.cuh"
+#include "umma.cuh"
+
+namespace fsw {
+
+constexpr int kMkThreads = 192, kMkStages = 5;
+constexpr uint32_t kMkW = 128 * 128;               // one weight k-tile: 128 rows x 64 k bf16
+constexpr uint32_t kMkA = kMkTT * 128;             // one activation k-tile: <= 64 tokens x 64 k bf16
+constexpr uint32_t kMkStage = kMkW + kMkA;
+constexpr uint32_t kMkCompute = 56 * 1024;         // attention (dh <= 64, T <= 128) / GEMV staging
+constexpr uint32_t kMkRing = kMkStages * kMkStage;
+constexpr uint32_t kMkTmemCols = 2 * kMkTT;        // two accumulator buffers
+constexpr uint64_t kMkWatchdogNs = 4ull * 1000 * 1000 * 1000;
+
+size_t mega_smem_bytes() { return 1024 + kMkRing + kMkCompute + 256; }
+
+__device__ __forceinline__ void mk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// mbarrier wait with a watchdog (a lost arrival must end the kernel, not hang the GPU)
+__device__ __forceinline__ void mk_wait(uint64_t* b, uint32_t parity, DevCtl* ctl) {
+    const uint32_t a = smem_u32(b);
+    uint32_t ok = 0, n = 0;
+    uint64_t t0 = 0;
+    for (;;) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+        if (ok) return;
+        if (++n == 64) t0 = globaltimer();
+        if (n > 64 && (n & 255) == 0 && globaltimer() - t0 > kMkWatchdogNs) {
+            atomicExch(&ctl->err, 4);
+            return;
+        }
+    }
+}
+
+// Spin until op `dep` has counted `need` tasks done (acquire), with back-off and a watchdog.
+__device__ __forceinline__ void mk_wait_op(const uint32_t* cnt, uint32_t need, DevCtl* ctl) {
+    if (ld_acquire_gpu(cnt) >= need) return;
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 32;
+    while (ld_acquire_gpu(cnt) < need) {
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+        if (globaltimer() - t0 > kWatchdogNs) {
+            atomicExch(&ctl->err, 4);
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ void mk_done(uint32_t* cnt) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+}
+
+struct MkTile {
+    uint32_t r, j, z, kt0, nk, rows_w;
+};
+__device__ __forceinline__ MkTile mk_tile(const MkOp& op, uint32_t g) {
+    MkTile t;
+    t.z = g % op.splits;
+    const uint32_t rem = g / op.splits;
+    t.j = rem % op.n_tt;
+    t.r = rem / op.n_tt;
+    t.kt0 = t.z * op.kt_per;
+    t.nk = min(op.gemm.K / 64, t.kt0 + op.kt_per) - t.kt0;
+    t.rows_w = min(128u, op.gemm.n_pad - t.r * 128);
+    return t;
+}
+
+// ---- epilogue of one GEMM output element ------------------------------------------------------------
+__device__ __forceinline__ void mk_store(const GemmArgs& a, uint32_t tok, uint32_t n, float x, float bias) {
+    x += bias;
+    if (a.res) {
+        const uint64_t ri = (uint64_t)tok * a.ld_res + n;
+        x += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
+                        : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
+    }
+    x = apply_act(a.act, x);
+    const uint64_t oi = (uint64_t)tok * a.ld_out + n;
+    if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
+    else reinterpret_cast<float*>(a.out)[oi] = x;
+    if (a.out2) a.out2[oi] = f32_to_bf16(x);
+}
+
+// ---- CUDA-core tasks (128 threads, tid e) --------------------------------------------------------------
+__device__ __forceinline__ void mk_embed(const DevDesc& dd, const EmbedArgs& a, uint32_t t, uint32_t e, DevCtl* ctl) {
+    uint32_t row[4];
+    for (int j = 0; j < a.n_tables; ++j) {
+        uint32_t r = a.rule[j] == FSW_RULE_IDS ? (uint32_t)__ldcg(a.ids + t) : (a.rule[j] == FSW_RULE_POSITION ? t : 0u);
+        if (r >= a.table_rows[j]) {
+            if (e == 0) atomicExch(&ctl->err, 3);
+            r = 0;
+        }
+        row[j] = r;
+    }
+    for (uint32_t c = e; c < a.C; c += 128) {
+        float s = 0.0f;
+        for (int j = 0; j < a.n_tables; ++j)
+            s += bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.table_off[j]))[(uint64_t)row[j] * a.C + c]);
+        if (a.out) a.out[(uint64_t)t * a.C + c] = s;
+        if (a.out_bf16) a.out_bf16[(uint64_t)t * a.C + c] = f32_to_bf16(s);
+    }
+}
+
+// one warp per row: fp32 two-pass statistics over the row read through L2 (as k_layernorm)
+__device__ __forceinline__ void mk_layernorm(const DevDesc& dd, const LnArgs& a, uint32_t r, uint32_t lane) {
+    if (r >= a.rows) return;
+    const float4* x = reinterpret_cast<const float4*>(a.in + (uint64_t)r * a.C);
+    const uint2* g = reinterpret_cast<const uint2*>(weight_ptr(dd, a.g_off));
+    const uint2* b = reinterpret_cast<const uint2*>(weight_ptr(dd, a.b_off));
+    const uint32_t n4 = a.C >> 2;
+    float s = 0.0f;
+    for (uint32_t c = lane; c < n4; c += 32) {
+        const float4 v = __ldcg(x + c);
+        s += (v.x + v.y) + (v.z + v.w);
+    }
+    const float mu = warp_sum(s) / (float)a.C;
+    float q = 0.0f;
+    for (uint32_t c = lane; c < n4; c += 32) {
+        const float4 v = __ldcg(x + c);
+        const float d0 = v.x - mu, d1 = v.y - mu, d2 = v.z - mu, d3 = v.w - mu;
+        q += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    }
+    const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
+    for (uint32_t c = lane; c < n4; c += 32) {
+        const float4 v = __ldcg(x + c);
+        const uint2 gv = g[c], bv = b[c];
+        float4 y;
+        y.x = (v.x - mu) * inv * __uint_as_float(gv.x << 16) + __uint_as_float(bv.x << 16);
+        y.y = (v.y - mu) * inv * __uint_as_float(gv.x & 0xffff0000u) + __uint_as_float(bv.x & 0xffff0000u);
+        y.z = (v.z - mu) * inv * __uint_as_float(gv.y << 16) + __uint_as_float(bv.y << 16);
+        y.w = (v.w - mu) * inv * __uint_as_float(gv.y & 0xffff0000u) + __uint_as_float(bv.y & 0xffff0000u);
+        if (a.out_f32) reinterpret_cast<float4*>(a.out_f32 + (uint64_t)r * a.C)[c] = y;
+        if (a.out_bf16) {
+            const uint32_t lo = (uint32_t)f32_to_bf16(y.x) | ((uint32_t)f32_to_bf16(y.y) << 16);
+            const uint32_t hi = (uint32_t)f32_to_bf16(y.z) | ((uint32_t)f32_to_bf16(y.w) << 16);
+            reinterpret_cast<uint2*>(a.out_bf16 + (uint64_t)r * a.C)[c] = make_uint2(lo, hi);
+        }
+    }
+}
+
+// GEMV task: features [o0, o0 + 64) of a rows <= 8 linear; x staged in shared memory as fp32
+constexpr uint32_t kMkGemvFeat = 64;
+template <int R>
+__device__ __forceinline__ void mk_gemv(const DevDesc& dd, const GemvArgs& a, uint32_t o0, float* xs, uint32_t e) {
+    for (uint32_t i = e; i < R * a.K; i += 128) {
+        const uint32_t r = i / a.K, k = i - r * a.K;
+        const uint64_t src = (uint64_t)(a.r0 + r) * a.ldx + k;
+        xs[i] = r >= a.rows ? 0.0f
+                : a.x_bf16  ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.x) + src))
+                            : __ldcg(reinterpret_cast<const float*>(a.x) + src);
+    }
+    mk_bar();
+    const uint32_t lane = e & 31, wq = e >> 5;
+    const uint8_t* wmat = weight_ptr(dd, a.w_off);
+    const uint16_t* bvec = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
+    const uint32_t k8n = a.K >> 3;
+    for (uint32_t f = wq; f < kMkGemvFeat; f += 4) {
+        const uint32_t o = o0 + f;
+        if (o >= a.N) break;
+        const uint4* wr = reinterpret_cast<const uint4*>(wmat + (uint64_t)o * a.K * 2);
+        float acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = 0.0f;
+        for (uint32_t k8 = lane; k8 < k8n; k8 += 32) {
+            const uint4 wv = __ldcg(wr + k8);
+            const uint32_t wu[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const float w0 = __uint_as_float(wu[h] << 16), w1 = __uint_as_float(wu[h] & 0xffff0000u);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float* xr = xs + r * a.K + k8 * 8 + 2 * h;
+                    acc[r] = fmaf(w0, xr[0], acc[r]);
+                    acc[r] = fmaf(w1, xr[1], acc[r]);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = warp_sum(acc[r]);
+        if (lane < (uint32_t)R && lane < a.rows) {
+            float v = 0.0f;
+#pragma unroll
+            for (int r = 0; r < R; ++r) v = (r == (int)lane) ? acc[r] : v;
+            const uint64_t oi = (uint64_t)lane * a.N + o;
+            if (bvec) v += bf16_to_f32(bvec[o]);
+            if (a.res) v += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + oi))
+                                       : __ldcg(reinterpret_cast<const float*>(a.res) + oi);
+            v = apply_act(a.act, v);
+            if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
+            else reinterpret_cast<float*>(a.out)[oi] = v;
+            if (a.out2) a.out2[oi] = f32_to_bf16(v);
+        }
+    }
+    mk_bar();  // xs is rewritten by the next task
+}
+
+__global__ void __launch_bounds__(kMkThreads, 1)
+    k_mega(const DevDesc* __restrict__ d, const MkOp* __restrict__ ops, uint32_t n_ops, uint32_t* op_cnt,
+           const CUtensorMap* __restrict__ tmaps, uint32_t* tile_ctr, float* part) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* ring = smem;
+    uint8_t* cmp = smem + kMkRing;  // compute region
+    uint64_t* full = reinterpret_cast<uint64_t*>(cmp + kMkCompute);
+    uint64_t* empty = full + kMkStages;
+    uint64_t* tfull = empty + kMkStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint32_t* flag = tmem_slot + 1;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const DevDesc dd = *d;
+    DevCtl* ctl = ops[0].w.ctl;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMkStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kMkTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ================= producer =================
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (uint32_t i = 0; i < n_ops; ++i) {
+                const MkOp& op = ops[i];
+                if (op.kind != MK_GEMM || blockIdx.x >= op.n_tasks) continue;
+                wait_ready_thread(op.w);  // the layer's weights landed (cold); no-op when resident
+                trace_max(op.layer, 1, globaltimer());
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                const GemmArgs& a = op.gemm;
+                const uint8_t* wt = weight_ptr(dd, a.w_off);
+                const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
+                const CUtensorMap* tm = tmaps + op.tmap;
+                bool dep_ok = op.dep < 0;
+                for (uint32_t g = blockIdx.x; g < op.n_tasks; g += gridDim.x) {
+                    const MkTile t = mk_tile(op, g);
+                    const uint32_t wbytes = t.rows_w * 128, abytes = op.tt * 128;
+                    const uint32_t pre = dep_ok ? 0u : min(t.nk, (uint32_t)kMkStages);
+                    // weights of the first stages before the activation dependency resolves
+                    for (uint32_t q = 0; q < pre; ++q) {
+                        const uint32_t s = (it + q) % kMkStages;
+                        mk_wait(&empty[s], (((it + q) / kMkStages) & 1) ^ 1, ctl);
+                        mbar_expect_tx(&full[s], wbytes + abytes);
+                        bulk_load(ring + s * kMkStage, wt + (t.kt0 + q) * ktile_stride + (uint64_t)(t.r * 16) * 1024, wbytes,
+                                  &full[s]);
+                    }
+                    if (!dep_ok) {
+                        mk_wait_op(op_cnt + op.dep, ops[op.dep].n_tasks, ctl);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        dep_ok = true;
+                    }
+                    for (uint32_t q = 0; q < pre; ++q) {
+                        const uint32_t s = (it + q) % kMkStages;
+                        tma_load_2d(ring + s * kMkStage + kMkW, tm, (int)((t.kt0 + q) * 64), (int)(t.j * op.tt), &full[s]);
+                    }
+                    for (uint32_t q = pre; q < t.nk; ++q) {
+                        const uint32_t s = (it + q) % kMkStages;
+                        mk_wait(&empty[s], (((it + q) / kMkStages) & 1) ^ 1, ctl);
+                        mbar_expect_tx(&full[s], wbytes + abytes);
+                        bulk_load(ring + s * kMkStage, wt + (t.kt0 + q) * ktile_stride + (uint64_t)(t.r * 16) * 1024, wbytes,
+                                  &full[s]);
+                        tma_load_2d(ring + s * kMkStage + kMkW, tm, (int)((t.kt0 + q) * 64), (int)(t.j * op.tt), &full[s]);
+                    }
+                    it += t.nk;
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ================= MMA issuer =================
+        if (lane == 0) {
+            uint32_t it = 0, acc = 0;
+            for (uint32_t i = 0; i < n_ops; ++i) {
+                const MkOp& op = ops[i];
+                if (op.kind != MK_GEMM) continue;
+                const uint32_t idesc = umma_idesc_bf16(128, (int)op.tt);
+                for (uint32_t g = blockIdx.x; g < op.n_tasks; g += gridDim.x) {
+                    const MkTile t = mk_tile(op, g);
+                    const uint32_t b = acc & 1;
+                    mk_wait(&tempty[b], ((acc >> 1) & 1) ^ 1, ctl);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t dcol = tmem + b * kMkTT;
+                    for (uint32_t q = 0; q < t.nk; ++q) {
+                        const uint32_t s = it % kMkStages;
+                        mk_wait(&full[s], (it / kMkStages) & 1, ctl);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint64_t ad = umma_desc_sw128(ring + s * kMkStage), bd = umma_desc_sw128(ring + s * kMkStage + kMkW);
+#pragma unroll
+                        for (uint32_t kk = 0; kk < 4; ++kk) umma_f16(dcol, ad + kk * 2, bd + kk * 2, idesc, (q | kk) != 0);
+                        umma_commit(&empty[s]);
+                        ++it;
+                    }
+                    umma_commit(&tfull[b]);
+                    ++acc;
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ================= epilogue / CUDA-core tasks (warps 2-5) =================
+        const uint32_t e = threadIdx.x - 64, quarter = warp & 3, ew = e >> 5;
+        uint32_t acc = 0;
+        for (uint32_t i = 0; i < n_ops; ++i) {
+            const MkOp& op = ops[i];
+            if (blockIdx.x >= op.n_tasks) continue;
+            // activations of op i - 1 and this op's weights are visible to the 128 threads
+            if (e == 0) {
+                if (op.dep >= 0) mk_wait_op(op_cnt + op.dep, ops[op.dep].n_tasks, ctl);
+                wait_ready_thread(op.w);
+                if (op.kind != MK_GEMM) trace_max(op.layer, 1, globaltimer());
+            }
+            mk_bar();
+            for (uint32_t g = blockIdx.x; g < op.n_tasks; g += gridDim.x) {
+                if (e == 0) trace_max(op.layer, 0, ~globaltimer());
+                switch (op.kind) {
+                    case MK_GEMM: {
+                        const GemmArgs& a = op.gemm;
+                        const MkTile t = mk_tile(op, g);
+                        const uint32_t b = acc & 1;
+                        mk_wait(&tfull[b], (acc >> 1) & 1, ctl);
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint32_t row = quarter * 32 + lane, n = t.r * 128 + row;
+                        const bool nok = n < a.N;
+                        const float bias = a.has_bias && nok ? bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off))[n])
+                                                            : 0.0f;
+                        const uint32_t tile = t.r * op.n_tt + t.j;
+                        float* myp = part + ((uint64_t)tile * op.splits + t.z) * (128 * kMkTT);
+                        for (uint32_t c0 = 0; c0 < op.tt; c0 += 32) {
+                            uint32_t v[32];
+                            tmem_ld32(tmem + ((quarter * 32) << 16) + b * kMkTT + c0, v);
+                            if (op.splits > 1) {
+#pragma unroll
+                                for (uint32_t c = 0; c < 32; ++c)
+                                    if (c0 + c < op.tt) __stcg(myp + (c0 + c) * 128 + row, __uint_as_float(v[c]));
+                            } else if (nok) {
+#pragma unroll
+                                for (uint32_t c = 0; c < 32; ++c) {
+                                    const uint32_t tok = t.j * op.tt + c0 + c;
+                                    if (c0 + c < op.tt && tok < a.M) mk_store(a, tok, n, __uint_as_float(v[c]), bias);
+                                }
+                            }
+                        }
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        mk_bar();
+                        if (e == 0) mbar_arrive(&tempty[b]);
+                        ++acc;
+                        if (op.splits > 1) {
+                            // the last split to arrive sums the partials in split order and runs the epilogue
+                            __threadfence();
+                            mk_bar();
+                            if (e == 0) *flag = atomicAdd(tile_ctr + tile, 1u) == op.splits - 1;
+                            mk_bar();
+                            if (*flag) {
+                                __threadfence();
+                                const float* p0 = part + (uint64_t)tile * op.splits * (128 * kMkTT);
+                                for (uint32_t c = 0; c < op.tt; ++c) {
+                                    const uint32_t tok = t.j * op.tt + c;
+                                    if (tok >= a.M || !nok) continue;
+                                    float x = __ldcg(p0 + c * 128 + row);
+                                    for (uint32_t z = 1; z < op.splits; ++z) x += __ldcg(p0 + (uint64_t)z * (128 * kMkTT) + c * 128 + row);
+                                    mk_store(a, tok, n, x, bias);
+                                }
+                                if (e == 0) tile_ctr[tile] = 0;  // self-reset for the next GEMM
+                            }
+                        }
+                        break;
+                    }
+                    case MK_LN:
+                        mk_layernorm(dd, op.ln, g * 4 + ew, lane);
+                        break;
+                    case MK_EMBED:
+                        mk_embed(dd, op.embed, g, e, ctl);
+                        break;
+                    case MK_GEMV:
+                        if (op.gemv.rows <= 1) mk_gemv<1>(dd, op.gemv, g * kMkGemvFeat, reinterpret_cast<float*>(cmp), e);
+                        else mk_gemv<8>(dd, op.gemv, g * kMkGemvFeat, reinterpret_cast<float*>(cmp), e);
+                        break;
+                    case MK_ATTN: {
+                        const AttnArgs& a = op.attn;
+                        const uint32_t h = g % a.H, q0 = (g / a.H) * kAttnSplitRows;
+                        uint16_t* kv = reinterpret_cast<uint16_t*>(cmp);
+                        if (a.dh == 64) attn_split_core<64>(a, h, q0, kv, e, mk_bar);
+                        else if (a.dh == 32) attn_split_core<32>(a, h, q0, kv, e, mk_bar);
+                        else attn_split_core<16>(a, h, q0, kv, e, mk_bar);
+                        mk_bar();  // the staging buffers are rewritten by the next task
+                        break;
+                    }
+                    default:
+                        break;
+                }
+                mk_bar();
+                if (e == 0) {
+                    mk_done(op_cnt + i);
+                    trace_max(op.layer, 2, globaltimer());
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kMkTmemCols) : "memory");
+}
+
+void launch_mega(cudaStream_t s, int ctas, const DevDesc* d, const MkOp* ops, uint32_t n_ops, uint32_t* op_cnt,
+                 const CUtensorMap* tmaps, uint32_t* tile_ctr, float* part) {
+    k_mega<<<ctas, kMkThreads, mega_smem_bytes(), s>>>(d, ops, n_ops, op_cnt, tmaps, tile_ctr, part);
+}
+
+void init_mega_attrs() {
+    cudaFuncSetAttribute(k_mega, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mega_smem_bytes());
+}
+
+void set_trace_mega(unsigned long long* t) { cudaMemcpyToSymbol(g_trace, &t, sizeof t); }
+
+}  // namespace fsw

@@ -49,6 +49,124 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
 }
 
 // ==========================================================================================
+// persistent transformer kernel (mega.cu): eligibility, tiling, op table
+// ==========================================================================================
+// Tiling of one swap-AB GEMM op of k_mega: tt tokens per tile (UMMA N) and `splits` K ranges, chosen by
+// a per-CTA cost model over one CTA per SM: a task streams kt_per k-tiles of (weight rows + tt tokens)
+// x 128 B into its SM (~45 GB/s per SM of L2 -> SM bandwidth) plus ~0.6 us of fixed
+// cost; split-K adds its partial write and the last split's reduction.
+struct MkTiling { uint32_t tt, splits, kt_per; };
+static MkTiling mega_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, int ctas) {
+    MkTiling best{kMkTT, 1, kt};
+    double best_c = 1e30;
+    for (uint32_t tt : {16u, 32u, 64u}) {
+        if (tt > kMkTT) break;
+        for (uint32_t s = 1; s <= 8 && s <= kt; ++s) {
+            const uint32_t kp = (kt + s - 1) / s;
+            if ((kt + kp - 1) / kp != s) continue;
+            const uint64_t tasks = (uint64_t)((n_pad + 127) / 128) * ((M + tt - 1) / tt) * s;
+            const double waves = (double)((tasks + ctas - 1) / ctas);
+            const double bytes = (double)kp * (std::min<uint32_t>(128, n_pad) * 128 + tt * 128);
+            double cost = waves * (0.6 + bytes / 45e3);
+            if (s > 1) cost += 1.0 + s * tt * 512.0 / 45e3;
+            if (cost < best_c - 1e-9) {
+                best_c = cost;
+                best = {tt, s, kp};
+            }
+        }
+    }
+    return best;
+}
+
+fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g) {
+    (void)c;
+    MegaPlan& mp = p.mega;
+    mp.on = false;
+    static const bool off = getenv("FSW_MEGA") && atoi(getenv("FSW_MEGA")) == 0;  // A/B: the per-op kernels
+    if (off) return FSW_OK;
+    // eligible: transformer ops only, shapes the kernel's shared memory holds
+    for (const Launch& x : p.launches) {
+        switch (x.kind) {
+            case K_EMBED: break;
+            case K_LN: if (x.ln.C % 4) return FSW_OK; break;
+            case K_GEMV: if ((x.gemv.rows <= 1 ? 1 : 8) * x.gemv.K * 4 > 56 * 1024 || x.gemv.K % 8) return FSW_OK; break;
+            case K_GEMM: if (x.gemm.conv || x.gemm.pair_t || !x.abase) return FSW_OK; break;
+            case K_ATTN: if (x.attn.T > 128 || !(x.attn.dh == 16 || x.attn.dh == 32 || x.attn.dh == 64)) return FSW_OK; break;
+            default: return FSW_OK;
+        }
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g.dev);
+    mp.ctas = sms;
+    std::vector<CUtensorMap> maps;
+    uint64_t part_bytes = 0;
+    mp.ops.clear();
+    for (const Launch& x : p.launches) {
+        MkOp op;
+        memset(&op, 0, sizeof op);
+        op.layer = x.layer;
+        op.dep = (int32_t)mp.ops.size() - 1;
+        switch (x.kind) {
+            case K_EMBED:
+                op.kind = MK_EMBED;
+                op.embed = x.embed;
+                op.n_tasks = x.embed.T;
+                break;
+            case K_LN:
+                op.kind = MK_LN;
+                op.ln = x.ln;
+                op.n_tasks = (x.ln.rows + 3) / 4;
+                break;
+            case K_GEMV:
+                op.kind = MK_GEMV;
+                op.gemv = x.gemv;
+                op.n_tasks = (x.gemv.N + 63) / 64;
+                break;
+            case K_ATTN:
+                op.kind = MK_ATTN;
+                op.attn = x.attn;
+                op.attn.layer = x.layer;
+                op.n_tasks = x.attn.H * ((x.attn.T + 15) / 16);
+                break;
+            case K_GEMM: {
+                op.kind = MK_GEMM;
+                op.gemm = x.gemm;
+                const MkTiling t = mega_tiling(x.gemm.M, x.gemm.n_pad, x.gemm.K / 64, sms);
+                op.tt = t.tt;
+                op.splits = t.splits;
+                op.kt_per = t.kt_per;
+                op.n_rt = (x.gemm.n_pad + 127) / 128;
+                op.n_tt = (x.gemm.M + t.tt - 1) / t.tt;
+                op.n_tasks = op.n_rt * op.n_tt * op.splits;
+                op.tmap = (uint32_t)maps.size();
+                CUtensorMap tm;
+                if (!make_tmap_act(&tm, x.abase, x.gemm.M, x.a_cols, x.a_cols, t.tt))
+                    return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (mega, layer %d)", x.layer);
+                maps.push_back(tm);
+                if (op.n_rt * op.n_tt > kGemmCtrs) return FSW_OK;
+                if (op.splits > 1) part_bytes = std::max<uint64_t>(part_bytes, (uint64_t)op.n_rt * op.n_tt * op.splits * 128 * kMkTT * 4);
+                break;
+            }
+            default:
+                return FSW_OK;
+        }
+        mp.ops.push_back(op);
+    }
+    if (mp.ops.empty()) return FSW_OK;
+    const uint64_t part_off = align_up(p.ws_bytes, 1024);
+    if (part_off + part_bytes > g.ws_bytes) return FSW_OK;  // no room: the per-op kernels run it
+    p.ws_bytes = align_up(part_off + part_bytes, 1024);
+    mp.part = reinterpret_cast<float*>(g.ws + part_off);
+    CU(cudaMalloc(&mp.op_cnt, sizeof(uint32_t) * mp.ops.size()));
+    if (!maps.empty()) {
+        CU(cudaMalloc(&mp.tmaps, sizeof(CUtensorMap) * maps.size()));
+        CU(cudaMemcpy(mp.tmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
+    }
+    mp.on = true;
+    return FSW_OK;
+}
+
+// ==========================================================================================
 // plan: workspace layout + kernel list for one (model, GPU)
 // ==========================================================================================
 fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
@@ -248,6 +366,8 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                         if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), pt / 2))
                             return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
                     } else {
+                        x.abase = abase;
+                        x.a_cols = slot_cols(si);
                         set_tiling(a, (a.M + 127) / 128, 128, 128 * 128);
                         if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), 128 / a.mc))
                             return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
@@ -345,6 +465,10 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
         return fail(FSW_ENOMEM, "plan: workspace needs %llu bytes > %llu", (unsigned long long)p->ws_bytes, (unsigned long long)g.ws_bytes);
     for (Launch& x : p->launches)
         if (x.kind == K_GEMM) x.gemm.part = reinterpret_cast<float*>(g.ws + part_off);
+    {
+        const fsw_status ms = build_mega(c, m, *p, g);
+        if (ms != FSW_OK) return ms;
+    }
     p->built = true;
     m.plans[gi] = std::move(p);
     return FSW_OK;

@@ -73,6 +73,8 @@ struct Launch {  // one kernel of the layer graph (addresses resolved for one GP
     AttnArgs attn;
     Im2colArgs im2col;
     PoolArgs pool;
+    const void* abase = nullptr;  // K_GEMM (linear): the bf16 activation matrix [M][a_cols] the A tiles come from
+    uint32_t a_cols = 0;
 };
 
 struct Gpu;
@@ -99,6 +101,7 @@ struct GraphKey {
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     uint64_t last_use = 0;
+    void* mk_ops = nullptr;  // the persistent kernel's op table of this graph (device memory), or null
 };
 constexpr size_t kMaxBakedGraphs = 8;
 
@@ -126,9 +129,23 @@ struct ZPieceSet {
     uint64_t cfrom = 0, cend = 0;                        // coded bytes [cfrom, cend) cover the pieces
 };
 
+// The persistent transformer kernel's plan (mega.cu): the op list without the per-invoke waits, one
+// activation tensor map per GEMM op (device array), the per-op completion counters.
+struct MegaPlan {
+    bool on = false;
+    std::vector<MkOp> ops;             // w filled per graph (cold / warm, engine)
+    std::vector<int> launch_of;        // index into Plan::launches of each op
+    CUtensorMap* tmaps = nullptr;      // device
+    uint32_t* op_cnt = nullptr;        // device, zeroed by the graph before the kernel
+    float* part = nullptr;             // split-K partials (workspace)
+    int ctas = 148;
+};
+
 struct Plan {  // one model on one GPU
     bool built = false;
     std::vector<Launch> launches;
+    MegaPlan mega;
+    void* last_mk_ops = nullptr;  // set by build_graph: the op table the new graph bakes
     std::vector<uint64_t> slot_off;      // workspace offset of each slot
     std::vector<int64_t> shadow_off;     // bf16 shadow of an f32 slot, or -1
     uint64_t ws_bytes = 0;
@@ -343,6 +360,7 @@ int gpu_numa_node(int dev);                                                     
 constexpr uint64_t kNumaChunk = 2ull << 20;  // NUMA binding unit of the host stores (one THP page)
 inline int chunk_node(const std::vector<int>& map, uint64_t off) { return map.empty() ? -1 : map[off / kNumaChunk]; }
 fsw_status build_plan(fsw_ctx* c, Model& m, int gi);                             // plan.cpp
+fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g);                   // plan.cpp
 fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint32_t seed, uint64_t from,
                       PieceSet** out);                                           // graph.cpp
 const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams, uint64_t from);

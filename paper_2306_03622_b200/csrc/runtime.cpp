@@ -106,6 +106,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaSetDevice(g.dev));
     CU(cudaFree(nullptr));  // create the context now (one shared runtime per GPU)
     init_gemm_attrs();
+    init_mega_attrs();
     init_ops_attrs();
     init_swap_attrs();
     CU(cudaStreamCreateWithFlags(&g.sx, cudaStreamNonBlocking));
@@ -158,6 +159,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
         set_trace_swap(g.trace);
         set_trace_ops(g.trace);
         set_trace_gemm(g.trace);
+        set_trace_mega(g.trace);
     }
     CU(cudaEventCreateWithFlags(&g.evfork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&g.evjoin, cudaEventDisableTiming));
@@ -241,8 +243,15 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
 
 void free_plan(Gpu& g, Plan& p) {
     cudaSetDevice(g.dev);
-    for (auto& kv : p.graphs) cudaGraphExecDestroy(kv.second.exec);
+    for (auto& kv : p.graphs) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaFree(kv.second.mk_ops);
+    }
     p.graphs.clear();
+    cudaFree(p.mega.tmaps);
+    cudaFree(p.mega.op_cnt);
+    p.mega.tmaps = nullptr;
+    p.mega.op_cnt = nullptr;
     for (auto& kv : p.pieces) cudaFree(kv.second.dev);
     p.pieces.clear();
     for (auto& kv : p.stripe) cudaFree(kv.second.dev);  // UVA: any current device
