@@ -92,19 +92,31 @@ __device__ __forceinline__ MkTile mk_tile(const MkOp& op, uint32_t g) {
     return t;
 }
 
-// ---- epilogue of one GEMM output element ------------------------------------------------------------
-__device__ __forceinline__ void mk_store(const GemmArgs& a, uint32_t tok, uint32_t n, float x, float bias) {
-    x += bias;
-    if (a.res) {
-        const uint64_t ri = (uint64_t)tok * a.ld_res + n;
-        x += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
-                        : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
+// ---- GEMM epilogue of 32 tokens [tok0, tok0 + 32) of output feature n ------------------------------------
+// All residual loads are issued before any use (one L2 round trip per 32 tokens, not one per token: the
+// per-token load -> add -> store chain cost ~1 us per token).  Output = act((acc + b) + res), the order
+// of the unfused definition.
+__device__ __forceinline__ void mk_store32(const GemmArgs& a, uint32_t tok0, uint32_t ntok, uint32_t n, const float (&acc)[32],
+                                           float bias) {
+    float rv[32];
+#pragma unroll
+    for (uint32_t c = 0; c < 32; ++c) {
+        rv[c] = 0.0f;
+        if (a.res && c < ntok) {
+            const uint64_t ri = (uint64_t)(tok0 + c) * a.ld_res + n;
+            rv[c] = a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
+                               : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
+        }
     }
-    x = apply_act(a.act, x);
-    const uint64_t oi = (uint64_t)tok * a.ld_out + n;
-    if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
-    else reinterpret_cast<float*>(a.out)[oi] = x;
-    if (a.out2) a.out2[oi] = f32_to_bf16(x);
+#pragma unroll
+    for (uint32_t c = 0; c < 32; ++c) {
+        if (c >= ntok) break;
+        const float x = apply_act(a.act, (acc[c] + bias) + rv[c]);
+        const uint64_t oi = (uint64_t)(tok0 + c) * a.ld_out + n;
+        if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
+        else reinterpret_cast<float*>(a.out)[oi] = x;
+        if (a.out2) a.out2[oi] = f32_to_bf16(x);
+    }
 }
 
 // ---- CUDA-core tasks (128 threads, tid e) --------------------------------------------------------------
@@ -118,50 +130,91 @@ __device__ __forceinline__ void mk_embed(const DevDesc& dd, const EmbedArgs& a, 
         }
         row[j] = r;
     }
-    for (uint32_t c = e; c < a.C; c += 128) {
-        float s = 0.0f;
-        for (int j = 0; j < a.n_tables; ++j)
-            s += bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.table_off[j]))[(uint64_t)row[j] * a.C + c]);
-        if (a.out) a.out[(uint64_t)t * a.C + c] = s;
-        if (a.out_bf16) a.out_bf16[(uint64_t)t * a.C + c] = f32_to_bf16(s);
+    // 8 columns per thread per pass, every table load of the pass in flight before the stores
+    for (uint32_t c0 = 0; c0 < a.C; c0 += 8 * 128) {
+        float s[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] = 0.0f;
+        for (int j = 0; j < a.n_tables; ++j) {
+            const unsigned short* tab = reinterpret_cast<const unsigned short*>(weight_ptr(dd, a.table_off[j])) + (uint64_t)row[j] * a.C;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t c = c0 + e + u * 128;
+                if (c < a.C) s[u] += bf16_to_f32(__ldcg(tab + c));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t c = c0 + e + u * 128;
+            if (c >= a.C) break;
+            if (a.out) a.out[(uint64_t)t * a.C + c] = s[u];
+            if (a.out_bf16) a.out_bf16[(uint64_t)t * a.C + c] = f32_to_bf16(s[u]);
+        }
     }
 }
 
-// one warp per row: fp32 two-pass statistics over the row read through L2 (as k_layernorm)
-__device__ __forceinline__ void mk_layernorm(const DevDesc& dd, const LnArgs& a, uint32_t r, uint32_t lane) {
+__device__ __forceinline__ void mk_ln_out(const LnArgs& a, uint32_t r, uint32_t c, float4 v, float mu, float inv, uint2 gv,
+                                          uint2 bv) {
+    float4 y;
+    y.x = (v.x - mu) * inv * __uint_as_float(gv.x << 16) + __uint_as_float(bv.x << 16);
+    y.y = (v.y - mu) * inv * __uint_as_float(gv.x & 0xffff0000u) + __uint_as_float(bv.x & 0xffff0000u);
+    y.z = (v.z - mu) * inv * __uint_as_float(gv.y << 16) + __uint_as_float(bv.y << 16);
+    y.w = (v.w - mu) * inv * __uint_as_float(gv.y & 0xffff0000u) + __uint_as_float(bv.y & 0xffff0000u);
+    if (a.out_f32) reinterpret_cast<float4*>(a.out_f32 + (uint64_t)r * a.C)[c] = y;
+    if (a.out_bf16) {
+        const uint32_t lo = (uint32_t)f32_to_bf16(y.x) | ((uint32_t)f32_to_bf16(y.y) << 16);
+        const uint32_t hi = (uint32_t)f32_to_bf16(y.z) | ((uint32_t)f32_to_bf16(y.w) << 16);
+        reinterpret_cast<uint2*>(a.out_bf16 + (uint64_t)r * a.C)[c] = make_uint2(lo, hi);
+    }
+}
+
+// one warp per row: the row held in registers (NV float4 per lane, all loads in flight at once), fp32
+// two-pass statistics (mean, then centred variance) as k_layernorm
+template <int NV>
+__device__ __forceinline__ void mk_layernorm_nv(const DevDesc& dd, const LnArgs& a, uint32_t r, uint32_t lane) {
     if (r >= a.rows) return;
     const float4* x = reinterpret_cast<const float4*>(a.in + (uint64_t)r * a.C);
     const uint2* g = reinterpret_cast<const uint2*>(weight_ptr(dd, a.g_off));
     const uint2* b = reinterpret_cast<const uint2*>(weight_ptr(dd, a.b_off));
     const uint32_t n4 = a.C >> 2;
-    float s = 0.0f;
-    for (uint32_t c = lane; c < n4; c += 32) {
-        const float4 v = __ldcg(x + c);
-        s += (v.x + v.y) + (v.z + v.w);
+    float4 v[NV];
+    uint2 gv[NV], bv[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const uint32_t c = lane + 32u * j;
+        v[j] = c < n4 ? __ldcg(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[j] = c < n4 ? g[c] : make_uint2(0u, 0u);
+        bv[j] = c < n4 ? b[c] : make_uint2(0u, 0u);
     }
+    float s = 0.0f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
     const float mu = warp_sum(s) / (float)a.C;
     float q = 0.0f;
-    for (uint32_t c = lane; c < n4; c += 32) {
-        const float4 v = __ldcg(x + c);
-        const float d0 = v.x - mu, d1 = v.y - mu, d2 = v.z - mu, d3 = v.w - mu;
-        q += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
-    }
-    const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
-    for (uint32_t c = lane; c < n4; c += 32) {
-        const float4 v = __ldcg(x + c);
-        const uint2 gv = g[c], bv = b[c];
-        float4 y;
-        y.x = (v.x - mu) * inv * __uint_as_float(gv.x << 16) + __uint_as_float(bv.x << 16);
-        y.y = (v.y - mu) * inv * __uint_as_float(gv.x & 0xffff0000u) + __uint_as_float(bv.x & 0xffff0000u);
-        y.z = (v.z - mu) * inv * __uint_as_float(gv.y << 16) + __uint_as_float(bv.y << 16);
-        y.w = (v.w - mu) * inv * __uint_as_float(gv.y & 0xffff0000u) + __uint_as_float(bv.y & 0xffff0000u);
-        if (a.out_f32) reinterpret_cast<float4*>(a.out_f32 + (uint64_t)r * a.C)[c] = y;
-        if (a.out_bf16) {
-            const uint32_t lo = (uint32_t)f32_to_bf16(y.x) | ((uint32_t)f32_to_bf16(y.y) << 16);
-            const uint32_t hi = (uint32_t)f32_to_bf16(y.z) | ((uint32_t)f32_to_bf16(y.w) << 16);
-            reinterpret_cast<uint2*>(a.out_bf16 + (uint64_t)r * a.C)[c] = make_uint2(lo, hi);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (lane + 32u * j < n4) {
+            const float d0 = v[j].x - mu, d1 = v[j].y - mu, d2 = v[j].z - mu, d3 = v[j].w - mu;
+            q += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
         }
     }
+    const float inv = rsqrtf(warp_sum(q) / (float)a.C + a.eps);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const uint32_t c = lane + 32u * j;
+        if (c >= n4) break;
+        mk_ln_out(a, r, c, v[j], mu, inv, gv[j], bv[j]);
+    }
+}
+
+__device__ __forceinline__ void mk_layernorm(const DevDesc& dd, const LnArgs& a, uint32_t r, uint32_t lane) {
+    const uint32_t nv = (a.C / 4 + 31) / 32;
+    if (nv <= 2) mk_layernorm_nv<2>(dd, a, r, lane);
+    else if (nv <= 4) mk_layernorm_nv<4>(dd, a, r, lane);
+    else if (nv <= 6) mk_layernorm_nv<6>(dd, a, r, lane);
+    else if (nv <= 8) mk_layernorm_nv<8>(dd, a, r, lane);
+    else if (nv <= 13) mk_layernorm_nv<13>(dd, a, r, lane);
+    else mk_layernorm_nv<16>(dd, a, r, lane);
 }
 
 // GEMV task: features [o0, o0 + 64) of a rows <= 8 linear; x staged in shared memory as fp32
@@ -375,11 +428,12 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                                 for (uint32_t c = 0; c < 32; ++c)
                                     if (c0 + c < op.tt) __stcg(myp + (c0 + c) * 128 + row, __uint_as_float(v[c]));
                             } else if (nok) {
+                                const uint32_t tok0 = t.j * op.tt + c0;
+                                const uint32_t ntok = tok0 < a.M ? min(min(32u, op.tt - c0), a.M - tok0) : 0u;
+                                float x[32];
 #pragma unroll
-                                for (uint32_t c = 0; c < 32; ++c) {
-                                    const uint32_t tok = t.j * op.tt + c0 + c;
-                                    if (c0 + c < op.tt && tok < a.M) mk_store(a, tok, n, __uint_as_float(v[c]), bias);
-                                }
+                                for (uint32_t c = 0; c < 32; ++c) x[c] = __uint_as_float(v[c]);
+                                mk_store32(a, tok0, ntok, n, x, bias);
                             }
                         }
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -395,12 +449,21 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                             if (*flag) {
                                 __threadfence();
                                 const float* p0 = part + (uint64_t)tile * op.splits * (128 * kMkTT);
-                                for (uint32_t c = 0; c < op.tt; ++c) {
-                                    const uint32_t tok = t.j * op.tt + c;
-                                    if (tok >= a.M || !nok) continue;
-                                    float x = __ldcg(p0 + c * 128 + row);
-                                    for (uint32_t z = 1; z < op.splits; ++z) x += __ldcg(p0 + (uint64_t)z * (128 * kMkTT) + c * 128 + row);
-                                    mk_store(a, tok, n, x, bias);
+                                for (uint32_t c0 = 0; nok && c0 < op.tt; c0 += 32) {
+                                    const uint32_t tok0 = t.j * op.tt + c0;
+                                    const uint32_t ntok = tok0 < a.M ? min(min(32u, op.tt - c0), a.M - tok0) : 0u;
+                                    float x[32];  // splits summed in split order, 32 loads in flight per split
+#pragma unroll
+                                    for (uint32_t c = 0; c < 32; ++c) x[c] = c < ntok ? __ldcg(p0 + (c0 + c) * 128 + row) : 0.0f;
+                                    for (uint32_t z = 1; z < op.splits; ++z) {
+                                        const float* pz = p0 + (uint64_t)z * (128 * kMkTT);
+                                        float y[32];
+#pragma unroll
+                                        for (uint32_t c = 0; c < 32; ++c) y[c] = c < ntok ? __ldcg(pz + (c0 + c) * 128 + row) : 0.0f;
+#pragma unroll
+                                        for (uint32_t c = 0; c < 32; ++c) x[c] += y[c];
+                                    }
+                                    mk_store32(a, tok0, ntok, n, x, bias);
                                 }
                                 if (e == 0) tile_ctr[tile] = 0;  // self-reset for the next GEMM
                             }
