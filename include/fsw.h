@@ -336,6 +336,14 @@ fsw_status fsw_debug_litmus(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint32
 fsw_status fsw_debug_trace_read(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint64_t* out, uint32_t cap_layers,
                                 uint64_t* t_invoke);
 
+/* Phase stamps of the persistent transformer kernel's last run on `gpu` (environment FSW_MEGA_STAMPS=1 at plan
+ * time; tools/mega_phases.py): out = [n_ops][ctas][8] %globaltimer ns (producer dependency resolved, MMA first
+ * stage full, last commit, epilogue accumulator ready, epilogue stored, task done, compute task dependency
+ * resolved, compute body done; 0 = none), ops_out (nullable) = [n_ops][4] (kind, n_tasks, tt, splits).  ESTATE
+ * without the persistent-kernel plan or stamps; EINVAL if cap < n_ops·ctas·8 (*n_ops, *ctas still set). */
+fsw_status fsw_debug_mega_stamps(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint64_t* out, uint32_t* ops_out, uint64_t cap,
+                                 uint32_t* n_ops, uint32_t* ctas);
+
 /* Debug / test read-back (copies into caller host memory). */
 fsw_status fsw_debug_read_resident(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, void* dst, uint64_t cap);
 fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);

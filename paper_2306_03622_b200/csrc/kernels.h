@@ -259,6 +259,7 @@ constexpr uint32_t kMkTT = 64;  // largest token tile
 void launch_mega(cudaStream_t s, int ctas, const DevDesc* d, const MkOp* ops, uint32_t n_ops, uint32_t* op_cnt,
                  const CUtensorMap* tmaps, uint32_t* tile_ctr, float* part);
 size_t mega_smem_bytes();
+void set_mega_stamps(unsigned long long* p);  // current device; phase stamps [n_ops][ctas][8] or nullptr
 void init_mega_attrs();
 
 void init_gemm_attrs();

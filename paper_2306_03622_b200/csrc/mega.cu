@@ -38,6 +38,17 @@ constexpr uint64_t kMkWatchdogNs = 4ull * 1000 * 1000 * 1000;
 
 size_t mega_smem_bytes() { return 1024 + kMkRing + kMkCompute + 256; }
 
+// Phase stamps (FSW_MEGA_STAMPS=1, tools/mega_phases.py): per (op, CTA) the %globaltimer of
+// [0] producer: dependency resolved (activation loads issued), [1] MMA: first stage full, [2] MMA: last
+// commit, [3] epilogue: accumulator ready, [4] epilogue: split-K partials published / output stored,
+// [5] task done (counter released), [6] compute task: dependency resolved, [7] compute task: body done.
+__device__ unsigned long long* g_mk_stamp = nullptr;
+__device__ __forceinline__ void mk_stamp(uint32_t op, uint32_t k) {
+    unsigned long long* p = g_mk_stamp;
+    if (p) p[((uint64_t)op * gridDim.x + blockIdx.x) * 8 + k] = globaltimer();
+}
+void set_mega_stamps(unsigned long long* p) { cudaMemcpyToSymbol(g_mk_stamp, &p, sizeof p); }
+
 __device__ __forceinline__ void mk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // mbarrier wait with a watchdog (a lost arrival must end the kernel, not hang the GPU)
@@ -344,6 +355,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         dep_ok = true;
                     }
+                    mk_stamp(i, 0);
                     for (uint32_t q = 0; q < pre; ++q) {
                         const uint32_t s = (it + q) % kMkStages;
                         tma_load_2d(ring + s * kMkStage + kMkW, tm, (int)((t.kt0 + q) * 64), (int)(t.j * op.tt), &full[s]);
@@ -378,6 +390,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                     for (uint32_t q = 0; q < t.nk; ++q) {
                         const uint32_t s = it % kMkStages;
                         mk_wait(&full[s], (it / kMkStages) & 1, ctl);
+                        if (q == 0) mk_stamp(i, 1);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         const uint64_t ad = umma_desc_sw128(ring + s * kMkStage), bd = umma_desc_sw128(ring + s * kMkStage + kMkW);
 #pragma unroll
@@ -386,6 +399,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                         ++it;
                     }
                     umma_commit(&tfull[b]);
+                    mk_stamp(i, 2);
                     ++acc;
                 }
             }
@@ -403,6 +417,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                 if (op.dep >= 0) mk_wait_op(op_cnt + op.dep, ops[op.dep].n_tasks, ctl);
                 wait_ready_thread(op.w);
                 if (op.kind != MK_GEMM) trace_max(op.layer, 1, globaltimer());
+                mk_stamp(i, 6);
             }
             mk_bar();
             for (uint32_t g = blockIdx.x; g < op.n_tasks; g += gridDim.x) {
@@ -414,6 +429,7 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                         const uint32_t b = acc & 1;
                         mk_wait(&tfull[b], (acc >> 1) & 1, ctl);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        if (e == 0) mk_stamp(i, 3);
                         const uint32_t row = quarter * 32 + lane, n = t.r * 128 + row;
                         const bool nok = n < a.N;
                         const float bias = a.has_bias && nok ? bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off))[n])
@@ -438,7 +454,10 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                         }
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         mk_bar();
-                        if (e == 0) mbar_arrive(&tempty[b]);
+                        if (e == 0) {
+                            mbar_arrive(&tempty[b]);
+                            mk_stamp(i, 4);
+                        }
                         ++acc;
                         if (op.splits > 1) {
                             // the last split to arrive sums the partials in split order and runs the epilogue
@@ -495,7 +514,9 @@ __global__ void __launch_bounds__(kMkThreads, 1)
                 }
                 mk_bar();
                 if (e == 0) {
+                    if (op.kind != MK_GEMM) mk_stamp(i, 7);
                     mk_done(op_cnt + i);
+                    mk_stamp(i, 5);
                     trace_max(op.layer, 2, globaltimer());
                 }
             }

@@ -162,6 +162,12 @@ fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g) {
         CU(cudaMalloc(&mp.tmaps, sizeof(CUtensorMap) * maps.size()));
         CU(cudaMemcpy(mp.tmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
     }
+    if (getenv("FSW_MEGA_STAMPS") && atoi(getenv("FSW_MEGA_STAMPS"))) {
+        const size_t n = mp.ops.size() * (size_t)mp.ctas * 8;
+        CU(cudaMalloc(&mp.stamps, n * sizeof(unsigned long long)));
+        CU(cudaMemset(mp.stamps, 0, n * sizeof(unsigned long long)));
+        set_mega_stamps(mp.stamps);  // one model at a time: the last planned model's buffer
+    }
     mp.on = true;
     return FSW_OK;
 }

@@ -139,6 +139,7 @@ struct MegaPlan {
     uint32_t* op_cnt = nullptr;        // device, zeroed by the graph before the kernel
     float* part = nullptr;             // split-K partials (workspace)
     int ctas = 148;
+    unsigned long long* stamps = nullptr;  // FSW_MEGA_STAMPS: [n_ops][ctas][8] phase stamps (device)
 };
 
 struct Plan {  // one model on one GPU

@@ -250,6 +250,8 @@ void free_plan(Gpu& g, Plan& p) {
     p.graphs.clear();
     cudaFree(p.mega.tmaps);
     cudaFree(p.mega.op_cnt);
+    cudaFree(p.mega.stamps);
+    p.mega.stamps = nullptr;
     p.mega.tmaps = nullptr;
     p.mega.op_cnt = nullptr;
     for (auto& kv : p.pieces) cudaFree(kv.second.dev);
@@ -402,6 +404,32 @@ extern "C" fsw_status fsw_debug_trace_read(fsw_ctx* c, uint32_t id, int32_t gpu,
         t_invoke[1] = ctl.t_last;
         t_invoke[2] = ctl.t_end;
     }
+    return FSW_OK;
+}
+
+// Phase stamps of the persistent kernel's last run (FSW_MEGA_STAMPS=1; tools/mega_phases.py): out receives
+// [n_ops][ctas][8] u64 and ops[n_ops][4] = (kind, n_tasks, tt, splits).  *n_ops / *ctas always set.
+extern "C" fsw_status fsw_debug_mega_stamps(fsw_ctx* c, uint32_t id, int32_t gpu, uint64_t* out, uint32_t* ops_out,
+                                            uint64_t cap, uint32_t* n_ops, uint32_t* ctas) {
+    if (!c || !n_ops || !ctas || gpu < 0 || gpu >= (int)c->gpus.size()) return fail(FSW_EINVAL, "mega_stamps: bad argument");
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!m->plans[gpu] || !m->plans[gpu]->mega.on) return fail(FSW_ESTATE, "mega_stamps: no persistent-kernel plan");
+    const MegaPlan& mp = m->plans[gpu]->mega;
+    *n_ops = (uint32_t)mp.ops.size();
+    *ctas = (uint32_t)mp.ctas;
+    if (!mp.stamps) return fail(FSW_ESTATE, "mega_stamps: FSW_MEGA_STAMPS was not set");
+    const size_t n = mp.ops.size() * (size_t)mp.ctas * 8;
+    if (!out || cap < n) return fail(FSW_EINVAL, "mega_stamps: cap");
+    CU(cudaSetDevice(c->gpus[gpu].dev));
+    CU(cudaMemcpy(out, mp.stamps, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (ops_out)
+        for (size_t i = 0; i < mp.ops.size(); ++i) {
+            ops_out[4 * i] = mp.ops[i].kind;
+            ops_out[4 * i + 1] = mp.ops[i].n_tasks;
+            ops_out[4 * i + 2] = mp.ops[i].tt;
+            ops_out[4 * i + 3] = mp.ops[i].splits;
+        }
     return FSW_OK;
 }
 

@@ -149,7 +149,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
            "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal",
            "fsw_debug_set_fault", "fsw_debug_litmus", "fsw_policy_heavy", "fsw_model_set_slo",
-           "fsw_set_heavy_policy", "fsw_debug_trace_read"]
+           "fsw_set_heavy_policy", "fsw_debug_trace_read", "fsw_debug_mega_stamps"]
 
 _lib = None
 
@@ -185,6 +185,7 @@ def lib():
         L.fsw_debug_dmaz_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
         L.fsw_debug_set_fault.argtypes = [vp, u32, u32]
         L.fsw_debug_trace_read.argtypes = [vp, u32, i32, vp, u32, vp]
+        L.fsw_debug_mega_stamps.argtypes = [vp, u32, i32, vp, vp, u64, ctypes.POINTER(u32), ctypes.POINTER(u32)]
         L.fsw_policy_heavy.argtypes = [dbl, dbl, dbl, dbl, dbl, ctypes.POINTER(i32)]
         L.fsw_model_set_slo.argtypes = [vp, u32, dbl]
         L.fsw_set_heavy_policy.argtypes = [vp, dbl, dbl]
@@ -478,6 +479,16 @@ class Runtime:
         ti = np.zeros(3, np.uint64)
         _check(lib().fsw_debug_trace_read(self.h, mid, gpu, out.ctypes.data, n, ti.ctypes.data))
         return out, ti
+
+    def mega_stamps(self, mid: int, gpu: int = 0):
+        """Persistent-kernel phase stamps (FSW_MEGA_STAMPS=1): ([n_ops][ctas][8] ns, [n_ops][4] op info)."""
+        n, c = u32(), u32()
+        lib().fsw_debug_mega_stamps(self.h, mid, gpu, None, None, 0, ctypes.byref(n), ctypes.byref(c))
+        out = np.zeros((n.value, c.value, 8), np.uint64)
+        ops = np.zeros((n.value, 4), np.uint32)
+        _check(lib().fsw_debug_mega_stamps(self.h, mid, gpu, out.ctypes.data, ops.ctypes.data, out.size,
+                                           ctypes.byref(n), ctypes.byref(c)))
+        return out, ops
 
     def read_slot(self, mid: int, slot: int, nbytes: int, gpu: int = 0) -> np.ndarray:
         buf = np.empty(nbytes, dtype=np.uint8)
