@@ -36,7 +36,9 @@ constexpr uint32_t kMkRing = kMkStages * kMkStage;
 constexpr uint32_t kMkTmemCols = 2 * kMkTT;        // two accumulator buffers
 constexpr uint64_t kMkWatchdogNs = 4ull * 1000 * 1000 * 1000;
 
-size_t mega_smem_bytes() { return 1024 + kMkRing + kMkCompute + 256; }
+static_assert(sizeof(MkOp) <= 1024, "MkOp must fit its shared-memory slot");
+constexpr uint32_t kMkOpSmem = 1024;  // the epilogue warps' copy of the current op (sizeof(MkOp) <= 1 KiB)
+size_t mega_smem_bytes() { return 1024 + kMkRing + kMkCompute + kMkOpSmem + 256; }
 
 // Phase stamps (FSW_MEGA_STAMPS=1, tools/mega_phases.py): per (op, CTA) the %globaltimer of
 // [0] producer: dependency resolved (activation loads issued), [1] MMA: first stage full, [2] MMA: last
@@ -284,14 +286,16 @@ __device__ __forceinline__ void mk_gemv(const DevDesc& dd, const GemvArgs& a, ui
     mk_bar();  // xs is rewritten by the next task
 }
 
-__global__ void __launch_bounds__(kMkThreads, 1)
+// 168 registers: 192 x 168 + a 256-thread swap CTA x 64 fit one SM's register file (cold invokes)
+__global__ void __maxnreg__(168)
     k_mega(const DevDesc* __restrict__ d, const MkOp* __restrict__ ops, uint32_t n_ops, uint32_t* op_cnt,
            const CUtensorMap* __restrict__ tmaps, uint32_t* tile_ctr, float* part) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* ring = smem;
     uint8_t* cmp = smem + kMkRing;  // compute region
-    uint64_t* full = reinterpret_cast<uint64_t*>(cmp + kMkCompute);
+    MkOp* sop = reinterpret_cast<MkOp*>(cmp + kMkCompute);  // epilogue warps: the current op, in shared memory
+    uint64_t* full = reinterpret_cast<uint64_t*>(cmp + kMkCompute + kMkOpSmem);
     uint64_t* empty = full + kMkStages;
     uint64_t* tfull = empty + kMkStages;
     uint64_t* tempty = tfull + 2;
@@ -410,8 +414,14 @@ __global__ void __launch_bounds__(kMkThreads, 1)
         const uint32_t e = threadIdx.x - 64, quarter = warp & 3, ew = e >> 5;
         uint32_t acc = 0;
         for (uint32_t i = 0; i < n_ops; ++i) {
-            const MkOp& op = ops[i];
-            if (blockIdx.x >= op.n_tasks) continue;
+            if (blockIdx.x >= ops[i].n_tasks) continue;
+            // the op's arguments in shared memory: global reads of them would miss L1 after every fence
+            // (CCTL.IVALL) and could not be kept in registers across the epilogue's stores
+            mk_bar();  // the previous op's readers are done with sop
+            for (uint32_t k = e; k < sizeof(MkOp) / 4; k += 128)
+                reinterpret_cast<uint32_t*>(sop)[k] = reinterpret_cast<const uint32_t*>(ops + i)[k];
+            mk_bar();
+            const MkOp& op = *sop;
             // activations of op i - 1 and this op's weights are visible to the 128 threads
             if (e == 0) {
                 if (op.dep >= 0) mk_wait_op(op_cnt + op.dep, ops[op.dep].n_tasks, ctl);

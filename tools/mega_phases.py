@@ -39,3 +39,19 @@ with Runtime(gpu_ids=[0], pool_bytes=4 << 30) as rt:
               f"{rel(ph[2], ph[1]):7.2f} | {rel(ph[3], ph[2]):7.2f} | {rel(ph[4], ph[3] if kind == 1 else ph[0]):7.2f} | "
               f"{rel(ph[5], ph[4]):7.2f} | {rel(end, t0):8.2f} (last done - first done {rel(end, float(s[:, 5][s[:, 5] > 0].min())):.2f})")
         prev_done = end
+    # spread: per GEMM op, the slowest CTAs and where their time went
+    print("\nslowest tasks per GEMM op: cta, phases (us): dep-prevdone, dep->full1, full1->commit, commit->acc, acc->stored, stored->done")
+    prev_done = t0
+    for i in range(min(nshow, len(ops))):
+        kind, nt, tt, sp = ops[i]
+        s = st[i, :nt].astype(np.float64)
+        if kind == 1:
+            tot = s[:, 5] - s[:, 0]
+            idx = np.argsort(-s[:, 5])[:4]
+            rows = []
+            for c in idx:
+                p = s[c]
+                rows.append(f"cta {c}: " + " ".join(f"{(p[k + 1] - p[k]) / 1e3 if k >= 0 else (p[0] - prev_done) / 1e3:.2f}"
+                                                    for k in [-1, 0, 1, 2, 3, 4]))
+            print(f"op {i} (tt {tt} splits {sp}): " + " | ".join(rows))
+        prev_done = float(s[:, 5].max())
