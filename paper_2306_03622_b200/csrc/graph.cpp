@@ -364,7 +364,7 @@ static fsw_status enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic,
     if (p.mega.on) {
         // the persistent transformer kernel: one launch; its op table (this invoke configuration's waits)
         // was written to device memory by build_graph before the capture began
-        cudaMemsetAsync(p.mega.op_cnt, 0, sizeof(uint32_t) * p.mega.ops.size(), s);
+        cudaMemsetAsync(p.mega.op_cnt, 0, 128 * (p.mega.ops.size() + (size_t)p.mega.ctas), s);
         launch_mega(s, p.mega.ctas, d, reinterpret_cast<const MkOp*>(p.last_mk_ops), (uint32_t)p.mega.ops.size(),
                     p.mega.op_cnt, p.mega.tmaps, g.gemm_ctr, p.mega.part);
         return FSW_OK;

@@ -70,14 +70,20 @@ __device__ __forceinline__ void mk_wait(uint64_t* b, uint32_t parity, DevCtl* ct
     }
 }
 
-// Spin until op `dep` has counted `need` tasks done (acquire), with back-off and a watchdog.
-__device__ __forceinline__ void mk_wait_op(const uint32_t* cnt, uint32_t need, DevCtl* ctl) {
-    if (ld_acquire_gpu(cnt) >= need) return;
+// Op completion (DESIGN.md §5 k_mega): every task adds 1 to its op's counter (acq_rel); the task that
+// brings it to n_tasks then publishes "ops 0..i are done" into every CTA's own epoch word (a fence, then
+// one store per CTA), so each CTA polls a private 128-B line instead of 300 threads polling one counter
+// (measured: that polling saturated the counter's L2 slice and slowed every load that hashed to it, the
+// split-K reductions 10-25 us).  Counters and epoch words are 128 B apart (kMkLine u32).
+constexpr uint32_t kMkLine = 32;
+__device__ __forceinline__ void mk_wait_op(const uint32_t* epoch, uint32_t dep, DevCtl* ctl) {
+    const uint32_t need = dep + 1;
+    if (ld_acquire_gpu(epoch) >= need) return;
     const uint64_t t0 = globaltimer();
     uint32_t ns = 32;
-    while (ld_acquire_gpu(cnt) < need) {
+    while (ld_acquire_gpu(epoch) < need) {
         __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
+        if (ns < 128) ns <<= 1;
         if (globaltimer() - t0 > kWatchdogNs) {
             atomicExch(&ctl->err, 4);
             return;
@@ -85,9 +91,15 @@ __device__ __forceinline__ void mk_wait_op(const uint32_t* cnt, uint32_t need, D
     }
 }
 
-__device__ __forceinline__ void mk_done(uint32_t* cnt) {
+__device__ __forceinline__ void mk_done(uint32_t* cnt, uint32_t n_tasks, uint32_t* epochs, uint32_t op) {
     __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    if (old + 1 == n_tasks) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (uint32_t c = 0; c < gridDim.x; ++c)
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(epochs + (uint64_t)c * kMkLine), "r"(op + 1) : "memory");
+    }
 }
 
 struct MkTile {
@@ -304,6 +316,8 @@ __global__ void __maxnreg__(168)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevDesc dd = *d;
     DevCtl* ctl = ops[0].w.ctl;
+    uint32_t* epochs = op_cnt + (uint64_t)n_ops * kMkLine;  // [ctas] epoch words after the op counters
+    const uint32_t* my_epoch = epochs + (uint64_t)blockIdx.x * kMkLine;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kMkStages; ++s) {
@@ -332,12 +346,12 @@ __global__ void __maxnreg__(168)
         if (lane == 0) {
             uint32_t it = 0;
             for (uint32_t i = 0; i < n_ops; ++i) {
-                const MkOp& op = ops[i];
+                const MkOp op = ops[i];  // a register / local copy: never reloaded after asm memory clobbers or stores
                 if (op.kind != MK_GEMM || blockIdx.x >= op.n_tasks) continue;
                 wait_ready_thread(op.w);  // the layer's weights landed (cold); no-op when resident
                 trace_max(op.layer, 1, globaltimer());
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                const GemmArgs& a = op.gemm;
+                const GemmArgs a = op.gemm;
                 const uint8_t* wt = weight_ptr(dd, a.w_off);
                 const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
                 const CUtensorMap* tm = tmaps + op.tmap;
@@ -355,7 +369,7 @@ __global__ void __maxnreg__(168)
                                   &full[s]);
                     }
                     if (!dep_ok) {
-                        mk_wait_op(op_cnt + op.dep, ops[op.dep].n_tasks, ctl);
+                        mk_wait_op(my_epoch, (uint32_t)op.dep, ctl);
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                         dep_ok = true;
                     }
@@ -382,7 +396,7 @@ __global__ void __maxnreg__(168)
         if (lane == 0) {
             uint32_t it = 0, acc = 0;
             for (uint32_t i = 0; i < n_ops; ++i) {
-                const MkOp& op = ops[i];
+                const MkOp op = ops[i];  // a register / local copy: never reloaded after asm memory clobbers or stores
                 if (op.kind != MK_GEMM) continue;
                 const uint32_t idesc = umma_idesc_bf16(128, (int)op.tt);
                 for (uint32_t g = blockIdx.x; g < op.n_tasks; g += gridDim.x) {
@@ -421,10 +435,10 @@ __global__ void __maxnreg__(168)
             for (uint32_t k = e; k < sizeof(MkOp) / 4; k += 128)
                 reinterpret_cast<uint32_t*>(sop)[k] = reinterpret_cast<const uint32_t*>(ops + i)[k];
             mk_bar();
-            const MkOp& op = *sop;
+            const MkOp op = *sop;  // thread-local copy: stores through generic pointers cannot alias it
             // activations of op i - 1 and this op's weights are visible to the 128 threads
             if (e == 0) {
-                if (op.dep >= 0) mk_wait_op(op_cnt + op.dep, ops[op.dep].n_tasks, ctl);
+                if (op.dep >= 0) mk_wait_op(my_epoch, (uint32_t)op.dep, ctl);
                 wait_ready_thread(op.w);
                 if (op.kind != MK_GEMM) trace_max(op.layer, 1, globaltimer());
                 mk_stamp(i, 6);
@@ -434,7 +448,7 @@ __global__ void __maxnreg__(168)
                 if (e == 0) trace_max(op.layer, 0, ~globaltimer());
                 switch (op.kind) {
                     case MK_GEMM: {
-                        const GemmArgs& a = op.gemm;
+                        const GemmArgs a = op.gemm;
                         const MkTile t = mk_tile(op, g);
                         const uint32_t b = acc & 1;
                         mk_wait(&tfull[b], (acc >> 1) & 1, ctl);
@@ -473,28 +487,94 @@ __global__ void __maxnreg__(168)
                             // the last split to arrive sums the partials in split order and runs the epilogue
                             __threadfence();
                             mk_bar();
-                            if (e == 0) *flag = atomicAdd(tile_ctr + tile, 1u) == op.splits - 1;
+                            if (e == 0) *flag = atomicAdd(tile_ctr + (uint64_t)tile * kMkLine, 1u) == op.splits - 1;
                             mk_bar();
+                            if (e == 0) mk_stamp(i, 6);
                             if (*flag) {
                                 __threadfence();
+                                // the tile's partials [split][token][row] read as float4 (4 rows of one token) by
+                                // all 128 threads in turn, summed in split order, then bias / residual /
+                                // activation and 8- or 16-B stores of 4 consecutive output features
                                 const float* p0 = part + (uint64_t)tile * op.splits * (128 * kMkTT);
-                                for (uint32_t c0 = 0; nok && c0 < op.tt; c0 += 32) {
-                                    const uint32_t tok0 = t.j * op.tt + c0;
-                                    const uint32_t ntok = tok0 < a.M ? min(min(32u, op.tt - c0), a.M - tok0) : 0u;
-                                    float x[32];  // splits summed in split order, 32 loads in flight per split
+                                const uint32_t nq = op.tt * 32;  // float4 units per split
+                                const uint16_t* bptr = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
+                                for (uint32_t u0 = 0; u0 < nq; u0 += 128 * 4) {
+                                    float4 sacc[4];
 #pragma unroll
-                                    for (uint32_t c = 0; c < 32; ++c) x[c] = c < ntok ? __ldcg(p0 + (c0 + c) * 128 + row) : 0.0f;
-                                    for (uint32_t z = 1; z < op.splits; ++z) {
-                                        const float* pz = p0 + (uint64_t)z * (128 * kMkTT);
-                                        float y[32];
-#pragma unroll
-                                        for (uint32_t c = 0; c < 32; ++c) y[c] = c < ntok ? __ldcg(pz + (c0 + c) * 128 + row) : 0.0f;
-#pragma unroll
-                                        for (uint32_t c = 0; c < 32; ++c) x[c] += y[c];
+                                    for (uint32_t k = 0; k < 4; ++k) {
+                                        const uint32_t u = u0 + k * 128 + e;
+                                        sacc[k] = u < nq ? __ldcg(reinterpret_cast<const float4*>(p0) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
                                     }
-                                    mk_store32(a, tok0, ntok, n, x, bias);
+                                    for (uint32_t z = 1; z < op.splits; ++z) {
+                                        const float4* pz = reinterpret_cast<const float4*>(p0 + (uint64_t)z * (128 * kMkTT));
+                                        float4 y[4];
+#pragma unroll
+                                        for (uint32_t k = 0; k < 4; ++k) {
+                                            const uint32_t u = u0 + k * 128 + e;
+                                            y[k] = u < nq ? __ldcg(pz + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+                                        }
+#pragma unroll
+                                        for (uint32_t k = 0; k < 4; ++k) {
+                                            sacc[k].x += y[k].x;
+                                            sacc[k].y += y[k].y;
+                                            sacc[k].z += y[k].z;
+                                            sacc[k].w += y[k].w;
+                                        }
+                                    }
+                                    float4 rv[4];
+#pragma unroll
+                                    for (uint32_t k = 0; k < 4; ++k) {
+                                        const uint32_t u = u0 + k * 128 + e, c = u >> 5, r4 = (u & 31) * 4;
+                                        const uint32_t tok = t.j * op.tt + c, n4 = t.r * 128 + r4;
+                                        rv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                                        if (u < nq && a.res && tok < a.M && n4 + 3 < a.N) {
+                                            const uint64_t ri = (uint64_t)tok * a.ld_res + n4;
+                                            if (a.res_bf16) {
+                                                const uint2 h = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.res) + ri));
+                                                rv[k] = make_float4(__uint_as_float(h.x << 16), __uint_as_float(h.x & 0xffff0000u),
+                                                                    __uint_as_float(h.y << 16), __uint_as_float(h.y & 0xffff0000u));
+                                            } else {
+                                                rv[k] = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + ri));
+                                            }
+                                        }
+                                    }
+#pragma unroll
+                                    for (uint32_t k = 0; k < 4; ++k) {
+                                        const uint32_t u = u0 + k * 128 + e, c = u >> 5, r4 = (u & 31) * 4;
+                                        const uint32_t tok = t.j * op.tt + c, n4 = t.r * 128 + r4;
+                                        if (u >= nq || tok >= a.M || n4 >= a.N) continue;
+                                        const float xs[4] = {sacc[k].x, sacc[k].y, sacc[k].z, sacc[k].w};
+                                        const float rs[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
+                                        if (n4 + 3 < a.N && a.ld_out % 4 == 0 && (!a.res || a.ld_res % 4 == 0)) {
+                                            float y4[4];
+#pragma unroll
+                                            for (int q = 0; q < 4; ++q)
+                                                y4[q] = apply_act(a.act, (xs[q] + (bptr ? bf16_to_f32(bptr[n4 + q]) : 0.0f)) + rs[q]);
+                                            const uint64_t oi = (uint64_t)tok * a.ld_out + n4;
+                                            const uint2 pk = make_uint2((uint32_t)f32_to_bf16(y4[0]) | ((uint32_t)f32_to_bf16(y4[1]) << 16),
+                                                                        (uint32_t)f32_to_bf16(y4[2]) | ((uint32_t)f32_to_bf16(y4[3]) << 16));
+                                            if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
+                                            else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = make_float4(y4[0], y4[1], y4[2], y4[3]);
+                                            if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
+                                        } else {  // feature tail / unaligned rows: scalar, residual loaded here
+                                            for (int q = 0; q < 4 && n4 + q < a.N; ++q) {
+                                                float x = xs[q] + (bptr ? bf16_to_f32(bptr[n4 + q]) : 0.0f);
+                                                if (a.res) {
+                                                    const uint64_t ri = (uint64_t)tok * a.ld_res + n4 + q;
+                                                    x += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
+                                                                    : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
+                                                }
+                                                x = apply_act(a.act, x);
+                                                const uint64_t oi = (uint64_t)tok * a.ld_out + n4 + q;
+                                                if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
+                                                else reinterpret_cast<float*>(a.out)[oi] = x;
+                                                if (a.out2) a.out2[oi] = f32_to_bf16(x);
+                                            }
+                                        }
+                                    }
                                 }
-                                if (e == 0) tile_ctr[tile] = 0;  // self-reset for the next GEMM
+                                if (e == 0) tile_ctr[(uint64_t)tile * kMkLine] = 0;  // self-reset for the next GEMM
+                                if (e == 0) mk_stamp(i, 7);
                             }
                         }
                         break;
@@ -510,7 +590,7 @@ __global__ void __maxnreg__(168)
                         else mk_gemv<8>(dd, op.gemv, g * kMkGemvFeat, reinterpret_cast<float*>(cmp), e);
                         break;
                     case MK_ATTN: {
-                        const AttnArgs& a = op.attn;
+                        const AttnArgs a = op.attn;
                         const uint32_t h = g % a.H, q0 = (g / a.H) * kAttnSplitRows;
                         uint16_t* kv = reinterpret_cast<uint16_t*>(cmp);
                         if (a.dh == 64) attn_split_core<64>(a, h, q0, kv, e, mk_bar);
@@ -525,7 +605,7 @@ __global__ void __maxnreg__(168)
                 mk_bar();
                 if (e == 0) {
                     if (op.kind != MK_GEMM) mk_stamp(i, 7);
-                    mk_done(op_cnt + i);
+                    mk_done(op_cnt + (uint64_t)i * kMkLine, op.n_tasks, epochs, i);
                     mk_stamp(i, 5);
                     trace_max(op.layer, 2, globaltimer());
                 }

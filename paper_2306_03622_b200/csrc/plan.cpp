@@ -59,16 +59,18 @@ struct MkTiling { uint32_t tt, splits, kt_per; };
 static MkTiling mega_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, int ctas) {
     MkTiling best{kMkTT, 1, kt};
     double best_c = 1e30;
+    static const uint32_t max_split = getenv("FSW_MEGA_MAXSPLIT") ? (uint32_t)atoi(getenv("FSW_MEGA_MAXSPLIT")) : 8;  // A/B
+    static const double split_cost = getenv("FSW_MEGA_SPLITCOST") ? atof(getenv("FSW_MEGA_SPLITCOST")) : 1.0;
     for (uint32_t tt : {16u, 32u, 64u}) {
         if (tt > kMkTT) break;
-        for (uint32_t s = 1; s <= 8 && s <= kt; ++s) {
+        for (uint32_t s = 1; s <= max_split && s <= kt; ++s) {
             const uint32_t kp = (kt + s - 1) / s;
             if ((kt + kp - 1) / kp != s) continue;
             const uint64_t tasks = (uint64_t)((n_pad + 127) / 128) * ((M + tt - 1) / tt) * s;
             const double waves = (double)((tasks + ctas - 1) / ctas);
             const double bytes = (double)kp * (std::min<uint32_t>(128, n_pad) * 128 + tt * 128);
             double cost = waves * (0.6 + bytes / 45e3);
-            if (s > 1) cost += 1.0 + s * tt * 512.0 / 45e3;
+            if (s > 1) cost += split_cost + s * tt * 512.0 / 45e3;
             if (cost < best_c - 1e-9) {
                 best_c = cost;
                 best = {tt, s, kp};
@@ -143,7 +145,7 @@ fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g) {
                 if (!make_tmap_act(&tm, x.abase, x.gemm.M, x.a_cols, x.a_cols, t.tt))
                     return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (mega, layer %d)", x.layer);
                 maps.push_back(tm);
-                if (op.n_rt * op.n_tt > kGemmCtrs) return FSW_OK;
+                if (op.n_rt * op.n_tt * 32 > kGemmCtrs) return FSW_OK;  // tile counters 128 B apart
                 if (op.splits > 1) part_bytes = std::max<uint64_t>(part_bytes, (uint64_t)op.n_rt * op.n_tt * op.splits * 128 * kMkTT * 4);
                 break;
             }
@@ -157,7 +159,8 @@ fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g) {
     if (part_off + part_bytes > g.ws_bytes) return FSW_OK;  // no room: the per-op kernels run it
     p.ws_bytes = align_up(part_off + part_bytes, 1024);
     mp.part = reinterpret_cast<float*>(g.ws + part_off);
-    CU(cudaMalloc(&mp.op_cnt, sizeof(uint32_t) * mp.ops.size()));
+    // per-op counters and per-CTA epoch words, 128 B apart (mega.cu kMkLine)
+    CU(cudaMalloc(&mp.op_cnt, 128 * (mp.ops.size() + (size_t)mp.ctas)));
     if (!maps.empty()) {
         CU(cudaMalloc(&mp.tmaps, sizeof(CUtensorMap) * maps.size()));
         CU(cudaMemcpy(mp.tmaps, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));

@@ -54,4 +54,9 @@ with Runtime(gpu_ids=[0], pool_bytes=4 << 30) as rt:
                 rows.append(f"cta {c}: " + " ".join(f"{(p[k + 1] - p[k]) / 1e3 if k >= 0 else (p[0] - prev_done) / 1e3:.2f}"
                                                     for k in [-1, 0, 1, 2, 3, 4]))
             print(f"op {i} (tt {tt} splits {sp}): " + " | ".join(rows))
+            if sp > 1:
+                last = s[:, 7] > 0
+                print(f"   split-K: stored->flag {np.median((s[:, 6] - s[:, 4])[s[:, 6] > 0]) / 1e3:.2f} us, last arrivers "
+                      f"{int(last.sum())}: flag->reduced median {np.median((s[last, 7] - s[last, 6])) / 1e3:.2f} max "
+                      f"{np.max(s[last, 7] - s[last, 6]) / 1e3:.2f}, reduced->done {np.median(s[last, 5] - s[last, 7]) / 1e3:.2f} us")
         prev_done = float(s[:, 5].max())
