@@ -117,30 +117,74 @@ __device__ __forceinline__ MkTile mk_tile(const MkOp& op, uint32_t g) {
     return t;
 }
 
-// ---- GEMM epilogue of 32 tokens [tok0, tok0 + 32) of output feature n ------------------------------------
-// All residual loads are issued before any use (one L2 round trip per 32 tokens, not one per token: the
-// per-token load -> add -> store chain cost ~1 us per token).  Output = act((acc + b) + res), the order
-// of the unfused definition.
-__device__ __forceinline__ void mk_store32(const GemmArgs& a, uint32_t tok0, uint32_t ntok, uint32_t n, const float (&acc)[32],
-                                           float bias) {
-    float rv[32];
+// ---- GEMM epilogue from the staged tile T[token][row] (fp32, row stride kMkLdt) ------------------------
+// Units of (token, 4 consecutive output features), consecutive threads on consecutive features, kE units
+// per thread with every residual load in flight before any store: out = act((acc + b) + res), the order of
+// the unfused definition, as 8-B (bf16) or 16-B (f32) stores.
+constexpr uint32_t kMkLdt = 132;
+__device__ __forceinline__ void mk_out_tile(const DevDesc& dd, const GemmArgs& a, const float* T, uint32_t tok0, uint32_t n0,
+                                            uint32_t tt, uint32_t e) {
+    const uint16_t* bptr = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
+    const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (!a.res || a.ld_res % 4 == 0);
+    constexpr uint32_t kE = 4;
+    const uint32_t units = tt * 32;
+    for (uint32_t u0 = 0; u0 < units; u0 += kE * 128) {
+        float4 rv[kE];
 #pragma unroll
-    for (uint32_t c = 0; c < 32; ++c) {
-        rv[c] = 0.0f;
-        if (a.res && c < ntok) {
-            const uint64_t ri = (uint64_t)(tok0 + c) * a.ld_res + n;
-            rv[c] = a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
-                               : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
+        for (uint32_t k = 0; k < kE; ++k) {
+            const uint32_t u = u0 + k * 128 + e, tok = tok0 + (u >> 5), n = n0 + (u & 31) * 4;
+            rv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (vec && a.res && u < units && tok < a.M && n < a.N) {
+                const uint64_t ri = (uint64_t)tok * a.ld_res + n;
+                if (a.res_bf16) {
+                    const uint2 h = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.res) + ri));
+                    rv[k] = make_float4(__uint_as_float(h.x << 16), __uint_as_float(h.x & 0xffff0000u), __uint_as_float(h.y << 16),
+                                        __uint_as_float(h.y & 0xffff0000u));
+                } else {
+                    rv[k] = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + ri));
+                }
+            }
         }
-    }
 #pragma unroll
-    for (uint32_t c = 0; c < 32; ++c) {
-        if (c >= ntok) break;
-        const float x = apply_act(a.act, (acc[c] + bias) + rv[c]);
-        const uint64_t oi = (uint64_t)(tok0 + c) * a.ld_out + n;
-        if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
-        else reinterpret_cast<float*>(a.out)[oi] = x;
-        if (a.out2) a.out2[oi] = f32_to_bf16(x);
+        for (uint32_t k = 0; k < kE; ++k) {
+            const uint32_t u = u0 + k * 128 + e, c = u >> 5, tok = tok0 + c, n = n0 + (u & 31) * 4;
+            if (u >= units || tok >= a.M || n >= a.N) continue;
+            const float4 x = *reinterpret_cast<const float4*>(T + c * kMkLdt + (u & 31) * 4);
+            if (vec) {
+                float y[4] = {x.x, x.y, x.z, x.w};
+                const float r[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
+                if (bptr) {
+                    const uint2 bv = *reinterpret_cast<const uint2*>(bptr + n);
+                    y[0] += __uint_as_float(bv.x << 16);
+                    y[1] += __uint_as_float(bv.x & 0xffff0000u);
+                    y[2] += __uint_as_float(bv.y << 16);
+                    y[3] += __uint_as_float(bv.y & 0xffff0000u);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y[q] = apply_act(a.act, y[q] + r[q]);
+                const uint64_t oi = (uint64_t)tok * a.ld_out + n;
+                const uint2 pk = make_uint2((uint32_t)f32_to_bf16(y[0]) | ((uint32_t)f32_to_bf16(y[1]) << 16),
+                                            (uint32_t)f32_to_bf16(y[2]) | ((uint32_t)f32_to_bf16(y[3]) << 16));
+                if (a.out_bf16) __stcg(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi), pk);
+                else __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi), make_float4(y[0], y[1], y[2], y[3]));
+                if (a.out2) __stcg(reinterpret_cast<uint2*>(a.out2 + oi), pk);
+            } else {  // N or a leading dimension not a multiple of 4 (e.g. a 2-wide QA head): scalar
+                const float xs[4] = {x.x, x.y, x.z, x.w};
+                for (uint32_t q = 0; q < 4 && n + q < a.N; ++q) {
+                    float v = xs[q] + (bptr ? bf16_to_f32(bptr[n + q]) : 0.0f);
+                    if (a.res) {
+                        const uint64_t ri = (uint64_t)tok * a.ld_res + n + q;
+                        v += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
+                                        : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
+                    }
+                    v = apply_act(a.act, v);
+                    const uint64_t oi = (uint64_t)tok * a.ld_out + n + q;
+                    if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
+                    else reinterpret_cast<float*>(a.out)[oi] = v;
+                    if (a.out2) a.out2[oi] = f32_to_bf16(v);
+                }
+            }
+        }
     }
 }
 
@@ -454,59 +498,48 @@ __global__ void __maxnreg__(168)
                         mk_wait(&tfull[b], (acc >> 1) & 1, ctl);
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         if (e == 0) mk_stamp(i, 3);
-                        const uint32_t row = quarter * 32 + lane, n = t.r * 128 + row;
-                        const bool nok = n < a.N;
-                        const float bias = a.has_bias && nok ? bf16_to_f32(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off))[n])
-                                                            : 0.0f;
-                        const uint32_t tile = t.r * op.n_tt + t.j;
-                        float* myp = part + ((uint64_t)tile * op.splits + t.z) * (128 * kMkTT);
+                        // 1) TMEM -> shared tile T[token][row] (fp32, row stride kMkLdt): the accumulator is
+                        //    free for the next task's MMAs as soon as it is read
+                        float* T = reinterpret_cast<float*>(cmp);
+                        const uint32_t row = quarter * 32 + lane;
                         for (uint32_t c0 = 0; c0 < op.tt; c0 += 32) {
                             uint32_t v[32];
                             tmem_ld32(tmem + ((quarter * 32) << 16) + b * kMkTT + c0, v);
-                            if (op.splits > 1) {
 #pragma unroll
-                                for (uint32_t c = 0; c < 32; ++c)
-                                    if (c0 + c < op.tt) __stcg(myp + (c0 + c) * 128 + row, __uint_as_float(v[c]));
-                            } else if (nok) {
-                                const uint32_t tok0 = t.j * op.tt + c0;
-                                const uint32_t ntok = tok0 < a.M ? min(min(32u, op.tt - c0), a.M - tok0) : 0u;
-                                float x[32];
-#pragma unroll
-                                for (uint32_t c = 0; c < 32; ++c) x[c] = __uint_as_float(v[c]);
-                                mk_store32(a, tok0, ntok, n, x, bias);
-                            }
+                            for (uint32_t c = 0; c < 32; ++c)
+                                if (c0 + c < op.tt) T[(c0 + c) * kMkLdt + row] = __uint_as_float(v[c]);
                         }
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         mk_bar();
-                        if (e == 0) {
-                            mbar_arrive(&tempty[b]);
-                            mk_stamp(i, 4);
-                        }
+                        if (e == 0) mbar_arrive(&tempty[b]);
                         ++acc;
-                        if (op.splits > 1) {
-                            // the last split to arrive sums the partials in split order and runs the epilogue
+                        const uint32_t tile = t.r * op.n_tt + t.j;
+                        bool out_now = op.splits == 1;
+                        if (!out_now) {
+                            // 2a) split-K: publish this split's partial [token][row] (float4, coalesced); the last
+                            //     split to arrive sums all of them in split order into T and runs the epilogue
+                            float4* myp = reinterpret_cast<float4*>(part + ((uint64_t)tile * op.splits + t.z) * (128 * kMkTT));
+                            for (uint32_t u = e; u < op.tt * 32; u += 128)
+                                __stcg(myp + u, *reinterpret_cast<const float4*>(T + (u >> 5) * kMkLdt + (u & 31) * 4));
                             __threadfence();
                             mk_bar();
                             if (e == 0) *flag = atomicAdd(tile_ctr + (uint64_t)tile * kMkLine, 1u) == op.splits - 1;
                             mk_bar();
                             if (e == 0) mk_stamp(i, 6);
-                            if (*flag) {
+                            out_now = *flag != 0;
+                            if (out_now) {
                                 __threadfence();
-                                // the tile's partials [split][token][row] read as float4 (4 rows of one token) by
-                                // all 128 threads in turn, summed in split order, then bias / residual /
-                                // activation and 8- or 16-B stores of 4 consecutive output features
-                                const float* p0 = part + (uint64_t)tile * op.splits * (128 * kMkTT);
-                                const uint32_t nq = op.tt * 32;  // float4 units per split
-                                const uint16_t* bptr = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
-                                for (uint32_t u0 = 0; u0 < nq; u0 += 128 * 4) {
-                                    float4 sacc[4];
+                                const float4* p0 = reinterpret_cast<const float4*>(part + (uint64_t)tile * op.splits * (128 * kMkTT));
+                                const uint32_t nq = op.tt * 32;
+                                for (uint32_t u0 = 0; u0 < nq; u0 += 4 * 128) {
+                                    float4 x[4];
 #pragma unroll
                                     for (uint32_t k = 0; k < 4; ++k) {
                                         const uint32_t u = u0 + k * 128 + e;
-                                        sacc[k] = u < nq ? __ldcg(reinterpret_cast<const float4*>(p0) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+                                        x[k] = u < nq ? __ldcg(p0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
                                     }
                                     for (uint32_t z = 1; z < op.splits; ++z) {
-                                        const float4* pz = reinterpret_cast<const float4*>(p0 + (uint64_t)z * (128 * kMkTT));
+                                        const float4* pz = p0 + (uint64_t)z * (128 * kMkTT / 4);
                                         float4 y[4];
 #pragma unroll
                                         for (uint32_t k = 0; k < 4; ++k) {
@@ -515,68 +548,29 @@ __global__ void __maxnreg__(168)
                                         }
 #pragma unroll
                                         for (uint32_t k = 0; k < 4; ++k) {
-                                            sacc[k].x += y[k].x;
-                                            sacc[k].y += y[k].y;
-                                            sacc[k].z += y[k].z;
-                                            sacc[k].w += y[k].w;
-                                        }
-                                    }
-                                    float4 rv[4];
-#pragma unroll
-                                    for (uint32_t k = 0; k < 4; ++k) {
-                                        const uint32_t u = u0 + k * 128 + e, c = u >> 5, r4 = (u & 31) * 4;
-                                        const uint32_t tok = t.j * op.tt + c, n4 = t.r * 128 + r4;
-                                        rv[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                                        if (u < nq && a.res && tok < a.M && n4 + 3 < a.N) {
-                                            const uint64_t ri = (uint64_t)tok * a.ld_res + n4;
-                                            if (a.res_bf16) {
-                                                const uint2 h = __ldcg(reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.res) + ri));
-                                                rv[k] = make_float4(__uint_as_float(h.x << 16), __uint_as_float(h.x & 0xffff0000u),
-                                                                    __uint_as_float(h.y << 16), __uint_as_float(h.y & 0xffff0000u));
-                                            } else {
-                                                rv[k] = __ldcg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.res) + ri));
-                                            }
+                                            x[k].x += y[k].x;
+                                            x[k].y += y[k].y;
+                                            x[k].z += y[k].z;
+                                            x[k].w += y[k].w;
                                         }
                                     }
 #pragma unroll
                                     for (uint32_t k = 0; k < 4; ++k) {
-                                        const uint32_t u = u0 + k * 128 + e, c = u >> 5, r4 = (u & 31) * 4;
-                                        const uint32_t tok = t.j * op.tt + c, n4 = t.r * 128 + r4;
-                                        if (u >= nq || tok >= a.M || n4 >= a.N) continue;
-                                        const float xs[4] = {sacc[k].x, sacc[k].y, sacc[k].z, sacc[k].w};
-                                        const float rs[4] = {rv[k].x, rv[k].y, rv[k].z, rv[k].w};
-                                        if (n4 + 3 < a.N && a.ld_out % 4 == 0 && (!a.res || a.ld_res % 4 == 0)) {
-                                            float y4[4];
-#pragma unroll
-                                            for (int q = 0; q < 4; ++q)
-                                                y4[q] = apply_act(a.act, (xs[q] + (bptr ? bf16_to_f32(bptr[n4 + q]) : 0.0f)) + rs[q]);
-                                            const uint64_t oi = (uint64_t)tok * a.ld_out + n4;
-                                            const uint2 pk = make_uint2((uint32_t)f32_to_bf16(y4[0]) | ((uint32_t)f32_to_bf16(y4[1]) << 16),
-                                                                        (uint32_t)f32_to_bf16(y4[2]) | ((uint32_t)f32_to_bf16(y4[3]) << 16));
-                                            if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
-                                            else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = make_float4(y4[0], y4[1], y4[2], y4[3]);
-                                            if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
-                                        } else {  // feature tail / unaligned rows: scalar, residual loaded here
-                                            for (int q = 0; q < 4 && n4 + q < a.N; ++q) {
-                                                float x = xs[q] + (bptr ? bf16_to_f32(bptr[n4 + q]) : 0.0f);
-                                                if (a.res) {
-                                                    const uint64_t ri = (uint64_t)tok * a.ld_res + n4 + q;
-                                                    x += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
-                                                                    : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
-                                                }
-                                                x = apply_act(a.act, x);
-                                                const uint64_t oi = (uint64_t)tok * a.ld_out + n4 + q;
-                                                if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(x);
-                                                else reinterpret_cast<float*>(a.out)[oi] = x;
-                                                if (a.out2) a.out2[oi] = f32_to_bf16(x);
-                                            }
-                                        }
+                                        const uint32_t u = u0 + k * 128 + e;
+                                        if (u < nq) *reinterpret_cast<float4*>(T + (u >> 5) * kMkLdt + (u & 31) * 4) = x[k];
                                     }
                                 }
                                 if (e == 0) tile_ctr[(uint64_t)tile * kMkLine] = 0;  // self-reset for the next GEMM
+                                mk_bar();
                                 if (e == 0) mk_stamp(i, 7);
                             }
                         }
+                        if (out_now) {
+                            // 2b) row-major pass over (token, 4 features) units: bias, residual (4 units' loads in
+                            //     flight per thread), activation, 8-B (bf16) / 16-B (f32) stores
+                            mk_out_tile(dd, a, T, t.j * op.tt, t.r * 128, op.tt, e);
+                        }
+                        if (e == 0) mk_stamp(i, 4);
                         break;
                     }
                     case MK_LN:
