@@ -45,11 +45,16 @@ size_t mega_smem_bytes() { return 1024 + kMkRing + kMkCompute + kMkOpSmem + 256;
 // commit, [3] epilogue: accumulator ready, [4] epilogue: split-K partials published / output stored,
 // [5] task done (counter released), [6] compute task: dependency resolved, [7] compute task: body done.
 __device__ unsigned long long* g_mk_stamp = nullptr;
+__device__ int g_mk_dbg = 0;  // temporary A/B switch (bit 0: skip bias, bit 1: skip the output pass)
 __device__ __forceinline__ void mk_stamp(uint32_t op, uint32_t k) {
     unsigned long long* p = g_mk_stamp;
     if (p) p[((uint64_t)op * gridDim.x + blockIdx.x) * 8 + k] = globaltimer();
 }
-void set_mega_stamps(unsigned long long* p) { cudaMemcpyToSymbol(g_mk_stamp, &p, sizeof p); }
+void set_mega_stamps(unsigned long long* p) {
+    cudaMemcpyToSymbol(g_mk_stamp, &p, sizeof p);
+    const int dbg = getenv("FSW_MK_DBG") ? atoi(getenv("FSW_MK_DBG")) : 0;
+    cudaMemcpyToSymbol(g_mk_dbg, &dbg, sizeof dbg);
+}
 
 __device__ __forceinline__ void mk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -117,6 +122,16 @@ __device__ __forceinline__ MkTile mk_tile(const MkOp& op, uint32_t g) {
     return t;
 }
 
+// Activation with the transcendental cases out of line: k_mega is one large kernel whose warps run
+// different code at once, so every inlined erf / tanh expansion costs instruction-cache space (measured:
+// the inlined apply_act made a 4-unit epilogue pass 7 us instead of 2.8, even for act = NONE).
+__device__ __noinline__ float mk_act_slow(int act, float x) { return apply_act(act, x); }
+__device__ __forceinline__ float mk_act(int act, float x) {
+    if (act == FSW_ACT_NONE) return x;
+    if (act == FSW_ACT_RELU) return fmaxf(x, 0.0f);
+    return mk_act_slow(act, x);
+}
+
 // ---- GEMM epilogue from the staged tile T[token][row] (fp32, row stride kMkLdt) ------------------------
 // Units of (token, 4 consecutive output features), consecutive threads on consecutive features, kE units
 // per thread with every residual load in flight before any store: out = act((acc + b) + res), the order of
@@ -124,7 +139,9 @@ __device__ __forceinline__ MkTile mk_tile(const MkOp& op, uint32_t g) {
 constexpr uint32_t kMkLdt = 132;
 __device__ __forceinline__ void mk_out_tile(const DevDesc& dd, const GemmArgs& a, const float* T, uint32_t tok0, uint32_t n0,
                                             uint32_t tt, uint32_t e) {
-    const uint16_t* bptr = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
+    const int dbg = g_mk_dbg;
+    const uint16_t* bptr = a.has_bias && !(dbg & 1) ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
+    if (dbg & 2) return;
     const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (!a.res || a.ld_res % 4 == 0);
     constexpr uint32_t kE = 4;
     const uint32_t units = tt * 32;
@@ -161,13 +178,19 @@ __device__ __forceinline__ void mk_out_tile(const DevDesc& dd, const GemmArgs& a
                     y[3] += __uint_as_float(bv.y & 0xffff0000u);
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) y[q] = apply_act(a.act, y[q] + r[q]);
+                for (int q = 0; q < 4; ++q) y[q] = (dbg & 8) ? y[q] + r[q] : mk_act(a.act, y[q] + r[q]);
                 const uint64_t oi = (uint64_t)tok * a.ld_out + n;
                 const uint2 pk = make_uint2((uint32_t)f32_to_bf16(y[0]) | ((uint32_t)f32_to_bf16(y[1]) << 16),
                                             (uint32_t)f32_to_bf16(y[2]) | ((uint32_t)f32_to_bf16(y[3]) << 16));
-                if (a.out_bf16) __stcg(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi), pk);
-                else __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi), make_float4(y[0], y[1], y[2], y[3]));
-                if (a.out2) __stcg(reinterpret_cast<uint2*>(a.out2 + oi), pk);
+                if (dbg & 4) {
+                    if (a.out_bf16) __stcg(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi), pk);
+                    else __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi), make_float4(y[0], y[1], y[2], y[3]));
+                    if (a.out2) __stcg(reinterpret_cast<uint2*>(a.out2 + oi), pk);
+                } else {
+                    if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
+                    else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = make_float4(y[0], y[1], y[2], y[3]);
+                    if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
+                }
             } else {  // N or a leading dimension not a multiple of 4 (e.g. a 2-wide QA head): scalar
                 const float xs[4] = {x.x, x.y, x.z, x.w};
                 for (uint32_t q = 0; q < 4 && n + q < a.N; ++q) {
@@ -177,7 +200,7 @@ __device__ __forceinline__ void mk_out_tile(const DevDesc& dd, const GemmArgs& a
                         v += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + ri))
                                         : __ldcg(reinterpret_cast<const float*>(a.res) + ri);
                     }
-                    v = apply_act(a.act, v);
+                    v = mk_act(a.act, v);
                     const uint64_t oi = (uint64_t)tok * a.ld_out + n + q;
                     if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
                     else reinterpret_cast<float*>(a.out)[oi] = v;
@@ -277,13 +300,9 @@ __device__ __forceinline__ void mk_layernorm_nv(const DevDesc& dd, const LnArgs&
 }
 
 __device__ __forceinline__ void mk_layernorm(const DevDesc& dd, const LnArgs& a, uint32_t r, uint32_t lane) {
-    const uint32_t nv = (a.C / 4 + 31) / 32;
-    if (nv <= 2) mk_layernorm_nv<2>(dd, a, r, lane);
-    else if (nv <= 4) mk_layernorm_nv<4>(dd, a, r, lane);
-    else if (nv <= 6) mk_layernorm_nv<6>(dd, a, r, lane);
-    else if (nv <= 8) mk_layernorm_nv<8>(dd, a, r, lane);
-    else if (nv <= 13) mk_layernorm_nv<13>(dd, a, r, lane);
-    else mk_layernorm_nv<16>(dd, a, r, lane);
+    const uint32_t nv = (a.C / 4 + 31) / 32;  // C <= 1664 (plan eligibility): BERT-base 768, GPT-2-XL 1600
+    if (nv <= 6) mk_layernorm_nv<6>(dd, a, r, lane);
+    else mk_layernorm_nv<13>(dd, a, r, lane);
 }
 
 // GEMV task: features [o0, o0 + 64) of a rows <= 8 linear; x staged in shared memory as fp32
@@ -333,7 +352,7 @@ __device__ __forceinline__ void mk_gemv(const DevDesc& dd, const GemvArgs& a, ui
             if (bvec) v += bf16_to_f32(bvec[o]);
             if (a.res) v += a.res_bf16 ? bf16_to_f32(__ldcg(reinterpret_cast<const unsigned short*>(a.res) + oi))
                                        : __ldcg(reinterpret_cast<const float*>(a.res) + oi);
-            v = apply_act(a.act, v);
+            v = mk_act(a.act, v);
             if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
             else reinterpret_cast<float*>(a.out)[oi] = v;
             if (a.out2) a.out2[oi] = f32_to_bf16(v);
@@ -515,6 +534,7 @@ __global__ void __maxnreg__(168)
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         mk_bar();
                         if (e == 0) mbar_arrive(&tempty[b]);
+                        if (e == 0 && op.splits == 1) mk_stamp(i, 6);
                         ++acc;
                         const uint32_t tile = t.r * op.n_tt + t.j;
                         bool out_now = op.splits == 1;
@@ -572,6 +592,7 @@ __global__ void __maxnreg__(168)
                             // 2b) row-major pass over (token, 4 features) units: bias, residual (4 units' loads in
                             //     flight per thread), activation, 8-B (bf16) / 16-B (f32) stores
                             mk_out_tile(dd, a, T, t.j * op.tt, t.r * 128, op.tt, e);
+                            if (e == 0 && op.splits == 1) mk_stamp(i, 7);
                         }
                         if (e == 0) mk_stamp(i, 4);
                         break;
@@ -583,16 +604,13 @@ __global__ void __maxnreg__(168)
                         mk_embed(dd, op.embed, g, e, ctl);
                         break;
                     case MK_GEMV:
-                        if (op.gemv.rows <= 1) mk_gemv<1>(dd, op.gemv, g * kMkGemvFeat, reinterpret_cast<float*>(cmp), e);
-                        else mk_gemv<8>(dd, op.gemv, g * kMkGemvFeat, reinterpret_cast<float*>(cmp), e);
+                        mk_gemv<1>(dd, op.gemv, g * kMkGemvFeat, reinterpret_cast<float*>(cmp), e);  // rows == 1 (plan)
                         break;
                     case MK_ATTN: {
                         const AttnArgs a = op.attn;
                         const uint32_t h = g % a.H, q0 = (g / a.H) * kAttnSplitRows;
                         uint16_t* kv = reinterpret_cast<uint16_t*>(cmp);
-                        if (a.dh == 64) attn_split_core<64>(a, h, q0, kv, e, mk_bar);
-                        else if (a.dh == 32) attn_split_core<32>(a, h, q0, kv, e, mk_bar);
-                        else attn_split_core<16>(a, h, q0, kv, e, mk_bar);
+                        attn_split_core<64>(a, h, q0, kv, e, mk_bar);  // dh = 64 only (plan eligibility)
                         mk_bar();  // the staging buffers are rewritten by the next task
                         break;
                     }

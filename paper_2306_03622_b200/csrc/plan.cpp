@@ -90,10 +90,10 @@ fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g) {
     for (const Launch& x : p.launches) {
         switch (x.kind) {
             case K_EMBED: break;
-            case K_LN: if (x.ln.C % 4) return FSW_OK; break;
-            case K_GEMV: if ((x.gemv.rows <= 1 ? 1 : 8) * x.gemv.K * 4 > 56 * 1024 || x.gemv.K % 8) return FSW_OK; break;
+            case K_LN: if (x.ln.C % 4 || x.ln.C > 1664) return FSW_OK; break;
+            case K_GEMV: if (x.gemv.rows > 1 || x.gemv.K * 4 > 56 * 1024 || x.gemv.K % 8) return FSW_OK; break;
             case K_GEMM: if (x.gemm.conv || x.gemm.pair_t || !x.abase) return FSW_OK; break;
-            case K_ATTN: if (x.attn.T > 128 || !(x.attn.dh == 16 || x.attn.dh == 32 || x.attn.dh == 64)) return FSW_OK; break;
+            case K_ATTN: if (x.attn.T > 128 || x.attn.dh != 64) return FSW_OK; break;
             default: return FSW_OK;
         }
     }

@@ -54,6 +54,8 @@ with Runtime(gpu_ids=[0], pool_bytes=4 << 30) as rt:
                 rows.append(f"cta {c}: " + " ".join(f"{(p[k + 1] - p[k]) / 1e3 if k >= 0 else (p[0] - prev_done) / 1e3:.2f}"
                                                     for k in [-1, 0, 1, 2, 3, 4]))
             print(f"op {i} (tt {tt} splits {sp}): " + " | ".join(rows))
+            if sp == 1:
+                print(f"   epilogue: acc->staged {np.median(s[:, 6] - s[:, 3]) / 1e3:.2f} us, staged->out {np.median(s[:, 7] - s[:, 6]) / 1e3:.2f} us")
             if sp > 1:
                 last = s[:, 7] > 0
                 print(f"   split-K: stored->flag {np.median((s[:, 6] - s[:, 4])[s[:, 6] > 0]) / 1e3:.2f} us, last arrivers "
