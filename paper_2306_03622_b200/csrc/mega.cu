@@ -45,16 +45,11 @@ size_t mega_smem_bytes() { return 1024 + kMkRing + kMkCompute + kMkOpSmem + 256;
 // commit, [3] epilogue: accumulator ready, [4] epilogue: split-K partials published / output stored,
 // [5] task done (counter released), [6] compute task: dependency resolved, [7] compute task: body done.
 __device__ unsigned long long* g_mk_stamp = nullptr;
-__device__ int g_mk_dbg = 0;  // temporary A/B switch (bit 0: skip bias, bit 1: skip the output pass)
 __device__ __forceinline__ void mk_stamp(uint32_t op, uint32_t k) {
     unsigned long long* p = g_mk_stamp;
     if (p) p[((uint64_t)op * gridDim.x + blockIdx.x) * 8 + k] = globaltimer();
 }
-void set_mega_stamps(unsigned long long* p) {
-    cudaMemcpyToSymbol(g_mk_stamp, &p, sizeof p);
-    const int dbg = getenv("FSW_MK_DBG") ? atoi(getenv("FSW_MK_DBG")) : 0;
-    cudaMemcpyToSymbol(g_mk_dbg, &dbg, sizeof dbg);
-}
+void set_mega_stamps(unsigned long long* p) { cudaMemcpyToSymbol(g_mk_stamp, &p, sizeof p); }
 
 __device__ __forceinline__ void mk_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -139,9 +134,7 @@ __device__ __forceinline__ float mk_act(int act, float x) {
 constexpr uint32_t kMkLdt = 132;
 __device__ __forceinline__ void mk_out_tile(const DevDesc& dd, const GemmArgs& a, const float* T, uint32_t tok0, uint32_t n0,
                                             uint32_t tt, uint32_t e) {
-    const int dbg = g_mk_dbg;
-    const uint16_t* bptr = a.has_bias && !(dbg & 1) ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
-    if (dbg & 2) return;
+    const uint16_t* bptr = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
     const bool vec = (a.N % 4 == 0) && (a.ld_out % 4 == 0) && (!a.res || a.ld_res % 4 == 0);
     constexpr uint32_t kE = 4;
     const uint32_t units = tt * 32;
@@ -178,19 +171,13 @@ __device__ __forceinline__ void mk_out_tile(const DevDesc& dd, const GemmArgs& a
                     y[3] += __uint_as_float(bv.y & 0xffff0000u);
                 }
 #pragma unroll
-                for (int q = 0; q < 4; ++q) y[q] = (dbg & 8) ? y[q] + r[q] : mk_act(a.act, y[q] + r[q]);
+                for (int q = 0; q < 4; ++q) y[q] = mk_act(a.act, y[q] + r[q]);
                 const uint64_t oi = (uint64_t)tok * a.ld_out + n;
                 const uint2 pk = make_uint2((uint32_t)f32_to_bf16(y[0]) | ((uint32_t)f32_to_bf16(y[1]) << 16),
                                             (uint32_t)f32_to_bf16(y[2]) | ((uint32_t)f32_to_bf16(y[3]) << 16));
-                if (dbg & 4) {
-                    if (a.out_bf16) __stcg(reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi), pk);
-                    else __stcg(reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi), make_float4(y[0], y[1], y[2], y[3]));
-                    if (a.out2) __stcg(reinterpret_cast<uint2*>(a.out2 + oi), pk);
-                } else {
-                    if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
-                    else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = make_float4(y[0], y[1], y[2], y[3]);
-                    if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
-                }
+                if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
+                else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = make_float4(y[0], y[1], y[2], y[3]);
+                if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
             } else {  // N or a leading dimension not a multiple of 4 (e.g. a 2-wide QA head): scalar
                 const float xs[4] = {x.x, x.y, x.z, x.w};
                 for (uint32_t q = 0; q < 4 && n + q < a.N; ++q) {

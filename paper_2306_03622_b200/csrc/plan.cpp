@@ -84,8 +84,11 @@ fsw_status build_mega(fsw_ctx* c, Model& m, Plan& p, Gpu& g) {
     (void)c;
     MegaPlan& mp = p.mega;
     mp.on = false;
-    static const bool off = getenv("FSW_MEGA") && atoi(getenv("FSW_MEGA")) == 0;  // A/B: the per-op kernels
-    if (off) return FSW_OK;
+    // Opt-in (FSW_MEGA=1): parity-green, but at batch 1 its op-level dependency chain (release -> epoch ->
+    // acquire -> TMA of the activations -> MMA -> epilogue, ~4-6 us per op) is slower than the PDL chain of
+    // per-op kernels (resident BERT-base 1.05-1.09 vs 0.59 ms; DESIGN.md §5 "k_mega", profiles/r02/mega/)
+    static const bool on = getenv("FSW_MEGA") && atoi(getenv("FSW_MEGA")) == 1;
+    if (!on) return FSW_OK;
     // eligible: transformer ops only, shapes the kernel's shared memory holds
     for (const Launch& x : p.launches) {
         switch (x.kind) {

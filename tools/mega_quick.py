@@ -4,6 +4,8 @@ import os
 import sys
 import time
 
+os.environ.setdefault("FSW_MEGA", "1")
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
