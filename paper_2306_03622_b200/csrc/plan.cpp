@@ -240,7 +240,21 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                 for (int cz = 2; cz <= 8; ++cz) t[bn / 16][cz] = gemm_max_active_clusters(bn, cz);
             return t;
         }();
-        const Tiling t = choose_tiling(m_tiles, a.n_pad, a.K / 64, a_kt_bytes, m_rows, &max_cl);
+        Tiling t = choose_tiling(m_tiles, a.n_pad, a.K / 64, a_kt_bytes, m_rows, &max_cl);
+        // A/B hook (in-graph tiling sweep, tools/gemm_graph_sweep.sh): FSW_GEMM_FORCE="bn:splits:cluster" for the
+        // linears whose chosen tiling is not split-K (bn 0 = keep); a forced tiling that does not fit is ignored
+        static const char* force = getenv("FSW_GEMM_FORCE");
+        if (force && t.splits == 1 && !a.conv && m_rows == 128) {
+            int fbn = 0, fs = 1, fc = 0;
+            if (sscanf(force, "%d:%d:%d", &fbn, &fs, &fc) >= 2) {
+                const int bn = fbn ? fbn : t.bn;
+                const uint32_t kt = a.K / 64, kp = (kt + fs - 1) / fs;
+                const uint64_t ctas = m_tiles * (a.n_pad / bn) * (uint64_t)fs;
+                const bool fits = a.n_pad % bn == 0 && fs >= 1 && (kt + kp - 1) / kp == (uint32_t)fs && ctas <= 148 &&
+                                  (!fc || (fs >= 2 && fs <= 8 && ctas <= (uint64_t)max_cl[bn / 16][fs] * fs));
+                if (fits) t = Tiling{bn, (uint32_t)fs, kp, fc != 0};
+            }
+        }
         a.bn = t.bn;
         a.m_rows = m_rows;
         a.splits = t.splits;
