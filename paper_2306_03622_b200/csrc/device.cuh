@@ -50,22 +50,23 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
                  : "memory");
 }
 
-// Device timeline (kernels.h kTraceStride): g_trace is this translation unit's copy of the per-GPU trace
-// buffer (nullptr unless FSW_TRACE); one thread per CTA records, with atomicMax (min fields complemented).
+// Device timeline (kernels.h kTraceStride).  The layer kernels get the per-GPU trace buffer as a kernel
+// parameter (Wait::trace, Args::trace: the constant bank, no memory round trip on the producer thread's
+// critical path; nullptr unless FSW_TRACE); the swap kernels read g_trace, this translation unit's copy,
+// once at kernel start.  One thread per CTA records, with atomicMax (min fields complemented).
 static __device__ unsigned long long* g_trace = nullptr;
-__device__ __forceinline__ void trace_max(int32_t layer, int field, unsigned long long v) {
-    unsigned long long* t = g_trace;
+__device__ __forceinline__ void trace_max(unsigned long long* t, int32_t layer, int field, unsigned long long v) {
     if (t && layer >= 0) atomicMax(t + (uint64_t)layer * kTraceStride + field, v);
 }
-__device__ __forceinline__ void trace_entry(int32_t layer) {
-    if (threadIdx.x == 0) trace_max(layer, 0, ~globaltimer());
-}
-// Records the CTA's exit when it goes out of scope (every return path); thread 0 of the CTA.
+// Records the CTA's entry now and its exit when it goes out of scope (every return path); thread 0.
 struct TraceExit {
+    unsigned long long* t;
     int32_t layer;
-    __device__ __forceinline__ explicit TraceExit(int32_t l) : layer(l) { trace_entry(l); }
+    __device__ __forceinline__ TraceExit(unsigned long long* tr, int32_t l) : t(tr), layer(l) {
+        if (t && threadIdx.x == 0) trace_max(t, layer, 0, ~globaltimer());
+    }
     __device__ __forceinline__ ~TraceExit() {
-        if (threadIdx.x == 0) trace_max(layer, 2, globaltimer());
+        if (t && threadIdx.x == 0) trace_max(t, layer, 2, globaltimer());
     }
 };
 
@@ -95,7 +96,7 @@ __device__ __forceinline__ void wait_ready_cta(const Wait& w) {
     if (w.n == 0) return;
     if (threadIdx.x == 0) {
         wait_ready_thread(w);
-        trace_max(w.layer, 1, globaltimer());
+        trace_max(w.trace, w.layer, 1, globaltimer());
     }
     __syncthreads();
 }

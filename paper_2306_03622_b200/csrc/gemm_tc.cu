@@ -76,7 +76,7 @@ constexpr int kGemmThreads = 512;  // warp 0 TMA producer, warp 1 MMA issuer, al
 template <int BN>
 __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA (<= 64 regs) still fits beside it
     k_gemm(const __grid_constant__ CUtensorMap tmA, const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
-    TraceExit tx(w.layer);
+    TraceExit tx(w.trace, w.layer);
     using C = Cfg<BN>;
     constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
     extern __shared__ uint8_t smem_raw[];
@@ -136,7 +136,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     if (warp == 0) {
         if (lane == 0) {
             wait_ready_thread(w);
-            trace_max(w.layer, 1, globaltimer());
+            trace_max(w.trace, w.layer, 1, globaltimer());
         }
         __syncwarp();  // the weights lane 0 acquired are visible to the warp
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -439,7 +439,7 @@ struct G2Cfg {
 template <int TT>
 __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW,
                                                const DevDesc* __restrict__ d, Wait w, GemmArgs a, int stages) {
-    TraceExit tx(w.layer);
+    TraceExit tx(w.trace, w.layer);
     using C = G2Cfg<TT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead[s]) : "r"(smem_u32(&full[s])));
         if (lane == 0) {
             wait_ready_thread(w);
-            trace_max(w.layer, 1, globaltimer());
+            trace_max(w.trace, w.layer, 1, globaltimer());
         }
         __syncwarp();
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -735,6 +735,5 @@ bool make_tmap_conv(CUtensorMap* map, const void* base, uint32_t H, uint32_t W, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-void set_trace_gemm(unsigned long long* t) { cudaMemcpyToSymbol(g_trace, &t, sizeof t); }
 
 }  // namespace fsw

@@ -342,6 +342,7 @@ static Wait layer_wait(Model& m, Gpu& g, const InvokeCfg& ic, int layer) {
     Wait w{};
     w.ctl = g.ctl;
     w.layer = layer;
+    w.trace = g.trace;
     if (ic.cold && m.region_bytes[layer] > 0 && m.region_off[layer] >= ic.from) {
         if (engine_bytes_ready(ic.engine)) {
             w.n = 1;
@@ -379,12 +380,14 @@ static fsw_status enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic,
             case K_ATTN: {
                 AttnArgs a = x.attn;
                 a.layer = x.layer;
+                a.trace = g.trace;
                 launch_attention(s, a);
                 break;
             }
             case K_IM2COL: {
                 Im2colArgs a = x.im2col;
                 a.layer = x.layer;
+                a.trace = g.trace;
                 launch_im2col(s, a);
                 break;
             }
@@ -392,6 +395,7 @@ static fsw_status enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic,
             case K_AVGPOOL: {
                 PoolArgs a = x.pool;
                 a.layer = x.layer;
+                a.trace = g.trace;
                 if (x.kind == K_MAXPOOL) launch_maxpool(s, a);
                 else launch_avgpool(s, a);
                 break;

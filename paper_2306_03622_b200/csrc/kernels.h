@@ -57,6 +57,7 @@ struct Wait {
     uint32_t sys;  // 1: counters are bumped by other GPUs (striped swap) -> system-scope acquire
     DevCtl* ctl;
     int32_t layer;
+    unsigned long long* trace;  // device timeline (FSW_TRACE) or nullptr
 };
 
 constexpr uint64_t kWatchdogNs = 20ull * 1000 * 1000 * 1000;  // 20 s
@@ -204,13 +205,14 @@ void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tm
                  const CUtensorMap* tmW = nullptr);
 bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes);
 
-struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; int32_t layer; };
+struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; int32_t layer; unsigned long long* trace; };
 void launch_attention(cudaStream_t s, const AttnArgs& a);
 
 struct Im2colArgs {
     const uint16_t* in; uint32_t H, W, C;
     uint16_t* out; uint32_t P, Q, R, S, stride, pad, K, Kpad;
     int32_t layer;
+    unsigned long long* trace;
 };
 void launch_im2col(cudaStream_t s, const Im2colArgs& a);
 
@@ -218,6 +220,7 @@ struct PoolArgs {
     const uint16_t* in; uint32_t H, W, C; uint32_t P, Q, k, stride, pad;
     uint16_t* out; float* out_f32;
     int32_t layer;
+    unsigned long long* trace;
 };
 void launch_maxpool(cudaStream_t s, const PoolArgs& a);
 void launch_avgpool(cudaStream_t s, const PoolArgs& a);
@@ -228,8 +231,6 @@ void launch_avgpool(cudaStream_t s, const PoolArgs& a);
 // Min fields are stored complemented so that one memset to 0 resets every field (atomicMax for all).
 constexpr uint32_t kTraceStride = 8;
 void set_trace_swap(unsigned long long* t);  // current device; nullptr = off (swap.cu)
-void set_trace_ops(unsigned long long* t);   // ops.cu
-void set_trace_gemm(unsigned long long* t);  // gemm_tc.cu
 void set_trace_mega(unsigned long long* t);  // mega.cu
 // ---- persistent transformer kernel (mega.cu; DESIGN.md §5 "k_mega") ---------------------------------
 // One launch runs every layer of a transformer (EMBED, LAYERNORM, LINEAR, ATTENTION) on one CTA per SM.

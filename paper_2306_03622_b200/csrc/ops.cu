@@ -12,7 +12,7 @@ namespace fsw {
 // EMBED: out[t][c] = Σ_j table_j[row_j(t)][c]   (fp32 sum of bf16 rows)
 // ------------------------------------------------------------------------------------------
 __global__ void k_embed(const DevDesc* __restrict__ d, Wait w, EmbedArgs a) {
-    TraceExit tx(w.layer);
+    TraceExit tx(w.trace, w.layer);
     wait_ready_cta(w);
     pdl_wait();
     const uint32_t t = blockIdx.x;
@@ -49,7 +49,7 @@ void launch_embed(cudaStream_t s, const DevDesc* d, Wait w, const EmbedArgs& a) 
 // ------------------------------------------------------------------------------------------
 template <int NV>
 __global__ void __launch_bounds__(128) k_layernorm(const DevDesc* __restrict__ d, Wait w, LnArgs a) {
-    TraceExit tx(w.layer);
+    TraceExit tx(w.trace, w.layer);
     wait_ready_cta(w);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t r = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -124,7 +124,7 @@ constexpr int kGemvMaxRows = 8;
 
 template <int R>
 __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wait w, GemvArgs a) {
-    TraceExit tx(w.layer);
+    TraceExit tx(w.trace, w.layer);
     extern __shared__ float xs[];  // [R][K]
     pdl_wait();
     for (uint32_t i = threadIdx.x; i < R * a.K; i += blockDim.x) {
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wai
     }
     if (threadIdx.x == 0) {
         wait_ready_thread(w);
-        trace_max(w.layer, 1, globaltimer());
+        trace_max(w.trace, w.layer, 1, globaltimer());
     }
     __syncthreads();  // publishes xs and the acquired weights to the CTA
     const uint32_t lane = threadIdx.x & 31;
@@ -202,7 +202,7 @@ void launch_gemv(cudaStream_t s, const DevDesc* d, Wait w, const GemvArgs& a) {
 constexpr int kAttnRows = 16;
 
 __global__ void __launch_bounds__(256) k_attention(AttnArgs a) {
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     extern __shared__ __align__(16) uint8_t sm_attn[];
     pdl_wait();
     const uint32_t T = a.T, dh = a.dh, D = a.H * dh, W3 = 3 * D;
@@ -288,7 +288,7 @@ constexpr int kAttnMmaRows = 64;
 
 template <int DH>
 __global__ void __launch_bounds__(128) k_attention_mma(AttnArgs a) {
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     constexpr int KS = DH / 16;        // k-steps of Q·Kᵀ
     constexpr int NO = DH / 8;         // n-tiles of O
     constexpr int NS = kAttnMmaMaxT / 8;  // n-tiles of S (keys)
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(128) k_attention_mma(AttnArgs a) {
 
 template <int DH>
 __global__ void __launch_bounds__(128) k_attention_mma2(AttnArgs a) {
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     extern __shared__ __align__(16) uint16_t sm_kv2[];
     pdl_wait();
     attn_split_core<DH>(a, blockIdx.x, blockIdx.y * kAttnSplitRows, sm_kv2, threadIdx.x, []() { __syncthreads(); });
@@ -477,7 +477,7 @@ void launch_attention(cudaStream_t s, const AttnArgs& a) {
 // IM2COL (NHWC bf16 -> [P·Q][Kpad] bf16, k = (r·S + s)·C + c, zero padding / tail)
 // ------------------------------------------------------------------------------------------
 __global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per thread
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     pdl_wait();
     const uint32_t k8n = a.Kpad >> 3;
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -495,7 +495,7 @@ __global__ void k_im2col_vec8(Im2colArgs a) {  // C % 8 == 0: one 16-B chunk per
 }
 
 __global__ void k_im2col_scalar(Im2colArgs a) {
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     pdl_wait();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * a.Kpad) return;
@@ -524,7 +524,7 @@ void launch_im2col(cudaStream_t s, const Im2colArgs& a) {
 // pooling (NHWC bf16)
 // ------------------------------------------------------------------------------------------
 __global__ void k_maxpool(PoolArgs a) {
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     pdl_wait();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)a.P * a.Q * a.C) return;
@@ -545,7 +545,7 @@ void launch_maxpool(cudaStream_t s, const PoolArgs& a) {
 }
 
 __global__ void k_avgpool(PoolArgs a) {
-    TraceExit tx(a.layer);
+    TraceExit tx(a.trace, a.layer);
     pdl_wait();
     const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= a.C) return;
@@ -573,6 +573,5 @@ void init_ops_attrs() {
     cudaFuncSetAttribute(k_attention_mma2<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-void set_trace_ops(unsigned long long* t) { cudaMemcpyToSymbol(g_trace, &t, sizeof t); }
 
 }  // namespace fsw

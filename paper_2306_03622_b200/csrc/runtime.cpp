@@ -156,9 +156,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     if (c->cfg.flags & FSW_TRACE) {  // device timeline: every kernel of this device records into it
         CU(cudaMalloc(&g.trace, sizeof(unsigned long long) * kTraceStride * g.ready_cap));
         CU(cudaMemset(g.trace, 0, sizeof(unsigned long long) * kTraceStride * g.ready_cap));
-        set_trace_swap(g.trace);
-        set_trace_ops(g.trace);
-        set_trace_gemm(g.trace);
+        set_trace_swap(g.trace);  // the layer kernels get it through their parameters (graph.cpp)
         set_trace_mega(g.trace);
     }
     CU(cudaEventCreateWithFlags(&g.evfork, cudaEventDisableTiming));
