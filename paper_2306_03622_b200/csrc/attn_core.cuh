@@ -20,19 +20,23 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 constexpr int kAttnMmaMaxT = 128;
+template <bool CG>
+__device__ __forceinline__ uint32_t ldq(const uint16_t* p) {
+    return CG ? __ldcg(reinterpret_cast<const unsigned int*>(p)) : *reinterpret_cast<const uint32_t*>(p);
+}
 // Key-split variant: one CTA per (head, 16 query rows); its 4 warps take a quarter of the keys each
 // (S, softmax and P·V over 32 keys at T = 128: a quarter of the dependent MMA chain of the kernel
 // above), then combine through shared memory with the usual max / sum rescaling:
 //   m = max_w m_w,  O = Σ_w e^(m_w − m) O_w,  l = Σ_w e^(m_w − m) l_w,  out = O / l.
 constexpr int kAttnSplitRows = 16, kAttnSplitWarps = 4;
 
-template <int DH, typename Sync>
+template <int DH, bool CG = false, typename Sync>
 __device__ __forceinline__ void attn_split_core(const AttnArgs& a, uint32_t h, uint32_t q0, uint16_t* sm_kv2, uint32_t tid,
                                                 Sync sync) {
     constexpr int KS = DH / 16, NO = DH / 8, LD = DH + 8;
     constexpr int NSW = kAttnMmaMaxT / 8 / kAttnSplitWarps;  // key n-tiles per warp (4 at T <= 128)
-    // activations through L2 only (ld.global.cg): in the persistent kernel (mega.cu) another SM rewrote
-    // this slot since an earlier layer's task may have cached it in this SM's L1
+    // CG: activations through L2 only (ld.global.cg) — in the persistent kernel (mega.cu) another SM may have
+    // rewritten this slot since an earlier layer's task cached it in this SM's L1
     const uint32_t T = a.T, D = a.H * DH, W3 = 3 * D;
     const uint32_t kend = a.causal ? min(T, q0 + kAttnSplitRows) : T;
     const uint32_t kpad = (kend + 15) & ~15u;
@@ -49,8 +53,8 @@ __device__ __forceinline__ void attn_split_core(const AttnArgs& a, uint32_t h, u
         uint4 kv = make_uint4(0, 0, 0, 0), vv = kv;
         if (j < kend) {
             const uint16_t* row = a.qkv + (uint64_t)j * W3 + h * DH + c;
-            kv = __ldcg(reinterpret_cast<const uint4*>(row + D));
-            vv = __ldcg(reinterpret_cast<const uint4*>(row + 2 * D));
+            kv = CG ? __ldcg(reinterpret_cast<const uint4*>(row + D)) : *reinterpret_cast<const uint4*>(row + D);
+            vv = CG ? __ldcg(reinterpret_cast<const uint4*>(row + 2 * D)) : *reinterpret_cast<const uint4*>(row + 2 * D);
         }
         *reinterpret_cast<uint4*>(Ks + j * LD + c) = kv;
         *reinterpret_cast<uint4*>(Vs + j * LD + c) = vv;
@@ -64,10 +68,10 @@ __device__ __forceinline__ void attn_split_core(const AttnArgs& a, uint32_t h, u
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
             const uint32_t c = kk * 16 + 2 * t;
-            qa[kk][0] = ra < T ? __ldcg(reinterpret_cast<const unsigned int*>(pa + c)) : 0u;
-            qa[kk][1] = rb < T ? __ldcg(reinterpret_cast<const unsigned int*>(pb + c)) : 0u;
-            qa[kk][2] = ra < T ? __ldcg(reinterpret_cast<const unsigned int*>(pa + c + 8)) : 0u;
-            qa[kk][3] = rb < T ? __ldcg(reinterpret_cast<const unsigned int*>(pb + c + 8)) : 0u;
+            qa[kk][0] = ra < T ? ldq<CG>(pa + c) : 0u;
+            qa[kk][1] = rb < T ? ldq<CG>(pb + c) : 0u;
+            qa[kk][2] = ra < T ? ldq<CG>(pa + c + 8) : 0u;
+            qa[kk][3] = rb < T ? ldq<CG>(pb + c + 8) : 0u;
         }
     }
     sync();

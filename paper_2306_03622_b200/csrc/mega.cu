@@ -598,7 +598,7 @@ __global__ void __maxnreg__(168)
                         const AttnArgs a = op.attn;
                         const uint32_t h = g % a.H, q0 = (g / a.H) * kAttnSplitRows;
                         uint16_t* kv = reinterpret_cast<uint16_t*>(cmp);
-                        attn_split_core<64>(a, h, q0, kv, e, mk_bar);  // dh = 64 only (plan eligibility)
+                        attn_split_core<64, true>(a, h, q0, kv, e, mk_bar);  // dh = 64 only (plan eligibility)
                         mk_bar();  // the staging buffers are rewritten by the next task
                         break;
                     }
