@@ -17,6 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 SO = os.path.join(PKG, "libfsw.so")
+SO_TRACE = os.path.join(PKG, "libfsw_trace.so")
 BUILD = os.path.join(PKG, "_build")
 
 CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu", "mega.cu"]
@@ -35,29 +36,33 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """libfsw.so; trace=True builds libfsw_trace.so, the same library with the device-timeline stamps compiled
+    into the kernels (FSW_TRACE_KERNELS; load it with FSW_LIB=libfsw_trace.so, tools/timeline.py)."""
+    build_dir = BUILD + ("_trace" if trace else "")
+    so = SO_TRACE if trace else SO
+    extra = ["-DFSW_TRACE_KERNELS"] if trace else []
+    os.makedirs(build_dir, exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "fsw.h")]
     objs = []
     for src in CU_SOURCES + CXX_SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(build_dir, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + hdrs):
-            cmd = [NVCC] + ARCH + COMMON + ["-c", path, "-o", obj]
+            cmd = [NVCC] + ARCH + COMMON + extra + ["-c", path, "-o", obj]
             if src.endswith(".cu"):
                 cmd += ["-Xptxas", "-v"] if verbose else []
             else:
-                cmd = [NVCC] + COMMON + ["-x", "c++", "-c", path, "-o", obj]
+                cmd = [NVCC] + COMMON + extra + ["-x", "c++", "-c", path, "-o", obj]
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.check_call(cmd)
-    if force or _stale(SO, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", SO] + objs
+    if force or _stale(so, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-o", so] + objs
         subprocess.check_call(cmd)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(SO)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

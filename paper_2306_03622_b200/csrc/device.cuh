@@ -50,25 +50,36 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
                  : "memory");
 }
 
-// Device timeline (kernels.h kTraceStride).  The layer kernels get the per-GPU trace buffer as a kernel
-// parameter (Wait::trace, Args::trace: the constant bank, no memory round trip on the producer thread's
-// critical path; nullptr unless FSW_TRACE); the swap kernels read g_trace, this translation unit's copy,
+// Device timeline (kernels.h kTraceStride), compiled in only for the tracing build of the library
+// (FSW_TRACE_KERNELS: libfsw_trace.so, loaded by FSW_LIB for tools/timeline.py) — in the default build the
+// stamps cost nothing (measured: the per-kernel stamps and their %globaltimer reads on the producer thread
+// added ~27 us to resident BERT-base even with tracing off).  The layer kernels get the per-GPU buffer as a
+// kernel parameter (Wait::trace, Args::trace); the swap kernels read g_trace, this translation unit's copy,
 // once at kernel start.  One thread per CTA records, with atomicMax (min fields complemented).
 static __device__ unsigned long long* g_trace = nullptr;
-__device__ __forceinline__ void trace_max(unsigned long long* t, int32_t layer, int field, unsigned long long v) {
-    if (t && layer >= 0) atomicMax(t + (uint64_t)layer * kTraceStride + field, v);
-}
+#ifdef FSW_TRACE_KERNELS
+#define FSW_TRACE_MAX(t, layer, field, value)                                                          \
+    do {                                                                                              \
+        unsigned long long* t_ = (t);                                                                 \
+        if (t_ && (layer) >= 0) atomicMax(t_ + (uint64_t)(layer) * kTraceStride + (field), (value));   \
+    } while (0)
 // Records the CTA's entry now and its exit when it goes out of scope (every return path); thread 0.
 struct TraceExit {
     unsigned long long* t;
     int32_t layer;
     __device__ __forceinline__ TraceExit(unsigned long long* tr, int32_t l) : t(tr), layer(l) {
-        if (t && threadIdx.x == 0) trace_max(t, layer, 0, ~globaltimer());
+        if (threadIdx.x == 0) FSW_TRACE_MAX(t, layer, 0, ~globaltimer());
     }
     __device__ __forceinline__ ~TraceExit() {
-        if (t && threadIdx.x == 0) trace_max(t, layer, 2, globaltimer());
+        if (threadIdx.x == 0) FSW_TRACE_MAX(t, layer, 2, globaltimer());
     }
 };
+#else
+#define FSW_TRACE_MAX(t, layer, field, value) do { } while (0)
+struct TraceExit {
+    __device__ __forceinline__ TraceExit(unsigned long long*, int32_t) {}
+};
+#endif
 
 // Layer-kernel side of the ready-flag protocol: one thread spins with
 // back-off until the layer's byte counter reaches its region size, then the caller does a
@@ -96,7 +107,7 @@ __device__ __forceinline__ void wait_ready_cta(const Wait& w) {
     if (w.n == 0) return;
     if (threadIdx.x == 0) {
         wait_ready_thread(w);
-        trace_max(w.trace, w.layer, 1, globaltimer());
+        FSW_TRACE_MAX(w.trace, w.layer, 1, globaltimer());
     }
     __syncthreads();
 }

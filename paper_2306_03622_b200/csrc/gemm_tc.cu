@@ -136,7 +136,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     if (warp == 0) {
         if (lane == 0) {
             wait_ready_thread(w);
-            trace_max(w.trace, w.layer, 1, globaltimer());
+            FSW_TRACE_MAX(w.trace, w.layer, 1, globaltimer());
         }
         __syncwarp();  // the weights lane 0 acquired are visible to the warp
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(lead[s]) : "r"(smem_u32(&full[s])));
         if (lane == 0) {
             wait_ready_thread(w);
-            trace_max(w.trace, w.layer, 1, globaltimer());
+            FSW_TRACE_MAX(w.trace, w.layer, 1, globaltimer());
         }
         __syncwarp();
         asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -369,7 +369,7 @@ __global__ void __maxnreg__(168)
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DevDesc dd = *d;
     DevCtl* ctl = ops[0].w.ctl;
-    unsigned long long* const g_tr = g_trace;
+    [[maybe_unused]] unsigned long long* const g_tr = g_trace;
     uint32_t* epochs = op_cnt + (uint64_t)n_ops * kMkLine;  // [ctas] epoch words after the op counters
     const uint32_t* my_epoch = epochs + (uint64_t)blockIdx.x * kMkLine;
 
@@ -403,7 +403,7 @@ __global__ void __maxnreg__(168)
                 const MkOp op = ops[i];  // a register / local copy: never reloaded after asm memory clobbers or stores
                 if (op.kind != MK_GEMM || blockIdx.x >= op.n_tasks) continue;
                 wait_ready_thread(op.w);  // the layer's weights landed (cold); no-op when resident
-                trace_max(g_tr, op.layer, 1, globaltimer());
+                FSW_TRACE_MAX(g_tr, op.layer, 1, globaltimer());
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 const GemmArgs a = op.gemm;
                 const uint8_t* wt = weight_ptr(dd, a.w_off);
@@ -494,12 +494,12 @@ __global__ void __maxnreg__(168)
             if (e == 0) {
                 if (op.dep >= 0) mk_wait_op(my_epoch, (uint32_t)op.dep, ctl);
                 wait_ready_thread(op.w);
-                if (op.kind != MK_GEMM) trace_max(g_tr, op.layer, 1, globaltimer());
+                if (op.kind != MK_GEMM) FSW_TRACE_MAX(g_tr, op.layer, 1, globaltimer());
                 mk_stamp(i, 6);
             }
             mk_bar();
             for (uint32_t g = blockIdx.x; g < op.n_tasks; g += gridDim.x) {
-                if (e == 0) trace_max(g_tr, op.layer, 0, ~globaltimer());
+                if (e == 0) FSW_TRACE_MAX(g_tr, op.layer, 0, ~globaltimer());
                 switch (op.kind) {
                     case MK_GEMM: {
                         const GemmArgs a = op.gemm;
@@ -610,7 +610,7 @@ __global__ void __maxnreg__(168)
                     if (op.kind != MK_GEMM) mk_stamp(i, 7);
                     mk_done(op_cnt + (uint64_t)i * kMkLine, op.n_tasks, epochs, i);
                     mk_stamp(i, 5);
-                    trace_max(g_tr, op.layer, 2, globaltimer());
+                    FSW_TRACE_MAX(g_tr, op.layer, 2, globaltimer());
                 }
             }
         }

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_gemv(const DevDesc* __restrict__ d, Wai
     }
     if (threadIdx.x == 0) {
         wait_ready_thread(w);
-        trace_max(w.trace, w.layer, 1, globaltimer());
+        FSW_TRACE_MAX(w.trace, w.layer, 1, globaltimer());
     }
     __syncthreads();  // publishes xs and the acquired weights to the CTA
     const uint32_t lane = threadIdx.x & 31;

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
     if (threadIdx.x == 0) gate_arrive(gate, sys);
     const DevDesc dd = desc ? *desc : dst;
     const uint32_t lane = threadIdx.x & 31u, drop = g_drop_piece;
-    unsigned long long* const tr = g_trace;
+    [[maybe_unused]] unsigned long long* const tr = g_trace;
     for (;;) {
         uint32_t p = 0;
         if (lane == 0) p = atomicAdd(&own->ticket, 1u);
@@ -66,8 +66,8 @@ __global__ void __launch_bounds__(512) k_swap(const uint8_t* __restrict__ host, 
         if (lane == 0) {
             const unsigned long long now = globaltimer();
             atomicMax(&own->t_last, now);
-            trace_max(tr, (int32_t)pc.layer, 3, ~now);
-            trace_max(tr, (int32_t)pc.layer, 4, now);
+            FSW_TRACE_MAX(tr, (int32_t)pc.layer, 3, ~now);
+            FSW_TRACE_MAX(tr, (int32_t)pc.layer, 4, now);
         }
     }
 }
@@ -219,7 +219,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
     if (threadIdx.x == 0) gate_arrive(gate, sys);
     const DevDesc dd = desc ? *desc : dst;
     const uint32_t lane = threadIdx.x & 31u, drop = g_drop_piece;
-    unsigned long long* const tr = g_trace;
+    [[maybe_unused]] unsigned long long* const tr = g_trace;
     for (;;) {
         uint32_t p = 0;
         if (lane == 0) p = atomicAdd(&own->ticket, 1u);
@@ -344,8 +344,8 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
         if (lane == 0) {
             const unsigned long long now = globaltimer();
             atomicMax(&own->t_last, now);
-            trace_max(tr, (int32_t)pc.layer, 3, ~now);
-            trace_max(tr, (int32_t)pc.layer, 4, now);
+            FSW_TRACE_MAX(tr, (int32_t)pc.layer, 3, ~now);
+            FSW_TRACE_MAX(tr, (int32_t)pc.layer, 4, now);
         }
     }
 }
@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
     uint64_t* bar = reinterpret_cast<uint64_t*>(zring + kZRing * kZBuf);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kZRing);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, drop = g_drop_piece;
-    unsigned long long* const tr = g_trace;
+    [[maybe_unused]] unsigned long long* const tr = g_trace;
     const DevDesc dd = desc ? *desc : dst;
     if (tid == 0) {
         gate_arrive(gate, sys);
@@ -476,8 +476,8 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
             else red_release_gpu_add(&ready[pc.layer], pc.bytes);
             const unsigned long long now = globaltimer();
             atomicMax(&own->t_last, now);
-            trace_max(tr, (int32_t)pc.layer, 3, ~now);
-            trace_max(tr, (int32_t)pc.layer, 4, now);
+            FSW_TRACE_MAX(tr, (int32_t)pc.layer, 3, ~now);
+            FSW_TRACE_MAX(tr, (int32_t)pc.layer, 4, now);
             issue(b);
         }
     }

@@ -14,7 +14,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfsw.so")
+# FSW_LIB selects another build of the library in this directory (libfsw_trace.so: the device-timeline
+# stamps compiled in, tools/timeline.py); default libfsw.so
+LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ.get("FSW_LIB", "libfsw.so")))
 
 OK, EINVAL, ENOTFOUND, ENOMEM, EBUSY, ESTATE, ECUDA, ETIMEOUT, ETOPO = range(9)
 STATUS_NAMES = ["OK", "EINVAL", "ENOTFOUND", "ENOMEM", "EBUSY", "ESTATE", "ECUDA", "ETIMEOUT", "ETOPO"]

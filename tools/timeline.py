@@ -4,13 +4,14 @@ weight wait, and when its last CTA exited — the evidence that "the transmissio
 [overlaps] with the computation of previous layers".  nsys is not in this image, so
 the timeline comes from %globaltimer stamps the kernels write themselves.
 
-    FSW_TRACE=1 python tools/timeline.py [--model bert-base] [--engine 0] [--out gpurun_out/timeline_bert.txt]
+    python -m paper_2306_03622_b200.build --trace; python tools/timeline.py [--model bert-base] [--engine 0] [--out gpurun_out/timeline_bert.txt]
 """
 import argparse
 import os
 import sys
 
 os.environ.setdefault("FSW_TRACE", "1")
+os.environ.setdefault("FSW_LIB", "libfsw_trace.so")  # the build with the stamps compiled into the kernels
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 
