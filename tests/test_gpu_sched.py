@@ -61,3 +61,22 @@ def test_pool_evicts_light_before_sole_copy_heavy():
         assert rt.invoke(a, x, gpu=0).stats["swap_kind"] == 1   # the light one was evicted
         rt.set_heavy(a, -1)
         assert rt.is_heavy(a)        # measured: cold / resident latency >> 1.25 at batch 1 on B200
+
+
+def test_heavy_light_by_slo_in_the_runtime(rt, registered):
+    """a model's class follows its measured swap time against its SLO slack — light under a
+    loose deadline, heavy under a tight one (and heavy by SPEC's exec-relative rule without a deadline)."""
+    spec, w, x, mid = registered("bert-tiny")
+    rt.set_heavy(mid, -1)
+    for _ in range(3):
+        rt.evict(mid)
+        rt.invoke(mid, x, gpu=0)
+        rt.invoke(mid, x, gpu=0)
+    rt.set_heavy_policy(0.05, 0.0)
+    rt.set_slo(mid, 1000.0)        # swap (~0.05 ms) << 0.05 x ~1000 ms
+    assert not rt.is_heavy(mid)
+    rt.set_slo(mid, 0.3)           # tightest deadline kept: slack ~0.2 ms, 5 % of it < the swap
+    assert rt.is_heavy(mid)
+    rt.set_heavy(mid, 0)           # an explicit class wins
+    assert not rt.is_heavy(mid)
+    rt.set_heavy(mid, -1)
