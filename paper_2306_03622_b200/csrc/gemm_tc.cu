@@ -564,21 +564,29 @@ __global__ void __launch_bounds__(128) k_gemm2(const __grid_constant__ CUtensorM
                        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
                      : "r"(tmem + ((warp * 32u) << 16) + (uint32_t)c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (n < a.N)
+        if (n < a.N) {
+            // every residual load of the 16 tokens before any store: the output may alias the residual as far
+            // as the compiler knows, so a load after a store waits for it (one round trip per token otherwise)
+            float rv[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const uint32_t t = tok0 + c0 + c;
+                rv[c] = 0.0f;
+                if (a.res && c0 + c < C::TH && t < a.M)
+                    rv[c] = a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[(uint64_t)t * a.ld_res + n])
+                                       : reinterpret_cast<const float*>(a.res)[(uint64_t)t * a.ld_res + n];
+            }
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
                 const uint32_t t = tok0 + c0 + c;
                 if (c0 + c >= C::TH || t >= a.M) break;
-                float v = __uint_as_float(r[c]) + bias;
-                if (a.res)
-                    v += a.res_bf16 ? bf16_to_f32(reinterpret_cast<const uint16_t*>(a.res)[(uint64_t)t * a.ld_res + n])
-                                    : reinterpret_cast<const float*>(a.res)[(uint64_t)t * a.ld_res + n];
-                v = apply_act(a.act, v);
+                const float v = apply_act(a.act, (__uint_as_float(r[c]) + bias) + rv[c]);
                 const uint64_t oi = (uint64_t)t * a.ld_out + n;
                 if (a.out_bf16) reinterpret_cast<uint16_t*>(a.out)[oi] = f32_to_bf16(v);
                 else reinterpret_cast<float*>(a.out)[oi] = v;
                 if (a.out2) a.out2[oi] = f32_to_bf16(v);
             }
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
