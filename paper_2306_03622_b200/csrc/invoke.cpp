@@ -204,6 +204,7 @@ static bool profiler_attached() {
 
 extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_opts* opts, const void* input,
                                     uint64_t input_bytes, void* output, uint64_t output_cap, fsw_invoke_stats* stats) {
+    NvtxRange nv_invoke("fsw_invoke");
     const double t_entry = now_ms();
     if (!c || !input || !output) return fail(FSW_EINVAL, "invoke: NULL argument");
     if (c->gpus.empty()) return fail(FSW_ECUDA, "invoke: context has no GPU (FSW_HOST_ONLY)");
@@ -461,7 +462,10 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             }
         }
         p.last_mk_ops = nullptr;
-        st = build_graph(c, *m, p, g, ic, &exec);
+        {
+            NvtxRange nv_build("build invoke graph");
+            st = build_graph(c, *m, p, g, ic, &exec);
+        }
         if (st != FSW_OK) {
             cudaFree(p.last_mk_ops);
             p.last_mk_ops = nullptr;
@@ -549,7 +553,10 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     }
     cudaEventRecord(g.ev1, g.sx);
     const double t_launched = now_ms();
-    if (e == cudaSuccess) e = cudaEventSynchronize(g.ev1);
+    if (e == cudaSuccess) {
+        NvtxRange nv_wait(cold ? "wait (cold: swap + layers)" : "wait (resident)");
+        e = cudaEventSynchronize(g.ev1);
+    }
     if (e != cudaSuccess) return finish(fail(FSW_ECUDA, "invoke: graph launch/sync: %s", cudaGetErrorString(e)));
     const DevCtl ctl = *g.hctl;
     if (ctl.err) {

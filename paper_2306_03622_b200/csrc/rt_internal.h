@@ -23,9 +23,28 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX 3: ranges cost nothing unless a tool (nsys) is attached
+
 #include "fsw.h"
 #include "kernels.h"
 #include "policy.h"
+
+// A host range in an nsys timeline (domain "fsw"): placement, plan / graph build, staging, the graph launch
+// and the wait for the output of every invoke, so its GPU work lines up with the call that issued it.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) {
+        static nvtxDomainHandle_t dom = nvtxDomainCreateA("fsw");
+        nvtxEventAttributes_t a{};
+        a.version = NVTX_VERSION;
+        a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        a.message.ascii = name;
+        nvtxDomainRangePushEx(dom, &a);
+        d = dom;
+    }
+    ~NvtxRange() { nvtxDomainRangePop(d); }
+    nvtxDomainHandle_t d;
+};
 
 using namespace fsw;
 
