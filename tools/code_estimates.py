@@ -48,11 +48,18 @@ def estimates(words):
             bits += 8.0 - (p * np.log2(p)).sum()
     raw = blk.size * 2
     f = lambda v: float(np.where(zero, 0, v).sum() / raw)
-    return f(v3), f(v4), f(un), bits / len(sample) / 16.0
+    # one static frequency table over d (clamped to 15) for the whole store: the ideal cost of an entropy coder
+    # (e.g. interleaved rANS) that ships one table per tensor / layer instead of adapting per block
+    dc = np.minimum(d, 15)
+    c = np.bincount(dc.ravel(), minlength=16).astype(np.float64) + 0.5
+    q = c / c.sum()
+    static = float((blk.shape[0] * 512 * 8 + (-np.log2(q[dc])).sum()) / (raw * 8))
+    return f(v3), f(v4), f(un), bits / len(sample) / 16.0, static
 
 
 for name in sys.argv[1:] or ["bert-base", "resnet50"]:
     spec = synth.build_model(name)
     w = spec.build_weights()
-    v3, v4, un, floor = estimates(np.frombuffer(np.asarray(w).tobytes(), dtype=np.uint16))
-    print(f"{name:10s} v3 {v3:.4f}  v4 {v4:.4f}  unary(8 levels) {un:.4f}  entropy floor {floor:.4f}", flush=True)
+    v3, v4, un, floor, static = estimates(np.frombuffer(np.asarray(w).tobytes(), dtype=np.uint16))
+    print(f"{name:10s} v3 {v3:.4f}  v4 {v4:.4f}  unary(8 levels) {un:.4f}  one static table {static:.4f}  "
+          f"per-block entropy floor {floor:.4f}", flush=True)
