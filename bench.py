@@ -269,7 +269,7 @@ def bf16_peak_tflops():
 
 
 
-ENGINE_NAMES = {1: "sm", 2: "dma", 3: "smz", 4: "dmaz"}
+ENGINE_NAMES = {1: "sm", 2: "dma", 3: "smz", 4: "dmaz", 5: "dmazt"}
 
 
 def host_cpu_info():

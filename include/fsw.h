@@ -111,7 +111,7 @@ typedef struct {
  *        of the piece's bytes on its layer's counter per piece (fine-grained, no per-copy setup);
  *   DMA: copy-engine cudaMemcpyAsync of layer-aligned groups on `dma_streams` streams; after each
  *        group a stream memory write (no SM) bumps that stream's group counter.               */
-enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SMZ = 3, FSW_ENGINE_DMAZ = 4 };
+enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SMZ = 3, FSW_ENGINE_DMAZ = 4, FSW_ENGINE_DMAZT = 5 };
 /* Link-coded engines (models registered with FSW_REG_LINK_CODE).  The host link carries
  * the model's exponent-coded store (lossless, 0.68 of the bytes with format v4 on the synthetic weights) and a kernel decodes it into the
  * extent, releasing each decoded piece's bytes on its layer's counter (the SM protocol):
@@ -120,7 +120,13 @@ enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SM
  *   DMAZ: copy-engine DMA of layer-ordered, tapered groups of coded pieces into a device staging
  *         buffer, each followed by a stream write of the group count; persistent decode CTAs wait for
  *         their piece's group, then decode from HBM.
- * AUTO picks DMAZ / SMZ (by dmaz_min_bytes) for link-coded models, DMA / SM (by dma_min_bytes) otherwise. */
+ *   DMAZT: DMAZ for the body of the coded store and SMZ for its tail (the last FSW_DMAZT_TAIL fraction of the
+ *         coded bytes, default 0.2): the copy engine's larger PCIe reads for most of the bytes, and no
+ *         copy-group latency at the end, where a group's decode and the last layers' compute would trail it.
+ *         The tail's CTAs are resident from the start (the gate counts them) and begin reading the host
+ *         store once the last body group has landed, so the link carries one transfer at a time.
+ * AUTO picks, for link-coded models, DMAZ at >= dmaz_min_bytes, DMAZT at >= dma_min_bytes, SMZ below; DMA / SM
+ * (by dma_min_bytes) otherwise. */
 
 typedef struct fsw_ctx fsw_ctx; /* opaque; one per process */
 

@@ -8,5 +8,5 @@ from .fsw import (  # noqa: F401
     Arena, FswError, Result, Runtime, lib, NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY,
     ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM, SWAP_RESIDENT, SWAP_HOST, ENGINE_AUTO, ENGINE_SM, ENGINE_DMA,
     NO_PEER_SWAP, SWAP_PEER, SWAP_STRIPED, Scheduler, ENGINE_SMZ, ENGINE_DMAZ, REG_LINK_CODE,
-    DEBUG_POISON, FAULT_NONE, FAULT_DROP_PIECE, FAULT_DROP_GROUP,
+    DEBUG_POISON, FAULT_NONE, FAULT_DROP_PIECE, FAULT_DROP_GROUP, ENGINE_DMAZT,
 )

@@ -131,12 +131,29 @@ extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group
 // copy streams; each piece records its group as (stream << 24 | index of the group on its stream).
 // Host part of a link-coded swap plan (no device memory): the pieces >= from in execution order, and
 // for DMAZ (grp > 0) the copy groups.  Used by get_zpieces and by the host-only debug export.
-static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32_t streams, ZPieceSet& zs) {
+// DMAZT (tail_permille > 0): the last max(1 MiB, tail_permille / 1000 of the coded bytes) — whole pieces —
+// form the zero-copy tail (n_body = the first tail piece); the copy groups cover only the body.
+uint32_t dmazt_tail_permille() {
+    static const uint32_t v = getenv("FSW_DMAZT_TAIL") ? (uint32_t)(atof(getenv("FSW_DMAZT_TAIL")) * 1000.0 + 0.5) : 200u;
+    return v;
+}
+
+static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32_t streams, ZPieceSet& zs,
+                             uint32_t tail_permille = 0) {
     for (const ZPiece& pc : m.zpieces)
         if (pc.off >= from) zs.host.push_back(pc);
     if (zs.host.empty()) return fail(FSW_EINVAL, "link-coded swap with nothing to move");
     zs.cfrom = zs.host.front().coff;
     zs.cend = align_up(zs.host.back().coff + zs.host.back().cbytes, 128);  // the coded store is 128-B padded
+    zs.n_body = (uint32_t)zs.host.size();
+    uint64_t body_end = zs.cend;
+    if (grp && tail_permille) {
+        const uint64_t tail = std::max<uint64_t>(1ull << 20, (zs.cend - zs.cfrom) * tail_permille / 1000);
+        uint32_t k = (uint32_t)zs.host.size();
+        while (k > 1 && zs.cend - zs.host[k - 1].coff <= tail) --k;
+        zs.n_body = k;  // at least one body piece
+        body_end = k < zs.host.size() ? zs.host[k].coff : zs.cend;
+    }
     if (grp) {
         // the DMA engine's plan (make_dma_plan) over coded bytes: tail taper inside layers, head ramp
         // at layer boundaries
@@ -146,12 +163,12 @@ static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32
         static const double taper = getenv("FSW_DMAZ_TAPER") ? atof(getenv("FSW_DMAZ_TAPER")) : 0.5;  // sweep hook
         const uint64_t tail_min = std::min<uint64_t>(grp, 1ull << 20);
         uint64_t lo = zs.cfrom;
-        for (size_t i = 0; i < zs.host.size(); ++i) {
+        for (size_t i = 0; i < zs.n_body; ++i) {
             ZPiece& pc = zs.host[i];
             const uint32_t gi = (uint32_t)zs.groups.size();
             pc.grp = ((gi % streams) << 24) | (gi / streams);
-            const bool last = i + 1 == zs.host.size();
-            const uint64_t hi = last ? zs.cend : zs.host[i + 1].coff;
+            const bool last = i + 1 == zs.n_body;
+            const uint64_t hi = last ? body_end : zs.host[i + 1].coff;
             const uint64_t want = std::min(grp, std::max(tail_min, (uint64_t)((double)(zs.cend - lo) * taper)));
             const uint64_t want_close =
                 ramp > 0 ? std::min(want, std::max(tail_min, (uint64_t)((double)(lo - zs.cfrom) * ramp))) : want;
@@ -166,20 +183,25 @@ static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32
 }
 
 fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
-                       uint32_t streams, ZPieceSet** out) {
-    const auto key = std::make_tuple(order, seed, from, grp, streams);
+                       uint32_t streams, ZPieceSet** out, uint32_t tail_permille) {
+    const auto key = std::make_tuple(order, seed, from, grp, streams, tail_permille);
     auto it = p.zp.find(key);
     if (it != p.zp.end()) {
         *out = &it->second;
         return FSW_OK;
     }
     ZPieceSet zs;
-    fsw_status st = make_zplan(m, from, grp, streams, zs);
+    fsw_status st = make_zplan(m, from, grp, streams, zs, tail_permille);
     if (st != FSW_OK) return st;
-    if (order == FSW_ORDER_REVERSE) std::reverse(zs.host.begin(), zs.host.end());
+    // claim orders permute within the body and within the tail (each kernel claims from its own table)
+    if (order == FSW_ORDER_REVERSE) {
+        std::reverse(zs.host.begin(), zs.host.begin() + zs.n_body);
+        std::reverse(zs.host.begin() + zs.n_body, zs.host.end());
+    }
     if (order == FSW_ORDER_RANDOM) {
         std::mt19937_64 rng(seed);
-        std::shuffle(zs.host.begin(), zs.host.end(), rng);
+        std::shuffle(zs.host.begin(), zs.host.begin() + zs.n_body, rng);
+        std::shuffle(zs.host.begin() + zs.n_body, zs.host.end(), rng);
     }
     CU(cudaSetDevice(g.dev));
     CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
@@ -423,10 +445,11 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
         if (s != FSW_OK) return s;
     }
     if (ic.cold && engine_coded(ic.engine) && !ic.striped) {
-        fsw_status s = get_zpieces(m, p, g, ic.order, ic.seed, ic.from, ic.engine == FSW_ENGINE_DMAZ ? ic.zgrp : 0,
-                                   ic.engine == FSW_ENGINE_DMAZ ? ic.zstreams : 1, &zs);
+        fsw_status s = get_zpieces(m, p, g, ic.order, ic.seed, ic.from, engine_dmaz(ic.engine) ? ic.zgrp : 0,
+                                   engine_dmaz(ic.engine) ? ic.zstreams : 1, &zs,
+                                   ic.engine == FSW_ENGINE_DMAZT ? dmazt_tail_permille() : 0);
         if (s != FSW_OK) return s;
-        if (ic.engine == FSW_ENGINE_DMAZ && zs->cend - zs->cfrom > g.zstage_cap) return fail(FSW_EINVAL, "staging buffer too small");
+        if (engine_dmaz(ic.engine) && zs->cend - zs->cfrom > g.zstage_cap) return fail(FSW_EINVAL, "staging buffer too small");
     }
     if (ic.cold && (engine_bytes_ready(ic.engine) || ic.striped) && m.layers.size() > g.ready_cap)
         return fail(FSW_EINVAL, "too many layers");
@@ -447,7 +470,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
     const bool dma_cold = ic.cold && !ic.striped && ic.engine == FSW_ENGINE_DMA;
     // DMAZ: the copy engine also needs only its group counters reset; the decode kernel waits for the
     // rest of the setup (descriptor, control block, ready counters) through evset
-    const bool dmaz_cold = ic.cold && !ic.striped && ic.engine == FSW_ENGINE_DMAZ;
+    const bool dmaz_cold = ic.cold && !ic.striped && engine_dmaz(ic.engine);
     if (dma_cold || dmaz_cold) cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
     if (dmaz_cold) {
         cudaEventRecord(g.evfork, sx);
@@ -456,6 +479,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
     if (!dma_cold) cudaMemcpyAsync(g.dstage, g.hstage, kStageHdr, cudaMemcpyHostToDevice, sx);
     // striped: the counters and the control block are reset before the sources start (outside)
     if (!ic.striped && !dma_cold) cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
+    if (ic.cold && ic.engine == FSW_ENGINE_DMAZT) cudaMemsetAsync(g.ctl_tail, 0, sizeof(DevCtl), sx);
     if (ic.cold && ic.striped && !ic.no_overlap && ic.local_ctas) launch_gate(sx, g.ctl, ic.local_ctas);
     if (ic.cold && !ic.striped) {
         if (engine_bytes_ready(ic.engine)) cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m.layers.size(), sx);
@@ -474,7 +498,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             // zero-copy decode: coded pieces straight from the mapped coded store over the host link
             launch_swapz(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.zstore, 0, DevDesc{}, desc, zs->dev,
                          (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 0, nullptr);
-        } else if (ic.engine == FSW_ENGINE_DMAZ) {
+        } else if (engine_dmaz(ic.engine)) {
             // copy engine moves coded groups into the staging buffer (a fenced stream write of the group
             // count after each); the decode kernel, forked onto its own stream, waits per piece for its
             // group and decodes from HBM into the extent
@@ -492,8 +516,20 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             for (uint32_t j = 1; j < ic.zstreams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
             auto decode = [&]() {
                 launch_swapz(sdec, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
-                             (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 1, g.progress);
+                             zs->n_body, g.ready, g.ctl, g.ctl, 0, 1, g.progress);
             };
+            // DMAZT: the zero-copy tail kernel on copy stream 1, resident from the start (the gate counts its CTAs);
+            // it reads the host store only once the last body group has landed (one transfer on the link at a time)
+            const uint32_t n_tail = (uint32_t)zs->host.size() - zs->n_body;
+            auto tail = [&](cudaStream_t st) {
+                launch_swapz_after(st, (int)ic.tail_ctas, m.zstore, DevDesc{}, desc, zs->dev + zs->n_body, n_tail, g.ready, g.ctl_tail,
+                                   g.ctl, g.progress, (uint32_t)zs->groups.size());
+            };
+            if (ic.engine == FSW_ENGINE_DMAZT && !serial) {
+                cudaStreamWaitEvent(g.sd[1], g.evd[0], 0);
+                cudaStreamWaitEvent(g.sd[1], g.evset, 0);
+                tail(g.sd[1]);
+            }
             if (!serial) decode();
             uint32_t cnt[kMaxWaitSrc] = {};
             for (size_t gi = 0; gi < zs->groups.size(); ++gi) {
@@ -510,9 +546,14 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             if (serial) {
                 cudaStreamWaitEvent(sc, g.evset, 0);  // the decode reads the descriptor and ready counters
                 decode();
+                if (ic.engine == FSW_ENGINE_DMAZT) tail(sc);
             } else {
                 cudaEventRecord(g.evz, g.sz);
                 cudaStreamWaitEvent(sc, g.evz, 0);
+                if (ic.engine == FSW_ENGINE_DMAZT) {
+                    cudaEventRecord(g.evd[1], g.sd[1]);
+                    cudaStreamWaitEvent(sc, g.evd[1], 0);
+                }
             }
         } else {
             // Copy-engine DMA from the pinned store (the paper's transfer) in
@@ -549,7 +590,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
     cudaMemcpyAsync(g.dstage + kStageHdr, g.hstage + kStageHdr, m.input_bytes, cudaMemcpyHostToDevice, sx);
     if (ic.cold && !ic.striped) {
         if (ic.no_overlap) cudaStreamWaitEvent(sx, g.evjoin, 0);
-        else if (engine_bytes_ready(ic.engine)) launch_gate(sx, g.ctl, ic.ctas);
+        else if (engine_bytes_ready(ic.engine)) launch_gate(sx, g.ctl, ic.ctas + ic.tail_ctas);
     }
     const fsw_status lst = enqueue_layers(m, p, g, ic, sx);
     if (lst != FSW_OK) {

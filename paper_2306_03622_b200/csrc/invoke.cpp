@@ -345,26 +345,30 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     if (baseline) engine = FSW_ENGINE_DMA;
     const bool big = m->store_bytes >= c->cfg.dma_min_bytes;
     if (engine == FSW_ENGINE_AUTO)
-        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ)
+        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ
+                              : big                                 ? FSW_ENGINE_DMAZT
+                                                                    : FSW_ENGINE_SMZ)
                            : (big ? FSW_ENGINE_DMA : FSW_ENGINE_SM);
     if (engine_coded(engine) && !m->zstore) return finish(fail(FSW_EINVAL, "invoke: model %u is not link-coded (FSW_REG_LINK_CODE)", id));
     // striped: sources store into the target with SM kernels (decoding ones for the coded engines):
     // DMAZ sources copy their runs into their own staging buffer with their copy engine and decode from
     // there (the copy engine's larger PCIe read requests: 55 vs 51.3 GB/s per link), SMZ
     // sources read the coded store zero-copy, plain stores use k_swap
-    if (striped) engine = engine_coded(engine) ? (engine == FSW_ENGINE_DMAZ ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ) : FSW_ENGINE_SM;
+    if (striped) engine = engine_coded(engine) ? (engine_dmaz(engine) ? FSW_ENGINE_DMAZ : FSW_ENGINE_SMZ) : FSW_ENGINE_SM;
     if (peer >= 0) engine = FSW_ENGINE_DMA;  // NVLink copy-engine transfer from the peer's extent
     const uint64_t dgrp = baseline ? (2ull << 20) : o.dma_group_bytes ? o.dma_group_bytes : c->cfg.dma_group_bytes;
     const uint32_t dstr = baseline ? 1u : o.dma_streams ? o.dma_streams : c->cfg.dma_streams;
-    if (engine > FSW_ENGINE_DMAZ || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
+    if (engine > FSW_ENGINE_DMAZT || dgrp == 0 || dgrp % 256 || dstr == 0 || dstr > (uint32_t)kMaxWaitSrc)
         return finish(fail(FSW_EINVAL, "invoke: bad engine / dma_group_bytes / dma_streams"));
+    if (cold && engine == FSW_ENGINE_DMAZT && dstr != 1)
+        return finish(fail(FSW_EINVAL, "invoke: DMAZT uses one copy stream (its tail kernel runs on the second)"));
     auto extents = [&](int i) {  // the model's extents on pool GPU i
         return DevDesc{c->gpus[i].pool + (m->pextent[i] >= 0 ? m->pextent[i] : 0), c->gpus[i].pool + m->extent[i], m->split, 0};
     };
     InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
                  o.copy_ctas                     ? o.copy_ctas
-                 : engine == FSW_ENGINE_DMAZ     ? std::max(c->cfg.copy_ctas, kDmazCtas)
+                 : engine_dmaz(engine)           ? std::max(c->cfg.copy_ctas, kDmazCtas)
                  : engine == FSW_ENGINE_SMZ      ? std::max(c->cfg.copy_ctas, kSmzCtas)
                                                  : c->cfg.copy_ctas,
                  extents(gi), nullptr};
@@ -373,7 +377,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr, ic.from);
     ic.zgrp = dgrp;
     ic.zstreams = dstr;
-    if (cold && engine == FSW_ENGINE_DMAZ && !striped && g.zstage_cap < m->zbytes) {
+    ic.tail_ctas = engine == FSW_ENGINE_DMAZT && !striped ? kSmzCtas : 0;
+    if (cold && engine_dmaz(engine) && !striped && g.zstage_cap < m->zbytes) {
         // grow the staging buffer (graphs bake its address: the generation is part of their key)
         cudaFree(g.zstage);
         g.zstage = nullptr;
@@ -431,7 +436,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                  cold && !striped ? (engine == FSW_ENGINE_SM ? ic.chunk : engine == FSW_ENGINE_SMZ ? 0 : dgrp) : 0,
                  cold && sm && !striped ? ic.seed : 0, cold ? (striped ? ic.local_ctas : sm ? ic.ctas : dstr) : 0, 0};
     key.from = cold ? ic.from : 0;
-    if (cold && engine == FSW_ENGINE_DMAZ && !striped) {
+    if (cold && engine_dmaz(engine) && !striped) {
         key.extra = g.zstage_gen;  // baked staging address
         key.pext = dstr;           // copy streams
     }
@@ -486,7 +491,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         if (cold) {
             launch_poison(g.sx, g.pool + m->extent[gi], m->store_bytes - m->split, pat);
             if (m->split && !pcached) launch_poison(g.sx, g.pool + m->pextent[gi], m->split, pat);
-            if (engine == FSW_ENGINE_DMAZ && !striped && g.zstage) launch_poison(g.sx, g.zstage, g.zstage_cap, pat ^ 0x20u);
+            if (engine_dmaz(engine) && !striped && g.zstage) launch_poison(g.sx, g.zstage, g.zstage_cap, pat ^ 0x20u);
         }
     }
     if (g.trace)  // device timeline of this invoke (FSW_TRACE): every field starts at 0
@@ -599,11 +604,14 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
             } else if (coded) {
                 if (ctl.t_last > ctl.t_first) stats->swap_span_ms = (ctl.t_last - ctl.t_first) * 1e-6;
                 if (ctl.t_end > ctl.t_last) stats->compute_tail_ms = (ctl.t_end - ctl.t_last) * 1e-6;
-                stats->n_kernels += ic.no_overlap ? 1 : 2;  // decoding swap kernel (+ gate)
+                stats->n_kernels += (ic.no_overlap ? 1 : 2) + (engine == FSW_ENGINE_DMAZT ? 1 : 0);  // decode (+ gate, + tail)
                 ZPieceSet* zs = nullptr;
-                if (get_zpieces(*m, p, g, ic.order, ic.seed, ic.from, engine == FSW_ENGINE_DMAZ ? dgrp : 0,
-                                engine == FSW_ENGINE_DMAZ ? dstr : 1, &zs) == FSW_OK) {
-                    stats->n_copies = (uint32_t)(engine == FSW_ENGINE_DMAZ ? zs->groups.size() : zs->host.size());
+                if (get_zpieces(*m, p, g, ic.order, ic.seed, ic.from, engine_dmaz(engine) ? dgrp : 0,
+                                engine_dmaz(engine) ? dstr : 1, &zs,
+                                engine == FSW_ENGINE_DMAZT ? dmazt_tail_permille() : 0) == FSW_OK) {
+                    // copy groups (+ the zero-copy tail's pieces for DMAZT), or pieces
+                    stats->n_copies = (uint32_t)(engine_dmaz(engine) ? zs->groups.size() + (zs->host.size() - zs->n_body)
+                                                                     : zs->host.size());
                     stats->wire_bytes = zs->cend - zs->cfrom;
                 }
             } else if (engine == FSW_ENGINE_SM) {

@@ -138,6 +138,12 @@ struct ZPiece {
 void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
                   const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
                   DevCtl* gate, int sys, int stage, const uint32_t* progress);
+// DMAZT tail: the zero-copy (SMZ) decoder over pieces of the mapped coded store, whose CTAs start their reads
+// once *start_ctr >= start_after (the DMAZ body's last copy group published); its last releases are also
+// stamped into the gate's t_last (the invoke's swap span).
+void launch_swapz_after(cudaStream_t s, int ctas, const uint8_t* zstore, DevDesc dst, const DevDesc* desc, const ZPiece* pieces,
+                        uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, const uint32_t* start_ctr,
+                        uint32_t start_after);
 
 void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl);
 

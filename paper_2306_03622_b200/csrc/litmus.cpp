@@ -8,7 +8,7 @@
 extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uint32_t engine, uint32_t ctas, uint32_t iters,
                                        uint64_t* bad_words, uint64_t* checked_bytes) {
     if (!c || !bad_words || !checked_bytes || gpu < 0 || gpu >= (int)c->gpus.size() || engine < FSW_ENGINE_SM ||
-        engine > FSW_ENGINE_DMAZ || ctas == 0 || ctas > 1024 || iters == 0)
+        engine > FSW_ENGINE_DMAZT || ctas == 0 || ctas > 1024 || iters == 0)
         return fail(FSW_EINVAL, "litmus: bad argument");
     Model* m = nullptr;
     Gpu& g = c->gpus[gpu];
@@ -57,7 +57,8 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
     fsw_status st = FSW_OK;
     if (engine == FSW_ENGINE_SM) st = get_pieces(*m, p, g, c->cfg.chunk_bytes, FSW_ORDER_EXEC, 0, 0, &ps);
     if (engine_coded((int)engine))
-        st = get_zpieces(*m, p, g, FSW_ORDER_EXEC, 0, 0, engine == FSW_ENGINE_DMAZ ? grp : 0, 1, &zs);
+        st = get_zpieces(*m, p, g, FSW_ORDER_EXEC, 0, 0, engine_dmaz((int)engine) ? grp : 0, 1, &zs,
+                         engine == FSW_ENGINE_DMAZT ? dmazt_tail_permille() : 0);
     if (st != FSW_OK) return finish(st);
     const DmaPlan* dp = engine == FSW_ENGINE_DMA ? &get_dma_plan(*m, p, grp, 1, 0) : nullptr;
     // the consumer's table: every non-empty layer region with its wait targets
@@ -81,7 +82,7 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
         cudaMemset(dcnt, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
         return finish(fail(FSW_ECUDA, "litmus: setup copies"));
     uint64_t stage_bytes = 0;
-    if (engine == FSW_ENGINE_DMAZ) {
+    if (engine_dmaz((int)engine)) {
         stage_bytes = zs->cend - zs->cfrom;
         if (cudaMalloc(&stage, stage_bytes) != cudaSuccess) return finish(fail(FSW_ENOMEM, "litmus: staging buffer"));
     }
@@ -96,6 +97,7 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
     if (stage) launch_poison(sx, stage, stage_bytes, pat ^ 0x20u);
     cudaMemsetAsync(g.ready, 0, sizeof(uint32_t) * m->layers.size(), sx);
     cudaMemsetAsync(g.ctl, 0, sizeof(DevCtl), sx);
+    cudaMemsetAsync(g.ctl_tail, 0, sizeof(DevCtl), sx);
     cudaMemsetAsync(g.progress, 0, 128 * kMaxWaitSrc, sx);
     cudaEventRecord(g.evfork, sx);
     cudaStreamWaitEvent(sc, g.evfork, 0);
@@ -115,11 +117,18 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
                 cudaMemcpyAsync(weight_ptr(dst, gr.lo), m->store + gr.lo, gr.hi - gr.lo, cudaMemcpyHostToDevice, sc);
             wv(sc, (CUdeviceptr)g.progress, (cuuint32_t)(++cnt), 0);
         }
-    } else {  // DMAZ: copy-engine groups into the staging buffer, decode kernel on its own stream
+    } else {  // DMAZ / DMAZT: copy-engine groups into the staging buffer, decode kernel on its own stream
         cudaEventRecord(g.evd[0], sc);
         cudaStreamWaitEvent(g.sz, g.evd[0], 0);
-        launch_swapz(g.sz, (int)ctas, threads, stage, zs->cfrom, dst, nullptr, zs->dev, (uint32_t)zs->host.size(), g.ready, g.ctl,
+        launch_swapz(g.sz, (int)ctas, threads, stage, zs->cfrom, dst, nullptr, zs->dev, zs->n_body, g.ready, g.ctl,
                      g.ctl, 0, 1, g.progress);
+        if (engine == FSW_ENGINE_DMAZT) {  // + the zero-copy tail after the last body group
+            cudaStreamWaitEvent(g.sd[1], g.evd[0], 0);
+            launch_swapz_after(g.sd[1], (int)kSmzCtas, m->zstore, dst, nullptr, zs->dev + zs->n_body,
+                               (uint32_t)zs->host.size() - zs->n_body, g.ready, g.ctl_tail, g.ctl, g.progress,
+                               (uint32_t)zs->groups.size());
+            gate += kSmzCtas;
+        }
         uint32_t cnt = 0;
         for (size_t gi = 0; gi < zs->groups.size(); ++gi) {
             const auto& gr = zs->groups[gi];
@@ -129,6 +138,10 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
         }
         cudaEventRecord(g.evz, g.sz);
         cudaStreamWaitEvent(sc, g.evz, 0);
+        if (engine == FSW_ENGINE_DMAZT) {
+            cudaEventRecord(g.evd[1], g.sd[1]);
+            cudaStreamWaitEvent(sc, g.evd[1], 0);
+        }
     }
     launch_litmus_check(sx, (int)ctas, dst, golden, dlayers, (uint32_t)ly.size(), wb, per_layer, g.ctl, gate, dcnt, dcnt + 1);
     cudaEventRecord(g.evjoin, sc);

@@ -146,6 +146,7 @@ struct ZPieceSet {
     struct Group { uint64_t lo, hi; uint32_t stream; };
     std::vector<Group> groups;                          // DMAZ: coded-store byte ranges, in order
     uint64_t cfrom = 0, cend = 0;                        // coded bytes [cfrom, cend) cover the pieces
+    uint32_t n_body = 0;   // DMAZT: pieces [0, n_body) move by copy groups, [n_body, size) zero-copy (SMZ tail)
 };
 
 // The persistent transformer kernel's plan (mega.cu): the op list without the per-invoke waits, one
@@ -176,7 +177,7 @@ struct Plan {  // one model on one GPU
     // striped swap: source j of n gets every n-th piece; its table lives on the source's device
     std::map<std::tuple<uint64_t, uint64_t, uint32_t, int, uint64_t>, PieceSet> stripe;  // (chunk, sources' nodes, j, device, from)
     // link-coded engines: (order, seed, from, DMAZ group bytes or 0 for SMZ) and striped (n, j, device, from)
-    std::map<std::tuple<int, uint32_t, uint64_t, uint64_t, uint32_t>, ZPieceSet> zp;  // + DMAZ copy streams
+    std::map<std::tuple<int, uint32_t, uint64_t, uint64_t, uint32_t, uint32_t>, ZPieceSet> zp;  // + DMAZ copy streams, tail ‰
     std::map<std::tuple<uint64_t, uint32_t, int, uint64_t>, ZPieceSet> zstripe;  // (sources' nodes, j, device, from)
     // DMAZ striped: source j's runs of coded pieces (copy groups) and its pieces with coff = staging offset
     std::map<std::tuple<uint64_t, uint32_t, int, uint64_t, uint64_t>, ZPieceSet> zstripe_dma;  // + run bytes
@@ -258,6 +259,7 @@ struct Gpu {
     uint32_t* ready = nullptr;
     uint32_t ready_cap = 0;
     DevCtl* ctl = nullptr;
+    DevCtl* ctl_tail = nullptr;  // DMAZT: the tail kernel's tickets and stamps
     uint8_t* zstage = nullptr;   // DMAZ: device staging buffer for coded bytes (grown on demand)
     uint64_t zstage_cap = 0;
     uint32_t zstage_gen = 0;     // bumped on every reallocation (graphs bake the address)
@@ -343,7 +345,9 @@ inline uint64_t tiled_off(uint64_t n, uint64_t k, uint64_t n_pad) {
 }
 
 // ---- swap engines ----------------------------------------------------------------------------
-inline bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_DMAZ; }
+inline bool engine_coded(int e) { return e == FSW_ENGINE_SMZ || e == FSW_ENGINE_DMAZ || e == FSW_ENGINE_DMAZT; }
+// Engines whose body moves by copy-engine groups into the DMAZ staging buffer.
+inline bool engine_dmaz(int e) { return e == FSW_ENGINE_DMAZ || e == FSW_ENGINE_DMAZT; }
 // Engines whose layer kernels wait on per-layer byte counters (released by a swap kernel).
 inline bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_coded(e); }
 
@@ -369,6 +373,7 @@ struct InvokeCfg {
     uint32_t local_ctas = 0;     // striped: swap CTAs running on the target GPU itself (gate)
     uint64_t zgrp = 0;           // DMAZ: copy-group bytes
     uint32_t zstreams = 1;       // DMAZ: copy streams (groups dealt round-robin, one counter each)
+    uint32_t tail_ctas = 0;      // DMAZT: CTAs of the zero-copy tail kernel
 };
 
 // ---- cross-unit functions ----------------------------------------------------------------
@@ -385,7 +390,8 @@ fsw_status get_pieces(Model& m, Plan& p, Gpu& g, uint64_t chunk, int order, uint
                       PieceSet** out);                                           // graph.cpp
 const DmaPlan& get_dma_plan(Model& m, Plan& p, uint64_t grp, uint32_t streams, uint64_t from);
 fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint64_t from, uint64_t grp,
-                       uint32_t streams, ZPieceSet** out);
+                       uint32_t streams, ZPieceSet** out, uint32_t tail_permille = 0);
+uint32_t dmazt_tail_permille();                                                  // graph.cpp: FSW_DMAZT_TAIL
 fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_node, uint32_t j, int dev, uint64_t from,
                               ZPieceSet** out);
 fsw_status get_stripe_pieces(Model& m, Plan& p, uint64_t chunk, const std::vector<int>& src_node, uint32_t j, int dev,

@@ -145,6 +145,8 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaMemset(g.ready, 0, sizeof(uint32_t) * g.ready_cap));
     CU(cudaMalloc(&g.ctl, sizeof(DevCtl)));
     CU(cudaMemset(g.ctl, 0, sizeof(DevCtl)));
+    CU(cudaMalloc(&g.ctl_tail, sizeof(DevCtl)));
+    CU(cudaMemset(g.ctl_tail, 0, sizeof(DevCtl)));
     g.stage_cap = 16ull << 20;
     g.out_cap = 16ull << 20;
     CU(cudaMalloc(&g.dstage, g.stage_cap));
@@ -191,7 +193,7 @@ extern "C" fsw_status fsw_init(const fsw_config* cfg, fsw_ctx** out) {
     if (c->cfg.dmaz_min_bytes == 0) c->cfg.dmaz_min_bytes = 128ull << 20;
     if (c->cfg.dma_group_bytes == 0) c->cfg.dma_group_bytes = 64ull << 20;
     if (c->cfg.dma_streams == 0) c->cfg.dma_streams = 1;
-    if (c->cfg.engine > FSW_ENGINE_DMAZ || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
+    if (c->cfg.engine > FSW_ENGINE_DMAZT || c->cfg.dma_streams > (uint32_t)kMaxWaitSrc || c->cfg.dma_group_bytes % 256)
         return fail(FSW_EINVAL, "fsw_init: engine, dma_streams (1..4) or dma_group_bytes (multiple of 256) invalid");
     if (c->cfg.chunk_bytes % 256 || c->cfg.copy_threads % 32 || c->cfg.copy_threads > 512)
         return fail(FSW_EINVAL, "fsw_init: chunk_bytes must be a multiple of 256, copy_threads a multiple of 32 <= 512");
@@ -297,6 +299,7 @@ extern "C" void fsw_shutdown(fsw_ctx* c) {
         cudaFree(g.ready);
         cudaFree(g.trace);
         cudaFree(g.ctl);
+        cudaFree(g.ctl_tail);
         cudaFree(g.dstage);
         cudaFree(g.zstage);
         cudaStreamDestroy(g.sz);

@@ -365,7 +365,7 @@ template <bool STAGE>
 __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ src, uint64_t src_base, DevDesc dst,
                                                    const DevDesc* __restrict__ desc, const ZPiece* __restrict__ pieces,
                                                    uint32_t n_pieces, uint32_t* __restrict__ ready, DevCtl* __restrict__ own,
-                                                   DevCtl* gate, int sys, const uint32_t* progress) {
+                                                   DevCtl* gate, int sys, const uint32_t* progress, uint32_t start_after = 0) {
     extern __shared__ __align__(128) uint8_t zring[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(zring + kZRing * kZBuf);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kZRing);
@@ -402,8 +402,11 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bb) : "memory");
         }
     };
-    if (tid == 0)
+    if (tid == 0) {
+        // DMAZT tail (zero-copy, !STAGE with a start counter): the host link is the body's until its last group landed
+        if (!STAGE && progress) wait_geq(progress, start_after, own);
         for (uint32_t b = 0; b < kZRing; ++b) issue(b);
+    }
     __syncthreads();
     for (uint32_t it = 0;; ++it) {
         const uint32_t b = it % kZRing, par = (it / kZRing) & 1u;
@@ -476,6 +479,7 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
             else red_release_gpu_add(&ready[pc.layer], pc.bytes);
             const unsigned long long now = globaltimer();
             atomicMax(&own->t_last, now);
+            if (!sys && gate != own) atomicMax(&gate->t_last, now);  // DMAZT tail: the invoke's last release
             FSW_TRACE_MAX(tr, (int32_t)pc.layer, 3, ~now);
             FSW_TRACE_MAX(tr, (int32_t)pc.layer, 4, now);
             issue(b);
@@ -499,6 +503,14 @@ void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uin
         k_swapz<false, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
     else  // src_base is 0 for the mapped host store (pieces address it by coff)
         k_swapz_tma<false><<<ctas, 128, smem, s>>>(src, 0, dst, desc, pieces, n_pieces, ready, own, gate, sys, nullptr);
+}
+
+void launch_swapz_after(cudaStream_t s, int ctas, const uint8_t* zstore, DevDesc dst, const DevDesc* desc, const ZPiece* pieces,
+                        uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, const uint32_t* start_ctr,
+                        uint32_t start_after) {
+    const size_t smem = kZRing * kZBuf + 64;
+    k_swapz_tma<false><<<ctas, 128, smem, s>>>(zstore, 0, dst, desc, pieces, n_pieces, ready, own, gate, 0, start_ctr,
+                                               start_after);
 }
 
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap

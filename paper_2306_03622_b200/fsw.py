@@ -24,7 +24,7 @@ NO_OVERLAP, DMA_BASELINE, HOST_WC, HOST_ONLY, NO_PEER_SWAP, DEBUG_POISON, TRACE 
 FAULT_NONE, FAULT_DROP_PIECE, FAULT_DROP_GROUP = 0, 1, 2
 ORDER_EXEC, ORDER_REVERSE, ORDER_RANDOM = 0, 1, 2
 SWAP_RESIDENT, SWAP_HOST, SWAP_PEER, SWAP_STRIPED = 0, 1, 2, 3
-ENGINE_AUTO, ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ = 0, 1, 2, 3, 4
+ENGINE_AUTO, ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT = 0, 1, 2, 3, 4, 5
 REG_LINK_CODE = 0x2
 EVICT_KEEP_PREFIX = 0x1
 

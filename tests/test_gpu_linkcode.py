@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import synth
-from paper_2306_03622_b200 import (DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, NO_OVERLAP,
+from paper_2306_03622_b200 import (DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_DMAZT, ENGINE_SM, ENGINE_SMZ, NO_OVERLAP,
                                    ORDER_RANDOM, ORDER_REVERSE, FswError)
 from paper_2306_03622_b200 import fsw as F
 from crafted import random_block_mixture, tier_offsets
@@ -27,7 +27,7 @@ def coded(rt, registered):
     return get
 
 
-@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 @pytest.mark.parametrize("name", ["mlp", "bert-base", "resnet50", "gpt2-2L"])
 def test_coded_swap_bit_exact_and_output_identical(rt, coded, name, engine):
     spec, w, x, plain, mid = coded(name)
@@ -46,7 +46,7 @@ def test_coded_swap_bit_exact_and_output_identical(rt, coded, name, engine):
 
 
 def test_auto_engine_picks_coded_engines(rt, coded):
-    for name, want in (("mlp", ENGINE_SMZ), ("bert-base", ENGINE_DMAZ)):
+    for name, want in (("mlp", ENGINE_SMZ), ("resnet50", ENGINE_DMAZT), ("bert-base", ENGINE_DMAZ)):
         spec, w, x, plain, mid = coded(name)
         rt.evict(mid)
         assert rt.invoke(mid, x, gpu=0).stats["engine"] == want
@@ -141,7 +141,7 @@ def test_striped_dmaz_two_pool_gpus_and_dropped_run(rt):
             rt2.set_fault(FAULT_NONE)
 
 
-@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 def test_coded_with_cached_prefix(rt, coded, engine):
     """Partial caching (NEXT #4) + link coding: only the coded suffix moves."""
     spec, w, x, plain, mid = coded("bert-base")
@@ -165,7 +165,7 @@ def test_coded_with_cached_prefix(rt, coded, engine):
 def test_coded_engine_on_plain_model_is_einval(rt, registered):
     spec, w, x, mid = registered("mlp")
     rt.evict(mid)
-    for engine in (ENGINE_SMZ, ENGINE_DMAZ):
+    for engine in (ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT):
         with pytest.raises(FswError) as e:
             rt.invoke(mid, x, gpu=0, engine=engine)
         assert e.value.status == F.EINVAL
@@ -208,7 +208,7 @@ def _crafted_weights(spec, w, seed=11):
     return w
 
 
-@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 def test_coded_rare_block_kinds_bit_exact(rt, engine):
     spec = synth.build_model("mlp")
     w = _crafted_weights(spec, spec.build_weights())
@@ -231,7 +231,7 @@ def test_coded_rare_block_kinds_bit_exact(rt, engine):
         rt.unregister(mid)
 
 
-@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 @pytest.mark.parametrize("seed", [1, 2])
 def test_coded_random_block_mixture_bit_exact(rt, engine, seed):
     """Every block of the MLP drawn from a random mixture of block kinds (tests/crafted.py): the coded
@@ -247,3 +247,35 @@ def test_coded_random_block_mixture_bit_exact(rt, engine, seed):
             np.testing.assert_array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
     finally:
         rt.unregister(mid)
+
+
+@pytest.mark.parametrize("tail", ["0.05", "0.5", "0.99"])
+def test_dmazt_tail_fractions_in_child_process(tail):
+    """DMAZT with tails from one piece to nearly the whole coded store (FSW_DMAZT_TAIL is read once per
+    process): bit-exact, and the output equals the plain SM engine's, in execution and reverse order."""
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = textwrap.dedent(f"""
+        import sys, numpy as np
+        sys.path.insert(0, {root!r})
+        import synth
+        from paper_2306_03622_b200 import Runtime, ENGINE_SM, ENGINE_DMAZT, ORDER_REVERSE
+        spec = synth.build_model("resnet50")
+        w, x = spec.build_weights(), spec.make_input()
+        with Runtime(gpu_ids=[0], pool_bytes=1 << 30) as rt:
+            mid = rt.register_spec(spec, w, link_code=True)
+            base = rt.invoke(mid, x, gpu=0, engine=ENGINE_SM).output.copy()
+            for order in (0, ORDER_REVERSE):
+                rt.evict(mid)
+                r = rt.invoke(mid, x, gpu=0, engine=ENGINE_DMAZT, order=order)
+                assert r.stats["engine"] == ENGINE_DMAZT, r.stats
+                assert np.array_equal(rt.read_resident(mid, 0), rt.read_store(mid))
+                assert np.array_equal(r.output, base)
+        print("ok")
+    """)
+    env = dict(os.environ, FSW_DMAZT_TAIL=tail)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-3000:]

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import synth
-from paper_2306_03622_b200 import (ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, FAULT_DROP_GROUP, FAULT_DROP_PIECE,
+from paper_2306_03622_b200 import (ENGINE_DMA, ENGINE_DMAZ, ENGINE_DMAZT, ENGINE_SM, ENGINE_SMZ, FAULT_DROP_GROUP, FAULT_DROP_PIECE,
                                    FAULT_NONE, FswError)
 
 pytestmark = pytest.mark.gpu
@@ -33,7 +33,7 @@ def litmus_model(rt):
 
 
 @pytest.mark.parametrize("ctas", [1, 16, 148])
-@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 def test_litmus_release_acquire_proxy(rt, litmus_model, engine, ctas):
     spec, mid = litmus_model
     store = rt.model_info(mid)["store_bytes"]
@@ -42,7 +42,7 @@ def test_litmus_release_acquire_proxy(rt, litmus_model, engine, ctas):
     assert bad == 0, f"{bad} stale 16-byte words seen by consumers over {ITERS} iterations"
 
 
-@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 def test_litmus_negative_control_drop_piece(rt, litmus_model, engine):
     spec, mid = litmus_model
     rt.set_fault(FAULT_DROP_PIECE, 3)
@@ -64,7 +64,7 @@ def test_litmus_negative_control_drop_group(rt, litmus_model, engine):
     assert bad > 0
 
 
-@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ])
+@pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 def test_dropped_piece_fails_bit_exact_check(rt, litmus_model, engine):
     """The bit-exact swap check of test_gpu_swap.py must FAIL when one piece's stores are dropped:
     the differing bytes are exactly one piece, holding the poison pattern, not stale model bytes."""

@@ -17,7 +17,7 @@ CHILD = textwrap.dedent("""
     import sys, numpy as np
     sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
     import oracle, synth
-    from paper_2306_03622_b200 import Runtime, ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ
+    from paper_2306_03622_b200 import Runtime, ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT
     from test_gpu_parity import rel_err, TOL
     with Runtime(gpu_ids=[0], pool_bytes=8 << 30) as rt:
         for name in ("bert-tiny", "gpt2-tiny", "bert-base", "gpt2-2L"):
@@ -26,7 +26,7 @@ CHILD = textwrap.dedent("""
             mid = rt.register_spec(spec, w, link_code=True)
             ref = oracle.output(spec, w, x)
             outs = []
-            for eng in (ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ):
+            for eng in (ENGINE_SM, ENGINE_DMA, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT):
                 rt.evict(mid)
                 r = rt.invoke(mid, x, gpu=0, engine=eng)
                 assert np.array_equal(rt.read_resident(mid, 0), rt.read_store(mid)), (name, eng)

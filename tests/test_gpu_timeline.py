@@ -18,12 +18,12 @@ CHILD = textwrap.dedent("""
     import sys, numpy as np
     sys.path.insert(0, {root!r})
     import synth
-    from paper_2306_03622_b200 import Runtime, ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ
+    from paper_2306_03622_b200 import Runtime, ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT
     spec = synth.build_model("bert-base")
     w, x = spec.build_weights(), spec.make_input()
     with Runtime(gpu_ids=[0], pool_bytes=2 << 30) as rt:
         mid = rt.register_spec(spec, w, link_code=True)
-        for eng in (ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ):
+        for eng in (ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT):
             for _ in range(3):
                 rt.evict(mid)
                 r = rt.invoke(mid, x, gpu=0, engine=eng)
@@ -50,4 +50,4 @@ def test_timeline_wait_after_release_and_overlap():
     env = dict(os.environ, FSW_LIB="libfsw_trace.so", FSW_TRACE="1")
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
-    assert r.stdout.count(" ok ") == 3, r.stdout
+    assert r.stdout.count(" ok ") == 4, r.stdout
