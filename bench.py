@@ -402,7 +402,7 @@ def measure_weight_distributions(rt, name, reps, warm, link_gbs, peak_tf):
 
 def run_fsw(args):
     import synth
-    from paper_2306_03622_b200 import DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_SM, ENGINE_SMZ, Runtime
+    from paper_2306_03622_b200 import DMA_BASELINE, ENGINE_DMA, ENGINE_DMAZ, ENGINE_DMAZT, ENGINE_SM, ENGINE_SMZ, Runtime
 
     rank, world, local = dist_env()
     if world > 1:
@@ -458,7 +458,8 @@ def run_fsw(args):
     for name, kw in (() if args.no_variants else
                      (("sm", dict(engine=ENGINE_SM)), ("dma", dict(engine=ENGINE_DMA)),
                       ("paper_dma_2MB_1stream", dict(flags=DMA_BASELINE))) +
-                     ((("smz", dict(engine=ENGINE_SMZ)), ("dmaz", dict(engine=ENGINE_DMAZ))) if info["coded_bytes"] else ())):
+                     ((("smz", dict(engine=ENGINE_SMZ)), ("dmaz", dict(engine=ENGINE_DMAZ)), ("dmazt", dict(engine=ENGINE_DMAZT)))
+                      if info["coded_bytes"] else ())):
         for _ in range(2):
             cold_step(**kw)
         st = [cold_step(**kw) for _ in range(max(5, args.steps // 2))]
@@ -560,8 +561,9 @@ def run_fsw(args):
         dec = json.load(open(tpath)).get(args.model + "-dmaz-decode") if os.path.exists(tpath) else None
     except Exception:
         dec = None
-    if engine == "dmaz":
-        roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA of link-coded groups into HBM staging + k_swapz decode",
+    if engine in ("dmaz", "dmazt"):
+        roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA of link-coded groups into HBM staging + k_swapz decode"
+                + (" (DMAZT: the last 7 MB of coded bytes zero-copy through the SMZ decoder)" if engine == "dmazt" else ""),
                 "achieved": round(wire_gbs, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                 "frac": round(wire_gbs / PCIE_GEN5_X16_GBS, 4), "store_bytes_gbs": round(achieved, 2),
                 "peak_note": "nominal PCIe Gen5 x16 per direction (MEASURED_PEAKS.json has no host-link figure); "

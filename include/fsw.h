@@ -120,13 +120,13 @@ enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SM
  *   DMAZ: copy-engine DMA of layer-ordered, tapered groups of coded pieces into a device staging
  *         buffer, each followed by a stream write of the group count; persistent decode CTAs wait for
  *         their piece's group, then decode from HBM.
- *   DMAZT: DMAZ for the body of the coded store and SMZ for its tail (the last FSW_DMAZT_TAIL fraction of the
- *         coded bytes, default 0.2): the copy engine's larger PCIe reads for most of the bytes, and no
- *         copy-group latency at the end, where a group's decode and the last layers' compute would trail it.
+ *   DMAZT: DMAZ for the body of the coded store and SMZ for its tail (the last 7 MB of coded bytes, at most a
+ *         quarter; FSW_DMAZT_TAIL_MB overrides): the copy engine's larger PCIe reads for most of the bytes, and
+ *         no copy-group latency at the end, where a group's decode and the last layers' compute would trail it.
  *         The tail's CTAs are resident from the start (the gate counts them) and begin reading the host
  *         store once the last body group has landed, so the link carries one transfer at a time.
- * AUTO picks, for link-coded models, DMAZ at >= dmaz_min_bytes, DMAZT at >= dma_min_bytes, SMZ below; DMA / SM
- * (by dma_min_bytes) otherwise. */
+ * AUTO picks, for link-coded models, DMAZT at >= dmaz_min_bytes, SMZ below; DMA / SM (by dma_min_bytes)
+ * otherwise. */
 
 typedef struct fsw_ctx fsw_ctx; /* opaque; one per process */
 

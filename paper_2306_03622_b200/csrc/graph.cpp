@@ -131,10 +131,13 @@ extern "C" fsw_status fsw_debug_dma_plan(fsw_ctx* c, uint32_t id, uint64_t group
 // copy streams; each piece records its group as (stream << 24 | index of the group on its stream).
 // Host part of a link-coded swap plan (no device memory): the pieces >= from in execution order, and
 // for DMAZ (grp > 0) the copy groups.  Used by get_zpieces and by the host-only debug export.
-// DMAZT (tail_permille > 0): the last max(1 MiB, tail_permille / 1000 of the coded bytes) — whole pieces —
-// form the zero-copy tail (n_body = the first tail piece); the copy groups cover only the body.
-uint32_t dmazt_tail_permille() {
-    static const uint32_t v = getenv("FSW_DMAZT_TAIL") ? (uint32_t)(atof(getenv("FSW_DMAZT_TAIL")) * 1000.0 + 0.5) : 200u;
+// DMAZT (tail > 0): the last `tail` KiB of coded bytes (whole pieces, at most a quarter of them) form the
+// zero-copy tail (n_body = the first tail piece); the copy groups cover only the body.  Measured
+// (tools/resnet_engine_probe.py): BERT-base 2.832 -> 2.771 ms with a 7-MB tail (it replaces the body's last,
+// tapered copy groups, ~8 us each, and the decode lag behind the last one); GPT-2-XL is unchanged within
+// noise; a 51-MB store (ResNet-50) gains nothing over SMZ.  FSW_DMAZT_TAIL_MB overrides (MB of coded bytes).
+uint32_t dmazt_tail_permille() {  // the tail in KiB (name kept for the key tuple)
+    static const uint32_t v = getenv("FSW_DMAZT_TAIL_MB") ? (uint32_t)(atof(getenv("FSW_DMAZT_TAIL_MB")) * 1024.0 + 0.5) : 7168u;
     return v;
 }
 
@@ -148,7 +151,7 @@ static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32
     zs.n_body = (uint32_t)zs.host.size();
     uint64_t body_end = zs.cend;
     if (grp && tail_permille) {
-        const uint64_t tail = std::max<uint64_t>(1ull << 20, (zs.cend - zs.cfrom) * tail_permille / 1000);
+        const uint64_t tail = std::min<uint64_t>((uint64_t)tail_permille << 10, (zs.cend - zs.cfrom) / 4);
         uint32_t k = (uint32_t)zs.host.size();
         while (k > 1 && zs.cend - zs.host[k - 1].coff <= tail) --k;
         zs.n_body = k;  // at least one body piece

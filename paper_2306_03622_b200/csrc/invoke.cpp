@@ -345,9 +345,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     if (baseline) engine = FSW_ENGINE_DMA;
     const bool big = m->store_bytes >= c->cfg.dma_min_bytes;
     if (engine == FSW_ENGINE_AUTO)
-        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZ
-                              : big                                 ? FSW_ENGINE_DMAZT
-                                                                    : FSW_ENGINE_SMZ)
+        engine = m->zstore ? (m->store_bytes >= c->cfg.dmaz_min_bytes ? FSW_ENGINE_DMAZT : FSW_ENGINE_SMZ)
                            : (big ? FSW_ENGINE_DMA : FSW_ENGINE_SM);
     if (engine_coded(engine) && !m->zstore) return finish(fail(FSW_EINVAL, "invoke: model %u is not link-coded (FSW_REG_LINK_CODE)", id));
     // striped: sources store into the target with SM kernels (decoding ones for the coded engines):

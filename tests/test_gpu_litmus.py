@@ -83,10 +83,14 @@ def test_dropped_piece_fails_bit_exact_check(rt, litmus_model, engine):
         rt.set_fault(FAULT_NONE)
     diff = np.flatnonzero(got != ref)
     assert diff.size > 0, "dropped stores went unnoticed"
-    lo, hi = diff.min(), diff.max() + 1
-    assert hi - lo <= 16384, (lo, hi)  # one piece (SM: 16 KiB pieces; coded: <= 16 KiB)
-    words = got[lo & ~15: (hi + 15) & ~15].view(np.uint32)
-    assert len(set((words[0::4] & 0xffff0000).tolist())) == 1  # a uniform poison pattern, not model bytes
+    # one piece per swap kernel (DMAZT runs two: the body's decode and the tail's), each <= 16 KiB of poison
+    runs = np.split(diff, np.flatnonzero(np.diff(diff) > 16384) + 1)
+    assert len(runs) <= (2 if engine == ENGINE_DMAZT else 1), [(r.min(), r.max()) for r in runs]
+    for r in runs:
+        lo, hi = r.min(), r.max() + 1
+        assert hi - lo <= 16384, (lo, hi)
+        words = got[lo & ~15: (hi + 15) & ~15].view(np.uint32)
+        assert len(set((words[0::4] & 0xffff0000).tolist())) == 1  # a uniform poison pattern, not model bytes
     rt.evict(mid)
     rt.invoke(mid, x, gpu=0, engine=engine)
     assert np.array_equal(rt.read_resident(mid, 0), ref)
