@@ -43,10 +43,8 @@ CHILD = textwrap.dedent("""
 
 
 def test_timeline_wait_after_release_and_overlap():
-    so = os.path.join(ROOT, "paper_2306_03622_b200", "libfsw_trace.so")
-    if not os.path.exists(so):
-        from paper_2306_03622_b200 import build as B
-        B.build(trace=True)
+    from paper_2306_03622_b200 import build as B
+    B.build(trace=True)  # incremental: the tracing build must match the sources
     env = dict(os.environ, FSW_LIB="libfsw_trace.so", FSW_TRACE="1")
     r = subprocess.run([sys.executable, "-c", CHILD.format(root=ROOT)], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
