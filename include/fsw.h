@@ -333,10 +333,12 @@ fsw_status fsw_debug_set_fault(fsw_ctx* ctx, uint32_t kind, uint32_t index);
 fsw_status fsw_debug_litmus(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint32_t engine, uint32_t ctas, uint32_t iters,
                             uint64_t* bad_words, uint64_t* checked_bytes);
 
-/* The device timeline of the last invoke of `model_id` on `gpu` (FSW_TRACE): out[5·L + i] for every layer
+/* The device timeline of the last invoke of `model_id` on `gpu` (FSW_TRACE): out[16·L + i] for every layer
  * L of the model = %globaltimer ns of i = 0 the first kernel CTA entry, 1 the last weight-wait completion,
  * 2 the last CTA exit, 3 the first and 4 the last release of one of the layer's swap pieces (kernel
- * engines; the copy engine records nothing); 0 = no event.  t_invoke (nullable, 3 entries): the
+ * engines; the copy engine records nothing), and for GEMM layers 5 the last return from the wait on the
+ * predecessor kernel (griddepcontrol.wait), 6 the last MMA completion, 7 the last epilogue start, 8-15
+ * kernel-specific epilogue phases; 0 = no event.  t_invoke (nullable, 3 entries): the
  * invoke's first piece claimed, last piece released, graph end.  ESTATE without FSW_TRACE; EINVAL if
  * cap_layers < the model's layers.                                                                   */
 fsw_status fsw_debug_trace_read(fsw_ctx* ctx, uint32_t model_id, int32_t gpu, uint64_t* out, uint32_t cap_layers,

@@ -142,6 +142,23 @@ __device__ __forceinline__ float apply_act(int act, float x) {
     }
 }
 
+// Epilogue activation with the transcendental cases out of line: a GEMM epilogue applies it to every output
+// element, and inlined erf / tanh expansions in an unrolled store loop made the epilogue code tens of KB —
+// instruction-cache misses on every launch (measured in k_mega and k_gemm_ws: 4-7 us store phases).
+static __device__ __noinline__ float4 act4_slow(int act, float4 v) {
+    return make_float4(apply_act(act, v.x), apply_act(act, v.y), apply_act(act, v.z), apply_act(act, v.w));
+}
+__device__ __forceinline__ float4 act4(int act, float4 v) {
+    if (act == FSW_ACT_NONE) return v;
+    if (act == FSW_ACT_RELU) return make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+    return act4_slow(act, v);
+}
+
+// L2 prefetch of [p, p + bytes) (bulk, no completion; bytes multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -175,6 +175,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
         const uint32_t pre = min((uint32_t)stages, nst);
         for (uint32_t st = 0; st < pre; ++st) load_w(st);
         pdl_wait();
+        if (lane == 0) FSW_TRACE_MAX(w.trace, w.layer, 5, globaltimer());
         asm volatile("fence.proxy.async.global;" ::: "memory");
         for (uint32_t st = 0; st < pre; ++st) load_a(st);
         for (uint32_t st = pre; st < nst; ++st) {
@@ -219,6 +220,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
     //    so the stage buffers are free to reuse).
     mbar_wait(done, 0);
     pdl_trigger();  // the successor's prologue and weight prefetch overlap this epilogue
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 6, globaltimer());
     STAMP(3);
     // this thread's 4 bias columns (weights: acquired by the producer before the MMAs completed), loaded
     // now so the round trip overlaps the TMEM drain
@@ -248,6 +250,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
     STAMP(4);
     pdl_wait();  // activations (residual in, output / partials out) only after the predecessor
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 7, globaltimer());
     uint32_t rows = min(a.m_rows, a.M - m0);
     const uint32_t cols = min((uint32_t)BN, a.N - n0);
     uint32_t rb = 0;  // first tile row this CTA's epilogue covers
@@ -379,10 +382,7 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
                 v.y = (v.y + bsum.y) + __uint_as_float(raw[j].y);
                 v.z = (v.z + bsum.z) + __uint_as_float(raw[j].z);
                 v.w = (v.w + bsum.w) + __uint_as_float(raw[j].w);
-                v.x = apply_act(a.act, v.x);
-                v.y = apply_act(a.act, v.y);
-                v.z = apply_act(a.act, v.z);
-                v.w = apply_act(a.act, v.w);
+                v = act4(a.act, v);
                 const uint64_t oi = (uint64_t)(m0 + r) * a.ld_out + n0 + c;
                 const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
                                             (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
@@ -662,6 +662,10 @@ int gemm_max_active_clusters(int bn, int cz) {
 }
 
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a, const CUtensorMap* tmW) {
+    if (a.ws_tt) {
+        launch_gemm_ws(s, d, w, tmA, a);
+        return;
+    }
     if (a.pair_t) {
         switch (a.pair_t) {
             case 16: launch_g2<16>(s, d, w, tmA, tmW, a); break;

@@ -1,0 +1,310 @@
+// gemm_ws.cu — K3c: the weight-stationary swap-AB tcgen05 GEMM for batch-1 transformer linears.
+//
+//   out[t][n] = act( Σ_k X[t][k]·W[n][k] + b[n] + res[t][n] )          fp32 accumulate in TMEM
+//
+// Why another GEMM ("k_gemm_ws"): at batch 1 a linear is a chain of latencies, and in the
+// invoke graph its successor can only start its arithmetic once its predecessor's activations are out
+// (griddepcontrol.wait).  k_gemm puts 128 TOKENS on the UMMA M operand, so every CTA streams the whole
+// 128 x K activation (196 KB at K = 768) AFTER that wait, through a ring whose stages it reuses.  Here the
+// roles are swapped and nothing the CTA needs after the wait is large:
+//   * the UMMA M operand is 128 WEIGHT rows (the store's pre-tiled K-major SWIZZLE_128B layout makes one
+//     128-row x 64-k sub-tile one contiguous 16-KiB bulk copy), the N operand is a tile of TT tokens;
+//   * a CTA owns ONE K range (split-K over a (1, 1, S) cluster) and ALL of its weight sub-tiles live in
+//     shared memory at once — no ring, no stage reuse, one mbarrier per k sub-tile.  They are loaded
+//     right after the layer's readiness wait (PAPER.md:588-590 pipelining), i.e. before the predecessor
+//     finishes when the CTA is resident early (programmatic dependent launch);
+//   * after the wait only the TT x K_range activation slice moves (TMA, one box per k sub-tile), and each
+//     sub-tile's 4 MMAs issue as soon as it lands;
+//   * the S partial tiles of a cluster are reduced over distributed shared memory: CTA z sums weight-row
+//     quads [z·32/S, (z+1)·32/S) of all S tiles in split order (deterministic) and runs the fused
+//     bias / residual / activation epilogue on them with 8-16-B coalesced accesses.
+// The grid is one wave: (ceil(N/128), ceil(M/TT), S) CTAs of 512 threads (16 warps share the epilogue: with one
+// warp per scheduler its dependent ALU chains — the GELU — were latency-bound, 4-5 us per epilogue).
+#include "device.cuh"
+#include "umma.cuh"
+
+namespace fsw {
+
+static __device__ int g_ws_debug = 0;  // FSW_WS_DEBUG (timing experiments only): 1 local-only reduction, 2 no stores
+namespace {
+constexpr int kWsMaxKt = 16;          // k sub-tiles one CTA holds (kt_per)
+constexpr uint32_t kWsW = 128 * 128;  // one 128-row x 64-k weight sub-tile: 16 KiB
+template <int TT>
+struct WsCfg {
+    static constexpr uint32_t kX = TT * 128;               // one TT-token x 64-k activation sub-tile
+    static constexpr uint32_t kStage = TT * 128 * 4;       // fp32 staging tile [TT][128 rows]
+    static constexpr uint32_t kTmemCols = TT < 32 ? 32 : TT;
+    __host__ __device__ static uint32_t wbytes(uint32_t kt) {  // weight region (also holds the staging tile)
+        const uint32_t w = kt * kWsW;
+        return w < kStage ? kStage : w;
+    }
+    __host__ __device__ static uint32_t smem(uint32_t kt) { return wbytes(kt) + kt * kX + 1024 + 1024; }
+};
+}  // namespace
+
+constexpr int kWsThreads = 512;  // thread 0 loads, thread 32 issues the MMAs; all 16 warps drain TMEM and run the epilogue
+
+template <int TT>
+__global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant__ CUtensorMap tmX, const DevDesc* __restrict__ d, Wait w,
+                                                 GemmArgs a) {
+    TraceExit tx(w.trace, w.layer);
+    using C = WsCfg<TT>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t kt0 = blockIdx.z * a.kt_per;
+    const uint32_t nkt = min(a.K / kBK, kt0 + a.kt_per) - kt0;  // >= 1 (host plan)
+    uint8_t* sw = smem;                                          // weight sub-tiles, then the staging tile
+    uint8_t* sx = smem + C::wbytes(a.kt_per);                    // activation sub-tiles
+    // 1-KiB control block: full[kWsMaxKt] | done | TMEM slot | (at +256) the tile's 128 bias values
+    uint8_t* ctl = sx + a.kt_per * C::kX;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
+    uint64_t* done = full + kWsMaxKt;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+    float* bias_s = reinterpret_cast<float*>(ctl + 256);
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t n0 = blockIdx.x * 128, t0 = blockIdx.y * TT;
+    const DevDesc dd = *d;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t j = 0; j < nkt; ++j) mbar_init(&full[j], 1);
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(C::kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+
+    if (threadIdx.x == 0) {
+        // producer: the layer's weights (ordered by the ready counters), then — after the predecessor — the
+        // activation slice.  Rows past the weight's padded height are not copied (their accumulators are
+        // never stored).
+        wait_ready_thread(w);
+        FSW_TRACE_MAX(w.trace, w.layer, 1, globaltimer());
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const uint32_t wrows = min(128u, a.n_pad - n0);
+        const uint8_t* wt = weight_ptr(dd, a.w_off) + (uint64_t)(n0 / 8) * 1024;
+        const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
+        for (uint32_t j = 0; j < nkt; ++j) {
+            mbar_expect_tx(&full[j], wrows * 128 + C::kX);
+            bulk_load(sw + j * kWsW, wt + (kt0 + j) * ktile_stride, wrows * 128, &full[j]);
+        }
+        if (a.pf_bytes && w.n == 0) {  // resident: this CTA's share of the next GEMM's weights into L2
+            const uint32_t ncta = gridDim.x * gridDim.y * gridDim.z;
+            const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            const uint64_t share = ((a.pf_bytes + ncta - 1) / ncta + 255) & ~255ull;
+            const uint64_t b0 = cta * share, b1 = a.pf_bytes < b0 + share ? a.pf_bytes : b0 + share;
+            const uint8_t* pf = weight_ptr(dd, a.pf_off);
+            for (uint64_t o = b0; o < b1; o += 65536) prefetch_l2(pf + o, (uint32_t)(b1 - o < 65536 ? b1 - o : 65536));
+        }
+        pdl_wait();
+        FSW_TRACE_MAX(w.trace, w.layer, 5, globaltimer());
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (uint32_t j = 0; j < nkt; ++j) tma_load_2d(sx + j * C::kX, &tmX, (int)((kt0 + j) * kBK), (int)t0, &full[j]);
+    } else if (threadIdx.x == 32) {
+        constexpr uint32_t idesc = umma_idesc_bf16(kBM, TT);
+        for (uint32_t j = 0; j < nkt; ++j) {
+            mbar_wait(&full[j], 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad = umma_desc_sw128(sw + j * kWsW), bd = umma_desc_sw128(sx + j * C::kX);
+#pragma unroll
+            for (uint32_t kk = 0; kk < kBK / 16; ++kk) umma_f16(tmem, ad + kk * 2, bd + kk * 2, idesc, (j | kk) != 0);
+        }
+        umma_commit(done);
+    }
+    __syncwarp();
+
+    mbar_wait(done, 0);
+    pdl_trigger();  // the successor's prologue and weight loads overlap this epilogue
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 6, globaltimer());
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 3) {  // bias of the tile's 128 rows into shared memory (weights are ready: `done` follows the acquire)
+        const uint16_t* bias = a.has_bias ? reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.b_off)) : nullptr;
+        for (uint32_t r = lane * 4; r < 128; r += 128) {
+            float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (bias && n0 + r < a.N) {
+                const uint2 v = *reinterpret_cast<const uint2*>(bias + n0 + r);
+                b = make_float4(__uint_as_float(v.x << 16), __uint_as_float(v.x & 0xffff0000u), __uint_as_float(v.y << 16),
+                                __uint_as_float(v.y & 0xffff0000u));
+            }
+            *reinterpret_cast<float4*>(bias_s + r) = b;
+        }
+    }
+    // TMEM (lane = weight row, column = token) -> staging tile [TT][128] fp32 in the (now idle) weight region.
+    // Warp w reads TMEM lane quarter w mod 4 and every (w / 4)-th 32-column block.
+    float* st = reinterpret_cast<float*>(sw);
+    {
+        const uint32_t q4 = warp & 3u, r = q4 * 32 + lane;
+        if constexpr (TT >= 32) {
+#pragma unroll 1
+            for (int c0 = 32 * (int)(warp >> 2); c0 < TT; c0 += 32 * (kWsThreads / 128)) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((q4 * 32u) << 16) + (uint32_t)c0, v);
+#pragma unroll
+                for (int c = 0; c < 32; ++c) st[(c0 + c) * 128 + r] = __uint_as_float(v[c]);
+            }
+        } else if (warp < 4) {
+            uint32_t v[16];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+                           "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                         : "r"(tmem + ((q4 * 32u) << 16)));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 16; ++c) st[c * 128 + r] = __uint_as_float(v[c]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 11, globaltimer());
+    const uint32_t S = gridDim.z;
+    if (S > 1) cluster_sync();  // every split's staging tile is complete (release / acquire over the cluster)
+    else __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols) : "memory");
+    pdl_wait();  // residual in / output out: only after the predecessor
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 7, globaltimer());
+
+    // reduction (split order) + epilogue over this CTA's weight-row quads x the tile's tokens
+    const uint32_t per = (32 + S - 1) / S, q0 = min(32u, blockIdx.z * per), nq = min(32u, q0 + per) - q0;
+    const uint32_t units = nq * TT;
+    const float* __restrict__ resf = a.res && !a.res_bf16 ? reinterpret_cast<const float*>(a.res) : nullptr;
+    const uint16_t* __restrict__ resh = a.res && a.res_bf16 ? reinterpret_cast<const uint16_t*>(a.res) : nullptr;
+    constexpr int kE = 2;
+    for (uint32_t u0 = threadIdx.x; u0 < units; u0 += kWsThreads * kE) {
+        float4 acc[kE];
+        uint4 rr[kE];
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+            const uint32_t u = u0 + e * kWsThreads;
+            acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+            rr[e] = make_uint4(0, 0, 0, 0);
+            if (u >= units) continue;
+            const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
+            const float* src = st + tok * 128 + 4 * q;
+            if (S > 1 && !(g_ws_debug & 1)) {
+                float4 v[8];
+#pragma unroll
+                for (uint32_t z = 0; z < 8; ++z)
+                    if (z < S) v[z] = ld_dsmem_f4(src, z);
+                acc[e] = v[0];
+#pragma unroll
+                for (uint32_t z = 1; z < 8; ++z) {
+                    if (z >= S) break;
+                    acc[e].x += v[z].x;
+                    acc[e].y += v[z].y;
+                    acc[e].z += v[z].z;
+                    acc[e].w += v[z].w;
+                }
+            } else {
+                acc[e] = *reinterpret_cast<const float4*>(src);
+            }
+            if (t < a.M && n < a.N) {
+                const uint64_t ri = (uint64_t)t * a.ld_res + n;
+                if (resf) rr[e] = *reinterpret_cast<const uint4*>(resf + ri);
+                else if (resh) {
+                    const uint2 h = *reinterpret_cast<const uint2*>(resh + ri);
+                    rr[e] = make_uint4(h.x << 16, h.x & 0xffff0000u, h.y << 16, h.y & 0xffff0000u);
+                }
+            }
+        }
+        if (threadIdx.x == 0 && u0 == 0) FSW_TRACE_MAX(w.trace, w.layer, 8, globaltimer());
+#pragma unroll
+        for (int e = 0; e < kE; ++e) {
+            const uint32_t u = u0 + e * kWsThreads;
+            if (u >= units) continue;
+            const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
+            if (t >= a.M || n >= a.N) continue;
+            const float4 b = *reinterpret_cast<const float4*>(bias_s + 4 * q);
+            float4 v = acc[e];
+            // (acc + bias) + residual, the order of the unfused definition (as k_gemm)
+            v.x = (v.x + b.x) + __uint_as_float(rr[e].x);
+            v.y = (v.y + b.y) + __uint_as_float(rr[e].y);
+            v.z = (v.z + b.z) + __uint_as_float(rr[e].z);
+            v.w = (v.w + b.w) + __uint_as_float(rr[e].w);
+            v = act4(a.act, v);
+            const uint64_t oi = (uint64_t)t * a.ld_out + n;
+            const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
+                                        (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
+            if (g_ws_debug & 2) continue;
+            if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
+            else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = v;
+            if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
+        }
+    }
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 9, globaltimer());
+    if (S > 1) cluster_sync();  // no CTA leaves while a peer may still read its staging tile
+    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 10, globaltimer());
+}
+
+template <int TT>
+static void launch_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a) {
+    using C = WsCfg<TT>;
+    const dim3 grid((a.n_pad + 127) / 128, (a.M + TT - 1) / TT, a.splits);
+    launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT>, grid, dim3(kWsThreads), C::smem(a.kt_per), s, dim3(1, 1, a.splits), *tmX, d, w, a);
+}
+
+void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a) {
+    switch (a.ws_tt) {
+        case 16: launch_ws<16>(s, d, w, tmX, a); break;
+        case 32: launch_ws<32>(s, d, w, tmX, a); break;
+        case 64: launch_ws<64>(s, d, w, tmX, a); break;
+        default: launch_ws<128>(s, d, w, tmX, a); break;
+    }
+}
+
+uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per) {
+    switch (tt) {
+        case 16: return WsCfg<16>::smem(kt_per);
+        case 32: return WsCfg<32>::smem(kt_per);
+        case 64: return WsCfg<64>::smem(kt_per);
+        default: return WsCfg<128>::smem(kt_per);
+    }
+}
+
+template <int TT>
+static int ws_max_clusters(uint32_t kt_per, int cz) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1, 1, cz);
+    cfg.blockDim = dim3(kWsThreads);
+    cfg.dynamicSmemBytes = WsCfg<TT>::smem(kt_per);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 1;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = cz;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_ws<TT>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz) {
+    switch (tt) {
+        case 16: return ws_max_clusters<16>(kt_per, cz);
+        case 32: return ws_max_clusters<32>(kt_per, cz);
+        case 64: return ws_max_clusters<64>(kt_per, cz);
+        default: return ws_max_clusters<128>(kt_per, cz);
+    }
+}
+
+void init_gemm_ws_attrs() {
+    {
+        static const int dbg = getenv("FSW_WS_DEBUG") ? atoi(getenv("FSW_WS_DEBUG")) : 0;
+        cudaMemcpyToSymbol(g_ws_debug, &dbg, sizeof dbg);
+    }
+    cudaFuncSetAttribute(k_gemm_ws<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm_ws<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+}  // namespace fsw

@@ -206,10 +206,21 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // GPU's pool base, the map's origin)
     uint32_t pair_t;
     const void* wpool;
+    // weight-stationary swap-AB GEMM (k_gemm_ws, gemm_ws.cu): ws_tt = tokens per tile (16, 32, 64 or 128),
+    // 0 = not used.  128 weight rows x ws_tt tokens per CTA; split-K over a (1, 1, splits) cluster (splits <= 8,
+    // kt_per k sub-tiles each, all resident in shared memory); the A tensor map's box is ws_tt rows
+    uint32_t ws_tt;
+    // L2 prefetch (k_gemm_ws, resident invokes): the next GEMM's weights [pf_off, pf_off + pf_bytes) of the
+    // store, dealt over this launch's CTAs; pf_bytes = 0: none
+    uint64_t pf_off, pf_bytes;
 };
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a,
                  const CUtensorMap* tmW = nullptr);
 bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes);
+void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a);
+uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per);                  // dynamic shared memory of one CTA
+int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz);  // clusters resident at once (this device)
+void init_gemm_ws_attrs();
 
 struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; int32_t layer; unsigned long long* trace; };
 void launch_attention(cudaStream_t s, const AttnArgs& a);
@@ -235,7 +246,7 @@ void launch_avgpool(cudaStream_t s, const PoolArgs& a);
 // kTraceStride u64 at trace + L·kTraceStride: [0] ~(first kernel CTA entry), [1] last weight-wait done,
 // [2] last kernel CTA exit, [3] ~(first piece of L released by a swap kernel), [4] last piece released.
 // Min fields are stored complemented so that one memset to 0 resets every field (atomicMax for all).
-constexpr uint32_t kTraceStride = 8;
+constexpr uint32_t kTraceStride = 16;
 void set_trace_swap(unsigned long long* t);  // current device; nullptr = off (swap.cu)
 void set_trace_mega(unsigned long long* t);  // mega.cu
 // ---- persistent transformer kernel (mega.cu; DESIGN.md §5 "k_mega") ---------------------------------

@@ -48,6 +48,62 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
     return best;
 }
 
+// Tiling of the weight-stationary swap-AB GEMM (k_gemm_ws, gemm_ws.cu): tt tokens per tile and `splits` K
+// ranges over a cluster, one wave.  Measured in the invoke graph (profiles/r02/gemm/ws_sweep.txt, resident
+// BERT-base): it beats k_gemm on the narrow linears (N <= 12 weight-row tiles: O-projection, FFN2), where k_gemm
+// has few CTAs each streaming the whole activation, and loses on the wide ones (QKV, FFN1), where its DSMEM
+// split-K reduction and larger epilogue cost more than the activation bytes it saves.  Cost (relative, fitted to
+// that sweep): the epilogue's token width, the split-K reduction, the MMA chain, and a penalty for CTAs too large
+// to be resident beside their predecessor.  ok = false: no tiling fits (k_gemm runs the linear).
+struct WsTiling { uint32_t tt, splits, kt_per; bool ok; };
+static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool any_width) {
+    WsTiling best{0, 0, 0, false};
+    double best_t = 1e30;
+    const uint64_t rt = (n_pad + 127) / 128;
+    // A/B hook: FSW_GEMM_WS_FORCE="tt:splits" for every shape, or "N:K:tt:splits,..." per weight shape (a shape
+    // not in the list runs k_gemm)
+    static const char* force = getenv("FSW_GEMM_WS_FORCE");
+    int ftt = 0, fs = 0;
+    if (force) {
+        int fn, fk, t, sp, used = 0;
+        const char* q = force;
+        if (sscanf(q, "%d:%d:%d:%d", &fn, &fk, &t, &sp) == 4) {
+            ftt = -1;
+            while (q && sscanf(q, "%d:%d:%d:%d%n", &fn, &fk, &t, &sp, &used) == 4) {
+                if ((uint32_t)fn == n_pad && (uint32_t)fk == kt * 64) ftt = t, fs = sp;
+                q = strchr(q, ',');
+                if (q) ++q;
+            }
+        } else {
+            sscanf(force, "%d:%d", &ftt, &fs);
+        }
+    }
+    if (ftt < 0 || M > 128 || (!any_width && !ftt && rt > 12)) return best;
+    for (uint32_t tt : {16u, 32u, 64u, 128u}) {
+        if (ftt && tt != (uint32_t)ftt) continue;
+        for (uint32_t s = 1; s <= 8 && s <= kt; ++s) {
+            if (fs && s != (uint32_t)fs) continue;
+            const uint32_t kp = (kt + s - 1) / s;
+            if ((kt + kp - 1) / kp != s || kp > 16) continue;
+            const uint64_t ctas = rt * ((M + tt - 1) / tt) * s;
+            const uint32_t smem = gemm_ws_smem(tt, kp);
+            if (smem > 200 * 1024) continue;
+            static std::map<uint64_t, int> cap_cache;
+            const uint64_t key = ((uint64_t)tt << 40) | ((uint64_t)kp << 20) | s;
+            auto it = cap_cache.find(key);
+            if (it == cap_cache.end())
+                it = cap_cache.emplace(key, s > 1 ? gemm_ws_max_active_clusters(tt, kp, (int)s) * (int)s : 148).first;
+            if (ctas > (uint64_t)std::min(it->second, 148)) continue;
+            const double t = 0.6 * (tt / 16.0) + 0.4 * (s - 1) + 0.1 * kp + (smem > 150 * 1024 ? 2.0 : 0.0);
+            if (t < best_t - 1e-9) {
+                best_t = t;
+                best = {tt, s, kp, true};
+            }
+        }
+    }
+    return best;
+}
+
 // ==========================================================================================
 // persistent transformer kernel (mega.cu): eligibility, tiling, op table
 // ==========================================================================================
@@ -380,7 +436,22 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                             if (dist < best) best = dist, pt = t;
                         }
                     }
-                    if (pt) {
+                    // Weight-stationary swap-AB GEMM (k_gemm_ws) for the narrow batch-1 linears (choose_ws_tiling);
+                    // FSW_GEMM_WS=0 turns it off, =2 allows it for every width (A/B hooks)
+                    static const int ws_mode = getenv("FSW_GEMM_WS") ? atoi(getenv("FSW_GEMM_WS")) : 1;
+                    WsTiling wt{0, 0, 0, false};
+                    if (ws_mode && !pt && a.N % 4 == 0) wt = choose_ws_tiling(a.M, a.n_pad, a.K / 64, ws_mode == 2);
+                    if (wt.ok) {
+                        a.ws_tt = wt.tt;
+                        a.bn = 128;
+                        a.m_rows = wt.tt;
+                        a.splits = wt.splits;
+                        a.kt_per = wt.kt_per;
+                        a.mc = 1;
+                        a.cz = wt.splits > 1 ? wt.splits : 0;
+                        if (!make_tmap_act(&x.tmap, abase, a.M, slot_cols(si), slot_cols(si), wt.tt))
+                            return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (layer %u)", li);
+                    } else if (pt) {
                         a.pair_t = pt;
                         a.wpool = g.pool;
                         a.bn = 128;
@@ -483,6 +554,27 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
             }
         }
         p->launches.push_back(x);
+    }
+    {  // L2 prefetch of the next GEMM's weights (FSW_GEMM_PF=1, A/B) and the chosen tilings (FSW_PLAN_VERBOSE=1)
+        static const bool pf = getenv("FSW_GEMM_PF") && atoi(getenv("FSW_GEMM_PF")) == 1;
+        static const bool verbose = getenv("FSW_PLAN_VERBOSE") && atoi(getenv("FSW_PLAN_VERBOSE")) == 1;
+        for (size_t i = 0; i < p->launches.size(); ++i) {
+            Launch& x = p->launches[i];
+            if (x.kind != K_GEMM) continue;
+            GemmArgs& a = x.gemm;
+            if (pf && a.ws_tt)
+                for (size_t j = i + 1; j < p->launches.size(); ++j)
+                    if (p->launches[j].kind == K_GEMM) {
+                        const GemmArgs& b = p->launches[j].gemm;
+                        a.pf_off = b.w_off;
+                        a.pf_bytes = (uint64_t)b.K * b.n_pad * 2;
+                        break;
+                    }
+            if (verbose)
+                fprintf(stderr, "[fsw plan] layer %d GEMM M=%u N=%u K=%u: %s tt/bn=%u splits=%u kt_per=%u cz=%u smem=%u pf=%llu\n",
+                        x.layer, a.M, a.N, a.K, a.ws_tt ? "ws" : a.pair_t ? "2cta" : "k_gemm", a.ws_tt ? a.ws_tt : (uint32_t)a.bn,
+                        a.splits, a.kt_per, a.cz, a.ws_tt ? gemm_ws_smem(a.ws_tt, a.kt_per) : 0u, (unsigned long long)a.pf_bytes);
+        }
     }
     // split-K partials live after the activations and the im2col scratch
     const uint64_t part_off = align_up(off, 1024);

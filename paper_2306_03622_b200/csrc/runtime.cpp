@@ -106,6 +106,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaSetDevice(g.dev));
     CU(cudaFree(nullptr));  // create the context now (one shared runtime per GPU)
     init_gemm_attrs();
+    init_gemm_ws_attrs();
     init_mega_attrs();
     init_ops_attrs();
     init_swap_attrs();
@@ -390,13 +391,11 @@ extern "C" fsw_status fsw_debug_trace_read(fsw_ctx* c, uint32_t id, int32_t gpu,
     CU(cudaSetDevice(g.dev));
     std::vector<unsigned long long> raw(nl * kTraceStride);
     CU(cudaMemcpy(raw.data(), g.trace, sizeof(unsigned long long) * raw.size(), cudaMemcpyDeviceToHost));
-    for (size_t l = 0; l < nl; ++l) {  // [entry, wait done, exit, first release, last release]; 0 = none
+    for (size_t l = 0; l < nl; ++l) {  // [entry, wait done, exit, first release, last release, GEMM phases]; 0 = none
         const unsigned long long* r = &raw[l * kTraceStride];
-        out[5 * l + 0] = r[0] ? ~r[0] : 0;
-        out[5 * l + 1] = r[1];
-        out[5 * l + 2] = r[2];
-        out[5 * l + 3] = r[3] ? ~r[3] : 0;
-        out[5 * l + 4] = r[4];
+        for (uint32_t i = 0; i < 16; ++i) out[16 * l + i] = r[i];
+        out[16 * l + 0] = r[0] ? ~r[0] : 0;
+        out[16 * l + 3] = r[3] ? ~r[3] : 0;
     }
     if (t_invoke) {  // the last invoke's control block: first piece claimed, last released, graph end
         DevCtl ctl{};

@@ -474,10 +474,11 @@ class Runtime:
         return bad.value, chk.value
 
     def trace(self, mid: int, gpu: int = 0):
-        """Device timeline of the last invoke (FSW_TRACE): ([n_layers][5] ns: entry, wait done, exit, first /
-        last piece released; 0 = none), [first piece claimed, last released, graph end] ns)."""
+        """Device timeline of the last invoke (FSW_TRACE): ([n_layers][16] ns: entry, wait done, exit, first /
+        last piece released, GEMM predecessor wait / MMA done / epilogue start / epilogue phases; 0 = none), [first piece claimed,
+        last released, graph end] ns)."""
         n = self.model_info(mid)["n_layers"]
-        out = np.zeros((n, 5), np.uint64)
+        out = np.zeros((n, 16), np.uint64)
         ti = np.zeros(3, np.uint64)
         _check(lib().fsw_debug_trace_read(self.h, mid, gpu, out.ctypes.data, n, ti.ctypes.data))
         return out, ti

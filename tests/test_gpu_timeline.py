@@ -30,7 +30,7 @@ CHILD = textwrap.dedent("""
             tr, ti = rt.trace(mid)
             has_w = [i for i, l in enumerate(spec.layers) if l.refs]
             for i in has_w:
-                entry, wait, exit_, first, last = (int(v) for v in tr[i])
+                entry, wait, exit_, first, last = (int(v) for v in tr[i, :5])
                 assert entry and exit_ and entry <= exit_, (eng, i, tr[i])
                 assert first and last and first <= last, (eng, i, tr[i])
                 assert wait >= last, ("weight wait passed before the last piece was released", eng, i, wait - last)

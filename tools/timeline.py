@@ -49,6 +49,8 @@ def main():
     ap.add_argument("--engine", type=int, default=0, help="0 auto (coded: DMAZ / SMZ), 1 SM, 2 DMA, 3 SMZ, 4 DMAZ")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--phases", action="store_true", help="resident GEMM phases (fields 5-7: last pdl_wait return, "
+                    "last MMA completion, last epilogue start)")
     args = ap.parse_args()
     spec = synth.build_model(args.model)
     w, x = spec.build_weights(), spec.make_input()
@@ -68,6 +70,17 @@ def main():
         out.append(f"\n{args.model}: resident invoke device {r.stats['device_ms']:.3f} ms")
         tr, ti = rt.trace(mid)
         table(spec, rt, mid, tr, ti, f"resident invoke ({args.model})", out)
+        if args.phases:
+            t0 = min(int(v) for v in tr[:, 0] if v)
+            us = lambda v: (int(v) - t0) / 1e3 if v else float("nan")
+            out.append(f"{'layer':>5} {'name':<22} {'entry':>8} {'wait.w':>8} {'pdl.wait':>8} {'mma.done':>8} {'staged':>8} {'epi':>8} "
+                       f"{'loaded':>8} {'stored':>8} {'synced':>8} {'exit':>8}")
+            for li, l in enumerate(spec.layers):
+                if int(l.op) != 3 or not tr[li, 5]:
+                    continue
+                e = tr[li]
+                out.append(f"{li:>5} {l.name[:22]:<22} {us(e[0]):>8.1f} {us(e[1]):>8.1f} {us(e[5]):>8.1f} "
+                           f"{us(e[6]):>8.1f} {us(e[11]):>8.1f} {us(e[7]):>8.1f} {us(e[8]):>8.1f} {us(e[9]):>8.1f} {us(e[10]):>8.1f} {us(e[2]):>8.1f}")
         # critical-path share per op kind in the resident run: exit(L) - exit(previous layer with a kernel)
         ex = [(li, int(tr[li, 2])) for li in range(len(spec.layers)) if tr[li, 2]]
         start = min(int(v) for v in tr[:, 0] if v)
