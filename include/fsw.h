@@ -377,6 +377,22 @@ fsw_status fsw_debug_read_store(fsw_ctx* ctx, uint32_t model_id, void* dst, uint
  * t_i < 3, else s_j < o ? s_j : s_j + 3.
  * ENOTFOUND / ESTATE (model not link-coded) / EINVAL (cap too small; *n is still set).              */
 typedef struct { uint64_t off, coff; uint32_t bytes, cbytes, layer, pad; uint32_t hdr[16]; } fsw_coded_piece;
+/* Entropy-coded pieces (format v5, b = 0x20): a piece either keeps the per-block codes above
+ * or has every coded block of kind 0x20 (raw and zero blocks may remain).  Header of a 0x20 block: h = bits
+ * 0-7, n_esc = bits 16-25.  Each word's offset s_i = min(h − e_i, 15) is coded with the model's canonical
+ * Huffman code (lengths_out below: length L_s of symbol s, 0 = unused, all <= 12; codes assigned in order of
+ * (L_s, s), MSB first); s = 15 marks an exception.  Stream A: 512 bytes m_i per 0x20 block (as above).
+ * Stream B: the E = Σ n_esc exception words (16 bits each, whole words, in order of (block, l, i)), zero-
+ * padded to a multiple of 16 bytes; then 4·K 16-bit code words, word j being word j / 4 of sub-stream
+ * j mod 4 (K = the longest sub-stream; shorter ones zero-padded), zero-padded to a multiple of 16 bytes.
+ * Sub-stream q carries the 0x20 blocks whose index in the piece is ≡ q (mod 4), in increasing order; 32
+ * lanes l each keep a bit buffer (empty at the piece's start).  For each of its blocks and i = 0..15: every
+ * lane whose buffer does not hold its next whole code (the code its bits start, read with zeros after them,
+ * is longer than the bits held) appends the sub-stream's next word (MSB first; the lanes that need one take
+ * consecutive words in increasing l), then every lane removes one code from the front of its buffer: s of
+ * word 16·l + i.  w = (m & 0x80) << 8 | ((h − s) & 0xff) << 7 | (m & 0x7f) for s < 15, else the next
+ * exception word.  lengths_out: 16 bytes, all 0 when the model has no entropy-coded piece.            */
+fsw_status fsw_debug_coded_code(fsw_ctx* ctx, uint32_t model_id, uint8_t* lengths_out);
 fsw_status fsw_debug_read_coded(fsw_ctx* ctx, uint32_t model_id, void* dst, uint64_t cap);
 fsw_status fsw_debug_coded_pieces(fsw_ctx* ctx, uint32_t model_id, fsw_coded_piece* out, uint32_t cap, uint32_t* n);
 /* Activation slot of the last invoke of `model_id` on `gpu` (valid until the next invoke). */

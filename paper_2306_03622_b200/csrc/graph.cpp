@@ -141,6 +141,15 @@ uint32_t dmazt_tail_permille() {  // the tail in KiB (name kept for the key tupl
     return v;
 }
 
+// The model's entropy-code decode table on the current device, beside a piece set (nullptr: no entropy-coded piece).
+static cudaError_t upload_htab(const Model& m, ZPieceSet& zs) {
+    zs.htab = nullptr;
+    if (m.htab.empty()) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&zs.htab, m.htab.size());
+    if (e == cudaSuccess) e = cudaMemcpy(zs.htab, m.htab.data(), m.htab.size(), cudaMemcpyHostToDevice);
+    return e;
+}
+
 static fsw_status make_zplan(const Model& m, uint64_t from, uint64_t grp, uint32_t streams, ZPieceSet& zs,
                              uint32_t tail_permille = 0) {
     for (const ZPiece& pc : m.zpieces)
@@ -208,6 +217,7 @@ fsw_status get_zpieces(Model& m, Plan& p, Gpu& g, int order, uint32_t seed, uint
     }
     CU(cudaSetDevice(g.dev));
     CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
+    CU(upload_htab(m, zs));
     CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
     *out = &p.zp.emplace(key, std::move(zs)).first->second;
     return FSW_OK;
@@ -269,6 +279,7 @@ fsw_status get_zstripe_pieces(Model& m, Plan& p, const std::vector<int>& src_nod
     CU(cudaSetDevice(dev));
     if (!zs.host.empty()) {
         CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
+        CU(upload_htab(m, zs));
         CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
     }
     *out = &p.zstripe.emplace(key, std::move(zs)).first->second;
@@ -324,6 +335,7 @@ fsw_status get_zstripe_dma(Model& m, Plan& p, const std::vector<int>& src_node, 
     CU(cudaSetDevice(dev));
     if (!zs.host.empty()) {
         CU(cudaMalloc(&zs.dev, sizeof(ZPiece) * zs.host.size()));
+        CU(upload_htab(m, zs));
         CU(cudaMemcpy(zs.dev, zs.host.data(), sizeof(ZPiece) * zs.host.size(), cudaMemcpyHostToDevice));
     }
     *out = &p.zstripe_dma.emplace(key, std::move(zs)).first->second;
@@ -500,7 +512,7 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
         } else if (ic.engine == FSW_ENGINE_SMZ) {
             // zero-copy decode: coded pieces straight from the mapped coded store over the host link
             launch_swapz(sc, (int)ic.ctas, (int)c->cfg.copy_threads, m.zstore, 0, DevDesc{}, desc, zs->dev,
-                         (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 0, nullptr);
+                         (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl, 0, 0, nullptr, zs->htab);
         } else if (engine_dmaz(ic.engine)) {
             // copy engine moves coded groups into the staging buffer (a fenced stream write of the group
             // count after each); the decode kernel, forked onto its own stream, waits per piece for its
@@ -519,14 +531,14 @@ fsw_status build_graph(fsw_ctx* c, Model& m, Plan& p, Gpu& g, const InvokeCfg& i
             for (uint32_t j = 1; j < ic.zstreams; ++j) cudaStreamWaitEvent(g.sd[j], g.evd[0], 0);
             auto decode = [&]() {
                 launch_swapz(sdec, (int)ic.ctas, (int)c->cfg.copy_threads, g.zstage, zs->cfrom, DevDesc{}, desc, zs->dev,
-                             zs->n_body, g.ready, g.ctl, g.ctl, 0, 1, g.progress);
+                             zs->n_body, g.ready, g.ctl, g.ctl, 0, 1, g.progress, zs->htab);
             };
             // DMAZT: the zero-copy tail kernel on copy stream 1, resident from the start (the gate counts its CTAs);
             // it reads the host store only once the last body group has landed (one transfer on the link at a time)
             const uint32_t n_tail = (uint32_t)zs->host.size() - zs->n_body;
             auto tail = [&](cudaStream_t st) {
                 launch_swapz_after(st, (int)ic.tail_ctas, m.zstore, DevDesc{}, desc, zs->dev + zs->n_body, n_tail, g.ready, g.ctl_tail,
-                                   g.ctl, g.progress, (uint32_t)zs->groups.size());
+                                   g.ctl, g.progress, (uint32_t)zs->groups.size(), zs->htab);
             };
             if (ic.engine == FSW_ENGINE_DMAZT && !serial) {
                 cudaStreamWaitEvent(g.sd[1], g.evd[0], 0);

@@ -366,8 +366,8 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     InvokeCfg ic{cold, (flags & FSW_NO_OVERLAP) != 0, engine,
                  o.chunk_bytes ? o.chunk_bytes : c->cfg.chunk_bytes, (int)o.order, o.order_seed,
                  o.copy_ctas                     ? o.copy_ctas
-                 : engine_dmaz(engine)           ? std::max(c->cfg.copy_ctas, kDmazCtas)
-                 : engine == FSW_ENGINE_SMZ      ? std::max(c->cfg.copy_ctas, kSmzCtas)
+                 : engine_dmaz(engine)           ? std::max(c->cfg.copy_ctas, m->htab.empty() ? kDmazCtas : dmaz_huff_ctas())
+                 : engine == FSW_ENGINE_SMZ      ? std::max(c->cfg.copy_ctas, m->htab.empty() ? kSmzCtas : smz_huff_ctas())
                                                  : c->cfg.copy_ctas,
                  extents(gi), nullptr};
     ic.from = pcached ? m->split : 0;
@@ -525,7 +525,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                 cudaEventRecord(sl.evfork, sl.st);
                 cudaStreamWaitEvent(sl.sdec, sl.evfork, 0);
                 launch_swapz(sl.sdec, (int)ic.ctas, (int)c->cfg.copy_threads, sl.stage, 0, ic.dst, nullptr, zps[j]->dev,
-                             (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 1, sl.progress);
+                             (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 1, sl.progress, zps[j]->htab);
                 uint32_t cnt = 0;
                 uint64_t soff = 0;  // run k sits at the sum of the earlier runs' bytes (get_zstripe_dma)
                 for (size_t gi2 = 0; gi2 < zps[j]->groups.size(); ++gi2) {
@@ -539,7 +539,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
                 cudaStreamWaitEvent(sl.st, sl.evjoin, 0);
             } else if (engine == FSW_ENGINE_SMZ)
                 launch_swapz(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->zstore, 0, ic.dst, nullptr, zps[j]->dev,
-                             (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 0, nullptr);
+                             (uint32_t)zps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1, 0, nullptr, zps[j]->htab);
             else
                 launch_swap(sl.st, (int)ic.ctas, (int)c->cfg.copy_threads, m->store, ic.dst, nullptr, sps[j]->dev,
                             (uint32_t)sps[j]->host.size(), g.ready, sl.ctl, g.ctl, 1);

@@ -98,9 +98,28 @@ void launch_gate(cudaStream_t s, DevCtl* ctl, uint32_t expected);
 // in word order (bit j of plane q = bit q of s_j; d = s_j < o ? s_j : s_j + 3, so escapes cover
 // d in [0, o) and [o + 3, 10]), then n_x exceptions as above (escaped words with d >= 11, s_j = 0),
 // zero-padded to a multiple of 16 bytes.  The encoder picks per block the kind with the fewest bytes.
+// Entropy-coded pieces (v5): every coded block of the piece is kind kZHuff (b = 0x20; raw and zero blocks
+// may sit between them).  Header: h = bits 0-7, the block's escape count n_esc = bits 16-25.  The offset
+// s_i = min(h − e_i, 15) of every word is a canonical Huffman code (MSB first) of the MODEL's 16 code lengths
+// (<= kZHuffLmax bits; s = 15 = escape: the whole word is an exception).  Stream A as for coded blocks
+// (512 sign|mantissa bytes); stream B of the piece = E = Σ n_esc exception words (16 bits, in (block,
+// lane, i) order), zero-padded to 16 B, then 4·K 16-bit code words: word j belongs to sub-stream j mod 4
+// (its (j / 4)-th word; K = the longest sub-stream, the others zero-padded), zero-padded to 16 B.
+// Sub-stream q carries the piece's kZHuff blocks with index ≡ q (mod 4), in order.  Decoding a block of
+// sub-stream q: for i = 0..15, every lane l (0..31) whose bit buffer does not hold its next whole code (the
+// code its bits start, read with zeros after them, is longer than the bits held) first appends the
+// sub-stream's next word (the needing lanes, in increasing l, take consecutive words), then every lane
+// decodes one code from the top of its buffer: s for word 16·l + i.  Buffers start empty at the piece's start.  The decoded word is (m_i & 0x80) << 8 | ((h − s) & 0xff) << 7 | (m_i & 0x7f), or the
+// next exception word when s = 15.  A piece is entropy-coded only when that is smaller than its v4 form
+// and its coded bytes fit one SMZ ring slot (kZBuf): the decoder reads it from shared memory.
 constexpr uint32_t kZPiece = 16384;
 constexpr uint32_t kZBlock = 1024;
-constexpr uint32_t kZRaw = 0xff, kZZero = 0xfe, kZTier = 0x10;
+constexpr uint32_t kZRaw = 0xff, kZZero = 0xfe, kZTier = 0x10, kZHuff = 0x20;
+constexpr uint32_t kZHuffLmax = 12, kZHuffEsc = 15;
+constexpr uint32_t kZHuffTabBytes = 1u << kZHuffLmax;  // decode table: s | L << 4 for every 12-bit window
+constexpr uint32_t kZBuf = 12288;  // SMZ ring slot: largest coded piece decoded from shared memory
+__host__ __device__ __forceinline__ bool zhuff(uint32_t hdr) { return ((hdr >> 8) & 0xffu) == kZHuff; }
+__host__ __device__ __forceinline__ uint32_t zhuff_nesc(uint32_t hdr) { return (hdr >> 16) & 0x3ffu; }
 // stream-A and stream-B bytes of one block
 __host__ __device__ __forceinline__ uint32_t zblock_a(uint32_t hdr, uint32_t raw_bytes) {
     const uint32_t b = (hdr >> 8) & 0xffu;
@@ -135,15 +154,18 @@ struct ZPiece {
 // (stage = 0, zero-copy over the host link) or the device staging buffer the copy engine filled
 // (stage = 1; each piece first waits until *progress > grp).  Destinations, ready counters, gate and
 // sys as launch_swap.
+// htab: the model's 4096-entry decode table of entropy-coded pieces (entry = s | len << 4 for every 12-bit
+// prefix), or nullptr when the model has none; such models decode through the shared-memory (TMA ring)
+// decoder on every path.
 void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
                   const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
-                  DevCtl* gate, int sys, int stage, const uint32_t* progress);
+                  DevCtl* gate, int sys, int stage, const uint32_t* progress, const uint8_t* htab);
 // DMAZT tail: the zero-copy (SMZ) decoder over pieces of the mapped coded store, whose CTAs start their reads
 // once *start_ctr >= start_after (the DMAZ body's last copy group published); its last releases are also
 // stamped into the gate's t_last (the invoke's swap span).
 void launch_swapz_after(cudaStream_t s, int ctas, const uint8_t* zstore, DevDesc dst, const DevDesc* desc, const ZPiece* pieces,
                         uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, const uint32_t* start_ctr,
-                        uint32_t start_after);
+                        uint32_t start_after, const uint8_t* htab);
 
 void launch_finish(cudaStream_t s, DevCtl* ctl, const uint8_t* out, uint64_t bytes, uint8_t* host_out, DevCtl* host_ctl);
 

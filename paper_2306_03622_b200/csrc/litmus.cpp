@@ -107,7 +107,7 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
         launch_swap(sc, (int)ctas, threads, m->store, dst, nullptr, ps->dev, (uint32_t)ps->host.size(), g.ready, g.ctl, g.ctl, 0);
     } else if (engine == FSW_ENGINE_SMZ) {
         launch_swapz(sc, (int)ctas, threads, m->zstore, 0, dst, nullptr, zs->dev, (uint32_t)zs->host.size(), g.ready, g.ctl, g.ctl,
-                     0, 0, nullptr);
+                     0, 0, nullptr, zs->htab);
     } else if (engine == FSW_ENGINE_DMA) {
         gate = 0;  // no producer kernel: the copy engine publishes with fenced stream writes
         uint32_t cnt = 0;
@@ -121,12 +121,12 @@ extern "C" fsw_status fsw_debug_litmus(fsw_ctx* c, uint32_t id, int32_t gpu, uin
         cudaEventRecord(g.evd[0], sc);
         cudaStreamWaitEvent(g.sz, g.evd[0], 0);
         launch_swapz(g.sz, (int)ctas, threads, stage, zs->cfrom, dst, nullptr, zs->dev, zs->n_body, g.ready, g.ctl,
-                     g.ctl, 0, 1, g.progress);
+                     g.ctl, 0, 1, g.progress, zs->htab);
         if (engine == FSW_ENGINE_DMAZT) {  // + the zero-copy tail after the last body group
             cudaStreamWaitEvent(g.sd[1], g.evd[0], 0);
             launch_swapz_after(g.sd[1], (int)kSmzCtas, m->zstore, dst, nullptr, zs->dev + zs->n_body,
                                (uint32_t)zs->host.size() - zs->n_body, g.ready, g.ctl_tail, g.ctl, g.progress,
-                               (uint32_t)zs->groups.size());
+                               (uint32_t)zs->groups.size(), zs->htab);
             gate += kSmzCtas;
         }
         uint32_t cnt = 0;

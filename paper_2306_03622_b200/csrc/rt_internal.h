@@ -147,6 +147,7 @@ struct ZPieceSet {
     std::vector<Group> groups;                          // DMAZ: coded-store byte ranges, in order
     uint64_t cfrom = 0, cend = 0;                        // coded bytes [cfrom, cend) cover the pieces
     uint32_t n_body = 0;   // DMAZT: pieces [0, n_body) move by copy groups, [n_body, size) zero-copy (SMZ tail)
+    uint8_t* htab = nullptr;  // the model's decode table on this set's device (entropy-coded pieces), or nullptr
 };
 
 // The persistent transformer kernel's plan (mega.cu): the op list without the per-invoke waits, one
@@ -204,6 +205,10 @@ struct Model {
     uint8_t* zstore = nullptr;
     uint64_t zbytes = 0, zalloc = 0;
     std::vector<ZPiece> zpieces;  // execution order, grp = 0
+    // entropy-coded pieces (v5, kernels.h kZHuff): the model's 16 canonical code lengths and the decoder's
+    // 4096-entry table (empty when no piece is entropy-coded)
+    uint8_t hlen[16] = {};
+    std::vector<uint8_t> htab;
     // residency per GPU
     std::vector<int64_t> extent;       // pool offset of the model (split = 0) or of its suffix, or -1
     // partial-parameter caching: store bytes [0, split) — whole layers —
@@ -357,6 +362,15 @@ inline bool engine_bytes_ready(int e) { return e == FSW_ENGINE_SM || engine_code
 // 168 GB/s on 48 (measured alone, tools/dmaz_probe.py); beside the layer kernels 32 CTAs fall behind
 // the copy engine (BERT-base 3.10 ms), 48 do not (2.82 ms, as 64 and 96).
 constexpr uint32_t kSmzCtas = 32, kDmazCtas = 48;
+// DMAZ decode CTAs (128-thread shared-memory decoder) for models with entropy-coded pieces (FSW_DMAZ_HUFF_CTAS)
+inline uint32_t smz_huff_ctas() {  // SMZ decode CTAs for models with entropy-coded pieces (FSW_SMZ_HUFF_CTAS)
+    static const uint32_t v = getenv("FSW_SMZ_HUFF_CTAS") ? (uint32_t)atoi(getenv("FSW_SMZ_HUFF_CTAS")) : 64u;
+    return v;
+}
+inline uint32_t dmaz_huff_ctas() {
+    static const uint32_t v = getenv("FSW_DMAZ_HUFF_CTAS") ? (uint32_t)atoi(getenv("FSW_DMAZ_HUFF_CTAS")) : 128u;
+    return v;
+}
 
 struct InvokeCfg {
     bool cold, no_overlap;

@@ -259,11 +259,11 @@ void free_plan(Gpu& g, Plan& p) {
     p.pieces.clear();
     for (auto& kv : p.stripe) cudaFree(kv.second.dev);  // UVA: any current device
     p.stripe.clear();
-    for (auto& kv : p.zp) cudaFree(kv.second.dev);
+    for (auto& kv : p.zp) cudaFree(kv.second.dev), cudaFree(kv.second.htab);
     p.zp.clear();
-    for (auto& kv : p.zstripe) cudaFree(kv.second.dev);
+    for (auto& kv : p.zstripe) cudaFree(kv.second.dev), cudaFree(kv.second.htab);
     p.zstripe.clear();
-    for (auto& kv : p.zstripe_dma) cudaFree(kv.second.dev);
+    for (auto& kv : p.zstripe_dma) cudaFree(kv.second.dev), cudaFree(kv.second.htab);
     p.zstripe_dma.clear();
 }
 
@@ -439,6 +439,15 @@ extern "C" fsw_status fsw_debug_read_coded(fsw_ctx* c, uint32_t id, void* dst, u
     if (!m->zstore) return fail(FSW_ESTATE, "model %u is not link-coded", id);
     if (!dst || cap < m->zbytes) return fail(FSW_EINVAL, "read_coded: cap %llu < %llu", (unsigned long long)cap, (unsigned long long)m->zbytes);
     memcpy(dst, m->zstore, m->zbytes);
+    return FSW_OK;
+}
+
+extern "C" fsw_status fsw_debug_coded_code(fsw_ctx* c, uint32_t id, uint8_t* lengths_out) {
+    Model* m = find_model(c, id);
+    if (!m) return fail(FSW_ENOTFOUND, "model %u not found", id);
+    if (!m->zstore) return fail(FSW_ESTATE, "model %u is not link-coded", id);
+    if (!lengths_out) return fail(FSW_EINVAL, "coded_code: lengths_out is NULL");
+    memcpy(lengths_out, m->hlen, 16);
     return FSW_OK;
 }
 

@@ -356,7 +356,7 @@ __global__ void __maxnreg__(64) k_swapz(const uint8_t* __restrict__ src, uint64_
 // pieces (<= kZBuf bytes) with cp.async.bulk into a double-buffered ring (the async copy engine of
 // the SM, completion on an mbarrier); the CTA's 4 warps decode the previous piece from shared memory
 // meanwhile (blocks w, w+4, ... per warp), store it, and release it on its layer's counter.
-constexpr uint32_t kZBuf = 12288, kZRing = 2;
+constexpr uint32_t kZRing = 2;  // kZBuf: kernels.h
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // STAGE: the same kernel decodes the DMAZ staging buffer (src + coff − src_base): thread 0 first waits
@@ -365,13 +365,18 @@ template <bool STAGE>
 __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ src, uint64_t src_base, DevDesc dst,
                                                    const DevDesc* __restrict__ desc, const ZPiece* __restrict__ pieces,
                                                    uint32_t n_pieces, uint32_t* __restrict__ ready, DevCtl* __restrict__ own,
-                                                   DevCtl* gate, int sys, const uint32_t* progress, uint32_t start_after = 0) {
+                                                   DevCtl* gate, int sys, const uint32_t* progress, uint32_t start_after,
+                                                   const uint8_t* __restrict__ htab) {
     extern __shared__ __align__(128) uint8_t zring[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(zring + kZRing * kZBuf);
     uint32_t* slot = reinterpret_cast<uint32_t*>(bar + kZRing);
+    uint8_t* htab_s = zring + kZRing * kZBuf + 64;  // the model's decode tables (entropy-coded pieces, kZHuffTabBytes)
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u, drop = g_drop_piece;
     [[maybe_unused]] unsigned long long* const tr = g_trace;
     const DevDesc dd = desc ? *desc : dst;
+    if (htab)
+        for (uint32_t i = tid; i < kZHuffTabBytes / 16u; i += blockDim.x)
+            reinterpret_cast<uint4*>(htab_s)[i] = __ldg(reinterpret_cast<const uint4*>(htab) + i);
     if (tid == 0) {
         gate_arrive(gate, sys);
         for (uint32_t b = 0; b < kZRing; ++b)
@@ -428,16 +433,25 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         const uint32_t hd = lane < nb ? __ldg(&pieces[p].hdr[lane]) : 0u;
         const uint32_t sa = lane < nb ? zblock_a(hd, min(kZBlock, pc.bytes - lane * kZBlock)) : 0u;
         const uint32_t sb = lane < nb ? zblock_b(hd) : 0u;
-        uint32_t ia = sa, ib = sb;
+        const uint32_t se = lane < nb && zhuff(hd) ? zhuff_nesc(hd) : 0u;  // entropy-coded blocks' escapes
+        uint32_t ia = sa, ib = sb, ie = se;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+            const uint32_t te = __shfl_up_sync(0xffffffffu, ie, o);
             if (lane >= (uint32_t)o) {
                 ia += ta;
                 ib += tb;
+                ie += te;
             }
         }
         const uint8_t* cb = cp + ((__shfl_sync(0xffffffffu, ia, 31) + 127u) & ~127u);
+        // entropy-coded piece (kernels.h kZHuff): exception words at the start of stream B, then the interleaved
+        // code words; this warp's blocks (warp, warp + 4, ...) are exactly sub-stream q = warp
+        const uint32_t etot = __shfl_sync(0xffffffffu, ie, 31);
+        const uint16_t* hexc = reinterpret_cast<const uint16_t*>(cb);
+        const uint16_t* hwords = reinterpret_cast<const uint16_t*>(cb + ((2u * etot + 15u) & ~15u));
+        uint32_t hbuf = 0, hbits = 0, hpos = 0;
         for (uint32_t blk = warp; blk < nb; blk += 4) {
             const uint32_t h = __shfl_sync(0xffffffffu, hd, blk), oa = __shfl_sync(0xffffffffu, ia - sa, blk);
             const uint32_t ob = __shfl_sync(0xffffffffu, ib - sb, blk);
@@ -450,6 +464,48 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
             } else if (kind == kZRaw) {
                 const uint32_t n16 = min(kZBlock, pc.bytes - blk * kZBlock) >> 4;
                 for (uint32_t i = lane; i < n16; i += 32) st_v4(o4 + i, *reinterpret_cast<const uint4*>(cp + oa + i * 16u));
+            } else if (kind == kZHuff) {
+                // lane l decodes words 16 l .. 16 l + 15: refill (lanes below kZHuffLmax bits take consecutive
+                // words of the sub-stream, in lane order), then one canonical code from the top of the buffer
+                const uint4 sm = *reinterpret_cast<const uint4*>(cp + oa + lane * 16u);
+                const uint32_t lt = (1u << lane) - 1u;
+                uint64_t dp = 0;
+                uint32_t em = 0;
+#pragma unroll
+                for (uint32_t i = 0; i < 16; ++i) {
+                    // the code at the front of the buffer (bits past hbits read as zero); when it is longer than
+                    // the bits held, the buffer lacks it — refill and look again
+                    uint32_t e = htab_s[hbuf >> (32u - kZHuffLmax)];
+                    const bool need = (e >> 4) > hbits;
+                    const uint32_t mk = __ballot_sync(0xffffffffu, need);
+                    if (need) {
+                        hbuf |= (uint32_t)hwords[4u * (hpos + __popc(mk & lt)) + warp] << (16u - hbits);
+                        hbits += 16u;
+                        e = htab_s[hbuf >> (32u - kZHuffLmax)];
+                    }
+                    hpos += __popc(mk);
+                    const uint32_t len = e >> 4, sy = e & 15u;
+                    hbuf <<= len;
+                    hbits -= len;
+                    dp |= (uint64_t)sy << (4u * i);
+                    em |= (sy == kZHuffEsc ? 1u : 0u) << i;
+                }
+                uint4 o0, o1;
+                zdecode16(sm, dp, h & 0xffu, o0, o1);
+                st_v4(o4 + 2 * lane, o0);
+                st_v4(o4 + 2 * lane + 1, o1);
+                if (zhuff_nesc(h)) {  // escaped words: the exception words in (block, lane, i) order
+                    const uint32_t cnt = __popc(em);
+                    uint32_t r = cnt;
+#pragma unroll
+                    for (int sft = 1; sft < 32; sft <<= 1) {
+                        const uint32_t t = __shfl_up_sync(0xffffffffu, r, sft);
+                        if (lane >= (uint32_t)sft) r += t;
+                    }
+                    uint32_t k = __shfl_sync(0xffffffffu, ie - se, blk) + r - cnt;
+                    uint16_t* o16 = reinterpret_cast<uint16_t*>(bo) + 16u * lane;
+                    for (uint32_t x = em; x; x &= x - 1u) o16[__ffs(x) - 1] = hexc[k++];  // after this lane's own stores
+                }
             } else {
                 const uint4 sm = *reinterpret_cast<const uint4*>(cp + oa + lane * 16u);
                 const uint32_t n = zexc_n(h), xo = zexc_off(h);
@@ -489,28 +545,29 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
 
 void launch_swapz(cudaStream_t s, int ctas, int threads, const uint8_t* src, uint64_t src_base, DevDesc dst,
                   const DevDesc* desc, const ZPiece* pieces, uint32_t n_pieces, uint32_t* ready, DevCtl* own,
-                  DevCtl* gate, int sys, int stage, const uint32_t* progress) {
+                  DevCtl* gate, int sys, int stage, const uint32_t* progress, const uint8_t* htab) {
     // A/B hooks: FSW_SWAPZ_REGS = the register decoder from host memory too, FSW_DMAZ_TMA = the TMA
     // ring decoder on the staging buffer (measured slower there: 128 threads per CTA decode 86 GB/s of
     // store bytes on 32 CTAs, the 256-thread register decoder 117; tools/dmaz_probe.py)
+    // Models with entropy-coded pieces (htab) always take the shared-memory decoder.
     static const bool swapz_regs = getenv("FSW_SWAPZ_REGS") != nullptr, dmaz_tma = getenv("FSW_DMAZ_TMA") != nullptr;
-    const size_t smem = kZRing * kZBuf + 64;
-    if (stage && !dmaz_tma)
+    const size_t smem = kZRing * kZBuf + 64 + (htab ? kZHuffTabBytes : 0u);
+    if (stage && !dmaz_tma && !htab)
         k_swapz<true, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
     else if (stage)
-        k_swapz_tma<true><<<ctas, 128, smem, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
-    else if (swapz_regs)
+        k_swapz_tma<true><<<ctas, 128, smem, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress, 0u, htab);
+    else if (swapz_regs && !htab)
         k_swapz<false, 2><<<ctas, threads, 0, s>>>(src, src_base, dst, desc, pieces, n_pieces, ready, own, gate, sys, progress);
     else  // src_base is 0 for the mapped host store (pieces address it by coff)
-        k_swapz_tma<false><<<ctas, 128, smem, s>>>(src, 0, dst, desc, pieces, n_pieces, ready, own, gate, sys, nullptr);
+        k_swapz_tma<false><<<ctas, 128, smem, s>>>(src, 0, dst, desc, pieces, n_pieces, ready, own, gate, sys, nullptr, 0u, htab);
 }
 
 void launch_swapz_after(cudaStream_t s, int ctas, const uint8_t* zstore, DevDesc dst, const DevDesc* desc, const ZPiece* pieces,
                         uint32_t n_pieces, uint32_t* ready, DevCtl* own, DevCtl* gate, const uint32_t* start_ctr,
-                        uint32_t start_after) {
-    const size_t smem = kZRing * kZBuf + 64;
+                        uint32_t start_after, const uint8_t* htab) {
+    const size_t smem = kZRing * kZBuf + 64 + (htab ? kZHuffTabBytes : 0u);
     k_swapz_tma<false><<<ctas, 128, smem, s>>>(zstore, 0, dst, desc, pieces, n_pieces, ready, own, gate, 0, start_ctr,
-                                               start_after);
+                                               start_after, htab);
 }
 
 // Gate: the first node of the layer stream.  Holds the layer kernels back until every swap

@@ -149,7 +149,7 @@ EXPORTS = ["fsw_init", "fsw_shutdown", "fsw_last_error", "fsw_version", "fsw_reg
            "fsw_policy_schedule", "fsw_policy_eviction_order", "fsw_model_set_heavy", "fsw_model_is_heavy",
            "fsw_sched_create", "fsw_sched_destroy", "fsw_function_register", "fsw_submit", "fsw_wait",
            "fsw_function_stats_get", "fsw_sched_stats_get", "fsw_evict_ex", "fsw_model_set_cache_prefix",
-           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal",
+           "fsw_debug_read_coded", "fsw_debug_coded_pieces", "fsw_debug_coded_code", "fsw_debug_dmaz_plan", "fsw_policy_stripe_deal",
            "fsw_debug_set_fault", "fsw_debug_litmus", "fsw_policy_heavy", "fsw_model_set_slo",
            "fsw_set_heavy_policy", "fsw_debug_trace_read", "fsw_debug_mega_stamps"]
 
@@ -184,6 +184,7 @@ def lib():
         L.fsw_debug_read_slot.argtypes = [vp, u32, i32, i32, vp, u64]
         L.fsw_debug_read_coded.argtypes = [vp, u32, vp, u64]
         L.fsw_debug_coded_pieces.argtypes = [vp, u32, vp, u32, ctypes.POINTER(u32)]
+        L.fsw_debug_coded_code.argtypes = [vp, u32, vp]
         L.fsw_debug_dmaz_plan.argtypes = [vp, u32, u64, u32, vp, vp, u32, ctypes.POINTER(u32), vp]
         L.fsw_debug_set_fault.argtypes = [vp, u32, u32]
         L.fsw_debug_trace_read.argtypes = [vp, u32, i32, vp, u32, vp]
@@ -441,6 +442,12 @@ class Runtime:
         buf = np.empty(n, dtype=np.uint8)
         _check(lib().fsw_debug_read_coded(self.h, mid, buf.ctypes.data, n))
         return buf
+
+    def coded_code(self, mid: int) -> np.ndarray:
+        """The model's 16 canonical code lengths of entropy-coded pieces (all 0: none; include/fsw.h)."""
+        out = np.zeros(16, np.uint8)
+        _check(lib().fsw_debug_coded_code(self.h, mid, out.ctypes.data))
+        return out
 
     def coded_pieces(self, mid: int) -> np.ndarray:
         """Piece table of the link-coded store: structured array (off, coff, bytes, cbytes, layer, hdr[16])."""

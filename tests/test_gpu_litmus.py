@@ -42,6 +42,43 @@ def test_litmus_release_acquire_proxy(rt, litmus_model, engine, ctas):
     assert bad == 0, f"{bad} stale 16-byte words seen by consumers over {ITERS} iterations"
 
 
+@pytest.fixture(scope="module")
+def litmus_model_huff(rt):
+    """The same store with entropy-coded pieces (format v5) forced on: the shared-memory decoder as producer."""
+    import os
+    spec = synth.mlp(width=256, n_layers=64, seed=43)
+    w = spec.build_weights()
+    old = os.environ.get("FSW_LINK_HUFF")
+    os.environ["FSW_LINK_HUFF"] = "1"  # read at registration
+    try:
+        mid = rt.register_spec(spec, w, link_code=True)
+    finally:
+        if old is None:
+            del os.environ["FSW_LINK_HUFF"]
+        else:
+            os.environ["FSW_LINK_HUFF"] = old
+    assert rt.coded_code(mid).any()
+    yield spec, mid
+    rt.set_fault(FAULT_NONE)
+    rt.unregister(mid)
+
+
+@pytest.mark.parametrize("ctas", [1, 16, 148])
+@pytest.mark.parametrize("engine", [ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
+def test_litmus_entropy_coded(rt, litmus_model_huff, engine, ctas):
+    spec, mid = litmus_model_huff
+    store = rt.model_info(mid)["store_bytes"]
+    bad, checked = rt.litmus(mid, engine, ctas, ITERS // 4)
+    assert checked == ITERS // 4 * store, (checked, ITERS // 4 * store)
+    assert bad == 0, f"{bad} stale 16-byte words seen by consumers"
+    rt.set_fault(FAULT_DROP_PIECE, 5)
+    try:
+        bad, _ = rt.litmus(mid, engine, 16, 20)
+    finally:
+        rt.set_fault(FAULT_NONE)
+    assert bad > 0, "a dropped entropy-coded piece must be seen as stale (poison) words"
+
+
 @pytest.mark.parametrize("engine", [ENGINE_SM, ENGINE_SMZ, ENGINE_DMAZ, ENGINE_DMAZT])
 def test_litmus_negative_control_drop_piece(rt, litmus_model, engine):
     spec, mid = litmus_model
