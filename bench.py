@@ -562,7 +562,8 @@ def run_fsw(args):
     except Exception:
         dec = None
     if engine in ("dmaz", "dmazt"):
-        roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA of link-coded groups into HBM staging + k_swapz decode"
+        roof = {"bound": "pcie", "kernel": "swap engine: copy-engine DMA of link-coded groups into HBM staging + "
+                + ("k_swapz_tma decode of the entropy-coded pieces (format v5)" if rt.coded_code(mid).any() else "k_swapz decode")
                 + (" (DMAZT: the last 7 MB of coded bytes zero-copy through the SMZ decoder)" if engine == "dmazt" else ""),
                 "achieved": round(wire_gbs, 2), "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                 "frac": round(wire_gbs / PCIE_GEN5_X16_GBS, 4), "store_bytes_gbs": round(achieved, 2),
@@ -570,7 +571,7 @@ def run_fsw(args):
                              "achieved = coded bytes over the link / swap time, store_bytes_gbs = decoded bytes / swap time",
                 "frac_of_measured_dma": round(wire_gbs / dma, 4) if dma else None,
                 "traffic": dec["dram_bytes"] if dec else None,
-                "traffic_note": "DRAM read+write bytes of the decode kernel k_swapz per cold invoke (ncu --set full, "
+                "traffic_note": "DRAM read+write bytes of the decode kernel per cold invoke (ncu --set full, "
                 "profiles/swap_traffic.json): it reads the staged coded bytes once and writes the store bytes (the "
                 "rest still in L2 at kernel end); the copy-engine transfer itself is not a kernel",
                 "decode_kernel_alone_ms": dec["duration_ms"] if dec else None}
