@@ -375,7 +375,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
     if (cold && engine == FSW_ENGINE_DMA) ic.dma_plan = &get_dma_plan(*m, p, dgrp, dstr, ic.from);
     ic.zgrp = dgrp;
     ic.zstreams = dstr;
-    ic.tail_ctas = engine == FSW_ENGINE_DMAZT && !striped ? kSmzCtas : 0;
+    ic.tail_ctas = engine == FSW_ENGINE_DMAZT && !striped ? (m->htab.empty() ? kSmzCtas : dmazt_huff_tail_ctas()) : 0;
     if (cold && engine_dmaz(engine) && !striped && g.zstage_cap < m->zbytes) {
         // grow the staging buffer (graphs bake its address: the generation is part of their key)
         cudaFree(g.zstage);

@@ -367,6 +367,10 @@ inline uint32_t smz_huff_ctas() {  // SMZ decode CTAs for models with entropy-co
     static const uint32_t v = getenv("FSW_SMZ_HUFF_CTAS") ? (uint32_t)atoi(getenv("FSW_SMZ_HUFF_CTAS")) : 64u;
     return v;
 }
+inline uint32_t dmazt_huff_tail_ctas() {  // DMAZT zero-copy tail CTAs, entropy-coded pieces (FSW_DMAZT_HUFF_TAIL_CTAS)
+    static const uint32_t v = getenv("FSW_DMAZT_HUFF_TAIL_CTAS") ? (uint32_t)atoi(getenv("FSW_DMAZT_HUFF_TAIL_CTAS")) : 64u;
+    return v;
+}
 inline uint32_t dmaz_huff_ctas() {
     static const uint32_t v = getenv("FSW_DMAZ_HUFF_CTAS") ? (uint32_t)atoi(getenv("FSW_DMAZ_HUFF_CTAS")) : 128u;
     return v;
