@@ -25,7 +25,6 @@
 
 namespace fsw {
 
-static __device__ int g_ws_debug = 0;  // FSW_WS_DEBUG (timing experiments only): 1 local-only reduction, 2 no stores
 namespace {
 constexpr int kWsMaxKt = 16;          // k sub-tiles one CTA holds (kt_per)
 constexpr uint32_t kWsW = 128 * 128;  // one 128-row x 64-k weight sub-tile: 16 KiB
@@ -186,19 +185,26 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
             if (u >= units) continue;
             const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
             const float* src = st + tok * 128 + 4 * q;
-            if (S > 1 && !(g_ws_debug & 1)) {
-                float4 v[8];
+            if (S > 1) {
+                // splits in order, 8 loads in flight at a time (clusters of up to 16: non-portable sizes)
+                acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (uint32_t z0 = 0; z0 < S; z0 += 8) {
+                    float4 v[8];
 #pragma unroll
-                for (uint32_t z = 0; z < 8; ++z)
-                    if (z < S) v[z] = ld_dsmem_f4(src, z);
-                acc[e] = v[0];
+                    for (uint32_t z = 0; z < 8; ++z)
+                        if (z0 + z < S) v[z] = ld_dsmem_f4(src, z0 + z);
 #pragma unroll
-                for (uint32_t z = 1; z < 8; ++z) {
-                    if (z >= S) break;
-                    acc[e].x += v[z].x;
-                    acc[e].y += v[z].y;
-                    acc[e].z += v[z].z;
-                    acc[e].w += v[z].w;
+                    for (uint32_t z = 0; z < 8; ++z) {
+                        if (z0 + z >= S) break;
+                        if (z0 + z == 0) {
+                            acc[e] = v[0];
+                            continue;
+                        }
+                        acc[e].x += v[z].x;
+                        acc[e].y += v[z].y;
+                        acc[e].z += v[z].z;
+                        acc[e].w += v[z].w;
+                    }
                 }
             } else {
                 acc[e] = *reinterpret_cast<const float4*>(src);
@@ -230,7 +236,6 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
             const uint64_t oi = (uint64_t)t * a.ld_out + n;
             const uint2 pk = make_uint2((uint32_t)f32_to_bf16(v.x) | ((uint32_t)f32_to_bf16(v.y) << 16),
                                         (uint32_t)f32_to_bf16(v.z) | ((uint32_t)f32_to_bf16(v.w) << 16));
-            if (g_ws_debug & 2) continue;
             if (a.out_bf16) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + oi) = pk;
             else *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oi) = v;
             if (a.out2) *reinterpret_cast<uint2*>(a.out2 + oi) = pk;
@@ -296,15 +301,17 @@ int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz) {
     }
 }
 
+template <int TT>
+static void ws_attrs() {
+    cudaFuncSetAttribute(k_gemm_ws<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_gemm_ws<TT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);  // split-K clusters up to 16
+}
+
 void init_gemm_ws_attrs() {
-    {
-        static const int dbg = getenv("FSW_WS_DEBUG") ? atoi(getenv("FSW_WS_DEBUG")) : 0;
-        cudaMemcpyToSymbol(g_ws_debug, &dbg, sizeof dbg);
-    }
-    cudaFuncSetAttribute(k_gemm_ws<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_gemm_ws<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_gemm_ws<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_gemm_ws<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    ws_attrs<16>();
+    ws_attrs<32>();
+    ws_attrs<64>();
+    ws_attrs<128>();
 }
 
 }  // namespace fsw

@@ -50,7 +50,8 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
 
 // Tiling of the weight-stationary swap-AB GEMM (k_gemm_ws, gemm_ws.cu): tt tokens per tile and `splits` K
 // ranges over a cluster, one wave.  Measured in the invoke graph (profiles/r02/gemm/ws_sweep.txt, resident
-// BERT-base): it beats k_gemm on the narrow linears (N <= 12 weight-row tiles: O-projection, FFN2), where k_gemm
+// BERT-base): it beats k_gemm on the narrow linears (N <= 16 weight-row tiles: O-projection, FFN2; GPT-2 attention
+// projection), where k_gemm
 // has few CTAs each streaming the whole activation, and loses on the wide ones (QKV, FFN1), where its DSMEM
 // split-K reduction and larger epilogue cost more than the activation bytes it saves.  Cost (relative, fitted to
 // that sweep): the epilogue's token width, the split-K reduction, the MMA chain, and a penalty for CTAs too large
@@ -78,10 +79,10 @@ static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool a
             sscanf(force, "%d:%d", &ftt, &fs);
         }
     }
-    if (ftt < 0 || M > 128 || (!any_width && !ftt && rt > 12)) return best;
+    if (ftt < 0 || M > 128 || (!any_width && !ftt && rt > 16)) return best;
     for (uint32_t tt : {16u, 32u, 64u, 128u}) {
         if (ftt && tt != (uint32_t)ftt) continue;
-        for (uint32_t s = 1; s <= 8 && s <= kt; ++s) {
+        for (uint32_t s = 1; s <= 16 && s <= kt; ++s) {  // clusters beyond 8 are non-portable (B200: 16)
             if (fs && s != (uint32_t)fs) continue;
             const uint32_t kp = (kt + s - 1) / s;
             if ((kt + kp - 1) / kp != s || kp > 16) continue;
