@@ -174,6 +174,14 @@ __global__ void __maxnreg__(96)  // 512 threads x 96 regs: a 256-thread swap CTA
         // weights of the first stages stream while the previous kernel is still running
         const uint32_t pre = min((uint32_t)stages, nst);
         for (uint32_t st = 0; st < pre; ++st) load_w(st);
+        if (lane == 0 && a.pf_bytes && w.n == 0) {  // resident (FSW_GEMM_PF): this CTA's share of the next GEMM's weights into L2
+            const uint32_t ncta = gridDim.x * gridDim.y * gridDim.z;
+            const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+            const uint64_t share = ((a.pf_bytes + ncta - 1) / ncta + 255) & ~255ull;
+            const uint64_t b0 = cta * share, b1 = a.pf_bytes < b0 + share ? a.pf_bytes : b0 + share;
+            const uint8_t* pf = weight_ptr(dd, a.pf_off);
+            for (uint64_t o = b0; o < b1; o += 65536) prefetch_l2(pf + o, (uint32_t)(b1 - o < 65536 ? b1 - o : 65536));
+        }
         pdl_wait();
         if (lane == 0) FSW_TRACE_MAX(w.trace, w.layer, 5, globaltimer());
         asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -232,8 +232,8 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // 0 = not used.  128 weight rows x ws_tt tokens per CTA; split-K over a (1, 1, splits) cluster (splits <= 8,
     // kt_per k sub-tiles each, all resident in shared memory); the A tensor map's box is ws_tt rows
     uint32_t ws_tt;
-    // L2 prefetch (k_gemm_ws, resident invokes): the next GEMM's weights [pf_off, pf_off + pf_bytes) of the
-    // store, dealt over this launch's CTAs; pf_bytes = 0: none
+    // L2 prefetch (k_gemm / k_gemm_ws, resident invokes): the next GEMM's weights [pf_off, pf_off + pf_bytes) of
+    // the store, dealt over this launch's CTAs; pf_bytes = 0: none
     uint64_t pf_off, pf_bytes;
 };
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a,
