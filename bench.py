@@ -538,7 +538,7 @@ def run_fsw(args):
     t_roof_coded = (roofline_ms(coded_lb.sum(), flops, coded_lb[0], PCIE_GEN5_X16_GBS, peak_tf) if coded_lb is not None
                     else t_roof)
     fractions = roofline_report(spec, p50, PCIE_GEN5_X16_GBS, peak_tf, coded_lb)
-    extras, dists = {}, {}
+    extras, dists, native = {}, {}, {}
     if not args.no_extras and args.model == "bert-base" and world == 1:
         for name, reps, warm_n in EXTRA_CONFIGS:
             try:
@@ -549,6 +549,21 @@ def run_fsw(args):
             dists = measure_weight_distributions(rt, "bert-base", 20, 5, PCIE_GEN5_X16_GBS, peak_tf)
         except Exception as e:
             dists = {"error": repr(e)}
+        try:  # SURVEY §8(d) step 2 context row: the same shapes as a plain PyTorch bf16 forward (cuBLAS / SDPA /
+            # cuDNN) in a CUDA graph, weights resident in HBM (tools/torch_native.py; bench-only, not the product)
+            import importlib.util
+            import torch
+            spec_tn = importlib.util.spec_from_file_location("torch_native", os.path.join(ROOT, "tools", "torch_native.py"))
+            tn = importlib.util.module_from_spec(spec_tn)
+            spec_tn.loader.exec_module(tn)
+            sys_argv, sys.argv = sys.argv, ["torch_native", "bert-base", "resnet50", "gpt2-xl"]
+            try:
+                native = tn.main()
+            finally:
+                sys.argv = sys_argv
+            torch.cuda.empty_cache()
+        except Exception as e:
+            native = {"error": repr(e)}
     cpu = None
     if not args.no_cpu_baseline:
         ct, omp_threads = cpu_oracle_timing(spec, w, x, budget_s=args.cpu_budget_s, max_reps=20)
@@ -631,6 +646,7 @@ def run_fsw(args):
         "engines": variants,
         "configs_1gpu": extras,
         "weight_distributions": dists,
+        "native_torch_resident_ms": native,
         "cpu_baseline": cpu,
         "e2e": {"value": round(percentile(e2e, 50), 4), "unit": "ms",
                 "h2d_bytes_per_step": int(info["input_bytes"]), "d2h_bytes_per_step": int(info["output_bytes"]),
