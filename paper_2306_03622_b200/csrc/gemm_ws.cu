@@ -15,9 +15,10 @@
 //     finishes when the CTA is resident early (programmatic dependent launch);
 //   * after the wait only the TT x K_range activation slice moves (TMA, one box per k sub-tile), and each
 //     sub-tile's 4 MMAs issue as soon as it lands;
-//   * the S partial tiles of a cluster are reduced over distributed shared memory: CTA z sums weight-row
-//     quads [z·32/S, (z+1)·32/S) of all S tiles in split order (deterministic) and runs the fused
-//     bias / residual / activation epilogue on them with 8-16-B coalesced accesses.
+//   * the S partial tiles of a cluster are reduced over distributed shared memory: each CTA pushes every row's
+//     partial into the receive region of the CTA that owns the row's sum (CTA z owns weight-row quads
+//     [z·per, (z+1)·per), per = ceil(32/S)); after one cluster barrier the owner sums its rows in split order
+//     (deterministic) and runs the fused bias / residual / activation epilogue with 8-16-B coalesced accesses.
 // The grid is one wave: (ceil(N/128), ceil(M/TT), S) CTAs of 512 threads (16 warps share the epilogue: with one
 // warp per scheduler its dependent ALU chains — the GELU — were latency-bound, 4-5 us per epilogue).
 #include "device.cuh"
@@ -31,13 +32,12 @@ constexpr uint32_t kWsW = 128 * 128;  // one 128-row x 64-k weight sub-tile: 16 
 template <int TT>
 struct WsCfg {
     static constexpr uint32_t kX = TT * 128;               // one TT-token x 64-k activation sub-tile
-    static constexpr uint32_t kStage = TT * 128 * 4;       // fp32 staging tile [TT][128 rows]
     static constexpr uint32_t kTmemCols = TT < 32 ? 32 : TT;
-    __host__ __device__ static uint32_t wbytes(uint32_t kt) {  // weight region (also holds the staging tile)
-        const uint32_t w = kt * kWsW;
-        return w < kStage ? kStage : w;
-    }
-    __host__ __device__ static uint32_t smem(uint32_t kt) { return wbytes(kt) + kt * kX + 1024 + 1024; }
+    // rows of the weight tile whose split-K sum CTA z of S owns: quads [z·per, (z+1)·per), per = ceil(32 / S)
+    __host__ __device__ static uint32_t rows_owned(uint32_t S) { return 4u * ((32u + S - 1u) / S); }
+    // receive region: every split's partial of the owned rows, [S][TT][rows_owned] fp32
+    __host__ __device__ static uint32_t rbytes(uint32_t S) { return S * TT * rows_owned(S) * 4u; }
+    __host__ __device__ static uint32_t smem(uint32_t kt, uint32_t S) { return kt * kWsW + kt * kX + rbytes(S) + 1024 + 1024; }
 };
 }  // namespace
 
@@ -52,10 +52,12 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t kt0 = blockIdx.z * a.kt_per;
     const uint32_t nkt = min(a.K / kBK, kt0 + a.kt_per) - kt0;  // >= 1 (host plan)
-    uint8_t* sw = smem;                                          // weight sub-tiles, then the staging tile
-    uint8_t* sx = smem + C::wbytes(a.kt_per);                    // activation sub-tiles
+    const uint32_t S = gridDim.z;
+    uint8_t* sw = smem;                                          // weight sub-tiles
+    uint8_t* sx = smem + a.kt_per * kWsW;                        // activation sub-tiles
+    float* recv = reinterpret_cast<float*>(sx + a.kt_per * C::kX);  // split partials of the owned rows
     // 1-KiB control block: full[kWsMaxKt] | done | TMEM slot | (at +256) the tile's 128 bias values
-    uint8_t* ctl = sx + a.kt_per * C::kX;
+    uint8_t* ctl = reinterpret_cast<uint8_t*>(recv) + C::rbytes(S);
     uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
     uint64_t* done = full + kWsMaxKt;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
@@ -135,18 +137,27 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
             *reinterpret_cast<float4*>(bias_s + r) = b;
         }
     }
-    // TMEM (lane = weight row, column = token) -> staging tile [TT][128] fp32 in the (now idle) weight region.
+    // TMEM (lane = weight row, column = token) -> PUSHED into the receive region of the CTA of the cluster that owns
+    // the row's split-K sum: recv[my split][token][row - owner's first row] (st.shared::cluster; the own CTA too).
+    // The receive region is nobody's operand memory, so a peer may push before this CTA's MMAs are done, and one
+    // cluster barrier orders every push before every reduction — no second barrier before exit (a pulling
+    // reduction needs one so that no CTA leaves while a peer still reads its shared memory).
     // Warp w reads TMEM lane quarter w mod 4 and every (w / 4)-th 32-column block.
-    float* st = reinterpret_cast<float*>(sw);
+    const uint32_t RO = C::rows_owned(S), rank = blockIdx.z;
     {
-        const uint32_t q4 = warp & 3u, r = q4 * 32 + lane;
+        const uint32_t q4 = warp & 3u, r = q4 * 32 + lane, zown = r / RO, rl = r - zown * RO;
+        uint32_t dst;  // element (src = rank, token 0, row rl) in the owner's receive region
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(recv + (rank * TT) * RO + rl)), "r"(zown));
+        auto push = [&](uint32_t c, uint32_t v) {
+            asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(dst + c * RO * 4u), "r"(v) : "memory");
+        };
         if constexpr (TT >= 32) {
 #pragma unroll 1
             for (int c0 = 32 * (int)(warp >> 2); c0 < TT; c0 += 32 * (kWsThreads / 128)) {
                 uint32_t v[32];
                 tmem_ld32(tmem + ((q4 * 32u) << 16) + (uint32_t)c0, v);
 #pragma unroll
-                for (int c = 0; c < 32; ++c) st[(c0 + c) * 128 + r] = __uint_as_float(v[c]);
+                for (int c = 0; c < 32; ++c) push((uint32_t)(c0 + c), v[c]);
             }
         } else if (warp < 4) {
             uint32_t v[16];
@@ -156,20 +167,19 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
                          : "r"(tmem + ((q4 * 32u) << 16)));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int c = 0; c < 16; ++c) st[c * 128 + r] = __uint_as_float(v[c]);
+            for (int c = 0; c < 16; ++c) push((uint32_t)c, v[c]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 11, globaltimer());
-    const uint32_t S = gridDim.z;
-    if (S > 1) cluster_sync();  // every split's staging tile is complete (release / acquire over the cluster)
+    if (S > 1) cluster_sync();  // every split's pushes have landed (release / acquire over the cluster)
     else __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols) : "memory");
     pdl_wait();  // residual in / output out: only after the predecessor
     if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 7, globaltimer());
 
     // reduction (split order) + epilogue over this CTA's weight-row quads x the tile's tokens
-    const uint32_t per = (32 + S - 1) / S, q0 = min(32u, blockIdx.z * per), nq = min(32u, q0 + per) - q0;
+    const uint32_t q0 = min(32u, rank * (RO / 4)), nq = min(32u, q0 + RO / 4) - q0;
     const uint32_t units = nq * TT;
     const float* __restrict__ resf = a.res && !a.res_bf16 ? reinterpret_cast<const float*>(a.res) : nullptr;
     const uint16_t* __restrict__ resh = a.res && a.res_bf16 ? reinterpret_cast<const uint16_t*>(a.res) : nullptr;
@@ -184,30 +194,15 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
             rr[e] = make_uint4(0, 0, 0, 0);
             if (u >= units) continue;
             const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
-            const float* src = st + tok * 128 + 4 * q;
-            if (S > 1) {
-                // splits in order, 8 loads in flight at a time (clusters of up to 16: non-portable sizes)
-                acc[e] = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (uint32_t z0 = 0; z0 < S; z0 += 8) {
-                    float4 v[8];
-#pragma unroll
-                    for (uint32_t z = 0; z < 8; ++z)
-                        if (z0 + z < S) v[z] = ld_dsmem_f4(src, z0 + z);
-#pragma unroll
-                    for (uint32_t z = 0; z < 8; ++z) {
-                        if (z0 + z >= S) break;
-                        if (z0 + z == 0) {
-                            acc[e] = v[0];
-                            continue;
-                        }
-                        acc[e].x += v[z].x;
-                        acc[e].y += v[z].y;
-                        acc[e].z += v[z].z;
-                        acc[e].w += v[z].w;
-                    }
-                }
-            } else {
-                acc[e] = *reinterpret_cast<const float4*>(src);
+            // splits in order (deterministic): recv[z][tok][4 (q - q0) .. + 3]
+            const float* src = recv + tok * RO + 4 * (q - q0);
+            acc[e] = *reinterpret_cast<const float4*>(src);
+            for (uint32_t z = 1; z < S; ++z) {
+                const float4 v = *reinterpret_cast<const float4*>(src + z * TT * RO);
+                acc[e].x += v.x;
+                acc[e].y += v.y;
+                acc[e].z += v.z;
+                acc[e].w += v.w;
             }
             if (t < a.M && n < a.N) {
                 const uint64_t ri = (uint64_t)t * a.ld_res + n;
@@ -242,15 +237,13 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         }
     }
     if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 9, globaltimer());
-    if (S > 1) cluster_sync();  // no CTA leaves while a peer may still read its staging tile
-    if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 10, globaltimer());
 }
 
 template <int TT>
 static void launch_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a) {
     using C = WsCfg<TT>;
     const dim3 grid((a.n_pad + 127) / 128, (a.M + TT - 1) / TT, a.splits);
-    launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT>, grid, dim3(kWsThreads), C::smem(a.kt_per), s, dim3(1, 1, a.splits), *tmX, d, w, a);
+    launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits), s, dim3(1, 1, a.splits), *tmX, d, w, a);
 }
 
 void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a) {
@@ -262,12 +255,12 @@ void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap*
     }
 }
 
-uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per) {
+uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per, uint32_t splits) {
     switch (tt) {
-        case 16: return WsCfg<16>::smem(kt_per);
-        case 32: return WsCfg<32>::smem(kt_per);
-        case 64: return WsCfg<64>::smem(kt_per);
-        default: return WsCfg<128>::smem(kt_per);
+        case 16: return WsCfg<16>::smem(kt_per, splits);
+        case 32: return WsCfg<32>::smem(kt_per, splits);
+        case 64: return WsCfg<64>::smem(kt_per, splits);
+        default: return WsCfg<128>::smem(kt_per, splits);
     }
 }
 
@@ -276,7 +269,7 @@ static int ws_max_clusters(uint32_t kt_per, int cz) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(1, 1, cz);
     cfg.blockDim = dim3(kWsThreads);
-    cfg.dynamicSmemBytes = WsCfg<TT>::smem(kt_per);
+    cfg.dynamicSmemBytes = WsCfg<TT>::smem(kt_per, (uint32_t)cz);
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 1;

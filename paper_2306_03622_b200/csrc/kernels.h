@@ -240,7 +240,7 @@ void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tm
                  const CUtensorMap* tmW = nullptr);
 bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes);
 void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a);
-uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per);                  // dynamic shared memory of one CTA
+uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per, uint32_t splits);  // dynamic shared memory of one CTA
 int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz);  // clusters resident at once (this device)
 void init_gemm_ws_attrs();
 
