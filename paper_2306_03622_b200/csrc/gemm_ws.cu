@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
     // The receive region is nobody's operand memory, so a peer may push before this CTA's MMAs are done, and one
     // cluster barrier orders every push before every reduction — no second barrier before exit (a pulling
     // reduction needs one so that no CTA leaves while a peer still reads its shared memory).
-    // Warp w reads TMEM lane quarter w mod 4 and every (w / 4)-th 32-column block.
+    // Warp w reads TMEM lane quarter w mod 4 and every (w / 4)-th 16-column block.
     const uint32_t RO = C::rows_owned(S), rank = blockIdx.z;
     {
         const uint32_t q4 = warp & 3u, r = q4 * 32 + lane, zown = r / RO, rl = r - zown * RO;
@@ -151,23 +151,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         auto push = [&](uint32_t c, uint32_t v) {
             asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(dst + c * RO * 4u), "r"(v) : "memory");
         };
-        if constexpr (TT >= 32) {
+        // 16-column chunks dealt over the 4 warp groups: for TT >= 64 every warp pushes (32-column chunks left half
+        // the warps idle at TT = 64 and the push was the epilogue's longest phase)
 #pragma unroll 1
-            for (int c0 = 32 * (int)(warp >> 2); c0 < TT; c0 += 32 * (kWsThreads / 128)) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((q4 * 32u) << 16) + (uint32_t)c0, v);
-#pragma unroll
-                for (int c = 0; c < 32; ++c) push((uint32_t)(c0 + c), v[c]);
-            }
-        } else if (warp < 4) {
+        for (int c0 = 16 * (int)(warp >> 2); c0 < TT; c0 += 16 * (kWsThreads / 128)) {
             uint32_t v[16];
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
                            "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                         : "r"(tmem + ((q4 * 32u) << 16)));
+                         : "r"(tmem + ((q4 * 32u) << 16) + (uint32_t)c0));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int c = 0; c < 16; ++c) push((uint32_t)c, v[c]);
+            for (int c = 0; c < 16; ++c) push((uint32_t)(c0 + c), v[c]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -578,7 +578,7 @@ extern "C" fsw_status fsw_invoke_ex(fsw_ctx* c, uint32_t id, const fsw_invoke_op
         stats->gpu = gi;
         stats->n_sources = cold ? (striped ? (uint32_t)srcs.size() : 1) : 0;
         stats->swap_kind = cold ? (striped ? FSW_SWAP_STRIPED : peer >= 0 ? FSW_SWAP_PEER : FSW_SWAP_HOST) : FSW_SWAP_RESIDENT;
-        stats->n_kernels = (uint32_t)p.launches.size() + 1 /*finish*/;
+        stats->n_kernels = (p.mega.on ? 1u : (uint32_t)p.launches.size()) + 1 /*finish*/;  // k_mega: one launch
         if (cold) {
             float swap_ms = 0;
             cudaEventElapsedTime(&swap_ms, g.evs0, g.evs1);

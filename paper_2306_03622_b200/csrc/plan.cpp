@@ -443,7 +443,9 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     }
                     // Weight-stationary swap-AB GEMM (k_gemm_ws) for the narrow batch-1 linears (choose_ws_tiling);
                     // FSW_GEMM_WS=0 turns it off, =2 allows it for every width (A/B hooks)
-                    static const int ws_mode = getenv("FSW_GEMM_WS") ? atoi(getenv("FSW_GEMM_WS")) : 1;
+                    // (off under FSW_MEGA=1: the persistent kernel takes its GEMMs from the k_gemm plan)
+                    static const int ws_mode = getenv("FSW_MEGA") && atoi(getenv("FSW_MEGA")) == 1 ? 0
+                                               : getenv("FSW_GEMM_WS") ? atoi(getenv("FSW_GEMM_WS")) : 1;
                     WsTiling wt{0, 0, 0, false};
                     if (ws_mode && !pt && a.N % 4 == 0) wt = choose_ws_tiling(a.M, a.n_pad, a.K / 64, ws_mode == 2);
                     if (wt.ok) {

@@ -31,7 +31,9 @@ CHILD = textwrap.dedent("""
                 r = rt.invoke(mid, x, gpu=0, engine=eng)
                 assert np.array_equal(rt.read_resident(mid, 0), rt.read_store(mid)), (name, eng)
                 outs.append(r.output.copy())
-            warm = rt.invoke(mid, x, gpu=0).output
+            rw = rt.invoke(mid, x, gpu=0)
+            warm = rw.output
+            assert rw.stats["n_kernels"] <= 4, ("the persistent kernel did not run", rw.stats["n_kernels"])
             for o in outs:
                 assert np.array_equal(o, warm), name
             err = rel_err(warm, ref)
