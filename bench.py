@@ -556,11 +556,7 @@ def run_fsw(args):
             spec_tn = importlib.util.spec_from_file_location("torch_native", os.path.join(ROOT, "tools", "torch_native.py"))
             tn = importlib.util.module_from_spec(spec_tn)
             spec_tn.loader.exec_module(tn)
-            sys_argv, sys.argv = sys.argv, ["torch_native", "bert-base", "resnet50", "gpt2-xl"]
-            try:
-                native = tn.main()
-            finally:
-                sys.argv = sys_argv
+            native = tn.main(["bert-base", "resnet50", "gpt2-xl"], verbose=False)
             torch.cuda.empty_cache()
         except Exception as e:
             native = {"error": repr(e)}

@@ -102,10 +102,12 @@ def timed(fn_a, fn_b, reps):
     return t[len(t) // 2]
 
 
-def main():
+def main(names=None, verbose=True):
+    """{model: median replay ms}; prints a line per model when verbose (bench.py calls it quietly: its stdout is
+    the one JSON line)."""
     dev = "cuda"
     torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = True
-    names = sys.argv[1:] or ["bert-base", "resnet50", "gpt2-xl"]
+    names = names or sys.argv[1:] or ["bert-base", "resnet50", "gpt2-xl"]
     out = {}
     with torch.inference_mode():
         for name in names:
@@ -122,7 +124,8 @@ def main():
                 x = torch.randn(1, 3, 224, 224, device=dev).to(torch.bfloat16).to(memory_format=torch.channels_last)
                 t = timed(lambda: ma(x), lambda: mb(x), 100)
             out[name] = round(t, 4)
-            print(f"torch bf16 native (CUDA graph, weights from HBM) {name}: {t:.4f} ms", flush=True)
+            if verbose:
+                print(f"torch bf16 native (CUDA graph, weights from HBM) {name}: {t:.4f} ms", flush=True)
     return out
 
 
