@@ -20,7 +20,7 @@ SO = os.path.join(PKG, "libfsw.so")
 SO_TRACE = os.path.join(PKG, "libfsw_trace.so")
 BUILD = os.path.join(PKG, "_build")
 
-CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu", "gemm_ws.cu", "mega.cu"]
+CU_SOURCES = ["swap.cu", "ops.cu", "gemm_tc.cu", "gemm_ws.cu", "attn_tc.cu", "mega.cu"]
 CXX_SOURCES = ["runtime.cpp", "store.cpp", "plan.cpp", "graph.cpp", "invoke.cpp", "sched.cpp", "litmus.cpp"]
 HEADERS = ["kernels.h", "device.cuh", "policy.h", "rt_internal.h", "umma.cuh", "attn_core.cuh"]
 

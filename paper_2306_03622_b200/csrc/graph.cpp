@@ -418,7 +418,8 @@ static fsw_status enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic,
                 AttnArgs a = x.attn;
                 a.layer = x.layer;
                 a.trace = g.trace;
-                launch_attention(s, a);
+                if (x.attn_tc) launch_attention_tc(s, &x.tmap, a);
+                else launch_attention(s, a);
                 break;
             }
             case K_IM2COL: {

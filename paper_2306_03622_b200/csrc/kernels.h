@@ -246,6 +246,10 @@ void init_gemm_ws_attrs();
 
 struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; int32_t layer; unsigned long long* trace; };
 void launch_attention(cudaStream_t s, const AttnArgs& a);
+// tcgen05 attention (attn_tc.cu): T <= 128, dh = 64; tm = TMA map over the QKV activation [T][3·H·64], 64 x 128 boxes
+bool attention_tc_ok(const AttnArgs& a);
+void launch_attention_tc(cudaStream_t s, const CUtensorMap* tm, const AttnArgs& a);
+void init_attn_tc_attrs();
 
 struct Im2colArgs {
     const uint16_t* in; uint32_t H, W, C;

@@ -483,6 +483,14 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                 x.kind = K_ATTN;
                 x.attn = {reinterpret_cast<const uint16_t*>(sptr(L.in0)), reinterpret_cast<uint16_t*>(sptr(L.out)),
                           si.shape[0], (uint32_t)L.attr[0], (uint32_t)L.attr[1], L.attr[2]};
+                // tcgen05 attention for T <= 128, head width 64 (FSW_ATTN_TC: 1 on, 0 off)
+                static const int attn_tc = getenv("FSW_ATTN_TC") ? atoi(getenv("FSW_ATTN_TC")) : 0;
+                if (attn_tc && attention_tc_ok(x.attn)) {
+                    const uint64_t cols = 3ull * x.attn.H * x.attn.dh;
+                    if (!make_tmap_act(&x.tmap, x.attn.qkv, x.attn.T, cols, cols, 128))
+                        return fail(FSW_ECUDA, "plan: cuTensorMapEncodeTiled failed (attention, layer %u)", li);
+                    x.attn_tc = true;
+                }
                 break;
             }
             case FSW_OP_CONV2D: {

@@ -107,6 +107,7 @@ static fsw_status init_gpu(fsw_ctx* c, Gpu& g) {
     CU(cudaFree(nullptr));  // create the context now (one shared runtime per GPU)
     init_gemm_attrs();
     init_gemm_ws_attrs();
+    init_attn_tc_attrs();
     init_mega_attrs();
     init_ops_attrs();
     init_swap_attrs();
