@@ -113,7 +113,8 @@ typedef struct {
  *        group a stream memory write (no SM) bumps that stream's group counter.               */
 enum { FSW_ENGINE_AUTO = 0, FSW_ENGINE_SM = 1, FSW_ENGINE_DMA = 2, FSW_ENGINE_SMZ = 3, FSW_ENGINE_DMAZ = 4, FSW_ENGINE_DMAZT = 5 };
 /* Link-coded engines (models registered with FSW_REG_LINK_CODE).  The host link carries
- * the model's exponent-coded store (lossless, 0.68 of the bytes with format v4 on the synthetic weights) and a kernel decodes it into the
+ * the model's exponent-coded store (lossless; on the synthetic weights 0.68 of the bytes with the per-block codes, 0.66 with
+ * the entropy-coded pieces of stores >= 32 MiB, see fsw_debug_coded_code) and a kernel decodes it into the
  * extent, releasing each decoded piece's bytes on its layer's counter (the SM protocol):
  *   SMZ : persistent CTAs stream coded pieces zero-copy from the mapped coded store with TMA bulk copies
  *         into a shared-memory ring and decode them from there;
@@ -174,7 +175,9 @@ typedef struct { uint32_t op, first_ref, n_refs; int32_t in0, in1, out; int32_t 
 #define FSW_REG_LINK_CODE 0x2u /* also build the exponent-coded copy of the store (pinned, mapped) that
                                   the SMZ / DMAZ engines move over the host link (format
                                   at fsw_coded_piece below).  Lossless: the extent receives the store's
-                                  bytes bit-exactly.  Costs ~0.68x the store in extra host memory.  */
+                                  bytes bit-exactly.  Costs ~0.66-0.68x the store in extra host memory;
+                                  entropy-coded pieces (format v5) are built for stores >= 32 MiB
+                                  (environment FSW_LINK_HUFF=0 / 1: never / always).             */
 
 typedef struct {
     const char* name;
