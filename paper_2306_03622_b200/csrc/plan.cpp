@@ -93,12 +93,19 @@ static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool a
             // cold invoke (measured: GPT-2-XL's attention projection at 128:7, 204 KB, took the cold invoke from 37.6
             // to 40.2 ms)
             if (smem > 184 * 1024) continue;
+            // one-wave capacity per (tt, kt_per, s), queried once; plans of different GPUs are built concurrently
+            static std::mutex cap_mu;
             static std::map<uint64_t, int> cap_cache;
             const uint64_t key = ((uint64_t)tt << 40) | ((uint64_t)kp << 20) | s;
-            auto it = cap_cache.find(key);
-            if (it == cap_cache.end())
-                it = cap_cache.emplace(key, s > 1 ? gemm_ws_max_active_clusters(tt, kp, (int)s) * (int)s : 148).first;
-            if (ctas > (uint64_t)std::min(it->second, 148)) continue;
+            int cap;
+            {
+                std::lock_guard<std::mutex> lk(cap_mu);
+                auto it = cap_cache.find(key);
+                if (it == cap_cache.end())
+                    it = cap_cache.emplace(key, s > 1 ? gemm_ws_max_active_clusters(tt, kp, (int)s) * (int)s : 148).first;
+                cap = it->second;
+            }
+            if (ctas > (uint64_t)std::min(cap, 148)) continue;
             const double t = 0.3 * (tt / 16.0) + 0.4 * (s - 1) + 0.1 * kp + (smem > 150 * 1024 ? 2.0 : 0.0) + (ctas > 120 ? 2.0 : 0.0);
             if (t < best_t - 1e-9) {
                 best_t = t;
