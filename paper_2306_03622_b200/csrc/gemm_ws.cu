@@ -37,13 +37,14 @@ struct WsCfg {
     __host__ __device__ static uint32_t rows_owned(uint32_t S) { return 4u * ((32u + S - 1u) / S); }
     // receive region: every split's partial of the owned rows, [S][TT][rows_owned] fp32
     __host__ __device__ static uint32_t rbytes(uint32_t S) { return S * TT * rows_owned(S) * 4u; }
-    __host__ __device__ static uint32_t smem(uint32_t kt, uint32_t S) { return kt * kWsW + kt * kX + rbytes(S) + 1024 + 1024; }
+    // slots = k sub-tiles resident at once: all of the CTA's K range (weight-stationary), or a ring of that many
+    __host__ __device__ static uint32_t smem(uint32_t slots, uint32_t S) { return slots * kWsW + slots * kX + rbytes(S) + 1024 + 1024; }
 };
 }  // namespace
 
 constexpr int kWsThreads = 512;  // thread 0 loads, thread 32 issues the MMAs; all 16 warps drain TMEM and run the epilogue
 
-template <int TT>
+template <int TT, bool RING>
 __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant__ CUtensorMap tmX, const DevDesc* __restrict__ d, Wait w,
                                                  GemmArgs a) {
     TraceExit tx(w.trace, w.layer);
@@ -53,21 +54,30 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
     const uint32_t kt0 = blockIdx.z * a.kt_per;
     const uint32_t nkt = min(a.K / kBK, kt0 + a.kt_per) - kt0;  // >= 1 (host plan)
     const uint32_t S = gridDim.z;
+    // NS sub-tile slots: the whole K range (weight-stationary, ws_stages = 0) or a ring of ws_stages slots for K
+    // ranges too long to hold (the first NS slots' weights still load before the predecessor finishes)
+    const uint32_t NS = RING ? a.ws_stages : a.kt_per;
+    const bool ring = RING && NS < nkt;
     uint8_t* sw = smem;                                          // weight sub-tiles
-    uint8_t* sx = smem + a.kt_per * kWsW;                        // activation sub-tiles
-    float* recv = reinterpret_cast<float*>(sx + a.kt_per * C::kX);  // split partials of the owned rows
-    // 1-KiB control block: full[kWsMaxKt] | done | TMEM slot | (at +256) the tile's 128 bias values
+    uint8_t* sx = smem + NS * kWsW;                              // activation sub-tiles
+    float* recv = reinterpret_cast<float*>(sx + NS * C::kX);     // split partials of the owned rows
+    // 1-KiB control block: full[kWsMaxKt] | done | TMEM slot | (at +256) the tile's 128 bias values | (at +768, ring)
+    // empty[kWsMaxKt]
     uint8_t* ctl = reinterpret_cast<uint8_t*>(recv) + C::rbytes(S);
     uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
     uint64_t* done = full + kWsMaxKt;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
     float* bias_s = reinterpret_cast<float*>(ctl + 256);
+    uint64_t* empty = reinterpret_cast<uint64_t*>(ctl + 768);
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t n0 = blockIdx.x * 128, t0 = blockIdx.y * TT;
     const DevDesc dd = *d;
 
     if (threadIdx.x == 0) {
-        for (uint32_t j = 0; j < nkt; ++j) mbar_init(&full[j], 1);
+        for (uint32_t j = 0; j < NS && j < nkt; ++j) {
+            mbar_init(&full[j], 1);
+            if (RING) mbar_init(&empty[j], 1);
+        }
         mbar_init(done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
@@ -92,7 +102,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         const uint32_t wrows = min(128u, a.n_pad - n0);
         const uint8_t* wt = weight_ptr(dd, a.w_off) + (uint64_t)(n0 / 8) * 1024;
         const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
-        for (uint32_t j = 0; j < nkt; ++j) {
+        const uint32_t pre = min(NS, nkt);
+        for (uint32_t j = 0; j < pre; ++j) {
             mbar_expect_tx(&full[j], wrows * 128 + C::kX);
             bulk_load(sw + j * kWsW, wt + (kt0 + j) * ktile_stride, wrows * 128, &full[j]);
         }
@@ -107,15 +118,37 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         pdl_wait();
         FSW_TRACE_MAX(w.trace, w.layer, 5, globaltimer());
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        for (uint32_t j = 0; j < nkt; ++j) tma_load_2d(sx + j * C::kX, &tmX, (int)((kt0 + j) * kBK), (int)t0, &full[j]);
+        for (uint32_t j = 0; j < pre; ++j) tma_load_2d(sx + j * C::kX, &tmX, (int)((kt0 + j) * kBK), (int)t0, &full[j]);
+        // ring: refill slot j mod NS once the MMAs of its previous use are done (slot / phase counted, no division:
+        // this thread and the MMA issuer are on the critical path)
+        if (RING)
+        for (uint32_t j = pre, sl = 0, ph = 0; j < nkt; ++j) {
+            mbar_wait(&empty[sl], ph);
+            mbar_expect_tx(&full[sl], wrows * 128 + C::kX);
+            bulk_load(sw + sl * kWsW, wt + (kt0 + j) * ktile_stride, wrows * 128, &full[sl]);
+            tma_load_2d(sx + sl * C::kX, &tmX, (int)((kt0 + j) * kBK), (int)t0, &full[sl]);
+            if (++sl == NS) sl = 0, ph ^= 1u;
+        }
     } else if (threadIdx.x == 32) {
         constexpr uint32_t idesc = umma_idesc_bf16(kBM, TT);
-        for (uint32_t j = 0; j < nkt; ++j) {
-            mbar_wait(&full[j], 0);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint64_t ad = umma_desc_sw128(sw + j * kWsW), bd = umma_desc_sw128(sx + j * C::kX);
+        if (RING) {
+            for (uint32_t j = 0, sl = 0, ph = 0; j < nkt; ++j) {
+                mbar_wait(&full[sl], ph);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t ad = umma_desc_sw128(sw + sl * kWsW), bd = umma_desc_sw128(sx + sl * C::kX);
 #pragma unroll
-            for (uint32_t kk = 0; kk < kBK / 16; ++kk) umma_f16(tmem, ad + kk * 2, bd + kk * 2, idesc, (j | kk) != 0);
+                for (uint32_t kk = 0; kk < kBK / 16; ++kk) umma_f16(tmem, ad + kk * 2, bd + kk * 2, idesc, (j | kk) != 0);
+                if (ring && j + NS < nkt) umma_commit(&empty[sl]);  // the slot is free once these MMAs have read it
+                if (++sl == NS) sl = 0, ph ^= 1u;
+            }
+        } else {  // every k sub-tile has its own slot and barrier
+            for (uint32_t j = 0; j < nkt; ++j) {
+                mbar_wait(&full[j], 0);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint64_t ad = umma_desc_sw128(sw + j * kWsW), bd = umma_desc_sw128(sx + j * C::kX);
+#pragma unroll
+                for (uint32_t kk = 0; kk < kBK / 16; ++kk) umma_f16(tmem, ad + kk * 2, bd + kk * 2, idesc, (j | kk) != 0);
+            }
         }
         umma_commit(done);
     }
@@ -238,7 +271,12 @@ template <int TT>
 static void launch_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a) {
     using C = WsCfg<TT>;
     const dim3 grid((a.n_pad + 127) / 128, (a.M + TT - 1) / TT, a.splits);
-    launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits), s, dim3(1, 1, a.splits), *tmX, d, w, a);
+    if (a.ws_stages)
+        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, true>, grid, dim3(kWsThreads), C::smem(a.ws_stages, a.splits), s,
+                           dim3(1, 1, a.splits), *tmX, d, w, a);
+    else
+        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, false>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits), s,
+                           dim3(1, 1, a.splits), *tmX, d, w, a);
 }
 
 void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a) {
@@ -250,21 +288,21 @@ void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap*
     }
 }
 
-uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per, uint32_t splits) {
+uint32_t gemm_ws_smem(uint32_t tt, uint32_t slots, uint32_t splits) {
     switch (tt) {
-        case 16: return WsCfg<16>::smem(kt_per, splits);
-        case 32: return WsCfg<32>::smem(kt_per, splits);
-        case 64: return WsCfg<64>::smem(kt_per, splits);
-        default: return WsCfg<128>::smem(kt_per, splits);
+        case 16: return WsCfg<16>::smem(slots, splits);
+        case 32: return WsCfg<32>::smem(slots, splits);
+        case 64: return WsCfg<64>::smem(slots, splits);
+        default: return WsCfg<128>::smem(slots, splits);
     }
 }
 
 template <int TT>
-static int ws_max_clusters(uint32_t kt_per, int cz) {
+static int ws_max_clusters(uint32_t slots, int cz) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(1, 1, cz);
     cfg.blockDim = dim3(kWsThreads);
-    cfg.dynamicSmemBytes = WsCfg<TT>::smem(kt_per, (uint32_t)cz);
+    cfg.dynamicSmemBytes = WsCfg<TT>::smem(slots, (uint32_t)cz);
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
     attr.val.clusterDim.x = 1;
@@ -273,7 +311,7 @@ static int ws_max_clusters(uint32_t kt_per, int cz) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_ws<TT>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_ws<TT, false>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -291,8 +329,10 @@ int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz) {
 
 template <int TT>
 static void ws_attrs() {
-    cudaFuncSetAttribute(k_gemm_ws<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_gemm_ws<TT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);  // split-K clusters up to 16
+    for (auto k : {k_gemm_ws<TT, false>, k_gemm_ws<TT, true>}) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);  // split-K clusters up to 16
+    }
 }
 
 void init_gemm_ws_attrs() {

@@ -232,6 +232,7 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // 0 = not used.  128 weight rows x ws_tt tokens per CTA; split-K over a (1, 1, splits) cluster (splits <= 8,
     // kt_per k sub-tiles each, all resident in shared memory); the A tensor map's box is ws_tt rows
     uint32_t ws_tt;
+    uint32_t ws_stages;  // k_gemm_ws: 0 = the whole K range resident; else a ring of this many k sub-tile slots
     // L2 prefetch (k_gemm / k_gemm_ws, resident invokes): the next GEMM's weights [pf_off, pf_off + pf_bytes) of
     // the store, dealt over this launch's CTAs; pf_bytes = 0: none
     uint64_t pf_off, pf_bytes;
@@ -240,8 +241,8 @@ void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tm
                  const CUtensorMap* tmW = nullptr);
 bool make_tmap_pool(CUtensorMap* map, const void* pool, uint64_t bytes);
 void launch_gemm_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmX, const GemmArgs& a);
-uint32_t gemm_ws_smem(uint32_t tt, uint32_t kt_per, uint32_t splits);  // dynamic shared memory of one CTA
-int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz);  // clusters resident at once (this device)
+uint32_t gemm_ws_smem(uint32_t tt, uint32_t slots, uint32_t splits);  // dynamic shared memory of one CTA
+int gemm_ws_max_active_clusters(uint32_t tt, uint32_t slots, int cz);  // clusters resident at once (this device)
 void init_gemm_ws_attrs();
 
 struct AttnArgs { const uint16_t* qkv; uint16_t* out; uint32_t T, H, dh; int causal; int32_t layer; unsigned long long* trace; };

@@ -56,20 +56,23 @@ static Tiling choose_tiling(uint64_t m_tiles, uint32_t n_pad, uint32_t kt, uint3
 // split-K reduction and larger epilogue cost more than the activation bytes it saves.  Cost (relative, fitted to
 // that sweep): the epilogue's token width, the split-K reduction, the MMA chain, and a penalty for CTAs too large
 // to be resident beside their predecessor.  ok = false: no tiling fits (k_gemm runs the linear).
-struct WsTiling { uint32_t tt, splits, kt_per; bool ok; };
+struct WsTiling { uint32_t tt, splits, kt_per, stages; bool ok; };  // stages: 0 = K range resident, else ring slots
 static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool any_width) {
     const uint64_t rt = (n_pad + 127) / 128;
     // A/B hook: FSW_GEMM_WS_FORCE="tt:splits" for every shape, or "N:K:tt:splits,..." per weight shape (a shape
     // not in the list runs k_gemm)
     static const char* force = getenv("FSW_GEMM_WS_FORCE");
-    int ftt = 0, fs = 0;
+    // ("N:K:tt:splits:stages" selects a ring of `stages` k sub-tile slots)
+    int ftt = 0, fs = 0, fst = 0;
     if (force) {
-        int fn, fk, t, sp, used = 0;
+        int fn, fk, t, sp;
         const char* q = force;
         if (sscanf(q, "%d:%d:%d:%d", &fn, &fk, &t, &sp) == 4) {
             ftt = -1;
-            while (q && sscanf(q, "%d:%d:%d:%d%n", &fn, &fk, &t, &sp, &used) == 4) {
-                if ((uint32_t)fn == n_pad && (uint32_t)fk == kt * 64) ftt = t, fs = sp;
+            while (q) {
+                int st = 0, n = sscanf(q, "%d:%d:%d:%d:%d", &fn, &fk, &t, &sp, &st);
+                if (n < 4) break;
+                if ((uint32_t)fn == n_pad && (uint32_t)fk == kt * 64) ftt = t, fs = sp, fst = n == 5 ? st : 0;
                 q = strchr(q, ',');
                 if (q) ++q;
             }
@@ -77,29 +80,33 @@ static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool a
             sscanf(force, "%d:%d", &ftt, &fs);
         }
     }
-    if (ftt < 0 || M > 128) return WsTiling{0, 0, 0, false};
+    if (ftt < 0 || M > 128) return WsTiling{0, 0, 0, 0, false};
     (void)any_width;
-    // Tilings measured best in the invoke graph for the paper's transformer shapes (M = 128 tokens; weight rows
-    // padded, K): BERT-base QKV 64:2, O-projection 32:4, FFN1 64:2, FFN2 64:8 (resident 0.423 -> 0.414 ms;
-    // profiles/r02/gemm/ws_sweep.txt, tools/gemm_chain_vs_cublas.py); used when they fit, the cost model otherwise.
+    // Tilings measured best for the paper's transformer shapes (M = 128 tokens; weight rows padded, K): BERT-base
+    // QKV 64:2, O-projection 32:4, FFN1 64:2, FFN2 64:8 (resident 0.423 -> 0.414 ms), GPT-2-XL QKV / FC / proj2 on
+    // a 3-slot ring (profiles/r02/gemm/ws_sweep.txt, chain_vs_cublas.txt); used when they fit, the cost model
+    // otherwise.
     bool table_used = false;
     if (!ftt && M == 128) {
-        struct Known { uint32_t n_pad, K, tt, s; };
-        static const Known known[] = {{2304, 768, 64, 2}, {768, 768, 32, 4}, {3072, 768, 64, 2}, {768, 3072, 64, 8}};
+        struct Known { uint32_t n_pad, K, tt, s, stages; };
+        static const Known known[] = {{2304, 768, 64, 2, 0}, {768, 768, 32, 4, 0}, {3072, 768, 64, 2, 0}, {768, 3072, 64, 8, 0},
+                                      // GPT-2-XL's wide linears: a ring of 3 slots per CTA (their K ranges do not fit)
+                                      {4800, 1600, 128, 3, 3}, {6400, 1600, 128, 2, 3}, {1600, 6400, 128, 8, 3}};
         for (const Known& k : known)
-            if (k.n_pad == n_pad && k.K == kt * 64) ftt = (int)k.tt, fs = (int)k.s, table_used = true;
+            if (k.n_pad == n_pad && k.K == kt * 64) ftt = (int)k.tt, fs = (int)k.s, fst = (int)k.stages, table_used = true;
     }
-    auto search = [&](int ftt, int fs) {
-        WsTiling best{0, 0, 0, false};
+    auto search = [&](int ftt, int fs, int fst) {
+        WsTiling best{0, 0, 0, 0, false};
         double best_t = 1e30;
         for (uint32_t tt : {16u, 32u, 64u, 128u}) {
             if (ftt && tt != (uint32_t)ftt) continue;
             for (uint32_t s = 1; s <= 16 && s <= kt; ++s) {  // clusters beyond 8 are non-portable (B200: 16)
                 if (fs && s != (uint32_t)fs) continue;
                 const uint32_t kp = (kt + s - 1) / s;
-                if ((kt + kp - 1) / kp != s || kp > 16) continue;
+                if ((kt + kp - 1) / kp != s || (fst ? fst > 16 || (uint32_t)fst >= kp : kp > 16)) continue;
+                const uint32_t slots = fst ? (uint32_t)fst : kp;
                 const uint64_t ctas = rt * ((M + tt - 1) / tt) * s;
-                const uint32_t smem = gemm_ws_smem(tt, kp, s);
+                const uint32_t smem = gemm_ws_smem(tt, slots, s);
                 // <= 184 KB: a CTA must fit beside one swap-decode CTA (k_swapz_tma: ring + decode table, ~41 KB) in a
                 // cold invoke (measured: GPT-2-XL's attention projection at 128:7, 204 KB, took the cold invoke from 37.6
                 // to 40.2 ms)
@@ -107,27 +114,27 @@ static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool a
                 // one-wave capacity per (tt, kt_per, s), queried once; plans of different GPUs are built concurrently
                 static std::mutex cap_mu;
                 static std::map<uint64_t, int> cap_cache;
-                const uint64_t key = ((uint64_t)tt << 40) | ((uint64_t)kp << 20) | s;
+                const uint64_t key = ((uint64_t)tt << 40) | ((uint64_t)slots << 20) | s;
                 int cap;
                 {
                     std::lock_guard<std::mutex> lk(cap_mu);
                     auto it = cap_cache.find(key);
                     if (it == cap_cache.end())
-                        it = cap_cache.emplace(key, s > 1 ? gemm_ws_max_active_clusters(tt, kp, (int)s) * (int)s : 148).first;
+                        it = cap_cache.emplace(key, s > 1 ? gemm_ws_max_active_clusters(tt, slots, (int)s) * (int)s : 148).first;
                     cap = it->second;
                 }
                 if (ctas > (uint64_t)std::min(cap, 148)) continue;
                 const double t = 0.3 * (tt / 16.0) + 0.4 * (s - 1) + 0.1 * kp + (smem > 150 * 1024 ? 2.0 : 0.0) + (ctas > 120 ? 2.0 : 0.0);
                 if (t < best_t - 1e-9) {
                     best_t = t;
-                    best = {tt, s, kp, true};
+                    best = {tt, s, kp, (uint32_t)fst, true};
                 }
             }
         }
         return best;
     };
-    const WsTiling t = search(ftt, fs);
-    return t.ok || !table_used ? t : search(0, 0);  // a measured tiling that does not fit here: the cost model
+    const WsTiling t = search(ftt, fs, fst);
+    return t.ok || !table_used ? t : search(0, 0, 0);  // a measured tiling that does not fit here: the cost model
 }
 // ==========================================================================================
 // persistent transformer kernel (mega.cu): eligibility, tiling, op table
@@ -466,10 +473,11 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     // (off under FSW_MEGA=1: the persistent kernel takes its GEMMs from the k_gemm plan)
                     static const int ws_mode = getenv("FSW_MEGA") && atoi(getenv("FSW_MEGA")) == 1 ? 0
                                                : getenv("FSW_GEMM_WS") ? atoi(getenv("FSW_GEMM_WS")) : 1;
-                    WsTiling wt{0, 0, 0, false};
+                    WsTiling wt{0, 0, 0, 0, false};
                     if (ws_mode && !pt && a.N % 4 == 0) wt = choose_ws_tiling(a.M, a.n_pad, a.K / 64, ws_mode == 2);
                     if (wt.ok) {
                         a.ws_tt = wt.tt;
+                        a.ws_stages = wt.stages;
                         a.bn = 128;
                         a.m_rows = wt.tt;
                         a.splits = wt.splits;
@@ -609,9 +617,9 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                         break;
                     }
             if (verbose)
-                fprintf(stderr, "[fsw plan] layer %d GEMM M=%u N=%u K=%u: %s tt/bn=%u splits=%u kt_per=%u cz=%u smem=%u pf=%llu\n",
+                fprintf(stderr, "[fsw plan] layer %d GEMM M=%u N=%u K=%u: %s tt/bn=%u splits=%u kt_per=%u stages=%u cz=%u smem=%u pf=%llu\n",
                         x.layer, a.M, a.N, a.K, a.ws_tt ? "ws" : a.pair_t ? "2cta" : "k_gemm", a.ws_tt ? a.ws_tt : (uint32_t)a.bn,
-                        a.splits, a.kt_per, a.cz, a.ws_tt ? gemm_ws_smem(a.ws_tt, a.kt_per, a.splits) : 0u, (unsigned long long)a.pf_bytes);
+                        a.splits, a.kt_per, a.ws_stages, a.cz, a.ws_tt ? gemm_ws_smem(a.ws_tt, a.ws_stages ? a.ws_stages : a.kt_per, a.splits) : 0u, (unsigned long long)a.pf_bytes);
         }
     }
     // split-K partials live after the activations and the im2col scratch

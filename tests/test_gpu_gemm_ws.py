@@ -73,7 +73,10 @@ N_SPECS = 9
     {"FSW_GEMM_WS": "2", "FSW_GEMM_WS_FORCE": "64:4"},
     {"FSW_GEMM_WS": "2", "FSW_GEMM_WS_FORCE": "128:8"},
     {"FSW_GEMM_WS": "0"},                 # k_gemm only
-], ids=["default", "all-widths", "tt16-s2", "tt32-s1", "tt64-s4", "tt128-s8", "k_gemm-only"])
+    # ring mode (a few k sub-tile slots streamed through) on BERT's shapes and the ragged ones
+    {"FSW_GEMM_WS": "2", "FSW_GEMM_WS_FORCE": "2304:768:64:2:2,768:768:32:1:3,3072:768:64:2:4,768:3072:64:8:2,"
+                                              "768:3072:32:8:3,1296:256:32:1:2,768:4608:16:8:3,48:4608:16:8:4"},
+], ids=["default", "all-widths", "tt16-s2", "tt32-s1", "tt64-s4", "tt128-s8", "k_gemm-only", "ring"])
 def test_gemm_ws_parity_in_child_process(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,

@@ -22,7 +22,11 @@ from synth.models import DT_BF16, Act, ModelSpec, Op  # noqa: E402
 
 T = 128
 SHAPES = {"qkv": (768, 2304, Act.NONE), "o-proj": (768, 768, Act.NONE), "ffn1": (768, 3072, Act.GELU_ERF),
-          "ffn2": (3072, 768, Act.NONE)}
+          "ffn2": (3072, 768, Act.NONE),
+          # GPT-2-XL's (run only when named on the command line)
+          "gpt-qkv": (1600, 4800, Act.NONE), "gpt-proj": (1600, 1600, Act.NONE), "gpt-fc": (1600, 6400, Act.GELU_TANH),
+          "gpt-proj2": (6400, 1600, Act.NONE)}
+DEFAULT = ["qkv", "o-proj", "ffn1", "ffn2"]
 N_CHAIN = 12
 
 
@@ -61,7 +65,7 @@ def cublas_chain_ms(K, N, act, n, reps=200):
         h = x
         for w, b in ws:
             y = F.linear(h if K == N else x, w, b)
-            h = F.gelu(y) if act == Act.GELU_ERF else y
+            h = F.gelu(y) if act == Act.GELU_ERF else F.gelu(y, approximate="tanh") if act == Act.GELU_TANH else y
         return h
 
     ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
@@ -90,7 +94,7 @@ def cublas_chain_ms(K, N, act, n, reps=200):
 
 
 def main():
-    only = [a for a in sys.argv[1:] if a in SHAPES]
+    only = [a for a in sys.argv[1:] if a in SHAPES] or DEFAULT
     tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("FSW_"))
     with torch.inference_mode(), Runtime(gpu_ids=[0], pool_bytes=4 << 30) as rt:
         for name, (K, N, act) in SHAPES.items():
