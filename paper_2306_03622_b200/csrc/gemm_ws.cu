@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tslot;
+    if (a.trig_early) pdl_trigger();
 
     if (threadIdx.x == 0) {
         // producer: the layer's weights (ordered by the ready counters), then — after the predecessor — the
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
     __syncwarp();
 
     mbar_wait(done, 0);
-    pdl_trigger();  // the successor's prologue and weight loads overlap this epilogue
+    if (!a.trig_early) pdl_trigger();  // the successor's prologue and weight loads overlap this epilogue
     if (threadIdx.x == 0) FSW_TRACE_MAX(w.trace, w.layer, 6, globaltimer());
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 3) {  // bias of the tile's 128 rows into shared memory (weights are ready: `done` follows the acquire)

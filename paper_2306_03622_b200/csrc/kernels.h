@@ -233,6 +233,7 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // kt_per k sub-tiles each, all resident in shared memory); the A tensor map's box is ws_tt rows
     uint32_t ws_tt;
     uint32_t ws_stages;  // k_gemm_ws: 0 = the whole K range resident; else a ring of this many k sub-tile slots
+    uint32_t trig_early;  // k_gemm_ws: 1 = release the successor's launch (PDL) at entry instead of after the MMAs
     // L2 prefetch (k_gemm / k_gemm_ws, resident invokes): the next GEMM's weights [pf_off, pf_off + pf_bytes) of
     // the store, dealt over this launch's CTAs; pf_bytes = 0: none
     uint64_t pf_off, pf_bytes;

@@ -603,6 +603,7 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
         // default on: resident BERT-base 0.476 -> 0.472 ms, GPT-2-XL 2.730 -> 2.682 ms (profiles/r02/gemm/ws_sweep.txt)
         static const bool pf = !(getenv("FSW_GEMM_PF") && atoi(getenv("FSW_GEMM_PF")) == 0);
         static const bool verbose = getenv("FSW_PLAN_VERBOSE") && atoi(getenv("FSW_PLAN_VERBOSE")) == 1;
+        static const int ws_trig = getenv("FSW_WS_TRIGGER") ? atoi(getenv("FSW_WS_TRIGGER")) : 0;
         for (size_t i = 0; i < p->launches.size(); ++i) {
             Launch& x = p->launches[i];
             if (x.kind != K_GEMM) continue;
@@ -616,6 +617,12 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                         a.pf_bytes = (uint64_t)b.K * b.n_pad * 2;
                         break;
                     }
+            // early PDL release (A/B hook FSW_WS_TRIGGER: 0 = after the MMAs, 1 = at entry for every k_gemm_ws,
+            // 2 = at entry when the successor is not a GEMM)
+            if (a.ws_tt && ws_trig) {
+                const bool next_gemm = i + 1 < p->launches.size() && p->launches[i + 1].kind == K_GEMM;
+                a.trig_early = ws_trig == 1 || !next_gemm;
+            }
             if (verbose)
                 fprintf(stderr, "[fsw plan] layer %d GEMM M=%u N=%u K=%u: %s tt/bn=%u splits=%u kt_per=%u stages=%u cz=%u smem=%u pf=%llu\n",
                         x.layer, a.M, a.N, a.K, a.ws_tt ? "ws" : a.pair_t ? "2cta" : "k_gemm", a.ws_tt ? a.ws_tt : (uint32_t)a.bn,
