@@ -385,18 +385,14 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
     }
     __syncthreads();
     // thread 0: claim the next piece into ring slot b and start its bulk copy (pieces larger than a
-    // slot are decoded straight from host memory instead; no copy, the barrier is just arrived on)
-    auto issue = [&](uint32_t b) {
-        const uint32_t p = atomicAdd(&own->ticket, 1u);
-        slot[b] = p;
-        if (p >= n_pieces) return;
-        if (p == 0) own->t_first = globaltimer();
-        const ZPiece& pc = pieces[p];
+    // slot are decoded straight from host memory instead; no copy, the barrier is just arrived on).
+    // Staged (DMAZ): a claimed piece whose copy group has not landed yet is left PENDING — its copy starts
+    // when the decode loop reaches slot b — so the other slot's landed piece is decoded and released
+    // meanwhile.  (Waiting here held one landed piece per CTA until the NEXT copy group landed: ResNet-50's
+    // layer3.1 bytes sat 250 us behind a 14-MB group, profiles/r02/timeline/timeline_resnet50_dmaz_r2e.txt.)
+    uint32_t pend = 0;  // thread 0: bit b = slot b's claimed piece still waits for its copy group
+    auto start = [&](uint32_t b, const ZPiece& pc) {
         const uint32_t bb = smem_addr(&bar[b]);
-        if (STAGE) {
-            wait_geq(progress + 32 * (pc.grp >> 24), (pc.grp & 0xffffffu) + 1, own);
-            asm volatile("fence.proxy.async.global;" ::: "memory");  // the landed bytes, to the bulk copy
-        }
         if (pc.cbytes <= kZBuf) {
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(pc.cbytes) : "memory");
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -406,6 +402,21 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         } else {
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bb) : "memory");
         }
+    };
+    auto issue = [&](uint32_t b) {
+        const uint32_t p = atomicAdd(&own->ticket, 1u);
+        slot[b] = p;
+        if (p >= n_pieces) return;
+        if (p == 0) own->t_first = globaltimer();
+        const ZPiece& pc = pieces[p];
+        if (STAGE) {
+            if (ld_acquire_gpu(progress + 32 * (pc.grp >> 24)) < (pc.grp & 0xffffffu) + 1) {
+                pend |= 1u << b;
+                return;
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // the landed bytes, to the bulk copy
+        }
+        start(b, pc);
     };
     if (tid == 0) {
         // DMAZT tail (zero-copy, !STAGE with a start counter): the host link is the body's until its last group landed
@@ -418,6 +429,12 @@ __global__ void __launch_bounds__(128) k_swapz_tma(const uint8_t* __restrict__ s
         const uint32_t p = slot[b];
         if (p >= n_pieces) break;  // tickets grow with it: every later slot is past the end too
         const ZPiece pc = pieces[p];
+        if (STAGE && tid == 0 && (pend >> b & 1u)) {  // its copy group, then its bulk copy
+            wait_geq(progress + 32 * (pc.grp >> 24), (pc.grp & 0xffffffu) + 1, own);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            start(b, pc);
+            pend &= ~(1u << b);
+        }
         {
             uint32_t ok = 0;
             const uint32_t bb = smem_addr(&bar[b]);
