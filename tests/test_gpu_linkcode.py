@@ -2,6 +2,7 @@
 DMA of coded groups into HBM staging + decode kernel) land the host store in the extent bit-exactly
 (SURVEY §8c 'Swap (K1/K2)' pin) for every model class, claim order, CTA count, group size and mode,
 and the outputs are bit-identical to the plain engines' (the decoded bytes are the same bytes)."""
+import os
 import numpy as np
 import pytest
 
@@ -69,10 +70,22 @@ def test_smz_orders_and_ctas_bit_exact(rt, ctas):
         rt.unregister(mid)
 
 
+@pytest.mark.parametrize("huff", [0, 1])
 @pytest.mark.parametrize("grp", [256, 4096, 64 << 10, 2 << 20, 64 << 20])
-def test_dmaz_group_sweep_bit_exact(rt, grp):
+def test_dmaz_group_sweep_bit_exact(rt, grp, huff):
+    """Every copy-group size, claim order and overlap mode lands bit-exactly; huff = 1 (entropy-coded pieces) runs
+    the shared-memory decoder, whose claims wait for their group only when the loop reaches their ring slot
+    (pending claims at every group boundary when the groups are small)."""
     spec = _odd_model([1, 256, 65537, 600_000])
-    mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
+    old = os.environ.get("FSW_LINK_HUFF")
+    os.environ["FSW_LINK_HUFF"] = str(huff)  # read at registration
+    try:
+        mid = rt.register_spec(spec, spec.build_weights(), link_code=True)
+    finally:
+        if old is None:
+            del os.environ["FSW_LINK_HUFF"]
+        else:
+            os.environ["FSW_LINK_HUFF"] = old
     try:
         for order, flags in ((0, 0), (0, NO_OVERLAP), (ORDER_REVERSE, 0), (ORDER_RANDOM, 0)):
             rt.evict(mid)
