@@ -43,6 +43,21 @@ struct WsCfg {
 }  // namespace
 
 constexpr int kWsThreads = 512;  // thread 0 loads, thread 32 issues the MMAs; all 16 warps drain TMEM and run the epilogue
+// folded LayerNorm (a.ln_x): warps 4..15 build the normalised operand tiles; (μ, rstd) of the tile's tokens in the
+// extra KiB after the control block
+constexpr uint32_t kLnWarp0 = 4, kLnWarps = kWsThreads / 32 - kLnWarp0;
+
+// Per-token partial of a folded LayerNorm's statistics over the nq lanes (a power of two dividing 32) that hold one
+// token's output columns: (mean, M2) of their 4·nq values, two shuffle passes (the LN kernel's two-pass form).
+__device__ __forceinline__ float2 ln_partial(const float4 v, uint32_t nq) {
+    float s = (v.x + v.y) + (v.z + v.w);
+    for (uint32_t o = 1; o < nq; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mu = s / (float)(4u * nq);
+    const float d0 = v.x - mu, d1 = v.y - mu, d2 = v.z - mu, d3 = v.w - mu;
+    float q = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    for (uint32_t o = 1; o < nq; o <<= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    return make_float2(mu, q);
+}
 
 template <int TT, bool RING>
 __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant__ CUtensorMap tmX, const DevDesc* __restrict__ d, Wait w,
@@ -75,7 +90,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
 
     if (threadIdx.x == 0) {
         for (uint32_t j = 0; j < NS && j < nkt; ++j) {
-            mbar_init(&full[j], 1);
+            mbar_init(&full[j], !RING && a.ln_x ? 1 + kLnWarps : 1);  // + the operand-building warps' arrivals
             if (RING) mbar_init(&empty[j], 1);
         }
         mbar_init(done, 1);
@@ -104,8 +119,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         const uint8_t* wt = weight_ptr(dd, a.w_off) + (uint64_t)(n0 / 8) * 1024;
         const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
         const uint32_t pre = min(NS, nkt);
+        const uint32_t xbytes = !RING && a.ln_x ? 0u : C::kX;  // a folded LayerNorm builds the operand in place
         for (uint32_t j = 0; j < pre; ++j) {
-            mbar_expect_tx(&full[j], wrows * 128 + C::kX);
+            mbar_expect_tx(&full[j], wrows * 128 + xbytes);
             bulk_load(sw + j * kWsW, wt + (kt0 + j) * ktile_stride, wrows * 128, &full[j]);
         }
         if (a.pf_bytes && w.n == 0) {  // resident: this CTA's share of the next GEMM's weights into L2
@@ -119,7 +135,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         pdl_wait();
         FSW_TRACE_MAX(w.trace, w.layer, 5, globaltimer());
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        for (uint32_t j = 0; j < pre; ++j) tma_load_2d(sx + j * C::kX, &tmX, (int)((kt0 + j) * kBK), (int)t0, &full[j]);
+        if (xbytes)
+            for (uint32_t j = 0; j < pre; ++j) tma_load_2d(sx + j * C::kX, &tmX, (int)((kt0 + j) * kBK), (int)t0, &full[j]);
         // ring: refill slot j mod NS once the MMAs of its previous use are done (slot / phase counted, no division:
         // this thread and the MMA issuer are on the critical path)
         if (RING)
@@ -152,6 +169,61 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
             }
         }
         umma_commit(done);
+    } else if (!RING && a.ln_x && warp >= kLnWarp0) {
+        // Folded LayerNorm: the operand is LN(x) of this CTA's tokens over its K range, built here.
+        // (1) per token, (μ, rstd) merged from the producer's per-slot (mean, M2) partials (Chan's formula, slots in
+        // order: deterministic); (2) per k sub-tile, 8 columns per thread: (x − μ)·rstd·γ + β rounded to bf16 and
+        // stored at the SWIZZLE_128B position the TMA box would have used (16-B chunk c of row r at c ^ (r & 7)),
+        // then a proxy fence and one arrival per warp on the sub-tile's barrier.
+        const uint32_t lw = warp - kLnWarp0, K = a.K;
+        float* mu_s = reinterpret_cast<float*>(ctl + 1024);
+        float* rs_s = mu_s + 128;
+        if (lane == 0) wait_ready_thread(w);  // the LayerNorm's γ / β (the Wait includes its layer)
+        __syncwarp();
+        const uint16_t* gam = reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.ln_g_off));
+        const uint16_t* bet = reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.ln_b_off));
+        pdl_wait();
+        const float cnt = (float)a.ln_cnt, inv_k = 1.0f / (float)K;
+        for (uint32_t tok = lw; tok < TT; tok += kLnWarps) {
+            const uint32_t t = min(t0 + tok, a.M - 1);
+            const float2 p0 = lane < a.ln_slots ? a.ln_st[(uint64_t)lane * a.M + t] : make_float2(0.f, 0.f);
+            const float2 p1 = lane + 32 < a.ln_slots ? a.ln_st[(uint64_t)(lane + 32) * a.M + t] : make_float2(0.f, 0.f);
+            const float mu = warp_sum(p0.x + p1.x) * cnt * inv_k;
+            const float e0 = p0.x - mu, e1 = p1.x - mu;
+            float q = (lane < a.ln_slots ? p0.y + cnt * e0 * e0 : 0.f) + (lane + 32 < a.ln_slots ? p1.y + cnt * e1 * e1 : 0.f);
+            const float rs = rsqrtf(warp_sum(q) * inv_k + a.ln_eps);
+            if (lane == 0) {
+                mu_s[tok] = mu;
+                rs_s[tok] = rs;
+                if (a.ln_musig && blockIdx.x == 0 && blockIdx.z == 0 && t0 + tok < a.M) a.ln_musig[t0 + tok] = make_float2(mu, rs);
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kLnWarps * 32) : "memory");  // every (μ, rstd) of the tile is in shared memory
+        for (uint32_t j = 0; j < nkt; ++j) {
+            uint8_t* xs = sx + j * C::kX;
+            for (uint32_t c = lw * 32 + lane; c < TT * 8; c += kLnWarps * 32) {
+                const uint32_t tok = c >> 3, ch = c & 7, t = t0 + tok, k = (kt0 + j) * kBK + ch * 8;
+                uint4 pk = make_uint4(0u, 0u, 0u, 0u);
+                if (t < a.M) {
+                    const float4* xp = reinterpret_cast<const float4*>(a.ln_x + (uint64_t)t * K + k);
+                    const float4 x0 = xp[0], x1 = xp[1];
+                    const uint4 gv = *reinterpret_cast<const uint4*>(gam + k), bv = *reinterpret_cast<const uint4*>(bet + k);
+                    const float mu = mu_s[tok], rs = rs_s[tok];
+                    auto y = [&](float x, uint32_t g2, uint32_t b2, bool hi) {
+                        const float gg = __uint_as_float(hi ? g2 & 0xffff0000u : g2 << 16), bb = __uint_as_float(hi ? b2 & 0xffff0000u : b2 << 16);
+                        return (uint32_t)f32_to_bf16((x - mu) * rs * gg + bb);
+                    };
+                    pk.x = y(x0.x, gv.x, bv.x, false) | (y(x0.y, gv.x, bv.x, true) << 16);
+                    pk.y = y(x0.z, gv.y, bv.y, false) | (y(x0.w, gv.y, bv.y, true) << 16);
+                    pk.z = y(x1.x, gv.z, bv.z, false) | (y(x1.y, gv.z, bv.z, true) << 16);
+                    pk.w = y(x1.z, gv.w, bv.w, false) | (y(x1.w, gv.w, bv.w, true) << 16);
+                }
+                *reinterpret_cast<uint4*>(xs + tok * 128u + ((ch ^ (tok & 7u)) << 4)) = pk;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> the tensor core's reads
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[j]);
+        }
     }
     __syncwarp();
 
@@ -240,12 +312,38 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
                     const uint2 h = *reinterpret_cast<const uint2*>(resh + ri);
                     rr[e] = make_uint4(h.x << 16, h.x & 0xffff0000u, h.y << 16, h.y & 0xffff0000u);
                 }
+                if (a.res_musig) {  // a folded LayerNorm's output as the residual: LN(res) from (μ, rstd), γ, β
+                    const float2 ms = a.res_musig[t];
+                    const uint2 g = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.res_g_off)) + n);
+                    const uint2 b = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.res_b_off)) + n);
+                    rr[e].x = __float_as_uint((__uint_as_float(rr[e].x) - ms.x) * ms.y * __uint_as_float(g.x << 16) + __uint_as_float(b.x << 16));
+                    rr[e].y = __float_as_uint((__uint_as_float(rr[e].y) - ms.x) * ms.y * __uint_as_float(g.x & 0xffff0000u) + __uint_as_float(b.x & 0xffff0000u));
+                    rr[e].z = __float_as_uint((__uint_as_float(rr[e].z) - ms.x) * ms.y * __uint_as_float(g.y << 16) + __uint_as_float(b.y << 16));
+                    rr[e].w = __float_as_uint((__uint_as_float(rr[e].w) - ms.x) * ms.y * __uint_as_float(g.y & 0xffff0000u) + __uint_as_float(b.y & 0xffff0000u));
+                }
             }
         }
         if (threadIdx.x == 0 && u0 == 0) FSW_TRACE_MAX(w.trace, w.layer, 8, globaltimer());
 #pragma unroll
         for (int e = 0; e < kE; ++e) {
             const uint32_t u = u0 + e * kWsThreads;
+            if (a.st_out && u0 + e * kWsThreads - lane < units) {
+                // a folded LayerNorm's producer: (mean, M2) of this token's columns in this slot (the plan allows it only
+                // when every slot holds 128 / splits valid columns of every token, nq a power of two); whole warps
+                const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
+                float4 v = acc[e];
+                if (u < units) {
+                    const float4 b = *reinterpret_cast<const float4*>(bias_s + 4 * q);
+                    v.x = (v.x + b.x) + __uint_as_float(rr[e].x);
+                    v.y = (v.y + b.y) + __uint_as_float(rr[e].y);
+                    v.z = (v.z + b.z) + __uint_as_float(rr[e].z);
+                    v.w = (v.w + b.w) + __uint_as_float(rr[e].w);
+                    v = act4(a.act, v);
+                }
+                const float2 pm = ln_partial(v, nq);
+                if ((u & (nq - 1)) == 0 && u < units && t < a.M && n < a.N)
+                    a.st_out[(uint64_t)(blockIdx.x * S + rank) * a.M + t] = pm;
+            }
             if (u >= units) continue;
             const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
             if (t >= a.M || n >= a.N) continue;
@@ -275,8 +373,8 @@ static void launch_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMa
     if (a.ws_stages)
         launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, true>, grid, dim3(kWsThreads), C::smem(a.ws_stages, a.splits), s,
                            dim3(1, 1, a.splits), *tmX, d, w, a);
-    else
-        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, false>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits), s,
+    else  // + 1 KiB for a folded LayerNorm's (μ, rstd) per token
+        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, false>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits) + (a.ln_x ? 1024u : 0u), s,
                            dim3(1, 1, a.splits), *tmX, d, w, a);
 }
 

@@ -408,7 +408,23 @@ static fsw_status enqueue_layers(Model& m, Plan& p, Gpu& g, const InvokeCfg& ic,
         return FSW_OK;
     }
     for (const Launch& x : p.launches) {
-        const Wait w = layer_wait(m, g, ic, x.layer);
+        Wait w = layer_wait(m, g, ic, x.layer);
+        if (x.wait_layer2 >= 0) {  // a folded LayerNorm: its γ / β must have landed too
+            const Wait w2 = layer_wait(m, g, ic, x.wait_layer2);
+            for (uint32_t j = 0; j < w2.n; ++j) {
+                uint32_t k = 0;
+                while (k < w.n && w.ready[k] != w2.ready[j]) ++k;
+                if (k < w.n) {
+                    w.target[k] = std::max(w.target[k], w2.target[j]);  // the same counter (DMA group counts)
+                } else if (w.n < (uint32_t)kMaxWaitSrc) {
+                    w.ready[w.n] = w2.ready[j];
+                    w.target[w.n++] = w2.target[j];
+                    w.sys = w.sys | w2.sys;
+                } else {
+                    return fail(FSW_EINVAL, "plan: too many readiness counters for layer %d", x.layer);
+                }
+            }
+        }
         switch (x.kind) {
             case K_EMBED: launch_embed(s, d, w, x.embed); break;
             case K_LN: launch_layernorm(s, d, w, x.ln); break;

@@ -237,6 +237,19 @@ struct GemmArgs {  // out[m][n] = act(A[m]·W[n] + b[n] + res[m][n]); A via TMA,
     // L2 prefetch (k_gemm / k_gemm_ws, resident invokes): the next GEMM's weights [pf_off, pf_off + pf_bytes) of
     // the store, dealt over this launch's CTAs; pf_bytes = 0: none
     uint64_t pf_off, pf_bytes;
+    // LayerNorm folded into the k_gemm_ws launches around it (FSW_LN_FUSE; plan.cpp fuse_layernorms):
+    //  * producer (st_out != null): the owner CTA of each (row tile, split) writes, per token, the (mean, M2) of
+    //    its 128 / splits output columns to st_out[(tile · splits + split) · M + token];
+    //  * A consumer (ln_x != null, stationary mode only): the operand tile is LN(ln_x) computed on load —
+    //    (μ, rstd) merged from the ln_slots partials (ln_cnt values each, Chan's formula), γ / β from the
+    //    store — written bf16 into the swizzled shared-memory tile instead of a TMA load; the launch with
+    //    blockIdx.x = z = 0 stores (μ, rstd) per token to ln_musig;
+    //  * residual consumer (res_musig != null): the residual is LN(res) = (res − μ)·rstd·γ + β recomputed from
+    //    the pre-LN fp32 stream `res` and those (μ, rstd).
+    float2* st_out;
+    const float* ln_x; const float2* ln_st; uint32_t ln_slots, ln_cnt; uint64_t ln_g_off, ln_b_off; float ln_eps;
+    float2* ln_musig;
+    const float2* res_musig; uint64_t res_g_off, res_b_off;
 };
 void launch_gemm(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMap* tmA, const GemmArgs& a,
                  const CUtensorMap* tmW = nullptr);

@@ -629,6 +629,91 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                         a.splits, a.kt_per, a.ws_stages, a.cz, a.ws_tt ? gemm_ws_smem(a.ws_tt, a.ws_stages ? a.ws_stages : a.kt_per, a.splits) : 0u, (unsigned long long)a.pf_bytes);
         }
     }
+    // LayerNorm folded into the k_gemm_ws launches around it (FSW_LN_FUSE=1; DESIGN §5 "folded LayerNorm"): the
+    // producing GEMM writes per-token partial statistics, the GEMM reading the LN output as its operand normalises
+    // on load, the GEMM reading it as a residual recomputes it from the pre-LN stream; the LN launch goes.  Only
+    // where every reader of the LN output is such a GEMM and the pre-LN stream outlives them (post-LN BERT: both
+    // LayerNorms of every layer but the last).
+    static const int ln_fuse = getenv("FSW_LN_FUSE") ? atoi(getenv("FSW_LN_FUSE")) : 0;
+    if (ln_fuse) {
+        std::vector<uint8_t> drop(p->launches.size(), 0);
+        auto pow2 = [](uint32_t v) { return v && !(v & (v - 1)); };
+        for (size_t i = 1; i < p->launches.size(); ++i) {
+            Launch& ln = p->launches[i];
+            Launch& pr = p->launches[i - 1];
+            if (ln.kind != K_LN || pr.kind != K_GEMM || drop[i - 1]) continue;
+            const GemmArgs& pa = pr.gemm;
+            const uint32_t C = ln.ln.C, M = ln.ln.rows;
+            if (!pa.ws_tt || (const void*)pa.out != (const void*)ln.ln.in || pa.out_bf16 || pa.N != C || pa.n_pad != C ||
+                C % 128 || !pow2(pa.splits) || pa.splits > 8 || pa.M != M || pa.st_out)
+                continue;
+            const uint32_t slots = (C / 128) * pa.splits;
+            if (slots > 64) continue;
+            const int s_in = m.layers[ln.layer].in0, s_out = m.layers[ln.layer].out;
+            if (s_out == m.output_slot || s_in == m.output_slot) continue;
+            int a_cons = -1, r_cons = -1;
+            bool ok = true, in_live = true;
+            for (size_t j = i + 1; j < p->launches.size() && ok; ++j) {
+                const fsw_layer& L = m.layers[p->launches[j].layer];
+                const Launch& y = p->launches[j];
+                const bool reads = L.in0 == s_out || L.in1 == s_out;
+                if (reads && !in_live) ok = false;  // the pre-LN stream was overwritten before this reader
+                if (L.in0 == s_out) {
+                    const GemmArgs& ya = y.gemm;
+                    if (a_cons >= 0 || y.kind != K_GEMM || !ya.ws_tt || ya.ws_stages || ya.M != M || ya.K != C || ya.ln_x ||
+                        gemm_ws_smem(ya.ws_tt, ya.kt_per, ya.splits) + 1024 > 184 * 1024)
+                        ok = false;
+                    a_cons = (int)j;
+                }
+                if (L.in1 == s_out) {
+                    const GemmArgs& ya = y.gemm;
+                    if (r_cons >= 0 || y.kind != K_GEMM || !ya.ws_tt || ya.res_bf16 || ya.ld_res != C || ya.M != M || ya.res_musig)
+                        ok = false;
+                    r_cons = (int)j;
+                }
+                if (L.out == s_out) break;  // rewritten: later readers see the new value
+                if (L.out == s_in) {
+                    if (reads) ok = false;  // it would overwrite the pre-LN stream it normalises
+                    in_live = false;
+                }
+            }
+            if (!ok || a_cons < 0) continue;
+            // scratch: the partials [slots][M] and (μ, rstd) [M]
+            const uint64_t st_off = align_up(off, 256), ms_off = align_up(st_off + (uint64_t)slots * M * 8, 256);
+            off = align_up(ms_off + (uint64_t)M * 8, 1024);
+            float2* st = reinterpret_cast<float2*>(g.ws + st_off);
+            float2* ms = reinterpret_cast<float2*>(g.ws + ms_off);
+            pr.gemm.st_out = st;
+            GemmArgs& ca = p->launches[a_cons].gemm;
+            ca.ln_x = ln.ln.in;
+            ca.ln_st = st;
+            ca.ln_slots = slots;
+            ca.ln_cnt = 128 / pa.splits;
+            ca.ln_g_off = ln.ln.g_off;
+            ca.ln_b_off = ln.ln.b_off;
+            ca.ln_eps = ln.ln.eps;
+            ca.ln_musig = r_cons >= 0 ? ms : nullptr;
+            p->launches[a_cons].wait_layer2 = ln.layer;
+            if (r_cons >= 0) {
+                GemmArgs& ra = p->launches[r_cons].gemm;
+                ra.res = ln.ln.in;
+                ra.res_bf16 = 0;
+                ra.ld_res = C;
+                ra.res_musig = ms;
+                ra.res_g_off = ln.ln.g_off;
+                ra.res_b_off = ln.ln.b_off;
+                p->launches[r_cons].wait_layer2 = ln.layer;
+            }
+            drop[i] = 1;
+            if (getenv("FSW_PLAN_VERBOSE") && atoi(getenv("FSW_PLAN_VERBOSE")) == 1)
+                fprintf(stderr, "[fsw plan] LayerNorm layer %d folded: statistics from layer %d (%u slots), operand of layer %d, residual of layer %d\n",
+                        ln.layer, pr.layer, slots, p->launches[a_cons].layer, r_cons >= 0 ? p->launches[r_cons].layer : -1);
+        }
+        std::vector<Launch> kept;
+        for (size_t i = 0; i < p->launches.size(); ++i)
+            if (!drop[i]) kept.push_back(p->launches[i]);
+        p->launches.swap(kept);
+    }
     // split-K partials live after the activations and the im2col scratch
     const uint64_t part_off = align_up(off, 1024);
     p->ws_bytes = align_up(part_off + part_bytes, 1024);

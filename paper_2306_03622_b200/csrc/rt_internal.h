@@ -95,6 +95,7 @@ struct Launch {  // one kernel of the layer graph (addresses resolved for one GP
     const void* abase = nullptr;  // K_GEMM (linear): the bf16 activation matrix [M][a_cols] the A tiles come from
     uint32_t a_cols = 0;
     bool attn_tc = false;         // K_ATTN: the tcgen05 kernel (attn_tc.cu), tmap over the QKV activation
+    int wait_layer2 = -1;         // K_GEMM with a folded LayerNorm: also wait for that layer's weights (its γ, β)
 };
 
 struct Gpu;
