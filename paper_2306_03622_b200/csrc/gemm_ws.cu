@@ -59,7 +59,9 @@ __device__ __forceinline__ float2 ln_partial(const float4 v, uint32_t nq) {
     return make_float2(mu, q);
 }
 
-template <int TT, bool RING>
+// LN: the folded-LayerNorm instantiation (FSW_LN_FUSE; stationary mode only), so the default kernels carry none of its
+// code (measured: 0.26 us per launch when they did)
+template <int TT, bool RING, bool LN>
 __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant__ CUtensorMap tmX, const DevDesc* __restrict__ d, Wait w,
                                                  GemmArgs a) {
     TraceExit tx(w.trace, w.layer);
@@ -90,7 +92,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
 
     if (threadIdx.x == 0) {
         for (uint32_t j = 0; j < NS && j < nkt; ++j) {
-            mbar_init(&full[j], !RING && a.ln_x ? 1 + kLnWarps : 1);  // + the operand-building warps' arrivals
+            mbar_init(&full[j], LN && a.ln_x ? 1 + kLnWarps : 1);  // + the operand-building warps' arrivals
             if (RING) mbar_init(&empty[j], 1);
         }
         mbar_init(done, 1);
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
         const uint8_t* wt = weight_ptr(dd, a.w_off) + (uint64_t)(n0 / 8) * 1024;
         const uint64_t ktile_stride = (uint64_t)(a.n_pad / 8) * 1024;
         const uint32_t pre = min(NS, nkt);
-        const uint32_t xbytes = !RING && a.ln_x ? 0u : C::kX;  // a folded LayerNorm builds the operand in place
+        const uint32_t xbytes = LN && a.ln_x ? 0u : C::kX;  // a folded LayerNorm builds the operand in place
         for (uint32_t j = 0; j < pre; ++j) {
             mbar_expect_tx(&full[j], wrows * 128 + xbytes);
             bulk_load(sw + j * kWsW, wt + (kt0 + j) * ktile_stride, wrows * 128, &full[j]);
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
             }
         }
         umma_commit(done);
-    } else if (!RING && a.ln_x && warp >= kLnWarp0) {
+    } else if (LN && a.ln_x && warp >= kLnWarp0) {
         // Folded LayerNorm: the operand is LN(x) of this CTA's tokens over its K range, built here.
         // (1) per token, (μ, rstd) merged from the producer's per-slot (mean, M2) partials (Chan's formula, slots in
         // order: deterministic); (2) per k sub-tile, 8 columns per thread: (x − μ)·rstd·γ + β rounded to bf16 and
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
                     const uint2 h = *reinterpret_cast<const uint2*>(resh + ri);
                     rr[e] = make_uint4(h.x << 16, h.x & 0xffff0000u, h.y << 16, h.y & 0xffff0000u);
                 }
-                if (a.res_musig) {  // a folded LayerNorm's output as the residual: LN(res) from (μ, rstd), γ, β
+                if (LN && a.res_musig) {  // a folded LayerNorm's output as the residual: LN(res) from (μ, rstd), γ, β
                     const float2 ms = a.res_musig[t];
                     const uint2 g = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.res_g_off)) + n);
                     const uint2 b = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(weight_ptr(dd, a.res_b_off)) + n);
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_gemm_ws(const __grid_constant
 #pragma unroll
         for (int e = 0; e < kE; ++e) {
             const uint32_t u = u0 + e * kWsThreads;
-            if (a.st_out && u0 + e * kWsThreads - lane < units) {
+            if (LN && a.st_out && u0 + e * kWsThreads - lane < units) {
                 // a folded LayerNorm's producer: (mean, M2) of this token's columns in this slot (the plan allows it only
                 // when every slot holds 128 / splits valid columns of every token, nq a power of two); whole warps
                 const uint32_t tok = u / nq, q = q0 + (u - tok * nq), n = n0 + 4 * q, t = t0 + tok;
@@ -371,10 +373,13 @@ static void launch_ws(cudaStream_t s, const DevDesc* d, Wait w, const CUtensorMa
     using C = WsCfg<TT>;
     const dim3 grid((a.n_pad + 127) / 128, (a.M + TT - 1) / TT, a.splits);
     if (a.ws_stages)
-        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, true>, grid, dim3(kWsThreads), C::smem(a.ws_stages, a.splits), s,
+        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, true, false>, grid, dim3(kWsThreads), C::smem(a.ws_stages, a.splits), s,
                            dim3(1, 1, a.splits), *tmX, d, w, a);
-    else  // + 1 KiB for a folded LayerNorm's (μ, rstd) per token
-        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, false>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits) + (a.ln_x ? 1024u : 0u), s,
+    else if (a.ln_x || a.st_out || a.res_musig)  // + 1 KiB for a folded LayerNorm's (μ, rstd) per token
+        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, false, true>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits) + 1024u, s,
+                           dim3(1, 1, a.splits), *tmX, d, w, a);
+    else
+        launch_pdl_cluster(PDL_GEMM, k_gemm_ws<TT, false, false>, grid, dim3(kWsThreads), C::smem(a.kt_per, a.splits), s,
                            dim3(1, 1, a.splits), *tmX, d, w, a);
 }
 
@@ -410,7 +415,7 @@ static int ws_max_clusters(uint32_t slots, int cz) {
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_ws<TT, false>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_ws<TT, false, false>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -428,7 +433,7 @@ int gemm_ws_max_active_clusters(uint32_t tt, uint32_t kt_per, int cz) {
 
 template <int TT>
 static void ws_attrs() {
-    for (auto k : {k_gemm_ws<TT, false>, k_gemm_ws<TT, true>}) {
+    for (auto k : {k_gemm_ws<TT, false, false>, k_gemm_ws<TT, true, false>, k_gemm_ws<TT, false, true>}) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);  // split-K clusters up to 16
     }

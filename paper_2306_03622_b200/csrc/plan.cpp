@@ -644,7 +644,7 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
             if (ln.kind != K_LN || pr.kind != K_GEMM || drop[i - 1]) continue;
             const GemmArgs& pa = pr.gemm;
             const uint32_t C = ln.ln.C, M = ln.ln.rows;
-            if (!pa.ws_tt || (const void*)pa.out != (const void*)ln.ln.in || pa.out_bf16 || pa.N != C || pa.n_pad != C ||
+            if (!pa.ws_tt || pa.ws_stages || (const void*)pa.out != (const void*)ln.ln.in || pa.out_bf16 || pa.N != C || pa.n_pad != C ||
                 C % 128 || !pow2(pa.splits) || pa.splits > 8 || pa.M != M || pa.st_out)
                 continue;
             const uint32_t slots = (C / 128) * pa.splits;
@@ -667,7 +667,8 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                 }
                 if (L.in1 == s_out) {
                     const GemmArgs& ya = y.gemm;
-                    if (r_cons >= 0 || y.kind != K_GEMM || !ya.ws_tt || ya.res_bf16 || ya.ld_res != C || ya.M != M || ya.res_musig)
+                    if (r_cons >= 0 || y.kind != K_GEMM || !ya.ws_tt || ya.ws_stages || ya.res_bf16 || ya.ld_res != C || ya.M != M ||
+                        ya.res_musig)
                         ok = false;
                     r_cons = (int)j;
                 }
