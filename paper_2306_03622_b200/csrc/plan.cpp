@@ -83,13 +83,14 @@ static WsTiling choose_ws_tiling(uint32_t M, uint32_t n_pad, uint32_t kt, bool a
     if (ftt < 0 || M > 128) return WsTiling{0, 0, 0, 0, false};
     (void)any_width;
     // Tilings measured best for the paper's transformer shapes (M = 128 tokens; weight rows padded, K): BERT-base
-    // QKV 64:2, O-projection 32:4, FFN1 64:2, FFN2 64:8 (resident 0.423 -> 0.414 ms), GPT-2-XL QKV / FC / proj2 on
-    // a 3-slot ring (profiles/r02/gemm/ws_sweep.txt, chain_vs_cublas.txt); used when they fit, the cost model
-    // otherwise.
+    // QKV 64:2, O-projection 32:4 (resident 0.423 -> 0.414 ms), FFN1 64:2 and FFN2 64:8 each on a 3-slot ring
+    // (106 KB per CTA instead of 179, so FFN2's CTAs become resident beside FFN1's and stage their first weights
+    // during it: 0.415 -> 0.411 ms; either ring alone is slower), GPT-2-XL QKV / FC / proj2 on a 3-slot ring
+    // (profiles/r02/gemm/ws_sweep.txt, chain_vs_cublas.txt); used when they fit, the cost model otherwise.
     bool table_used = false;
     if (!ftt && M == 128) {
         struct Known { uint32_t n_pad, K, tt, s, stages; };
-        static const Known known[] = {{2304, 768, 64, 2, 0}, {768, 768, 32, 4, 0}, {3072, 768, 64, 2, 0}, {768, 3072, 64, 8, 0},
+        static const Known known[] = {{2304, 768, 64, 2, 0}, {768, 768, 32, 4, 0}, {3072, 768, 64, 2, 3}, {768, 3072, 64, 8, 3},
                                       // GPT-2-XL's wide linears: a ring of 3 slots per CTA (their K ranges do not fit)
                                       {4800, 1600, 128, 3, 3}, {6400, 1600, 128, 2, 3}, {1600, 6400, 128, 8, 3}};
         for (const Known& k : known)
