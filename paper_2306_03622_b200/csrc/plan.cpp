@@ -662,6 +662,7 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                 if (L.in0 == s_out) {
                     const GemmArgs& ya = y.gemm;
                     if (a_cons >= 0 || y.kind != K_GEMM || !ya.ws_tt || ya.ws_stages || ya.M != M || ya.K != C || ya.ln_x ||
+                        y.wait_layer2 >= 0 ||  // one extra readiness wait per launch (the LayerNorm's weights)
                         gemm_ws_smem(ya.ws_tt, ya.kt_per, ya.splits) + 1024 > 184 * 1024)
                         ok = false;
                     a_cons = (int)j;
@@ -669,7 +670,7 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                 if (L.in1 == s_out) {
                     const GemmArgs& ya = y.gemm;
                     if (r_cons >= 0 || y.kind != K_GEMM || !ya.ws_tt || ya.ws_stages || ya.res_bf16 || ya.ld_res != C || ya.M != M ||
-                        ya.res_musig)
+                        ya.res_musig || y.wait_layer2 >= 0)
                         ok = false;
                     r_cons = (int)j;
                 }
@@ -679,7 +680,7 @@ fsw_status build_plan(fsw_ctx* c, Model& m, int gi) {
                     in_live = false;
                 }
             }
-            if (!ok || a_cons < 0) continue;
+            if (!ok || a_cons < 0 || a_cons == r_cons) continue;
             // scratch: the partials [slots][M] and (μ, rstd) [M]
             const uint64_t st_off = align_up(off, 256), ms_off = align_up(st_off + (uint64_t)slots * M * 8, 256);
             off = align_up(ms_off + (uint64_t)M * 8, 1024);
