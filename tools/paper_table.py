@@ -5,7 +5,7 @@ the link-coded store; the paper's V100 numbers beside them (different hardware, 
 
     python tools/paper_table.py [--reps 20] [models...]
 """
-import json, os, sys
+import json, os, sys, time
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
@@ -24,8 +24,11 @@ with Runtime(gpu_ids=[0], pool_bytes=16 << 30) as rt:
         plain = rt.register_spec(spec, w)
         coded = rt.register_spec(spec, w, link_code=True)
 
-        def med(fn):
-            v = [fn() for _ in range(reps + 5)][5:]
+        def med(fn, warm_s=0.5):  # untimed warm-up by time (the first cold invokes after registration run slower)
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < warm_s:
+                fn()
+            v = [fn() for _ in range(reps)]
             return round(float(np.median(v)), 4)
 
         def cold(mid, **kw):
